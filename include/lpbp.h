@@ -1,0 +1,110 @@
+/*
+ * lpbp.h — C ABI of the B200-native log-polar backprojection library
+ * (liblpbp.so, sm_100a).  Drop-in for the fastbp backprojection / FBP path.
+ *
+ * Reference interfaces replaced (paths under pkg/src/fastbp of arXiv 1608.03589's
+ * reference package):
+ *   lpbp_execute (filter = 0)    logpolar_backproject(g, n_out, opts)        logpolar.py:121-136
+ *   lpbp_execute (filter = 1)    fbp(g, spec, engine="logpolar", n, opts)    filtering.py:73-98
+ *   lpbp_filter                  filter_sinogram(g, spec)                    filtering.py:54-70
+ *   lpbp_logpolar                _logpolar_convolve(sinogram_to_semipolar(g), rho0, nrho)
+ *                                                                            logpolar.py:100-118, grids.py:290-347
+ *   lpbp_readout                 logpolar_to_cartesian(l, n, n)              grids.py:399-443
+ *   lpbp_naive_backproject       backproject_naive(g, n)                     reference.py:21-37
+ *   lpbp_plan_create             LogPolarOptions / FilterSpec validation, adaptive_rho0, _mesh_for,
+ *                                make_logpolar_kernel, the kernel spectrum   logpolar.py:50-97, grids.py:385-391,
+ *                                                                            filtering.py:30-51
+ *
+ * Layouts (C-contiguous fp32, as the reference's .values arrays):
+ *   sinogram [batch][nt][ntheta]    image [batch][n][n]    log-polar [batch][nrho][2*ntheta]
+ * Pointers named *_dev are device pointers on the plan's device; *_host are host
+ * pointers (page-locked memory gives copy/compute overlap).  `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Calls are asynchronous with
+ * respect to the host unless stated otherwise.
+ *
+ * Errors: every function returns an LPBP_* status; lpbp_last_error() returns the
+ * message of the last failure on the calling thread.  LPBP_EINVAL carries the
+ * reference's ValueError messages.
+ */
+#ifndef LPBP_H_
+#define LPBP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LPBP_OK 0
+#define LPBP_EINVAL 1       /* invalid argument (reference ValueError)            */
+#define LPBP_ECUDA 2        /* CUDA runtime / launch failure                      */
+#define LPBP_EUNSUPPORTED 3 /* size has no compiled kernel instantiation          */
+#define LPBP_ENOMEM 4       /* device or host allocation failed                   */
+
+typedef struct lpbp_plan lpbp_plan;
+
+typedef struct lpbp_params {
+  int32_t nt;        /* detector bins (Sinogram.nt)                                      */
+  int32_t ntheta;    /* projection angles (Sinogram.ntheta); nphi = 2*ntheta             */
+  int32_t n_out;     /* output image side                                               */
+  int32_t has_rho0;  /* 0: adaptive_rho0(n_out, n_out); 1: use rho0 (LogPolarOptions.rho0) */
+  double rho0;
+  int32_t nrho;      /* 0: _mesh_for default; else LogPolarOptions.nrho                 */
+  int32_t filter;    /* 0: backprojection; 1: FBP = filter_sinogram, backproject, 1/(2pi) */
+  double lam;        /* FilterSpec.lam (filter = 1)                                     */
+  double cutoff;     /* FilterSpec.cutoff (filter = 1)                                  */
+  int32_t device;    /* CUDA device ordinal; < 0 builds a host-only plan (tables and info
+                        only, no device memory, every execute call fails with EINVAL)   */
+} lpbp_params;
+
+typedef struct lpbp_plan_info {
+  int32_t nt, ntheta, n_out, ns, nphi, nrho, L, M, kernel_nnz, kmax, filter, device;
+  double rho0, drho, dphi, out_scale;
+  size_t table_bytes;          /* device bytes of constant tables owned by the plan */
+  size_t workspace_per_slice;  /* lpbp_execute workspace bytes per slice in flight  */
+} lpbp_plan_info;
+
+int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan);
+void lpbp_plan_destroy(lpbp_plan* plan);
+int lpbp_plan_get_info(const lpbp_plan* plan, lpbp_plan_info* info);
+
+/* Workspace for lpbp_execute / lpbp_logpolar processing `chunk` slices at a time. */
+int lpbp_workspace_bytes(const lpbp_plan* plan, int32_t chunk, size_t* bytes);
+
+/* Full path: sinogram -> image for `batch` slices (device pointers).  The batch is
+ * processed in chunks that fit ws_bytes (>= one slice).  ws = NULL uses a workspace
+ * owned by the plan (then calls on one plan must not overlap). */
+int lpbp_execute(const lpbp_plan* plan, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
+                 size_t ws_bytes, void* stream);
+
+/* Same, from host to host: chunked H2D / compute / D2H overlapped on internal
+ * streams.  Blocks until the images are in img_host. */
+int lpbp_execute_host(lpbp_plan* plan, const float* sino_host, float* img_host, int32_t batch, int32_t chunk);
+
+/* Stages (parity testing and composition). */
+int lpbp_filter(const lpbp_plan* plan, const float* sino_dev, float* out_dev, int32_t batch, void* stream);
+int lpbp_logpolar(const lpbp_plan* plan, const float* sino_dev, float* lp_dev, int32_t batch, void* ws,
+                  size_t ws_bytes, void* stream);
+int lpbp_readout(const lpbp_plan* plan, const float* lp_dev, float* img_dev, int32_t batch, void* stream);
+
+/* Direct O(n^2 ntheta) pixel-driven backprojector.  ws: batch*nt*ntheta floats. */
+int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, int32_t ntheta, int32_t n,
+                           int32_t batch, float* ws_dev, void* stream);
+
+/* Host copies of plan tables for tests: which = "kernel_cells" (int32 pairs k,l),
+ * "ramp" (float M), "khat" (float2 nh*L), "ab" (int32 pairs ns), "wab" (float4 ns),
+ * "ki" (int32 nrho), "wi" (float2 nrho), "qidx" (uint32 nq*nq), "qw" (float2 nq*nq).  Returns the element count in *count;
+ * if dst is non-NULL copies min(count, capacity) elements. */
+int lpbp_plan_table(const lpbp_plan* plan, const char* which, void* dst, size_t capacity, size_t* count);
+
+/* Number of kernel launches the last lpbp_execute/lpbp_execute_host issued on the calling thread. */
+int64_t lpbp_last_launch_count(void);
+
+const char* lpbp_last_error(void);
+int32_t lpbp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LPBP_H_ */

@@ -1,0 +1,283 @@
+"""CPU oracle for the log-polar backprojection / FBP path.
+
+TEST INFRASTRUCTURE ONLY.  This module restates, in numpy/scipy (float64), the
+algorithm of the fastbp reference package (arXiv 1608.03589,
+/root/reference/pkg/src/fastbp) for the path this repository accelerates.  It is
+imported only by tests/, by __graft_entry__.smoke() as the checker, and by
+bench.py's CPU-baseline / --impl reference legs.  The product path
+(paper_1608_03589_b200) never imports it.
+
+Pinning: tests/test_oracle_pin.py checks every function here against golden
+vectors produced by the reference itself (tests/golden/make_golden.py, run in a
+container where /root/reference is importable) and, when the reference is
+importable, directly against it.
+
+Third-party arithmetic: the reference's FFTs are scipy.fft (pocketfft, scipy
+1.18.1 in this image; next_fast_len = smallest 11-smooth length >= target).
+The oracle calls the same scipy.fft entry points with the same lengths.
+
+Conventions (grids.py:1-15): t_i = -1 + i*2/nt, theta_j = j*pi/ntheta, pixel
+centres x_j = -1 + (j + 1/2)*2/n, semi-polar s_k = k/(ns-1), log-polar
+rho_i = rho0 + (i+1)*drho with drho = -rho0/nrho, phi_j = j*2*pi/nphi.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+from scipy import fft as sfft
+
+LOGPOLAR_SCALE = 0.5          # logpolar.py:47
+FBP_SCALE = 1.0 / (2.0 * math.pi)  # filtering.py:27
+
+
+# --------------------------------------------------------------------------
+# interpolation primitives
+# --------------------------------------------------------------------------
+
+def lerp_rows(values: np.ndarray, fidx: np.ndarray) -> np.ndarray:
+    """Per-column linear interpolation at fractional row positions; rows outside
+    [0, n) contribute zero.  Restates grids.py:255-269 (_lerp_axis0)."""
+    nrows = values.shape[0]
+    lo = np.floor(fidx).astype(np.int64)
+    frac = fidx - lo
+    hi = lo + 1
+    v_lo = np.take_along_axis(values, np.clip(lo, 0, nrows - 1), axis=0)
+    v_hi = np.take_along_axis(values, np.clip(hi, 0, nrows - 1), axis=0)
+    v_lo = np.where((lo >= 0) & (lo < nrows), v_lo, 0.0)
+    v_hi = np.where((hi >= 0) & (hi < nrows), v_hi, 0.0)
+    return v_lo * (1.0 - frac) + v_hi * frac
+
+
+def lerp_1d(profile: np.ndarray, fidx: np.ndarray) -> np.ndarray:
+    """1-D linear interpolation, zero outside.  Restates grids.py:272-282."""
+    n = profile.shape[0]
+    lo = np.floor(fidx).astype(np.int64)
+    frac = fidx - lo
+    a = np.where((lo >= 0) & (lo < n), profile[np.clip(lo, 0, n - 1)], 0.0)
+    b = np.where((lo + 1 >= 0) & (lo + 1 < n), profile[np.clip(lo + 1, 0, n - 1)], 0.0)
+    return a * (1.0 - frac) + b * frac
+
+
+# --------------------------------------------------------------------------
+# mesh sizing
+# --------------------------------------------------------------------------
+
+def adaptive_rho0(nx: int, ny: int) -> float:
+    """grids.py:385-391: one octave below the finest pixel pitch."""
+    if nx < 2 or ny < 2:
+        raise ValueError("counts must be >= 2")
+    return math.log(min(2.0 / nx, 2.0 / ny)) - math.log(2.0)
+
+
+def compute_nrho(ns: int, nx: int, ny: int) -> int:
+    """grids.py:372-382."""
+    if ns < 2 or nx < 2 or ny < 2:
+        raise ValueError("all counts must be >= 2")
+    v = math.ceil(math.log(min(1.0 / nx, 1.0 / ny)) / math.log(1.0 - 2.0 / ns))
+    return int(min(max(v, 2), 64 * ns))
+
+
+def mesh_for(ns: int, rho0: float, nrho: int | None) -> int:
+    """logpolar.py:84-97: resolution rule 1 - e^{-drho} <= 2/ns."""
+    step = 2.0 / ns
+    if nrho is None:
+        nrho = max(2, int(math.ceil(-rho0 / -math.log1p(-step))))
+    drho = -rho0 / nrho
+    largest = 1.0 - math.exp(-drho)
+    if largest > step * (1.0 + 1e-9):
+        raise ValueError(
+            "log-polar mesh too coarse: largest radial step "
+            f"{largest:.3e} exceeds the sinogram step {step:.3e}"
+        )
+    return nrho
+
+
+# --------------------------------------------------------------------------
+# resampling: sinogram -> semi-polar -> log-polar
+# --------------------------------------------------------------------------
+
+def semipolar(g: np.ndarray, ns: int | None = None) -> np.ndarray:
+    """Semi-polar unfolding p[ns][2*ntheta] of g[nt][ntheta] (grids.py:290-311):
+    columns < ntheta read g at t = +s, the others at t = -s (the phi >= pi half)."""
+    nt, ntheta = g.shape
+    ns = nt // 2 if ns is None else ns
+    if ns < 2:
+        raise ValueError("ns must be >= 2")
+    s = np.arange(ns) / (ns - 1.0)
+    inv_dt = 1.0 / (2.0 / nt)
+    pos = lerp_rows(g, np.broadcast_to(((s + 1.0) * inv_dt)[:, None], (ns, ntheta)).copy())
+    neg = lerp_rows(g, np.broadcast_to(((1.0 - s) * inv_dt)[:, None], (ns, ntheta)).copy())
+    return np.concatenate([pos, neg], axis=1)
+
+
+def logpolar_resample(p: np.ndarray, rho0: float, nrho: int) -> np.ndarray:
+    """Radial resampling s = e^rho onto rows rho_i = rho0 + (i+1)*drho
+    (grids.py:332-347)."""
+    if nrho < 2:
+        raise ValueError("nrho must be >= 2")
+    if not rho0 < 0:
+        raise ValueError("rho0 must be negative")
+    ns, nphi = p.shape
+    drho = -rho0 / nrho
+    rows = rho0 + (np.arange(nrho) + 1) * drho
+    f = np.exp(rows) * (ns - 1.0)
+    return lerp_rows(p, np.broadcast_to(f[:, None], (nrho, nphi)).copy())
+
+
+# --------------------------------------------------------------------------
+# kernel and convolution
+# --------------------------------------------------------------------------
+
+def lp_kernel(nrho: int, nphi: int, drho: float) -> np.ndarray:
+    """Box-discretised delta kernel on the lag mesh (logpolar.py:66-81):
+    1/drho where |e^{rho} cos(theta) - 1| <= drho, theta_j = -pi + j*2pi/nphi."""
+    if nrho < 2 or nphi < 2:
+        raise ValueError("kernel mesh must be at least 2 x 2")
+    if not drho > 0:
+        raise ValueError("drho must be positive")
+    lag_rho = np.arange(nrho)[:, None] * drho
+    lag_theta = -math.pi + np.arange(nphi)[None, :] * (2.0 * math.pi / nphi)
+    hit = np.abs(np.exp(lag_rho) * np.cos(lag_theta) - 1.0) <= drho
+    return hit * (1.0 / drho)
+
+
+def lp_convolve(lp: np.ndarray, drho: float) -> np.ndarray:
+    """FFT convolution of a log-polar image with the kernel, causal in rho
+    (zero padding to next_fast_len(2*nrho)) and cyclic in phi; scaled by
+    LOGPOLAR_SCALE*drho*dphi (logpolar.py:100-118)."""
+    nrho, nphi = lp.shape
+    kern = np.roll(lp_kernel(nrho, nphi, drho), -(nphi // 2), axis=1)
+    length = sfft.next_fast_len(2 * nrho)
+    spec = sfft.rfft2(lp, s=(length, nphi)) * sfft.rfft2(kern, s=(length, nphi))
+    out = sfft.irfft2(spec, s=(length, nphi))[:nrho]
+    return LOGPOLAR_SCALE * drho * (2.0 * math.pi / nphi) * out
+
+
+def lp_readout(lp: np.ndarray, rho0: float, nx: int, ny: int) -> np.ndarray:
+    """Bilinear sampling of a log-polar array at the Cartesian pixel centres
+    (grids.py:399-443): zero for r > 1, r == 0 or ln r < rho0; periodic in phi;
+    the sliver between rho0 and the first row clamps to row 0."""
+    if nx < 2 or ny < 2:
+        raise ValueError("nx and ny must be >= 2")
+    nrho, nphi = lp.shape
+    drho = -rho0 / nrho
+    dphi = 2.0 * math.pi / nphi
+    X, Y = np.meshgrid(-1.0 + (np.arange(nx) + 0.5) * (2.0 / nx), -1.0 + (np.arange(ny) + 0.5) * (2.0 / ny))
+    r = np.hypot(X, Y)
+    out = np.zeros((ny, nx))
+    sel = (r <= 1.0) & (r > 0.0)
+    if not sel.any():
+        return out
+    rho = np.log(r[sel])
+    fi = (rho - rho0) / drho - 1.0
+    fi = np.where((fi >= -1.0) & (fi < 0.0), 0.0, fi)
+    fi = np.clip(fi, 0.0, nrho - 1.0)
+    fj = np.mod(np.arctan2(Y[sel], X[sel]), 2.0 * math.pi) / dphi
+    i0 = np.floor(fi).astype(np.int64)
+    j0 = np.floor(fj).astype(np.int64)
+    wi = fi - i0
+    wj = fj - j0
+    j0 = np.mod(j0, nphi)
+    j1 = np.mod(j0 + 1, nphi)
+    i1 = np.minimum(i0 + 1, nrho - 1)
+    val = ((lp[i0, j0] * (1 - wi) + lp[i1, j0] * wi) * (1 - wj)
+           + (lp[i0, j1] * (1 - wi) + lp[i1, j1] * wi) * wj)
+    out[sel] = np.where(rho >= rho0, val, 0.0)
+    return out
+
+
+# --------------------------------------------------------------------------
+# engines
+# --------------------------------------------------------------------------
+
+def lp_geometry(nt: int, n_out: int, rho0: float | None = None, nrho: int | None = None):
+    """(ns, rho0, nrho, drho) exactly as logpolar_backproject derives them
+    (logpolar.py:128-133)."""
+    if n_out < 2:
+        raise ValueError("n_out must be >= 2")
+    if rho0 is not None and not rho0 < 0:
+        raise ValueError("rho0 must be negative")
+    if nrho is not None and nrho < 2:
+        raise ValueError("nrho must be >= 2")
+    ns = nt // 2
+    r0 = rho0 if rho0 is not None else adaptive_rho0(n_out, n_out)
+    nr = mesh_for(ns, r0, nrho)
+    return ns, r0, nr, -r0 / nr
+
+
+def logpolar_stage(g: np.ndarray, n_out: int, rho0: float | None = None, nrho: int | None = None) -> np.ndarray:
+    """Convolved log-polar image: _logpolar_convolve(sinogram_to_semipolar(g))
+    (logpolar.py:100-118, 134-135)."""
+    g = np.asarray(g, dtype=np.float64)
+    _, r0, nr, drho = lp_geometry(g.shape[0], n_out, rho0, nrho)
+    return lp_convolve(logpolar_resample(semipolar(g), r0, nr), drho)
+
+
+def logpolar_backproject(g: np.ndarray, n_out: int, rho0: float | None = None, nrho: int | None = None) -> np.ndarray:
+    """logpolar.py:121-136."""
+    g = np.asarray(g, dtype=np.float64)
+    _, r0, nr, _ = lp_geometry(g.shape[0], n_out, rho0, nrho)
+    return lp_readout(logpolar_stage(g, n_out, rho0, nrho), r0, n_out, n_out)
+
+
+def ramp_filter(g: np.ndarray, lam: float = 0.0, cutoff: float = 1.0) -> np.ndarray:
+    """filter_sinogram (filtering.py:54-70) with FilterSpec(lam, cutoff):
+    per-angle FFT over t zero-padded to next_fast_len(8*nt), response
+    |sigma|/(1+lam|sigma|) cut above cutoff*Nyquist, inverse, real part."""
+    if lam < 0:
+        raise ValueError("lambda must be >= 0")
+    if not (0.0 < cutoff <= 1.0):
+        raise ValueError("cutoff must lie in (0, 1]")
+    g = np.asarray(g, dtype=np.float64)
+    nt = g.shape[0]
+    dt = 2.0 / nt
+    length = sfft.next_fast_len(8 * nt)
+    sigma = 2.0 * math.pi * np.fft.fftfreq(length, d=dt)
+    mag = np.abs(sigma)
+    resp = mag / (1.0 + lam * mag)
+    resp[np.abs(sigma) > cutoff * math.pi / dt] = 0.0
+    return sfft.ifft(sfft.fft(g, n=length, axis=0) * resp[:, None], axis=0).real[:nt]
+
+
+def fbp_logpolar(g: np.ndarray, n: int, lam: float = 0.0, cutoff: float = 1.0,
+                 rho0: float | None = None, nrho: int | None = None) -> np.ndarray:
+    """fbp(g, FilterSpec(lam, cutoff), engine='logpolar', n) (filtering.py:73-98)."""
+    return FBP_SCALE * logpolar_backproject(ramp_filter(g, lam, cutoff), n, rho0, nrho)
+
+
+def backproject_naive(g: np.ndarray, n: int, rows: np.ndarray | None = None) -> np.ndarray:
+    """Pixel-driven backprojection b(x) = dtheta * sum_k lerp_t(g[:,k], (x.xi_k + 1)/dt)
+    (reference.py:21-37).  `rows` restricts the evaluation to those image rows
+    (returns shape (len(rows), n)) so large cases can be sampled."""
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    g = np.asarray(g, dtype=np.float64)
+    nt, ntheta = g.shape
+    xs = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+    ys = xs if rows is None else xs[np.asarray(rows)]
+    X, Y = np.meshgrid(xs, ys)
+    acc = np.zeros(X.shape)
+    inv_dt = 1.0 / (2.0 / nt)
+    dtheta = math.pi / ntheta
+    for k in range(ntheta):
+        th = k * dtheta
+        acc += lerp_1d(g[:, k], (X * math.cos(th) + Y * math.sin(th) + 1.0) * inv_dt)
+    return acc * dtheta
+
+
+def relative_l2(a, b) -> float:
+    """metrics.py:29-36: ||a - b|| / ||b||, b the reference."""
+    x = np.asarray(a, dtype=np.float64)
+    y = np.asarray(b, dtype=np.float64)
+    if x.shape != y.shape:
+        raise ValueError(f"dimension mismatch: {x.shape} vs {y.shape}")
+    den = np.linalg.norm(y)
+    if den == 0.0:
+        return 0.0 if np.linalg.norm(x) == 0.0 else float("inf")
+    return float(np.linalg.norm(x - y) / den)
+
+
+def max_abs(a, b) -> float:
+    return float(np.max(np.abs(np.asarray(a, dtype=np.float64) - np.asarray(b, dtype=np.float64))))

@@ -1,0 +1,26 @@
+"""B200-native (sm_100a) log-polar fast backprojection — drop-in for the fastbp
+backprojection / FBP path of arXiv 1608.03589 (reference package pkg/src/fastbp).
+
+Same names and signatures as the reference for the path:
+  Sinogram, CartesianImage, LogPolarImage, LogPolarOptions, FilterSpec,
+  logpolar_backproject, filter_sinogram, fbp, backproject_naive,
+  adaptive_rho0, compute_nrho, relative_l2
+plus batched device entry points (torch CUDA tensors) and LogPolarPlan.
+All compute runs in liblpbp.so; there is no CPU fallback.
+"""
+
+from .grids import CartesianImage, LogPolarImage, Sinogram, adaptive_rho0, compute_nrho
+from .logpolar import (
+    LOGPOLAR_SCALE,
+    LogPolarOptions,
+    logpolar_backproject,
+    logpolar_backproject_batch,
+    logpolar_convolve,
+    mesh_for,
+)
+from .filtering import FBP_SCALE, FilterSpec, fbp, fbp_batch, filter_sinogram
+from .reference import backproject_naive, backproject_naive_batch
+from .metrics import max_abs_error, relative_l2
+from .plan import LogPolarPlan, get_plan, naive_backproject
+
+__version__ = "0.1.0"

@@ -1,0 +1,478 @@
+// C ABI (include/lpbp.h): plan lifetime, device tables, chunked executors.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/lpbp.h"
+#include "kernels.cuh"
+#include "plan_host.h"
+
+using lpbp::DevTables;
+using lpbp::Dims;
+using lpbp::HostPlan;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int64_t g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(LPBP_ECUDA, std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+int launch_fail(cudaError_t e, const char* where) {
+  if (e == cudaErrorNotSupported) return fail(LPBP_EUNSUPPORTED, std::string(where) + ": size not supported");
+  return cuda_fail(e, where);
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = (prev == dev) || cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+}  // namespace
+
+struct lpbp_plan {
+  HostPlan h;
+  Dims d{};
+  DevTables t{};
+  int device = 0;
+  std::vector<void*> allocs;
+  size_t table_bytes = 0;
+  size_t szA = 0, szB = 0;  // per-slice workspace regions (aliased by stage lifetime)
+
+  std::mutex mu;  // guards the owned workspace and the host pipeline
+  void* own_ws = nullptr;
+  size_t own_ws_bytes = 0;
+  struct Pipe {
+    int chunk = 0;
+    cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+    float* in[2] = {};
+    float* out[2] = {};
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+  } pipe;
+
+  template <typename T>
+  int upload(const std::vector<T>& v, const T** dst) {
+    if (v.empty()) {
+      *dst = nullptr;
+      return LPBP_OK;
+    }
+    void* p = nullptr;
+    const size_t bytes = v.size() * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(plan table)");
+    allocs.push_back(p);
+    e = cudaMemcpy(p, v.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(plan table)");
+    table_bytes += bytes;
+    *dst = static_cast<const T*>(p);
+    return LPBP_OK;
+  }
+
+  void release_pipe() {
+    for (int i = 0; i < 2; ++i) {
+      if (pipe.ev_in[i]) cudaEventDestroy(pipe.ev_in[i]);
+      if (pipe.ev_comp[i]) cudaEventDestroy(pipe.ev_comp[i]);
+      if (pipe.ev_out[i]) cudaEventDestroy(pipe.ev_out[i]);
+      if (pipe.in[i]) cudaFree(pipe.in[i]);
+      if (pipe.out[i]) cudaFree(pipe.out[i]);
+    }
+    if (pipe.ws) cudaFree(pipe.ws);
+    if (pipe.s_in) cudaStreamDestroy(pipe.s_in);
+    if (pipe.s_comp) cudaStreamDestroy(pipe.s_comp);
+    if (pipe.s_out) cudaStreamDestroy(pipe.s_out);
+    pipe = Pipe{};
+  }
+
+  ~lpbp_plan() {
+    DeviceGuard g(device);
+    release_pipe();
+    if (own_ws) cudaFree(own_ws);
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+namespace {
+
+// Run the stages for one chunk already resident on the device.
+// stop_after_lp: write the log-polar image to lp_out and skip filter/readout.
+int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, cudaStream_t s, bool stop_after_lp,
+              float* lp_out) {
+  const Dims& d = P->d;
+  char* A = ws;
+  char* B = ws + align256(P->szA * c);
+  const float* src = in;
+  cudaError_t e;
+  if (P->h.filter && !stop_after_lp) {
+    e = lpbp::launch_ramp(d, P->t, in, reinterpret_cast<float*>(A), c, s);
+    if (e) return launch_fail(e, "ramp_filter");
+    ++g_launches;
+    src = reinterpret_cast<const float*>(A);
+  }
+  e = lpbp::launch_row_rdft(d, P->t, src, reinterpret_cast<float2*>(B), c, s);
+  if (e) return launch_fail(e, "row_rdft");
+  ++g_launches;
+  e = lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c, s);
+  if (e) return launch_fail(e, "rho_conv");
+  ++g_launches;
+  float* lp = stop_after_lp ? lp_out : reinterpret_cast<float*>(B);
+  e = lpbp::launch_row_irdft(d, P->t, reinterpret_cast<const float2*>(A), lp, c, s);
+  if (e) return launch_fail(e, "row_irdft");
+  ++g_launches;
+  if (stop_after_lp) return LPBP_OK;
+  e = lpbp::launch_readout(d, P->t, lp, out, c, s);
+  if (e) return launch_fail(e, "readout");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+size_t ws_per_slice(const lpbp_plan* P) { return align256(P->szA) + align256(P->szB); }
+
+int ensure_own_ws(lpbp_plan* P, size_t bytes) {
+  if (P->own_ws_bytes >= bytes) return LPBP_OK;
+  if (P->own_ws) cudaFree(P->own_ws);
+  P->own_ws = nullptr;
+  P->own_ws_bytes = 0;
+  cudaError_t e = cudaMalloc(&P->own_ws, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(workspace)");
+  P->own_ws_bytes = bytes;
+  return LPBP_OK;
+}
+
+int run_batched(const lpbp_plan* Pc, const float* in, float* out, int batch, void* ws, size_t ws_bytes,
+                cudaStream_t s, bool stop_after_lp) {
+  lpbp_plan* P = const_cast<lpbp_plan*>(Pc);
+  const size_t per = P->szA + P->szB;
+  std::unique_lock<std::mutex> lock(P->mu, std::defer_lock);
+  if (!ws) {
+    lock.lock();
+    const int chunk = std::max(1, std::min(batch, 16));
+    int rc = ensure_own_ws(P, align256(P->szA * chunk) + align256(P->szB * chunk));
+    if (rc) return rc;
+    ws = P->own_ws;
+    ws_bytes = P->own_ws_bytes;
+  }
+  int chunk = 1;
+  while (chunk < batch && align256(P->szA * (chunk + 1)) + align256(P->szB * (chunk + 1)) <= ws_bytes) ++chunk;
+  if (align256(P->szA * chunk) + align256(P->szB * chunk) > ws_bytes)
+    return fail(LPBP_EINVAL, "workspace too small for one slice (need " + std::to_string(ws_per_slice(P)) + " bytes)");
+  (void)per;
+  const size_t in_slice = (size_t)P->d.nt * P->d.ntheta;
+  const size_t out_slice = stop_after_lp ? (size_t)P->d.nrho * P->d.nphi : (size_t)P->d.n * P->d.n;
+  for (int off = 0; off < batch; off += chunk) {
+    const int c = std::min(chunk, batch - off);
+    int rc = run_chunk(P, in + off * in_slice, stop_after_lp ? nullptr : out + off * out_slice, c,
+                       static_cast<char*>(ws), s, stop_after_lp, stop_after_lp ? out + off * out_slice : nullptr);
+    if (rc) return rc;
+  }
+  return LPBP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
+  g_last_error.clear();
+  if (!params || !plan) return fail(LPBP_EINVAL, "null argument");
+  *plan = nullptr;
+  lpbp::HostPlanParams hp{params->nt, params->ntheta, params->n_out, params->has_rho0 != 0, params->rho0,
+                          params->nrho, params->filter != 0, params->lam, params->cutoff};
+  lpbp_plan* P = new (std::nothrow) lpbp_plan();
+  if (!P) return fail(LPBP_ENOMEM, "host allocation failed");
+  std::string err = lpbp::build_host_plan(hp, P->h);
+  if (!err.empty()) {
+    delete P;
+    return fail(LPBP_EINVAL, err);
+  }
+  const HostPlan& h = P->h;
+  if (params->device >= 0 && !lpbp::sizes_supported(h.nt, h.ntheta, h.L, h.filter)) {
+    delete P;
+    return fail(LPBP_EUNSUPPORTED, "no kernel instantiation for nt=" + std::to_string(h.nt) + ", ntheta=" +
+                                       std::to_string(h.ntheta) + ", L=" + std::to_string(h.L) +
+                                       " (this build: 2*ntheta and 2*nt powers of two in [512, 4096])");
+  }
+  P->device = params->device;
+  if (P->device >= 0) {
+    DeviceGuard g(P->device);
+    if (!g.ok) {
+      delete P;
+      return fail(LPBP_ECUDA, "cannot select CUDA device " + std::to_string(params->device));
+    }
+    int rc = LPBP_OK;
+    rc = rc ? rc : P->upload(h.tw_phi, reinterpret_cast<const lpbp::F2**>(&P->t.tw_phi));
+    rc = rc ? rc : P->upload(h.tw_rho, reinterpret_cast<const lpbp::F2**>(&P->t.tw_rho));
+    rc = rc ? rc : P->upload(h.tw_ramp, reinterpret_cast<const lpbp::F2**>(&P->t.tw_ramp));
+    rc = rc ? rc : P->upload(h.ramp, &P->t.ramp);
+    rc = rc ? rc : P->upload(h.ab, reinterpret_cast<const lpbp::I2**>(&P->t.ab));
+    rc = rc ? rc : P->upload(h.wab, reinterpret_cast<const lpbp::F4**>(&P->t.wab));
+    rc = rc ? rc : P->upload(h.ki, &P->t.ki);
+    rc = rc ? rc : P->upload(h.wi, reinterpret_cast<const lpbp::F2**>(&P->t.wi));
+    rc = rc ? rc : P->upload(h.khat, reinterpret_cast<const lpbp::F2**>(&P->t.khat));
+    rc = rc ? rc : P->upload(h.qidx, &P->t.qidx);
+    rc = rc ? rc : P->upload(h.qw, reinterpret_cast<const lpbp::F2**>(&P->t.qw));
+    rc = rc ? rc : P->upload(h.naive_cs, reinterpret_cast<const lpbp::F2**>(&P->t.naive_cs));
+    if (rc) {
+      std::string msg = g_last_error;
+      delete P;
+      return fail(rc, msg);
+    }
+  }
+  Dims& d = P->d;
+  d.nt = h.nt;
+  d.ntheta = h.ntheta;
+  d.n = h.n;
+  d.ns = h.ns;
+  d.nphi = h.nphi;
+  d.nh = h.nh;
+  d.nrho = h.nrho;
+  d.nrho_pad = h.nrho_pad;
+  d.L = h.L;
+  d.M = h.M;
+  d.nq = h.nq;
+  d.out_scale = (float)h.out_scale;
+  const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;
+  const size_t Y = (size_t)h.nh * h.nrho_pad * sizeof(float2);
+  const size_t G = (size_t)h.nh * h.nt * sizeof(float2);
+  const size_t lp = (size_t)h.nrho * h.nphi * sizeof(float);
+  P->szA = std::max(fg, Y);
+  P->szB = std::max(G, lp);
+  *plan = P;
+  return LPBP_OK;
+}
+
+void lpbp_plan_destroy(lpbp_plan* plan) { delete plan; }
+
+int lpbp_plan_get_info(const lpbp_plan* P, lpbp_plan_info* info) {
+  if (!P || !info) return fail(LPBP_EINVAL, "null argument");
+  const HostPlan& h = P->h;
+  info->nt = h.nt;
+  info->ntheta = h.ntheta;
+  info->n_out = h.n;
+  info->ns = h.ns;
+  info->nphi = h.nphi;
+  info->nrho = h.nrho;
+  info->L = h.L;
+  info->M = h.M;
+  info->kernel_nnz = h.nnz;
+  info->kmax = h.kmax;
+  info->filter = h.filter ? 1 : 0;
+  info->device = P->device;
+  info->rho0 = h.rho0;
+  info->drho = h.drho;
+  info->dphi = h.dphi;
+  info->out_scale = h.out_scale;
+  info->table_bytes = P->table_bytes;
+  info->workspace_per_slice = ws_per_slice(P);
+  return LPBP_OK;
+}
+
+int lpbp_workspace_bytes(const lpbp_plan* P, int32_t chunk, size_t* bytes) {
+  if (!P || !bytes || chunk < 1) return fail(LPBP_EINVAL, "invalid argument");
+  *bytes = align256(P->szA * chunk) + align256(P->szB * chunk);
+  return LPBP_OK;
+}
+
+int lpbp_execute(const lpbp_plan* P, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
+                 size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!P || !sino_dev || !img_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  DeviceGuard g(P->device);
+  return run_batched(P, sino_dev, img_dev, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream), false);
+}
+
+int lpbp_logpolar(const lpbp_plan* P, const float* sino_dev, float* lp_dev, int32_t batch, void* ws,
+                  size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!P || !sino_dev || !lp_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  DeviceGuard g(P->device);
+  return run_batched(P, sino_dev, lp_dev, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream), true);
+}
+
+int lpbp_filter(const lpbp_plan* P, const float* sino_dev, float* out_dev, int32_t batch, void* stream) {
+  g_launches = 0;
+  if (!P || !sino_dev || !out_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (!P->h.filter) return fail(LPBP_EINVAL, "plan was created without a filter (filter = 0)");
+  if (batch == 0) return LPBP_OK;
+  DeviceGuard g(P->device);
+  cudaError_t e = lpbp::launch_ramp(P->d, P->t, sino_dev, out_dev, batch, static_cast<cudaStream_t>(stream));
+  if (e) return launch_fail(e, "ramp_filter");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+int lpbp_readout(const lpbp_plan* P, const float* lp_dev, float* img_dev, int32_t batch, void* stream) {
+  g_launches = 0;
+  if (!P || !lp_dev || !img_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  DeviceGuard g(P->device);
+  cudaError_t e = lpbp::launch_readout(P->d, P->t, lp_dev, img_dev, batch, static_cast<cudaStream_t>(stream));
+  if (e) return launch_fail(e, "readout");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+int lpbp_execute_host(lpbp_plan* P, const float* sino_host, float* img_host, int32_t batch, int32_t chunk) {
+  g_launches = 0;
+  if (!P || !sino_host || !img_host || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  if (chunk <= 0) chunk = 4;
+  chunk = std::min(chunk, batch);
+  DeviceGuard g(P->device);
+  std::lock_guard<std::mutex> lock(P->mu);
+  auto& pp = P->pipe;
+  const size_t in_slice = (size_t)P->d.nt * P->d.ntheta * sizeof(float);
+  const size_t out_slice = (size_t)P->d.n * P->d.n * sizeof(float);
+  if (pp.chunk < chunk) {
+    P->release_pipe();
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaMalloc(&pp.in[i], in_slice * chunk);
+      if (e == cudaSuccess) e = cudaMalloc(&pp.out[i], out_slice * chunk);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_in[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_comp[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_out[i], cudaEventDisableTiming);
+    }
+    pp.ws_bytes = align256(P->szA * chunk) + align256(P->szB * chunk);
+    if (e == cudaSuccess) e = cudaMalloc(&pp.ws, pp.ws_bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_comp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_out, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      P->release_pipe();
+      return cuda_fail(e, "host pipeline setup");
+    }
+    pp.chunk = chunk;
+  }
+  const int nchunks = (batch + chunk - 1) / chunk;
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int slot = ci & 1;
+    const int off = ci * chunk;
+    const int c = std::min(chunk, batch - off);
+    cudaError_t e;
+    if (ci >= 2) cudaStreamWaitEvent(pp.s_in, pp.ev_comp[slot], 0);
+    e = cudaMemcpyAsync(pp.in[slot], sino_host + (size_t)off * (in_slice / sizeof(float)), in_slice * c,
+                        cudaMemcpyHostToDevice, pp.s_in);
+    if (e) return cuda_fail(e, "H2D");
+    cudaEventRecord(pp.ev_in[slot], pp.s_in);
+    cudaStreamWaitEvent(pp.s_comp, pp.ev_in[slot], 0);
+    if (ci >= 2) cudaStreamWaitEvent(pp.s_comp, pp.ev_out[slot], 0);
+    const int64_t before = g_launches;
+    int rc = run_chunk(P, pp.in[slot], pp.out[slot], c, static_cast<char*>(pp.ws), pp.s_comp, false, nullptr);
+    if (rc) return rc;
+    (void)before;
+    cudaEventRecord(pp.ev_comp[slot], pp.s_comp);
+    cudaStreamWaitEvent(pp.s_out, pp.ev_comp[slot], 0);
+    e = cudaMemcpyAsync(img_host + (size_t)off * (out_slice / sizeof(float)), pp.out[slot], out_slice * c,
+                        cudaMemcpyDeviceToHost, pp.s_out);
+    if (e) return cuda_fail(e, "D2H");
+    cudaEventRecord(pp.ev_out[slot], pp.s_out);
+  }
+  cudaError_t e = cudaStreamSynchronize(pp.s_out);
+  if (e) return cuda_fail(e, "execute_host sync");
+  e = cudaStreamSynchronize(pp.s_comp);
+  if (e) return cuda_fail(e, "execute_host sync");
+  return LPBP_OK;
+}
+
+int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, int32_t ntheta, int32_t n,
+                           int32_t batch, float* ws_dev, void* stream) {
+  g_launches = 0;
+  if (!sino_dev || !img_dev || !ws_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (n < 2) return fail(LPBP_EINVAL, "n must be >= 2");
+  if (nt < 2 || ntheta < 1) return fail(LPBP_EINVAL, "nt must be >= 2 and ntheta >= 1");
+  if (batch == 0) return LPBP_OK;
+  // angle table (reference.py:30-36): cos/sin(k*pi/ntheta) * nt/(2n)
+  std::vector<lpbp::F2> cs(ntheta);
+  const double dtheta = 3.14159265358979323846 / ntheta;
+  for (int k = 0; k < ntheta; ++k) {
+    const double th = k * dtheta;
+    cs[k] = lpbp::F2{(float)(std::cos(th) * nt / (2.0 * n)), (float)(std::sin(th) * nt / (2.0 * n))};
+  }
+  void* dcs = nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMallocAsync(&dcs, cs.size() * sizeof(lpbp::F2), s);
+  if (e) return cuda_fail(e, "cudaMallocAsync(angles)");
+  e = cudaMemcpyAsync(dcs, cs.data(), cs.size() * sizeof(lpbp::F2), cudaMemcpyHostToDevice, s);
+  if (e) return cuda_fail(e, "angles H2D");
+  e = lpbp::launch_naive(nt, ntheta, n, static_cast<const float2*>(dcs), (float)dtheta, sino_dev, ws_dev, img_dev,
+                         batch, s);
+  g_launches += 2;
+  cudaError_t e2 = cudaStreamSynchronize(s);  // cs lives on the host stack until the copy completes
+  cudaFreeAsync(dcs, s);
+  if (e) return cuda_fail(e, "naive_backproject");
+  if (e2) return cuda_fail(e2, "naive_backproject");
+  return LPBP_OK;
+}
+
+int lpbp_plan_table(const lpbp_plan* P, const char* which, void* dst, size_t capacity, size_t* count) {
+  if (!P || !which || !count) return fail(LPBP_EINVAL, "invalid argument");
+  const HostPlan& h = P->h;
+  if (!std::strcmp(which, "kernel_cells")) {
+    *count = h.cell_k.size();
+    if (dst) {
+      int32_t* o = static_cast<int32_t*>(dst);
+      for (size_t i = 0; i < std::min(capacity, *count); ++i) {
+        o[2 * i] = h.cell_k[i];
+        o[2 * i + 1] = h.cell_l[i];
+      }
+    }
+    return LPBP_OK;
+  }
+  if (!std::strcmp(which, "ramp")) {
+    *count = h.ramp.size();
+    if (dst) std::memcpy(dst, h.ramp.data(), std::min(capacity, *count) * sizeof(float));
+    return LPBP_OK;
+  }
+  if (!std::strcmp(which, "khat")) {
+    *count = h.khat.size();
+    if (dst) std::memcpy(dst, h.khat.data(), std::min(capacity, *count) * sizeof(lpbp::F2));
+    return LPBP_OK;
+  }
+  auto copy_vec = [&](const auto& v) {
+    *count = v.size();
+    if (dst) std::memcpy(dst, v.data(), std::min(capacity, *count) * sizeof(v[0]));
+    return LPBP_OK;
+  };
+  if (!std::strcmp(which, "ab")) return copy_vec(h.ab);         // int32 pairs (a_k, b_k)
+  if (!std::strcmp(which, "wab")) return copy_vec(h.wab);       // float quads
+  if (!std::strcmp(which, "ki")) return copy_vec(h.ki);         // int32
+  if (!std::strcmp(which, "wi")) return copy_vec(h.wi);         // float pairs
+  if (!std::strcmp(which, "qidx")) return copy_vec(h.qidx);     // uint32
+  if (!std::strcmp(which, "qw")) return copy_vec(h.qw);         // float pairs
+  return fail(LPBP_EINVAL, std::string("unknown table ") + which);
+}
+
+int64_t lpbp_last_launch_count(void) { return g_launches; }
+const char* lpbp_last_error(void) { return g_last_error.c_str(); }
+int32_t lpbp_version(void) { return 100; }
+
+}  // extern "C"

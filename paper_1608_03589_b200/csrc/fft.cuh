@@ -1,0 +1,330 @@
+// Block-cooperative Stockham FFT building blocks for sm_100a.
+//
+// A CTA-resident complex FFT of size N is executed by T = N / E threads, each
+// holding E complex values in registers.  A pass of radix R (R divides E)
+// performs E/R butterflies per thread:
+//
+//   butterfly j (k = j mod Ns):
+//     v[r]  = buf[j + r*N/R]                     (r = 0..R-1)
+//     v[r] *= W_{Ns*R}^{+-r*k}                   (inter-pass twiddle)
+//     v     = DFT_R(v)                           (registers, constant twiddles)
+//     buf[(j/Ns)*Ns*R + k + r*Ns] = v[r]
+//
+// (Stockham autosort: natural order in, natural order out, Ns = product of the
+// radices already applied.)  All values of a pass live in registers between
+// its load and its store, so a single shared buffer plus two barriers per pass
+// suffices.  Shared addresses are padded by one float2 every 16 elements
+// (pad(i) = i + i/16) so the Ns = 1 scatter (stride R) is bank-conflict free.
+//
+// Twiddles come from a per-size fp32 table tw[i] = exp(-2*pi*i*I/N) built in
+// fp64 on the host; the inverse direction uses the conjugate.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <utility>
+
+namespace lpbp {
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+__host__ __device__ constexpr int pad16(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int n) { return n + (n >> 4); }
+
+// cos(2*pi*k/32) and sin(2*pi*k/32), k = 0..8 (first octant); the rest by symmetry.
+__host__ __device__ constexpr double cos32_oct(int k) {
+  return k == 0 ? 1.0
+       : k == 1 ? 0.98078528040323044912618223613424
+       : k == 2 ? 0.92387953251128675612818318939679
+       : k == 3 ? 0.83146961230254523707878837761791
+       : k == 4 ? 0.70710678118654752440084436210485
+       : k == 5 ? 0.55557023301960222474283081394853
+       : k == 6 ? 0.38268343236508977172845998403040
+       : k == 7 ? 0.19509032201612826784828486847702
+       : 0.0;
+}
+// cos(2*pi*k/32) for any k (mod 32)
+__host__ __device__ constexpr double cos32(int k) {
+  k = ((k % 32) + 32) % 32;
+  return k <= 8 ? cos32_oct(k) : k <= 16 ? -cos32_oct(16 - k) : k <= 24 ? -cos32_oct(k - 16) : cos32_oct(32 - k);
+}
+__host__ __device__ constexpr double sin32(int k) { return cos32(k - 8); }
+
+// x * exp(s * 2*pi*i*K/R) with s = -1 (forward) or +1 (inverse); K, R compile-time.
+template <int K, int R, bool INV>
+__device__ __forceinline__ float2 twc(float2 x) {
+  constexpr int k = ((K % R) + R) % R;
+  if constexpr (k == 0) {
+    return x;
+  } else if constexpr (4 * k == R) {  // exp(-+i*pi/2) = -+i
+    return INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
+  } else if constexpr (2 * k == R) {
+    return make_float2(-x.x, -x.y);
+  } else if constexpr (4 * k == 3 * R) {
+    return INV ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);
+  } else {
+    constexpr int k32 = k * (32 / R);
+    constexpr float c = (float)cos32(k32);
+    constexpr float s = INV ? (float)sin32(k32) : -(float)sin32(k32);
+    return make_float2(fmaf(c, x.x, -s * x.y), fmaf(s, x.x, c * x.y));
+  }
+}
+
+template <int I, int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(f);
+  }
+}
+
+// Radix-R DFT in registers, natural order in and out (recursive radix-2 DIT,
+// fully unrolled at compile time).  STRIDE/OFF select the subsequence of v.
+template <int R, bool INV>
+struct Dft {
+  template <int OFF, int STRIDE, int LEN>
+  __device__ __forceinline__ static void run_sub(const float2 (&in)[LEN], float2 (&out)[R]) {
+    if constexpr (R == 1) {
+      out[0] = in[OFF];
+    } else if constexpr (R == 2) {
+      float2 a = in[OFF], b = in[OFF + STRIDE];
+      out[0] = cadd(a, b);
+      out[1] = csub(a, b);
+    } else {
+      float2 E[R / 2], O[R / 2];
+      Dft<R / 2, INV>::template run_sub<OFF, STRIDE * 2, LEN>(in, E);
+      Dft<R / 2, INV>::template run_sub<OFF + STRIDE, STRIDE * 2, LEN>(in, O);
+      static_for<0, R / 2>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        float2 t = twc<k, R, INV>(O[k]);
+        out[k] = cadd(E[k], t);
+        out[k + R / 2] = csub(E[k], t);
+      });
+    }
+  }
+  __device__ __forceinline__ static void run(float2 (&v)[R]) {
+    float2 out[R];
+    run_sub<0, 1, R>(v, out);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = out[i];
+  }
+};
+
+// Multiply v[r] (r = 1..R-1) by tw^(r*k) where tw = exp(-+2*pi*i/(Ns*R)), using
+// the global table of size N: index = r*k*(N/(Ns*R)).
+template <int N, int R, int Ns, bool INV>
+__device__ __forceinline__ void apply_twiddles(float2 (&v)[R], int k, const float2* __restrict__ tw) {
+  if constexpr (Ns > 1) {
+    constexpr int step = N / (Ns * R);
+    const int base = k * step;
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      float2 w = __ldg(tw + base * r);
+      v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
+    }
+  }
+}
+
+// Load the R inputs of butterfly j of a pass from (padded) shared memory.
+template <int N, int R>
+__device__ __forceinline__ void pass_load(const float2* buf, int j, float2 (&v)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = buf[pad16(j + r * (N / R))];
+}
+template <int N, int R, int Ns>
+__device__ __forceinline__ void pass_store(float2* buf, int j, const float2 (&v)[R]) {
+  const int k = j % Ns;
+  const int d = (j / Ns) * Ns * R + k;
+#pragma unroll
+  for (int r = 0; r < R; ++r) buf[pad16(d + r * Ns)] = v[r];
+}
+
+// One full smem->smem Stockham pass for a group of T threads (ti in [0,T)).
+// Caller provides the barrier that separates the previous pass's stores from
+// these loads; this function places the barrier between loads and stores.
+template <int N, int R, int Ns, int T, bool INV, typename Sync>
+__device__ __forceinline__ void pass_smem(float2* buf, int ti, const float2* __restrict__ tw, Sync&& sync) {
+  constexpr int NB = (N / R) / T;  // butterflies per thread
+  static_assert(NB >= 1 && NB * T * R == N, "bad pass shape");
+  float2 v[NB][R];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = ti + b * T;
+    pass_load<N, R>(buf, j, v[b]);
+    apply_twiddles<N, R, Ns, INV>(v[b], j % Ns, tw);
+    Dft<R, INV>::run(v[b]);
+  }
+  sync();
+#pragma unroll
+  for (int b = 0; b < NB; ++b) pass_store<N, R, Ns>(buf, ti + b * T, v[b]);
+}
+
+// Radix plans (forward order; the inverse runs them reversed).  Every plan
+// starts with radix 16 so Ns >= 16 for every store after the first pass.
+template <int N> struct RadixPlan;
+template <> struct RadixPlan<256>   { static constexpr int P = 2; static constexpr int r[3] = {16, 16, 1}; static constexpr int E = 16; };
+template <> struct RadixPlan<512>   { static constexpr int P = 3; static constexpr int r[3] = {16, 8, 4};  static constexpr int E = 16; };
+template <> struct RadixPlan<1024>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 4}; static constexpr int E = 16; };
+template <> struct RadixPlan<2048>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 8}; static constexpr int E = 16; };
+template <> struct RadixPlan<4096>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 16}; static constexpr int E = 16; };
+template <> struct RadixPlan<8192>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 32}; static constexpr int E = 32; };
+
+template <int N, bool INV>
+struct FftPlan {
+  using RP = RadixPlan<N>;
+  static constexpr int P = RP::P;
+  static constexpr int E = RP::E;
+  static constexpr int T = N / E;  // threads per FFT
+  static constexpr int radix(int i) { return INV ? RP::r[P - 1 - i] : RP::r[i]; }
+  static constexpr int ns(int i) {
+    int s = 1;
+    for (int q = 0; q < i; ++q) s *= radix(q);
+    return s;
+  }
+};
+
+// Full size-N FFT over a group of T = N/E threads (ti in [0,T)).
+//   load(idx)       -> float2 : input element idx (first pass reads it directly)
+//   store(idx, val)           : output element idx (last pass writes it directly)
+//   sync()                    : barrier covering every thread that shares buf
+// LAST_SYNC places a barrier between the last pass's loads and its stores (needed
+// when store() writes back into buf).
+// The caller must guarantee buf is free on entry (no thread still reading it).
+// Middle passes go through the padded shared buffer buf (padded_len(N) float2).
+template <int N, bool INV, bool LAST_SYNC, typename Load, typename Store, typename Sync>
+__device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __restrict__ tw,
+                                          Load&& load, Store&& store, Sync&& sync) {
+  using FP = FftPlan<N, INV>;
+  constexpr int T = FP::T;
+  constexpr int P = FP::P;
+  {  // pass 0: Ns = 1, no twiddles
+    constexpr int R = FP::radix(0);
+    constexpr int NB = (N / R) / T;
+    float2 v[NB][R];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = ti + b * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
+      Dft<R, INV>::run(v[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) pass_store<N, R, 1>(buf, ti + b * T, v[b]);
+  }
+  sync();
+  static_for<1, P - 1>([&](auto ic) {
+    constexpr int I = decltype(ic)::value;
+    pass_smem<N, FP::radix(I), FP::ns(I), T, INV>(buf, ti, tw, sync);
+    sync();
+  });
+  {  // last pass: outputs at j + r*Ns (Ns = N/R, j < Ns)
+    constexpr int R = FP::radix(P - 1);
+    constexpr int Ns = FP::ns(P - 1);
+    constexpr int NB = (N / R) / T;
+    static_assert(Ns * R == N, "plan does not multiply to N");
+    float2 v[NB][R];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = ti + b * T;
+      pass_load<N, R>(buf, j, v[b]);
+      apply_twiddles<N, R, Ns, INV>(v[b], j, tw);
+      Dft<R, INV>::run(v[b]);
+    }
+    if constexpr (LAST_SYNC) sync();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = ti + b * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) store(j + r * Ns, v[b][r]);
+    }
+  }
+}
+
+// Circular convolution core: y = IFFT_N( mul(FFT_N(x)) ), unnormalised inverse.
+// The last forward pass and the first inverse pass share their radix and the
+// butterfly->thread map, so the spectrum never touches shared memory: each
+// thread multiplies its own outputs (mul(idx, val) -> val) and runs the first
+// inverse butterfly in registers.
+template <int N, typename Load, typename Mul, typename Store, typename Sync>
+__device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __restrict__ tw,
+                                           Load&& load, Mul&& mul, Store&& store, Sync&& sync) {
+  using F = FftPlan<N, false>;
+  using B = FftPlan<N, true>;
+  constexpr int T = F::T;
+  constexpr int P = F::P;
+  static_assert(F::radix(P - 1) == B::radix(0), "fused middle needs matching radices");
+  {  // forward pass 0
+    constexpr int R = F::radix(0);
+    constexpr int NB = (N / R) / T;
+    float2 v[NB][R];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = ti + b * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
+      Dft<R, false>::run(v[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) pass_store<N, R, 1>(buf, ti + b * T, v[b]);
+  }
+  sync();
+  static_for<1, P - 1>([&](auto ic) {
+    constexpr int I = decltype(ic)::value;
+    pass_smem<N, F::radix(I), F::ns(I), T, false>(buf, ti, tw, sync);
+    sync();
+  });
+  {  // forward last pass -> pointwise multiply -> inverse pass 0, all in registers
+    constexpr int R = F::radix(P - 1);
+    constexpr int Ns = F::ns(P - 1);
+    constexpr int NB = (N / R) / T;
+    float2 v[NB][R];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = ti + b * T;
+      pass_load<N, R>(buf, j, v[b]);
+      apply_twiddles<N, R, Ns, false>(v[b], j, tw);
+      Dft<R, false>::run(v[b]);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b][r] = mul(j + r * Ns, v[b][r]);
+      Dft<R, true>::run(v[b]);  // inverse pass 0 (Ns = 1: no twiddles)
+    }
+    sync();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) pass_store<N, R, 1>(buf, ti + b * T, v[b]);
+  }
+  sync();
+  static_for<1, P - 1>([&](auto ic) {
+    constexpr int I = decltype(ic)::value;
+    pass_smem<N, B::radix(I), B::ns(I), T, true>(buf, ti, tw, sync);
+    sync();
+  });
+  {  // inverse last pass
+    constexpr int R = B::radix(P - 1);
+    constexpr int Ns = B::ns(P - 1);
+    constexpr int NB = (N / R) / T;
+    float2 v[NB][R];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = ti + b * T;
+      pass_load<N, R>(buf, j, v[b]);
+      apply_twiddles<N, R, Ns, true>(v[b], j, tw);
+      Dft<R, true>::run(v[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = ti + b * T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) store(j + r * Ns, v[b][r]);
+    }
+  }
+}
+
+}  // namespace lpbp

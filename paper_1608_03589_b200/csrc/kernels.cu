@@ -1,0 +1,446 @@
+// Device kernels of the log-polar backprojection hot path (sm_100a, fp32).
+//
+// Pipeline per slice (fastbp reference in parentheses):
+//   K1 ramp_filter   g -> g_f                  (filtering.py:54-70 filter_sinogram)
+//   K2 row_rdft      g -> G[m][t]              (first half of the rfft2 in logpolar.py:113,
+//                                               applied to sinogram rows, see below)
+//   K3 rho_conv      G -> Y[m][rho]            (grids.py:290-347 resampling + logpolar.py:100-118
+//                                               rho-axis FFT convolution with the kernel)
+//   K4 row_irdft     Y -> lp[rho][phi]         (phi-axis half of irfft2, logpolar.py:113-117)
+//   K5 readout       lp -> img                 (grids.py:399-443 logpolar_to_cartesian)
+//
+// Why K2 transforms sinogram rows rather than log-polar rows: both resampling
+// steps (sinogram->semi-polar->log-polar) act only along t/s with weights that
+// depend only on the row, and the phi<pi / phi>=pi halves are the same sinogram
+// columns.  So the phi-DFT of log-polar row i is a <=8-term combination of the
+// phi-DFTs of sinogram rows (the phi>=pi half picks up (-1)^m from its nphi/2
+// shift).  nt row FFTs replace nrho (~1.9x fewer) and the row mix moves into K3,
+// where it feeds the first rho-FFT pass straight from shared memory.
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace lpbp {
+
+namespace {
+__device__ __forceinline__ void block_sync() { __syncthreads(); }
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// K1: ramp filter along t (strided columns of g).  Two theta-columns are packed
+// as re/im of one complex M-point FFT (the response is real and even, so no
+// unpacking is needed).  Tile: all nt rows x TC columns staged in smem.
+// ---------------------------------------------------------------------------
+template <int M, int TC, int G>
+__global__ void __launch_bounds__(G * FftPlan<M, false>::T)
+k_ramp(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
+       const float* __restrict__ resp, const float2* __restrict__ tw) {
+  constexpr int T = FftPlan<M, false>::T;
+  constexpr int TP = TC + 1;  // tile pitch (floats)
+  extern __shared__ __align__(16) float2 smem_k1[];
+  float* tile = reinterpret_cast<float*>(smem_k1);                         // nt * TP floats
+  float2* bufs = smem_k1 + ((nt * TP + 1) / 2);
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  float2* buf = bufs + gi * padded_len(M);
+  const int c0 = blockIdx.x * TC;
+  const size_t slice = (size_t)blockIdx.y * nt * ntheta;
+  const float* src = g + slice;
+  float* dst = out + slice;
+
+  for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
+    const int t = e / TC, c = e % TC;
+    tile[t * TP + c] = __ldg(src + (size_t)t * ntheta + c0 + c);
+  }
+  __syncthreads();
+  for (int round = 0; round < TC / 2 / G; ++round) {
+    const int q = round * G + gi;
+    auto load = [&](int idx) -> float2 {
+      return idx < nt ? make_float2(tile[idx * TP + 2 * q], tile[idx * TP + 2 * q + 1]) : make_float2(0.f, 0.f);
+    };
+    auto mul = [&](int idx, float2 v) -> float2 { return cscale(v, __ldg(resp + idx)); };
+    auto store = [&](int idx, float2 v) {
+      if (idx < nt) {
+        tile[idx * TP + 2 * q] = v.x;
+        tile[idx * TP + 2 * q + 1] = v.y;
+      }
+    };
+    block_conv<M>(buf, ti, tw, load, mul, store, block_sync);
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
+    const int t = e / TC, c = e % TC;
+    dst[(size_t)t * ntheta + c0 + c] = tile[t * TP + c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: real DFT of sinogram rows, zero-padded from ntheta to nphi = 2 ntheta.
+// Rows t, t+1 are packed as re/im; spectra are separated with
+//   A[m] = (Z[m] + conj Z[-m]) / 2,  B[m] = (Z[m] - conj Z[-m]) / 2i
+// and staged as [m][TR] so the write of G[m][t0..t0+TR) is contiguous.
+// ---------------------------------------------------------------------------
+template <int NPHI, int TR, int G>
+__global__ void __launch_bounds__(G * FftPlan<NPHI, false>::T)
+k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const float2* __restrict__ tw) {
+  constexpr int T = FftPlan<NPHI, false>::T;
+  constexpr int NTH = NPHI / 2;
+  constexpr int NH = NPHI / 2 + 1;
+  constexpr int SP = TR + 1;
+  extern __shared__ __align__(16) float2 smem_k2[];
+  float2* stg = smem_k2;
+  float2* buf = smem_k2 + NH * SP + (threadIdx.x / T) * padded_len(NPHI);
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  const int t0 = blockIdx.x * TR;
+  const float* src = g + (size_t)blockIdx.y * nt * NTH;
+
+  for (int round = 0; round < TR / 2 / G; ++round) {
+    const int q = round * G + gi;
+    const float* ra = src + (size_t)(t0 + 2 * q) * NTH;
+    const float* rb = ra + NTH;
+    auto load = [&](int idx) -> float2 {
+      return idx < NTH ? make_float2(__ldg(ra + idx), __ldg(rb + idx)) : make_float2(0.f, 0.f);
+    };
+    auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
+    block_fft<NPHI, false, true>(buf, ti, tw, load, store, block_sync);
+    __syncthreads();
+    for (int m = ti; m < NH; m += T) {
+      const float2 z = buf[pad16(m)];
+      const float2 w = buf[pad16((NPHI - m) & (NPHI - 1))];
+      stg[m * SP + 2 * q] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
+      stg[m * SP + 2 * q + 1] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+    }
+    __syncthreads();
+  }
+  float2* dst = Gh + (size_t)blockIdx.y * NH * nt + t0;
+  for (int e = threadIdx.x; e < NH * TR; e += blockDim.x) {
+    const int m = e / TR, c = e % TR;
+    dst[(size_t)m * nt + c] = stg[m * SP + c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: per phi-frequency column m (one CTA), for every slice of the batch:
+//   p[k]  = wa0 G[a_k] + wa1 G[a_k+1] + (-1)^m (wb0 G[b_k] + wb1 G[b_k+1])   (semi-polar, grids.py:290-311)
+//   x[i]  = w0 p[k_i] + w1 p[k_i+1], i < nrho, 0 for i >= nrho            (log-polar, grids.py:332-347)
+//   Y[m]  = IFFT_L( FFT_L(x) * Khat[m] )[:nrho]                           (logpolar.py:112-117)
+// The row mix is evaluated inside the first forward pass; the multiply by
+// Khat is fused between the last forward and first inverse pass.
+// ---------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(FftPlan<L, false>::T)
+k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int ns, int nrho,
+           int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
+           const int* __restrict__ ki, const float2* __restrict__ wi, const float2* __restrict__ khat,
+           const float2* __restrict__ tw) {
+  constexpr int T = FftPlan<L, false>::T;
+  extern __shared__ __align__(16) float2 smem_k3[];
+  float2* buf = smem_k3;
+  float2* p = smem_k3 + padded_len(L);
+  const int m = blockIdx.x;
+  const float sg = (m & 1) ? -1.f : 1.f;
+  const int ti = threadIdx.x;
+  const float2* kcol = khat + (size_t)m * L;
+
+  for (int b = 0; b < batch; ++b) {
+    const float2* col = Gh + ((size_t)b * nh + m) * nt;
+    for (int k = ti; k < ns; k += T) {
+      const int2 A = __ldg(ab + k);
+      const float4 W = __ldg(wab + k);
+      const float2 g0 = __ldg(col + A.x), g1 = __ldg(col + A.x + 1);
+      const float2 h0 = __ldg(col + A.y), h1 = __ldg(col + A.y + 1);
+      float2 v;
+      v.x = fmaf(W.x, g0.x, W.y * g1.x) + sg * fmaf(W.z, h0.x, W.w * h1.x);
+      v.y = fmaf(W.x, g0.y, W.y * g1.y) + sg * fmaf(W.z, h0.y, W.w * h1.y);
+      p[k] = v;
+    }
+    __syncthreads();
+    auto load = [&](int idx) -> float2 {
+      if (idx >= nrho) return make_float2(0.f, 0.f);
+      const int k = __ldg(ki + idx);
+      const float2 w = __ldg(wi + idx);
+      const float2 p0 = p[k], p1 = p[k + 1];
+      return make_float2(fmaf(w.x, p0.x, w.y * p1.x), fmaf(w.x, p0.y, w.y * p1.y));
+    };
+    auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(kcol + idx)); };
+    float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
+    auto store = [&](int idx, float2 v) {
+      if (idx < nrho) ycol[idx] = v;
+    };
+    block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: inverse real DFT along phi for TR log-polar rows per CTA.  Rows i, i+1 are
+// packed: Z[k] = X_i[k] + i X_{i+1}[k] with Hermitian extension for k > nphi/2;
+// DC and Nyquist imaginary parts are dropped (numpy irfft convention).
+// ---------------------------------------------------------------------------
+template <int NPHI, int TR, int G>
+__global__ void __launch_bounds__(G * FftPlan<NPHI, true>::T)
+k_row_irdft(const float2* __restrict__ Yh, float* __restrict__ lp, int nrho, int nrho_pad,
+            const float2* __restrict__ tw) {
+  constexpr int T = FftPlan<NPHI, true>::T;
+  constexpr int NH = NPHI / 2 + 1;
+  constexpr int SP = TR + 1;
+  extern __shared__ __align__(16) float2 smem_k4[];
+  float2* stg = smem_k4;
+  float2* buf = smem_k4 + NH * SP + (threadIdx.x / T) * padded_len(NPHI);
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  const int i0 = blockIdx.x * TR;
+  const float2* src = Yh + (size_t)blockIdx.y * NH * nrho_pad + i0;
+  float* dst = lp + (size_t)blockIdx.y * nrho * NPHI;
+
+  for (int e = threadIdx.x; e < NH * TR; e += blockDim.x) {
+    const int m = e / TR, c = e % TR;
+    stg[m * SP + c] = (i0 + c < nrho) ? src[(size_t)m * nrho_pad + c] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  for (int round = 0; round < TR / 2 / G; ++round) {
+    const int q = round * G + gi;
+    const int ia = i0 + 2 * q, ib = ia + 1;
+    auto load = [&](int idx) -> float2 {
+      const bool hi = idx > NPHI / 2;
+      const int mm = hi ? NPHI - idx : idx;
+      float2 xa = stg[mm * SP + 2 * q], xb = stg[mm * SP + 2 * q + 1];
+      if (mm == 0 || mm == NPHI / 2) {
+        xa.y = 0.f;
+        xb.y = 0.f;
+      }
+      if (hi) {
+        xa.y = -xa.y;
+        xb.y = -xb.y;
+      }
+      return make_float2(xa.x - xb.y, xa.y + xb.x);
+    };
+    auto store = [&](int idx, float2 v) {
+      if (ia < nrho) dst[(size_t)ia * NPHI + idx] = v.x;
+      if (ib < nrho) dst[(size_t)ib * NPHI + idx] = v.y;
+    };
+    block_fft<NPHI, true, false>(buf, ti, tw, load, store, block_sync);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: bilinear readout at the Cartesian pixel centres.  Coordinates come from
+// the plan's fp64-built quadrant table; the other quadrants reflect phi:
+//   x<0,y>=0: pi - phi   x<0,y<0: pi + phi   x>=0,y<0: 2 pi - phi
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, int nrho, int nphi,
+          const uint32_t* __restrict__ qidx, const float2* __restrict__ qw, float scale) {
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= n * n) return;
+  const int iy = pix / n, jx = pix - iy * n;
+  const int c = n / 2;
+  const bool yneg = iy < c, xneg = jx < c;
+  const int qy = yneg ? (n - 1 - iy) - c : iy - c;
+  const int qx = xneg ? (n - 1 - jx) - c : jx - c;
+  const size_t slice = (size_t)blockIdx.y * n * n;
+  const uint32_t e = __ldg(qidx + qy * nq + qx);
+  float v = 0.f;
+  if (e != 0xFFFFFFFFu) {
+    const float2 w = __ldg(qw + qy * nq + qx);
+    const int i0 = (int)(e & 0xFFFFu);
+    const int jr = (int)(e >> 16);
+    int j0;
+    float wj;
+    if (!xneg && !yneg) {
+      j0 = jr;
+      wj = w.y;
+    } else if (xneg && yneg) {
+      j0 = nphi / 2 + jr;
+      wj = w.y;
+    } else {
+      const int Q = xneg ? nphi / 2 : nphi;  // fj = Q - fj_rep
+      if (w.y == 0.f) {
+        j0 = Q - jr;
+        wj = 0.f;
+      } else {
+        j0 = Q - jr - 1;
+        wj = 1.f - w.y;
+      }
+    }
+    if (j0 >= nphi) j0 -= nphi;
+    const int j1 = (j0 + 1 == nphi) ? 0 : j0 + 1;
+    const int i1 = min(i0 + 1, nrho - 1);
+    const float* l = lp + (size_t)blockIdx.y * nrho * nphi;
+    const float a00 = __ldg(l + (size_t)i0 * nphi + j0), a01 = __ldg(l + (size_t)i0 * nphi + j1);
+    const float a10 = __ldg(l + (size_t)i1 * nphi + j0), a11 = __ldg(l + (size_t)i1 * nphi + j1);
+    const float wi = w.x;
+    const float r0 = fmaf(wj, a01 - a00, a00);
+    const float r1 = fmaf(wj, a11 - a10, a10);
+    v = fmaf(wi, r1 - r0, r0) * scale;
+  }
+  img[slice + pix] = v;
+}
+
+// ---------------------------------------------------------------------------
+// Direct pixel-driven backprojector (reference.py:21-37), the accuracy
+// cross-check: b(x) = dtheta * sum_k lerp_t(g[:, k], (x . xi_k + 1) / dt).
+// The sinogram is transposed to angle-major first so a warp's 32 pixels read
+// one or two sectors per angle.
+// ---------------------------------------------------------------------------
+__global__ void k_transpose(const float* __restrict__ g, float* __restrict__ gT, int nt, int ntheta) {
+  __shared__ float tile[32][33];
+  const size_t slice = (size_t)blockIdx.z * nt * ntheta;
+  const int th0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int t = t0 + r, th = th0 + threadIdx.x;
+    if (t < nt && th < ntheta) tile[r][threadIdx.x] = g[slice + (size_t)t * ntheta + th];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int th = th0 + r, t = t0 + threadIdx.x;
+    if (t < nt && th < ntheta) gT[slice + (size_t)th * nt + t] = tile[threadIdx.x][r];
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_naive(const float* __restrict__ gT, float* __restrict__ img, int nt, int ntheta, int n,
+        const float2* __restrict__ cs, float dtheta) {
+  const int jx = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int iy = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (jx >= n || iy >= n) return;
+  const float a = (float)(2 * jx + 1 - n);
+  const float b = (float)(2 * iy + 1 - n);
+  const float half = 0.5f * (float)nt;
+  const float* src = gT + (size_t)blockIdx.z * nt * ntheta;
+  float acc = 0.f;
+#pragma unroll 4
+  for (int k = 0; k < ntheta; ++k) {
+    const float2 c = __ldg(cs + k);
+    const float f = fmaf(a, c.x, b * c.y) + half;
+    const float fl = floorf(f);
+    const float w = f - fl;
+    const int i0 = (int)fl;
+    const float* row = src + (size_t)k * nt;
+    const float v0 = (i0 >= 0 && i0 < nt) ? __ldg(row + i0) : 0.f;
+    const float v1 = (i0 + 1 >= 0 && i0 + 1 < nt) ? __ldg(row + i0 + 1) : 0.f;
+    acc += fmaf(w, v1 - v0, v0);
+  }
+  img[(size_t)blockIdx.z * n * n + (size_t)iy * n + jx] = acc * dtheta;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+namespace {
+template <typename K>
+cudaError_t prep(K kernel, size_t smem) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <int M, int TC, int G>
+cudaError_t ramp_impl(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s) {
+  if (d.ntheta % TC) return cudaErrorNotSupported;
+  const size_t smem = ((size_t)(d.nt * (TC + 1) + 1) / 2 + (size_t)G * padded_len(M)) * sizeof(float2);
+  auto k = k_ramp<M, TC, G>;
+  cudaError_t e = prep(k, smem);
+  if (e) return e;
+  k<<<dim3(d.ntheta / TC, batch), G * FftPlan<M, false>::T, smem, s>>>(g, out, d.nt, d.ntheta, t.ramp, t.tw_ramp);
+  return cudaGetLastError();
+}
+
+template <int NPHI, int TR, int G>
+cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch, cudaStream_t s) {
+  if (d.nt % TR) return cudaErrorNotSupported;
+  const size_t smem = ((size_t)(NPHI / 2 + 1) * (TR + 1) + (size_t)G * padded_len(NPHI)) * sizeof(float2);
+  auto k = k_row_rdft<NPHI, TR, G>;
+  cudaError_t e = prep(k, smem);
+  if (e) return e;
+  k<<<dim3(d.nt / TR, batch), G * FftPlan<NPHI, false>::T, smem, s>>>(g, Gh, d.nt, t.tw_phi);
+  return cudaGetLastError();
+}
+
+template <int L>
+cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
+  const size_t smem = ((size_t)padded_len(L) + d.ns) * sizeof(float2);
+  auto k = k_rho_conv<L>;
+  cudaError_t e = prep(k, smem);
+  if (e) return e;
+  k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, d.ns, d.nrho, d.nrho_pad, d.nh, t.ab, t.wab,
+                                              t.ki, t.wi, t.khat, t.tw_rho);
+  return cudaGetLastError();
+}
+
+template <int NPHI, int TR, int G>
+cudaError_t irdft_impl(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch, cudaStream_t s) {
+  if (d.nrho_pad % TR) return cudaErrorNotSupported;
+  const size_t smem = ((size_t)(NPHI / 2 + 1) * (TR + 1) + (size_t)G * padded_len(NPHI)) * sizeof(float2);
+  auto k = k_row_irdft<NPHI, TR, G>;
+  cudaError_t e = prep(k, smem);
+  if (e) return e;
+  k<<<dim3(d.nrho_pad / TR, batch), G * FftPlan<NPHI, true>::T, smem, s>>>(Yh, lp, d.nrho, d.nrho_pad, t.tw_phi);
+  return cudaGetLastError();
+}
+}  // namespace
+
+// Tile shapes per size: (columns or rows per CTA, concurrent FFTs per CTA).
+cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s) {
+  switch (d.M) {
+    case 512: return ramp_impl<512, 16, 4>(d, t, g, out, batch, s);
+    case 1024: return ramp_impl<1024, 16, 2>(d, t, g, out, batch, s);
+    case 2048: return ramp_impl<2048, 16, 2>(d, t, g, out, batch, s);
+    case 4096: return ramp_impl<4096, 16, 2>(d, t, g, out, batch, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch, cudaStream_t s) {
+  switch (d.nphi) {
+    case 512: return rdft_impl<512, 16, 4>(d, t, g, Gh, batch, s);
+    case 1024: return rdft_impl<1024, 16, 2>(d, t, g, Gh, batch, s);
+    case 2048: return rdft_impl<2048, 8, 2>(d, t, g, Gh, batch, s);
+    case 4096: return rdft_impl<4096, 8, 2>(d, t, g, Gh, batch, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
+  switch (d.L) {
+    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, s);
+    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, s);
+    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, s);
+    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, s);
+    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch, cudaStream_t s) {
+  switch (d.nphi) {
+    case 512: return irdft_impl<512, 16, 4>(d, t, Yh, lp, batch, s);
+    case 1024: return irdft_impl<1024, 16, 2>(d, t, Yh, lp, batch, s);
+    case 2048: return irdft_impl<2048, 8, 2>(d, t, Yh, lp, batch, s);
+    case 4096: return irdft_impl<4096, 8, 2>(d, t, Yh, lp, batch, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, float* img, int batch, cudaStream_t s) {
+  const int npix = d.n * d.n;
+  k_readout<<<dim3((npix + 255) / 256, batch), 256, 0, s>>>(lp, img, d.n, d.nq, d.nrho, d.nphi, t.qidx, t.qw,
+                                                            d.out_scale);
+  return cudaGetLastError();
+}
+cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dtheta, const float* g, float* gT,
+                         float* img, int batch, cudaStream_t s) {
+  k_transpose<<<dim3((ntheta + 31) / 32, (nt + 31) / 32, batch), dim3(32, 8), 0, s>>>(g, gT, nt, ntheta);
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  k_naive<<<dim3((n + 31) / 32, (n + 7) / 8, batch), 256, 0, s>>>(gT, img, nt, ntheta, n, cs, dtheta);
+  return cudaGetLastError();
+}
+
+bool sizes_supported(int nt, int ntheta, int L, bool filter) {
+  const int nphi = 2 * ntheta;
+  auto pow2in = [](int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; };
+  if (!pow2in(nphi, 512, 4096)) return false;
+  if (!pow2in(L, 512, 8192)) return false;
+  if (nt % 16) return false;
+  if (filter && !pow2in(2 * nt, 512, 4096)) return false;
+  if (filter && ntheta % 16) return false;
+  return true;
+}
+
+}  // namespace lpbp

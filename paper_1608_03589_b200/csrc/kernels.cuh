@@ -1,0 +1,47 @@
+// Launch wrappers for the log-polar backprojection kernels (sm_100a).
+// Layouts (all C-contiguous, fp32 / complex64 as float2):
+//   sinogram  g  [B][nt][ntheta]              (fastbp Sinogram.values, t outer)
+//   row spectra G [B][nh][nt]    nh = nphi/2+1 (phi-frequency major, t contiguous)
+//   conv spectra Y [B][nh][nrho_pad]          (phi-frequency major, rho contiguous)
+//   log-polar  lp [B][nrho][nphi]             (fastbp LogPolarImage.values)
+//   image     img [B][n][n]                   (fastbp CartesianImage.values, y outer)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lpbp {
+
+struct DevTables {
+  // twiddle tables exp(-2 pi i k / N), k < N
+  const float2* tw_phi;   // N = nphi
+  const float2* tw_rho;   // N = L
+  const float2* tw_ramp;  // N = M = 2 nt (FBP only)
+  const float* ramp;      // [M] real even filter response incl. 1/M (FBP only)
+  const int2* ab;         // [ns] t-rows (a_k, b_k) of the semi-polar lerp
+  const float4* wab;      // [ns] weights (wa0, wa1, wb0, wb1)
+  const int* ki;          // [nrho] s-row of the log-polar lerp
+  const float2* wi;       // [nrho] weights (w0, w1)
+  const float2* khat;     // [nh][L] kernel spectrum incl. 0.5*drho*dphi/(L*nphi)
+  const uint32_t* qidx;   // [nq][nq] readout quadrant table: i0 | j0 << 16, ~0 = zero pixel
+  const float2* qw;       // [nq][nq] readout weights (wi, wj)
+  const float2* naive_cs; // [ntheta] (cos, sin) * nt/(2n) for the direct backprojector
+};
+
+struct Dims {
+  int nt, ntheta, n, ns, nphi, nh, nrho, nrho_pad, L, M, nq;
+  float out_scale;        // 1 (backprojection) or 1/(2 pi) (fbp)
+};
+
+// Each returns cudaGetLastError() after the launch (0 on success) or
+// cudaErrorNotSupported when no instantiation exists for the size.
+cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s);
+cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* G, int batch, cudaStream_t s);
+cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, cudaStream_t s);
+cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch, cudaStream_t s);
+cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, float* img, int batch, cudaStream_t s);
+cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dtheta, const float* g, float* gT,
+                         float* img, int batch, cudaStream_t s);
+
+bool sizes_supported(int nt, int ntheta, int L, bool filter);
+
+}  // namespace lpbp

@@ -1,0 +1,302 @@
+// fp64 host construction of plan tables.  See plan_host.h.
+#include "plan_host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <thread>
+
+namespace lpbp {
+
+namespace {
+
+using cd = std::complex<double>;
+constexpr double kPi = 3.14159265358979323846;
+
+int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// In-place iterative radix-2 complex FFT (forward, exp(-2 pi i nk/N)), fp64.
+void fft_pow2(std::vector<cd>& a, const std::vector<cd>& w /* w[k] = exp(-2 pi i k/N), k < N/2 */) {
+  const int n = (int)a.size();
+  for (int i = 1, j = 0; i < n; ++i) {
+    int bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (int len = 2; len <= n; len <<= 1) {
+    const int step = n / len;
+    for (int i = 0; i < n; i += len) {
+      for (int k = 0; k < len / 2; ++k) {
+        const cd u = a[i + k], v = a[i + k + len / 2] * w[k * step];
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+    }
+  }
+}
+
+std::vector<F2> twiddle_table(int N) {
+  std::vector<F2> t(N);
+  for (int k = 0; k < N; ++k) {
+    const double a = -2.0 * kPi * (double)k / (double)N;
+    t[k] = F2{(float)std::cos(a), (float)std::sin(a)};
+  }
+  return t;
+}
+
+// Linear-interpolation tap of fastbp.grids._lerp_axis0 (grids.py:255-269):
+//   value = [0<=i0<n] v[i0] (1-w) + [0<=i0+1<n] v[i0+1] w,  i0 = floor(f), w = f - i0
+// re-expressed as (base, w0, w1) over rows base, base+1 with base in [0, n-2]
+// and out-of-range terms folded to zero weight.
+void lerp_tap(double f, int n, int32_t& base, double& w0, double& w1) {
+  const double fl = std::floor(f);
+  const long long i0 = (long long)fl;
+  const double w = f - fl;
+  const double a0 = (i0 >= 0 && i0 < n) ? (1.0 - w) : 0.0;       // weight of row i0
+  const double a1 = (i0 + 1 >= 0 && i0 + 1 < n) ? w : 0.0;        // weight of row i0+1
+  if (i0 >= 0 && i0 <= n - 2) {
+    base = (int32_t)i0; w0 = a0; w1 = a1;
+  } else if (i0 == n - 1) {
+    base = n - 2; w0 = 0.0; w1 = a0;
+  } else if (i0 == -1) {
+    base = 0; w0 = a1; w1 = 0.0;
+  } else {
+    base = i0 < 0 ? 0 : n - 2; w0 = 0.0; w1 = 0.0;
+  }
+}
+
+}  // namespace
+
+double adaptive_rho0(int nx, int ny) { return std::log(std::min(2.0 / nx, 2.0 / ny)) - std::log(2.0); }
+
+std::string mesh_for(int ns, double rho0, int nrho_in, int& nrho_out) {
+  const double ds = 2.0 / ns;
+  int nrho = nrho_in;
+  if (nrho <= 0) nrho = std::max(2, (int)std::ceil(-rho0 / -std::log1p(-ds)));
+  const double drho = -rho0 / nrho;
+  if (1.0 - std::exp(-drho) > ds * (1.0 + 1e-9)) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf,
+                  "log-polar mesh too coarse: largest radial step %.3e exceeds the sinogram step %.3e",
+                  1.0 - std::exp(-drho), ds);
+    return buf;
+  }
+  nrho_out = nrho;
+  return "";
+}
+
+int next_fast_len(int target) {
+  if (target <= 1) return 1;
+  for (int v = target;; ++v) {
+    int r = v;
+    for (int p : {2, 3, 5, 7, 11})
+      while (r % p == 0) r /= p;
+    if (r == 1) return v;
+  }
+}
+
+std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
+  if (p.nt < 2 || p.ntheta < 1) return "nt must be >= 2 and ntheta >= 1";
+  if (p.n < 2) return "n_out must be >= 2";
+  if (p.has_rho0 && !(p.rho0 < 0)) return "rho0 must be negative";
+  if (p.nrho != 0 && p.nrho < 2) return "nrho must be >= 2";
+  if (p.filter) {
+    if (p.lam < 0) return "lambda must be >= 0";
+    if (!(p.cutoff > 0.0 && p.cutoff <= 1.0)) return "cutoff must lie in (0, 1]";
+  }
+  h.nt = p.nt;
+  h.ntheta = p.ntheta;
+  h.n = p.n;
+  h.filter = p.filter;
+  h.ns = p.nt / 2;  // logpolar.py:131
+  if (h.ns < 2) return "ns must be >= 2";
+  h.nphi = 2 * p.ntheta;  // grids.py:303
+  h.nh = h.nphi / 2 + 1;
+  h.rho0 = p.has_rho0 ? p.rho0 : adaptive_rho0(p.n, p.n);  // logpolar.py:132
+  std::string err = mesh_for(h.ns, h.rho0, p.nrho, h.nrho);  // logpolar.py:133
+  if (!err.empty()) return err;
+  h.drho = -h.rho0 / h.nrho;              // grids.py:183
+  h.dphi = 2.0 * kPi / h.nphi;            // grids.py:187
+  h.nrho_pad = (h.nrho + 15) / 16 * 16;
+  h.out_scale = p.filter ? 1.0 / (2.0 * kPi) : 1.0;  // filtering.py:27,98
+  const int nt = p.nt, ns = h.ns, nrho = h.nrho, nphi = h.nphi, nh = h.nh;
+  const double dt = 2.0 / nt;  // grids.py:112
+
+  // --- semi-polar taps (grids.py:290-311): s_k = k/(ns-1), f = (+-s + 1)/dt
+  h.ab.resize(ns);
+  h.wab.resize(ns);
+  for (int k = 0; k < ns; ++k) {
+    const double s = (double)k / (ns - 1.0);
+    int32_t a, b;
+    double wa0, wa1, wb0, wb1;
+    lerp_tap((s + 1.0) / dt, nt, a, wa0, wa1);
+    lerp_tap((-s + 1.0) / dt, nt, b, wb0, wb1);
+    h.ab[k] = I2{a, b};
+    h.wab[k] = F4{(float)wa0, (float)wa1, (float)wb0, (float)wb1};
+  }
+  // --- log-polar taps (grids.py:332-347): rho_i = rho0 + (i+1) drho, f = e^rho (ns-1)
+  h.ki.resize(nrho);
+  h.wi.resize(nrho);
+  for (int i = 0; i < nrho; ++i) {
+    const double rho = h.rho0 + (double)(i + 1) * h.drho;
+    int32_t k;
+    double w0, w1;
+    lerp_tap(std::exp(rho) * (ns - 1.0), ns, k, w0, w1);
+    h.ki[i] = k;
+    h.wi[i] = F2{(float)w0, (float)w1};
+  }
+
+  // --- kernel support (logpolar.py:66-81, rolled by -nphi/2 at :110):
+  // cell (k, l) holds 1/drho iff |e^{k drho} cos(theta_j) - 1| <= drho with
+  // theta_j = -pi + j*2pi/nphi and j = (l + nphi/2) mod nphi.
+  std::vector<double> costab(nphi);
+  for (int j = 0; j < nphi; ++j) costab[j] = std::cos(-kPi + (double)j * (2.0 * kPi / nphi));
+  std::vector<std::vector<int>> cells(nrho);
+  h.kmax = 0;
+  h.nnz = 0;
+  h.cell_k.clear();
+  h.cell_l.clear();
+  for (int k = 0; k < nrho; ++k) {
+    const double e = std::exp((double)k * h.drho);
+    for (int l = 0; l < nphi; ++l) {
+      const int j = (l + nphi / 2) % nphi;
+      if (std::fabs(e * costab[j] - 1.0) <= h.drho) {
+        cells[k].push_back(l);
+        h.cell_k.push_back(k);
+        h.cell_l.push_back(l);
+        h.kmax = k;
+        ++h.nnz;
+      }
+    }
+  }
+  h.L = std::max(512, next_pow2(nrho + h.kmax));
+  const int L = h.L;
+
+  // --- kernel spectrum Khat[m][kappa] = FFT_L over k of KPhi[k][m], with
+  // KPhi[k][m] = sum_{l in cells_k} (1/drho) e^{-2 pi i l m / nphi} and the
+  // output scale LOGPOLAR_SCALE * drho * dphi (logpolar.py:47,117) plus the
+  // unnormalised inverse FFTs' 1/(L * nphi) folded in.
+  std::vector<cd> ctab(nphi);
+  for (int q = 0; q < nphi; ++q) ctab[q] = std::polar(1.0, -2.0 * kPi * (double)q / nphi);
+  std::vector<cd> wL(L / 2);
+  for (int k = 0; k < L / 2; ++k) wL[k] = std::polar(1.0, -2.0 * kPi * (double)k / L);
+  const double kscale = 0.5 * h.drho * h.dphi / ((double)L * nphi) / h.drho;  // cell value 1/drho
+  h.khat.assign((size_t)nh * L, F2{0, 0});
+  {
+    const int nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int tid = 0; tid < nthreads; ++tid) {
+      pool.emplace_back([&, tid]() {
+        std::vector<cd> col(L);
+        for (int m = tid; m < nh; m += nthreads) {
+          std::fill(col.begin(), col.end(), cd(0, 0));
+          for (int k = 0; k <= h.kmax; ++k) {
+            cd acc(0, 0);
+            for (int l : cells[k]) acc += ctab[(int)(((long long)l * m) % nphi)];
+            col[k] = acc;
+          }
+          fft_pow2(col, wL);
+          F2* dst = h.khat.data() + (size_t)m * L;
+          for (int q = 0; q < L; ++q) dst[q] = F2{(float)(col[q].real() * kscale), (float)(col[q].imag() * kscale)};
+        }
+      });
+    }
+    for (auto& t : pool) t.join();
+  }
+
+  // --- twiddle tables
+  h.tw_phi = twiddle_table(nphi);
+  h.tw_rho = twiddle_table(L);
+
+  // --- ramp / Tikhonov filter (filtering.py:54-70).  The reference multiplies
+  // by resp on an Lr = next_fast_len(8 nt) grid; that is a convolution with the
+  // real even taps h[d] = (1/Lr) sum_k resp_k cos(2 pi k d / Lr), |d| < nt.
+  // The same taps periodised on M = 2 nt give an exact circular embedding.
+  if (p.filter) {
+    const int Lr = next_fast_len(8 * nt);
+    h.ramp_len_ref = Lr;
+    const double val = 1.0 / (Lr * dt);  // numpy.fft.fftfreq
+    const double cut = p.cutoff * kPi / dt;
+    std::vector<double> resp(Lr);
+    const int Npos = (Lr - 1) / 2 + 1;
+    for (int k = 0; k < Lr; ++k) {
+      const long long f = k < Npos ? k : (long long)k - Lr;
+      const double sigma = 2.0 * kPi * ((double)f * val);
+      const double a = std::fabs(sigma);
+      resp[k] = (std::fabs(sigma) > cut) ? 0.0 : a / (1.0 + p.lam * a);
+    }
+    std::vector<double> cosr(Lr);
+    for (int q = 0; q < Lr; ++q) cosr[q] = std::cos(2.0 * kPi * (double)q / Lr);
+    std::vector<double> taps(nt);
+    for (int d = 0; d < nt; ++d) {
+      double acc = 0.0;
+      long long ph = 0;
+      for (int k = 0; k < Lr; ++k) {
+        acc += resp[k] * cosr[ph];
+        ph += d;
+        if (ph >= Lr) ph -= Lr;
+      }
+      taps[d] = acc / Lr;
+    }
+    h.M = 2 * nt;
+    const int M = h.M;
+    std::vector<double> cosm(M);
+    for (int q = 0; q < M; ++q) cosm[q] = std::cos(2.0 * kPi * (double)q / M);
+    h.ramp.resize(M);
+    for (int kap = 0; kap < M; ++kap) {
+      double acc = taps[0];
+      long long ph = 0;
+      for (int d = 1; d < nt; ++d) {
+        ph += kap;
+        if (ph >= M) ph -= M;
+        acc += 2.0 * taps[d] * cosm[ph];
+      }
+      h.ramp[kap] = (float)(acc / M);
+    }
+    h.tw_ramp = twiddle_table(M);
+  }
+
+  // --- readout quadrant table (grids.py:399-443) at x, y >= 0; the device
+  // reflects phi for the other quadrants.
+  const int c = p.n / 2;
+  h.nq = p.n - c;
+  h.qidx.assign((size_t)h.nq * h.nq, 0xFFFFFFFFu);
+  h.qw.assign((size_t)h.nq * h.nq, F2{0, 0});
+  for (int qy = 0; qy < h.nq; ++qy) {
+    const double y = -1.0 + ((double)(c + qy) + 0.5) * (2.0 / p.n);
+    for (int qx = 0; qx < h.nq; ++qx) {
+      const double x = -1.0 + ((double)(c + qx) + 0.5) * (2.0 / p.n);
+      const double r = std::hypot(x, y);
+      if (!(r <= 1.0 && r > 0.0)) continue;
+      const double rho = std::log(r);
+      if (!(rho >= h.rho0)) continue;
+      double fi = (rho - h.rho0) / h.drho - 1.0;
+      if (fi >= -1.0 && fi < 0.0) fi = 0.0;
+      fi = std::min(std::max(fi, 0.0), (double)(nrho - 1));
+      double phi = std::fmod(std::atan2(y, x), 2.0 * kPi);
+      if (phi < 0) phi += 2.0 * kPi;
+      const double fj = phi / h.dphi;
+      const double i0 = std::floor(fi), j0 = std::floor(fj);
+      const int ji = ((int)j0 % nphi + nphi) % nphi;
+      h.qidx[(size_t)qy * h.nq + qx] = (uint32_t)i0 | ((uint32_t)ji << 16);
+      h.qw[(size_t)qy * h.nq + qx] = F2{(float)(fi - i0), (float)(fj - j0)};
+    }
+  }
+
+  // --- direct backprojector angle table (reference.py:30-36)
+  h.naive_cs.resize(p.ntheta);
+  const double dtheta = kPi / p.ntheta;
+  for (int k = 0; k < p.ntheta; ++k) {
+    const double th = k * dtheta;
+    h.naive_cs[k] = F2{(float)(std::cos(th) * nt / (2.0 * p.n)), (float)(std::sin(th) * nt / (2.0 * p.n))};
+  }
+  return "";
+}
+
+}  // namespace lpbp

@@ -1,0 +1,52 @@
+// Host-side (fp64) construction of the constant tables of a log-polar
+// backprojection plan.  Every formula restates the fastbp reference so the
+// device pipeline reproduces it; file:line citations refer to
+// /root/reference/pkg/src/fastbp.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace lpbp {
+
+struct F2 { float x, y; };
+struct I2 { int32_t x, y; };
+struct F4 { float x, y, z, w; };
+
+struct HostPlanParams {
+  int nt, ntheta, n;
+  bool has_rho0;
+  double rho0;
+  int nrho;       // 0 = automatic (_mesh_for)
+  bool filter;    // fbp: filter_sinogram + 1/(2 pi)
+  double lam, cutoff;
+};
+
+struct HostPlan {
+  // geometry
+  int nt = 0, ntheta = 0, n = 0, ns = 0, nphi = 0, nh = 0, nrho = 0, nrho_pad = 0, L = 0, M = 0, nq = 0;
+  int kmax = 0, nnz = 0, ramp_len_ref = 0;
+  double rho0 = 0, drho = 0, dphi = 0, out_scale = 1;
+  bool filter = false;
+  // tables (uploaded to the device)
+  std::vector<F2> tw_phi, tw_rho, tw_ramp, khat, wi, qw, naive_cs;
+  std::vector<float> ramp;
+  std::vector<I2> ab;
+  std::vector<F4> wab;
+  std::vector<int32_t> ki;
+  std::vector<uint32_t> qidx;
+  // kernel support (for diagnostics/tests): cells (k, l) of the rolled kernel
+  std::vector<int32_t> cell_k, cell_l;
+};
+
+// Returns "" on success, else the error message (ValueError semantics).
+std::string build_host_plan(const HostPlanParams& p, HostPlan& out);
+
+// fastbp.grids.adaptive_rho0 (grids.py:385-391)
+double adaptive_rho0(int nx, int ny);
+// fastbp.logpolar._mesh_for (logpolar.py:84-97); returns "" or error message
+std::string mesh_for(int ns, double rho0, int nrho_in, int& nrho_out);
+// scipy.fft.next_fast_len(target) for complex transforms: smallest 11-smooth >= target
+int next_fast_len(int target);
+
+}  // namespace lpbp

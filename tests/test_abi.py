@@ -1,0 +1,185 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol of
+include/lpbp.h, validates arguments with the reference's messages, and its
+host-only plans (device = -1) build fp64 tables that reproduce the oracle when
+the device dataflow is emulated in numpy."""
+
+import ctypes
+import math
+import os
+import re
+from ctypes import byref, c_size_t, c_void_p
+
+import numpy as np
+import pytest
+
+from oracle import fastbp_oracle as O
+from paper_1608_03589_b200 import _native as N
+
+from conftest import REPO
+
+
+def header_symbols():
+    text = open(os.path.join(REPO, "include", "lpbp.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:[\w\*]+\s+)+\**(lpbp_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_exports_every_header_symbol():
+    lib = N.lib()
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(N.SIGNATURES) == syms
+    assert lib.lpbp_version() >= 100
+
+
+def make(nt, ntheta, n, rho0=None, nrho=None, filt=None, device=-1):
+    p = N.Params()
+    p.nt, p.ntheta, p.n_out = nt, ntheta, n
+    p.has_rho0, p.rho0 = (0, 0.0) if rho0 is None else (1, rho0)
+    p.nrho = nrho or 0
+    p.filter, (p.lam, p.cutoff) = (0, (0.0, 1.0)) if filt is None else (1, filt)
+    p.device = device
+    h = c_void_p()
+    N.check(N.lib().lpbp_plan_create(byref(p), byref(h)))
+    return h
+
+
+class HostPlan:
+    def __init__(self, *a, **k):
+        self.h = make(*a, **k)
+        self.info = N.PlanInfo()
+        N.check(N.lib().lpbp_plan_get_info(self.h, byref(self.info)))
+
+    def __del__(self):
+        N.lib().lpbp_plan_destroy(self.h)
+
+    def table(self, which, dtype, width=1):
+        n = c_size_t()
+        N.check(N.lib().lpbp_plan_table(self.h, which.encode(), None, 0, byref(n)))
+        a = np.zeros(n.value * width, dtype=dtype)
+        N.check(N.lib().lpbp_plan_table(self.h, which.encode(), c_void_p(a.ctypes.data), n.value, byref(n)))
+        return a.reshape(-1, width) if width > 1 else a
+
+
+@pytest.mark.parametrize("nt,n", [(256, 256), (512, 512), (2048, 2048)])
+def test_geometry_and_kernel_support(nt, n):
+    hp = HostPlan(nt, nt, n, filt=(0.0, 1.0))
+    ns, r0, nr, drho = O.lp_geometry(nt, n)
+    i = hp.info
+    assert (i.ns, i.nrho, i.nphi) == (ns, nr, 2 * nt)
+    assert i.rho0 == r0 and i.drho == drho
+    kern = np.roll(O.lp_kernel(nr, 2 * nt, drho), -nt, axis=1)
+    k, l = np.nonzero(kern)
+    cells = hp.table("kernel_cells", np.int32, 2)
+    assert np.array_equal(cells[:, 0], k) and np.array_equal(cells[:, 1], l)
+    assert i.kmax == k.max() and i.L >= nr + i.kmax and (i.L & (i.L - 1)) == 0
+    assert i.M == 2 * nt and abs(i.out_scale - 1 / (2 * math.pi)) < 1e-15
+
+
+def emulate_device(hp, g):
+    """numpy (fp64) emulation of the K2..K5 dataflow using the plan's tables."""
+    i = hp.info
+    nt, nth = g.shape
+    nphi, nh, nrho, L, ns = i.nphi, i.nphi // 2 + 1, i.nrho, i.L, i.ns
+    G = np.fft.rfft(g, n=nphi, axis=1).T  # [m][t]     (K2)
+    ab = hp.table("ab", np.int32, 2)
+    wab = hp.table("wab", np.float32, 4).astype(np.float64)
+    ki = hp.table("ki", np.int32)
+    wi = hp.table("wi", np.float32, 2).astype(np.float64)
+    khat = hp.table("khat", np.complex64).reshape(nh, L).astype(np.complex128)
+    sg = np.where(np.arange(nh) % 2 == 1, -1.0, 1.0)[:, None]
+    p = (wab[:, 0] * G[:, ab[:, 0]] + wab[:, 1] * G[:, ab[:, 0] + 1]
+         + sg * (wab[:, 2] * G[:, ab[:, 1]] + wab[:, 3] * G[:, ab[:, 1] + 1]))      # [m][k]   (K3 p)
+    x = wi[:, 0] * p[:, ki] + wi[:, 1] * p[:, ki + 1]                              # [m][i]
+    y = np.fft.ifft(np.fft.fft(x, n=L, axis=1) * khat, axis=1)[:, :nrho] * L       # unnormalised inverse
+    yt = y.T.copy()
+    yt[:, 0] = yt[:, 0].real
+    yt[:, -1] = yt[:, -1].real
+    lp = np.fft.irfft(yt, n=nphi, axis=1) * nphi                                   # (K4)
+    return lp
+
+
+def emulate_readout(hp, lp):
+    i = hp.info
+    n, nrho, nphi = i.n_out, i.nrho, i.nphi
+    qidx = hp.table("qidx", np.uint32)
+    qw = hp.table("qw", np.float32, 2)
+    c = n // 2
+    nq = n - c
+    iy, jx = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    yneg, xneg = iy < c, jx < c
+    qy = np.where(yneg, (n - 1 - iy) - c, iy - c)
+    qx = np.where(xneg, (n - 1 - jx) - c, jx - c)
+    e = qidx[qy * nq + qx]
+    w = qw[qy * nq + qx].astype(np.float64)
+    valid = e != 0xFFFFFFFF
+    i0 = (e & 0xFFFF).astype(np.int64)
+    jr = np.where(valid, (e >> 16).astype(np.int64), 0)
+    wjr = w[..., 1]
+    Q = np.where(xneg & ~yneg, nphi // 2, nphi)
+    refl = xneg ^ yneg
+    j0 = np.where(~refl, np.where(xneg & yneg, nphi // 2 + jr, jr), np.where(wjr == 0, Q - jr, Q - jr - 1))
+    wj = np.where(~refl, wjr, np.where(wjr == 0, 0.0, 1.0 - wjr))
+    j0 = np.where(j0 >= nphi, j0 - nphi, j0)
+    j1 = np.where(j0 + 1 == nphi, 0, j0 + 1)
+    i0 = np.where(valid, i0, 0)
+    i1 = np.minimum(i0 + 1, nrho - 1)
+    wi = w[..., 0]
+    r0 = lp[i0, j0] + wj * (lp[i0, j1] - lp[i0, j0])
+    r1 = lp[i1, j0] + wj * (lp[i1, j1] - lp[i1, j0])
+    return np.where(valid, (r0 + wi * (r1 - r0)) * i.out_scale, 0.0)
+
+
+@pytest.mark.parametrize("nt,nth,n,rho0,nrho", [(256, 256, 256, None, None), (512, 256, 300, None, None),
+                                                (512, 256, 256, -4.0, 600), (256, 128, 255, None, None)])
+def test_tables_reproduce_oracle(golden, nt, nth, n, rho0, nrho):
+    rng = np.random.default_rng(nt + n)
+    g = rng.standard_normal((nt, nth)).cumsum(axis=0) * 0.05
+    hp = HostPlan(nt, nth, n, rho0=rho0, nrho=nrho)
+    lp = emulate_device(hp, g)
+    ref_lp = O.logpolar_stage(g, n, rho0, nrho)
+    assert O.relative_l2(lp, ref_lp) < 2e-6  # fp32-rounded tables
+    img = emulate_readout(hp, ref_lp)
+    ref = O.lp_readout(ref_lp, hp.info.rho0, n, n)
+    assert O.relative_l2(img, ref) < 1e-6
+    assert np.array_equal(img == 0, ref == 0)
+
+
+def test_ramp_table_reproduces_filter_sinogram():
+    nt, nth = 512, 64
+    rng = np.random.default_rng(3)
+    g = rng.standard_normal((nt, nth))
+    for lam, cut in ((0.0, 1.0), (0.05, 0.8)):
+        hp = HostPlan(nt, nth, 128, filt=(lam, cut))
+        H = hp.table("ramp", np.float32).astype(np.float64)
+        M = hp.info.M
+        out = np.fft.ifft(np.fft.fft(g, n=M, axis=0) * H[:, None], axis=0).real[:nt] * M
+        assert O.relative_l2(out, O.ramp_filter(g, lam, cut)) < 1e-6
+
+
+def test_validation_messages():
+    with pytest.raises(ValueError, match="n_out must be >= 2"):
+        make(256, 256, 1)
+    with pytest.raises(ValueError, match="rho0 must be negative"):
+        make(256, 256, 64, rho0=0.25)
+    with pytest.raises(ValueError, match="nrho must be >= 2"):
+        make(256, 256, 64, nrho=1)
+    with pytest.raises(ValueError, match="log-polar mesh too coarse"):
+        make(64, 16, 16, nrho=3)
+    with pytest.raises(ValueError, match="nt must be >= 2"):
+        make(1, 16, 16)
+    with pytest.raises(ValueError, match="cutoff must lie in"):
+        make(256, 256, 64, filt=(0.0, 1.5))
+    with pytest.raises(ValueError, match="lambda must be >= 0"):
+        make(256, 256, 64, filt=(-1.0, 1.0))
+
+
+def test_host_only_plan_refuses_execution():
+    hp = HostPlan(256, 256, 256)
+    buf = (ctypes.c_float * 16)()
+    with pytest.raises(ValueError, match="host-only"):
+        N.check(N.lib().lpbp_execute(hp.h, ctypes.addressof(buf), ctypes.addressof(buf), 1, None, 0, None))
+    ws = c_size_t()
+    N.check(N.lib().lpbp_workspace_bytes(hp.h, 4, byref(ws)))
+    assert ws.value >= 4 * hp.info.workspace_per_slice - 1024

@@ -1,0 +1,181 @@
+"""GPU parity: the sm_100a path (through liblpbp.so's C ABI) against the
+reference's golden vectors and the CPU oracle.  Bar: relative L2 <= 1e-4 in
+fp32 (BASELINE.json north_star), max-abs reported."""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import fastbp_oracle as O
+from oracle import phantoms
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4  # north_star: relative L2 <= 1e-4 in fp32
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    import paper_1608_03589_b200 as p
+    return p
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def report(name, got, ref):
+    r = O.relative_l2(got, ref)
+    m = O.max_abs(got, ref)
+    print(f"{name}: rel_l2={r:.3e} max_abs={m:.3e}")
+    return r
+
+
+def test_native_library_is_loaded(pkg):
+    import ctypes
+    from paper_1608_03589_b200 import _native
+    lib = _native.lib()
+    assert lib._name.endswith("liblpbp.so")
+
+
+def test_cfg0_backprojection_vs_reference_golden(pkg, golden):
+    z = golden("cfg0.npz")
+    g = pkg.Sinogram(256, 256, z["sino"].astype(np.float64))
+    img = pkg.logpolar_backproject(g, 256)
+    assert report("cfg0 bp", img.values, z["bp"]) <= RTOL
+
+
+def test_cfg0_stages(pkg, golden):
+    z = golden("cfg0.npz")
+    plan = pkg.get_plan(256, 256, 256, None, None, None)
+    lp = plan.logpolar(dev(z["sino"])[None])[0].cpu().numpy()
+    assert report("cfg0 logpolar stage", lp, z["lp"]) <= RTOL
+    # readout alone, fed the oracle's log-polar image
+    ref_lp = O.logpolar_stage(z["sino"].astype(np.float64), 256)
+    img = plan.readout(dev(ref_lp)[None])[0].cpu().numpy()
+    assert report("cfg0 readout", img, O.lp_readout(ref_lp, plan.rho0, 256, 256)) <= 1e-6
+
+
+def test_cfg0_fbp_and_filter(pkg, golden):
+    z = golden("cfg0.npz")
+    g = pkg.Sinogram(256, 256, z["sino"].astype(np.float64))
+    f = pkg.filter_sinogram(g, pkg.FilterSpec())
+    assert report("cfg0 filter", f.values, z["filtered"]) <= 1e-5
+    img = pkg.fbp(g, pkg.FilterSpec(), engine="logpolar", n=256)
+    assert report("cfg0 fbp", img.values, z["fbp"]) <= RTOL
+
+
+def test_cfg1_fbp_batch_vs_oracle(pkg, golden):
+    z = golden("cfg1.npz")
+    sinos = np.stack([phantoms.config_sinogram(1, i) for i in range(16)])
+    assert np.array_equal(sinos[0], z["sino"])
+    out = pkg.fbp_batch(dev(sinos), pkg.FilterSpec(), 512).cpu().numpy()
+    assert report("cfg1 fbp slice0 vs reference", out[0], z["fbp"]) <= RTOL
+    for i in (1, 7, 15):
+        ref = O.fbp_logpolar(sinos[i].astype(np.float64), 512)
+        assert report(f"cfg1 fbp slice{i} vs oracle", out[i], ref) <= RTOL
+
+
+def test_tikhonov_cutoff(pkg, golden):
+    z = golden("cfg1.npz")
+    g = pkg.Sinogram(512, 512, z["sino"].astype(np.float64))
+    img = pkg.fbp(g, pkg.FilterSpec(lam=0.02, cutoff=0.9), engine="logpolar", n=512)
+    assert report("cfg1 tikhonov", img.values, z["fbp_tik"]) <= RTOL
+
+
+def test_options_nonsquare_odd(pkg, golden):
+    z = golden("opts.npz")
+    g = pkg.Sinogram(512, 256, z["sino"].astype(np.float64))
+    assert report("opts default", pkg.logpolar_backproject(g, 256).values, z["bp_default"]) <= RTOL
+    o = pkg.LogPolarOptions(rho0=-4.0, nrho=600)
+    assert report("opts rho0/nrho", pkg.logpolar_backproject(g, 256, o).values, z["bp_opts"]) <= RTOL
+    assert report("opts n=300", pkg.logpolar_backproject(g, 300).values, z["bp_n300"]) <= RTOL
+    ref = O.logpolar_backproject(z["sino"].astype(np.float64), 255)
+    assert report("opts n=255 (odd)", pkg.logpolar_backproject(g, 255).values, ref) <= RTOL
+
+
+def test_zero_linearity_and_batch_invariance(pkg):
+    plan = pkg.get_plan(512, 512, 512, None, None, (0.0, 1.0))
+    zero = torch.zeros((2, 512, 512), device="cuda")
+    assert torch.count_nonzero(plan.execute(zero)) == 0
+    a = dev(phantoms.config_sinogram(1, 3))[None]
+    b = dev(phantoms.config_sinogram(1, 4))[None]
+    ia, ib = plan.execute(a), plan.execute(b)
+    iab = plan.execute(2.0 * a - 0.5 * b)
+    assert O.relative_l2((iab).cpu().numpy(), (2.0 * ia - 0.5 * ib).cpu().numpy()) < 1e-5
+    # a slice's result does not depend on its batch neighbours or the chunking
+    batch = torch.cat([b, a, b, a, a], 0)
+    full = plan.execute(batch, chunk=5)
+    ch = plan.execute(batch, chunk=2)
+    assert torch.equal(full, ch)
+    assert torch.equal(full[1], ia[0]) and torch.equal(full[0], ib[0])
+
+
+def test_host_to_host_matches_device(pkg):
+    plan = pkg.get_plan(512, 512, 512, None, None, (0.0, 1.0))
+    sinos = np.stack([phantoms.config_sinogram(1, i) for i in range(6)])
+    ref = plan.execute(dev(sinos)).cpu().numpy()
+    host = torch.from_numpy(sinos).pin_memory()
+    out = plan.execute_host(host, chunk=4)
+    assert np.array_equal(out.numpy(), ref)
+    out2 = plan.execute_host(sinos, chunk=1)
+    assert np.array_equal(out2, ref)
+
+
+def test_naive_backprojector(pkg, golden):
+    z = golden("cfg0.npz")
+    g = pkg.Sinogram(256, 256, z["sino"].astype(np.float64))
+    img = pkg.backproject_naive(g, 256)
+    assert report("cfg0 naive", img.values, z["naive"]) <= RTOL
+    img = pkg.fbp(g, pkg.FilterSpec(), engine="naive", n=200)
+    ref = O.FBP_SCALE * O.backproject_naive(O.ramp_filter(z["sino"].astype(np.float64)), 200)
+    assert report("cfg0 fbp naive", img.values, ref) <= RTOL
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_samples(pkg):
+    """2048 bins x 2048 angles -> 2048^2 backprojection on sampled slices (oracle ~5 s each)."""
+    sinos = np.stack([phantoms.config_sinogram(2, i) for i in (0, 1)])
+    out = pkg.logpolar_backproject_batch(dev(sinos), 2048).cpu().numpy()
+    for i in range(2):
+        ref = O.logpolar_backproject(sinos[i].astype(np.float64), 2048)
+        assert report(f"cfg2 slice{i}", out[i], ref) <= RTOL
+
+
+@pytest.mark.slow
+def test_cfg3_fbp_full_size_sample(pkg):
+    s = phantoms.config_sinogram(3, 5)
+    out = pkg.fbp_batch(dev(s)[None], pkg.FilterSpec(), 2048).cpu().numpy()[0]
+    ref = O.fbp_logpolar(s.astype(np.float64), 2048)
+    assert report("cfg3 slice5 fbp", out, ref) <= RTOL
+
+
+@pytest.mark.slow
+def test_cfg4_naive_cross_check(pkg):
+    """Direct backprojector at 2048^2: parity vs the oracle on sampled rows, and the
+    LP-vs-direct discretisation gap inside the unit disk (a property, not a 1e-4 bar)."""
+    s = phantoms.config_sinogram(4, 0)
+    d = dev(s)[None]
+    nv = pkg.backproject_naive_batch(d, 2048)[0].cpu().numpy()
+    rows = np.arange(3, 2048, 97)
+    ref_rows = O.backproject_naive(s.astype(np.float64), 2048, rows=rows)
+    assert report("cfg4 naive rows", nv[rows], ref_rows) <= RTOL
+    lp = pkg.logpolar_backproject_batch(d, 2048)[0].cpu().numpy()
+    xs = -1.0 + (np.arange(2048) + 0.5) * (2.0 / 2048)
+    X, Y = np.meshgrid(xs, xs)
+    disk = np.hypot(X, Y) <= 1.0
+    gap = O.relative_l2(lp[disk], nv[disk])
+    print(f"cfg4 LP vs direct in unit disk: {gap:.3e}")
+    assert gap < 1e-2
+
+
+def test_unsupported_size_is_loud(pkg):
+    g = pkg.Sinogram(128, 90, np.ones((128, 90)))
+    with pytest.raises(NotImplementedError):
+        pkg.logpolar_backproject(g, 64)
+    with pytest.raises(NotImplementedError):
+        pkg.fbp(g, pkg.FilterSpec(), engine="bst", n=64)
