@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark: log-polar FBP of 2048^2 slices (BASELINE.json metric
+"backprojected 2048^2 slices/sec at 1/2/4/8 B200; HBM GB/s vs peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 3] [--slices S] [--e2e-slices E]
+
+One process per GPU (torchrun for N > 1).  A step is one pass of the FBP hot
+path over the rank's resident batch of S slices (default: configs[3], S = 2048
+slices of 2048 angles x 2048 bins per rank -> weak scaling; no inter-GPU data
+exchange, torch.distributed carries only the barrier and the max-over-ranks
+timing).  Inputs (34 GB per rank) are far larger than L2, so no L2 flush is
+needed between steps.
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port, oracle/fastbp_oracle.py: numpy/scipy restatement of fastbp) on the
+host's cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "backprojected 2048^2 slices/sec at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "slices/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--slices", type=int, default=0, help="slices per rank per step (0 = config default)")
+    ap.add_argument("--chunk", type=int, default=32, help="slices per internal pipeline chunk")
+    ap.add_argument("--e2e-slices", type=int, default=64)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-workers", type=int, default=0, help="0 = min(cores, memory/2.5GB, 32)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+# distributed plumbing (barrier + max over ranks; no data-path collective)
+# ----------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo")
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def shard(total: int, world: int, rank: int) -> range:
+    """Contiguous slice-index block of `rank`."""
+    lo = total * rank // world
+    hi = total * (rank + 1) // world
+    return range(lo, hi)
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int, path: str | None):
+        self.gpu, self.path, self.proc = gpu, path, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+            if self.path:
+                with open(self.path, "w") as f:
+                    f.write(self.Q + "\n" + "\n".join(self.lines) + "\n")
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx or None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference algorithm), one slice per worker
+# ----------------------------------------------------------------------------
+def _cpu_worker(args):
+    cfg, idx = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import fastbp_oracle as O
+    from oracle import phantoms
+
+    c = phantoms.CONFIGS[cfg]
+    g = phantoms.config_sinogram(cfg, idx).astype("float64")
+    t = time.perf_counter()
+    if c["fbp"]:
+        O.fbp_logpolar(g, c["n"])
+    else:
+        O.logpolar_backproject(g, c["n"])
+    return time.perf_counter() - t
+
+
+def cpu_workers(requested: int) -> int:
+    if requested > 0:
+        return requested
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    try:
+        avail_gb = int(open("/proc/meminfo").read().split("MemAvailable:")[1].split()[0]) / 1e6
+    except Exception:
+        avail_gb = 16.0
+    return max(1, min(ncpu, int(avail_gb / 2.5), 32))
+
+
+def cpu_baseline(cfg: int, workers: int, slices_per_worker: int = 1):
+    """Throughput of the oracle port on `workers` host cores (one process per
+    core, each running whole slices): slices / wall."""
+    env = {"OMP_NUM_THREADS": "1", "OPENBLAS_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"}
+    os.environ.update(env)
+    jobs = [(cfg, 1000 + i) for i in range(workers * slices_per_worker)]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(workers) as pool:
+        t = time.perf_counter()
+        per = pool.map(_cpu_worker, jobs, chunksize=1)
+        wall = time.perf_counter() - t
+    return len(jobs) / wall, wall, per
+
+
+def cpu_model() -> str:
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------
+def run_reference(a, d: Dist):
+    """--impl reference: the reference algorithm on the host cores, rank 0 only."""
+    if d.rank != 0:
+        d.close()
+        return
+    from oracle import phantoms
+
+    c = phantoms.CONFIGS[a.config]
+    workers = cpu_workers(a.cpu_workers)
+    vals = []
+    for i in range(a.warmup + a.steps):
+        v, wall, _ = cpu_baseline(a.config, workers, 1)
+        if i >= a.warmup:
+            vals.append((v, wall))
+    v = sum(x for x, _ in vals) / len(vals)
+    ms = sum(w for _, w in vals) / len(vals) * 1000.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded random-ellipse sinograms + 1% Gaussian noise)",
+        "config": {"workload": f"config{a.config}: {'FBP' if c['fbp'] else 'BP'} {c['nt']}x{c['ntheta']} -> {c['n']}^2",
+                   "slices_per_step": workers},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"{workers} slices per step, one per worker process, oracle/fastbp_oracle.py "
+                                   f"(numpy/scipy restatement of fastbp), CPU {cpu_model()}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    d.close()
+
+
+def run_ours(a, d: Dist):
+    import numpy as np
+    import torch
+
+    import paper_1608_03589_b200 as p
+    from oracle import phantoms
+
+    torch.cuda.set_device(d.local)
+    dev = torch.device("cuda", d.local)
+    c = phantoms.CONFIGS[a.config]
+    nt, nth, n = c["nt"], c["ntheta"], c["n"]
+    S = a.slices or c["slices"]
+    spec = (0.0, 1.0) if c["fbp"] else None
+    plan = p.get_plan(nt, nth, n, None, None, spec)
+
+    # ---- synthetic inputs, generated on the device (per-slice seeds)
+    global_ids = range(d.rank * S, (d.rank + 1) * S)  # weak scaling: S slices per rank
+    sino = p.synth.config_batch(a.config, list(global_ids), dev)
+    out = torch.empty((S, n, n), dtype=torch.float32, device=dev)
+    chunk = min(a.chunk, S)
+    ws = torch.empty(plan.workspace_bytes(chunk), dtype=torch.uint8, device=dev)
+
+    def step():
+        plan.execute(sino, out=out, workspace=ws)
+        return plan.last_launches
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
+    clk = ClockSampler(d.local, os.path.join(REPO, "gpurun_out", f"clocks_rank{d.rank}.csv"))
+    plan.profile(True)
+    d.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with clk:
+        time.sleep(0.3)
+        e0.record(stream)
+        for _ in range(a.steps):
+            launches += step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    d.barrier()
+    stages = plan.profile_read()
+    plan.profile(False)
+    ms_total = e0.elapsed_time(e1)
+    ms_max = d.max(ms_total)
+    total_slices = d.sum(S * a.steps)
+    value = total_slices / (ms_max / 1000.0)
+
+    # ---- roofline of the dominant kernel (largest share of device time)
+    info = plan.info
+    ab = p.algorithmic_bytes(plan)
+    dom = max(stages, key=lambda k: stages[k]["ms"])
+    st = stages[dom]
+    per_launch_ms = st["ms"] / max(1, st["launches"])
+    slices_per_launch = st["slices"] / max(1, st["launches"])
+    bytes_per_launch = ab[dom]["per_slice"] * slices_per_launch + ab[dom]["per_launch"]
+    peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
+    achieved = bytes_per_launch / (per_launch_ms / 1000.0) / 1e9
+    pipe_bytes = sum(ab[k]["per_slice"] for k in ab if k in stages) + sum(
+        ab[k]["per_launch"] * stages[k]["launches"] for k in stages) / max(1, S * a.steps)
+
+    # ---- end to end through the public host API (pinned host in/out, H2D + D2H inside)
+    E = min(a.e2e_slices, S)
+    host_in = torch.empty((E, nt, nth), dtype=torch.float32, pin_memory=True)
+    host_in.copy_(sino[:E])
+    host_out = torch.empty((E, n, n), dtype=torch.float32, pin_memory=True)
+    plan.execute_host(host_in, host_out, chunk=8)
+    d.barrier()
+    t = time.perf_counter()
+    for _ in range(a.e2e_steps):
+        plan.execute_host(host_in, host_out, chunk=8)
+    e2e_s = d.max(time.perf_counter() - t)
+    e2e_value = d.sum(E * a.e2e_steps) / e2e_s
+
+    cpu = None
+    if d.rank == 0 and a.gpus == 1 and not a.no_cpu_baseline:
+        w = cpu_workers(a.cpu_workers)
+        v, wall, per = cpu_baseline(a.config, w, 1)
+        cpu = {"value": v, "unit": UNIT, "cores": w, "kind": "port",
+               "sample": f"{w} config-{a.config} slices, one per worker process ({wall:.1f} s wall, "
+                         f"{np.mean(per):.2f} s/slice/core), oracle/fastbp_oracle.py, CPU {cpu_model()}"}
+
+    if d.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (device-generated seeded random-ellipse sinograms, K=50, 1% Gaussian noise)",
+            "config": {"workload": f"config{a.config}: {'FBP' if c['fbp'] else 'BP'} {nt} bins x {nth} angles -> {n}^2 fp32",
+                       "slices_per_rank": S, "chunk": chunk, "parallelism": f"slice-shard x{d.world}",
+                       "l2": "no flush: 34 GB input per step >> 126 MB L2",
+                       "nrho": info["nrho"], "L": info["L"], "nphi": info["nphi"]},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": per_launch_ms,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+            "pipeline": {"stage_ms_per_slice": {k: v["ms"] / max(1, v["slices"]) for k, v in stages.items()},
+                         "algorithmic_bytes_per_slice": pipe_bytes,
+                         "hbm_equiv_gbs": pipe_bytes * value / d.world / 1e9,
+                         "hbm_equiv_frac": pipe_bytes * value / d.world / 1e9 / peak},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": E * nt * nth * 4,
+                    "d2h_bytes_per_step": E * n * n * 4, "slices_per_step": E, "api": "LogPolarPlan.execute_host"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    d.close()
+
+
+def main():
+    a = parse()
+    d = Dist()
+    if a.impl == "reference":
+        run_reference(a, d)
+    else:
+        run_ours(a, d)
+
+
+if __name__ == "__main__":
+    main()
