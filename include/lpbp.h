@@ -63,6 +63,7 @@ typedef struct lpbp_plan_info {
   double rho0, drho, dphi, out_scale;
   size_t table_bytes;          /* device bytes of constant tables owned by the plan */
   size_t workspace_per_slice;  /* lpbp_execute workspace bytes per slice in flight  */
+  size_t readout_sector_bytes; /* distinct 32-byte log-polar sectors the readout taps (x32) */
 } lpbp_plan_info;
 
 int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan);
@@ -97,6 +98,20 @@ int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, in
  * "ki" (int32 nrho), "wi" (float2 nrho), "qidx" (uint32 nq*nq), "qw" (float2 nq*nq).  Returns the element count in *count;
  * if dst is non-NULL copies min(count, capacity) elements. */
 int lpbp_plan_table(const lpbp_plan* plan, const char* which, void* dst, size_t capacity, size_t* count);
+
+/* Per-stage CUDA-event timing of lpbp_execute / lpbp_logpolar / lpbp_execute_host
+ * launches (stages: 0 ramp filter, 1 row DFT, 2 rho convolution, 3 row inverse DFT,
+ * 4 readout).  Events are recorded on the launching stream around each kernel;
+ * lpbp_profile_read waits for them, returns the sums since the last read and resets. */
+int lpbp_profile_enable(lpbp_plan* plan, int32_t enable);
+int lpbp_profile_read(lpbp_plan* plan, double* stage_ms, int64_t* stage_launches, int64_t* stage_slices,
+                      int32_t nstages);
+
+/* Analytic ellipse-phantom sinograms (harness input generator; restates
+ * fastbp.radon.radon_ellipses, radon.py:38-61, in fp64 on the device).
+ * params_dev: [batch][k][6] doubles (cx, cy, a, b, tilt, rho); out: [batch][nt][ntheta] fp32. */
+int lpbp_radon_ellipses(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch,
+                        float* out_dev, void* stream);
 
 /* Number of kernel launches the last lpbp_execute/lpbp_execute_host issued on the calling thread. */
 int64_t lpbp_last_launch_count(void);

@@ -22,5 +22,7 @@ from .filtering import FBP_SCALE, FilterSpec, fbp, fbp_batch, filter_sinogram
 from .reference import backproject_naive, backproject_naive_batch
 from .metrics import max_abs_error, relative_l2
 from .plan import LogPolarPlan, get_plan, naive_backproject
+from .roofline import algorithmic_bytes
+from . import synth
 
 __version__ = "0.1.0"

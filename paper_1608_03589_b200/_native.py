@@ -43,7 +43,7 @@ class PlanInfo(ctypes.Structure):
         ("nrho", c_int32), ("L", c_int32), ("M", c_int32), ("kernel_nnz", c_int32), ("kmax", c_int32),
         ("filter", c_int32), ("device", c_int32),
         ("rho0", c_double), ("drho", c_double), ("dphi", c_double), ("out_scale", c_double),
-        ("table_bytes", c_size_t), ("workspace_per_slice", c_size_t),
+        ("table_bytes", c_size_t), ("workspace_per_slice", c_size_t), ("readout_sector_bytes", c_size_t),
     ]
 
 
@@ -60,6 +60,9 @@ SIGNATURES = {
     "lpbp_readout": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "lpbp_naive_backproject": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "lpbp_plan_table": (c_int32, [c_void_p, c_char_p, c_void_p, c_size_t, POINTER(c_size_t)]),
+    "lpbp_profile_enable": (c_int32, [c_void_p, c_int32]),
+    "lpbp_profile_read": (c_int32, [c_void_p, POINTER(ctypes.c_double), POINTER(c_int64), POINTER(c_int64), c_int32]),
+    "lpbp_radon_ellipses": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "lpbp_last_launch_count": (c_int64, []),
     "lpbp_last_error": (c_char_p, []),
     "lpbp_version": (c_int32, []),

@@ -59,6 +59,13 @@ struct lpbp_plan {
   size_t table_bytes = 0;
   size_t szA = 0, szB = 0;  // per-slice workspace regions (aliased by stage lifetime)
 
+  // optional per-stage CUDA-event profiling (lpbp_profile_enable / _read)
+  struct Rec { int stage; int slices; cudaEvent_t a, b; };
+  bool profiling = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  std::mutex prof_mu;
+
   std::mutex mu;  // guards the owned workspace and the host pipeline
   void* own_ws = nullptr;
   size_t own_ws_bytes = 0;
@@ -107,6 +114,8 @@ struct lpbp_plan {
 
   ~lpbp_plan() {
     DeviceGuard g(device);
+    for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
+    for (auto e : ev_pool) cudaEventDestroy(e);
     release_pipe();
     if (own_ws) cudaFree(own_ws);
     for (void* p : allocs) cudaFree(p);
@@ -114,6 +123,33 @@ struct lpbp_plan {
 };
 
 namespace {
+
+// Stage ids for profiling: 0 ramp, 1 row_rdft, 2 rho_conv, 3 row_irdft, 4 readout.
+constexpr int kStages = 5;
+
+cudaEvent_t take_event(lpbp_plan* P) {
+  if (!P->ev_pool.empty()) {
+    cudaEvent_t e = P->ev_pool.back();
+    P->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <typename F>
+cudaError_t staged(const lpbp_plan* Pc, int stage, int slices, cudaStream_t s, F&& launch) {
+  lpbp_plan* P = const_cast<lpbp_plan*>(Pc);
+  if (!P->profiling) return launch();
+  std::lock_guard<std::mutex> lk(P->prof_mu);
+  cudaEvent_t a = take_event(P), b = take_event(P);
+  cudaEventRecord(a, s);
+  cudaError_t e = launch();
+  cudaEventRecord(b, s);
+  P->recs.push_back({stage, slices, a, b});
+  return e;
+}
 
 // Run the stages for one chunk already resident on the device.
 // stop_after_lp: write the log-polar image to lp_out and skip filter/readout.
@@ -125,23 +161,26 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   const float* src = in;
   cudaError_t e;
   if (P->h.filter && !stop_after_lp) {
-    e = lpbp::launch_ramp(d, P->t, in, reinterpret_cast<float*>(A), c, s);
+    e = staged(P, 0, c, s, [&] { return lpbp::launch_ramp(d, P->t, in, reinterpret_cast<float*>(A), c, s); });
     if (e) return launch_fail(e, "ramp_filter");
     ++g_launches;
     src = reinterpret_cast<const float*>(A);
   }
-  e = lpbp::launch_row_rdft(d, P->t, src, reinterpret_cast<float2*>(B), c, s);
+  e = staged(P, 1, c, s, [&] { return lpbp::launch_row_rdft(d, P->t, src, reinterpret_cast<float2*>(B), c, s); });
   if (e) return launch_fail(e, "row_rdft");
   ++g_launches;
-  e = lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c, s);
+  e = staged(P, 2, c, s, [&] {
+    return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c, s);
+  });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
   float* lp = stop_after_lp ? lp_out : reinterpret_cast<float*>(B);
-  e = lpbp::launch_row_irdft(d, P->t, reinterpret_cast<const float2*>(A), lp, c, s);
+  e = staged(P, 3, c, s,
+             [&] { return lpbp::launch_row_irdft(d, P->t, reinterpret_cast<const float2*>(A), lp, c, s); });
   if (e) return launch_fail(e, "row_irdft");
   ++g_launches;
   if (stop_after_lp) return LPBP_OK;
-  e = lpbp::launch_readout(d, P->t, lp, out, c, s);
+  e = staged(P, 4, c, s, [&] { return lpbp::launch_readout(d, P->t, lp, out, c, s); });
   if (e) return launch_fail(e, "readout");
   ++g_launches;
   return LPBP_OK;
@@ -285,6 +324,7 @@ int lpbp_plan_get_info(const lpbp_plan* P, lpbp_plan_info* info) {
   info->out_scale = h.out_scale;
   info->table_bytes = P->table_bytes;
   info->workspace_per_slice = ws_per_slice(P);
+  info->readout_sector_bytes = h.readout_sector_bytes;
   return LPBP_OK;
 }
 
@@ -469,6 +509,51 @@ int lpbp_plan_table(const lpbp_plan* P, const char* which, void* dst, size_t cap
   if (!std::strcmp(which, "qidx")) return copy_vec(h.qidx);     // uint32
   if (!std::strcmp(which, "qw")) return copy_vec(h.qw);         // float pairs
   return fail(LPBP_EINVAL, std::string("unknown table ") + which);
+}
+
+int lpbp_profile_enable(lpbp_plan* P, int32_t enable) {
+  if (!P) return fail(LPBP_EINVAL, "invalid argument");
+  std::lock_guard<std::mutex> lk(P->prof_mu);
+  P->profiling = enable != 0;
+  return LPBP_OK;
+}
+
+int lpbp_profile_read(lpbp_plan* P, double* stage_ms, int64_t* stage_launches, int64_t* stage_slices,
+                      int32_t nstages) {
+  if (!P || !stage_ms || !stage_launches || !stage_slices || nstages < kStages)
+    return fail(LPBP_EINVAL, "invalid argument");
+  DeviceGuard g(P->device);
+  std::lock_guard<std::mutex> lk(P->prof_mu);
+  for (int i = 0; i < nstages; ++i) {
+    stage_ms[i] = 0;
+    stage_launches[i] = 0;
+    stage_slices[i] = 0;
+  }
+  int rc = LPBP_OK;
+  for (auto& r : P->recs) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (e != cudaSuccess && rc == LPBP_OK) rc = cuda_fail(e, "profile_read");
+    stage_ms[r.stage] += ms;
+    stage_launches[r.stage] += 1;
+    stage_slices[r.stage] += r.slices;
+    P->ev_pool.push_back(r.a);
+    P->ev_pool.push_back(r.b);
+  }
+  P->recs.clear();
+  return rc;
+}
+
+int lpbp_radon_ellipses(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch,
+                        float* out_dev, void* stream) {
+  if (!params_dev || !out_dev || k < 1 || k > 256 || nt < 2 || ntheta < 1 || batch < 0)
+    return fail(LPBP_EINVAL, "invalid argument");
+  if (batch == 0) return LPBP_OK;
+  cudaError_t e = lpbp::launch_radon_ellipses(params_dev, k, nt, ntheta, batch, out_dev,
+                                              static_cast<cudaStream_t>(stream));
+  if (e) return cuda_fail(e, "radon_ellipses");
+  return LPBP_OK;
 }
 
 int64_t lpbp_last_launch_count(void) { return g_launches; }

@@ -42,6 +42,9 @@ cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, f
 cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dtheta, const float* g, float* gT,
                          float* img, int batch, cudaStream_t s);
 
+cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int ntheta, int batch, float* out,
+                                  cudaStream_t s);
+
 bool sizes_supported(int nt, int ntheta, int L, bool filter);
 
 }  // namespace lpbp

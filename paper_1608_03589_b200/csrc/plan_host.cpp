@@ -289,6 +289,39 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
     }
   }
 
+  // --- distinct 32-byte sectors of the fp32 log-polar image read by the readout
+  // taps over the whole image (reflections as on the device): the readout's
+  // compulsory read traffic.
+  {
+    std::vector<uint8_t> hit(((size_t)nrho * nphi + 7) / 8 + 1, 0);
+    auto mark = [&](int i, int j) { hit[((size_t)i * nphi + j) / 8] = 1; };
+    for (int iy = 0; iy < p.n; ++iy) {
+      for (int jx = 0; jx < p.n; ++jx) {
+        const bool yneg = iy < c, xneg = jx < c;
+        const int qy = yneg ? (p.n - 1 - iy) - c : iy - c;
+        const int qx = xneg ? (p.n - 1 - jx) - c : jx - c;
+        const uint32_t e = h.qidx[(size_t)qy * h.nq + qx];
+        if (e == 0xFFFFFFFFu) continue;
+        const float wjr = h.qw[(size_t)qy * h.nq + qx].y;
+        const int i0 = (int)(e & 0xFFFFu), jr = (int)(e >> 16);
+        int j0;
+        if (!xneg && !yneg) j0 = jr;
+        else if (xneg && yneg) j0 = nphi / 2 + jr;
+        else {
+          const int Q = xneg ? nphi / 2 : nphi;
+          j0 = (wjr == 0.f) ? Q - jr : Q - jr - 1;
+        }
+        if (j0 >= nphi) j0 -= nphi;
+        const int j1 = (j0 + 1 == nphi) ? 0 : j0 + 1;
+        const int i1 = std::min(i0 + 1, nrho - 1);
+        mark(i0, j0); mark(i0, j1); mark(i1, j0); mark(i1, j1);
+      }
+    }
+    size_t cnt = 0;
+    for (uint8_t v : hit) cnt += v;
+    h.readout_sector_bytes = cnt * 32;
+  }
+
   // --- direct backprojector angle table (reference.py:30-36)
   h.naive_cs.resize(p.ntheta);
   const double dtheta = kPi / p.ntheta;

@@ -26,6 +26,7 @@ struct HostPlan {
   // geometry
   int nt = 0, ntheta = 0, n = 0, ns = 0, nphi = 0, nh = 0, nrho = 0, nrho_pad = 0, L = 0, M = 0, nq = 0;
   int kmax = 0, nnz = 0, ramp_len_ref = 0;
+  size_t readout_sector_bytes = 0;
   double rho0 = 0, drho = 0, dphi = 0, out_scale = 1;
   bool filter = false;
   // tables (uploaded to the device)

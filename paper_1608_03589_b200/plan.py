@@ -176,6 +176,22 @@ class LogPolarPlan:
         self.last_launches = int(lib().lpbp_last_launch_count())
         return out
 
+    STAGES = ("ramp_filter", "row_rdft", "rho_conv", "row_irdft", "readout")
+
+    def profile(self, enable: bool) -> None:
+        """Record CUDA events around every stage launch (on the launching stream)."""
+        check(lib().lpbp_profile_enable(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{stage: {"ms", "launches", "slices"}} summed since the last read (waits for the events)."""
+        n = len(self.STAGES)
+        ms = (ctypes.c_double * n)()
+        launches = (ctypes.c_int64 * n)()
+        slices = (ctypes.c_int64 * n)()
+        check(lib().lpbp_profile_read(self._h, ms, launches, slices, n))
+        return {name: {"ms": ms[i], "launches": launches[i], "slices": slices[i]}
+                for i, name in enumerate(self.STAGES) if launches[i]}
+
     def table(self, which: str) -> np.ndarray:
         n = c_size_t()
         check(lib().lpbp_plan_table(self._h, which.encode(), None, 0, byref(n)))

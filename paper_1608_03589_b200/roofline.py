@@ -1,0 +1,35 @@
+"""Algorithmic (compulsory) HBM bytes of each pipeline kernel: every kernel reads
+its input once and writes its output once (fp32 real / complex64 spectra).
+DESIGN.md §4 states the per-kernel figures; SURVEY §8(d) gives the
+stage-decomposition totals for the whole path (279.258 MB per FBP slice at
+2048^2) that the pipeline-level HBM-equivalent figure uses."""
+
+from __future__ import annotations
+
+# SURVEY §8(d) compulsory bytes per slice for the reference's stage decomposition
+SURVEY_BYTES_PER_SLICE = {(256, False): 3.014e6, (512, True): 15.252e6, (2048, False): 245.704e6,
+                          (2048, True): 279.258e6}
+
+
+def algorithmic_bytes(plan) -> dict:
+    """{stage: {"per_slice": bytes, "per_launch": bytes}} for a LogPolarPlan."""
+    i = plan.info
+    nt, nth, n = i["nt"], i["ntheta"], i["n_out"]
+    nphi, nrho, L = i["nphi"], i["nrho"], i["L"]
+    nh = nphi // 2 + 1
+    sino = nt * nth * 4
+    G = nh * nt * 8
+    Y = nh * nrho * 8
+    lp = nrho * nphi * 4
+    img = n * n * 4
+    return {
+        "ramp_filter": {"per_slice": 2 * sino, "per_launch": 0},
+        "row_rdft": {"per_slice": sino + G, "per_launch": 0},
+        "rho_conv": {"per_slice": G + Y, "per_launch": nh * L * 8},  # kernel spectrum once per launch
+        "row_irdft": {"per_slice": Y + lp, "per_launch": 0},
+        "readout": {"per_slice": i["readout_sector_bytes"] + img, "per_launch": 0},
+    }
+
+
+def survey_bytes_per_slice(plan) -> float | None:
+    return SURVEY_BYTES_PER_SLICE.get((plan.info["n_out"], bool(plan.info["filter"])))

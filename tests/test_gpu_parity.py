@@ -179,3 +179,27 @@ def test_unsupported_size_is_loud(pkg):
         pkg.logpolar_backproject(g, 64)
     with pytest.raises(NotImplementedError):
         pkg.fbp(g, pkg.FilterSpec(), engine="bst", n=64)
+
+
+def test_device_sinogram_generator_matches_oracle(pkg):
+    """synth (device, fp64 line integrals) vs oracle/phantoms (numpy) on noiseless inputs."""
+    from paper_1608_03589_b200 import synth
+    for cfg, idx in ((0, 0), (2, 3)):
+        c = phantoms.CONFIGS[cfg]
+        seed = phantoms.BASE_SEED + 7919 * cfg + idx
+        prm = synth.ellipse_params(seed, c["k"], c["amin"], c["amax"])
+        ref = phantoms.radon_ellipses(phantoms.random_ellipses(seed, c["k"], c["amin"], c["amax"]), c["nt"], c["ntheta"])
+        got = synth.radon_ellipses(prm[None], c["nt"], c["ntheta"], torch.device("cuda"))[0].cpu().numpy()
+        assert report(f"synth cfg{cfg}", got, ref) < 1e-6
+
+
+def test_profiled_stage_times_cover_every_stage(pkg):
+    plan = pkg.get_plan(512, 512, 512, None, None, (0.0, 1.0))
+    x = dev(np.stack([phantoms.config_sinogram(1, i) for i in range(4)]))
+    plan.profile(True)
+    plan.execute(x, chunk=2)
+    st = plan.profile_read()
+    plan.profile(False)
+    assert set(st) == {"ramp_filter", "row_rdft", "rho_conv", "row_irdft", "readout"}
+    assert all(v["launches"] == 2 and v["slices"] == 4 and v["ms"] > 0 for v in st.values())
+    assert plan.last_launches == 10
