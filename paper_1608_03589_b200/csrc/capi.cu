@@ -97,6 +97,22 @@ struct lpbp_plan {
     return LPBP_OK;
   }
 
+  // device-generated pass-twiddle table for FFT size N
+  int twiddles(int N, const float2** dst) {
+    const int len = lpbp::twiddle_table_len(N);
+    if (len < 0) return fail(LPBP_EUNSUPPORTED, "no FFT plan for size " + std::to_string(N));
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, (size_t)len * sizeof(float2));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(twiddles)");
+    allocs.push_back(p);
+    e = lpbp::launch_init_twiddles(N, static_cast<float2*>(p), nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "init_twiddles");
+    table_bytes += (size_t)len * sizeof(float2);
+    *dst = static_cast<const float2*>(p);
+    return LPBP_OK;
+  }
+
   void release_pipe() {
     for (int i = 0; i < 2; ++i) {
       if (pipe.ev_in[i]) cudaEventDestroy(pipe.ev_in[i]);
@@ -260,9 +276,9 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
       return fail(LPBP_ECUDA, "cannot select CUDA device " + std::to_string(params->device));
     }
     int rc = LPBP_OK;
-    rc = rc ? rc : P->upload(h.tw_phi, reinterpret_cast<const lpbp::F2**>(&P->t.tw_phi));
-    rc = rc ? rc : P->upload(h.tw_rho, reinterpret_cast<const lpbp::F2**>(&P->t.tw_rho));
-    rc = rc ? rc : P->upload(h.tw_ramp, reinterpret_cast<const lpbp::F2**>(&P->t.tw_ramp));
+    rc = rc ? rc : P->twiddles(h.nphi, &P->t.tw_phi);
+    rc = rc ? rc : P->twiddles(h.L, &P->t.tw_rho);
+    if (h.filter) rc = rc ? rc : P->twiddles(h.M, &P->t.tw_ramp);
     rc = rc ? rc : P->upload(h.ramp, &P->t.ramp);
     rc = rc ? rc : P->upload(h.ab, reinterpret_cast<const lpbp::I2**>(&P->t.ab));
     rc = rc ? rc : P->upload(h.wab, reinterpret_cast<const lpbp::F4**>(&P->t.wab));

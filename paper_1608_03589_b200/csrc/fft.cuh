@@ -36,6 +36,10 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
+// Shared-memory padding: one float2 every 2^S elements.  S = 4 makes the
+// radix-16 Ns = 1 scatter (stride 16) conflict-free, S = 5 the radix-32 one.
+template <int S>
+__host__ __device__ constexpr int padS(int i) { return i + (i >> S); }
 __host__ __device__ constexpr int pad16(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int padded_len(int n) { return n + (n >> 4); }
 
@@ -118,39 +122,36 @@ struct Dft {
   }
 };
 
-// Multiply v[r] (r = 1..R-1) by tw^(r*k) where tw = exp(-+2*pi*i/(Ns*R)), using
-// the global table of size N: index = r*k*(N/(Ns*R)).
-template <int N, int R, int Ns, bool INV>
+// Multiply v[r] (r = 1..R-1) by the inter-pass twiddle exp(-+2 pi i r k / (Ns R)).
+// tw points at this pass's block of the per-size pass table, laid out
+// [r-1][k] (k < Ns) so consecutive butterflies read consecutive entries; the
+// inverse passes' blocks hold the conjugates.
+template <int R, int Ns>
 __device__ __forceinline__ void apply_twiddles(float2 (&v)[R], int k, const float2* __restrict__ tw) {
   if constexpr (Ns > 1) {
-    constexpr int step = N / (Ns * R);
-    const int base = k * step;
 #pragma unroll
-    for (int r = 1; r < R; ++r) {
-      float2 w = __ldg(tw + base * r);
-      v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
-    }
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + (r - 1) * Ns + k));
   }
 }
 
 // Load the R inputs of butterfly j of a pass from (padded) shared memory.
-template <int N, int R>
+template <int N, int R, int S>
 __device__ __forceinline__ void pass_load(const float2* buf, int j, float2 (&v)[R]) {
 #pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = buf[pad16(j + r * (N / R))];
+  for (int r = 0; r < R; ++r) v[r] = buf[padS<S>(j + r * (N / R))];
 }
-template <int N, int R, int Ns>
+template <int N, int R, int Ns, int S>
 __device__ __forceinline__ void pass_store(float2* buf, int j, const float2 (&v)[R]) {
   const int k = j % Ns;
   const int d = (j / Ns) * Ns * R + k;
 #pragma unroll
-  for (int r = 0; r < R; ++r) buf[pad16(d + r * Ns)] = v[r];
+  for (int r = 0; r < R; ++r) buf[padS<S>(d + r * Ns)] = v[r];
 }
 
 // One full smem->smem Stockham pass for a group of T threads (ti in [0,T)).
 // Caller provides the barrier that separates the previous pass's stores from
 // these loads; this function places the barrier between loads and stores.
-template <int N, int R, int Ns, int T, bool INV, typename Sync>
+template <int N, int R, int Ns, int T, bool INV, int S, typename Sync>
 __device__ __forceinline__ void pass_smem(float2* buf, int ti, const float2* __restrict__ tw, Sync&& sync) {
   constexpr int NB = (N / R) / T;  // butterflies per thread
   static_assert(NB >= 1 && NB * T * R == N, "bad pass shape");
@@ -158,13 +159,13 @@ __device__ __forceinline__ void pass_smem(float2* buf, int ti, const float2* __r
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int j = ti + b * T;
-    pass_load<N, R>(buf, j, v[b]);
-    apply_twiddles<N, R, Ns, INV>(v[b], j % Ns, tw);
+    pass_load<N, R, S>(buf, j, v[b]);
+    apply_twiddles<R, Ns>(v[b], j % Ns, tw);
     Dft<R, INV>::run(v[b]);
   }
   sync();
 #pragma unroll
-  for (int b = 0; b < NB; ++b) pass_store<N, R, Ns>(buf, ti + b * T, v[b]);
+  for (int b = 0; b < NB; ++b) pass_store<N, R, Ns, S>(buf, ti + b * T, v[b]);
 }
 
 // Radix plans (forward order; the inverse runs them reversed).  Every plan
@@ -189,6 +190,23 @@ struct FftPlan {
     for (int q = 0; q < i; ++q) s *= radix(q);
     return s;
   }
+  // padding shift for this direction: match the first pass's Ns = 1 scatter stride
+  static constexpr int S = radix(0) >= 32 ? 5 : 4;
+  // offset (float2 entries) of pass i's twiddle block inside this direction's table
+  static constexpr int tw_off(int i) {
+    int o = 0;
+    for (int q = 1; q < i; ++q) o += (radix(q) - 1) * ns(q);
+    return o;
+  }
+  static constexpr int tw_len = tw_off(P);
+};
+
+// Per-size twiddle table: forward passes' blocks, then inverse passes' blocks.
+template <int N>
+struct TwTable {
+  static constexpr int fwd = 0;
+  static constexpr int inv = FftPlan<N, false>::tw_len;
+  static constexpr int len = FftPlan<N, false>::tw_len + FftPlan<N, true>::tw_len;
 };
 
 // Full size-N FFT over a group of T = N/E threads (ti in [0,T)).
@@ -200,11 +218,13 @@ struct FftPlan {
 // The caller must guarantee buf is free on entry (no thread still reading it).
 // Middle passes go through the padded shared buffer buf (padded_len(N) float2).
 template <int N, bool INV, bool LAST_SYNC, typename Load, typename Store, typename Sync>
-__device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __restrict__ tw,
+__device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __restrict__ twt,
                                           Load&& load, Store&& store, Sync&& sync) {
   using FP = FftPlan<N, INV>;
   constexpr int T = FP::T;
   constexpr int P = FP::P;
+  constexpr int S = FP::S;
+  const float2* tw = twt + (INV ? TwTable<N>::inv : TwTable<N>::fwd);
   {  // pass 0: Ns = 1, no twiddles
     constexpr int R = FP::radix(0);
     constexpr int NB = (N / R) / T;
@@ -217,12 +237,12 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
       Dft<R, INV>::run(v[b]);
     }
 #pragma unroll
-    for (int b = 0; b < NB; ++b) pass_store<N, R, 1>(buf, ti + b * T, v[b]);
+    for (int b = 0; b < NB; ++b) pass_store<N, R, 1, S>(buf, ti + b * T, v[b]);
   }
   sync();
   static_for<1, P - 1>([&](auto ic) {
     constexpr int I = decltype(ic)::value;
-    pass_smem<N, FP::radix(I), FP::ns(I), T, INV>(buf, ti, tw, sync);
+    pass_smem<N, FP::radix(I), FP::ns(I), T, INV, S>(buf, ti, tw + FP::tw_off(I), sync);
     sync();
   });
   {  // last pass: outputs at j + r*Ns (Ns = N/R, j < Ns)
@@ -234,8 +254,8 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
-      pass_load<N, R>(buf, j, v[b]);
-      apply_twiddles<N, R, Ns, INV>(v[b], j, tw);
+      pass_load<N, R, S>(buf, j, v[b]);
+      apply_twiddles<R, Ns>(v[b], j, tw + FP::tw_off(P - 1));
       Dft<R, INV>::run(v[b]);
     }
     if constexpr (LAST_SYNC) sync();
@@ -254,13 +274,15 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
 // thread multiplies its own outputs (mul(idx, val) -> val) and runs the first
 // inverse butterfly in registers.
 template <int N, typename Load, typename Mul, typename Store, typename Sync>
-__device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __restrict__ tw,
+__device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __restrict__ twt,
                                            Load&& load, Mul&& mul, Store&& store, Sync&& sync) {
   using F = FftPlan<N, false>;
   using B = FftPlan<N, true>;
   constexpr int T = F::T;
   constexpr int P = F::P;
   static_assert(F::radix(P - 1) == B::radix(0), "fused middle needs matching radices");
+  const float2* twf = twt + TwTable<N>::fwd;
+  const float2* twi = twt + TwTable<N>::inv;
   {  // forward pass 0
     constexpr int R = F::radix(0);
     constexpr int NB = (N / R) / T;
@@ -273,12 +295,12 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
       Dft<R, false>::run(v[b]);
     }
 #pragma unroll
-    for (int b = 0; b < NB; ++b) pass_store<N, R, 1>(buf, ti + b * T, v[b]);
+    for (int b = 0; b < NB; ++b) pass_store<N, R, 1, F::S>(buf, ti + b * T, v[b]);
   }
   sync();
   static_for<1, P - 1>([&](auto ic) {
     constexpr int I = decltype(ic)::value;
-    pass_smem<N, F::radix(I), F::ns(I), T, false>(buf, ti, tw, sync);
+    pass_smem<N, F::radix(I), F::ns(I), T, false, F::S>(buf, ti, twf + F::tw_off(I), sync);
     sync();
   });
   {  // forward last pass -> pointwise multiply -> inverse pass 0, all in registers
@@ -289,8 +311,8 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
-      pass_load<N, R>(buf, j, v[b]);
-      apply_twiddles<N, R, Ns, false>(v[b], j, tw);
+      pass_load<N, R, F::S>(buf, j, v[b]);
+      apply_twiddles<R, Ns>(v[b], j, twf + F::tw_off(P - 1));
       Dft<R, false>::run(v[b]);
 #pragma unroll
       for (int r = 0; r < R; ++r) v[b][r] = mul(j + r * Ns, v[b][r]);
@@ -298,12 +320,12 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
     }
     sync();
 #pragma unroll
-    for (int b = 0; b < NB; ++b) pass_store<N, R, 1>(buf, ti + b * T, v[b]);
+    for (int b = 0; b < NB; ++b) pass_store<N, R, 1, B::S>(buf, ti + b * T, v[b]);
   }
   sync();
   static_for<1, P - 1>([&](auto ic) {
     constexpr int I = decltype(ic)::value;
-    pass_smem<N, B::radix(I), B::ns(I), T, true>(buf, ti, tw, sync);
+    pass_smem<N, B::radix(I), B::ns(I), T, true, B::S>(buf, ti, twi + B::tw_off(I), sync);
     sync();
   });
   {  // inverse last pass
@@ -314,8 +336,8 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
-      pass_load<N, R>(buf, j, v[b]);
-      apply_twiddles<N, R, Ns, true>(v[b], j, tw);
+      pass_load<N, R, B::S>(buf, j, v[b]);
+      apply_twiddles<R, Ns>(v[b], j, twi + B::tw_off(P - 1));
       Dft<R, true>::run(v[b]);
     }
 #pragma unroll
@@ -325,6 +347,29 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
       for (int r = 0; r < R; ++r) store(j + r * Ns, v[b][r]);
     }
   }
+}
+
+// Fill the pass-twiddle table of size N (TwTable<N>::len entries) in fp64.
+template <int N>
+__global__ void k_init_twiddles(float2* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= TwTable<N>::len) return;
+  auto fill = [&](auto fp, int base, double sgn) {
+    using FP = decltype(fp);
+    static_for<1, FP::P>([&](auto ic) {
+      constexpr int I = decltype(ic)::value;
+      constexpr int R = FP::radix(I), Ns = FP::ns(I);
+      const int lo = base + FP::tw_off(I), hi = lo + (R - 1) * Ns;
+      if (e >= lo && e < hi) {
+        const int r = (e - lo) / Ns + 1, k = (e - lo) % Ns;
+        double sn, cs;
+        sincospi(sgn * 2.0 * (double)(r * k) / (double)(Ns * R), &sn, &cs);
+        out[e] = make_float2((float)cs, (float)sn);
+      }
+    });
+  };
+  fill(FftPlan<N, false>{}, TwTable<N>::fwd, -1.0);
+  fill(FftPlan<N, true>{}, TwTable<N>::inv, +1.0);
 }
 
 }  // namespace lpbp

@@ -16,6 +16,7 @@
 // phi-DFTs of sinogram rows (the phi>=pi half picks up (-1)^m from its nphi/2
 // shift).  nt row FFTs replace nrho (~1.9x fewer) and the row mix moves into K3,
 // where it feeds the first rho-FFT pass straight from shared memory.
+#include "async.cuh"
 #include "fft.cuh"
 #include "kernels.cuh"
 
@@ -31,24 +32,33 @@ __device__ __forceinline__ void block_sync() { __syncthreads(); }
 // unpacking is needed).  Tile: all nt rows x TC columns staged in smem.
 // ---------------------------------------------------------------------------
 template <int M, int TC, int G>
-__global__ void __launch_bounds__(G * FftPlan<M, false>::T)
+__global__ void __launch_bounds__(G * FftPlan<M, false>::T, 1)
 k_ramp(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
        const float* __restrict__ resp, const float2* __restrict__ tw) {
   constexpr int T = FftPlan<M, false>::T;
-  constexpr int TP = TC + 1;  // tile pitch (floats)
+  constexpr int TP = TC + 1;  // tile pitch (floats): conflict-free column reads
+  constexpr int V = TC / 4;   // float4 per tile row
   extern __shared__ __align__(16) float2 smem_k1[];
-  float* tile = reinterpret_cast<float*>(smem_k1);                         // nt * TP floats
+  float* tile = reinterpret_cast<float*>(smem_k1);  // nt * TP floats
   float2* bufs = smem_k1 + ((nt * TP + 1) / 2);
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   float2* buf = bufs + gi * padded_len(M);
   const int c0 = blockIdx.x * TC;
   const size_t slice = (size_t)blockIdx.y * nt * ntheta;
-  const float* src = g + slice;
-  float* dst = out + slice;
+  const float* src = g + slice + c0;
+  float* dst = out + slice + c0;
 
-  for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
-    const int t = e / TC, c = e % TC;
-    tile[t * TP + c] = __ldg(src + (size_t)t * ntheta + c0 + c);
+  // 16-byte loads, 8 in flight per thread
+  const int total = nt * V;
+#pragma unroll 8
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int t = e / V, c = (e % V) * 4;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(src + (size_t)t * ntheta + c));
+    float* r = tile + t * TP + c;
+    r[0] = v.x;
+    r[1] = v.y;
+    r[2] = v.z;
+    r[3] = v.w;
   }
   __syncthreads();
   for (int round = 0; round < TC / 2 / G; ++round) {
@@ -66,9 +76,11 @@ k_ramp(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
     block_conv<M>(buf, ti, tw, load, mul, store, block_sync);
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
-    const int t = e / TC, c = e % TC;
-    dst[(size_t)t * ntheta + c0 + c] = tile[t * TP + c];
+#pragma unroll 8
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int t = e / V, c = (e % V) * 4;
+    const float* r = tile + t * TP + c;
+    *reinterpret_cast<float4*>(dst + (size_t)t * ntheta + c) = make_float4(r[0], r[1], r[2], r[3]);
   }
 }
 
@@ -84,7 +96,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
   constexpr int T = FftPlan<NPHI, false>::T;
   constexpr int NTH = NPHI / 2;
   constexpr int NH = NPHI / 2 + 1;
-  constexpr int SP = TR + 1;
+  constexpr int SP = TR + 1;  // odd pitch: conflict-free staging writes
   extern __shared__ __align__(16) float2 smem_k2[];
   float2* stg = smem_k2;
   float2* buf = smem_k2 + NH * SP + (threadIdx.x / T) * padded_len(NPHI);
@@ -111,6 +123,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
     __syncthreads();
   }
   float2* dst = Gh + (size_t)blockIdx.y * NH * nt + t0;
+#pragma unroll 8
   for (int e = threadIdx.x; e < NH * TR; e += blockDim.x) {
     const int m = e / TR, c = e % TR;
     dst[(size_t)m * nt + c] = stg[m * SP + c];
@@ -126,27 +139,47 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
 // Khat is fused between the last forward and first inverse pass.
 // ---------------------------------------------------------------------------
 template <int L>
-__global__ void __launch_bounds__(FftPlan<L, false>::T)
+__global__ void __launch_bounds__(FftPlan<L, false>::T, 2)
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int ns, int nrho,
            int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
            const int* __restrict__ ki, const float2* __restrict__ wi, const float2* __restrict__ khat,
            const float2* __restrict__ tw) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
-  float2* buf = smem_k3;
-  float2* p = smem_k3 + padded_len(L);
+  __shared__ __align__(8) uint64_t bars[2];
+  float2* buf = smem_k3;                          // padded_len(L)
+  float2* p = buf + padded_len(L);                // ns
+  float2* gcol = p + ((ns + 1) & ~1);             // 2 x nt  (16-B aligned)
   const int m = blockIdx.x;
   const float sg = (m & 1) ? -1.f : 1.f;
   const int ti = threadIdx.x;
   const float2* kcol = khat + (size_t)m * L;
+  const uint32_t col_bytes = (uint32_t)nt * sizeof(float2);
+
+  if (ti == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (ti == 0) {
+    mbar_arrive_expect_tx(&bars[0], col_bytes);
+    tma_bulk_g2s(gcol, Gh + (size_t)m * nt, col_bytes, &bars[0]);
+  }
 
   for (int b = 0; b < batch; ++b) {
-    const float2* col = Gh + ((size_t)b * nh + m) * nt;
+    const int s = b & 1;
+    if (ti == 0 && b + 1 < batch) {  // prefetch the next slice's column into the other buffer
+      mbar_arrive_expect_tx(&bars[s ^ 1], col_bytes);
+      tma_bulk_g2s(gcol + (s ^ 1) * nt, Gh + ((size_t)(b + 1) * nh + m) * nt, col_bytes, &bars[s ^ 1]);
+    }
+    mbar_wait(&bars[s], (b >> 1) & 1);
+    const float2* col = gcol + s * nt;
     for (int k = ti; k < ns; k += T) {
       const int2 A = __ldg(ab + k);
       const float4 W = __ldg(wab + k);
-      const float2 g0 = __ldg(col + A.x), g1 = __ldg(col + A.x + 1);
-      const float2 h0 = __ldg(col + A.y), h1 = __ldg(col + A.y + 1);
+      const float2 g0 = col[A.x], g1 = col[A.x + 1];
+      const float2 h0 = col[A.y], h1 = col[A.y + 1];
       float2 v;
       v.x = fmaf(W.x, g0.x, W.y * g1.x) + sg * fmaf(W.z, h0.x, W.w * h1.x);
       v.y = fmaf(W.x, g0.y, W.y * g1.y) + sg * fmaf(W.z, h0.y, W.w * h1.y);
@@ -180,7 +213,7 @@ k_row_irdft(const float2* __restrict__ Yh, float* __restrict__ lp, int nrho, int
             const float2* __restrict__ tw) {
   constexpr int T = FftPlan<NPHI, true>::T;
   constexpr int NH = NPHI / 2 + 1;
-  constexpr int SP = TR + 1;
+  constexpr int SP = TR + 1;  // odd pitch: conflict-free FFT reads
   extern __shared__ __align__(16) float2 smem_k4[];
   float2* stg = smem_k4;
   float2* buf = smem_k4 + NH * SP + (threadIdx.x / T) * padded_len(NPHI);
@@ -189,18 +222,24 @@ k_row_irdft(const float2* __restrict__ Yh, float* __restrict__ lp, int nrho, int
   const float2* src = Yh + (size_t)blockIdx.y * NH * nrho_pad + i0;
   float* dst = lp + (size_t)blockIdx.y * nrho * NPHI;
 
+#pragma unroll 8
   for (int e = threadIdx.x; e < NH * TR; e += blockDim.x) {
     const int m = e / TR, c = e % TR;
-    stg[m * SP + c] = (i0 + c < nrho) ? src[(size_t)m * nrho_pad + c] : make_float2(0.f, 0.f);
+    cp_async8(stg + m * SP + c, src + (size_t)m * nrho_pad + c);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   for (int round = 0; round < TR / 2 / G; ++round) {
     const int q = round * G + gi;
     const int ia = i0 + 2 * q, ib = ia + 1;
+    const bool va = ia < nrho, vb = ib < nrho;  // rows past nrho read padding: force zero
     auto load = [&](int idx) -> float2 {
       const bool hi = idx > NPHI / 2;
       const int mm = hi ? NPHI - idx : idx;
       float2 xa = stg[mm * SP + 2 * q], xb = stg[mm * SP + 2 * q + 1];
+      if (!va) xa = make_float2(0.f, 0.f);
+      if (!vb) xb = make_float2(0.f, 0.f);
       if (mm == 0 || mm == NPHI / 2) {
         xa.y = 0.f;
         xb.y = 0.f;
@@ -225,53 +264,72 @@ k_row_irdft(const float2* __restrict__ Yh, float* __restrict__ lp, int nrho, int
 // the plan's fp64-built quadrant table; the other quadrants reflect phi:
 //   x<0,y>=0: pi - phi   x<0,y<0: pi + phi   x>=0,y<0: 2 pi - phi
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, int nrho, int nphi,
-          const uint32_t* __restrict__ qidx, const float2* __restrict__ qw, float scale) {
-  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pix >= n * n) return;
-  const int iy = pix / n, jx = pix - iy * n;
+__device__ __forceinline__ float readout_pixel(const float* __restrict__ l, int iy, int jx, int n, int nq, int nrho,
+                                               int nphi, const uint32_t* __restrict__ qidx,
+                                               const float2* __restrict__ qw) {
   const int c = n / 2;
   const bool yneg = iy < c, xneg = jx < c;
   const int qy = yneg ? (n - 1 - iy) - c : iy - c;
   const int qx = xneg ? (n - 1 - jx) - c : jx - c;
-  const size_t slice = (size_t)blockIdx.y * n * n;
   const uint32_t e = __ldg(qidx + qy * nq + qx);
-  float v = 0.f;
-  if (e != 0xFFFFFFFFu) {
-    const float2 w = __ldg(qw + qy * nq + qx);
-    const int i0 = (int)(e & 0xFFFFu);
-    const int jr = (int)(e >> 16);
-    int j0;
-    float wj;
-    if (!xneg && !yneg) {
-      j0 = jr;
-      wj = w.y;
-    } else if (xneg && yneg) {
-      j0 = nphi / 2 + jr;
-      wj = w.y;
+  if (e == 0xFFFFFFFFu) return 0.f;
+  const float2 w = __ldg(qw + qy * nq + qx);
+  const int i0 = (int)(e & 0xFFFFu);
+  const int jr = (int)(e >> 16);
+  int j0;
+  float wj;
+  if (!xneg && !yneg) {
+    j0 = jr;
+    wj = w.y;
+  } else if (xneg && yneg) {
+    j0 = nphi / 2 + jr;
+    wj = w.y;
+  } else {
+    const int Q = xneg ? nphi / 2 : nphi;  // fj = Q - fj_rep
+    if (w.y == 0.f) {
+      j0 = Q - jr;
+      wj = 0.f;
     } else {
-      const int Q = xneg ? nphi / 2 : nphi;  // fj = Q - fj_rep
-      if (w.y == 0.f) {
-        j0 = Q - jr;
-        wj = 0.f;
-      } else {
-        j0 = Q - jr - 1;
-        wj = 1.f - w.y;
-      }
+      j0 = Q - jr - 1;
+      wj = 1.f - w.y;
     }
-    if (j0 >= nphi) j0 -= nphi;
-    const int j1 = (j0 + 1 == nphi) ? 0 : j0 + 1;
-    const int i1 = min(i0 + 1, nrho - 1);
-    const float* l = lp + (size_t)blockIdx.y * nrho * nphi;
-    const float a00 = __ldg(l + (size_t)i0 * nphi + j0), a01 = __ldg(l + (size_t)i0 * nphi + j1);
-    const float a10 = __ldg(l + (size_t)i1 * nphi + j0), a11 = __ldg(l + (size_t)i1 * nphi + j1);
-    const float wi = w.x;
-    const float r0 = fmaf(wj, a01 - a00, a00);
-    const float r1 = fmaf(wj, a11 - a10, a10);
-    v = fmaf(wi, r1 - r0, r0) * scale;
   }
-  img[slice + pix] = v;
+  if (j0 >= nphi) j0 -= nphi;
+  const int j1 = (j0 + 1 == nphi) ? 0 : j0 + 1;
+  const int i1 = min(i0 + 1, nrho - 1);
+  const float a00 = __ldg(l + (size_t)i0 * nphi + j0), a01 = __ldg(l + (size_t)i0 * nphi + j1);
+  const float a10 = __ldg(l + (size_t)i1 * nphi + j0), a11 = __ldg(l + (size_t)i1 * nphi + j1);
+  const float r0 = fmaf(wj, a01 - a00, a00);
+  const float r1 = fmaf(wj, a11 - a10, a10);
+  return fmaf(w.x, r1 - r0, r0);
+}
+
+// 4 pixels per thread (independent gathers in flight); grid.x covers n*n/4.
+__global__ void __launch_bounds__(256)
+k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, int nrho, int nphi,
+          const uint32_t* __restrict__ qidx, const float2* __restrict__ qw, float scale) {
+  const int npix = n * n;
+  const int base = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (base >= npix) return;
+  const float* l = lp + (size_t)blockIdx.y * nrho * nphi;
+  float* o = img + (size_t)blockIdx.y * npix;
+  float v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int pix = base + u;
+    v[u] = 0.f;
+    if (pix < npix) {
+      const int iy = pix / n;
+      v[u] = readout_pixel(l, iy, pix - iy * n, n, nq, nrho, nphi, qidx, qw) * scale;
+    }
+  }
+  if (base + 3 < npix && ((reinterpret_cast<uintptr_t>(o + base) & 15) == 0)) {
+    *reinterpret_cast<float4*>(o + base) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + u < npix) o[base + u] = v[u];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -414,7 +472,7 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
 
 template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
-  const size_t smem = ((size_t)padded_len(L) + d.ns) * sizeof(float2);
+  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + 2 * (size_t)d.nt) * sizeof(float2);
   auto k = k_rho_conv<L>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
@@ -475,7 +533,7 @@ cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Yh
 }
 cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, float* img, int batch, cudaStream_t s) {
   const int npix = d.n * d.n;
-  k_readout<<<dim3((npix + 255) / 256, batch), 256, 0, s>>>(lp, img, d.n, d.nq, d.nrho, d.nphi, t.qidx, t.qw,
+  k_readout<<<dim3((npix + 1023) / 1024, batch), 256, 0, s>>>(lp, img, d.n, d.nq, d.nrho, d.nphi, t.qidx, t.qw,
                                                             d.out_scale);
   return cudaGetLastError();
 }
@@ -485,6 +543,33 @@ cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dthe
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   k_naive<<<dim3((n + 31) / 32, (n + 7) / 8, batch), 256, 0, s>>>(gT, img, nt, ntheta, n, cs, dtheta);
+  return cudaGetLastError();
+}
+
+int twiddle_table_len(int N) {
+  switch (N) {
+    case 256: return TwTable<256>::len;
+    case 512: return TwTable<512>::len;
+    case 1024: return TwTable<1024>::len;
+    case 2048: return TwTable<2048>::len;
+    case 4096: return TwTable<4096>::len;
+    case 8192: return TwTable<8192>::len;
+    default: return -1;
+  }
+}
+
+cudaError_t launch_init_twiddles(int N, float2* out, cudaStream_t s) {
+  const int len = twiddle_table_len(N);
+  if (len < 0) return cudaErrorNotSupported;
+  const dim3 grid((len + 255) / 256);
+  switch (N) {
+    case 256: k_init_twiddles<256><<<grid, 256, 0, s>>>(out); break;
+    case 512: k_init_twiddles<512><<<grid, 256, 0, s>>>(out); break;
+    case 1024: k_init_twiddles<1024><<<grid, 256, 0, s>>>(out); break;
+    case 2048: k_init_twiddles<2048><<<grid, 256, 0, s>>>(out); break;
+    case 4096: k_init_twiddles<4096><<<grid, 256, 0, s>>>(out); break;
+    case 8192: k_init_twiddles<8192><<<grid, 256, 0, s>>>(out); break;
+  }
   return cudaGetLastError();
 }
 

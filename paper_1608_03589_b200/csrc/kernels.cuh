@@ -12,7 +12,7 @@
 namespace lpbp {
 
 struct DevTables {
-  // twiddle tables exp(-2 pi i k / N), k < N
+  // pass-twiddle tables (fft.cuh TwTable layout) of size
   const float2* tw_phi;   // N = nphi
   const float2* tw_rho;   // N = L
   const float2* tw_ramp;  // N = M = 2 nt (FBP only)
@@ -46,5 +46,9 @@ cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int nthet
                                   cudaStream_t s);
 
 bool sizes_supported(int nt, int ntheta, int L, bool filter);
+// Pass-twiddle tables (fft.cuh TwTable): entry count for size N (-1 if unsupported)
+// and a device fill kernel.
+int twiddle_table_len(int N);
+cudaError_t launch_init_twiddles(int N, float2* out, cudaStream_t s);
 
 }  // namespace lpbp

@@ -41,15 +41,6 @@ void fft_pow2(std::vector<cd>& a, const std::vector<cd>& w /* w[k] = exp(-2 pi i
   }
 }
 
-std::vector<F2> twiddle_table(int N) {
-  std::vector<F2> t(N);
-  for (int k = 0; k < N; ++k) {
-    const double a = -2.0 * kPi * (double)k / (double)N;
-    t[k] = F2{(float)std::cos(a), (float)std::sin(a)};
-  }
-  return t;
-}
-
 // Linear-interpolation tap of fastbp.grids._lerp_axis0 (grids.py:255-269):
 //   value = [0<=i0<n] v[i0] (1-w) + [0<=i0+1<n] v[i0+1] w,  i0 = floor(f), w = f - i0
 // re-expressed as (base, w0, w1) over rows base, base+1 with base in [0, n-2]
@@ -210,9 +201,7 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
     for (auto& t : pool) t.join();
   }
 
-  // --- twiddle tables
-  h.tw_phi = twiddle_table(nphi);
-  h.tw_rho = twiddle_table(L);
+  // (FFT twiddle tables are generated on the device from the compile-time radix plans.)
 
   // --- ramp / Tikhonov filter (filtering.py:54-70).  The reference multiplies
   // by resp on an Lr = next_fast_len(8 nt) grid; that is a convolution with the
@@ -259,7 +248,6 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
       }
       h.ramp[kap] = (float)(acc / M);
     }
-    h.tw_ramp = twiddle_table(M);
   }
 
   // --- readout quadrant table (grids.py:399-443) at x, y >= 0; the device

@@ -30,7 +30,7 @@ struct HostPlan {
   double rho0 = 0, drho = 0, dphi = 0, out_scale = 1;
   bool filter = false;
   // tables (uploaded to the device)
-  std::vector<F2> tw_phi, tw_rho, tw_ramp, khat, wi, qw, naive_cs;
+  std::vector<F2> khat, wi, qw, naive_cs;
   std::vector<float> ramp;
   std::vector<I2> ab;
   std::vector<F4> wab;

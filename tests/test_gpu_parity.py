@@ -203,3 +203,17 @@ def test_profiled_stage_times_cover_every_stage(pkg):
     assert set(st) == {"ramp_filter", "row_rdft", "rho_conv", "row_irdft", "readout"}
     assert all(v["launches"] == 2 and v["slices"] == 4 and v["ms"] > 0 for v in st.values())
     assert plan.last_launches == 10
+
+
+@pytest.mark.parametrize("fbp", [False, True])
+def test_full_size_executes_and_is_linear(pkg, fbp):
+    """2048^2 kernels launch (shared-memory/launch limits) and stay linear; no oracle."""
+    from paper_1608_03589_b200 import synth
+    plan = pkg.get_plan(2048, 2048, 2048, None, None, (0.0, 1.0) if fbp else None)
+    x = synth.config_batch(3 if fbp else 2, [0, 1], torch.device("cuda"))
+    y = plan.execute(x)
+    assert torch.isfinite(y).all() and y.abs().max() > 0
+    y2 = plan.execute(torch.stack([x[1], 3.0 * x[0]]))
+    assert torch.equal(y2[0], y[1])
+    assert O.relative_l2(y2[1].cpu().numpy(), 3.0 * y[0].cpu().numpy()) < 1e-6
+    assert torch.count_nonzero(plan.execute(torch.zeros_like(x))) == 0
