@@ -64,6 +64,7 @@ typedef struct lpbp_plan_info {
   size_t table_bytes;          /* device bytes of constant tables owned by the plan */
   size_t workspace_per_slice;  /* lpbp_execute workspace bytes per slice in flight  */
   size_t readout_sector_bytes; /* distinct 32-byte log-polar sectors the readout taps (x32) */
+  int32_t band_rows, row_min, nbands; /* fused inverse-DFT + readout banding               */
 } lpbp_plan_info;
 
 int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan);
@@ -95,13 +96,14 @@ int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, in
 
 /* Host copies of plan tables for tests: which = "kernel_cells" (int32 pairs k,l),
  * "ramp" (float M), "khat" (float2 nh*L), "ab" (int32 pairs ns), "wab" (float4 ns),
- * "ki" (int32 nrho), "wi" (float2 nrho), "qidx" (uint32 nq*nq), "qw" (float2 nq*nq).  Returns the element count in *count;
+ * "ki" (int32 nrho), "wi" (float2 nrho), "qidx" (uint32 nq*nq), "qw" (float2 nq*nq),
+ * "band_off" (uint32 nbands+1), "band_entries" (uint32).  Returns the element count in *count;
  * if dst is non-NULL copies min(count, capacity) elements. */
 int lpbp_plan_table(const lpbp_plan* plan, const char* which, void* dst, size_t capacity, size_t* count);
 
 /* Per-stage CUDA-event timing of lpbp_execute / lpbp_logpolar / lpbp_execute_host
  * launches (stages: 0 ramp filter, 1 row DFT, 2 rho convolution, 3 row inverse DFT,
- * 4 readout).  Events are recorded on the launching stream around each kernel;
+ * 4 readout, 5 fused row inverse DFT + readout).  Events are recorded on the launching stream around each kernel;
  * lpbp_profile_read waits for them, returns the sums since the last read and resets. */
 int lpbp_profile_enable(lpbp_plan* plan, int32_t enable);
 int lpbp_profile_read(lpbp_plan* plan, double* stage_ms, int64_t* stage_launches, int64_t* stage_slices,

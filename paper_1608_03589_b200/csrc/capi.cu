@@ -140,8 +140,9 @@ struct lpbp_plan {
 
 namespace {
 
-// Stage ids for profiling: 0 ramp, 1 row_rdft, 2 rho_conv, 3 row_irdft, 4 readout.
-constexpr int kStages = 5;
+// Stage ids for profiling: 0 ramp, 1 row_rdft, 2 rho_conv, 3 row_irdft, 4 readout,
+// 5 fused row_irdft + readout.
+constexpr int kStages = 6;
 
 cudaEvent_t take_event(lpbp_plan* P) {
   if (!P->ev_pool.empty()) {
@@ -190,14 +191,16 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
-  float* lp = stop_after_lp ? lp_out : reinterpret_cast<float*>(B);
-  e = staged(P, 3, c, s,
-             [&] { return lpbp::launch_row_irdft(d, P->t, reinterpret_cast<const float2*>(A), lp, c, s); });
-  if (e) return launch_fail(e, "row_irdft");
-  ++g_launches;
-  if (stop_after_lp) return LPBP_OK;
-  e = staged(P, 4, c, s, [&] { return lpbp::launch_readout(d, P->t, lp, out, c, s); });
-  if (e) return launch_fail(e, "readout");
+  if (stop_after_lp) {
+    e = staged(P, 3, c, s,
+               [&] { return lpbp::launch_row_irdft(d, P->t, reinterpret_cast<const float2*>(A), lp_out, c, s); });
+    if (e) return launch_fail(e, "row_irdft");
+    ++g_launches;
+    return LPBP_OK;
+  }
+  e = staged(P, 5, c, s,
+             [&] { return lpbp::launch_irdft_readout(d, P->t, reinterpret_cast<const float2*>(A), out, c, s); });
+  if (e) return launch_fail(e, "irdft_readout");
   ++g_launches;
   return LPBP_OK;
 }
@@ -269,6 +272,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
                                        " (this build: 2*ntheta and 2*nt powers of two in [512, 4096])");
   }
   P->device = params->device;
+  if (lpbp::fused_band_rows(P->h.nphi) > 0) lpbp::build_bands(P->h, lpbp::fused_band_rows(P->h.nphi));
   if (P->device >= 0) {
     DeviceGuard g(P->device);
     if (!g.ok) {
@@ -288,6 +292,10 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     rc = rc ? rc : P->upload(h.qidx, &P->t.qidx);
     rc = rc ? rc : P->upload(h.qw, reinterpret_cast<const lpbp::F2**>(&P->t.qw));
     rc = rc ? rc : P->upload(h.naive_cs, reinterpret_cast<const lpbp::F2**>(&P->t.naive_cs));
+    if (!rc) {
+      rc = P->upload(P->h.band_off, &P->t.band_off);
+      rc = rc ? rc : P->upload(P->h.band_entries, &P->t.band_entries);
+    }
     if (rc) {
       std::string msg = g_last_error;
       delete P;
@@ -307,6 +315,8 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   d.M = h.M;
   d.nq = h.nq;
   d.out_scale = (float)h.out_scale;
+  d.row_min = h.row_min;
+  d.nbands = h.nbands;
   const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;
   const size_t Y = (size_t)h.nh * h.nrho_pad * sizeof(float2);
   const size_t G = (size_t)h.nh * h.nt * sizeof(float2);
@@ -341,6 +351,9 @@ int lpbp_plan_get_info(const lpbp_plan* P, lpbp_plan_info* info) {
   info->table_bytes = P->table_bytes;
   info->workspace_per_slice = ws_per_slice(P);
   info->readout_sector_bytes = h.readout_sector_bytes;
+  info->band_rows = h.band_rows;
+  info->row_min = h.row_min;
+  info->nbands = h.nbands;
   return LPBP_OK;
 }
 
@@ -524,6 +537,8 @@ int lpbp_plan_table(const lpbp_plan* P, const char* which, void* dst, size_t cap
   if (!std::strcmp(which, "wi")) return copy_vec(h.wi);         // float pairs
   if (!std::strcmp(which, "qidx")) return copy_vec(h.qidx);     // uint32
   if (!std::strcmp(which, "qw")) return copy_vec(h.qw);         // float pairs
+  if (!std::strcmp(which, "band_off")) return copy_vec(h.band_off);          // uint32 nbands+1
+  if (!std::strcmp(which, "band_entries")) return copy_vec(h.band_entries);  // uint32
   return fail(LPBP_EINVAL, std::string("unknown table ") + which);
 }
 

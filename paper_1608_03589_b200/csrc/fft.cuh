@@ -214,10 +214,11 @@ struct TwTable {
 //   store(idx, val)           : output element idx (last pass writes it directly)
 //   sync()                    : barrier covering every thread that shares buf
 // LAST_SYNC places a barrier between the last pass's loads and its stores (needed
-// when store() writes back into buf).
+// when store() writes back into buf); FIRST_SYNC does the same for pass 0 (needed
+// when load() reads buf).
 // The caller must guarantee buf is free on entry (no thread still reading it).
 // Middle passes go through the padded shared buffer buf (padded_len(N) float2).
-template <int N, bool INV, bool LAST_SYNC, typename Load, typename Store, typename Sync>
+template <int N, bool INV, bool LAST_SYNC, bool FIRST_SYNC = false, typename Load, typename Store, typename Sync>
 __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __restrict__ twt,
                                           Load&& load, Store&& store, Sync&& sync) {
   using FP = FftPlan<N, INV>;
@@ -236,6 +237,7 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
       for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
       Dft<R, INV>::run(v[b]);
     }
+    if constexpr (FIRST_SYNC) sync();  // load() reads buf itself
 #pragma unroll
     for (int b = 0; b < NB; ++b) pass_store<N, R, 1, S>(buf, ti + b * T, v[b]);
   }

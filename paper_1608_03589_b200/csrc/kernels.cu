@@ -333,6 +333,121 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 }
 
 // ---------------------------------------------------------------------------
+// K45: fused inverse phi-DFT + Cartesian readout.  One CTA per band of RB = 2*NPAIR
+// consecutive log-polar rows (bands overlap by one row so every pixel's two taps
+// i0, i0+1 lie in one band).  Each pair's spectra are staged into its own shared
+// region, transformed in place, and the real rows stay in shared memory for the
+// bilinear readout of the band's pixels (plan-time list of quadrant pixels; each
+// entry writes its four mirror pixels).  The log-polar image never reaches HBM.
+// ---------------------------------------------------------------------------
+template <int NPHI>
+struct FusedShape;
+template <> struct FusedShape<512>  { static constexpr int NPAIR = 8, G = 4; };
+template <> struct FusedShape<1024> { static constexpr int NPAIR = 8, G = 4; };
+template <> struct FusedShape<2048> { static constexpr int NPAIR = 8, G = 2; };
+template <> struct FusedShape<4096> { static constexpr int NPAIR = 6, G = 2; };
+
+template <int NPHI>
+__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
+k_irdft_readout(const float2* __restrict__ Yh, float* __restrict__ img, int nrho, int nrho_pad, int n, int nq,
+                int row_min, int nbands, const uint32_t* __restrict__ band_off,
+                const uint32_t* __restrict__ entries, const uint32_t* __restrict__ qidx,
+                const float2* __restrict__ qw, float scale, const float2* __restrict__ tw) {
+  constexpr int NPAIR = FusedShape<NPHI>::NPAIR;
+  constexpr int G = FusedShape<NPHI>::G;
+  constexpr int T = FftPlan<NPHI, true>::T;
+  constexpr int NH = NPHI / 2 + 1;
+  constexpr int REG = padded_len(NPHI);  // float2 per pair region
+  constexpr int RB = 2 * NPAIR;
+  constexpr int RPITCH = NPHI + 16;      // floats from row a to row b inside a region
+  static_assert(2 * NH <= REG && RPITCH + NPHI <= 2 * REG, "pair region too small");
+  static_assert(NPAIR % G == 0, "pairs must split evenly over FFT groups");
+  extern __shared__ __align__(16) float2 smem_k45[];
+  const int band = nbands - 1 - (int)blockIdx.x;  // outer (pixel-heavy) bands first
+  const int r0 = row_min + band * (RB - 1);
+  const float2* src = Yh + (size_t)blockIdx.y * NH * nrho_pad;
+
+  for (int e = threadIdx.x; e < NH * RB; e += blockDim.x) {
+    const int m = e / RB, c = e - (e / RB) * RB;
+    float2* dst = smem_k45 + (c >> 1) * REG + (c & 1) * NH + m;
+    const int row = r0 + c;
+    if (row < nrho) cp_async8(dst, src + (size_t)m * nrho_pad + row);
+    else *dst = make_float2(0.f, 0.f);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+#pragma unroll 1
+  for (int round = 0; round < NPAIR / G; ++round) {
+    const int q = round * G + gi;
+    float2* R = smem_k45 + q * REG;
+    float* Rf = reinterpret_cast<float*>(R);
+    auto load = [&](int idx) -> float2 {
+      const bool hi = idx > NPHI / 2;
+      const int mm = hi ? NPHI - idx : idx;
+      float2 xa = R[mm], xb = R[NH + mm];
+      if (mm == 0 || mm == NPHI / 2) {
+        xa.y = 0.f;
+        xb.y = 0.f;
+      }
+      if (hi) {
+        xa.y = -xa.y;
+        xb.y = -xb.y;
+      }
+      return make_float2(xa.x - xb.y, xa.y + xb.x);
+    };
+    auto store = [&](int idx, float2 v) {
+      Rf[idx] = v.x;
+      Rf[RPITCH + idx] = v.y;
+    };
+    block_fft<NPHI, true, true, true>(R, ti, tw, load, store, block_sync);
+  }
+  __syncthreads();
+
+  const uint32_t e0 = __ldg(band_off + band), e1 = __ldg(band_off + band + 1);
+  const int c = n / 2;
+  float* out = img + (size_t)blockIdx.y * n * n;
+  for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const uint32_t ent = __ldg(entries + e);
+    const int qq = (int)(ent & 0x7FFFFFFFu);
+    const int qy = qq / nq, qx = qq - (qq / nq) * nq;
+    const int iyp = c + qy, iyn = n - 1 - c - qy;
+    const int jxp = c + qx, jxn = n - 1 - c - qx;
+    const bool dupy = iyn == iyp, dupx = jxn == jxp;  // odd n: centre row / column
+    float v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f;
+    if (!(ent & 0x80000000u)) {
+      const uint32_t qe = __ldg(qidx + qq);
+      const float2 w = __ldg(qw + qq);
+      const int i0 = (int)(qe & 0xFFFFu), jr = (int)(qe >> 16);
+      const int li0 = i0 - r0, li1 = min(i0 + 1, nrho - 1) - r0;
+      const float* row0 = reinterpret_cast<const float*>(smem_k45 + (li0 >> 1) * REG) + (li0 & 1) * RPITCH;
+      const float* row1 = reinterpret_cast<const float*>(smem_k45 + (li1 >> 1) * REG) + (li1 & 1) * RPITCH;
+      auto sample = [&](int j0, float wj) {
+        if (j0 >= NPHI) j0 -= NPHI;
+        const int j1 = (j0 + 1 == NPHI) ? 0 : j0 + 1;
+        const float a0 = fmaf(wj, row0[j1] - row0[j0], row0[j0]);
+        const float a1 = fmaf(wj, row1[j1] - row1[j0], row1[j0]);
+        return fmaf(w.x, a1 - a0, a0) * scale;
+      };
+      const bool wz = w.y == 0.f;
+      const float wm = wz ? 0.f : 1.f - w.y;
+      v1 = sample(jr, w.y);                                      // x >= 0, y >= 0
+      v2 = sample(wz ? NPHI / 2 - jr : NPHI / 2 - jr - 1, wm);  // x < 0, y >= 0: pi - phi
+      v3 = sample(NPHI / 2 + jr, w.y);                           // x < 0, y < 0: pi + phi
+      v4 = sample(wz ? NPHI - jr : NPHI - jr - 1, wm);          // x >= 0, y < 0: 2 pi - phi
+    }
+    out[(size_t)iyp * n + jxp] = v1;
+    if (!dupx) out[(size_t)iyp * n + jxn] = v2;
+    if (!dupy) {
+      out[(size_t)iyn * n + jxp] = v4;
+      if (!dupx) out[(size_t)iyn * n + jxn] = v3;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Direct pixel-driven backprojector (reference.py:21-37), the accuracy
 // cross-check: b(x) = dtheta * sum_k lerp_t(g[:, k], (x . xi_k + 1) / dt).
 // The sinogram is transposed to angle-major first so a warp's 32 pixels read
@@ -544,6 +659,42 @@ cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dthe
   if (e) return e;
   k_naive<<<dim3((n + 31) / 32, (n + 7) / 8, batch), 256, 0, s>>>(gT, img, nt, ntheta, n, cs, dtheta);
   return cudaGetLastError();
+}
+
+int fused_band_rows(int nphi) {
+  switch (nphi) {
+    case 512: return 2 * FusedShape<512>::NPAIR;
+    case 1024: return 2 * FusedShape<1024>::NPAIR;
+    case 2048: return 2 * FusedShape<2048>::NPAIR;
+    case 4096: return 2 * FusedShape<4096>::NPAIR;
+    default: return -1;
+  }
+}
+
+namespace {
+template <int NPHI>
+cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch, cudaStream_t s) {
+  constexpr int G = FusedShape<NPHI>::G, NPAIR = FusedShape<NPHI>::NPAIR;
+  const size_t smem = (size_t)NPAIR * padded_len(NPHI) * sizeof(float2);
+  auto k = k_irdft_readout<NPHI>;
+  cudaError_t e = prep(k, smem);
+  if (e) return e;
+  k<<<dim3(d.nbands, batch), G * FftPlan<NPHI, true>::T, smem, s>>>(
+      Yh, img, d.nrho, d.nrho_pad, d.n, d.nq, d.row_min, d.nbands, t.band_off, t.band_entries, t.qidx, t.qw,
+      d.out_scale, t.tw_phi);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch,
+                                 cudaStream_t s) {
+  switch (d.nphi) {
+    case 512: return fused_impl<512>(d, t, Yh, img, batch, s);
+    case 1024: return fused_impl<1024>(d, t, Yh, img, batch, s);
+    case 2048: return fused_impl<2048>(d, t, Yh, img, batch, s);
+    case 4096: return fused_impl<4096>(d, t, Yh, img, batch, s);
+    default: return cudaErrorNotSupported;
+  }
 }
 
 int twiddle_table_len(int N) {

@@ -25,10 +25,13 @@ struct DevTables {
   const uint32_t* qidx;   // [nq][nq] readout quadrant table: i0 | j0 << 16, ~0 = zero pixel
   const float2* qw;       // [nq][nq] readout weights (wi, wj)
   const float2* naive_cs; // [ntheta] (cos, sin) * nt/(2n) for the direct backprojector
+  const uint32_t* band_off;      // [nbands+1] fused readout: entry range per band
+  const uint32_t* band_entries;  // quadrant pixels per band (bit 31: write zero)
 };
 
 struct Dims {
   int nt, ntheta, n, ns, nphi, nh, nrho, nrho_pad, L, M, nq;
+  int row_min, nbands;    // fused inverse-DFT + readout bands
   float out_scale;        // 1 (backprojection) or 1/(2 pi) (fbp)
 };
 
@@ -38,6 +41,9 @@ cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float
 cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* G, int batch, cudaStream_t s);
 cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, cudaStream_t s);
 cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch, cudaStream_t s);
+cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Y, float* img, int batch,
+                                 cudaStream_t s);
+int fused_band_rows(int nphi);
 cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, float* img, int batch, cudaStream_t s);
 cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dtheta, const float* g, float* gT,
                          float* img, int batch, cudaStream_t s);

@@ -64,6 +64,37 @@ void lerp_tap(double f, int n, int32_t& base, double& w0, double& w1) {
 
 }  // namespace
 
+void build_bands(HostPlan& h, int band_rows) {
+  const size_t nqq = (size_t)h.nq * h.nq;
+  int rmin = h.nrho;
+  for (size_t e = 0; e < nqq; ++e)
+    if (h.qidx[e] != 0xFFFFFFFFu) rmin = std::min(rmin, (int)(h.qidx[e] & 0xFFFFu));
+  if (rmin == h.nrho) rmin = 0;
+  const int step = band_rows - 1;
+  h.band_rows = band_rows;
+  h.row_min = rmin;
+  h.nbands = std::max(1, (h.nrho - rmin + step - 1) / step);
+  std::vector<std::vector<uint32_t>> valid(h.nbands), zero(h.nbands);
+  size_t nzero = 0;
+  for (size_t e = 0; e < nqq; ++e) {
+    const uint32_t q = h.qidx[e];
+    if (q == 0xFFFFFFFFu) {
+      zero[nzero++ % h.nbands].push_back((uint32_t)e | 0x80000000u);  // spread zero-writes evenly
+    } else {
+      const int b = std::min(h.nbands - 1, ((int)(q & 0xFFFFu) - rmin) / step);
+      valid[b].push_back((uint32_t)e);
+    }
+  }
+  h.band_entries.clear();
+  h.band_off.assign(h.nbands + 1, 0);
+  for (int b = 0; b < h.nbands; ++b) {
+    h.band_off[b] = (uint32_t)h.band_entries.size();
+    h.band_entries.insert(h.band_entries.end(), valid[b].begin(), valid[b].end());
+    h.band_entries.insert(h.band_entries.end(), zero[b].begin(), zero[b].end());
+  }
+  h.band_off[h.nbands] = (uint32_t)h.band_entries.size();
+}
+
 double adaptive_rho0(int nx, int ny) { return std::log(std::min(2.0 / nx, 2.0 / ny)) - std::log(2.0); }
 
 std::string mesh_for(int ns, double rho0, int nrho_in, int& nrho_out) {

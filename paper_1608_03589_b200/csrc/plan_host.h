@@ -36,12 +36,19 @@ struct HostPlan {
   std::vector<F4> wab;
   std::vector<int32_t> ki;
   std::vector<uint32_t> qidx;
+  // fused inverse-DFT + readout: bands of band_rows log-polar rows starting at
+  // row_min + b*(band_rows-1); band_entries lists quadrant pixels (qy*nq + qx)
+  // whose i0 falls in the band (bit 31 set = write zero), band_off[b..b+1).
+  int band_rows = 0, row_min = 0, nbands = 0;
+  std::vector<uint32_t> band_entries, band_off;
   // kernel support (for diagnostics/tests): cells (k, l) of the rolled kernel
   std::vector<int32_t> cell_k, cell_l;
 };
 
 // Returns "" on success, else the error message (ValueError semantics).
 std::string build_host_plan(const HostPlanParams& p, HostPlan& out);
+// Fill band_* for bands of `band_rows` rows (needs qidx built).
+void build_bands(HostPlan& h, int band_rows);
 
 // fastbp.grids.adaptive_rho0 (grids.py:385-391)
 double adaptive_rho0(int nx, int ny);

@@ -176,7 +176,7 @@ class LogPolarPlan:
         self.last_launches = int(lib().lpbp_last_launch_count())
         return out
 
-    STAGES = ("ramp_filter", "row_rdft", "rho_conv", "row_irdft", "readout")
+    STAGES = ("ramp_filter", "row_rdft", "rho_conv", "row_irdft", "readout", "irdft_readout")
 
     def profile(self, enable: bool) -> None:
         """Record CUDA events around every stage launch (on the launching stream)."""

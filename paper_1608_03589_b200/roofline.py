@@ -28,6 +28,8 @@ def algorithmic_bytes(plan) -> dict:
         "rho_conv": {"per_slice": G + Y, "per_launch": nh * L * 8},  # kernel spectrum once per launch
         "row_irdft": {"per_slice": Y + lp, "per_launch": 0},
         "readout": {"per_slice": i["readout_sector_bytes"] + img, "per_launch": 0},
+        # fused inverse DFT + readout: spectra in, image out (log-polar rows stay on chip)
+        "irdft_readout": {"per_slice": Y + img, "per_launch": 0},
     }
 
 

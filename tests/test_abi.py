@@ -183,3 +183,43 @@ def test_host_only_plan_refuses_execution():
     ws = c_size_t()
     N.check(N.lib().lpbp_workspace_bytes(hp.h, 4, byref(ws)))
     assert ws.value >= 4 * hp.info.workspace_per_slice - 1024
+
+
+@pytest.mark.parametrize("nt,nth,n,rho0", [(256, 256, 256, None), (512, 256, 255, None), (512, 256, 300, -4.0),
+                                           (2048, 2048, 2048, None)])
+def test_fused_readout_bands_cover_every_pixel_once(nt, nth, n, rho0):
+    """Band lists of the fused inverse-DFT + readout kernel: every output pixel is
+    written exactly once, zero exactly where the reference readout is zero, and each
+    pixel's taps (i0, i0+1) lie inside its band's rows."""
+    hp = HostPlan(nt, nth, n, rho0=rho0)
+    i = hp.info
+    off = hp.table("band_off", np.uint32).astype(np.int64)
+    ent = hp.table("band_entries", np.uint32)
+    qidx = hp.table("qidx", np.uint32)
+    assert len(off) == i.nbands + 1 and off[-1] == len(ent) == len(qidx)
+    c, nq = n // 2, n - n // 2
+    writes = np.zeros((n, n), dtype=np.int32)
+    zero = np.zeros((n, n), dtype=bool)
+    for b in range(i.nbands):
+        e = ent[off[b]:off[b + 1]]
+        q = (e & 0x7FFFFFFF).astype(np.int64)
+        z = (e & 0x80000000) != 0
+        qy, qx = q // nq, q % nq
+        r0 = i.row_min + b * (i.band_rows - 1)
+        qi = qidx[q[~z]]
+        assert np.all(qi[qi != 0xFFFFFFFF] != 0xFFFFFFFF)
+        i0 = (qi & 0xFFFF).astype(np.int64)
+        assert np.all(i0 >= r0) and np.all(np.minimum(i0 + 1, i.nrho - 1) < r0 + i.band_rows)
+        assert np.all(qidx[q[z]] == 0xFFFFFFFF)
+        iyp, iyn, jxp, jxn = c + qy, n - 1 - c - qy, c + qx, n - 1 - c - qx
+        dupy, dupx = iyn == iyp, jxn == jxp  # odd n: centre row/column mirror onto themselves
+        for iy, jx, keep in ((iyp, jxp, np.ones_like(dupx)), (iyp, jxn, ~dupx), (iyn, jxp, ~dupy), (iyn, jxn, ~dupx & ~dupy)):
+            pix = (iy * n + jx)[keep]
+            np.add.at(writes.reshape(-1), pix, 1)
+            zero.reshape(-1)[(iy * n + jx)[keep & z]] = True
+    assert writes.min() == 1 and writes.max() == 1
+    xs = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+    X, Y = np.meshgrid(xs, xs)
+    R = np.hypot(X, Y)
+    ref_zero = ~((R <= 1.0) & (R > 0) & (np.log(np.maximum(R, 1e-300)) >= i.rho0))
+    assert np.array_equal(zero, ref_zero)
