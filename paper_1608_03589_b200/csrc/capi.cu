@@ -294,7 +294,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     rc = rc ? rc : P->upload(h.naive_cs, reinterpret_cast<const lpbp::F2**>(&P->t.naive_cs));
     if (!rc) {
       rc = P->upload(P->h.band_off, &P->t.band_off);
-      rc = rc ? rc : P->upload(P->h.band_entries, &P->t.band_entries);
+      rc = rc ? rc : P->upload(P->h.band_packed, &P->t.band_entries);
     }
     if (rc) {
       std::string msg = g_last_error;

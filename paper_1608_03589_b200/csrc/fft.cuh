@@ -135,17 +135,37 @@ __device__ __forceinline__ void apply_twiddles(float2 (&v)[R], int k, const floa
 }
 
 // Load the R inputs of butterfly j of a pass from (padded) shared memory.
+// Padded addressing: when the stride between a butterfly's elements is a
+// multiple of 2^S, pad(base + r*stride) = pad(base) + r*(stride + stride/2^S),
+// so every element is one base register plus a compile-time immediate.
 template <int N, int R, int S>
 __device__ __forceinline__ void pass_load(const float2* buf, int j, float2 (&v)[R]) {
+  constexpr int STRIDE = N / R;
+  if constexpr (STRIDE % (1 << S) == 0) {
+    const float2* b = buf + padS<S>(j);
 #pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = buf[padS<S>(j + r * (N / R))];
+    for (int r = 0; r < R; ++r) v[r] = b[r * (STRIDE + (STRIDE >> S))];
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = buf[padS<S>(j + r * STRIDE)];
+  }
 }
 template <int N, int R, int Ns, int S>
 __device__ __forceinline__ void pass_store(float2* buf, int j, const float2 (&v)[R]) {
-  const int k = j % Ns;
-  const int d = (j / Ns) * Ns * R + k;
+  if constexpr (Ns == 1 && R == (1 << S)) {
+    // d = j*R, pad(d + r) = j*(R+1) + r
+    float2* b = buf + j * (R + 1);
 #pragma unroll
-  for (int r = 0; r < R; ++r) buf[padS<S>(d + r * Ns)] = v[r];
+    for (int r = 0; r < R; ++r) b[r] = v[r];
+  } else if constexpr (Ns % (1 << S) == 0) {
+    float2* b = buf + padS<S>((j / Ns) * Ns * R + (j % Ns));
+#pragma unroll
+    for (int r = 0; r < R; ++r) b[r * (Ns + (Ns >> S))] = v[r];
+  } else {
+    const int d = (j / Ns) * Ns * R + (j % Ns);
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[padS<S>(d + r * Ns)] = v[r];
+  }
 }
 
 // One full smem->smem Stockham pass for a group of T threads (ti in [0,T)).

@@ -350,16 +350,18 @@ template <> struct FusedShape<4096> { static constexpr int NPAIR = 6, G = 2; };
 template <int NPHI>
 __global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
 k_irdft_readout(const float2* __restrict__ Yh, float* __restrict__ img, int nrho, int nrho_pad, int n, int nq,
-                int row_min, int nbands, const uint32_t* __restrict__ band_off,
-                const uint32_t* __restrict__ entries, const uint32_t* __restrict__ qidx,
-                const float2* __restrict__ qw, float scale, const float2* __restrict__ tw) {
+                int row_min, int nbands, const uint32_t* __restrict__ band_off, const uint4* __restrict__ entries,
+                float scale, const float2* __restrict__ tw) {
   constexpr int NPAIR = FusedShape<NPHI>::NPAIR;
   constexpr int G = FusedShape<NPHI>::G;
   constexpr int T = FftPlan<NPHI, true>::T;
   constexpr int NH = NPHI / 2 + 1;
-  constexpr int REG = padded_len(NPHI);  // float2 per pair region
+  // pair region: spectra interleaved [m][2] (row a, row b), then the FFT buffer,
+  // then the two real rows; pitch = 2 (mod 16) float2 so regions skew across banks
+  constexpr int REG = (padded_len(NPHI) + 13) / 16 * 16 + 2;
   constexpr int RB = 2 * NPAIR;
-  constexpr int RPITCH = NPHI + 16;      // floats from row a to row b inside a region
+  constexpr int RPITCH = NPHI + 16;  // floats from row a to row b inside a region
+  constexpr int ROUNDS = NPAIR / G;
   static_assert(2 * NH <= REG && RPITCH + NPHI <= 2 * REG, "pair region too small");
   static_assert(NPAIR % G == 0, "pairs must split evenly over FFT groups");
   extern __shared__ __align__(16) float2 smem_k45[];
@@ -367,36 +369,47 @@ k_irdft_readout(const float2* __restrict__ Yh, float* __restrict__ img, int nrho
   const int r0 = row_min + band * (RB - 1);
   const float2* src = Yh + (size_t)blockIdx.y * NH * nrho_pad;
 
-  for (int e = threadIdx.x; e < NH * RB; e += blockDim.x) {
-    const int m = e / RB, c = e - (e / RB) * RB;
-    float2* dst = smem_k45 + (c >> 1) * REG + (c & 1) * NH + m;
-    const int row = r0 + c;
-    if (row < nrho) cp_async8(dst, src + (size_t)m * nrho_pad + row);
-    else *dst = make_float2(0.f, 0.f);
+  // stage spectra round by round (one cp.async group per round) so later pairs
+  // stream in while earlier pairs are transformed
+#pragma unroll 1
+  for (int rd = 0; rd < ROUNDS; ++rd) {
+    constexpr int RR = 2 * G;  // rows per round
+    for (int e = threadIdx.x; e < NH * RR; e += blockDim.x) {
+      const int m = e / RR, c = rd * RR + (e - (e / RR) * RR);
+      float2* dst = smem_k45 + (c >> 1) * REG + 2 * m + (c & 1);
+      const int row = r0 + c;
+      if (row < nrho) cp_async8(dst, src + (size_t)m * nrho_pad + row);
+      else *dst = make_float2(0.f, 0.f);
+    }
+    cp_async_commit();
   }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
 
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
-#pragma unroll 1
-  for (int round = 0; round < NPAIR / G; ++round) {
+  static_assert(ROUNDS <= 4, "extend the wait ladder");
+#pragma unroll
+  for (int round = 0; round < ROUNDS; ++round) {
+    if (ROUNDS - 1 - round >= 3) cp_async_wait<3>();
+    else if (ROUNDS - 1 - round == 2) cp_async_wait<2>();
+    else if (ROUNDS - 1 - round == 1) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
     const int q = round * G + gi;
     float2* R = smem_k45 + q * REG;
     float* Rf = reinterpret_cast<float*>(R);
     auto load = [&](int idx) -> float2 {
       const bool hi = idx > NPHI / 2;
       const int mm = hi ? NPHI - idx : idx;
-      float2 xa = R[mm], xb = R[NH + mm];
+      const float4 x = *reinterpret_cast<const float4*>(R + 2 * mm);  // (Xa, Xb) at mm
+      float ay = x.y, by = x.w;
       if (mm == 0 || mm == NPHI / 2) {
-        xa.y = 0.f;
-        xb.y = 0.f;
+        ay = 0.f;
+        by = 0.f;
       }
       if (hi) {
-        xa.y = -xa.y;
-        xb.y = -xb.y;
+        ay = -ay;
+        by = -by;
       }
-      return make_float2(xa.x - xb.y, xa.y + xb.x);
+      return make_float2(x.x - by, ay + x.z);
     };
     auto store = [&](int idx, float2 v) {
       Rf[idx] = v.x;
@@ -410,17 +423,16 @@ k_irdft_readout(const float2* __restrict__ Yh, float* __restrict__ img, int nrho
   const int c = n / 2;
   float* out = img + (size_t)blockIdx.y * n * n;
   for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const uint32_t ent = __ldg(entries + e);
-    const int qq = (int)(ent & 0x7FFFFFFFu);
+    const uint4 ent = __ldg(entries + e);
+    const int qq = (int)(ent.x & 0x7FFFFFFFu);
     const int qy = qq / nq, qx = qq - (qq / nq) * nq;
     const int iyp = c + qy, iyn = n - 1 - c - qy;
     const int jxp = c + qx, jxn = n - 1 - c - qx;
     const bool dupy = iyn == iyp, dupx = jxn == jxp;  // odd n: centre row / column
     float v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f;
-    if (!(ent & 0x80000000u)) {
-      const uint32_t qe = __ldg(qidx + qq);
-      const float2 w = __ldg(qw + qq);
-      const int i0 = (int)(qe & 0xFFFFu), jr = (int)(qe >> 16);
+    if (!(ent.x & 0x80000000u)) {
+      const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
+      const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
       const int li0 = i0 - r0, li1 = min(i0 + 1, nrho - 1) - r0;
       const float* row0 = reinterpret_cast<const float*>(smem_k45 + (li0 >> 1) * REG) + (li0 & 1) * RPITCH;
       const float* row1 = reinterpret_cast<const float*>(smem_k45 + (li1 >> 1) * REG) + (li1 & 1) * RPITCH;
@@ -429,13 +441,13 @@ k_irdft_readout(const float2* __restrict__ Yh, float* __restrict__ img, int nrho
         const int j1 = (j0 + 1 == NPHI) ? 0 : j0 + 1;
         const float a0 = fmaf(wj, row0[j1] - row0[j0], row0[j0]);
         const float a1 = fmaf(wj, row1[j1] - row1[j0], row1[j0]);
-        return fmaf(w.x, a1 - a0, a0) * scale;
+        return fmaf(wi, a1 - a0, a0) * scale;
       };
-      const bool wz = w.y == 0.f;
-      const float wm = wz ? 0.f : 1.f - w.y;
-      v1 = sample(jr, w.y);                                      // x >= 0, y >= 0
+      const bool wz = wjr == 0.f;
+      const float wm = wz ? 0.f : 1.f - wjr;
+      v1 = sample(jr, wjr);                                      // x >= 0, y >= 0
       v2 = sample(wz ? NPHI / 2 - jr : NPHI / 2 - jr - 1, wm);  // x < 0, y >= 0: pi - phi
-      v3 = sample(NPHI / 2 + jr, w.y);                           // x < 0, y < 0: pi + phi
+      v3 = sample(NPHI / 2 + jr, wjr);                           // x < 0, y < 0: pi + phi
       v4 = sample(wz ? NPHI - jr : NPHI - jr - 1, wm);          // x >= 0, y < 0: 2 pi - phi
     }
     out[(size_t)iyp * n + jxp] = v1;
@@ -675,13 +687,14 @@ namespace {
 template <int NPHI>
 cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch, cudaStream_t s) {
   constexpr int G = FusedShape<NPHI>::G, NPAIR = FusedShape<NPHI>::NPAIR;
-  const size_t smem = (size_t)NPAIR * padded_len(NPHI) * sizeof(float2);
+  constexpr int REG = (padded_len(NPHI) + 13) / 16 * 16 + 2;
+  const size_t smem = (size_t)NPAIR * REG * sizeof(float2);
   auto k = k_irdft_readout<NPHI>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
   k<<<dim3(d.nbands, batch), G * FftPlan<NPHI, true>::T, smem, s>>>(
-      Yh, img, d.nrho, d.nrho_pad, d.n, d.nq, d.row_min, d.nbands, t.band_off, t.band_entries, t.qidx, t.qw,
-      d.out_scale, t.tw_phi);
+      Yh, img, d.nrho, d.nrho_pad, d.n, d.nq, d.row_min, d.nbands, t.band_off,
+      reinterpret_cast<const uint4*>(t.band_entries), d.out_scale, t.tw_phi);
   return cudaGetLastError();
 }
 }  // namespace

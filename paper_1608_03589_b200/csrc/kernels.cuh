@@ -26,7 +26,7 @@ struct DevTables {
   const float2* qw;       // [nq][nq] readout weights (wi, wj)
   const float2* naive_cs; // [ntheta] (cos, sin) * nt/(2n) for the direct backprojector
   const uint32_t* band_off;      // [nbands+1] fused readout: entry range per band
-  const uint32_t* band_entries;  // quadrant pixels per band (bit 31: write zero)
+  const uint32_t* band_entries;  // per band: uint4 {qq | bit31 zero, qidx, wi, wj} (plan_host band_packed)
 };
 
 struct Dims {

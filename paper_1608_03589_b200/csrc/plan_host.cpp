@@ -5,6 +5,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstring>
 #include <thread>
 
 namespace lpbp {
@@ -93,6 +94,18 @@ void build_bands(HostPlan& h, int band_rows) {
     h.band_entries.insert(h.band_entries.end(), zero[b].begin(), zero[b].end());
   }
   h.band_off[h.nbands] = (uint32_t)h.band_entries.size();
+  h.band_packed.resize(h.band_entries.size() * 4);
+  for (size_t e = 0; e < h.band_entries.size(); ++e) {
+    const uint32_t ent = h.band_entries[e];
+    const uint32_t qq = ent & 0x7FFFFFFFu;
+    uint32_t wi = 0, wj = 0;
+    std::memcpy(&wi, &h.qw[qq].x, 4);
+    std::memcpy(&wj, &h.qw[qq].y, 4);
+    h.band_packed[4 * e + 0] = ent;
+    h.band_packed[4 * e + 1] = h.qidx[qq];
+    h.band_packed[4 * e + 2] = wi;
+    h.band_packed[4 * e + 3] = wj;
+  }
 }
 
 double adaptive_rho0(int nx, int ny) { return std::log(std::min(2.0 / nx, 2.0 / ny)) - std::log(2.0); }

@@ -41,6 +41,8 @@ struct HostPlan {
   // whose i0 falls in the band (bit 31 set = write zero), band_off[b..b+1).
   int band_rows = 0, row_min = 0, nbands = 0;
   std::vector<uint32_t> band_entries, band_off;
+  // self-contained 16-byte entries {qq | zero flag, qidx, wi bits, wj bits}
+  std::vector<uint32_t> band_packed;
   // kernel support (for diagnostics/tests): cells (k, l) of the rolled kernel
   std::vector<int32_t> cell_k, cell_l;
 };
