@@ -138,12 +138,21 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
 // The row mix is evaluated inside the first forward pass; the multiply by
 // Khat is fused between the last forward and first inverse pass.
 // ---------------------------------------------------------------------------
-template <int L>
+// Output layouts: plain Y[b][m][rho] (nrho_pad pitch) for the stage API, or
+// BANDED Y[b][band][pair][m][2]: the exact shared-memory image of the fused
+// readout's pair regions (rows rho = row_min + band*(band_rows-1) + 2*pair + h;
+// the row shared by two bands is written to both), so that kernel fills each
+// region with one TMA bulk copy.
+struct BandedOut {
+  int row_min, step, npair, nbands;  // step = band_rows - 1
+};
+
+template <int L, bool BANDED>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, 2)
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int ns, int nrho,
            int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
            const int* __restrict__ ki, const float2* __restrict__ wi, const float2* __restrict__ khat,
-           const float2* __restrict__ tw) {
+           const float2* __restrict__ tw, BandedOut bo) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
   __shared__ __align__(8) uint64_t bars[2];
@@ -194,11 +203,25 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       return make_float2(fmaf(w.x, p0.x, w.y * p1.x), fmaf(w.x, p0.y, w.y * p1.y));
     };
     auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(kcol + idx)); };
-    float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
-    auto store = [&](int idx, float2 v) {
-      if (idx < nrho) ycol[idx] = v;
-    };
-    block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
+    if constexpr (!BANDED) {
+      float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
+      auto store = [&](int idx, float2 v) {
+        if (idx < nrho) ycol[idx] = v;
+      };
+      block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
+    } else {
+      const size_t ps = (size_t)nh * 2;           // pair stride (float2)
+      const size_t bs = ps * bo.npair;            // band stride
+      float2* yb = Yh + (size_t)b * bs * bo.nbands + 2 * m;
+      auto store = [&](int idx, float2 v) {
+        const int rel = idx - bo.row_min;
+        if (idx >= nrho || rel < 0) return;
+        const int band = rel / bo.step, c = rel - band * bo.step;
+        yb[band * bs + (c >> 1) * ps + (c & 1)] = v;
+        if (c == 0 && band > 0) yb[(band - 1) * bs + (bo.step >> 1) * ps + (bo.step & 1)] = v;
+      };
+      block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
+    }
   }
 }
 
@@ -365,41 +388,42 @@ k_irdft_readout(const float2* __restrict__ Yh, float* __restrict__ img, int nrho
   static_assert(2 * NH <= REG && RPITCH + NPHI <= 2 * REG, "pair region too small");
   static_assert(NPAIR % G == 0, "pairs must split evenly over FFT groups");
   extern __shared__ __align__(16) float2 smem_k45[];
+  __shared__ __align__(8) uint64_t bars[ROUNDS];
   const int band = nbands - 1 - (int)blockIdx.x;  // outer (pixel-heavy) bands first
   const int r0 = row_min + band * (RB - 1);
-  const float2* src = Yh + (size_t)blockIdx.y * NH * nrho_pad;
-
-  // stage spectra round by round (one cp.async group per round) so later pairs
-  // stream in while earlier pairs are transformed
-#pragma unroll 1
-  for (int rd = 0; rd < ROUNDS; ++rd) {
-    constexpr int RR = 2 * G;  // rows per round
-    for (int e = threadIdx.x; e < NH * RR; e += blockDim.x) {
-      const int m = e / RR, c = rd * RR + (e - (e / RR) * RR);
-      float2* dst = smem_k45 + (c >> 1) * REG + 2 * m + (c & 1);
-      const int row = r0 + c;
-      if (row < nrho) cp_async8(dst, src + (size_t)m * nrho_pad + row);
-      else *dst = make_float2(0.f, 0.f);
-    }
-    cp_async_commit();
+  // banded spectra (k_rho_conv<.., true>): this band's NPAIR pair images, each
+  // 2*NH float2 laid out [m][2] exactly as the shared pair region
+  const float2* src = Yh + ((size_t)blockIdx.y * nbands + band) * NPAIR * (2 * NH);
+  constexpr uint32_t PAIR_BYTES = 2 * NH * sizeof(float2);
+  static_assert(PAIR_BYTES % 16 == 0 && (REG * sizeof(float2)) % 16 == 0, "bulk copy granularity");
+  if (threadIdx.x == 0) {
+    for (int rd = 0; rd < ROUNDS; ++rd) mbar_init(&bars[rd], 1);
+    fence_mbar_init();
   }
-
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one TMA bulk copy per pair, one barrier per round of G pairs
+    for (int rd = 0; rd < ROUNDS; ++rd) {
+      mbar_arrive_expect_tx(&bars[rd], G * PAIR_BYTES);
+      for (int g = 0; g < G; ++g) {
+        const int q = rd * G + g;
+        tma_bulk_g2s(smem_k45 + q * REG, src + (size_t)q * (2 * NH), PAIR_BYTES, &bars[rd]);
+      }
+    }
+  }
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
-  static_assert(ROUNDS <= 4, "extend the wait ladder");
-#pragma unroll
+#pragma unroll 1
   for (int round = 0; round < ROUNDS; ++round) {
-    if (ROUNDS - 1 - round >= 3) cp_async_wait<3>();
-    else if (ROUNDS - 1 - round == 2) cp_async_wait<2>();
-    else if (ROUNDS - 1 - round == 1) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    __syncthreads();
+    mbar_wait(&bars[round], 0);
     const int q = round * G + gi;
     float2* R = smem_k45 + q * REG;
     float* Rf = reinterpret_cast<float*>(R);
+    const bool va = r0 + 2 * q < nrho, vb = r0 + 2 * q + 1 < nrho;  // rows past nrho are zero
     auto load = [&](int idx) -> float2 {
       const bool hi = idx > NPHI / 2;
       const int mm = hi ? NPHI - idx : idx;
-      const float4 x = *reinterpret_cast<const float4*>(R + 2 * mm);  // (Xa, Xb) at mm
+      float4 x = *reinterpret_cast<const float4*>(R + 2 * mm);  // (Xa, Xb) at mm
+      if (!va) x.x = x.y = 0.f;
+      if (!vb) x.z = x.w = 0.f;
       float ay = x.y, by = x.w;
       if (mm == 0 || mm == NPHI / 2) {
         ay = 0.f;
@@ -597,14 +621,15 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
   return cudaGetLastError();
 }
 
-template <int L>
+template <int L, bool BANDED>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
   const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + 2 * (size_t)d.nt) * sizeof(float2);
-  auto k = k_rho_conv<L>;
+  auto k = k_rho_conv<L, BANDED>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
+  const BandedOut bo{d.row_min, d.band_rows - 1, d.band_rows / 2, d.nbands};
   k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, d.ns, d.nrho, d.nrho_pad, d.nh, t.ab, t.wab,
-                                              t.ki, t.wi, t.khat, t.tw_rho);
+                                              t.ki, t.wi, t.khat, t.tw_rho, bo);
   return cudaGetLastError();
 }
 
@@ -639,13 +664,19 @@ cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, f
     default: return cudaErrorNotSupported;
   }
 }
-cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
-  switch (d.L) {
-    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, s);
-    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, s);
-    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, s);
-    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, s);
-    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, s);
+cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, bool banded,
+                            cudaStream_t s) {
+  switch (d.L * 2 + (banded ? 1 : 0)) {
+    case 1024: return conv_impl<512, false>(d, t, Gh, Yh, batch, s);
+    case 1025: return conv_impl<512, true>(d, t, Gh, Yh, batch, s);
+    case 2048: return conv_impl<1024, false>(d, t, Gh, Yh, batch, s);
+    case 2049: return conv_impl<1024, true>(d, t, Gh, Yh, batch, s);
+    case 4096: return conv_impl<2048, false>(d, t, Gh, Yh, batch, s);
+    case 4097: return conv_impl<2048, true>(d, t, Gh, Yh, batch, s);
+    case 8192: return conv_impl<4096, false>(d, t, Gh, Yh, batch, s);
+    case 8193: return conv_impl<4096, true>(d, t, Gh, Yh, batch, s);
+    case 16384: return conv_impl<8192, false>(d, t, Gh, Yh, batch, s);
+    case 16385: return conv_impl<8192, true>(d, t, Gh, Yh, batch, s);
     default: return cudaErrorNotSupported;
   }
 }
@@ -689,6 +720,7 @@ cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
   constexpr int G = FusedShape<NPHI>::G, NPAIR = FusedShape<NPHI>::NPAIR;
   constexpr int REG = (padded_len(NPHI) + 13) / 16 * 16 + 2;
   const size_t smem = (size_t)NPAIR * REG * sizeof(float2);
+  if (d.band_rows != 2 * NPAIR) return cudaErrorInvalidValue;
   auto k = k_irdft_readout<NPHI>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
