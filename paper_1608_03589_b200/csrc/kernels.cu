@@ -16,6 +16,9 @@
 // phi-DFTs of sinogram rows (the phi>=pi half picks up (-1)^m from its nphi/2
 // shift).  nt row FFTs replace nrho (~1.9x fewer) and the row mix moves into K3,
 // where it feeds the first rho-FFT pass straight from shared memory.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "async.cuh"
 #include "fft.cuh"
 #include "kernels.cuh"
@@ -139,10 +142,10 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
 // Khat is fused between the last forward and first inverse pass.
 // ---------------------------------------------------------------------------
 // Output layouts: plain Y[b][m][rho] (nrho_pad pitch) for the stage API, or
-// BANDED Y[b][band][pair][m][2]: the exact shared-memory image of the fused
-// readout's pair regions (rows rho = row_min + band*(band_rows-1) + 2*pair + h;
-// the row shared by two bands is written to both), so that kernel fills each
-// region with one TMA bulk copy.
+// BANDED Y[b][band][m][c]: rows rho = row_min + band*(band_rows-1) + c, c <
+// band_rows, contiguous per (band, m) (the row shared by two bands is written to
+// both).  The fused readout pulls {2 rows x 256 m} boxes of it with a 3-D TMA
+// tensor map straight into its [m][2] pair regions.
 struct BandedOut {
   int row_min, step, npair, nbands;  // step = band_rows - 1
 };
@@ -210,15 +213,15 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       };
       block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
     } else {
-      const size_t ps = (size_t)nh * 2;           // pair stride (float2)
-      const size_t bs = ps * bo.npair;            // band stride
-      float2* yb = Yh + (size_t)b * bs * bo.nbands + 2 * m;
+      const int rb = bo.step + 1;                 // rows per band
+      const size_t bs = (size_t)nh * rb;          // band stride (float2)
+      float2* yb = Yh + (size_t)b * bs * bo.nbands + (size_t)m * rb;
       auto store = [&](int idx, float2 v) {
         const int rel = idx - bo.row_min;
         if (idx >= nrho || rel < 0) return;
         const int band = rel / bo.step, c = rel - band * bo.step;
-        yb[band * bs + (c >> 1) * ps + (c & 1)] = v;
-        if (c == 0 && band > 0) yb[(band - 1) * bs + (bo.step >> 1) * ps + (bo.step & 1)] = v;
+        yb[band * bs + c] = v;
+        if (c == 0 && band > 0) yb[(band - 1) * bs + bo.step] = v;
       };
       block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
     }
@@ -372,7 +375,7 @@ template <> struct FusedShape<4096> { static constexpr int NPAIR = 6, G = 2; };
 
 template <int NPHI>
 __global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
-k_irdft_readout(const float2* __restrict__ Yh, float* __restrict__ img, int nrho, int nrho_pad, int n, int nq,
+k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ img, int nrho, int n, int nq,
                 int row_min, int nbands, const uint32_t* __restrict__ band_off, const uint4* __restrict__ entries,
                 float scale, const float2* __restrict__ tw) {
   constexpr int NPAIR = FusedShape<NPHI>::NPAIR;
@@ -391,22 +394,28 @@ k_irdft_readout(const float2* __restrict__ Yh, float* __restrict__ img, int nrho
   __shared__ __align__(8) uint64_t bars[ROUNDS];
   const int band = nbands - 1 - (int)blockIdx.x;  // outer (pixel-heavy) bands first
   const int r0 = row_min + band * (RB - 1);
-  // banded spectra (k_rho_conv<.., true>): this band's NPAIR pair images, each
-  // 2*NH float2 laid out [m][2] exactly as the shared pair region
-  const float2* src = Yh + ((size_t)blockIdx.y * nbands + band) * NPAIR * (2 * NH);
-  constexpr uint32_t PAIR_BYTES = 2 * NH * sizeof(float2);
-  static_assert(PAIR_BYTES % 16 == 0 && (REG * sizeof(float2)) % 16 == 0, "bulk copy granularity");
+  // banded spectra (k_rho_conv<.., true>) viewed as a 3-D tensor of floats
+  // {2*band_rows, NH, nbands*batch}: box {4 floats = rows 2q, 2q+1; 256 m; 1}
+  // lands as [m][2] float2 in pair region q.  ceil(NH/256) boxes per pair, the
+  // last one shifted back to end at NH-1 (rewrites identical values).
+  constexpr int NBOX = (NH + 255) / 256;
+  constexpr uint32_t PAIR_BYTES = NBOX * 256 * 16;
+  static_assert(NH >= 256 && 2 * NH <= REG, "box tiling");
   if (threadIdx.x == 0) {
     for (int rd = 0; rd < ROUNDS; ++rd) mbar_init(&bars[rd], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // one TMA bulk copy per pair, one barrier per round of G pairs
+  if (threadIdx.x == 0) {
+    const int zc = (int)blockIdx.y * nbands + band;
     for (int rd = 0; rd < ROUNDS; ++rd) {
       mbar_arrive_expect_tx(&bars[rd], G * PAIR_BYTES);
       for (int g = 0; g < G; ++g) {
         const int q = rd * G + g;
-        tma_bulk_g2s(smem_k45 + q * REG, src + (size_t)q * (2 * NH), PAIR_BYTES, &bars[rd]);
+        for (int bx = 0; bx < NBOX; ++bx) {
+          const int m0 = bx + 1 < NBOX ? bx * 256 : NH - 256;
+          tma_load_3d(smem_k45 + q * REG + 2 * m0, &ymap, 4 * q, m0, zc, &bars[rd]);
+        }
       }
     }
   }
@@ -704,6 +713,35 @@ cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dthe
   return cudaGetLastError();
 }
 
+namespace {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// Banded spectra Y[z][m][rb] (complex) as floats {2*rb, nh, nz}; box {4, 256, 1}.
+cudaError_t encode_band_map(CUtensorMap* map, const float2* Y, int rb, int nh, int nz) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * rb), (cuuint64_t)nh, (cuuint64_t)nz};
+  const cuuint64_t strides[2] = {(cuuint64_t)rb * 8, (cuuint64_t)rb * 8 * nh};
+  const cuuint32_t box[3] = {4, 256, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(Y), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+}  // namespace
+
 int fused_band_rows(int nphi) {
   switch (nphi) {
     case 512: return 2 * FusedShape<512>::NPAIR;
@@ -724,9 +762,12 @@ cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
   auto k = k_irdft_readout<NPHI>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
+  CUtensorMap map;
+  e = encode_band_map(&map, Yh, 2 * NPAIR, NPHI / 2 + 1, d.nbands * batch);
+  if (e) return e;
   k<<<dim3(d.nbands, batch), G * FftPlan<NPHI, true>::T, smem, s>>>(
-      Yh, img, d.nrho, d.nrho_pad, d.n, d.nq, d.row_min, d.nbands, t.band_off,
-      reinterpret_cast<const uint4*>(t.band_entries), d.out_scale, t.tw_phi);
+      map, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, t.band_off, reinterpret_cast<const uint4*>(t.band_entries),
+      d.out_scale, t.tw_phi);
   return cudaGetLastError();
 }
 }  // namespace
