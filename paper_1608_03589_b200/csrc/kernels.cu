@@ -368,10 +368,20 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 // ---------------------------------------------------------------------------
 template <int NPHI>
 struct FusedShape;
-template <> struct FusedShape<512>  { static constexpr int NPAIR = 8, G = 4; };
-template <> struct FusedShape<1024> { static constexpr int NPAIR = 8, G = 4; };
-template <> struct FusedShape<2048> { static constexpr int NPAIR = 8, G = 2; };
-template <> struct FusedShape<4096> { static constexpr int NPAIR = 6, G = 2; };
+template <int NPHI, int NPAIR_, int G_>
+struct FusedShapeBase {
+  static constexpr int NPAIR = NPAIR_, G = G_;
+  // region pitch (float2): holds ceil(NH/256) whole TMA boxes of [256][2] and the
+  // padded FFT buffer; multiple of 16 float2 (128 B) for TMA destinations
+  static constexpr int NBOX = (NPHI / 2 + 1 + 255) / 256;
+  static constexpr int RAW = 2 * NBOX * 256 > padded_len(NPHI) ? 2 * NBOX * 256 : padded_len(NPHI);
+  static constexpr int REG = (RAW + 15) / 16 * 16;
+  static constexpr size_t SMEM = (size_t)NPAIR * REG * 8 + 64;  // + mbarriers
+};
+template <> struct FusedShape<512> : FusedShapeBase<512, 8, 4> {};
+template <> struct FusedShape<1024> : FusedShapeBase<1024, 8, 4> {};
+template <> struct FusedShape<2048> : FusedShapeBase<2048, 8, 2> {};
+template <> struct FusedShape<4096> : FusedShapeBase<4096, 6, 2> {};
 
 template <int NPHI>
 __global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
@@ -382,25 +392,24 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
   constexpr int G = FusedShape<NPHI>::G;
   constexpr int T = FftPlan<NPHI, true>::T;
   constexpr int NH = NPHI / 2 + 1;
-  // pair region: spectra interleaved [m][2] (row a, row b), then the FFT buffer,
-  // then the two real rows; pitch = 2 (mod 16) float2 so regions skew across banks
-  constexpr int REG = (padded_len(NPHI) + 13) / 16 * 16 + 2;
+  // pair region: spectra interleaved [m][2] (row a, row b) as whole 256-row TMA
+  // boxes, then the FFT buffer, then the two real rows; 128-B aligned pitch
+  constexpr int REG = FusedShape<NPHI>::REG;
   constexpr int RB = 2 * NPAIR;
   constexpr int RPITCH = NPHI + 16;  // floats from row a to row b inside a region
   constexpr int ROUNDS = NPAIR / G;
   static_assert(2 * NH <= REG && RPITCH + NPHI <= 2 * REG, "pair region too small");
   static_assert(NPAIR % G == 0, "pairs must split evenly over FFT groups");
-  extern __shared__ __align__(16) float2 smem_k45[];
-  __shared__ __align__(8) uint64_t bars[ROUNDS];
+  extern __shared__ __align__(128) float2 smem_k45[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NPAIR * REG);
   const int band = nbands - 1 - (int)blockIdx.x;  // outer (pixel-heavy) bands first
   const int r0 = row_min + band * (RB - 1);
   // banded spectra (k_rho_conv<.., true>) viewed as a 3-D tensor of floats
   // {2*band_rows, NH, nbands*batch}: box {4 floats = rows 2q, 2q+1; 256 m; 1}
-  // lands as [m][2] float2 in pair region q.  ceil(NH/256) boxes per pair, the
-  // last one shifted back to end at NH-1 (rewrites identical values).
+  // lands as [m][2] float2 in pair region q (rows m >= NH are zero-filled).
   constexpr int NBOX = (NH + 255) / 256;
   constexpr uint32_t PAIR_BYTES = NBOX * 256 * 16;
-  static_assert(NH >= 256 && 2 * NH <= REG, "box tiling");
+  static_assert(2 * NBOX * 256 <= REG && REG % 16 == 0, "box tiling");
   if (threadIdx.x == 0) {
     for (int rd = 0; rd < ROUNDS; ++rd) mbar_init(&bars[rd], 1);
     fence_mbar_init();
@@ -412,10 +421,8 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
       mbar_arrive_expect_tx(&bars[rd], G * PAIR_BYTES);
       for (int g = 0; g < G; ++g) {
         const int q = rd * G + g;
-        for (int bx = 0; bx < NBOX; ++bx) {
-          const int m0 = bx + 1 < NBOX ? bx * 256 : NH - 256;
-          tma_load_3d(smem_k45 + q * REG + 2 * m0, &ymap, 4 * q, m0, zc, &bars[rd]);
-        }
+        for (int bx = 0; bx < NBOX; ++bx)
+          tma_load_3d(smem_k45 + q * REG + 2 * (bx * 256), &ymap, 4 * q, bx * 256, zc, &bars[rd]);
       }
     }
   }
@@ -756,8 +763,7 @@ namespace {
 template <int NPHI>
 cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch, cudaStream_t s) {
   constexpr int G = FusedShape<NPHI>::G, NPAIR = FusedShape<NPHI>::NPAIR;
-  constexpr int REG = (padded_len(NPHI) + 13) / 16 * 16 + 2;
-  const size_t smem = (size_t)NPAIR * REG * sizeof(float2);
+  const size_t smem = FusedShape<NPHI>::SMEM;
   if (d.band_rows != 2 * NPAIR) return cudaErrorInvalidValue;
   auto k = k_irdft_readout<NPHI>;
   cudaError_t e = prep(k, smem);
