@@ -187,8 +187,7 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   if (e) return launch_fail(e, "row_rdft");
   ++g_launches;
   e = staged(P, 2, c, s, [&] {
-    return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c,
-                                 !stop_after_lp, s);
+    return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c, s);
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
@@ -320,7 +319,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   d.nbands = h.nbands;
   d.band_rows = h.band_rows;
   const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;
-  const size_t Y = std::max((size_t)h.nh * h.nrho_pad, (size_t)h.nbands * h.band_rows * h.nh) * sizeof(float2);
+  const size_t Y = (size_t)h.nh * h.nrho_pad * sizeof(float2);
   const size_t G = (size_t)h.nh * h.nt * sizeof(float2);
   const size_t lp = (size_t)h.nrho * h.nphi * sizeof(float);
   P->szA = std::max(fg, Y);

@@ -141,21 +141,12 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
 // The row mix is evaluated inside the first forward pass; the multiply by
 // Khat is fused between the last forward and first inverse pass.
 // ---------------------------------------------------------------------------
-// Output layouts: plain Y[b][m][rho] (nrho_pad pitch) for the stage API, or
-// BANDED Y[b][band][m][c]: rows rho = row_min + band*(band_rows-1) + c, c <
-// band_rows, contiguous per (band, m) (the row shared by two bands is written to
-// both).  The fused readout pulls {2 rows x 256 m} boxes of it with a 3-D TMA
-// tensor map straight into its [m][2] pair regions.
-struct BandedOut {
-  int row_min, step, npair, nbands;  // step = band_rows - 1
-};
-
-template <int L, bool BANDED>
+template <int L>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, 2)
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int ns, int nrho,
            int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
            const int* __restrict__ ki, const float2* __restrict__ wi, const float2* __restrict__ khat,
-           const float2* __restrict__ tw, BandedOut bo) {
+           const float2* __restrict__ tw) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
   __shared__ __align__(8) uint64_t bars[2];
@@ -206,25 +197,11 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       return make_float2(fmaf(w.x, p0.x, w.y * p1.x), fmaf(w.x, p0.y, w.y * p1.y));
     };
     auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(kcol + idx)); };
-    if constexpr (!BANDED) {
-      float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
-      auto store = [&](int idx, float2 v) {
-        if (idx < nrho) ycol[idx] = v;
-      };
-      block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
-    } else {
-      const int rb = bo.step + 1;                 // rows per band
-      const size_t bs = (size_t)nh * rb;          // band stride (float2)
-      float2* yb = Yh + (size_t)b * bs * bo.nbands + (size_t)m * rb;
-      auto store = [&](int idx, float2 v) {
-        const int rel = idx - bo.row_min;
-        if (idx >= nrho || rel < 0) return;
-        const int band = rel / bo.step, c = rel - band * bo.step;
-        yb[band * bs + c] = v;
-        if (c == 0 && band > 0) yb[(band - 1) * bs + bo.step] = v;
-      };
-      block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
-    }
+    float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
+    auto store = [&](int idx, float2 v) {
+      if (idx < nrho) ycol[idx] = v;
+    };
+    block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
   }
 }
 
@@ -359,85 +336,70 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 }
 
 // ---------------------------------------------------------------------------
-// K45: fused inverse phi-DFT + Cartesian readout.  One CTA per band of RB = 2*NPAIR
+// K45: fused inverse phi-DFT + Cartesian readout.  One CTA per band of RB = 4*NQ
 // consecutive log-polar rows (bands overlap by one row so every pixel's two taps
-// i0, i0+1 lie in one band).  Each pair's spectra are staged into its own shared
-// region, transformed in place, and the real rows stay in shared memory for the
-// bilinear readout of the band's pixels (plan-time list of quadrant pixels; each
-// entry writes its four mirror pixels).  The log-polar image never reaches HBM.
+// i0, i0+1 lie in one band).  The band's spectra arrive by TMA: a 3-D tensor map
+// over Y[b][m][rho] with box {4 rows (32 B), 256 m} lands [m][4] in a "quad"
+// region; the CTA's two FFT groups transform the quad's two row pairs in place
+// (each in its half of the region), so the real log-polar rows stay in shared
+// memory for the bilinear readout of the band's pixels (plan-time list of
+// quadrant pixels; each entry writes its four mirror pixels).  The log-polar
+// image never reaches HBM.
 // ---------------------------------------------------------------------------
 template <int NPHI>
-struct FusedShape;
-template <int NPHI, int NPAIR_, int G_>
-struct FusedShapeBase {
-  static constexpr int NPAIR = NPAIR_, G = G_;
-  // region pitch (float2): holds ceil(NH/256) whole TMA boxes of [256][2] and the
-  // padded FFT buffer; multiple of 16 float2 (128 B) for TMA destinations
+struct FusedShape {
+  static constexpr int NQ = NPHI >= 4096 ? 3 : 4;   // quads (4 rows) per band
+  static constexpr int G = 2;                        // FFT groups = pairs per quad
   static constexpr int NBOX = (NPHI / 2 + 1 + 255) / 256;
-  static constexpr int RAW = 2 * NBOX * 256 > padded_len(NPHI) ? 2 * NBOX * 256 : padded_len(NPHI);
-  static constexpr int REG = (RAW + 15) / 16 * 16;
-  static constexpr size_t SMEM = (size_t)NPAIR * REG * 8 + 64;  // + mbarriers
+  static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16;  // FFT buffer / row storage per group
+  static constexpr int QREG0 = 4 * 256 * NBOX > 2 * HALF ? 4 * 256 * NBOX : 2 * HALF;
+  static constexpr int QREG = (QREG0 + 15) / 16 * 16;             // float2, 128-B multiple
+  static constexpr int RB = 4 * NQ;
+  static constexpr size_t SMEM = (size_t)NQ * QREG * 8 + 64;       // + mbarriers
 };
-template <> struct FusedShape<512> : FusedShapeBase<512, 8, 4> {};
-template <> struct FusedShape<1024> : FusedShapeBase<1024, 8, 4> {};
-template <> struct FusedShape<2048> : FusedShapeBase<2048, 8, 2> {};
-template <> struct FusedShape<4096> : FusedShapeBase<4096, 6, 2> {};
 
 template <int NPHI>
 __global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
 k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ img, int nrho, int n, int nq,
                 int row_min, int nbands, const uint32_t* __restrict__ band_off, const uint4* __restrict__ entries,
                 float scale, const float2* __restrict__ tw) {
-  constexpr int NPAIR = FusedShape<NPHI>::NPAIR;
-  constexpr int G = FusedShape<NPHI>::G;
+  using FS = FusedShape<NPHI>;
+  constexpr int NQ = FS::NQ, G = FS::G, QREG = FS::QREG, HALF = FS::HALF, RB = FS::RB, NBOX = FS::NBOX;
   constexpr int T = FftPlan<NPHI, true>::T;
-  constexpr int NH = NPHI / 2 + 1;
-  // pair region: spectra interleaved [m][2] (row a, row b) as whole 256-row TMA
-  // boxes, then the FFT buffer, then the two real rows; 128-B aligned pitch
-  constexpr int REG = FusedShape<NPHI>::REG;
-  constexpr int RB = 2 * NPAIR;
-  constexpr int RPITCH = NPHI + 16;  // floats from row a to row b inside a region
-  constexpr int ROUNDS = NPAIR / G;
-  static_assert(2 * NH <= REG && RPITCH + NPHI <= 2 * REG, "pair region too small");
-  static_assert(NPAIR % G == 0, "pairs must split evenly over FFT groups");
+  constexpr int RPITCH = NPHI + 16;  // floats from row a to row b inside a group half
+  static_assert(RPITCH + NPHI <= 2 * HALF, "row storage");
   extern __shared__ __align__(128) float2 smem_k45[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NPAIR * REG);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NQ * QREG);
   const int band = nbands - 1 - (int)blockIdx.x;  // outer (pixel-heavy) bands first
   const int r0 = row_min + band * (RB - 1);
-  // banded spectra (k_rho_conv<.., true>) viewed as a 3-D tensor of floats
-  // {2*band_rows, NH, nbands*batch}: box {4 floats = rows 2q, 2q+1; 256 m; 1}
-  // lands as [m][2] float2 in pair region q (rows m >= NH are zero-filled).
-  constexpr int NBOX = (NH + 255) / 256;
-  constexpr uint32_t PAIR_BYTES = NBOX * 256 * 16;
-  static_assert(2 * NBOX * 256 <= REG && REG % 16 == 0, "box tiling");
+  constexpr uint32_t QUAD_BYTES = NBOX * 256 * 32;
   if (threadIdx.x == 0) {
-    for (int rd = 0; rd < ROUNDS; ++rd) mbar_init(&bars[rd], 1);
+    for (int k = 0; k < NQ; ++k) mbar_init(&bars[k], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const int zc = (int)blockIdx.y * nbands + band;
-    for (int rd = 0; rd < ROUNDS; ++rd) {
-      mbar_arrive_expect_tx(&bars[rd], G * PAIR_BYTES);
-      for (int g = 0; g < G; ++g) {
-        const int q = rd * G + g;
-        for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_3d(smem_k45 + q * REG + 2 * (bx * 256), &ymap, 4 * q, bx * 256, zc, &bars[rd]);
-      }
+  if (threadIdx.x == 0) {  // all quads in flight at once; quad k completes on bars[k]
+    for (int k = 0; k < NQ; ++k) {
+      mbar_arrive_expect_tx(&bars[k], QUAD_BYTES);
+      for (int bx = 0; bx < NBOX; ++bx)
+        tma_load_3d(smem_k45 + k * QREG + 4 * (bx * 256), &ymap, 2 * (r0 + 4 * k), bx * 256, (int)blockIdx.y,
+                    &bars[k]);
     }
   }
+
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
 #pragma unroll 1
-  for (int round = 0; round < ROUNDS; ++round) {
-    mbar_wait(&bars[round], 0);
-    const int q = round * G + gi;
-    float2* R = smem_k45 + q * REG;
+  for (int k = 0; k < NQ; ++k) {
+    mbar_wait(&bars[k], 0);
+    float2* Q = smem_k45 + k * QREG;
+    float2* R = Q + gi * HALF;  // this group's FFT buffer, later its two real rows
     float* Rf = reinterpret_cast<float*>(R);
-    const bool va = r0 + 2 * q < nrho, vb = r0 + 2 * q + 1 < nrho;  // rows past nrho are zero
+    const int ra = r0 + 4 * k + 2 * gi;
+    const bool va = ra < nrho, vb = ra + 1 < nrho;  // rows past nrho read padding: zero
     auto load = [&](int idx) -> float2 {
       const bool hi = idx > NPHI / 2;
       const int mm = hi ? NPHI - idx : idx;
-      float4 x = *reinterpret_cast<const float4*>(R + 2 * mm);  // (Xa, Xb) at mm
+      float4 x = *reinterpret_cast<const float4*>(Q + 4 * mm + 2 * gi);  // (Xa, Xb) at mm
       if (!va) x.x = x.y = 0.f;
       if (!vb) x.z = x.w = 0.f;
       float ay = x.y, by = x.w;
@@ -459,6 +421,9 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
   }
   __syncthreads();
 
+  auto row_ptr = [&](int li) {  // local row li -> quad li/4, group (li/2)%2, row li%2
+    return reinterpret_cast<const float*>(smem_k45 + (li >> 2) * QREG + ((li >> 1) & 1) * HALF) + (li & 1) * RPITCH;
+  };
   const uint32_t e0 = __ldg(band_off + band), e1 = __ldg(band_off + band + 1);
   const int c = n / 2;
   float* out = img + (size_t)blockIdx.y * n * n;
@@ -473,9 +438,8 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
     if (!(ent.x & 0x80000000u)) {
       const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
       const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
-      const int li0 = i0 - r0, li1 = min(i0 + 1, nrho - 1) - r0;
-      const float* row0 = reinterpret_cast<const float*>(smem_k45 + (li0 >> 1) * REG) + (li0 & 1) * RPITCH;
-      const float* row1 = reinterpret_cast<const float*>(smem_k45 + (li1 >> 1) * REG) + (li1 & 1) * RPITCH;
+      const float* row0 = row_ptr(i0 - r0);
+      const float* row1 = row_ptr(min(i0 + 1, nrho - 1) - r0);
       auto sample = [&](int j0, float wj) {
         if (j0 >= NPHI) j0 -= NPHI;
         const int j1 = (j0 + 1 == NPHI) ? 0 : j0 + 1;
@@ -637,15 +601,14 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
   return cudaGetLastError();
 }
 
-template <int L, bool BANDED>
+template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
   const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + 2 * (size_t)d.nt) * sizeof(float2);
-  auto k = k_rho_conv<L, BANDED>;
+  auto k = k_rho_conv<L>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
-  const BandedOut bo{d.row_min, d.band_rows - 1, d.band_rows / 2, d.nbands};
   k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, d.ns, d.nrho, d.nrho_pad, d.nh, t.ab, t.wab,
-                                              t.ki, t.wi, t.khat, t.tw_rho, bo);
+                                              t.ki, t.wi, t.khat, t.tw_rho);
   return cudaGetLastError();
 }
 
@@ -680,19 +643,13 @@ cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, f
     default: return cudaErrorNotSupported;
   }
 }
-cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, bool banded,
-                            cudaStream_t s) {
-  switch (d.L * 2 + (banded ? 1 : 0)) {
-    case 1024: return conv_impl<512, false>(d, t, Gh, Yh, batch, s);
-    case 1025: return conv_impl<512, true>(d, t, Gh, Yh, batch, s);
-    case 2048: return conv_impl<1024, false>(d, t, Gh, Yh, batch, s);
-    case 2049: return conv_impl<1024, true>(d, t, Gh, Yh, batch, s);
-    case 4096: return conv_impl<2048, false>(d, t, Gh, Yh, batch, s);
-    case 4097: return conv_impl<2048, true>(d, t, Gh, Yh, batch, s);
-    case 8192: return conv_impl<4096, false>(d, t, Gh, Yh, batch, s);
-    case 8193: return conv_impl<4096, true>(d, t, Gh, Yh, batch, s);
-    case 16384: return conv_impl<8192, false>(d, t, Gh, Yh, batch, s);
-    case 16385: return conv_impl<8192, true>(d, t, Gh, Yh, batch, s);
+cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
+  switch (d.L) {
+    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, s);
+    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, s);
+    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, s);
+    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, s);
+    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, s);
     default: return cudaErrorNotSupported;
   }
 }
@@ -734,13 +691,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// Banded spectra Y[z][m][rb] (complex) as floats {2*rb, nh, nz}; box {4, 256, 1}.
-cudaError_t encode_band_map(CUtensorMap* map, const float2* Y, int rb, int nh, int nz) {
+// Spectra Y[b][m][rho] (complex, rho pitch nrho_pad) as floats {2*nrho_pad, nh, batch};
+// box {8 floats = 4 rows, 256 m, 1}.
+cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, int nh, int batch) {
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
-  const cuuint64_t dims[3] = {(cuuint64_t)(2 * rb), (cuuint64_t)nh, (cuuint64_t)nz};
-  const cuuint64_t strides[2] = {(cuuint64_t)rb * 8, (cuuint64_t)rb * 8 * nh};
-  const cuuint32_t box[3] = {4, 256, 1};
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * nrho_pad), (cuuint64_t)nh, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)nrho_pad * 8, (cuuint64_t)nrho_pad * 8 * nh};
+  const cuuint32_t box[3] = {8, 256, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(Y), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -751,10 +709,10 @@ cudaError_t encode_band_map(CUtensorMap* map, const float2* Y, int rb, int nh, i
 
 int fused_band_rows(int nphi) {
   switch (nphi) {
-    case 512: return 2 * FusedShape<512>::NPAIR;
-    case 1024: return 2 * FusedShape<1024>::NPAIR;
-    case 2048: return 2 * FusedShape<2048>::NPAIR;
-    case 4096: return 2 * FusedShape<4096>::NPAIR;
+    case 512: return FusedShape<512>::RB;
+    case 1024: return FusedShape<1024>::RB;
+    case 2048: return FusedShape<2048>::RB;
+    case 4096: return FusedShape<4096>::RB;
     default: return -1;
   }
 }
@@ -762,16 +720,15 @@ int fused_band_rows(int nphi) {
 namespace {
 template <int NPHI>
 cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch, cudaStream_t s) {
-  constexpr int G = FusedShape<NPHI>::G, NPAIR = FusedShape<NPHI>::NPAIR;
-  const size_t smem = FusedShape<NPHI>::SMEM;
-  if (d.band_rows != 2 * NPAIR) return cudaErrorInvalidValue;
+  using FS = FusedShape<NPHI>;
+  if (d.band_rows != FS::RB) return cudaErrorInvalidValue;
   auto k = k_irdft_readout<NPHI>;
-  cudaError_t e = prep(k, smem);
+  cudaError_t e = prep(k, FS::SMEM);
   if (e) return e;
   CUtensorMap map;
-  e = encode_band_map(&map, Yh, 2 * NPAIR, NPHI / 2 + 1, d.nbands * batch);
+  e = encode_spectra_map(&map, Yh, d.nrho_pad, NPHI / 2 + 1, batch);
   if (e) return e;
-  k<<<dim3(d.nbands, batch), G * FftPlan<NPHI, true>::T, smem, s>>>(
+  k<<<dim3(d.nbands, batch), FS::G * FftPlan<NPHI, true>::T, FS::SMEM, s>>>(
       map, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, t.band_off, reinterpret_cast<const uint4*>(t.band_entries),
       d.out_scale, t.tw_phi);
   return cudaGetLastError();

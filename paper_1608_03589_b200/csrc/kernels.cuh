@@ -39,9 +39,7 @@ struct Dims {
 // cudaErrorNotSupported when no instantiation exists for the size.
 cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s);
 cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* G, int batch, cudaStream_t s);
-// banded: write Y in the fused readout's band layout (see k_rho_conv) instead of [b][m][rho]
-cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, bool banded,
-                            cudaStream_t s);
+cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, cudaStream_t s);
 cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch, cudaStream_t s);
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Y, float* img, int batch,
                                  cudaStream_t s);
