@@ -337,8 +337,8 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 
 // ---------------------------------------------------------------------------
 // K45: fused inverse phi-DFT + Cartesian readout.  One CTA per band of RB = 4*NQ
-// consecutive log-polar rows (bands overlap by one row so every pixel's two taps
-// i0, i0+1 lie in one band).  The band's spectra arrive by TMA: a 3-D tensor map
+// consecutive log-polar rows starting at an even row (bands overlap by two rows
+// so every pixel's two taps i0, i0+1 lie in one band).  The band's spectra arrive by TMA: a 3-D tensor map
 // over Y[b][m][rho] with box {4 rows (32 B), 256 m} lands [m][4] in a "quad"
 // region; the CTA's two FFT groups transform the quad's two row pairs in place
 // (each in its half of the region), so the real log-polar rows stay in shared
@@ -371,7 +371,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
   extern __shared__ __align__(128) float2 smem_k45[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NQ * QREG);
   const int band = nbands - 1 - (int)blockIdx.x;  // outer (pixel-heavy) bands first
-  const int r0 = row_min + band * (RB - 1);
+  const int r0 = row_min + band * (RB - 2);  // even: TMA box rows start 16-B aligned
   constexpr uint32_t QUAD_BYTES = NBOX * 256 * 32;
   if (threadIdx.x == 0) {
     for (int k = 0; k < NQ; ++k) mbar_init(&bars[k], 1);

@@ -71,7 +71,8 @@ void build_bands(HostPlan& h, int band_rows) {
   for (size_t e = 0; e < nqq; ++e)
     if (h.qidx[e] != 0xFFFFFFFFu) rmin = std::min(rmin, (int)(h.qidx[e] & 0xFFFFu));
   if (rmin == h.nrho) rmin = 0;
-  const int step = band_rows - 1;
+  rmin &= ~1;                      // even band starts: 16-B aligned TMA boxes of row pairs
+  const int step = band_rows - 2;  // bands overlap by two rows (taps i0, i0+1 stay inside)
   h.band_rows = band_rows;
   h.row_min = rmin;
   h.nbands = std::max(1, (h.nrho - rmin + step - 1) / step);

@@ -37,7 +37,7 @@ struct HostPlan {
   std::vector<int32_t> ki;
   std::vector<uint32_t> qidx;
   // fused inverse-DFT + readout: bands of band_rows log-polar rows starting at
-  // row_min + b*(band_rows-1); band_entries lists quadrant pixels (qy*nq + qx)
+  // row_min + b*(band_rows-2) (row_min even); band_entries lists quadrant pixels (qy*nq + qx)
   // whose i0 falls in the band (bit 31 set = write zero), band_off[b..b+1).
   int band_rows = 0, row_min = 0, nbands = 0;
   std::vector<uint32_t> band_entries, band_off;

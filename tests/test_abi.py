@@ -205,7 +205,8 @@ def test_fused_readout_bands_cover_every_pixel_once(nt, nth, n, rho0):
         q = (e & 0x7FFFFFFF).astype(np.int64)
         z = (e & 0x80000000) != 0
         qy, qx = q // nq, q % nq
-        r0 = i.row_min + b * (i.band_rows - 1)
+        r0 = i.row_min + b * (i.band_rows - 2)
+        assert r0 % 2 == 0
         qi = qidx[q[~z]]
         assert np.all(qi[qi != 0xFFFFFFFF] != 0xFFFFFFFF)
         i0 = (qi & 0xFFFF).astype(np.int64)
