@@ -25,19 +25,51 @@
 
 namespace lpbp {
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Complex arithmetic on sm_100a packed-fp32 pipes (FADD2 / FMUL2 / FFMA2).  ptxas
+// folds lane broadcasts, lane swaps and single-lane negation into the f32x2
+// operands, so a complex add is one instruction and a complex multiply two.
+__device__ __forceinline__ unsigned long long pk2(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 v2mul(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return up2(r);
+}
+__device__ __forceinline__ float2 v2fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return up2(r);
+}
+// a * b = (a.x b.x, a.y b.x) + b.y (-a.y, a.x)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  const float2 t = v2mul(pk2(a.x, a.y), pk2(b.x, b.x));
+  return v2fma(pk2(-a.y, a.x), pk2(b.y, b.y), pk2(t.x, t.y));
 }
-// a * conj(b)
+// a * conj(b) = (a.x b.x, a.y b.x) + b.y (a.y, -a.x)
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+  const float2 t = v2mul(pk2(a.x, a.y), pk2(b.x, b.x));
+  return v2fma(pk2(a.y, -a.x), pk2(b.y, b.y), pk2(t.x, t.y));
 }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return v2mul(pk2(a.x, a.y), pk2(s, s)); }
 
-// Shared-memory padding: one float2 every 2^S elements.  S = 4 makes the
-// radix-16 Ns = 1 scatter (stride 16) conflict-free, S = 5 the radix-32 one.
 template <int S>
 __host__ __device__ constexpr int padS(int i) { return i + (i >> S); }
 __host__ __device__ constexpr int pad16(int i) { return i + (i >> 4); }
@@ -78,7 +110,7 @@ __device__ __forceinline__ float2 twc(float2 x) {
     constexpr int k32 = k * (32 / R);
     constexpr float c = (float)cos32(k32);
     constexpr float s = INV ? (float)sin32(k32) : -(float)sin32(k32);
-    return make_float2(fmaf(c, x.x, -s * x.y), fmaf(s, x.x, c * x.y));
+    return cmul(x, make_float2(c, s));
   }
 }
 

@@ -378,7 +378,11 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
     fence_mbar_init();
   }
   __syncthreads();
+  const uint32_t e0 = __ldg(band_off + band), e1 = __ldg(band_off + band + 1);
   if (threadIdx.x == 0) {  // all quads in flight at once; quad k completes on bars[k]
+    // warm L2 with this band's pixel entries (read after the transforms)
+    for (uint32_t off = e0 & ~3u; off < e1; off += 4096)
+      prefetch_l2_bulk(entries + off, 16u * (min(e1, off + 4096) - off));
     for (int k = 0; k < NQ; ++k) {
       mbar_arrive_expect_tx(&bars[k], QUAD_BYTES);
       for (int bx = 0; bx < NBOX; ++bx)
@@ -424,9 +428,9 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
   auto row_ptr = [&](int li) {  // local row li -> quad li/4, group (li/2)%2, row li%2
     return reinterpret_cast<const float*>(smem_k45 + (li >> 2) * QREG + ((li >> 1) & 1) * HALF) + (li & 1) * RPITCH;
   };
-  const uint32_t e0 = __ldg(band_off + band), e1 = __ldg(band_off + band + 1);
   const int c = n / 2;
   float* out = img + (size_t)blockIdx.y * n * n;
+#pragma unroll 2
   for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const uint4 ent = __ldg(entries + e);
     const int qq = (int)(ent.x & 0x7FFFFFFFu);
