@@ -35,7 +35,7 @@ __device__ __forceinline__ void block_sync() { __syncthreads(); }
 // unpacking is needed).  Tile: all nt rows x TC columns staged in smem.
 // ---------------------------------------------------------------------------
 template <int M, int TC, int G>
-__global__ void __launch_bounds__(G * FftPlan<M, false>::T, 1)
+__global__ void __launch_bounds__(G * FftPlan<M, false>::T, (G == 1 ? 2 : 1))
 k_ramp(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
        const float* __restrict__ resp, const float2* __restrict__ tw) {
   constexpr int T = FftPlan<M, false>::T;
@@ -93,16 +93,23 @@ k_ramp(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
 //   A[m] = (Z[m] + conj Z[-m]) / 2,  B[m] = (Z[m] - conj Z[-m]) / 2i
 // and staged as [m][TR] so the write of G[m][t0..t0+TR) is contiguous.
 // ---------------------------------------------------------------------------
+// Dense staging [m][TR] with an XOR swizzle of the column: for 16 consecutive m the
+// 8-byte slots (TR*m + (c ^ sw(m))) mod 16 are all distinct -> conflict-free.
+template <int TR>
+__device__ __forceinline__ int stg_col(int m, int c) {
+  static_assert(TR >= 2 && TR <= 16 && (TR & (TR - 1)) == 0, "TR power of two <= 16");
+  return c ^ ((m / (16 / TR)) & (TR - 1));
+}
+
 template <int NPHI, int TR, int G>
-__global__ void __launch_bounds__(G * FftPlan<NPHI, false>::T)
+__global__ void __launch_bounds__(G * FftPlan<NPHI, false>::T, (G == 1 ? 2 : 1))
 k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const float2* __restrict__ tw) {
   constexpr int T = FftPlan<NPHI, false>::T;
   constexpr int NTH = NPHI / 2;
   constexpr int NH = NPHI / 2 + 1;
-  constexpr int SP = TR + 1;  // odd pitch: conflict-free staging writes
   extern __shared__ __align__(16) float2 smem_k2[];
-  float2* stg = smem_k2;
-  float2* buf = smem_k2 + NH * SP + (threadIdx.x / T) * padded_len(NPHI);
+  float2* stg = smem_k2;  // [NH][TR], swizzled columns
+  float2* buf = smem_k2 + ((NH * TR + 15) & ~15) + (threadIdx.x / T) * padded_len(NPHI);
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int t0 = blockIdx.x * TR;
   const float* src = g + (size_t)blockIdx.y * nt * NTH;
@@ -120,8 +127,8 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
     for (int m = ti; m < NH; m += T) {
       const float2 z = buf[pad16(m)];
       const float2 w = buf[pad16((NPHI - m) & (NPHI - 1))];
-      stg[m * SP + 2 * q] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
-      stg[m * SP + 2 * q + 1] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+      stg[m * TR + stg_col<TR>(m, 2 * q)] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
+      stg[m * TR + stg_col<TR>(m, 2 * q + 1)] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
     }
     __syncthreads();
   }
@@ -129,7 +136,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
 #pragma unroll 8
   for (int e = threadIdx.x; e < NH * TR; e += blockDim.x) {
     const int m = e / TR, c = e % TR;
-    dst[(size_t)m * nt + c] = stg[m * SP + c];
+    dst[(size_t)m * nt + c] = stg[m * TR + stg_col<TR>(m, c)];
   }
 }
 
@@ -597,7 +604,7 @@ cudaError_t ramp_impl(const Dims& d, const DevTables& t, const float* g, float* 
 template <int NPHI, int TR, int G>
 cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch, cudaStream_t s) {
   if (d.nt % TR) return cudaErrorNotSupported;
-  const size_t smem = ((size_t)(NPHI / 2 + 1) * (TR + 1) + (size_t)G * padded_len(NPHI)) * sizeof(float2);
+  const size_t smem = ((size_t)(((NPHI / 2 + 1) * TR + 15) & ~15) + (size_t)G * padded_len(NPHI)) * sizeof(float2);
   auto k = k_row_rdft<NPHI, TR, G>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
@@ -633,8 +640,8 @@ cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float
   switch (d.M) {
     case 512: return ramp_impl<512, 16, 4>(d, t, g, out, batch, s);
     case 1024: return ramp_impl<1024, 16, 2>(d, t, g, out, batch, s);
-    case 2048: return ramp_impl<2048, 16, 2>(d, t, g, out, batch, s);
-    case 4096: return ramp_impl<4096, 16, 2>(d, t, g, out, batch, s);
+    case 2048: return ramp_impl<2048, 8, 1>(d, t, g, out, batch, s);
+    case 4096: return ramp_impl<4096, 8, 1>(d, t, g, out, batch, s);
     default: return cudaErrorNotSupported;
   }
 }
@@ -642,8 +649,8 @@ cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, f
   switch (d.nphi) {
     case 512: return rdft_impl<512, 16, 4>(d, t, g, Gh, batch, s);
     case 1024: return rdft_impl<1024, 16, 2>(d, t, g, Gh, batch, s);
-    case 2048: return rdft_impl<2048, 8, 2>(d, t, g, Gh, batch, s);
-    case 4096: return rdft_impl<4096, 8, 2>(d, t, g, Gh, batch, s);
+    case 2048: return rdft_impl<2048, 4, 1>(d, t, g, Gh, batch, s);
+    case 4096: return rdft_impl<4096, 4, 1>(d, t, g, Gh, batch, s);
     default: return cudaErrorNotSupported;
   }
 }
