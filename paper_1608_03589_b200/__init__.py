@@ -24,5 +24,6 @@ from .metrics import max_abs_error, relative_l2
 from .plan import LogPolarPlan, get_plan, naive_backproject
 from .roofline import algorithmic_bytes
 from . import synth
+from .multi import VolumeReconstructor, shard_bounds
 
 __version__ = "0.1.0"

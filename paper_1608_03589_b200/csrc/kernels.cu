@@ -358,7 +358,8 @@ struct FusedShape {
   static constexpr int NQ = NPHI >= 4096 ? 3 : 4;   // quads (4 rows) per band
   static constexpr int G = 2;                        // FFT groups = pairs per quad
   static constexpr int NBOX = (NPHI / 2 + 1 + 255) / 256;
-  static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16;  // FFT buffer / row storage per group
+  // FFT buffer / row storage per group; +8 float2 skews the group's rows by 16 banks
+  static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16 + 8;
   static constexpr int QREG0 = 4 * 256 * NBOX > 2 * HALF ? 4 * 256 * NBOX : 2 * HALF;
   static constexpr int QREG = (QREG0 + 15) / 16 * 16;             // float2, 128-B multiple
   static constexpr int RB = 4 * NQ;
@@ -373,7 +374,9 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
   using FS = FusedShape<NPHI>;
   constexpr int NQ = FS::NQ, G = FS::G, QREG = FS::QREG, HALF = FS::HALF, RB = FS::RB, NBOX = FS::NBOX;
   constexpr int T = FftPlan<NPHI, true>::T;
-  constexpr int RPITCH = NPHI + 16;  // floats from row a to row b inside a group half
+  // floats from row a to row b inside a group half; with HALF the four rows of a
+  // quad start 8 banks apart, so taps on neighbouring rows do not collide
+  constexpr int RPITCH = NPHI + 8;
   static_assert(RPITCH + NPHI <= 2 * HALF, "row storage");
   extern __shared__ __align__(128) float2 smem_k45[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NQ * QREG);

@@ -169,6 +169,8 @@ class LogPolarPlan:
             src_ptr = sino.ctypes.data
             if out is None:
                 out = np.empty((b, self.n_out, self.n_out), dtype=np.float32)
+            if not (out.flags.c_contiguous and out.dtype == np.float32 and out.shape == (b, self.n_out, self.n_out)):
+                raise ValueError("out must be a C-contiguous float32 array of shape (B, n, n)")
             dst_ptr = out.ctypes.data
         if sino.shape[1:] != (self.nt, self.ntheta):
             raise ValueError(f"sinogram batch must have shape (B, {self.nt}, {self.ntheta})")

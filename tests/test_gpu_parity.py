@@ -217,3 +217,14 @@ def test_full_size_executes_and_is_linear(pkg, fbp):
     assert torch.equal(y2[0], y[1])
     assert O.relative_l2(y2[1].cpu().numpy(), 3.0 * y[0].cpu().numpy()) < 1e-6
     assert torch.count_nonzero(plan.execute(torch.zeros_like(x))) == 0
+
+
+def test_volume_reconstructor_shards_match_single_plan(pkg):
+    """Slice-sharded multi-plan execution (here: three plans on one GPU, one host
+    thread each) is bitwise identical to one plan over the whole volume."""
+    vol = np.stack([phantoms.config_sinogram(1, i) for i in range(7)])
+    ref = pkg.get_plan(512, 512, 512, None, None, (0.0, 1.0)).execute(dev(vol)).cpu().numpy()
+    vr = pkg.VolumeReconstructor(512, 512, 512, filter_spec=(0.0, 1.0), devices=[0, 0, 0], chunk=2)
+    out = vr.run(vol)
+    assert np.array_equal(out, ref)
+    assert pkg.shard_bounds(7, 3) == [(0, 2), (2, 4), (4, 7)]
