@@ -123,34 +123,57 @@ __device__ __forceinline__ void static_for(F&& f) {
 }
 
 // Radix-R DFT in registers, natural order in and out (recursive radix-2 DIT,
-// fully unrolled at compile time).  STRIDE/OFF select the subsequence of v.
+// fully unrolled at compile time).  STRIDE/OFF select the subsequence of the
+// length-LEN input.  ZU: inputs at index >= LEN/2 are known zero (leaf butterflies
+// pairing x[j] with x[j+LEN/2] collapse to copies).  LOW: only outputs < R/2 of
+// the top-level transform are needed.
 template <int R, bool INV>
 struct Dft {
-  template <int OFF, int STRIDE, int LEN>
+  template <int OFF, int STRIDE, int LEN, bool ZU, bool LOW>
   __device__ __forceinline__ static void run_sub(const float2 (&in)[LEN], float2 (&out)[R]) {
     if constexpr (R == 1) {
       out[0] = in[OFF];
     } else if constexpr (R == 2) {
-      float2 a = in[OFF], b = in[OFF + STRIDE];
-      out[0] = cadd(a, b);
-      out[1] = csub(a, b);
+      const float2 a = in[OFF];
+      if constexpr (ZU && OFF + STRIDE >= LEN / 2) {
+        out[0] = a;
+        out[1] = a;
+      } else {
+        const float2 b = in[OFF + STRIDE];
+        out[0] = cadd(a, b);
+        if constexpr (!LOW) out[1] = csub(a, b);
+      }
     } else {
       float2 E[R / 2], O[R / 2];
-      Dft<R / 2, INV>::template run_sub<OFF, STRIDE * 2, LEN>(in, E);
-      Dft<R / 2, INV>::template run_sub<OFF + STRIDE, STRIDE * 2, LEN>(in, O);
+      Dft<R / 2, INV>::template run_sub<OFF, STRIDE * 2, LEN, ZU, false>(in, E);
+      Dft<R / 2, INV>::template run_sub<OFF + STRIDE, STRIDE * 2, LEN, ZU, false>(in, O);
       static_for<0, R / 2>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
-        float2 t = twc<k, R, INV>(O[k]);
+        const float2 t = twc<k, R, INV>(O[k]);
         out[k] = cadd(E[k], t);
-        out[k + R / 2] = csub(E[k], t);
+        if constexpr (!LOW) out[k + R / 2] = csub(E[k], t);
       });
     }
   }
   __device__ __forceinline__ static void run(float2 (&v)[R]) {
     float2 out[R];
-    run_sub<0, 1, R>(v, out);
+    run_sub<0, 1, R, false, false>(v, out);
 #pragma unroll
     for (int i = 0; i < R; ++i) v[i] = out[i];
+  }
+  // v[R/2..R-1] are zero on entry
+  __device__ __forceinline__ static void run_zu(float2 (&v)[R]) {
+    float2 out[R];
+    run_sub<0, 1, R, true, false>(v, out);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = out[i];
+  }
+  // only v[0..R/2) are produced
+  __device__ __forceinline__ static void run_low(float2 (&v)[R]) {
+    float2 out[R];
+    run_sub<0, 1, R, false, true>(v, out);
+#pragma unroll
+    for (int i = 0; i < R / 2; ++i) v[i] = out[i];
   }
 };
 
@@ -227,7 +250,7 @@ template <> struct RadixPlan<256>   { static constexpr int P = 2; static constex
 template <> struct RadixPlan<512>   { static constexpr int P = 3; static constexpr int r[3] = {16, 8, 4};  static constexpr int E = 16; };
 template <> struct RadixPlan<1024>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 4}; static constexpr int E = 16; };
 template <> struct RadixPlan<2048>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 8}; static constexpr int E = 16; };
-template <> struct RadixPlan<4096>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 16}; static constexpr int E = 16; };
+template <> struct RadixPlan<4096>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 16}; static constexpr int E = 32; };
 template <> struct RadixPlan<8192>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 32}; static constexpr int E = 32; };
 
 template <int N, bool INV>
@@ -270,7 +293,9 @@ struct TwTable {
 // when load() reads buf).
 // The caller must guarantee buf is free on entry (no thread still reading it).
 // Middle passes go through the padded shared buffer buf (padded_len(N) float2).
-template <int N, bool INV, bool LAST_SYNC, bool FIRST_SYNC = false, typename Load, typename Store, typename Sync>
+// IN_HALF: load(idx) is zero for idx >= N/2 (never called there).
+template <int N, bool INV, bool LAST_SYNC, bool FIRST_SYNC = false, bool IN_HALF = false, typename Load,
+          typename Store, typename Sync>
 __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __restrict__ twt,
                                           Load&& load, Store&& store, Sync&& sync) {
   using FP = FftPlan<N, INV>;
@@ -285,9 +310,15 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
+      if constexpr (IN_HALF) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
-      Dft<R, INV>::run(v[b]);
+        for (int r = 0; r < R / 2; ++r) v[b][r] = load(j + r * (N / R));
+        Dft<R, INV>::run_zu(v[b]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
+        Dft<R, INV>::run(v[b]);
+      }
     }
     if constexpr (FIRST_SYNC) sync();  // load() reads buf itself
 #pragma unroll
@@ -327,7 +358,10 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
 // butterfly->thread map, so the spectrum never touches shared memory: each
 // thread multiplies its own outputs (mul(idx, val) -> val) and runs the first
 // inverse butterfly in registers.
-template <int N, typename Load, typename Mul, typename Store, typename Sync>
+// PRUNE: load(idx) is zero for idx >= N/2 and store() is only needed for idx < N/2
+// (zero-padded linear convolution): first forward pass and last inverse pass
+// skip the known-zero inputs / unneeded outputs.
+template <int N, bool PRUNE = false, typename Load, typename Mul, typename Store, typename Sync>
 __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __restrict__ twt,
                                            Load&& load, Mul&& mul, Store&& store, Sync&& sync) {
   using F = FftPlan<N, false>;
@@ -344,9 +378,15 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
+      if constexpr (PRUNE) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
-      Dft<R, false>::run(v[b]);
+        for (int r = 0; r < R / 2; ++r) v[b][r] = load(j + r * (N / R));
+        Dft<R, false>::run_zu(v[b]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
+        Dft<R, false>::run(v[b]);
+      }
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) pass_store<N, R, 1, F::S>(buf, ti + b * T, v[b]);
@@ -392,13 +432,15 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
       const int j = ti + b * T;
       pass_load<N, R, B::S>(buf, j, v[b]);
       apply_twiddles<R, Ns>(v[b], j, twi + B::tw_off(P - 1));
-      Dft<R, true>::run(v[b]);
+      if constexpr (PRUNE) Dft<R, true>::run_low(v[b]);
+      else Dft<R, true>::run(v[b]);
     }
+    constexpr int RO = PRUNE ? R / 2 : R;  // outputs j + r*Ns, r < RO
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
 #pragma unroll
-      for (int r = 0; r < R; ++r) store(j + r * Ns, v[b][r]);
+      for (int r = 0; r < RO; ++r) store(j + r * Ns, v[b][r]);
     }
   }
 }

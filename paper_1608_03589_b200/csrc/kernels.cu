@@ -76,7 +76,7 @@ k_ramp(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
         tile[idx * TP + 2 * q + 1] = v.y;
       }
     };
-    block_conv<M>(buf, ti, tw, load, mul, store, block_sync);
+    block_conv<M, true>(buf, ti, tw, load, mul, store, block_sync);  // M = 2 nt: half-zero in, low half out
     __syncthreads();
   }
 #pragma unroll 8
@@ -122,7 +122,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
       return idx < NTH ? make_float2(__ldg(ra + idx), __ldg(rb + idx)) : make_float2(0.f, 0.f);
     };
     auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
-    block_fft<NPHI, false, true>(buf, ti, tw, load, store, block_sync);
+    block_fft<NPHI, false, true, false, true>(buf, ti, tw, load, store, block_sync);  // zero-padded rows
     __syncthreads();
     for (int m = ti; m < NH; m += T) {
       const float2 z = buf[pad16(m)];
@@ -148,7 +148,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
 // The row mix is evaluated inside the first forward pass; the multiply by
 // Khat is fused between the last forward and first inverse pass.
 // ---------------------------------------------------------------------------
-template <int L>
+template <int L, bool PRUNE>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, 2)
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int ns, int nrho,
            int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
@@ -208,7 +208,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     auto store = [&](int idx, float2 v) {
       if (idx < nrho) ycol[idx] = v;
     };
-    block_conv<L>(buf, ti, tw, load, mul, store, block_sync);
+    block_conv<L, PRUNE>(buf, ti, tw, load, mul, store, block_sync);
   }
 }
 
@@ -618,7 +618,8 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
 template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
   const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + 2 * (size_t)d.nt) * sizeof(float2);
-  auto k = k_rho_conv<L>;
+  // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
+  auto k = (2 * d.nrho <= L) ? k_rho_conv<L, true> : k_rho_conv<L, false>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
   k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, d.ns, d.nrho, d.nrho_pad, d.nh, t.ab, t.wab,
