@@ -250,7 +250,7 @@ template <> struct RadixPlan<256>   { static constexpr int P = 2; static constex
 template <> struct RadixPlan<512>   { static constexpr int P = 3; static constexpr int r[3] = {16, 8, 4};  static constexpr int E = 16; };
 template <> struct RadixPlan<1024>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 4}; static constexpr int E = 16; };
 template <> struct RadixPlan<2048>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 8}; static constexpr int E = 16; };
-template <> struct RadixPlan<4096>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 16}; static constexpr int E = 32; };
+template <> struct RadixPlan<4096>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 16}; static constexpr int E = 16; };
 template <> struct RadixPlan<8192>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 32}; static constexpr int E = 32; };
 
 template <int N, bool INV>
