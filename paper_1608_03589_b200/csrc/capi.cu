@@ -175,6 +175,7 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   const Dims& d = P->d;
   char* A = ws;
   char* B = ws + align256(P->szA * c);
+  int* counter = reinterpret_cast<int*>(B + align256(P->szB * c));
   const float* src = in;
   cudaError_t e;
   if (P->h.filter && !stop_after_lp) {
@@ -199,13 +200,14 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
     return LPBP_OK;
   }
   e = staged(P, 5, c, s,
-             [&] { return lpbp::launch_irdft_readout(d, P->t, reinterpret_cast<const float2*>(A), out, c, s); });
+             [&] { return lpbp::launch_irdft_readout(d, P->t, reinterpret_cast<const float2*>(A), out, c, counter, s); });
   if (e) return launch_fail(e, "irdft_readout");
   ++g_launches;
   return LPBP_OK;
 }
 
-size_t ws_per_slice(const lpbp_plan* P) { return align256(P->szA) + align256(P->szB); }
+size_t ws_bytes_for(const lpbp_plan* P, int chunk) { return align256(P->szA * chunk) + align256(P->szB * chunk) + 256; }
+size_t ws_per_slice(const lpbp_plan* P) { return ws_bytes_for(P, 1); }
 
 int ensure_own_ws(lpbp_plan* P, size_t bytes) {
   if (P->own_ws_bytes >= bytes) return LPBP_OK;
@@ -226,14 +228,14 @@ int run_batched(const lpbp_plan* Pc, const float* in, float* out, int batch, voi
   if (!ws) {
     lock.lock();
     const int chunk = std::max(1, std::min(batch, 16));
-    int rc = ensure_own_ws(P, align256(P->szA * chunk) + align256(P->szB * chunk));
+    int rc = ensure_own_ws(P, ws_bytes_for(P, chunk));
     if (rc) return rc;
     ws = P->own_ws;
     ws_bytes = P->own_ws_bytes;
   }
   int chunk = 1;
-  while (chunk < batch && align256(P->szA * (chunk + 1)) + align256(P->szB * (chunk + 1)) <= ws_bytes) ++chunk;
-  if (align256(P->szA * chunk) + align256(P->szB * chunk) > ws_bytes)
+  while (chunk < batch && ws_bytes_for(P, chunk + 1) <= ws_bytes) ++chunk;
+  if (ws_bytes_for(P, chunk) > ws_bytes)
     return fail(LPBP_EINVAL, "workspace too small for one slice (need " + std::to_string(ws_per_slice(P)) + " bytes)");
   (void)per;
   const size_t in_slice = (size_t)P->d.nt * P->d.ntheta;
@@ -318,6 +320,8 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   d.row_min = h.row_min;
   d.nbands = h.nbands;
   d.band_rows = h.band_rows;
+  d.nsm = 148;
+  if (P->device >= 0) cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, P->device);
   const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;
   const size_t Y = (size_t)h.nh * h.nrho_pad * sizeof(float2);
   const size_t G = (size_t)h.nh * h.nt * sizeof(float2);
@@ -360,7 +364,7 @@ int lpbp_plan_get_info(const lpbp_plan* P, lpbp_plan_info* info) {
 
 int lpbp_workspace_bytes(const lpbp_plan* P, int32_t chunk, size_t* bytes) {
   if (!P || !bytes || chunk < 1) return fail(LPBP_EINVAL, "invalid argument");
-  *bytes = align256(P->szA * chunk) + align256(P->szB * chunk);
+  *bytes = ws_bytes_for(P, chunk);
   return LPBP_OK;
 }
 
@@ -431,7 +435,7 @@ int lpbp_execute_host(lpbp_plan* P, const float* sino_host, float* img_host, int
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_comp[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_out[i], cudaEventDisableTiming);
     }
-    pp.ws_bytes = align256(P->szA * chunk) + align256(P->szB * chunk);
+    pp.ws_bytes = ws_bytes_for(P, chunk);
     if (e == cudaSuccess) e = cudaMalloc(&pp.ws, pp.ws_bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_in, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_comp, cudaStreamNonBlocking);

@@ -343,136 +343,163 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 }
 
 // ---------------------------------------------------------------------------
-// K45: fused inverse phi-DFT + Cartesian readout.  One CTA per band of RB = 4*NQ
-// consecutive log-polar rows starting at an even row (bands overlap by two rows
-// so every pixel's two taps i0, i0+1 lie in one band).  The band's spectra arrive by TMA: a 3-D tensor map
-// over Y[b][m][rho] with box {4 rows (32 B), 256 m} lands [m][4] in a "quad"
-// region; the CTA's two FFT groups transform the quad's two row pairs in place
-// (each in its half of the region), so the real log-polar rows stay in shared
-// memory for the bilinear readout of the band's pixels (plan-time list of
-// quadrant pixels; each entry writes its four mirror pixels).  The log-polar
-// image never reaches HBM.
+// K45: fused inverse phi-DFT + Cartesian readout, streamed along rho.
+// Persistent CTAs take work units (slice, 16 consecutive quads of 4 log-polar
+// rows) from an atomic counter, outermost (pixel-heavy) units first.  Per quad:
+// a 3-D TMA tensor map over Y[b][m][rho] with box {4 rows (32 B), 256 m} lands
+// the quad's spectra as [m][4] in one of NR ring regions (prefetched NR-1 quads
+// ahead); the two FFT groups inverse-transform the quad's two row pairs in place;
+// the quad's pixels (taps i0, i0+1 with i0 in [r0-1, r0+3)) are sampled from the
+// region plus a carry copy of the previous quad's last row.  The log-polar image
+// never reaches HBM and no row is transformed twice inside a unit.
 // ---------------------------------------------------------------------------
 template <int NPHI>
 struct FusedShape {
-  static constexpr int NQ = NPHI >= 4096 ? 3 : 4;   // quads (4 rows) per band
-  static constexpr int G = 2;                        // FFT groups = pairs per quad
+  static constexpr int G = 2;   // FFT groups = row pairs per quad
+  static constexpr int NR = 3;  // ring regions (quads in flight)
+  static constexpr int UQ = 16; // quads per work unit
   static constexpr int NBOX = (NPHI / 2 + 1 + 255) / 256;
-  // FFT buffer / row storage per group; +8 float2 skews the group's rows by 16 banks
+  // FFT buffer / row storage per group; +8 float2 skews the two groups' rows by 16 banks
   static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16 + 8;
   static constexpr int QREG0 = 4 * 256 * NBOX > 2 * HALF ? 4 * 256 * NBOX : 2 * HALF;
-  static constexpr int QREG = (QREG0 + 15) / 16 * 16;             // float2, 128-B multiple
-  static constexpr int RB = 4 * NQ;
-  static constexpr size_t SMEM = (size_t)NQ * QREG * 8 + 64;       // + mbarriers
+  static constexpr int QREG = (QREG0 + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
+  static constexpr size_t SMEM = ((size_t)NR * QREG + NPHI / 2) * 8 + 128;  // regions + carry row + barriers
 };
 
 template <int NPHI>
 __global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
 k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ img, int nrho, int n, int nq,
-                int row_min, int nbands, const uint32_t* __restrict__ band_off, const uint4* __restrict__ entries,
-                float scale, const float2* __restrict__ tw) {
+                int row_min, int nquads, int batch, int* __restrict__ counter, const uint32_t* __restrict__ quad_off,
+                const uint4* __restrict__ entries, float scale, const float2* __restrict__ tw) {
   using FS = FusedShape<NPHI>;
-  constexpr int NQ = FS::NQ, G = FS::G, QREG = FS::QREG, HALF = FS::HALF, RB = FS::RB, NBOX = FS::NBOX;
+  constexpr int G = FS::G, NR = FS::NR, UQ = FS::UQ, QREG = FS::QREG, HALF = FS::HALF, NBOX = FS::NBOX;
   constexpr int T = FftPlan<NPHI, true>::T;
-  // floats from row a to row b inside a group half; with HALF the four rows of a
-  // quad start 8 banks apart, so taps on neighbouring rows do not collide
-  constexpr int RPITCH = NPHI + 8;
+  constexpr int RPITCH = NPHI + 8;  // floats from row a to row b inside a group half (8-bank skew)
   static_assert(RPITCH + NPHI <= 2 * HALF, "row storage");
-  extern __shared__ __align__(128) float2 smem_k45[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NQ * QREG);
-  const int band = nbands - 1 - (int)blockIdx.x;  // outer (pixel-heavy) bands first
-  const int r0 = row_min + band * (RB - 2);  // even: TMA box rows start 16-B aligned
   constexpr uint32_t QUAD_BYTES = NBOX * 256 * 32;
+  extern __shared__ __align__(128) float2 smem_k45[];
+  float* carry = reinterpret_cast<float*>(smem_k45 + NR * QREG);            // NPHI floats
+  uint64_t* bars = reinterpret_cast<uint64_t*>(carry + NPHI);               // NR
+  int* unit_slot = reinterpret_cast<int*>(bars + NR);
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  const int units_per_slice = (nquads + UQ - 1) / UQ;
+  const int total_units = units_per_slice * batch;
+  const int c = n / 2;
+
   if (threadIdx.x == 0) {
-    for (int k = 0; k < NQ; ++k) mbar_init(&bars[k], 1);
+    for (int r = 0; r < NR; ++r) mbar_init(&bars[r], 1);
     fence_mbar_init();
   }
-  __syncthreads();
-  const uint32_t e0 = __ldg(band_off + band), e1 = __ldg(band_off + band + 1);
-  if (threadIdx.x == 0) {  // all quads in flight at once; quad k completes on bars[k]
-    // warm L2 with this band's pixel entries (read after the transforms)
-    for (uint32_t off = e0 & ~3u; off < e1; off += 4096)
-      prefetch_l2_bulk(entries + off, 16u * (min(e1, off + 4096) - off));
-    for (int k = 0; k < NQ; ++k) {
-      mbar_arrive_expect_tx(&bars[k], QUAD_BYTES);
-      for (int bx = 0; bx < NBOX; ++bx)
-        tma_load_3d(smem_k45 + k * QREG + 4 * (bx * 256), &ymap, 2 * (r0 + 4 * k), bx * 256, (int)blockIdx.y,
-                    &bars[k]);
-    }
-  }
-
-  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
-#pragma unroll 1
-  for (int k = 0; k < NQ; ++k) {
-    mbar_wait(&bars[k], 0);
-    float2* Q = smem_k45 + k * QREG;
-    float2* R = Q + gi * HALF;  // this group's FFT buffer, later its two real rows
-    float* Rf = reinterpret_cast<float*>(R);
-    const int ra = r0 + 4 * k + 2 * gi;
-    const bool va = ra < nrho, vb = ra + 1 < nrho;  // rows past nrho read padding: zero
-    auto load = [&](int idx) -> float2 {
-      const bool hi = idx > NPHI / 2;
-      const int mm = hi ? NPHI - idx : idx;
-      float4 x = *reinterpret_cast<const float4*>(Q + 4 * mm + 2 * gi);  // (Xa, Xb) at mm
-      if (!va) x.x = x.y = 0.f;
-      if (!vb) x.z = x.w = 0.f;
-      float ay = x.y, by = x.w;
-      if (mm == 0 || mm == NPHI / 2) {
-        ay = 0.f;
-        by = 0.f;
-      }
-      if (hi) {
-        ay = -ay;
-        by = -by;
-      }
-      return make_float2(x.x - by, ay + x.z);
-    };
-    auto store = [&](int idx, float2 v) {
-      Rf[idx] = v.x;
-      Rf[RPITCH + idx] = v.y;
-    };
-    block_fft<NPHI, true, true, true>(R, ti, tw, load, store, block_sync);
-  }
-  __syncthreads();
-
-  auto row_ptr = [&](int li) {  // local row li -> quad li/4, group (li/2)%2, row li%2
-    return reinterpret_cast<const float*>(smem_k45 + (li >> 2) * QREG + ((li >> 1) & 1) * HALF) + (li & 1) * RPITCH;
+  uint32_t phase = 0;  // bit r: parity of the next wait on bars[r] (uniform across threads)
+  auto issue = [&](int region, int quad, int slice) {
+    fence_proxy_async_smem();  // order earlier generic accesses to the region before the TMA writes
+    mbar_arrive_expect_tx(&bars[region], QUAD_BYTES);
+    for (int bx = 0; bx < NBOX; ++bx)
+      tma_load_3d(smem_k45 + region * QREG + 4 * (bx * 256), &ymap, 2 * (row_min + 4 * quad), bx * 256, slice,
+                  &bars[region]);
   };
-  const int c = n / 2;
-  float* out = img + (size_t)blockIdx.y * n * n;
-#pragma unroll 2
-  for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const uint4 ent = __ldg(entries + e);
-    const int qq = (int)(ent.x & 0x7FFFFFFFu);
-    const int qy = qq / nq, qx = qq - (qq / nq) * nq;
-    const int iyp = c + qy, iyn = n - 1 - c - qy;
-    const int jxp = c + qx, jxn = n - 1 - c - qx;
-    const bool dupy = iyn == iyp, dupx = jxn == jxp;  // odd n: centre row / column
-    float v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f;
-    if (!(ent.x & 0x80000000u)) {
-      const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
-      const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
-      const float* row0 = row_ptr(i0 - r0);
-      const float* row1 = row_ptr(min(i0 + 1, nrho - 1) - r0);
-      auto sample = [&](int j0, float wj) {
-        if (j0 >= NPHI) j0 -= NPHI;
-        const int j1 = (j0 + 1 == NPHI) ? 0 : j0 + 1;
-        const float a0 = fmaf(wj, row0[j1] - row0[j0], row0[j0]);
-        const float a1 = fmaf(wj, row1[j1] - row1[j0], row1[j0]);
-        return fmaf(wi, a1 - a0, a0) * scale;
+  auto row_ptr = [&](const float2* Q, int li) -> const float* {  // li in [-1, 3]
+    if (li < 0) return carry;
+    return reinterpret_cast<const float*>(Q + ((li >> 1) & 1) * HALF) + (li & 1) * RPITCH;
+  };
+
+  for (;;) {
+    if (threadIdx.x == 0) *unit_slot = atomicAdd(counter, 1);
+    __syncthreads();
+    const int u = *unit_slot;
+    __syncthreads();
+    if (u >= total_units) break;
+    const int slice = u % batch;
+    const int k0 = (units_per_slice - 1 - u / batch) * UQ;  // outermost units first
+    const int k1 = min(k0 + UQ, nquads);
+    const int ks = k0 > 0 ? k0 - 1 : 0;  // previous quad only feeds the carry row
+    if (threadIdx.x == 0)
+      for (int q = ks; q < min(ks + NR, k1); ++q) issue((q - ks) % NR, q, slice);
+    float* out = img + (size_t)slice * n * n;
+
+#pragma unroll 1
+    for (int kk = ks; kk < k1; ++kk) {
+      const int R = (kk - ks) % NR;
+      float2* Q = smem_k45 + R * QREG;
+      const int r0 = row_min + 4 * kk;
+      mbar_wait(&bars[R], (phase >> R) & 1);
+      phase ^= 1u << R;
+      // inverse DFTs of rows (r0 + 2 gi, r0 + 2 gi + 1), in place in this group's half
+      float2* H = Q + gi * HALF;
+      float* Hf = reinterpret_cast<float*>(H);
+      const int ra = r0 + 2 * gi;
+      const bool va = ra < nrho, vb = ra + 1 < nrho;  // rows past nrho read padding: zero
+      auto load = [&](int idx) -> float2 {
+        const bool hi = idx > NPHI / 2;
+        const int mm = hi ? NPHI - idx : idx;
+        float4 x = *reinterpret_cast<const float4*>(Q + 4 * mm + 2 * gi);  // (Xa, Xb) at mm
+        if (!va) x.x = x.y = 0.f;
+        if (!vb) x.z = x.w = 0.f;
+        float ay = x.y, by = x.w;
+        if (mm == 0 || mm == NPHI / 2) {
+          ay = 0.f;
+          by = 0.f;
+        }
+        if (hi) {
+          ay = -ay;
+          by = -by;
+        }
+        return make_float2(x.x - by, ay + x.z);
       };
-      const bool wz = wjr == 0.f;
-      const float wm = wz ? 0.f : 1.f - wjr;
-      v1 = sample(jr, wjr);                                      // x >= 0, y >= 0
-      v2 = sample(wz ? NPHI / 2 - jr : NPHI / 2 - jr - 1, wm);  // x < 0, y >= 0: pi - phi
-      v3 = sample(NPHI / 2 + jr, wjr);                           // x < 0, y < 0: pi + phi
-      v4 = sample(wz ? NPHI - jr : NPHI - jr - 1, wm);          // x >= 0, y < 0: 2 pi - phi
-    }
-    out[(size_t)iyp * n + jxp] = v1;
-    if (!dupx) out[(size_t)iyp * n + jxn] = v2;
-    if (!dupy) {
-      out[(size_t)iyn * n + jxp] = v4;
-      if (!dupx) out[(size_t)iyn * n + jxn] = v3;
+      auto store = [&](int idx, float2 v) {
+        Hf[idx] = v.x;
+        Hf[RPITCH + idx] = v.y;
+      };
+      block_fft<NPHI, true, true, true>(H, ti, tw, load, store, block_sync);
+      __syncthreads();
+
+      if (kk >= k0) {  // readout of this quad's pixels
+        const uint32_t e0 = __ldg(quad_off + kk), e1 = __ldg(quad_off + kk + 1);
+#pragma unroll 2
+        for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+          const uint4 ent = __ldg(entries + e);
+          const int qq = (int)(ent.x & 0x7FFFFFFFu);
+          const int qy = qq / nq, qx = qq - (qq / nq) * nq;
+          const int iyp = c + qy, iyn = n - 1 - c - qy;
+          const int jxp = c + qx, jxn = n - 1 - c - qx;
+          const bool dupy = iyn == iyp, dupx = jxn == jxp;  // odd n: centre row / column
+          float v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f;
+          if (!(ent.x & 0x80000000u)) {
+            const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
+            const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
+            const float* row0 = row_ptr(Q, i0 - r0);
+            const float* row1 = row_ptr(Q, min(i0 + 1, nrho - 1) - r0);
+            auto sample = [&](int j0, float wj) {
+              if (j0 >= NPHI) j0 -= NPHI;
+              const int j1 = (j0 + 1 == NPHI) ? 0 : j0 + 1;
+              const float a0 = fmaf(wj, row0[j1] - row0[j0], row0[j0]);
+              const float a1 = fmaf(wj, row1[j1] - row1[j0], row1[j0]);
+              return fmaf(wi, a1 - a0, a0) * scale;
+            };
+            const bool wz = wjr == 0.f;
+            const float wm = wz ? 0.f : 1.f - wjr;
+            v1 = sample(jr, wjr);                                      // x >= 0, y >= 0
+            v2 = sample(wz ? NPHI / 2 - jr : NPHI / 2 - jr - 1, wm);  // x < 0, y >= 0: pi - phi
+            v3 = sample(NPHI / 2 + jr, wjr);                           // x < 0, y < 0: pi + phi
+            v4 = sample(wz ? NPHI - jr : NPHI - jr - 1, wm);          // x >= 0, y < 0: 2 pi - phi
+          }
+          out[(size_t)iyp * n + jxp] = v1;
+          if (!dupx) out[(size_t)iyp * n + jxn] = v2;
+          if (!dupy) {
+            out[(size_t)iyn * n + jxp] = v4;
+            if (!dupx) out[(size_t)iyn * n + jxn] = v3;
+          }
+        }
+        __syncthreads();
+      }
+      // carry this quad's last row (group 1, row b) for the next quad's readout
+      if (kk + 1 < k1) {
+        const float4* src = reinterpret_cast<const float4*>(row_ptr(Q, 3));
+        float4* dst = reinterpret_cast<float4*>(carry);
+        for (int e = threadIdx.x; e < NPHI / 4; e += blockDim.x) dst[e] = src[e];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0 && kk + NR < k1) issue(R, kk + NR, slice);  // refill the freed region
     }
   }
 }
@@ -722,41 +749,39 @@ cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, 
 }
 }  // namespace
 
-int fused_band_rows(int nphi) {
-  switch (nphi) {
-    case 512: return FusedShape<512>::RB;
-    case 1024: return FusedShape<1024>::RB;
-    case 2048: return FusedShape<2048>::RB;
-    case 4096: return FusedShape<4096>::RB;
-    default: return -1;
-  }
-}
+int fused_band_rows(int nphi) { return (nphi == 512 || nphi == 1024 || nphi == 2048 || nphi == 4096) ? 4 : -1; }
 
 namespace {
 template <int NPHI>
-cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch, cudaStream_t s) {
+cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch, int* counter,
+                       cudaStream_t s) {
   using FS = FusedShape<NPHI>;
-  if (d.band_rows != FS::RB) return cudaErrorInvalidValue;
+  if (d.band_rows != 4) return cudaErrorInvalidValue;
   auto k = k_irdft_readout<NPHI>;
   cudaError_t e = prep(k, FS::SMEM);
   if (e) return e;
   CUtensorMap map;
   e = encode_spectra_map(&map, Yh, d.nrho_pad, NPHI / 2 + 1, batch);
   if (e) return e;
-  k<<<dim3(d.nbands, batch), FS::G * FftPlan<NPHI, true>::T, FS::SMEM, s>>>(
-      map, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, t.band_off, reinterpret_cast<const uint4*>(t.band_entries),
-      d.out_scale, t.tw_phi);
+  e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+  if (e) return e;
+  const int units = (d.nbands + FS::UQ - 1) / FS::UQ * batch;
+  const int grid = units < d.nsm ? units : d.nsm;
+  k<<<grid, FS::G * FftPlan<NPHI, true>::T, FS::SMEM, s>>>(map, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, batch,
+                                                          counter, t.band_off,
+                                                          reinterpret_cast<const uint4*>(t.band_entries),
+                                                          d.out_scale, t.tw_phi);
   return cudaGetLastError();
 }
 }  // namespace
 
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch,
-                                 cudaStream_t s) {
+                                 int* counter, cudaStream_t s) {
   switch (d.nphi) {
-    case 512: return fused_impl<512>(d, t, Yh, img, batch, s);
-    case 1024: return fused_impl<1024>(d, t, Yh, img, batch, s);
-    case 2048: return fused_impl<2048>(d, t, Yh, img, batch, s);
-    case 4096: return fused_impl<4096>(d, t, Yh, img, batch, s);
+    case 512: return fused_impl<512>(d, t, Yh, img, batch, counter, s);
+    case 1024: return fused_impl<1024>(d, t, Yh, img, batch, counter, s);
+    case 2048: return fused_impl<2048>(d, t, Yh, img, batch, counter, s);
+    case 4096: return fused_impl<4096>(d, t, Yh, img, batch, counter, s);
     default: return cudaErrorNotSupported;
   }
 }

@@ -31,7 +31,8 @@ struct DevTables {
 
 struct Dims {
   int nt, ntheta, n, ns, nphi, nh, nrho, nrho_pad, L, M, nq;
-  int row_min, nbands, band_rows;  // fused inverse-DFT + readout bands
+  int row_min, nbands, band_rows;  // fused inverse-DFT + readout quads (band_rows = 4)
+  int nsm;                         // SMs of the plan's device (persistent grids)
   float out_scale;        // 1 (backprojection) or 1/(2 pi) (fbp)
 };
 
@@ -41,8 +42,9 @@ cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float
 cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* G, int batch, cudaStream_t s);
 cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, cudaStream_t s);
 cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch, cudaStream_t s);
+// counter: one device int of workspace (zeroed by the launcher on s)
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Y, float* img, int batch,
-                                 cudaStream_t s);
+                                 int* counter, cudaStream_t s);
 int fused_band_rows(int nphi);
 cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, float* img, int batch, cudaStream_t s);
 cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dtheta, const float* g, float* gT,

@@ -66,16 +66,18 @@ void lerp_tap(double f, int n, int32_t& base, double& w0, double& w1) {
 }  // namespace
 
 void build_bands(HostPlan& h, int band_rows) {
+  // Quads of band_rows (= 4) rows for the streaming fused readout: quad b owns the
+  // pixels with i0 in [r0 - 1, r0 + band_rows - 1), r0 = row_min + band_rows*b, so
+  // its taps are the previous quad's last row (kept in a carry buffer) and its own.
   const size_t nqq = (size_t)h.nq * h.nq;
   int rmin = h.nrho;
   for (size_t e = 0; e < nqq; ++e)
     if (h.qidx[e] != 0xFFFFFFFFu) rmin = std::min(rmin, (int)(h.qidx[e] & 0xFFFFu));
   if (rmin == h.nrho) rmin = 0;
-  rmin &= ~1;                      // even band starts: 16-B aligned TMA boxes of row pairs
-  const int step = band_rows - 2;  // bands overlap by two rows (taps i0, i0+1 stay inside)
+  rmin &= ~1;  // even quad starts: 16-B aligned TMA boxes of row pairs
   h.band_rows = band_rows;
   h.row_min = rmin;
-  h.nbands = std::max(1, (h.nrho - rmin + step - 1) / step);
+  h.nbands = (h.nrho - rmin) / band_rows + 1;
   std::vector<std::vector<uint32_t>> valid(h.nbands), zero(h.nbands);
   size_t nzero = 0;
   for (size_t e = 0; e < nqq; ++e) {
@@ -83,7 +85,7 @@ void build_bands(HostPlan& h, int band_rows) {
     if (q == 0xFFFFFFFFu) {
       zero[nzero++ % h.nbands].push_back((uint32_t)e | 0x80000000u);  // spread zero-writes evenly
     } else {
-      const int b = std::min(h.nbands - 1, ((int)(q & 0xFFFFu) - rmin) / step);
+      const int b = ((int)(q & 0xFFFFu) + 1 - rmin) / band_rows;
       valid[b].push_back((uint32_t)e);
     }
   }

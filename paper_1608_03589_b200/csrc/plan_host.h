@@ -36,9 +36,9 @@ struct HostPlan {
   std::vector<F4> wab;
   std::vector<int32_t> ki;
   std::vector<uint32_t> qidx;
-  // fused inverse-DFT + readout: bands of band_rows log-polar rows starting at
-  // row_min + b*(band_rows-2) (row_min even); band_entries lists quadrant pixels (qy*nq + qx)
-  // whose i0 falls in the band (bit 31 set = write zero), band_off[b..b+1).
+  // fused inverse-DFT + readout: quads of band_rows (4) log-polar rows starting at
+  // r0 = row_min + 4b (row_min even); band_entries lists the quadrant pixels (qy*nq + qx)
+  // with i0 in [r0 - 1, r0 + 3) (bit 31 set = write zero), band_off[b..b+1).
   int band_rows = 0, row_min = 0, nbands = 0;
   std::vector<uint32_t> band_entries, band_off;
   // self-contained 16-byte entries {qq | zero flag, qidx, wi bits, wj bits}
