@@ -358,25 +358,28 @@ struct FusedShape {
   static constexpr int G = 2;   // FFT groups = row pairs per quad
   static constexpr int NR = 3;  // ring regions (quads in flight)
   static constexpr int UQ = 16; // quads per work unit
-  static constexpr int NBOX = (NPHI / 2 + 1 + 255) / 256;
+  // spectra m = 0 .. NPHI/2: NFULL boxes of 256 rows + one 1-row tail box
+  static constexpr int NFULL = (NPHI / 2) / 256;
+  static_assert(NFULL * 256 + 1 == NPHI / 2 + 1, "tail box is one row");
   // FFT buffer / row storage per group; +8 float2 skews the two groups' rows by 16 banks
   static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16 + 8;
-  static constexpr int QREG0 = 4 * 256 * NBOX > 2 * HALF ? 4 * 256 * NBOX : 2 * HALF;
+  static constexpr int QREG0 = 4 * (NPHI / 2 + 1) > 2 * HALF ? 4 * (NPHI / 2 + 1) : 2 * HALF;
   static constexpr int QREG = (QREG0 + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
   static constexpr size_t SMEM = ((size_t)NR * QREG + NPHI / 2) * 8 + 128;  // regions + carry row + barriers
 };
 
 template <int NPHI>
 __global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
-k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ img, int nrho, int n, int nq,
+k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ytail,
+                float* __restrict__ img, int nrho, int n, int nq,
                 int row_min, int nquads, int batch, int* __restrict__ counter, const uint32_t* __restrict__ quad_off,
                 const uint4* __restrict__ entries, float scale, const float2* __restrict__ tw) {
   using FS = FusedShape<NPHI>;
-  constexpr int G = FS::G, NR = FS::NR, UQ = FS::UQ, QREG = FS::QREG, HALF = FS::HALF, NBOX = FS::NBOX;
+  constexpr int G = FS::G, NR = FS::NR, UQ = FS::UQ, QREG = FS::QREG, HALF = FS::HALF, NFULL = FS::NFULL;
   constexpr int T = FftPlan<NPHI, true>::T;
   constexpr int RPITCH = NPHI + 8;  // floats from row a to row b inside a group half (8-bank skew)
   static_assert(RPITCH + NPHI <= 2 * HALF, "row storage");
-  constexpr uint32_t QUAD_BYTES = NBOX * 256 * 32;
+  constexpr uint32_t QUAD_BYTES = (NFULL * 256 + 1) * 32;
   extern __shared__ __align__(128) float2 smem_k45[];
   float* carry = reinterpret_cast<float*>(smem_k45 + NR * QREG);            // NPHI floats
   uint64_t* bars = reinterpret_cast<uint64_t*>(carry + NPHI);               // NR
@@ -394,9 +397,10 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, float* __restrict__ im
   auto issue = [&](int region, int quad, int slice) {
     fence_proxy_async_smem();  // order earlier generic accesses to the region before the TMA writes
     mbar_arrive_expect_tx(&bars[region], QUAD_BYTES);
-    for (int bx = 0; bx < NBOX; ++bx)
-      tma_load_3d(smem_k45 + region * QREG + 4 * (bx * 256), &ymap, 2 * (row_min + 4 * quad), bx * 256, slice,
-                  &bars[region]);
+    const int c0 = 2 * (row_min + 4 * quad);
+    for (int bx = 0; bx < NFULL; ++bx)
+      tma_load_3d(smem_k45 + region * QREG + 4 * (bx * 256), &ymap, c0, bx * 256, slice, &bars[region]);
+    tma_load_3d(smem_k45 + region * QREG + 4 * (NFULL * 256), &ytail, c0, NFULL * 256, slice, &bars[region]);
   };
   auto row_ptr = [&](const float2* Q, int li) -> const float* {  // li in [-1, 3]
     if (li < 0) return carry;
@@ -734,13 +738,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // Spectra Y[b][m][rho] (complex, rho pitch nrho_pad) as floats {2*nrho_pad, nh, batch};
-// box {8 floats = 4 rows, 256 m, 1}.
-cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, int nh, int batch) {
+// box {8 floats = 4 rows, box_m m, 1}.
+cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, int nh, int batch, int box_m) {
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   const cuuint64_t dims[3] = {(cuuint64_t)(2 * nrho_pad), (cuuint64_t)nh, (cuuint64_t)batch};
   const cuuint64_t strides[2] = {(cuuint64_t)nrho_pad * 8, (cuuint64_t)nrho_pad * 8 * nh};
-  const cuuint32_t box[3] = {8, 256, 1};
+  const cuuint32_t box[3] = {8, (cuuint32_t)box_m, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(Y), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -760,14 +764,16 @@ cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
   auto k = k_irdft_readout<NPHI>;
   cudaError_t e = prep(k, FS::SMEM);
   if (e) return e;
-  CUtensorMap map;
-  e = encode_spectra_map(&map, Yh, d.nrho_pad, NPHI / 2 + 1, batch);
+  CUtensorMap map, tail;
+  e = encode_spectra_map(&map, Yh, d.nrho_pad, NPHI / 2 + 1, batch, 256);
+  if (e) return e;
+  e = encode_spectra_map(&tail, Yh, d.nrho_pad, NPHI / 2 + 1, batch, 1);
   if (e) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), s);
   if (e) return e;
   const int units = (d.nbands + FS::UQ - 1) / FS::UQ * batch;
   const int grid = units < d.nsm ? units : d.nsm;
-  k<<<grid, FS::G * FftPlan<NPHI, true>::T, FS::SMEM, s>>>(map, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, batch,
+  k<<<grid, FS::G * FftPlan<NPHI, true>::T, FS::SMEM, s>>>(map, tail, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, batch,
                                                           counter, t.band_off,
                                                           reinterpret_cast<const uint4*>(t.band_entries),
                                                           d.out_scale, t.tw_phi);
