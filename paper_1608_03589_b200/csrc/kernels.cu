@@ -365,7 +365,7 @@ struct FusedShape {
   static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16 + 8;
   static constexpr int QREG0 = 4 * (NPHI / 2 + 1) > 2 * HALF ? 4 * (NPHI / 2 + 1) : 2 * HALF;
   static constexpr int QREG = (QREG0 + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
-  static constexpr size_t SMEM = ((size_t)NR * QREG + NPHI / 2) * 8 + 128;  // regions + carry row + barriers
+  static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 128;  // regions + barriers
 };
 
 template <int NPHI>
@@ -376,13 +376,13 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
                 const uint4* __restrict__ entries, float scale, const float2* __restrict__ tw) {
   using FS = FusedShape<NPHI>;
   constexpr int G = FS::G, NR = FS::NR, UQ = FS::UQ, QREG = FS::QREG, HALF = FS::HALF, NFULL = FS::NFULL;
+  static_assert(NR == 3, "ring = previous (its last row feeds the readout), current, next");
   constexpr int T = FftPlan<NPHI, true>::T;
   constexpr int RPITCH = NPHI + 8;  // floats from row a to row b inside a group half (8-bank skew)
   static_assert(RPITCH + NPHI <= 2 * HALF, "row storage");
   constexpr uint32_t QUAD_BYTES = (NFULL * 256 + 1) * 32;
   extern __shared__ __align__(128) float2 smem_k45[];
-  float* carry = reinterpret_cast<float*>(smem_k45 + NR * QREG);            // NPHI floats
-  uint64_t* bars = reinterpret_cast<uint64_t*>(carry + NPHI);               // NR
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NR * QREG);  // NR
   int* unit_slot = reinterpret_cast<int*>(bars + NR);
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int units_per_slice = (nquads + UQ - 1) / UQ;
@@ -401,9 +401,10 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     for (int bx = 0; bx < NFULL; ++bx)
       tma_load_3d(smem_k45 + region * QREG + 4 * (bx * 256), &ymap, c0, bx * 256, slice, &bars[region]);
     tma_load_3d(smem_k45 + region * QREG + 4 * (NFULL * 256), &ytail, c0, NFULL * 256, slice, &bars[region]);
+    const uint32_t a = __ldg(quad_off + quad), b = __ldg(quad_off + quad + 1);  // warm L2 with its pixels
+    if (b > a) prefetch_l2_bulk(entries + a, 16u * (b - a));
   };
-  auto row_ptr = [&](const float2* Q, int li) -> const float* {  // li in [-1, 3]
-    if (li < 0) return carry;
+  auto row_of = [&](const float2* Q, int li) -> const float* {  // row li in [0, 3] of a quad region
     return reinterpret_cast<const float*>(Q + ((li >> 1) & 1) * HALF) + (li & 1) * RPITCH;
   };
 
@@ -416,16 +417,24 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     const int slice = u % batch;
     const int k0 = (units_per_slice - 1 - u / batch) * UQ;  // outermost units first
     const int k1 = min(k0 + UQ, nquads);
-    const int ks = k0 > 0 ? k0 - 1 : 0;  // previous quad only feeds the carry row
+    const int ks = k0 > 0 ? k0 - 1 : 0;  // the previous quad only feeds its last row
     if (threadIdx.x == 0)
-      for (int q = ks; q < min(ks + NR, k1); ++q) issue((q - ks) % NR, q, slice);
+      for (int q = ks; q < min(ks + 2, k1); ++q) issue((q - ks) % NR, q, slice);
     float* out = img + (size_t)slice * n * n;
 
 #pragma unroll 1
     for (int kk = ks; kk < k1; ++kk) {
       const int R = (kk - ks) % NR;
+      const float2* Qprev = smem_k45 + ((kk - ks + NR - 1) % NR) * QREG;
       float2* Q = smem_k45 + R * QREG;
       const int r0 = row_min + 4 * kk;
+      // first pixel entries of this quad: loads in flight across the transforms
+      const bool rd = kk >= k0;
+      const uint32_t e0 = rd ? __ldg(quad_off + kk) : 0u, e1 = rd ? __ldg(quad_off + kk + 1) : 0u;
+      uint4 pre = make_uint4(0x80000000u, 0, 0, 0);
+      const uint32_t ep = e0 + threadIdx.x;
+      if (ep < e1) pre = __ldg(entries + ep);
+
       mbar_wait(&bars[R], (phase >> R) & 1);
       phase ^= 1u << R;
       // inverse DFTs of rows (r0 + 2 gi, r0 + 2 gi + 1), in place in this group's half
@@ -457,11 +466,8 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       block_fft<NPHI, true, true, true>(H, ti, tw, load, store, block_sync);
       __syncthreads();
 
-      if (kk >= k0) {  // readout of this quad's pixels
-        const uint32_t e0 = __ldg(quad_off + kk), e1 = __ldg(quad_off + kk + 1);
-#pragma unroll 2
-        for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-          const uint4 ent = __ldg(entries + e);
+      if (rd) {  // readout: taps from this quad's rows and the previous quad's last row
+        auto pixel = [&](const uint4& ent) {
           const int qq = (int)(ent.x & 0x7FFFFFFFu);
           const int qy = qq / nq, qx = qq - (qq / nq) * nq;
           const int iyp = c + qy, iyn = n - 1 - c - qy;
@@ -471,8 +477,9 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
           if (!(ent.x & 0x80000000u)) {
             const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
             const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
-            const float* row0 = row_ptr(Q, i0 - r0);
-            const float* row1 = row_ptr(Q, min(i0 + 1, nrho - 1) - r0);
+            const int l0 = i0 - r0, l1 = min(i0 + 1, nrho - 1) - r0;
+            const float* row0 = l0 < 0 ? row_of(Qprev, 3) : row_of(Q, l0);
+            const float* row1 = row_of(Q, l1);
             auto sample = [&](int j0, float wj) {
               if (j0 >= NPHI) j0 -= NPHI;
               const int j1 = (j0 + 1 == NPHI) ? 0 : j0 + 1;
@@ -493,17 +500,13 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
             out[(size_t)iyn * n + jxp] = v4;
             if (!dupx) out[(size_t)iyn * n + jxn] = v3;
           }
-        }
-        __syncthreads();
+        };
+        if (ep < e1) pixel(pre);
+#pragma unroll 2
+        for (uint32_t e = ep + blockDim.x; e < e1; e += blockDim.x) pixel(__ldg(entries + e));
       }
-      // carry this quad's last row (group 1, row b) for the next quad's readout
-      if (kk + 1 < k1) {
-        const float4* src = reinterpret_cast<const float4*>(row_ptr(Q, 3));
-        float4* dst = reinterpret_cast<float4*>(carry);
-        for (int e = threadIdx.x; e < NPHI / 4; e += blockDim.x) dst[e] = src[e];
-        __syncthreads();
-      }
-      if (threadIdx.x == 0 && kk + NR < k1) issue(R, kk + NR, slice);  // refill the freed region
+      __syncthreads();  // region of kk-1 is free now: refill it with quad kk+2
+      if (threadIdx.x == 0 && kk + 2 < k1) issue((kk + 2 - ks) % NR, kk + 2, slice);
     }
   }
 }
