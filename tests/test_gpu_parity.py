@@ -228,3 +228,33 @@ def test_volume_reconstructor_shards_match_single_plan(pkg):
     out = vr.run(vol)
     assert np.array_equal(out, ref)
     assert pkg.shard_bounds(7, 3) == [(0, 2), (2, 4), (4, 7)]
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 64, 129])
+def test_small_and_odd_outputs(pkg, golden, n):
+    z = golden("cfg0.npz")
+    g = pkg.Sinogram(256, 256, z["sino"].astype(np.float64))
+    ref = O.logpolar_backproject(z["sino"].astype(np.float64), n)
+    assert report(f"bp n={n}", pkg.logpolar_backproject(g, n).values, ref) <= RTOL
+
+
+def test_thin_annulus_and_all_fovea(pkg, golden):
+    """Explicit rho0 close to 0: only pixels with ln r >= rho0 are non-zero (exact predicate)."""
+    z = golden("cfg0.npz")
+    gd = z["sino"].astype(np.float64)
+    g = pkg.Sinogram(256, 256, gd)
+    o = pkg.LogPolarOptions(rho0=-0.1, nrho=40)
+    ref = O.logpolar_backproject(gd, 256, rho0=-0.1, nrho=40)
+    got = pkg.logpolar_backproject(g, 256, o).values
+    assert np.array_equal(got == 0, ref == 0)
+    assert report("thin annulus", got, ref) <= RTOL
+
+
+def test_empty_batch_and_stage_api_full_size(pkg):
+    plan = pkg.get_plan(2048, 2048, 2048, None, None, None)
+    out = plan.execute(torch.empty((0, 2048, 2048), device="cuda"))
+    assert out.shape == (0, 2048, 2048)
+    s = phantoms.config_sinogram(2, 7)
+    lp = plan.logpolar(dev(s)[None])[0].cpu().numpy()
+    ref = O.logpolar_stage(s.astype(np.float64), 2048)
+    assert report("cfg2 logpolar stage", lp, ref) <= RTOL
