@@ -371,9 +371,10 @@ int lpbp_workspace_bytes(const lpbp_plan* P, int32_t chunk, size_t* bytes) {
 int lpbp_execute(const lpbp_plan* P, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
                  size_t ws_bytes, void* stream) {
   g_launches = 0;
-  if (!P || !sino_dev || !img_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
   if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
   if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !img_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
   return run_batched(P, sino_dev, img_dev, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream), false);
 }
@@ -381,19 +382,21 @@ int lpbp_execute(const lpbp_plan* P, const float* sino_dev, float* img_dev, int3
 int lpbp_logpolar(const lpbp_plan* P, const float* sino_dev, float* lp_dev, int32_t batch, void* ws,
                   size_t ws_bytes, void* stream) {
   g_launches = 0;
-  if (!P || !sino_dev || !lp_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
   if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
   if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !lp_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
   return run_batched(P, sino_dev, lp_dev, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream), true);
 }
 
 int lpbp_filter(const lpbp_plan* P, const float* sino_dev, float* out_dev, int32_t batch, void* stream) {
   g_launches = 0;
-  if (!P || !sino_dev || !out_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
   if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
   if (!P->h.filter) return fail(LPBP_EINVAL, "plan was created without a filter (filter = 0)");
   if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !out_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
   cudaError_t e = lpbp::launch_ramp(P->d, P->t, sino_dev, out_dev, batch, static_cast<cudaStream_t>(stream));
   if (e) return launch_fail(e, "ramp_filter");
@@ -403,9 +406,10 @@ int lpbp_filter(const lpbp_plan* P, const float* sino_dev, float* out_dev, int32
 
 int lpbp_readout(const lpbp_plan* P, const float* lp_dev, float* img_dev, int32_t batch, void* stream) {
   g_launches = 0;
-  if (!P || !lp_dev || !img_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
   if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
   if (batch == 0) return LPBP_OK;
+  if (!lp_dev || !img_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
   cudaError_t e = lpbp::launch_readout(P->d, P->t, lp_dev, img_dev, batch, static_cast<cudaStream_t>(stream));
   if (e) return launch_fail(e, "readout");
@@ -415,9 +419,10 @@ int lpbp_readout(const lpbp_plan* P, const float* lp_dev, float* img_dev, int32_
 
 int lpbp_execute_host(lpbp_plan* P, const float* sino_host, float* img_host, int32_t batch, int32_t chunk) {
   g_launches = 0;
-  if (!P || !sino_host || !img_host || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
   if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
   if (batch == 0) return LPBP_OK;
+  if (!sino_host || !img_host) return fail(LPBP_EINVAL, "invalid argument");
   if (chunk <= 0) chunk = 4;
   chunk = std::min(chunk, batch);
   DeviceGuard g(P->device);
@@ -480,10 +485,11 @@ int lpbp_execute_host(lpbp_plan* P, const float* sino_host, float* img_host, int
 int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, int32_t ntheta, int32_t n,
                            int32_t batch, float* ws_dev, void* stream) {
   g_launches = 0;
-  if (!sino_dev || !img_dev || !ws_dev || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (batch < 0) return fail(LPBP_EINVAL, "invalid argument");
   if (n < 2) return fail(LPBP_EINVAL, "n must be >= 2");
   if (nt < 2 || ntheta < 1) return fail(LPBP_EINVAL, "nt must be >= 2 and ntheta >= 1");
   if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !img_dev || !ws_dev) return fail(LPBP_EINVAL, "invalid argument");
   // angle table (reference.py:30-36): cos/sin(k*pi/ntheta) * nt/(2n)
   std::vector<lpbp::F2> cs(ntheta);
   const double dtheta = 3.14159265358979323846 / ntheta;
