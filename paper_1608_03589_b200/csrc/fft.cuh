@@ -189,6 +189,25 @@ __device__ __forceinline__ void apply_twiddles(float2 (&v)[R], int k, const floa
   }
 }
 
+// Same twiddles generated on the SFU: exact integer phase e = r*k mod (Ns*R),
+// folded into (-pi, pi], then MUFU sin/cos (abs error ~4e-7).  Trades the
+// twiddle-table loads (L2 latency) for the otherwise idle SFU pipe.
+template <int R, int Ns, bool INV>
+__device__ __forceinline__ void apply_twiddles_sfu(float2 (&v)[R], int k) {
+  if constexpr (Ns > 1) {
+    constexpr int M = Ns * R;
+    constexpr float kStep = (INV ? 6.283185307179586f : -6.283185307179586f) / (float)M;
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      int e = (r * k) & (M - 1);
+      e = e > M / 2 ? e - M : e;
+      float sn, cs;
+      __sincosf(kStep * (float)e, &sn, &cs);
+      v[r] = cmul(v[r], make_float2(cs, sn));
+    }
+  }
+}
+
 // Load the R inputs of butterfly j of a pass from (padded) shared memory.
 // Padded addressing: when the stride between a butterfly's elements is a
 // multiple of 2^S, pad(base + r*stride) = pad(base) + r*(stride + stride/2^S),
@@ -361,7 +380,8 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
 // PRUNE: load(idx) is zero for idx >= N/2 and store() is only needed for idx < N/2
 // (zero-padded linear convolution): first forward pass and last inverse pass
 // skip the known-zero inputs / unneeded outputs.
-template <int N, bool PRUNE = false, typename Load, typename Mul, typename Store, typename Sync>
+// SFU_TW: passes with Ns >= 64 take their twiddles from the SFU instead of the table.
+template <int N, bool PRUNE = false, bool SFU_TW = false, typename Load, typename Mul, typename Store, typename Sync>
 __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __restrict__ twt,
                                            Load&& load, Mul&& mul, Store&& store, Sync&& sync) {
   using F = FftPlan<N, false>;
@@ -406,7 +426,8 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       pass_load<N, R, F::S>(buf, j, v[b]);
-      apply_twiddles<R, Ns>(v[b], j, twf + F::tw_off(P - 1));
+      if constexpr (SFU_TW && Ns >= 64) apply_twiddles_sfu<R, Ns, false>(v[b], j);
+      else apply_twiddles<R, Ns>(v[b], j, twf + F::tw_off(P - 1));
       Dft<R, false>::run(v[b]);
 #pragma unroll
       for (int r = 0; r < R; ++r) v[b][r] = mul(j + r * Ns, v[b][r]);
@@ -431,7 +452,8 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       pass_load<N, R, B::S>(buf, j, v[b]);
-      apply_twiddles<R, Ns>(v[b], j, twi + B::tw_off(P - 1));
+      if constexpr (SFU_TW && Ns >= 64) apply_twiddles_sfu<R, Ns, true>(v[b], j);
+      else apply_twiddles<R, Ns>(v[b], j, twi + B::tw_off(P - 1));
       if constexpr (PRUNE) Dft<R, true>::run_low(v[b]);
       else Dft<R, true>::run(v[b]);
     }

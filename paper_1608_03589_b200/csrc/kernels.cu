@@ -208,7 +208,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     auto store = [&](int idx, float2 v) {
       if (idx < nrho) ycol[idx] = v;
     };
-    block_conv<L, PRUNE>(buf, ti, tw, load, mul, store, block_sync);
+    block_conv<L, PRUNE, true>(buf, ti, tw, load, mul, store, block_sync);
   }
 }
 
