@@ -189,9 +189,6 @@ __device__ __forceinline__ void apply_twiddles(float2 (&v)[R], int k, const floa
   }
 }
 
-// Passes with Ns >= kSfuMinNs use SFU twiddles when a driver asks for them.
-constexpr int kSfuMinNs = 16;
-
 // Same twiddles generated on the SFU: exact integer phase e = r*k mod (Ns*R),
 // folded into (-pi, pi], then MUFU sin/cos (abs error ~4e-7).  Trades the
 // twiddle-table loads (L2 latency) for the otherwise idle SFU pipe.
@@ -248,7 +245,8 @@ __device__ __forceinline__ void pass_store(float2* buf, int j, const float2 (&v)
 // One full smem->smem Stockham pass for a group of T threads (ti in [0,T)).
 // Caller provides the barrier that separates the previous pass's stores from
 // these loads; this function places the barrier between loads and stores.
-template <int N, int R, int Ns, int T, bool INV, int S, bool SFU = false, typename Sync>
+// SFU_MIN: passes with Ns >= SFU_MIN take SFU twiddles (0 = always the table).
+template <int N, int R, int Ns, int T, bool INV, int S, int SFU_MIN = 0, typename Sync>
 __device__ __forceinline__ void pass_smem(float2* buf, int ti, const float2* __restrict__ tw, Sync&& sync) {
   constexpr int NB = (N / R) / T;  // butterflies per thread
   static_assert(NB >= 1 && NB * T * R == N, "bad pass shape");
@@ -257,7 +255,7 @@ __device__ __forceinline__ void pass_smem(float2* buf, int ti, const float2* __r
   for (int b = 0; b < NB; ++b) {
     const int j = ti + b * T;
     pass_load<N, R, S>(buf, j, v[b]);
-    if constexpr (SFU && Ns >= kSfuMinNs) apply_twiddles_sfu<R, Ns, INV>(v[b], j % Ns);
+    if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu<R, Ns, INV>(v[b], j % Ns);
     else apply_twiddles<R, Ns>(v[b], j % Ns, tw);
     Dft<R, INV>::run(v[b]);
   }
@@ -317,7 +315,7 @@ struct TwTable {
 // The caller must guarantee buf is free on entry (no thread still reading it).
 // Middle passes go through the padded shared buffer buf (padded_len(N) float2).
 // IN_HALF: load(idx) is zero for idx >= N/2 (never called there).
-template <int N, bool INV, bool LAST_SYNC, bool FIRST_SYNC = false, bool IN_HALF = false, bool SFU_TW = false,
+template <int N, bool INV, bool LAST_SYNC, bool FIRST_SYNC = false, bool IN_HALF = false, int SFU_MIN = 0,
           typename Load, typename Store, typename Sync>
 __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __restrict__ twt,
                                           Load&& load, Store&& store, Sync&& sync) {
@@ -350,7 +348,7 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
   sync();
   static_for<1, P - 1>([&](auto ic) {
     constexpr int I = decltype(ic)::value;
-    pass_smem<N, FP::radix(I), FP::ns(I), T, INV, S, SFU_TW>(buf, ti, tw + FP::tw_off(I), sync);
+    pass_smem<N, FP::radix(I), FP::ns(I), T, INV, S, SFU_MIN>(buf, ti, tw + FP::tw_off(I), sync);
     sync();
   });
   {  // last pass: outputs at j + r*Ns (Ns = N/R, j < Ns)
@@ -363,7 +361,7 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       pass_load<N, R, S>(buf, j, v[b]);
-      if constexpr (SFU_TW && Ns >= kSfuMinNs) apply_twiddles_sfu<R, Ns, INV>(v[b], j);
+      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu<R, Ns, INV>(v[b], j);
       else apply_twiddles<R, Ns>(v[b], j, tw + FP::tw_off(P - 1));
       Dft<R, INV>::run(v[b]);
     }
@@ -385,8 +383,8 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
 // PRUNE: load(idx) is zero for idx >= N/2 and store() is only needed for idx < N/2
 // (zero-padded linear convolution): first forward pass and last inverse pass
 // skip the known-zero inputs / unneeded outputs.
-// SFU_TW: passes with Ns >= 64 take their twiddles from the SFU instead of the table.
-template <int N, bool PRUNE = false, bool SFU_TW = false, typename Load, typename Mul, typename Store, typename Sync>
+// SFU_MIN: passes with Ns >= SFU_MIN take their twiddles from the SFU instead of the table (0 = never).
+template <int N, bool PRUNE = false, int SFU_MIN = 0, typename Load, typename Mul, typename Store, typename Sync>
 __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __restrict__ twt,
                                            Load&& load, Mul&& mul, Store&& store, Sync&& sync) {
   using F = FftPlan<N, false>;
@@ -419,7 +417,7 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
   sync();
   static_for<1, P - 1>([&](auto ic) {
     constexpr int I = decltype(ic)::value;
-    pass_smem<N, F::radix(I), F::ns(I), T, false, F::S, SFU_TW>(buf, ti, twf + F::tw_off(I), sync);
+    pass_smem<N, F::radix(I), F::ns(I), T, false, F::S, SFU_MIN>(buf, ti, twf + F::tw_off(I), sync);
     sync();
   });
   {  // forward last pass -> pointwise multiply -> inverse pass 0, all in registers
@@ -431,7 +429,7 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       pass_load<N, R, F::S>(buf, j, v[b]);
-      if constexpr (SFU_TW && Ns >= kSfuMinNs) apply_twiddles_sfu<R, Ns, false>(v[b], j);
+      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu<R, Ns, false>(v[b], j);
       else apply_twiddles<R, Ns>(v[b], j, twf + F::tw_off(P - 1));
       Dft<R, false>::run(v[b]);
 #pragma unroll
@@ -445,7 +443,7 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
   sync();
   static_for<1, P - 1>([&](auto ic) {
     constexpr int I = decltype(ic)::value;
-    pass_smem<N, B::radix(I), B::ns(I), T, true, B::S, SFU_TW>(buf, ti, twi + B::tw_off(I), sync);
+    pass_smem<N, B::radix(I), B::ns(I), T, true, B::S, SFU_MIN>(buf, ti, twi + B::tw_off(I), sync);
     sync();
   });
   {  // inverse last pass
@@ -457,7 +455,7 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       pass_load<N, R, B::S>(buf, j, v[b]);
-      if constexpr (SFU_TW && Ns >= kSfuMinNs) apply_twiddles_sfu<R, Ns, true>(v[b], j);
+      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu<R, Ns, true>(v[b], j);
       else apply_twiddles<R, Ns>(v[b], j, twi + B::tw_off(P - 1));
       if constexpr (PRUNE) Dft<R, true>::run_low(v[b]);
       else Dft<R, true>::run(v[b]);

@@ -76,7 +76,7 @@ k_ramp(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
         tile[idx * TP + 2 * q + 1] = v.y;
       }
     };
-    block_conv<M, true, true>(buf, ti, tw, load, mul, store, block_sync);  // M = 2 nt: half-zero in, low half out
+    block_conv<M, true, 16>(buf, ti, tw, load, mul, store, block_sync);  // M = 2 nt: half-zero in, low half out
     __syncthreads();
   }
 #pragma unroll 8
@@ -122,7 +122,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
       return idx < NTH ? make_float2(__ldg(ra + idx), __ldg(rb + idx)) : make_float2(0.f, 0.f);
     };
     auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
-    block_fft<NPHI, false, true, false, true, true>(buf, ti, tw, load, store, block_sync);  // zero-padded rows
+    block_fft<NPHI, false, true, false, true, 16>(buf, ti, tw, load, store, block_sync);  // zero-padded rows
     __syncthreads();
     for (int m = ti; m < NH; m += T) {
       const float2 z = buf[pad16(m)];
@@ -208,7 +208,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     auto store = [&](int idx, float2 v) {
       if (idx < nrho) ycol[idx] = v;
     };
-    block_conv<L, PRUNE, true>(buf, ti, tw, load, mul, store, block_sync);
+    block_conv<L, PRUNE, 64>(buf, ti, tw, load, mul, store, block_sync);  // SFU only for the two large passes
   }
 }
 
@@ -463,7 +463,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
         Hf[idx] = v.x;
         Hf[RPITCH + idx] = v.y;
       };
-      block_fft<NPHI, true, true, true, false, true>(H, ti, tw, load, store, block_sync);
+      block_fft<NPHI, true, true, true, false, 16>(H, ti, tw, load, store, block_sync);
       __syncthreads();
 
       if (rd) {  // readout: taps from this quad's rows and the previous quad's last row
