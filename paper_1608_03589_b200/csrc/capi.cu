@@ -188,7 +188,8 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   if (e) return launch_fail(e, "row_rdft");
   ++g_launches;
   e = staged(P, 2, c, s, [&] {
-    return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c, s);
+    return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c,
+                                 stop_after_lp ? 0 : d.row_min, s);
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;

@@ -150,7 +150,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const f
 // ---------------------------------------------------------------------------
 template <int L, bool PRUNE>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, 2)
-k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int ns, int nrho,
+k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int ns, int nrho, int row_lo,
            int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
            const int* __restrict__ ki, const float2* __restrict__ wi, const float2* __restrict__ khat,
            const float2* __restrict__ tw) {
@@ -205,8 +205,8 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     };
     auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(kcol + idx)); };
     float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
-    auto store = [&](int idx, float2 v) {
-      if (idx < nrho) ycol[idx] = v;
+    auto store = [&](int idx, float2 v) {  // rows below row_lo are never read downstream
+      if (idx < nrho && idx >= row_lo) ycol[idx] = v;
     };
     block_conv<L, PRUNE, 64>(buf, ti, tw, load, mul, store, block_sync);  // SFU only for the two large passes
   }
@@ -650,13 +650,14 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
 }
 
 template <int L>
-cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
+cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
+                      cudaStream_t s) {
   const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + 2 * (size_t)d.nt) * sizeof(float2);
   // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
   auto k = (2 * d.nrho <= L) ? k_rho_conv<L, true> : k_rho_conv<L, false>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
-  k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, d.ns, d.nrho, d.nrho_pad, d.nh, t.ab, t.wab,
+  k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.ab, t.wab,
                                               t.ki, t.wi, t.khat, t.tw_rho);
   return cudaGetLastError();
 }
@@ -692,13 +693,14 @@ cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, f
     default: return cudaErrorNotSupported;
   }
 }
-cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, cudaStream_t s) {
+cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
+                            cudaStream_t s) {
   switch (d.L) {
-    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, s);
-    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, s);
-    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, s);
-    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, s);
-    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, s);
+    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, row_lo, s);
+    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, row_lo, s);
+    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, row_lo, s);
+    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, row_lo, s);
+    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, row_lo, s);
     default: return cudaErrorNotSupported;
   }
 }

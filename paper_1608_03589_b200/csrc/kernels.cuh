@@ -40,7 +40,9 @@ struct Dims {
 // cudaErrorNotSupported when no instantiation exists for the size.
 cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s);
 cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* G, int batch, cudaStream_t s);
-cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, cudaStream_t s);
+// rows < row_lo of Y are not written (0 = all rows)
+cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, int row_lo,
+                            cudaStream_t s);
 cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch, cudaStream_t s);
 // counter: one device int of workspace (zeroed by the launcher on s)
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Y, float* img, int batch,

@@ -79,15 +79,20 @@ void build_bands(HostPlan& h, int band_rows) {
   h.row_min = rmin;
   h.nbands = (h.nrho - rmin) / band_rows + 1;
   std::vector<std::vector<uint32_t>> valid(h.nbands), zero(h.nbands);
-  size_t nzero = 0;
+  std::vector<uint32_t> zeros;  // raster order
   for (size_t e = 0; e < nqq; ++e) {
     const uint32_t q = h.qidx[e];
     if (q == 0xFFFFFFFFu) {
-      zero[nzero++ % h.nbands].push_back((uint32_t)e | 0x80000000u);  // spread zero-writes evenly
+      zeros.push_back((uint32_t)e | 0x80000000u);
     } else {
       const int b = ((int)(q & 0xFFFFu) + 1 - rmin) / band_rows;
       valid[b].push_back((uint32_t)e);
     }
+  }
+  // zero-writes: contiguous raster chunks per quad, so they fill whole sectors
+  for (int b = 0; b < h.nbands; ++b) {
+    const size_t lo = zeros.size() * b / h.nbands, hi = zeros.size() * (b + 1) / h.nbands;
+    zero[b].assign(zeros.begin() + lo, zeros.begin() + hi);
   }
   h.band_entries.clear();
   h.band_off.assign(h.nbands + 1, 0);
