@@ -74,7 +74,7 @@ void build_bands(HostPlan& h, int band_rows) {
   for (size_t e = 0; e < nqq; ++e)
     if (h.qidx[e] != 0xFFFFFFFFu) rmin = std::min(rmin, (int)(h.qidx[e] & 0xFFFFu));
   if (rmin == h.nrho) rmin = 0;
-  rmin &= ~1;  // even quad starts: 16-B aligned TMA boxes of row pairs
+  rmin &= ~3;  // quad starts at multiples of 4 rows: 32-B TMA box rows are whole sectors
   h.band_rows = band_rows;
   h.row_min = rmin;
   h.nbands = (h.nrho - rmin) / band_rows + 1;
