@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--slices", type=int, default=0, help="slices per rank per step (0 = config default)")
     ap.add_argument("--chunk", type=int, default=32, help="slices per internal pipeline chunk")
-    ap.add_argument("--e2e-slices", type=int, default=64)
+    ap.add_argument("--e2e-slices", type=int, default=128)
+    ap.add_argument("--e2e-chunk", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = min(cores, memory/2.5GB, 32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -315,11 +316,11 @@ def run_ours(a, d: Dist):
     host_in = torch.empty((E, nt, nth), dtype=torch.float32, pin_memory=True)
     host_in.copy_(sino[:E])
     host_out = torch.empty((E, n, n), dtype=torch.float32, pin_memory=True)
-    plan.execute_host(host_in, host_out, chunk=8)
+    plan.execute_host(host_in, host_out, chunk=a.e2e_chunk)
     d.barrier()
     t = time.perf_counter()
     for _ in range(a.e2e_steps):
-        plan.execute_host(host_in, host_out, chunk=8)
+        plan.execute_host(host_in, host_out, chunk=a.e2e_chunk)
     e2e_s = d.max(time.perf_counter() - t)
     e2e_value = d.sum(E * a.e2e_steps) / e2e_s
 
