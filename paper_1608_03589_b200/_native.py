@@ -59,6 +59,7 @@ SIGNATURES = {
     "lpbp_filter": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "lpbp_logpolar": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
     "lpbp_readout": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
+    "lpbp_naive_workspace_bytes": (c_int32, [c_int32, c_int32, c_int32, POINTER(c_size_t)]),
     "lpbp_naive_backproject": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "lpbp_plan_table": (c_int32, [c_void_p, c_char_p, c_void_p, c_size_t, POINTER(c_size_t)]),
     "lpbp_profile_enable": (c_int32, [c_void_p, c_int32]),

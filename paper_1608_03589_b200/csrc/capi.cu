@@ -483,6 +483,12 @@ int lpbp_execute_host(lpbp_plan* P, const float* sino_host, float* img_host, int
   return LPBP_OK;
 }
 
+int lpbp_naive_workspace_bytes(int32_t nt, int32_t ntheta, int32_t batch, size_t* bytes) {
+  if (!bytes || nt < 2 || ntheta < 1 || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  *bytes = lpbp::naive_workspace_floats(nt, ntheta, batch) * sizeof(float);
+  return LPBP_OK;
+}
+
 int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, int32_t ntheta, int32_t n,
                            int32_t batch, float* ws_dev, void* stream) {
   g_launches = 0;

@@ -517,9 +517,13 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
 // The sinogram is transposed to angle-major first so a warp's 32 pixels read
 // one or two sectors per angle.
 // ---------------------------------------------------------------------------
-__global__ void k_transpose(const float* __restrict__ g, float* __restrict__ gT, int nt, int ntheta) {
+// gT[k][PAD + t] = g[t][k]; the PAD zeros on each side make every tap of a pixel
+// inside [-1,1]^2 addressable without bounds checks (|t| <= sqrt 2).
+__global__ void k_transpose(const float* __restrict__ g, float* __restrict__ gT, int nt, int ntheta, int ntp,
+                            int pad) {
   __shared__ float tile[32][33];
   const size_t slice = (size_t)blockIdx.z * nt * ntheta;
+  const size_t tslice = (size_t)blockIdx.z * ntheta * ntp;
   const int th0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int t = t0 + r, th = th0 + threadIdx.x;
@@ -528,34 +532,45 @@ __global__ void k_transpose(const float* __restrict__ g, float* __restrict__ gT,
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int th = th0 + r, t = t0 + threadIdx.x;
-    if (t < nt && th < ntheta) gT[slice + (size_t)th * nt + t] = tile[threadIdx.x][r];
+    if (t < nt && th < ntheta) gT[tslice + (size_t)th * ntp + pad + t] = tile[threadIdx.x][r];
   }
 }
 
+// 4 pixels per thread (rows iy, iy+8, iy+16, iy+24 of a 32x32 tile) share each
+// angle's table entry; f = a*C + b*S + nt/2 + PAD is positive, so truncation is floor.
 __global__ void __launch_bounds__(256)
-k_naive(const float* __restrict__ gT, float* __restrict__ img, int nt, int ntheta, int n,
+k_naive(const float* __restrict__ gT, float* __restrict__ img, int nt, int ntheta, int n, int ntp, int pad,
         const float2* __restrict__ cs, float dtheta) {
   const int jx = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int iy = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (jx >= n || iy >= n) return;
+  const int iy0 = blockIdx.y * 32 + (threadIdx.x >> 5);
   const float a = (float)(2 * jx + 1 - n);
-  const float b = (float)(2 * iy + 1 - n);
-  const float half = 0.5f * (float)nt;
-  const float* src = gT + (size_t)blockIdx.z * nt * ntheta;
-  float acc = 0.f;
-#pragma unroll 4
+  float b[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) b[u] = (float)(2 * (iy0 + 8 * u) + 1 - n);
+  const float off = 0.5f * (float)nt + (float)pad;
+  const float* src = gT + (size_t)blockIdx.z * ntheta * ntp;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
   for (int k = 0; k < ntheta; ++k) {
     const float2 c = __ldg(cs + k);
-    const float f = fmaf(a, c.x, b * c.y) + half;
-    const float fl = floorf(f);
-    const float w = f - fl;
-    const int i0 = (int)fl;
-    const float* row = src + (size_t)k * nt;
-    const float v0 = (i0 >= 0 && i0 < nt) ? __ldg(row + i0) : 0.f;
-    const float v1 = (i0 + 1 >= 0 && i0 + 1 < nt) ? __ldg(row + i0 + 1) : 0.f;
-    acc += fmaf(w, v1 - v0, v0);
+    const float base = fmaf(a, c.x, off);
+    const float* row = src + (size_t)k * ntp;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float f = fmaf(b[u], c.y, base);
+      const int i0 = (int)f;
+      const float w = f - (float)i0;
+      const float v0 = __ldg(row + i0), v1 = __ldg(row + i0 + 1);
+      acc[u] += fmaf(w, v1 - v0, v0);
+    }
   }
-  img[(size_t)blockIdx.z * n * n + (size_t)iy * n + jx] = acc * dtheta;
+  if (jx < n) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int iy = iy0 + 8 * u;
+      if (iy < n) img[(size_t)blockIdx.z * n * n + (size_t)iy * n + jx] = acc[u] * dtheta;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -719,12 +734,20 @@ cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, f
                                                             d.out_scale);
   return cudaGetLastError();
 }
+int naive_pad(int nt) { return nt / 4 + 8; }  // >= (sqrt 2 - 1) nt/2 + 2
+size_t naive_workspace_floats(int nt, int ntheta, int batch) {
+  return (size_t)batch * ntheta * (nt + 2 * naive_pad(nt));
+}
+
 cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dtheta, const float* g, float* gT,
                          float* img, int batch, cudaStream_t s) {
-  k_transpose<<<dim3((ntheta + 31) / 32, (nt + 31) / 32, batch), dim3(32, 8), 0, s>>>(g, gT, nt, ntheta);
-  cudaError_t e = cudaGetLastError();
+  const int pad = naive_pad(nt), ntp = nt + 2 * pad;
+  cudaError_t e = cudaMemsetAsync(gT, 0, naive_workspace_floats(nt, ntheta, batch) * sizeof(float), s);
   if (e) return e;
-  k_naive<<<dim3((n + 31) / 32, (n + 7) / 8, batch), 256, 0, s>>>(gT, img, nt, ntheta, n, cs, dtheta);
+  k_transpose<<<dim3((ntheta + 31) / 32, (nt + 31) / 32, batch), dim3(32, 8), 0, s>>>(g, gT, nt, ntheta, ntp, pad);
+  e = cudaGetLastError();
+  if (e) return e;
+  k_naive<<<dim3((n + 31) / 32, (n + 31) / 32, batch), 256, 0, s>>>(gT, img, nt, ntheta, n, ntp, pad, cs, dtheta);
   return cudaGetLastError();
 }
 

@@ -215,7 +215,9 @@ def naive_backproject(sino: torch.Tensor, n: int) -> torch.Tensor:
     sino = _as_f32_contig(sino, 3, "sinogram batch")
     b, nt, ntheta = sino.shape
     out = torch.empty((b, n, n), dtype=torch.float32, device=sino.device)
-    ws = torch.empty_like(sino)
+    nbytes = c_size_t()
+    check(lib().lpbp_naive_workspace_bytes(nt, ntheta, b, byref(nbytes)))
+    ws = torch.empty(max(1, nbytes.value // 4), dtype=torch.float32, device=sino.device)
     with torch.cuda.device(sino.device):
         check(lib().lpbp_naive_backproject(c_void_p(sino.data_ptr()), c_void_p(out.data_ptr()), nt, ntheta, int(n), b,
                                            c_void_p(ws.data_ptr()), _stream(sino.device)))
