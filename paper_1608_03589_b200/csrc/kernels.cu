@@ -101,42 +101,85 @@ __device__ __forceinline__ int stg_col(int m, int c) {
   return c ^ ((m / (16 / TR)) & (TR - 1));
 }
 
-template <int NPHI, int TR, int G>
-__global__ void __launch_bounds__(G * FftPlan<NPHI, false>::T, (G == 1 ? 2 : 1))
-k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, const float2* __restrict__ tw) {
-  constexpr int T = FftPlan<NPHI, false>::T;
-  constexpr int NTH = NPHI / 2;
-  constexpr int NH = NPHI / 2 + 1;
-  extern __shared__ __align__(16) float2 smem_k2[];
-  float2* stg = smem_k2;  // [NH][TR], swizzled columns
-  float2* buf = smem_k2 + ((NH * TR + 15) & ~15) + (threadIdx.x / T) * padded_len(NPHI);
-  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
-  const int t0 = blockIdx.x * TR;
-  const float* src = g + (size_t)blockIdx.y * nt * NTH;
+// Persistent: each CTA walks tiles (slice, 4 consecutive rows); a tile's rows are
+// contiguous (4 x NTH floats) and arrive by one TMA bulk copy into a double
+// buffer, two tiles ahead of use.  Group g (of 2) transforms row pair g.
+template <int NPHI>
+struct RdftShape {
+  static constexpr int TR = 4, G = 2;
+  static constexpr int NTH = NPHI / 2, NH = NPHI / 2 + 1;
+  static constexpr int IN = TR * NTH / 2;                    // float2 per input tile
+  static constexpr int STG = ((NH * TR) + 15) & ~15;         // float2 staging
+  static constexpr int BUF = (padded_len(NPHI) + 15) & ~15;  // float2 per FFT buffer
+  static constexpr size_t SMEM = ((size_t)2 * IN + STG + G * BUF) * 8 + 64;
+};
 
-  for (int round = 0; round < TR / 2 / G; ++round) {
-    const int q = round * G + gi;
-    const float* ra = src + (size_t)(t0 + 2 * q) * NTH;
+template <int NPHI>
+__global__ void __launch_bounds__(RdftShape<NPHI>::G * FftPlan<NPHI, false>::T, 1)
+k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int ntiles_per_slice, int ntiles,
+           const float2* __restrict__ tw) {
+  using RS = RdftShape<NPHI>;
+  constexpr int T = FftPlan<NPHI, false>::T;
+  constexpr int TR = RS::TR, NTH = RS::NTH, NH = RS::NH;
+  extern __shared__ __align__(128) float2 smem_k2[];
+  float* in0 = reinterpret_cast<float*>(smem_k2);               // 2 x TR*NTH floats
+  float2* stg = smem_k2 + 2 * RS::IN;                            // [NH][TR], swizzled columns
+  float2* buf = stg + RS::STG + (threadIdx.x / T) * RS::BUF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + RS::STG + RS::G * RS::BUF);
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  constexpr uint32_t TILE_BYTES = TR * NTH * 4;
+  auto tile_src = [&](int tile) {
+    const int b = tile / ntiles_per_slice, t0 = (tile - b * ntiles_per_slice) * TR;
+    return g + ((size_t)b * nt + t0) * NTH;
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int first = blockIdx.x, stride = gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      const int tile = first + k * stride;
+      if (tile < ntiles) {
+        mbar_arrive_expect_tx(&bars[k], TILE_BYTES);
+        tma_bulk_g2s(in0 + k * TR * NTH, tile_src(tile), TILE_BYTES, &bars[k]);
+      }
+    }
+  }
+  int it = 0;
+#pragma unroll 1
+  for (int tile = first; tile < ntiles; tile += stride, ++it) {
+    const int sl = it & 1;
+    mbar_wait(&bars[sl], (it >> 1) & 1);
+    const float* ra = in0 + sl * TR * NTH + (2 * gi) * NTH;
     const float* rb = ra + NTH;
-    auto load = [&](int idx) -> float2 {
-      return idx < NTH ? make_float2(__ldg(ra + idx), __ldg(rb + idx)) : make_float2(0.f, 0.f);
-    };
+    auto load = [&](int idx) -> float2 { return make_float2(ra[idx], rb[idx]); };  // idx < NTH (IN_HALF)
     auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
-    block_fft<NPHI, false, true, false, true, 16>(buf, ti, tw, load, store, block_sync);  // zero-padded rows
+    block_fft<NPHI, false, true, false, true, 16>(buf, ti, tw, load, store, block_sync);
+    // every thread is past pass 0: the input slot is free for the tile two ahead
+    if (threadIdx.x == 0 && tile + 2 * stride < ntiles) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bars[sl], TILE_BYTES);
+      tma_bulk_g2s(in0 + sl * TR * NTH, tile_src(tile + 2 * stride), TILE_BYTES, &bars[sl]);
+    }
     __syncthreads();
     for (int m = ti; m < NH; m += T) {
       const float2 z = buf[pad16(m)];
       const float2 w = buf[pad16((NPHI - m) & (NPHI - 1))];
-      stg[m * TR + stg_col<TR>(m, 2 * q)] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
-      stg[m * TR + stg_col<TR>(m, 2 * q + 1)] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+      stg[m * TR + stg_col<TR>(m, 2 * gi)] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
+      stg[m * TR + stg_col<TR>(m, 2 * gi + 1)] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
     }
     __syncthreads();
-  }
-  float2* dst = Gh + (size_t)blockIdx.y * NH * nt + t0;
+    const int b = tile / ntiles_per_slice, t0 = (tile - b * ntiles_per_slice) * TR;
+    float2* dst = Gh + (size_t)b * NH * nt + t0;
 #pragma unroll 8
-  for (int e = threadIdx.x; e < NH * TR; e += blockDim.x) {
-    const int m = e / TR, c = e % TR;
-    dst[(size_t)m * nt + c] = stg[m * TR + stg_col<TR>(m, c)];
+    for (int e = threadIdx.x; e < NH * TR; e += blockDim.x) {
+      const int m = e / TR, c = e % TR;
+      dst[(size_t)m * nt + c] = stg[m * TR + stg_col<TR>(m, c)];
+    }
+    // next tile's separation rewrites stg only after its FFT's barriers
   }
 }
 
@@ -653,14 +696,19 @@ cudaError_t ramp_impl(const Dims& d, const DevTables& t, const float* g, float* 
   return cudaGetLastError();
 }
 
-template <int NPHI, int TR, int G>
+template <int NPHI>
 cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch, cudaStream_t s) {
-  if (d.nt % TR) return cudaErrorNotSupported;
-  const size_t smem = ((size_t)(((NPHI / 2 + 1) * TR + 15) & ~15) + (size_t)G * padded_len(NPHI)) * sizeof(float2);
-  auto k = k_row_rdft<NPHI, TR, G>;
-  cudaError_t e = prep(k, smem);
+  using RS = RdftShape<NPHI>;
+  if (d.nt % RS::TR) return cudaErrorNotSupported;
+  auto k = k_row_rdft<NPHI>;
+  cudaError_t e = prep(k, RS::SMEM);
   if (e) return e;
-  k<<<dim3(d.nt / TR, batch), G * FftPlan<NPHI, false>::T, smem, s>>>(g, Gh, d.nt, t.tw_phi);
+  const int per = d.nt / RS::TR, tiles = per * batch;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, RS::G * FftPlan<NPHI, false>::T, RS::SMEM);
+  const int slots = d.nsm * (occ > 0 ? occ : 1);
+  const int grid = tiles < slots ? tiles : slots;
+  k<<<grid, RS::G * FftPlan<NPHI, false>::T, RS::SMEM, s>>>(g, Gh, d.nt, per, tiles, t.tw_phi);
   return cudaGetLastError();
 }
 
@@ -701,10 +749,10 @@ cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float
 }
 cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch, cudaStream_t s) {
   switch (d.nphi) {
-    case 512: return rdft_impl<512, 16, 4>(d, t, g, Gh, batch, s);
-    case 1024: return rdft_impl<1024, 16, 2>(d, t, g, Gh, batch, s);
-    case 2048: return rdft_impl<2048, 4, 1>(d, t, g, Gh, batch, s);
-    case 4096: return rdft_impl<4096, 4, 1>(d, t, g, Gh, batch, s);
+    case 512: return rdft_impl<512>(d, t, g, Gh, batch, s);
+    case 1024: return rdft_impl<1024>(d, t, g, Gh, batch, s);
+    case 2048: return rdft_impl<2048>(d, t, g, Gh, batch, s);
+    case 4096: return rdft_impl<4096>(d, t, g, Gh, batch, s);
     default: return cudaErrorNotSupported;
   }
 }
