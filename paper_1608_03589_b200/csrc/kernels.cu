@@ -398,37 +398,39 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 // ---------------------------------------------------------------------------
 template <int NPHI>
 struct FusedShape {
-  static constexpr int G = 2;   // FFT groups = row pairs per quad
-  static constexpr int NR = 3;  // ring regions (quads in flight)
-  static constexpr int UQ = 16; // quads per work unit
+  static constexpr int S = 2;       // log-polar rows per step (one packed pair per FFT group)
+  static constexpr int G = S / 2;   // FFT groups
+  static constexpr int NR = 3;      // ring regions (previous, current, next step)
+  static constexpr int UQ = 32;     // steps per work unit
   // spectra m = 0 .. NPHI/2: NFULL boxes of 256 rows + one 1-row tail box
   static constexpr int NFULL = (NPHI / 2) / 256;
   static_assert(NFULL * 256 + 1 == NPHI / 2 + 1, "tail box is one row");
-  // FFT buffer / row storage per group; +8 float2 skews the two groups' rows by 16 banks
+  // FFT buffer / row storage per group; +8 float2 skews the groups' rows by 16 banks
   static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16 + 8;
-  static constexpr int QREG0 = 4 * (NPHI / 2 + 1) > 2 * HALF ? 4 * (NPHI / 2 + 1) : 2 * HALF;
+  static constexpr int QREG0 = S * (NPHI / 2 + 1) > G * HALF ? S * (NPHI / 2 + 1) : G * HALF;
   static constexpr int QREG = (QREG0 + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
   static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 128;  // regions + barriers
 };
 
 template <int NPHI>
-__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
+__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 2)
 k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ytail,
                 float* __restrict__ img, int nrho, int n, int nq,
-                int row_min, int nquads, int batch, int* __restrict__ counter, const uint32_t* __restrict__ quad_off,
+                int row_min, int nsteps, int batch, int* __restrict__ counter, const uint32_t* __restrict__ step_off,
                 const uint4* __restrict__ entries, float scale, const float2* __restrict__ tw) {
   using FS = FusedShape<NPHI>;
-  constexpr int G = FS::G, NR = FS::NR, UQ = FS::UQ, QREG = FS::QREG, HALF = FS::HALF, NFULL = FS::NFULL;
+  constexpr int S = FS::S, G = FS::G, NR = FS::NR, UQ = FS::UQ, QREG = FS::QREG, HALF = FS::HALF;
+  constexpr int NFULL = FS::NFULL;
   static_assert(NR == 3, "ring = previous (its last row feeds the readout), current, next");
   constexpr int T = FftPlan<NPHI, true>::T;
   constexpr int RPITCH = NPHI + 8;  // floats from row a to row b inside a group half (8-bank skew)
   static_assert(RPITCH + NPHI <= 2 * HALF, "row storage");
-  constexpr uint32_t QUAD_BYTES = (NFULL * 256 + 1) * 32;
+  constexpr uint32_t STEP_BYTES = (NFULL * 256 + 1) * S * 8;
   extern __shared__ __align__(128) float2 smem_k45[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NR * QREG);  // NR
   int* unit_slot = reinterpret_cast<int*>(bars + NR);
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
-  const int units_per_slice = (nquads + UQ - 1) / UQ;
+  const int units_per_slice = (nsteps + UQ - 1) / UQ;
   const int total_units = units_per_slice * batch;
   const int c = n / 2;
 
@@ -437,18 +439,18 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     fence_mbar_init();
   }
   uint32_t phase = 0;  // bit r: parity of the next wait on bars[r] (uniform across threads)
-  auto issue = [&](int region, int quad, int slice) {
+  auto issue = [&](int region, int step, int slice) {
     fence_proxy_async_smem();  // order earlier generic accesses to the region before the TMA writes
-    mbar_arrive_expect_tx(&bars[region], QUAD_BYTES);
-    const int c0 = 2 * (row_min + 4 * quad);
+    mbar_arrive_expect_tx(&bars[region], STEP_BYTES);
+    const int c0 = 2 * (row_min + S * step);
     for (int bx = 0; bx < NFULL; ++bx)
-      tma_load_3d(smem_k45 + region * QREG + 4 * (bx * 256), &ymap, c0, bx * 256, slice, &bars[region]);
-    tma_load_3d(smem_k45 + region * QREG + 4 * (NFULL * 256), &ytail, c0, NFULL * 256, slice, &bars[region]);
-    const uint32_t a = __ldg(quad_off + quad), b = __ldg(quad_off + quad + 1);  // warm L2 with its pixels
+      tma_load_3d(smem_k45 + region * QREG + S * (bx * 256), &ymap, c0, bx * 256, slice, &bars[region]);
+    tma_load_3d(smem_k45 + region * QREG + S * (NFULL * 256), &ytail, c0, NFULL * 256, slice, &bars[region]);
+    const uint32_t a = __ldg(step_off + step), b = __ldg(step_off + step + 1);  // warm L2 with its pixels
     if (b > a) prefetch_l2_bulk(entries + a, 16u * (b - a));
   };
-  auto row_of = [&](const float2* Q, int li) -> const float* {  // row li in [0, 3] of a quad region
-    return reinterpret_cast<const float*>(Q + ((li >> 1) & 1) * HALF) + (li & 1) * RPITCH;
+  auto row_of = [&](const float2* Q, int li) -> const float* {  // row li in [0, S) of a step region
+    return reinterpret_cast<const float*>(Q + (li >> 1) * HALF) + (li & 1) * RPITCH;
   };
 
   for (;;) {
@@ -459,8 +461,8 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     if (u >= total_units) break;
     const int slice = u % batch;
     const int k0 = (units_per_slice - 1 - u / batch) * UQ;  // outermost units first
-    const int k1 = min(k0 + UQ, nquads);
-    const int ks = k0 > 0 ? k0 - 1 : 0;  // the previous quad only feeds its last row
+    const int k1 = min(k0 + UQ, nsteps);
+    const int ks = k0 > 0 ? k0 - 1 : 0;  // the previous step only feeds its last row
     if (threadIdx.x == 0)
       for (int q = ks; q < min(ks + 2, k1); ++q) issue((q - ks) % NR, q, slice);
     float* out = img + (size_t)slice * n * n;
@@ -470,17 +472,17 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       const int R = (kk - ks) % NR;
       const float2* Qprev = smem_k45 + ((kk - ks + NR - 1) % NR) * QREG;
       float2* Q = smem_k45 + R * QREG;
-      const int r0 = row_min + 4 * kk;
-      // first pixel entries of this quad: loads in flight across the transforms
+      const int r0 = row_min + S * kk;
+      // first pixel entries of this step: loads in flight across the transforms
       const bool rd = kk >= k0;
-      const uint32_t e0 = rd ? __ldg(quad_off + kk) : 0u, e1 = rd ? __ldg(quad_off + kk + 1) : 0u;
+      const uint32_t e0 = rd ? __ldg(step_off + kk) : 0u, e1 = rd ? __ldg(step_off + kk + 1) : 0u;
       uint4 pre = make_uint4(0x80000000u, 0, 0, 0);
       const uint32_t ep = e0 + threadIdx.x;
       if (ep < e1) pre = __ldg(entries + ep);
 
       mbar_wait(&bars[R], (phase >> R) & 1);
       phase ^= 1u << R;
-      // inverse DFTs of rows (r0 + 2 gi, r0 + 2 gi + 1), in place in this group's half
+      // inverse DFTs of rows (r0 + 2 gi, r0 + 2 gi + 1), in place in this group's part
       float2* H = Q + gi * HALF;
       float* Hf = reinterpret_cast<float*>(H);
       const int ra = r0 + 2 * gi;
@@ -488,7 +490,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       auto load = [&](int idx) -> float2 {
         const bool hi = idx > NPHI / 2;
         const int mm = hi ? NPHI - idx : idx;
-        float4 x = *reinterpret_cast<const float4*>(Q + 4 * mm + 2 * gi);  // (Xa, Xb) at mm
+        float4 x = *reinterpret_cast<const float4*>(Q + S * mm + 2 * gi);  // (Xa, Xb) at mm
         if (!va) x.x = x.y = 0.f;
         if (!vb) x.z = x.w = 0.f;
         float ay = x.y, by = x.w;
@@ -509,7 +511,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       block_fft<NPHI, true, true, true, false, 16>(H, ti, tw, load, store, block_sync);
       __syncthreads();
 
-      if (rd) {  // readout: taps from this quad's rows and the previous quad's last row
+      if (rd) {  // readout: taps from this step's rows and the previous step's last row
         auto pixel = [&](const uint4& ent) {
           const int qq = (int)(ent.x & 0x7FFFFFFFu);
           const int qy = qq / nq, qx = qq - (qq / nq) * nq;
@@ -521,7 +523,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
             const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
             const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
             const int l0 = i0 - r0, l1 = min(i0 + 1, nrho - 1) - r0;
-            const float* row0 = l0 < 0 ? row_of(Qprev, 3) : row_of(Q, l0);
+            const float* row0 = l0 < 0 ? row_of(Qprev, S - 1) : row_of(Q, l0);
             const float* row1 = row_of(Q, l1);
             auto sample = [&](int j0, float wj) {
               if (j0 >= NPHI) j0 -= NPHI;
@@ -548,7 +550,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
 #pragma unroll 2
         for (uint32_t e = ep + blockDim.x; e < e1; e += blockDim.x) pixel(__ldg(entries + e));
       }
-      __syncthreads();  // region of kk-1 is free now: refill it with quad kk+2
+      __syncthreads();  // region of kk-1 is free now: refill it with step kk+2
       if (threadIdx.x == 0 && kk + 2 < k1) issue((kk + 2 - ks) % NR, kk + 2, slice);
     }
   }
@@ -814,13 +816,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // Spectra Y[b][m][rho] (complex, rho pitch nrho_pad) as floats {2*nrho_pad, nh, batch};
-// box {8 floats = 4 rows, box_m m, 1}.
-cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, int nh, int batch, int box_m) {
+// box {2*rows floats, box_m m, 1}.
+cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, int nh, int batch, int rows,
+                               int box_m) {
   auto enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   const cuuint64_t dims[3] = {(cuuint64_t)(2 * nrho_pad), (cuuint64_t)nh, (cuuint64_t)batch};
   const cuuint64_t strides[2] = {(cuuint64_t)nrho_pad * 8, (cuuint64_t)nrho_pad * 8 * nh};
-  const cuuint32_t box[3] = {8, (cuuint32_t)box_m, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * rows), (cuuint32_t)box_m, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(Y), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -829,26 +832,37 @@ cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, 
 }
 }  // namespace
 
-int fused_band_rows(int nphi) { return (nphi == 512 || nphi == 1024 || nphi == 2048 || nphi == 4096) ? 4 : -1; }
+int fused_band_rows(int nphi) {
+  switch (nphi) {
+    case 512: return FusedShape<512>::S;
+    case 1024: return FusedShape<1024>::S;
+    case 2048: return FusedShape<2048>::S;
+    case 4096: return FusedShape<4096>::S;
+    default: return -1;
+  }
+}
 
 namespace {
 template <int NPHI>
 cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch, int* counter,
                        cudaStream_t s) {
   using FS = FusedShape<NPHI>;
-  if (d.band_rows != 4) return cudaErrorInvalidValue;
+  if (d.band_rows != FS::S) return cudaErrorInvalidValue;
   auto k = k_irdft_readout<NPHI>;
   cudaError_t e = prep(k, FS::SMEM);
   if (e) return e;
   CUtensorMap map, tail;
-  e = encode_spectra_map(&map, Yh, d.nrho_pad, NPHI / 2 + 1, batch, 256);
+  e = encode_spectra_map(&map, Yh, d.nrho_pad, NPHI / 2 + 1, batch, FS::S, 256);
   if (e) return e;
-  e = encode_spectra_map(&tail, Yh, d.nrho_pad, NPHI / 2 + 1, batch, 1);
+  e = encode_spectra_map(&tail, Yh, d.nrho_pad, NPHI / 2 + 1, batch, FS::S, 1);
   if (e) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), s);
   if (e) return e;
   const int units = (d.nbands + FS::UQ - 1) / FS::UQ * batch;
-  const int grid = units < d.nsm ? units : d.nsm;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, FS::G * FftPlan<NPHI, true>::T, FS::SMEM);
+  const int slots = d.nsm * (occ > 0 ? occ : 1);
+  const int grid = units < slots ? units : slots;
   k<<<grid, FS::G * FftPlan<NPHI, true>::T, FS::SMEM, s>>>(map, tail, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, batch,
                                                           counter, t.band_off,
                                                           reinterpret_cast<const uint4*>(t.band_entries),

@@ -66,15 +66,15 @@ void lerp_tap(double f, int n, int32_t& base, double& w0, double& w1) {
 }  // namespace
 
 void build_bands(HostPlan& h, int band_rows) {
-  // Quads of band_rows (= 4) rows for the streaming fused readout: quad b owns the
-  // pixels with i0 in [r0 - 1, r0 + band_rows - 1), r0 = row_min + band_rows*b, so
-  // its taps are the previous quad's last row (kept in a carry buffer) and its own.
+  // Steps of band_rows (2 or 4) rows for the streaming fused readout: step b owns
+  // the pixels with i0 in [r0 - 1, r0 + band_rows - 1), r0 = row_min + band_rows*b,
+  // so its taps are the previous step's last row (still resident) and its own.
   const size_t nqq = (size_t)h.nq * h.nq;
   int rmin = h.nrho;
   for (size_t e = 0; e < nqq; ++e)
     if (h.qidx[e] != 0xFFFFFFFFu) rmin = std::min(rmin, (int)(h.qidx[e] & 0xFFFFu));
   if (rmin == h.nrho) rmin = 0;
-  rmin &= ~3;  // quad starts at multiples of 4 rows: 32-B TMA box rows are whole sectors
+  rmin &= ~3;  // steps start at multiples of 4 rows: TMA box rows start 16/32-B aligned
   h.band_rows = band_rows;
   h.row_min = rmin;
   h.nbands = (h.nrho - rmin) / band_rows + 1;
