@@ -398,10 +398,10 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 // ---------------------------------------------------------------------------
 template <int NPHI>
 struct FusedShape {
-  static constexpr int S = 2;       // log-polar rows per step (one packed pair per FFT group)
+  static constexpr int S = 4;       // log-polar rows per step (one packed pair per FFT group); 2 measured slower
   static constexpr int G = S / 2;   // FFT groups
   static constexpr int NR = 3;      // ring regions (previous, current, next step)
-  static constexpr int UQ = 32;     // steps per work unit
+  static constexpr int UQ = 16;     // steps per work unit
   // spectra m = 0 .. NPHI/2: NFULL boxes of 256 rows + one 1-row tail box
   static constexpr int NFULL = (NPHI / 2) / 256;
   static_assert(NFULL * 256 + 1 == NPHI / 2 + 1, "tail box is one row");
@@ -413,7 +413,7 @@ struct FusedShape {
 };
 
 template <int NPHI>
-__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 2)
+__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
 k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ytail,
                 float* __restrict__ img, int nrho, int n, int nq,
                 int row_min, int nsteps, int batch, int* __restrict__ counter, const uint32_t* __restrict__ step_off,

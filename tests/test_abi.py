@@ -206,7 +206,7 @@ def test_fused_readout_bands_cover_every_pixel_once(nt, nth, n, rho0):
         z = (e & 0x80000000) != 0
         qy, qx = q // nq, q % nq
         r0 = i.row_min + b * i.band_rows
-        assert r0 % 2 == 0
+        assert r0 % 4 == 0
         qi = qidx[q[~z]]
         assert np.all(qi[qi != 0xFFFFFFFF] != 0xFFFFFFFF)
         i0 = (qi & 0xFFFF).astype(np.int64)
