@@ -27,6 +27,13 @@ namespace lpbp {
 
 namespace {
 __device__ __forceinline__ void block_sync() { __syncthreads(); }
+// named barrier for one FFT group of `count` threads (ids 1.. ; 0 is __syncthreads)
+struct GroupSync {
+  int id, count;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  }
+};
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -157,14 +164,14 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int nti
     const float* rb = ra + NTH;
     auto load = [&](int idx) -> float2 { return make_float2(ra[idx], rb[idx]); };  // idx < NTH (IN_HALF)
     auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
-    block_fft<NPHI, false, true, false, true, 16>(buf, ti, tw, load, store, block_sync);
+    block_fft<NPHI, false, true, false, true, 16>(buf, ti, tw, load, store, GroupSync{1 + gi, T});
+    __syncthreads();
     // every thread is past pass 0: the input slot is free for the tile two ahead
     if (threadIdx.x == 0 && tile + 2 * stride < ntiles) {
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&bars[sl], TILE_BYTES);
       tma_bulk_g2s(in0 + sl * TR * NTH, tile_src(tile + 2 * stride), TILE_BYTES, &bars[sl]);
     }
-    __syncthreads();
     for (int m = ti; m < NH; m += T) {
       const float2 z = buf[pad16(m)];
       const float2 w = buf[pad16((NPHI - m) & (NPHI - 1))];
@@ -508,7 +515,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
         Hf[idx] = v.x;
         Hf[RPITCH + idx] = v.y;
       };
-      block_fft<NPHI, true, true, true, false, 16>(H, ti, tw, load, store, block_sync);
+      block_fft<NPHI, true, true, true, false, 16>(H, ti, tw, load, store, GroupSync{1 + gi, T});
       __syncthreads();
 
       if (rd) {  // readout: taps from this step's rows and the previous step's last row
