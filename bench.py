@@ -32,6 +32,14 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "backprojected 2048^2 slices/sec at 1/2/4/8 B200; HBM GB/s vs peak"
+try:
+    MEASURED = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+except (OSError, ValueError):
+    MEASURED = {}
+# dram__bytes_read.sum + dram__bytes_write.sum per slice from the committed ncu --set full
+# capture (profiles/r01b_summary.md, 32-slice launches at 2048^2 FBP)
+TRAFFIC_PER_SLICE = {"rho_conv": (1.212429e9 + 1.996124e9) / 32, "irdft_readout": (3.04e9 + 0.815e9) / 32,
+                     "ramp_filter": (0.536934e9 + 0.496182e9) / 32, "row_rdft": (0.536892e9 + 1.023551e9) / 32}
 UNIT = "slices/s"
 
 
@@ -308,6 +316,11 @@ def run_ours(a, d: Dist):
     peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
     achieved = bytes_per_launch / (per_launch_ms / 1000.0) / 1e9
+    flops = p.roofline.nominal_flops(plan)
+    fp_ach = flops.get(dom, 0.0) * slices_per_launch / (per_launch_ms / 1000.0) / 1e12
+    fp_peak = p.roofline.fp32_peak_tflops(float(MEASURED.get("sm_max_mhz", 1965.0)))
+    traffic = TRAFFIC_PER_SLICE.get(dom)
+    traffic = traffic * slices_per_launch if traffic else None
     pipe_bytes = sum(ab[k]["per_slice"] for k in ab if k in stages) + sum(
         ab[k]["per_launch"] * stages[k]["launches"] for k in stages) / max(1, S * a.steps)
 
@@ -343,9 +356,12 @@ def run_ours(a, d: Dist):
                        "l2": "no flush: 34 GB input per step >> 126 MB L2",
                        "nrho": info["nrho"], "L": info["L"], "nphi": info["nphi"]},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": per_launch_ms,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                         "fp32_pipe": {"achieved_tflops": fp_ach, "peak_tflops": fp_peak, "frac": fp_ach / fp_peak,
+                                       "note": "nominal FFT flops (5 N log2 N) of the kernel / launch time vs "
+                                               "148 SMs x 128 lanes x 2 x clock; FFT stages are FP32-pipe bound"}},
             "pipeline": {"stage_ms_per_slice": {k: v["ms"] / max(1, v["slices"]) for k, v in stages.items()},
                          "algorithmic_bytes_per_slice": pipe_bytes,
                          "hbm_equiv_gbs": pipe_bytes * value / d.world / 1e9,

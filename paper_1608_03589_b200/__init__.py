@@ -23,6 +23,7 @@ from .reference import backproject_naive, backproject_naive_batch
 from .metrics import max_abs_error, relative_l2
 from .plan import LogPolarPlan, get_plan, naive_backproject
 from .roofline import algorithmic_bytes
+from . import roofline
 from . import synth
 from .multi import VolumeReconstructor, shard_bounds
 

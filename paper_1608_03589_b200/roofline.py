@@ -35,3 +35,26 @@ def algorithmic_bytes(plan) -> dict:
 
 def survey_bytes_per_slice(plan) -> float | None:
     return SURVEY_BYTES_PER_SLICE.get((plan.info["n_out"], bool(plan.info["filter"])))
+
+
+def fp32_peak_tflops(sm_mhz: float = 1965.0, sms: int = 148) -> float:
+    """FP32 CUDA-core peak: SMs x 128 lanes x 2 (FMA) x clock."""
+    return sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+def nominal_flops(plan) -> dict:
+    """Nominal FFT flop counts per slice (5 N log2 N per complex N-point FFT,
+    pointwise complex multiply 6 flops) for each stage; the FFT kernels' honest
+    bound is the FP32 pipe, reported beside the HBM fraction."""
+    import math
+
+    i = plan.info
+    nt, nphi, nrho, L, M = i["nt"], i["nphi"], i["nrho"], i["L"], i["M"]
+    nh = nphi // 2 + 1
+    f = lambda n: 5.0 * n * math.log2(n)  # noqa: E731
+    return {
+        "ramp_filter": (i["ntheta"] / 2) * (2 * f(M) + 6 * M) if M else 0.0,  # packed column pairs
+        "row_rdft": (nt / 2) * f(nphi),                                        # packed row pairs
+        "rho_conv": nh * (2 * f(L) + 6 * L),
+        "irdft_readout": (nrho / 2) * f(nphi),
+    }
