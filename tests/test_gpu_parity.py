@@ -258,3 +258,31 @@ def test_empty_batch_and_stage_api_full_size(pkg):
     lp = plan.logpolar(dev(s)[None])[0].cpu().numpy()
     ref = O.logpolar_stage(s.astype(np.float64), 2048)
     assert report("cfg2 logpolar stage", lp, ref) <= RTOL
+
+
+@pytest.mark.parametrize("nt,n,fbp", [(256, 256, False), (256, 255, True), (512, 300, True), (2048, 2048, True)])
+def test_no_out_of_bounds_writes(pkg, nt, n, fbp):
+    """compute-sanitizer is unavailable on this pool: carve input, output and
+    workspace out of one NaN-filled buffer with guard zones and check that every
+    guard element survives a full execute (all kernels, TMA paths included)."""
+    plan = pkg.get_plan(nt, nt, n, None, None, (0.0, 1.0) if fbp else None)
+    b = 3
+    guard = 1 << 16  # floats
+    n_in, n_out = b * nt * nt, b * n * n
+    ws_floats = (plan.workspace_bytes(2) + 3) // 4
+    total = 4 * guard + n_in + n_out + ws_floats
+    big = torch.full((total,), float("nan"), device="cuda")
+    o_in, o_out, o_ws = guard, 2 * guard + n_in, 3 * guard + n_in + n_out
+    x = pkg.synth.config_batch(3 if nt == 2048 else 0 if nt == 256 else 1, range(b), torch.device("cuda"))
+    big[o_in:o_in + n_in] = x.reshape(-1)
+    sino = big[o_in:o_in + n_in].view(b, nt, nt)
+    out = big[o_out:o_out + n_out].view(b, n, n)
+    ws = big[o_ws:o_ws + ws_floats].view(torch.uint8)
+    plan.execute(sino, out=out, workspace=ws)
+    torch.cuda.synchronize()
+    for lo, hi in ((0, o_in), (o_in + n_in, o_out), (o_out + n_out, o_ws), (o_ws + ws_floats, total)):
+        assert torch.isnan(big[lo:hi]).all(), f"guard [{lo},{hi}) overwritten"
+    assert torch.equal(big[o_in:o_in + n_in], x.reshape(-1))  # input untouched
+    assert torch.isfinite(out).all()
+    ref = plan.execute(x)
+    assert torch.equal(out, ref)
