@@ -76,7 +76,8 @@ int lpbp_workspace_bytes(const lpbp_plan* plan, int32_t chunk, size_t* bytes);
 
 /* Full path: sinogram -> image for `batch` slices (device pointers).  The batch is
  * processed in chunks that fit ws_bytes (>= one slice).  ws = NULL uses a workspace
- * owned by the plan (then calls on one plan must not overlap). */
+ * owned by the plan (then calls on one plan must not overlap).  Alignment: sino_dev
+ * 16 bytes (TMA bulk loads), ws 256 bytes (cudaMalloc pointers satisfy both). */
 int lpbp_execute(const lpbp_plan* plan, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
                  size_t ws_bytes, void* stream);
 

@@ -224,6 +224,9 @@ int ensure_own_ws(lpbp_plan* P, size_t bytes) {
 int run_batched(const lpbp_plan* Pc, const float* in, float* out, int batch, void* ws, size_t ws_bytes,
                 cudaStream_t s, bool stop_after_lp) {
   lpbp_plan* P = const_cast<lpbp_plan*>(Pc);
+  // TMA bulk loads read the sinogram rows and the workspace regions directly
+  if (reinterpret_cast<uintptr_t>(in) % 16) return fail(LPBP_EINVAL, "sinogram pointer must be 16-byte aligned");
+  if (ws && reinterpret_cast<uintptr_t>(ws) % 256) return fail(LPBP_EINVAL, "workspace must be 256-byte aligned");
   const size_t per = P->szA + P->szB;
   std::unique_lock<std::mutex> lock(P->mu, std::defer_lock);
   if (!ws) {
@@ -466,7 +469,7 @@ int lpbp_execute_host(lpbp_plan* P, const float* sino_host, float* img_host, int
     cudaStreamWaitEvent(pp.s_comp, pp.ev_in[slot], 0);
     if (ci >= 2) cudaStreamWaitEvent(pp.s_comp, pp.ev_out[slot], 0);
     const int64_t before = g_launches;
-    int rc = run_chunk(P, pp.in[slot], pp.out[slot], c, static_cast<char*>(pp.ws), pp.s_comp, false, nullptr);
+    int rc = run_chunk(P, pp.in[slot], pp.out[slot], c, static_cast<char*>(pp.ws), pp.s_comp, false, nullptr);  // cudaMalloc'd: aligned
     if (rc) return rc;
     (void)before;
     cudaEventRecord(pp.ev_comp[slot], pp.s_comp);

@@ -90,6 +90,8 @@ class LogPolarPlan:
     def _check_sino(self, sino: torch.Tensor) -> torch.Tensor:
         _require_cuda(sino)
         sino = _as_f32_contig(sino, 3, "sinogram batch")
+        if sino.data_ptr() % 16:  # the kernels stream rows with 16-byte TMA bulk copies
+            sino = sino.clone()
         if tuple(sino.shape[1:]) != (self.nt, self.ntheta):
             raise ValueError(f"sinogram batch must have shape (B, {self.nt}, {self.ntheta}), got {tuple(sino.shape)}")
         if sino.device != self.device:

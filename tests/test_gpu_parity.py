@@ -270,9 +270,12 @@ def test_no_out_of_bounds_writes(pkg, nt, n, fbp):
     guard = 1 << 16  # floats
     n_in, n_out = b * nt * nt, b * n * n
     ws_floats = (plan.workspace_bytes(2) + 3) // 4
-    total = 4 * guard + n_in + n_out + ws_floats
+    up = lambda v: (v + 63) // 64 * 64  # noqa: E731  (256-byte aligned carve-outs: the ABI's contract)
+    o_in = guard
+    o_out = up(o_in + n_in + guard)
+    o_ws = up(o_out + n_out + guard)
+    total = o_ws + ws_floats + guard
     big = torch.full((total,), float("nan"), device="cuda")
-    o_in, o_out, o_ws = guard, 2 * guard + n_in, 3 * guard + n_in + n_out
     x = pkg.synth.config_batch(3 if nt == 2048 else 0 if nt == 256 else 1, range(b), torch.device("cuda"))
     big[o_in:o_in + n_in] = x.reshape(-1)
     sino = big[o_in:o_in + n_in].view(b, nt, nt)
@@ -286,3 +289,5 @@ def test_no_out_of_bounds_writes(pkg, nt, n, fbp):
     assert torch.isfinite(out).all()
     ref = plan.execute(x)
     assert torch.equal(out, ref)
+    with pytest.raises(ValueError, match="256-byte aligned"):
+        plan.execute(sino, out=out, workspace=big[o_ws + 1:o_ws + 1 + ws_floats].view(torch.uint8))
