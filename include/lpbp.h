@@ -65,6 +65,7 @@ typedef struct lpbp_plan_info {
   size_t workspace_per_slice;  /* lpbp_execute workspace bytes per slice in flight  */
   size_t readout_sector_bytes; /* distinct 32-byte log-polar sectors the readout taps (x32) */
   int32_t band_rows, row_min, nbands; /* fused inverse-DFT + readout banding               */
+  int32_t generic, MB;         /* 1: any-size path (Bluestein length-nphi DFTs on MB-point FFTs) */
 } lpbp_plan_info;
 
 int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan);
@@ -100,7 +101,8 @@ int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, in
 /* Host copies of plan tables for tests: which = "kernel_cells" (int32 pairs k,l),
  * "ramp" (float M), "khat" (float2 nh*L), "ab" (int32 pairs ns), "wab" (float4 ns),
  * "ki" (int32 nrho), "wi" (float2 nrho), "qidx" (uint32 nq*nq), "qw" (float2 nq*nq),
- * "band_off" (uint32 nbands+1), "band_entries" (uint32).  Returns the element count in *count;
+ * "band_off" (uint32 nbands+1), "band_entries" (uint32), "chirp" (float2 nphi),
+ * "bhat_f" / "bhat_i" (float2 MB; generic-size plans only).  Returns the element count in *count;
  * if dst is non-NULL copies min(count, capacity) elements. */
 int lpbp_plan_table(const lpbp_plan* plan, const char* which, void* dst, size_t capacity, size_t* count);
 

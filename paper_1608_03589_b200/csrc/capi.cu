@@ -178,25 +178,40 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   int* counter = reinterpret_cast<int*>(B + align256(P->szB * c));
   const float* src = in;
   cudaError_t e;
+  const bool gen = d.generic != 0;
   if (P->h.filter && !stop_after_lp) {
-    e = staged(P, 0, c, s, [&] { return lpbp::launch_ramp(d, P->t, in, reinterpret_cast<float*>(A), c, s); });
+    e = staged(P, 0, c, s, [&] {
+      return gen ? lpbp::launch_ramp_generic(d, P->t, in, reinterpret_cast<float*>(A), c, s)
+                 : lpbp::launch_ramp(d, P->t, in, reinterpret_cast<float*>(A), c, s);
+    });
     if (e) return launch_fail(e, "ramp_filter");
     ++g_launches;
     src = reinterpret_cast<const float*>(A);
   }
-  e = staged(P, 1, c, s, [&] { return lpbp::launch_row_rdft(d, P->t, src, reinterpret_cast<float2*>(B), c, s); });
+  e = staged(P, 1, c, s, [&] {
+    return gen ? lpbp::launch_row_rdft_generic(d, P->t, src, reinterpret_cast<float2*>(B), c, s)
+               : lpbp::launch_row_rdft(d, P->t, src, reinterpret_cast<float2*>(B), c, s);
+  });
   if (e) return launch_fail(e, "row_rdft");
   ++g_launches;
   e = staged(P, 2, c, s, [&] {
     return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c,
-                                 stop_after_lp ? 0 : d.row_min, s);
+                                 (stop_after_lp || gen) ? 0 : d.row_min, s);
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
-  if (stop_after_lp) {
-    e = staged(P, 3, c, s,
-               [&] { return lpbp::launch_row_irdft(d, P->t, reinterpret_cast<const float2*>(A), lp_out, c, s); });
+  if (stop_after_lp || gen) {
+    // generic sizes: unfused inverse DFT into B (or the caller's buffer), then the readout
+    float* lp = stop_after_lp ? lp_out : reinterpret_cast<float*>(B);
+    e = staged(P, 3, c, s, [&] {
+      return gen ? lpbp::launch_row_irdft_generic(d, P->t, reinterpret_cast<const float2*>(A), lp, c, s)
+                 : lpbp::launch_row_irdft(d, P->t, reinterpret_cast<const float2*>(A), lp, c, s);
+    });
     if (e) return launch_fail(e, "row_irdft");
+    ++g_launches;
+    if (stop_after_lp) return LPBP_OK;
+    e = staged(P, 4, c, s, [&] { return lpbp::launch_readout(d, P->t, lp, out, c, s); });
+    if (e) return launch_fail(e, "readout");
     ++g_launches;
     return LPBP_OK;
   }
@@ -271,11 +286,11 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     return fail(LPBP_EINVAL, err);
   }
   const HostPlan& h = P->h;
-  if (params->device >= 0 && !lpbp::sizes_supported(h.nt, h.ntheta, h.L, h.filter)) {
+  if (params->device >= 0 && !lpbp::sizes_supported(h.nt, h.ntheta, h.L, h.M, h.MB, h.filter, h.generic)) {
     delete P;
     return fail(LPBP_EUNSUPPORTED, "no kernel instantiation for nt=" + std::to_string(h.nt) + ", ntheta=" +
                                        std::to_string(h.ntheta) + ", L=" + std::to_string(h.L) +
-                                       " (this build: 2*ntheta and 2*nt powers of two in [512, 4096])");
+                                       " (this build: nt even, 2*ntheta <= 4096, 2*nt <= 4096, rho FFT <= 8192)");
   }
   P->device = params->device;
   if (lpbp::fused_band_rows(P->h.nphi) > 0) lpbp::build_bands(P->h, lpbp::fused_band_rows(P->h.nphi));
@@ -289,6 +304,12 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     rc = rc ? rc : P->twiddles(h.nphi, &P->t.tw_phi);
     rc = rc ? rc : P->twiddles(h.L, &P->t.tw_rho);
     if (h.filter) rc = rc ? rc : P->twiddles(h.M, &P->t.tw_ramp);
+    if (h.generic) {
+      rc = rc ? rc : P->twiddles(h.MB, &P->t.tw_blue);
+      rc = rc ? rc : P->upload(h.chirp, reinterpret_cast<const lpbp::F2**>(&P->t.chirp));
+      rc = rc ? rc : P->upload(h.bhat_f, reinterpret_cast<const lpbp::F2**>(&P->t.bhat_f));
+      rc = rc ? rc : P->upload(h.bhat_i, reinterpret_cast<const lpbp::F2**>(&P->t.bhat_i));
+    }
     rc = rc ? rc : P->upload(h.ramp, &P->t.ramp);
     rc = rc ? rc : P->upload(h.ab, reinterpret_cast<const lpbp::I2**>(&P->t.ab));
     rc = rc ? rc : P->upload(h.wab, reinterpret_cast<const lpbp::F4**>(&P->t.wab));
@@ -324,6 +345,8 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   d.row_min = h.row_min;
   d.nbands = h.nbands;
   d.band_rows = h.band_rows;
+  d.generic = h.generic ? 1 : 0;
+  d.MB = h.MB;
   d.nsm = 148;
   if (P->device >= 0) cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, P->device);
   const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;
@@ -363,6 +386,8 @@ int lpbp_plan_get_info(const lpbp_plan* P, lpbp_plan_info* info) {
   info->band_rows = h.band_rows;
   info->row_min = h.row_min;
   info->nbands = h.nbands;
+  info->generic = h.generic ? 1 : 0;
+  info->MB = h.MB;
   return LPBP_OK;
 }
 
@@ -402,7 +427,9 @@ int lpbp_filter(const lpbp_plan* P, const float* sino_dev, float* out_dev, int32
   if (batch == 0) return LPBP_OK;
   if (!sino_dev || !out_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
-  cudaError_t e = lpbp::launch_ramp(P->d, P->t, sino_dev, out_dev, batch, static_cast<cudaStream_t>(stream));
+  cudaError_t e = P->d.generic
+                      ? lpbp::launch_ramp_generic(P->d, P->t, sino_dev, out_dev, batch, static_cast<cudaStream_t>(stream))
+                      : lpbp::launch_ramp(P->d, P->t, sino_dev, out_dev, batch, static_cast<cudaStream_t>(stream));
   if (e) return launch_fail(e, "ramp_filter");
   ++g_launches;
   return LPBP_OK;
@@ -558,6 +585,9 @@ int lpbp_plan_table(const lpbp_plan* P, const char* which, void* dst, size_t cap
   if (!std::strcmp(which, "wi")) return copy_vec(h.wi);         // float pairs
   if (!std::strcmp(which, "qidx")) return copy_vec(h.qidx);     // uint32
   if (!std::strcmp(which, "qw")) return copy_vec(h.qw);         // float pairs
+  if (!std::strcmp(which, "chirp")) return copy_vec(h.chirp);      // float2 nphi (generic sizes)
+  if (!std::strcmp(which, "bhat_f")) return copy_vec(h.bhat_f);    // float2 MB
+  if (!std::strcmp(which, "bhat_i")) return copy_vec(h.bhat_i);    // float2 MB
   if (!std::strcmp(which, "band_off")) return copy_vec(h.band_off);          // uint32 nbands+1
   if (!std::strcmp(which, "band_entries")) return copy_vec(h.band_entries);  // uint32
   return fail(LPBP_EINVAL, std::string("unknown table ") + which);

@@ -626,6 +626,106 @@ k_naive(const float* __restrict__ gT, float* __restrict__ img, int nt, int nthet
 }
 
 // ---------------------------------------------------------------------------
+// Generic sizes (any nt, any ntheta; nphi = 2 ntheta need not be a power of two).
+// The length-nphi DFTs use Bluestein's identity with the same pow2 block_conv:
+//   X[k] = c[k] sum_n (x[n] c[n]) conj c[k-n],  c[n] = exp(-i pi n^2 / nphi),
+// a circular MB-point convolution (MB = pow2 >= 2 nphi) with the plan's
+// precomputed spectrum of the chirp filter.  One CTA per row (column) pair.
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__(FftPlan<M, false>::T)
+k_ramp_generic(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
+               const float* __restrict__ resp, const float2* __restrict__ tw) {
+  extern __shared__ __align__(16) float2 smem_g1[];
+  const int ca = 2 * blockIdx.x, cb = ca + 1;
+  const bool hb = cb < ntheta;
+  const size_t slice = (size_t)blockIdx.y * nt * ntheta;
+  const float* src = g + slice;
+  float* dst = out + slice;
+  auto load = [&](int idx) -> float2 {
+    if (idx >= nt) return make_float2(0.f, 0.f);
+    const float* r = src + (size_t)idx * ntheta;
+    return make_float2(__ldg(r + ca), hb ? __ldg(r + cb) : 0.f);
+  };
+  auto mul = [&](int idx, float2 v) -> float2 { return cscale(v, __ldg(resp + idx)); };
+  auto store = [&](int idx, float2 v) {
+    if (idx < nt) {
+      dst[(size_t)idx * ntheta + ca] = v.x;
+      if (hb) dst[(size_t)idx * ntheta + cb] = v.y;
+    }
+  };
+  block_conv<M, true>(smem_g1, threadIdx.x, tw, load, mul, store, block_sync);  // M >= 2 nt
+}
+
+template <int MB>
+__global__ void __launch_bounds__(FftPlan<MB, false>::T)
+k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int ntheta,
+                   const float2* __restrict__ chirp, const float2* __restrict__ bhat, const float2* __restrict__ tw) {
+  extern __shared__ __align__(16) float2 smem_g2[];
+  const int nphi = 2 * ntheta, nh = ntheta + 1;
+  float2* buf = smem_g2;
+  float2* Z = smem_g2 + padded_len(MB);  // [nphi]
+  const int ta = 2 * blockIdx.x, tb = ta + 1;
+  const bool hb = tb < nt;
+  const float* ra = g + ((size_t)blockIdx.y * nt + ta) * ntheta;
+  const float* rb = ra + ntheta;
+  auto load = [&](int idx) -> float2 {  // a[n] = z[n] c[n]; z is zero for n >= ntheta
+    if (idx >= ntheta) return make_float2(0.f, 0.f);
+    const float2 z = make_float2(__ldg(ra + idx), hb ? __ldg(rb + idx) : 0.f);
+    return cmul(z, __ldg(chirp + idx));
+  };
+  auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(bhat + idx)); };
+  auto store = [&](int idx, float2 v) {
+    if (idx < nphi) Z[idx] = cmul(v, __ldg(chirp + idx));
+  };
+  block_conv<MB, true>(buf, threadIdx.x, tw, load, mul, store, block_sync);
+  __syncthreads();
+  float2* dst = Gh + (size_t)blockIdx.y * nh * nt + ta;
+  for (int m = threadIdx.x; m < nh; m += blockDim.x) {
+    const float2 z = Z[m], w = Z[m == 0 ? 0 : nphi - m];
+    dst[(size_t)m * nt] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
+    if (hb) dst[(size_t)m * nt + 1] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+  }
+}
+
+template <int MB>
+__global__ void __launch_bounds__(FftPlan<MB, false>::T)
+k_row_irdft_generic(const float2* __restrict__ Yh, float* __restrict__ lp, int nrho, int nrho_pad, int ntheta,
+                    const float2* __restrict__ chirp, const float2* __restrict__ bhat, const float2* __restrict__ tw) {
+  extern __shared__ __align__(16) float2 smem_g4[];
+  const int nphi = 2 * ntheta, nh = ntheta + 1;
+  const int ia = 2 * blockIdx.x, ib = ia + 1;
+  const bool hb = ib < nrho;
+  const float2* src = Yh + (size_t)blockIdx.y * nh * nrho_pad;
+  float* dst = lp + (size_t)blockIdx.y * nrho * nphi;
+  auto load = [&](int idx) -> float2 {  // a[k] = Z[k] conj c[k], Z Hermitian-assembled from Y
+    if (idx >= nphi) return make_float2(0.f, 0.f);
+    const bool hi = idx > ntheta;
+    const int mm = hi ? nphi - idx : idx;
+    float2 xa = src[(size_t)mm * nrho_pad + ia];
+    float2 xb = hb ? src[(size_t)mm * nrho_pad + ib] : make_float2(0.f, 0.f);
+    if (mm == 0 || mm == ntheta) {
+      xa.y = 0.f;
+      xb.y = 0.f;
+    }
+    if (hi) {
+      xa.y = -xa.y;
+      xb.y = -xb.y;
+    }
+    return cmulc(make_float2(xa.x - xb.y, xa.y + xb.x), __ldg(chirp + idx));
+  };
+  auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(bhat + idx)); };
+  auto store = [&](int idx, float2 v) {
+    if (idx < nphi) {
+      const float2 z = cmulc(v, __ldg(chirp + idx));
+      dst[(size_t)ia * nphi + idx] = z.x;
+      if (hb) dst[(size_t)ib * nphi + idx] = z.y;
+    }
+  };
+  block_conv<MB, true>(smem_g4, threadIdx.x, tw, load, mul, store, block_sync);
+}
+
+// ---------------------------------------------------------------------------
 // Harness input generator: exact ellipse line integrals (radon.py:38-61) in fp64,
 // 2 rho A B sqrt(w^2 - tau^2) / w^2, tau = t - c.xi_theta,
 // w^2 = A^2 cos^2(theta - gamma) + B^2 sin^2(theta - gamma).
@@ -839,6 +939,69 @@ cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, 
 }
 }  // namespace
 
+namespace {
+template <int M>
+cudaError_t ramp_generic_impl(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s) {
+  const size_t smem = (size_t)padded_len(M) * sizeof(float2);
+  auto k = k_ramp_generic<M>;
+  cudaError_t e = prep(k, smem);
+  if (e) return e;
+  k<<<dim3((d.ntheta + 1) / 2, batch), FftPlan<M, false>::T, smem, s>>>(g, out, d.nt, d.ntheta, t.ramp, t.tw_ramp);
+  return cudaGetLastError();
+}
+template <int MB>
+cudaError_t rdft_generic_impl(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch,
+                              cudaStream_t s) {
+  const size_t smem = ((size_t)padded_len(MB) + d.nphi) * sizeof(float2);
+  auto k = k_row_rdft_generic<MB>;
+  cudaError_t e = prep(k, smem);
+  if (e) return e;
+  k<<<dim3((d.nt + 1) / 2, batch), FftPlan<MB, false>::T, smem, s>>>(g, Gh, d.nt, d.ntheta, t.chirp, t.bhat_f,
+                                                                    t.tw_blue);
+  return cudaGetLastError();
+}
+template <int MB>
+cudaError_t irdft_generic_impl(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch,
+                               cudaStream_t s) {
+  const size_t smem = (size_t)padded_len(MB) * sizeof(float2);
+  auto k = k_row_irdft_generic<MB>;
+  cudaError_t e = prep(k, smem);
+  if (e) return e;
+  k<<<dim3((d.nrho + 1) / 2, batch), FftPlan<MB, false>::T, smem, s>>>(Yh, lp, d.nrho, d.nrho_pad, d.ntheta,
+                                                                      t.chirp, t.bhat_i, t.tw_blue);
+  return cudaGetLastError();
+}
+}  // namespace
+
+#define LPBP_POW2_SWITCH(N, CALL)                 \
+  switch (N) {                                    \
+    case 512: return CALL(512);                   \
+    case 1024: return CALL(1024);                 \
+    case 2048: return CALL(2048);                 \
+    case 4096: return CALL(4096);                 \
+    case 8192: return CALL(8192);                 \
+    default: return cudaErrorNotSupported;        \
+  }
+
+cudaError_t launch_ramp_generic(const Dims& d, const DevTables& t, const float* g, float* out, int batch,
+                                cudaStream_t s) {
+#define LPBP_CALL(M) ramp_generic_impl<M>(d, t, g, out, batch, s)
+  LPBP_POW2_SWITCH(d.M, LPBP_CALL)
+#undef LPBP_CALL
+}
+cudaError_t launch_row_rdft_generic(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch,
+                                    cudaStream_t s) {
+#define LPBP_CALL(M) rdft_generic_impl<M>(d, t, g, Gh, batch, s)
+  LPBP_POW2_SWITCH(d.MB, LPBP_CALL)
+#undef LPBP_CALL
+}
+cudaError_t launch_row_irdft_generic(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch,
+                                     cudaStream_t s) {
+#define LPBP_CALL(M) irdft_generic_impl<M>(d, t, Yh, lp, batch, s)
+  LPBP_POW2_SWITCH(d.MB, LPBP_CALL)
+#undef LPBP_CALL
+}
+
 int fused_band_rows(int nphi) {
   switch (nphi) {
     case 512: return FusedShape<512>::S;
@@ -916,14 +1079,14 @@ cudaError_t launch_init_twiddles(int N, float2* out, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-bool sizes_supported(int nt, int ntheta, int L, bool filter) {
-  const int nphi = 2 * ntheta;
+bool sizes_supported(int nt, int ntheta, int L, int M, int MB, bool filter, bool generic) {
   auto pow2in = [](int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; };
-  if (!pow2in(nphi, 512, 4096)) return false;
   if (!pow2in(L, 512, 8192)) return false;
-  if (nt % 16) return false;
-  if (filter && !pow2in(2 * nt, 512, 4096)) return false;
-  if (filter && ntheta % 16) return false;
+  if (filter && !pow2in(M, 512, 8192)) return false;
+  if (generic) return pow2in(MB, 512, 8192) && (nt % 2) == 0;
+  const int nphi = 2 * ntheta;
+  if (!pow2in(nphi, 512, 4096) || nt % 4) return false;
+  if (filter && (ntheta % 8 || M > 4096)) return false;
   return true;
 }
 

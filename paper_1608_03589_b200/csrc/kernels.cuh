@@ -27,12 +27,18 @@ struct DevTables {
   const float2* naive_cs; // [ntheta] (cos, sin) * nt/(2n) for the direct backprojector
   const uint32_t* band_off;      // [nbands+1] fused readout: entry range per band
   const uint32_t* band_entries;  // per band: uint4 {qq | bit31 zero, qidx, wi, wj} (plan_host band_packed)
+  // generic sizes (Bluestein)
+  const float2* chirp;   // [nphi]
+  const float2* bhat_f;  // [MB]
+  const float2* bhat_i;  // [MB]
+  const float2* tw_blue; // pass twiddles, N = MB
 };
 
 struct Dims {
   int nt, ntheta, n, ns, nphi, nh, nrho, nrho_pad, L, M, nq;
   int row_min, nbands, band_rows;  // fused inverse-DFT + readout quads (band_rows = 4)
   int nsm;                         // SMs of the plan's device (persistent grids)
+  int generic, MB;                 // generic-size path (Bluestein length-nphi DFTs via MB-point convolutions)
   float out_scale;        // 1 (backprojection) or 1/(2 pi) (fbp)
 };
 
@@ -57,7 +63,14 @@ cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dthe
 cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int ntheta, int batch, float* out,
                                   cudaStream_t s);
 
-bool sizes_supported(int nt, int ntheta, int L, bool filter);
+bool sizes_supported(int nt, int ntheta, int L, int M, int MB, bool filter, bool generic);
+// generic-size kernels: ramp over bounds-checked column pairs, Bluestein row DFT / inverse DFT
+cudaError_t launch_ramp_generic(const Dims& d, const DevTables& t, const float* g, float* out, int batch,
+                                cudaStream_t s);
+cudaError_t launch_row_rdft_generic(const Dims& d, const DevTables& t, const float* g, float2* G, int batch,
+                                    cudaStream_t s);
+cudaError_t launch_row_irdft_generic(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch,
+                                     cudaStream_t s);
 // Pass-twiddle tables (fft.cuh TwTable): entry count for size N (-1 if unsupported)
 // and a device fill kernel.
 int twiddle_table_len(int N);

@@ -255,6 +255,35 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
 
   // (FFT twiddle tables are generated on the device from the compile-time radix plans.)
 
+  // --- generic-size path: Bluestein chirps for the length-nphi DFTs
+  const bool pow2_phi = (nphi & (nphi - 1)) == 0 && nphi >= 512 && nphi <= 4096;
+  h.generic = !pow2_phi || (nt % 4) != 0 || (p.filter && (p.ntheta % 8) != 0);
+  if (h.generic) {
+    h.MB = std::max(512, next_pow2(2 * nphi));
+    const int MB = h.MB;
+    h.chirp.resize(nphi);
+    std::vector<cd> c(nphi);
+    for (int k = 0; k < nphi; ++k) {
+      const long long q = ((long long)k * k) % (2LL * nphi);  // exact phase reduction
+      c[k] = std::polar(1.0, -kPi * (double)q / nphi);
+      h.chirp[k] = F2{(float)c[k].real(), (float)c[k].imag()};
+    }
+    std::vector<cd> wM(MB / 2);
+    for (int k = 0; k < MB / 2; ++k) wM[k] = std::polar(1.0, -2.0 * kPi * (double)k / MB);
+    for (int dir = 0; dir < 2; ++dir) {  // forward: b[j] = conj c[|j|]; inverse: b[j] = c[|j|]
+      std::vector<cd> b(MB, cd(0, 0));
+      for (int j = 0; j < nphi; ++j) {
+        const cd v = dir == 0 ? std::conj(c[j]) : c[j];
+        b[j] = v;
+        if (j) b[MB - j] = v;
+      }
+      fft_pow2(b, wM);
+      auto& dst = dir == 0 ? h.bhat_f : h.bhat_i;
+      dst.resize(MB);
+      for (int q = 0; q < MB; ++q) dst[q] = F2{(float)(b[q].real() / MB), (float)(b[q].imag() / MB)};
+    }
+  }
+
   // --- ramp / Tikhonov filter (filtering.py:54-70).  The reference multiplies
   // by resp on an Lr = next_fast_len(8 nt) grid; that is a convolution with the
   // real even taps h[d] = (1/Lr) sum_k resp_k cos(2 pi k d / Lr), |d| < nt.
@@ -285,7 +314,7 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
       }
       taps[d] = acc / Lr;
     }
-    h.M = 2 * nt;
+    h.M = std::max(512, next_pow2(2 * nt));  // any M >= 2 nt - 1 embeds the Toeplitz filter
     const int M = h.M;
     std::vector<double> cosm(M);
     for (int q = 0; q < M; ++q) cosm[q] = std::cos(2.0 * kPi * (double)q / M);

@@ -43,6 +43,12 @@ struct HostPlan {
   std::vector<uint32_t> band_entries, band_off;
   // self-contained 16-byte entries {qq | zero flag, qidx, wi bits, wj bits}
   std::vector<uint32_t> band_packed;
+  // generic sizes (nphi not a power of two in [512, 4096], ...): Bluestein DFTs of
+  // length nphi through MB-point convolutions, MB = pow2 >= 2 nphi
+  bool generic = false;
+  int MB = 0;
+  std::vector<F2> chirp;          // [nphi] exp(-i pi n^2 / nphi)
+  std::vector<F2> bhat_f, bhat_i; // [MB] FFT_MB of the forward / inverse chirp filter, incl. 1/MB
   // kernel support (for diagnostics/tests): cells (k, l) of the rolled kernel
   std::vector<int32_t> cell_k, cell_l;
 };

@@ -224,3 +224,31 @@ def test_fused_readout_bands_cover_every_pixel_once(nt, nth, n, rho0):
     R = np.hypot(X, Y)
     ref_zero = ~((R <= 1.0) & (R > 0) & (np.log(np.maximum(R, 1e-300)) >= i.rho0))
     assert np.array_equal(zero, ref_zero)
+
+
+@pytest.mark.parametrize("nt,nth", [(128, 90), (256, 180), (200, 96)])
+def test_generic_size_bluestein_tables(nt, nth):
+    """Generic sizes: the chirp / chirp-filter spectra make an MB-point circular
+    convolution equal the length-nphi DFT (forward and inverse), and the ramp is
+    embedded on M = pow2 >= 2 nt."""
+    hp = HostPlan(nt, nth, 64, filt=(0.0, 1.0))
+    i = hp.info
+    nphi = 2 * nth
+    assert i.generic == 1 and i.MB >= 2 * nphi and (i.MB & (i.MB - 1)) == 0
+    assert i.M >= 2 * nt and (i.M & (i.M - 1)) == 0
+    c = hp.table("chirp", np.complex64).astype(np.complex128)
+    bf = hp.table("bhat_f", np.complex64).astype(np.complex128)
+    bi = hp.table("bhat_i", np.complex64).astype(np.complex128)
+    rng = np.random.default_rng(nphi)
+    x = rng.standard_normal(nphi) + 1j * rng.standard_normal(nphi)
+    MB = i.MB
+    conv = np.fft.ifft(np.fft.fft(x * c, MB) * bf * MB)   # block_conv: unnormalised inverse, 1/MB in bhat
+    X = c * conv[:nphi]
+    assert np.abs(X - np.fft.fft(x)).max() / np.abs(X).max() < 1e-5
+    conv = np.fft.ifft(np.fft.fft(x * np.conj(c), MB) * bi * MB)
+    xi = np.conj(c) * conv[:nphi]
+    assert np.abs(xi - np.fft.ifft(x) * nphi).max() / np.abs(xi).max() < 1e-5
+    g = rng.standard_normal((nt, nth))
+    H = hp.table("ramp", np.float32).astype(np.float64)
+    out = np.fft.ifft(np.fft.fft(g, n=i.M, axis=0) * H[:, None], axis=0).real[:nt] * i.M
+    assert O.relative_l2(out, O.ramp_filter(g)) < 1e-6

@@ -174,7 +174,7 @@ def test_cfg4_naive_cross_check(pkg):
 
 
 def test_unsupported_size_is_loud(pkg):
-    g = pkg.Sinogram(128, 90, np.ones((128, 90)))
+    g = pkg.Sinogram(129, 90, np.ones((129, 90)))  # odd nt: no instantiation
     with pytest.raises(NotImplementedError):
         pkg.logpolar_backproject(g, 64)
     with pytest.raises(NotImplementedError):
@@ -291,3 +291,36 @@ def test_no_out_of_bounds_writes(pkg, nt, n, fbp):
     assert torch.equal(out, ref)
     with pytest.raises(ValueError, match="256-byte aligned"):
         plan.execute(sino, out=out, workspace=big[o_ws + 1:o_ws + 1 + ws_floats].view(torch.uint8))
+
+
+@pytest.mark.parametrize("nt,nth,n", [(128, 90, 64), (256, 180, 128), (200, 96, 100), (512, 360, 256)])
+def test_generic_sizes_vs_oracle(pkg, nt, nth, n):
+    """Non-power-of-two angle counts (the reference's own examples use 90/180) run
+    the Bluestein path; BP and FBP match the oracle."""
+    rng = np.random.default_rng(nt + nth)
+    gd = np.cumsum(rng.standard_normal((nt, nth)), axis=0).astype(np.float32).astype(np.float64) * 0.05
+    g = pkg.Sinogram(nt, nth, gd)
+    assert report(f"generic bp {nt}x{nth}->{n}", pkg.logpolar_backproject(g, n).values,
+                  O.logpolar_backproject(gd, n)) <= RTOL
+    assert report(f"generic fbp {nt}x{nth}->{n}", pkg.fbp(g, pkg.FilterSpec(), engine="logpolar", n=n).values,
+                  O.fbp_logpolar(gd, n)) <= RTOL
+    assert report(f"generic filter {nt}x{nth}", pkg.filter_sinogram(g, pkg.FilterSpec(lam=0.01)).values,
+                  O.ramp_filter(gd, 0.01)) <= 1e-5
+
+
+def test_reference_known_answers_on_device(pkg):
+    """scratch_lp.py known answers (constant sinogram, pinned in tests/golden/kat.json)
+    reproduced by the device path: interior means 3.05565 and 3.09808."""
+    import json
+    import os
+    from conftest import GOLDEN
+    kat = json.load(open(os.path.join(GOLDEN, "kat.json")))
+    for nt, nth, n in ((128, 90, 64), (256, 180, 128)):
+        b = pkg.logpolar_backproject(pkg.Sinogram(nt, nth, np.ones((nt, nth))), n).values
+        xs = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+        X, Y = np.meshgrid(xs, xs)
+        R = np.hypot(X, Y)
+        inner = (R > 2 * math.exp(pkg.adaptive_rho0(n, n))) & (R <= 0.8)
+        got, want = b[inner].mean(), kat[f"const_mean_{nt}_{nth}_{n}"]
+        print(f"const mean {nt}x{nth}->{n}: {got:.6f} (reference {want:.6f})")
+        assert abs(got - want) < 1e-5 * abs(want)
