@@ -301,7 +301,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
       return fail(LPBP_ECUDA, "cannot select CUDA device " + std::to_string(params->device));
     }
     int rc = LPBP_OK;
-    rc = rc ? rc : P->twiddles(h.nphi, &P->t.tw_phi);
+    if (!h.generic) rc = rc ? rc : P->twiddles(h.nphi, &P->t.tw_phi);
     rc = rc ? rc : P->twiddles(h.L, &P->t.tw_rho);
     if (h.filter) rc = rc ? rc : P->twiddles(h.M, &P->t.tw_ramp);
     if (h.generic) {
