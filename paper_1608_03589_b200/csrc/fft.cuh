@@ -94,6 +94,16 @@ __host__ __device__ constexpr double cos32(int k) {
 }
 __host__ __device__ constexpr double sin32(int k) { return cos32(k - 8); }
 
+// e + (c + i s) o as two FFMA2: (e.x + c o.x, e.y + s o.x) + o.y (-s, c)
+__device__ __forceinline__ float2 cfma_const(float2 e, float2 o, float c, float s) {
+  const float2 t = v2fma(pk2(o.x, o.x), pk2(c, s), pk2(e.x, e.y));
+  return v2fma(pk2(o.y, o.y), pk2(-s, c), pk2(t.x, t.y));
+}
+// 2 e - p (one FFMA2): the partner output of a butterfly whose first output is p = e + t
+__device__ __forceinline__ float2 ctwice_minus(float2 e, float2 p) {
+  return v2fma(pk2(e.x, e.y), pk2(2.f, 2.f), pk2(-p.x, -p.y));
+}
+
 // x * exp(s * 2*pi*i*K/R) with s = -1 (forward) or +1 (inverse); K, R compile-time.
 template <int K, int R, bool INV>
 __device__ __forceinline__ float2 twc(float2 x) {
@@ -149,9 +159,17 @@ struct Dft {
       Dft<R / 2, INV>::template run_sub<OFF + STRIDE, STRIDE * 2, LEN, ZU, false>(in, O);
       static_for<0, R / 2>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
-        const float2 t = twc<k, R, INV>(O[k]);
-        out[k] = cadd(E[k], t);
-        if constexpr (!LOW) out[k + R / 2] = csub(E[k], t);
+        if constexpr (k == 0 || 4 * k == R) {  // multiplier 1 or -+i: free
+          const float2 t = twc<k, R, INV>(O[k]);
+          out[k] = cadd(E[k], t);
+          if constexpr (!LOW) out[k + R / 2] = csub(E[k], t);
+        } else {  // E + w O as two FFMA2, E - w O = 2E - (E + w O) as one
+          constexpr int k32 = k * (32 / R);
+          constexpr float c = (float)cos32(k32);
+          constexpr float sn = INV ? (float)sin32(k32) : -(float)sin32(k32);
+          out[k] = cfma_const(E[k], O[k], c, sn);
+          if constexpr (!LOW) out[k + R / 2] = ctwice_minus(E[k], out[k]);
+        }
       });
     }
   }
