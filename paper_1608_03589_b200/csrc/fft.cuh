@@ -328,7 +328,7 @@ struct TwTable {
 //   store(idx, val)           : output element idx (last pass writes it directly)
 //   sync()                    : barrier covering every thread that shares buf
 // LAST_SYNC places a barrier between the last pass's loads and its stores (needed
-// when store() writes back into buf); FIRST_SYNC places a CTA-wide barrier between
+// when store() writes back into buf); FIRST_SYNC places a sync() barrier between
 // pass 0's loads and stores (needed when load() reads buf or a region other
 // groups' buffers overlap).
 // The caller must guarantee buf is free on entry (no thread still reading it).
@@ -360,7 +360,7 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
         Dft<R, INV>::run(v[b]);
       }
     }
-    if constexpr (FIRST_SYNC) __syncthreads();  // load() reads buf (CTA-wide: groups may share the source)
+    if constexpr (FIRST_SYNC) sync();  // load() reads buf: everyone's pass-0 loads before any store
 #pragma unroll
     for (int b = 0; b < NB; ++b) pass_store<N, R, 1, S>(buf, ti + b * T, v[b]);
   }

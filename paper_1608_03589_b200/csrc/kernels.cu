@@ -397,7 +397,7 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 // Persistent CTAs take work units (slice, 16 consecutive quads of 4 log-polar
 // rows) from an atomic counter, outermost (pixel-heavy) units first.  Per quad:
 // a 3-D TMA tensor map over Y[b][m][rho] with box {4 rows (32 B), 256 m} lands
-// the quad's spectra as [m][4] in one of NR ring regions (prefetched NR-1 quads
+// the quad's spectra ([m][2] per row pair) in one of NR ring regions (prefetched NR-1 quads
 // ahead); the two FFT groups inverse-transform the quad's two row pairs in place;
 // the quad's pixels (taps i0, i0+1 with i0 in [r0-1, r0+3)) are sampled from the
 // region plus a carry copy of the previous quad's last row.  The log-polar image
@@ -414,8 +414,10 @@ struct FusedShape {
   static_assert(NFULL * 256 + 1 == NPHI / 2 + 1, "tail box is one row");
   // FFT buffer / row storage per group; +8 float2 skews the groups' rows by 16 banks
   static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16 + 8;
-  static constexpr int QREG0 = S * (NPHI / 2 + 1) > G * HALF ? S * (NPHI / 2 + 1) : G * HALF;
-  static constexpr int QREG = (QREG0 + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
+  // group g's two spectra rows arrive as [m][2] at g * IN_PITCH (128-B aligned, inside its own half)
+  static constexpr int IN_PITCH = (HALF + 15) / 16 * 16;
+  static_assert(IN_PITCH + 2 * (NPHI / 2 + 1) <= G * HALF, "group input inside its FFT half");
+  static constexpr int QREG = (G * HALF + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
   static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 128;  // regions + barriers
 };
 
@@ -449,10 +451,12 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
   auto issue = [&](int region, int step, int slice) {
     fence_proxy_async_smem();  // order earlier generic accesses to the region before the TMA writes
     mbar_arrive_expect_tx(&bars[region], STEP_BYTES);
-    const int c0 = 2 * (row_min + S * step);
-    for (int bx = 0; bx < NFULL; ++bx)
-      tma_load_3d(smem_k45 + region * QREG + S * (bx * 256), &ymap, c0, bx * 256, slice, &bars[region]);
-    tma_load_3d(smem_k45 + region * QREG + S * (NFULL * 256), &ytail, c0, NFULL * 256, slice, &bars[region]);
+    for (int g = 0; g < G; ++g) {  // rows (r0 + 2g, r0 + 2g + 1) -> group g's input as [m][2]
+      const int c0 = 2 * (row_min + S * step + 2 * g);
+      float2* dst = smem_k45 + region * QREG + g * FS::IN_PITCH;
+      for (int bx = 0; bx < NFULL; ++bx) tma_load_3d(dst + 2 * (bx * 256), &ymap, c0, bx * 256, slice, &bars[region]);
+      tma_load_3d(dst + 2 * (NFULL * 256), &ytail, c0, NFULL * 256, slice, &bars[region]);
+    }
     const uint32_t a = __ldg(step_off + step), b = __ldg(step_off + step + 1);  // warm L2 with its pixels
     if (b > a) prefetch_l2_bulk(entries + a, 16u * (b - a));
   };
@@ -483,21 +487,23 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       // first pixel entries of this step: loads in flight across the transforms
       const bool rd = kk >= k0;
       const uint32_t e0 = rd ? __ldg(step_off + kk) : 0u, e1 = rd ? __ldg(step_off + kk + 1) : 0u;
-      uint4 pre = make_uint4(0x80000000u, 0, 0, 0);
+      uint4 pre = make_uint4(0x80000000u, 0, 0, 0), pre2 = pre;
       const uint32_t ep = e0 + threadIdx.x;
       if (ep < e1) pre = __ldg(entries + ep);
+      if (ep + blockDim.x < e1) pre2 = __ldg(entries + ep + blockDim.x);
 
       mbar_wait(&bars[R], (phase >> R) & 1);
       phase ^= 1u << R;
       // inverse DFTs of rows (r0 + 2 gi, r0 + 2 gi + 1), in place in this group's part
       float2* H = Q + gi * HALF;
       float* Hf = reinterpret_cast<float*>(H);
+      const float2* Qin = Q + gi * FS::IN_PITCH;
       const int ra = r0 + 2 * gi;
       const bool va = ra < nrho, vb = ra + 1 < nrho;  // rows past nrho read padding: zero
       auto load = [&](int idx) -> float2 {
         const bool hi = idx > NPHI / 2;
         const int mm = hi ? NPHI - idx : idx;
-        float4 x = *reinterpret_cast<const float4*>(Q + S * mm + 2 * gi);  // (Xa, Xb) at mm
+        float4 x = *reinterpret_cast<const float4*>(Qin + 2 * mm);  // (Xa, Xb) at mm
         if (!va) x.x = x.y = 0.f;
         if (!vb) x.z = x.w = 0.f;
         float ay = x.y, by = x.w;
@@ -515,7 +521,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
         Hf[idx] = v.x;
         Hf[RPITCH + idx] = v.y;
       };
-      block_fft<NPHI, true, true, true, false, 16>(H, ti, tw, load, store, GroupSync{1 + gi, T});
+      block_fft<NPHI, true, true, true, false, 16>(H, ti, tw, load, store, GroupSync{1 + gi, T});  // group-local
       __syncthreads();
 
       if (rd) {  // readout: taps from this step's rows and the previous step's last row
@@ -553,9 +559,20 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
             if (!dupx) out[(size_t)iyn * n + jxn] = v3;
           }
         };
-        if (ep < e1) pixel(pre);
-#pragma unroll 2
-        for (uint32_t e = ep + blockDim.x; e < e1; e += blockDim.x) pixel(__ldg(entries + e));
+        if (ep < e1) {  // entry loads run two pixels ahead of their use
+          uint4 cur = pre, nxt = pre2;
+          uint32_t e = ep;
+#pragma unroll 1
+          for (;;) {
+            uint4 nn = make_uint4(0x80000000u, 0, 0, 0);
+            if (e + 2 * blockDim.x < e1) nn = __ldg(entries + e + 2 * blockDim.x);
+            pixel(cur);
+            e += blockDim.x;
+            if (e >= e1) break;
+            cur = nxt;
+            nxt = nn;
+          }
+        }
       }
       __syncthreads();  // region of kk-1 is free now: refill it with step kk+2
       if (threadIdx.x == 0 && kk + 2 < k1) issue((kk + 2 - ks) % NR, kk + 2, slice);
@@ -1022,9 +1039,9 @@ cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
   cudaError_t e = prep(k, FS::SMEM);
   if (e) return e;
   CUtensorMap map, tail;
-  e = encode_spectra_map(&map, Yh, d.nrho_pad, NPHI / 2 + 1, batch, FS::S, 256);
+  e = encode_spectra_map(&map, Yh, d.nrho_pad, NPHI / 2 + 1, batch, 2, 256);
   if (e) return e;
-  e = encode_spectra_map(&tail, Yh, d.nrho_pad, NPHI / 2 + 1, batch, FS::S, 1);
+  e = encode_spectra_map(&tail, Yh, d.nrho_pad, NPHI / 2 + 1, batch, 2, 1);
   if (e) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), s);
   if (e) return e;
