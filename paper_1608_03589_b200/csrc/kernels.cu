@@ -559,18 +559,25 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
             if (!dupx) out[(size_t)iyn * n + jxn] = v3;
           }
         };
-        if (ep < e1) {  // entry loads run two pixels ahead of their use
-          uint4 cur = pre, nxt = pre2;
+        if (ep < e1) {  // entry loads run two pixels ahead; three rotating registers, no copies
+          uint4 ea = pre, eb = pre2, ec;
+          const uint32_t stp = blockDim.x;
           uint32_t e = ep;
+          auto fetch = [&](uint4& dst) {
+            dst = make_uint4(0x80000000u, 0, 0, 0);
+            if (e + 2 * stp < e1) dst = __ldg(entries + e + 2 * stp);
+          };
 #pragma unroll 1
           for (;;) {
-            uint4 nn = make_uint4(0x80000000u, 0, 0, 0);
-            if (e + 2 * blockDim.x < e1) nn = __ldg(entries + e + 2 * blockDim.x);
-            pixel(cur);
-            e += blockDim.x;
-            if (e >= e1) break;
-            cur = nxt;
-            nxt = nn;
+            fetch(ec);
+            pixel(ea);
+            if ((e += stp) >= e1) break;
+            fetch(ea);
+            pixel(eb);
+            if ((e += stp) >= e1) break;
+            fetch(eb);
+            pixel(ec);
+            if ((e += stp) >= e1) break;
           }
         }
       }
