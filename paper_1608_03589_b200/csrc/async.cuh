@@ -60,6 +60,12 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes
 }
 
 // ---- cp.async 16 B (L2 only, bypass L1) ----------------------------------------
+// Read-only streaming load that bypasses L1 allocation (keeps small hot tables resident).
+__device__ __forceinline__ float2 ldg_stream_f2(const float2* p) {
+  float2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }

@@ -96,8 +96,9 @@ __host__ __device__ constexpr double sin32(int k) { return cos32(k - 8); }
 
 // e + (c + i s) o as two FFMA2: (e.x + c o.x, e.y + s o.x) + o.y (-s, c)
 __device__ __forceinline__ float2 cfma_const(float2 e, float2 o, float c, float s) {
-  const float2 t = v2fma(pk2(o.x, o.x), pk2(c, s), pk2(e.x, e.y));
-  return v2fma(pk2(o.y, o.y), pk2(-s, c), pk2(t.x, t.y));
+  // e + c o + s (-o.y, o.x): both constants enter as broadcast immediates (no register pairs)
+  const float2 t = v2fma(pk2(o.x, o.y), pk2(c, c), pk2(e.x, e.y));
+  return v2fma(pk2(-o.y, o.x), pk2(s, s), pk2(t.x, t.y));
 }
 // 2 e - p (one FFMA2): the partner output of a butterfly whose first output is p = e + t
 __device__ __forceinline__ float2 ctwice_minus(float2 e, float2 p) {

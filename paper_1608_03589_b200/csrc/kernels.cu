@@ -206,10 +206,10 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
            const float2* __restrict__ tw) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bar;
   float2* buf = smem_k3;                          // padded_len(L)
   float2* p = buf + padded_len(L);                // ns
-  float2* gcol = p + ((ns + 1) & ~1);             // 2 x nt  (16-B aligned)
+  float2* gcol = p + ((ns + 1) & ~1);             // nt (16-B aligned); refilled as soon as the row mix is done
   const int m = blockIdx.x;
   const float sg = (m & 1) ? -1.f : 1.f;
   const int ti = threadIdx.x;
@@ -217,24 +217,18 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   const uint32_t col_bytes = (uint32_t)nt * sizeof(float2);
 
   if (ti == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    mbar_init(&bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (ti == 0) {
-    mbar_arrive_expect_tx(&bars[0], col_bytes);
-    tma_bulk_g2s(gcol, Gh + (size_t)m * nt, col_bytes, &bars[0]);
+    mbar_arrive_expect_tx(&bar, col_bytes);
+    tma_bulk_g2s(gcol, Gh + (size_t)m * nt, col_bytes, &bar);
   }
 
   for (int b = 0; b < batch; ++b) {
-    const int s = b & 1;
-    if (ti == 0 && b + 1 < batch) {  // prefetch the next slice's column into the other buffer
-      mbar_arrive_expect_tx(&bars[s ^ 1], col_bytes);
-      tma_bulk_g2s(gcol + (s ^ 1) * nt, Gh + ((size_t)(b + 1) * nh + m) * nt, col_bytes, &bars[s ^ 1]);
-    }
-    mbar_wait(&bars[s], (b >> 1) & 1);
-    const float2* col = gcol + s * nt;
+    mbar_wait(&bar, b & 1);
+    const float2* col = gcol;
     for (int k = ti; k < ns; k += T) {
       const int2 A = __ldg(ab + k);
       const float4 W = __ldg(wab + k);
@@ -246,6 +240,11 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       p[k] = v;
     }
     __syncthreads();
+    if (ti == 0 && b + 1 < batch) {  // the column is consumed: fetch the next slice's across the transforms
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bar, col_bytes);
+      tma_bulk_g2s(gcol, Gh + ((size_t)(b + 1) * nh + m) * nt, col_bytes, &bar);
+    }
     auto load = [&](int idx) -> float2 {
       if (idx >= nrho) return make_float2(0.f, 0.f);
       const int k = __ldg(ki + idx);
@@ -848,7 +847,7 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
 template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
                       cudaStream_t s) {
-  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + 2 * (size_t)d.nt) * sizeof(float2);
+  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)d.nt) * sizeof(float2);
   // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
   auto k = (2 * d.nrho <= L) ? k_rho_conv<L, true> : k_rho_conv<L, false>;
   cudaError_t e = prep(k, smem);
