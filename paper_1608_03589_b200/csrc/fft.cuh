@@ -227,6 +227,36 @@ __device__ __forceinline__ void apply_twiddles_sfu(float2 (&v)[R], int k) {
   }
 }
 
+// SFU twiddles with a radix-4 split r = 4a + b: w^(4a) and w^b (b < 4) come from
+// the SFU, the rest is one complex product each (error ~2x a single SFU value).
+template <int R, int Ns, bool INV>
+__device__ __forceinline__ void apply_twiddles_sfu4(float2 (&v)[R], int k) {
+  if constexpr (Ns > 1) {
+    constexpr int M = Ns * R;
+    constexpr float kStep = (INV ? 6.283185307179586f : -6.283185307179586f) / (float)M;
+    auto sfu = [&](int r) {
+      int e = (r * k) & (M - 1);
+      e = e > M / 2 ? e - M : e;
+      float sn, cs;
+      __sincosf(kStep * (float)e, &sn, &cs);
+      return make_float2(cs, sn);
+    };
+    float2 wb[4];
+#pragma unroll
+    for (int b = 1; b < 4 && b < R; ++b) {
+      wb[b] = sfu(b);
+      v[b] = cmul(v[b], wb[b]);
+    }
+#pragma unroll
+    for (int a = 1; a < R / 4; ++a) {
+      const float2 wa = sfu(4 * a);
+      v[4 * a] = cmul(v[4 * a], wa);
+#pragma unroll
+      for (int b = 1; b < 4; ++b) v[4 * a + b] = cmul(v[4 * a + b], cmul(wa, wb[b]));
+    }
+  }
+}
+
 // Load the R inputs of butterfly j of a pass from (padded) shared memory.
 // Padded addressing: when the stride between a butterfly's elements is a
 // multiple of 2^S, pad(base + r*stride) = pad(base) + r*(stride + stride/2^S),
@@ -274,7 +304,7 @@ __device__ __forceinline__ void pass_smem(float2* buf, int ti, const float2* __r
   for (int b = 0; b < NB; ++b) {
     const int j = ti + b * T;
     pass_load<N, R, S>(buf, j, v[b]);
-    if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu<R, Ns, INV>(v[b], j % Ns);
+    if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu4<R, Ns, INV>(v[b], j % Ns);
     else apply_twiddles<R, Ns>(v[b], j % Ns, tw);
     Dft<R, INV>::run(v[b]);
   }
@@ -381,7 +411,7 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       pass_load<N, R, S>(buf, j, v[b]);
-      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu<R, Ns, INV>(v[b], j);
+      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu4<R, Ns, INV>(v[b], j);
       else apply_twiddles<R, Ns>(v[b], j, tw + FP::tw_off(P - 1));
       Dft<R, INV>::run(v[b]);
     }
@@ -449,7 +479,7 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       pass_load<N, R, F::S>(buf, j, v[b]);
-      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu<R, Ns, false>(v[b], j);
+      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu4<R, Ns, false>(v[b], j);
       else apply_twiddles<R, Ns>(v[b], j, twf + F::tw_off(P - 1));
       Dft<R, false>::run(v[b]);
 #pragma unroll
@@ -475,7 +505,7 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       pass_load<N, R, B::S>(buf, j, v[b]);
-      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu<R, Ns, true>(v[b], j);
+      if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu4<R, Ns, true>(v[b], j);
       else apply_twiddles<R, Ns>(v[b], j, twi + B::tw_off(P - 1));
       if constexpr (PRUNE) Dft<R, true>::run_low(v[b]);
       else Dft<R, true>::run(v[b]);
