@@ -257,7 +257,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     auto store = [&](int idx, float2 v) {  // rows below row_lo are never read downstream
       if (idx < nrho && idx >= row_lo) ycol[idx] = v;
     };
-    block_conv<L, PRUNE, 64>(buf, ti, tw, load, mul, store, block_sync);  // SFU only for the two large passes
+    block_conv<L, PRUNE, 16>(buf, ti, tw, load, mul, store, block_sync);  // SFU twiddles for every pass
   }
 }
 
