@@ -37,9 +37,9 @@ try:
 except (OSError, ValueError):
     MEASURED = {}
 # dram__bytes_read.sum + dram__bytes_write.sum per slice from the committed ncu --set full
-# capture (profiles/r01b_summary.md, 32-slice launches at 2048^2 FBP)
-TRAFFIC_PER_SLICE = {"rho_conv": (1.212429e9 + 1.996124e9) / 32, "irdft_readout": (3.04e9 + 0.815e9) / 32,
-                     "ramp_filter": (0.536934e9 + 0.496182e9) / 32, "row_rdft": (0.536892e9 + 1.023551e9) / 32}
+# capture (profiles/r01d_summary.md, 32-slice launches at 2048^2 FBP)
+TRAFFIC_PER_SLICE = {"rho_conv": (1.212462e9 + 1.906935e9) / 32, "irdft_readout": (3.017933e9 + 0.816704e9) / 32,
+                     "ramp_filter": (0.536975e9 + 0.497815e9) / 32, "row_rdft": (0.536896e9 + 1.022953e9) / 32}
 UNIT = "slices/s"
 
 
