@@ -21,6 +21,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 #include <utility>
 
 namespace lpbp {
@@ -257,6 +258,16 @@ __device__ __forceinline__ void apply_twiddles_sfu4(float2 (&v)[R], int k) {
   }
 }
 
+// Pass-0 input element r of butterfly j (index j + r*STRIDE).  A loader may take
+// (j, integral_constant<r>) instead of the flat index to specialise on r.
+template <int RIDX, int STRIDE, typename Load>
+__device__ __forceinline__ float2 load_at(Load& load, int j) {
+  if constexpr (std::is_invocable_v<Load&, int, std::integral_constant<int, RIDX>>)
+    return load(j, std::integral_constant<int, RIDX>{});
+  else
+    return load(j + RIDX * STRIDE);
+}
+
 // Load the R inputs of butterfly j of a pass from (padded) shared memory.
 // Padded addressing: when the stride between a butterfly's elements is a
 // multiple of 2^S, pad(base + r*stride) = pad(base) + r*(stride + stride/2^S),
@@ -382,12 +393,10 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
     for (int b = 0; b < NB; ++b) {
       const int j = ti + b * T;
       if constexpr (IN_HALF) {
-#pragma unroll
-        for (int r = 0; r < R / 2; ++r) v[b][r] = load(j + r * (N / R));
+        static_for<0, R / 2>([&](auto rc) { v[b][rc.value] = load_at<rc.value, N / R>(load, j); });
         Dft<R, INV>::run_zu(v[b]);
       } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
+        static_for<0, R>([&](auto rc) { v[b][rc.value] = load_at<rc.value, N / R>(load, j); });
         Dft<R, INV>::run(v[b]);
       }
     }

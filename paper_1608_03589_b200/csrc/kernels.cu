@@ -257,6 +257,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     auto store = [&](int idx, float2 v) {  // rows below row_lo are never read downstream
       if (idx < nrho && idx >= row_lo) ycol[idx] = v;
     };
+    if (ti < nrho_pad - nrho) ycol[nrho + ti] = make_float2(0.f, 0.f);  // padding rows read as zero (K45)
     block_conv<L, PRUNE, 16>(buf, ti, tw, load, mul, store, block_sync);  // SFU twiddles for every pass
   }
 }
@@ -497,24 +498,25 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       float2* H = Q + gi * HALF;
       float* Hf = reinterpret_cast<float*>(H);
       const float2* Qin = Q + gi * FS::IN_PITCH;
-      const int ra = r0 + 2 * gi;
-      const bool va = ra < nrho, vb = ra + 1 < nrho;  // rows past nrho read padding: zero
-      auto load = [&](int idx) -> float2 {
-        const bool hi = idx > NPHI / 2;
-        const int mm = hi ? NPHI - idx : idx;
-        float4 x = *reinterpret_cast<const float4*>(Qin + 2 * mm);  // (Xa, Xb) at mm
-        if (!va) x.x = x.y = 0.f;
-        if (!vb) x.z = x.w = 0.f;
-        float ay = x.y, by = x.w;
-        if (mm == 0 || mm == NPHI / 2) {
-          ay = 0.f;
-          by = 0.f;
+      // packed Z[k] = Xa[k] + i Xb[k], Hermitian extension for k > nphi/2; element r of pass 0
+      // (k = j + r*QS) sits in the low half for r < R0/2.  DC / Nyquist imaginary parts dropped.
+      // Rows in [nrho, nrho_pad) are zero (written by K3), rows past nrho_pad arrive as TMA zero fill.
+      constexpr int R0 = FftPlan<NPHI, true>::radix(0), QS = NPHI / R0;
+      auto load = [&](int j, auto rc) -> float2 {
+        constexpr int r = decltype(rc)::value;
+        if constexpr (r < R0 / 2) {
+          const float4 x = *reinterpret_cast<const float4*>(Qin + 2 * (j + r * QS));
+          float2 z = make_float2(x.x - x.w, x.y + x.z);
+          if constexpr (r == 0)
+            if (j == 0) z = make_float2(x.x, x.z);
+          return z;
+        } else {
+          const float4 x = *reinterpret_cast<const float4*>(Qin + 2 * ((R0 - r) * QS - j));
+          float2 z = make_float2(x.x + x.w, x.z - x.y);
+          if constexpr (r == R0 / 2)
+            if (j == 0) z = make_float2(x.x, x.z);
+          return z;
         }
-        if (hi) {
-          ay = -ay;
-          by = -by;
-        }
-        return make_float2(x.x - by, ay + x.z);
       };
       auto store = [&](int idx, float2 v) {
         Hf[idx] = v.x;

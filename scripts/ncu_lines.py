@@ -22,6 +22,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
 ia, ist, isrc = h.index("Address"), h.index("Warp Stall Sampling (All Samples)"), h.index("Source")
+iex = h.index("Instructions Executed")
 samples = {}
 base = None
 for r in rows[2:]:
@@ -32,7 +33,7 @@ for r in rows[2:]:
     if a in samples:  # the listing repeats itself
         break
     base = a if base is None else min(base, a)
-    samples[a] = (int(r[ist] or 0), r[isrc].strip())
+    samples[a] = (int(r[ist] or 0), r[isrc].strip(), int(r[iex] or 0))
 
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
@@ -60,15 +61,17 @@ for cub in os.listdir(tmp):
     if chain_of:
         break
 
-tot = sum(s for s, _ in samples.values()) or 1
-by_chain = defaultdict(int)
-by_site = defaultdict(int)
-for a, (s, src) in samples.items():
+tot = sum(v[0] for v in samples.values()) or 1
+tex = sum(v[2] for v in samples.values()) or 1
+by_site = defaultdict(lambda: [0, 0])
+for a, (s, src, ex) in samples.items():
     ch = chain_of.get(a - base, "?")
-    by_chain[ch] += s
     parts = ch.split(" <- ")
-    by_site[" <- ".join(parts[-NF:])] += s
-print(f"total samples {tot}, instructions {len(samples)}, mapped {sum(1 for a in samples if a - base in chain_of)}")
-print("-- by outer call site (last NF frames)")
-for k, v in sorted(by_site.items(), key=lambda x: -x[1])[:top]:
-    print(f"{100 * v / tot:5.1f}%  {k}")
+    k = " <- ".join(parts[-NF:])
+    by_site[k][0] += s
+    by_site[k][1] += ex
+print(f"total samples {tot}, warp-instructions executed {tex:.3g}, SASS lines {len(samples)}, "
+      f"mapped {sum(1 for a in samples if a - base in chain_of)}")
+print("-- by outer call site (last NF frames): % of stall samples, % of executed instructions")
+for k, v in sorted(by_site.items(), key=lambda x: -x[1][0])[:top]:
+    print(f"{100 * v[0] / tot:5.1f}%  {100 * v[1] / tex:5.1f}%  {k}")
