@@ -253,6 +253,32 @@ def run_reference(a, d: Dist):
     d.close()
 
 
+def copy_ceiling(host_in, host_out, chunk: int, steps: int, d: Dist) -> float:
+    """Slices/s that PCIe alone allows for the e2e traffic on this box: the same pinned
+    buffers and chunking, H2D on one stream and D2H on another, no compute."""
+    import torch
+    E = host_in.shape[0]
+    din = torch.empty((2, chunk) + tuple(host_in.shape[1:]), dtype=torch.float32, device="cuda")
+    dout = torch.empty((2, chunk) + tuple(host_out.shape[1:]), dtype=torch.float32, device="cuda")
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def once():
+        for i, k in enumerate(range(0, E, chunk)):
+            m = min(chunk, E - k)
+            with torch.cuda.stream(s_in):
+                din[i & 1, :m].copy_(host_in[k:k + m], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                host_out[k:k + m].copy_(dout[i & 1, :m], non_blocking=True)
+        torch.cuda.synchronize()
+
+    once()
+    d.barrier()
+    t = time.perf_counter()
+    for _ in range(steps):
+        once()
+    return d.sum(E * steps) / d.max(time.perf_counter() - t)
+
+
 def run_ours(a, d: Dist):
     import numpy as np
     import torch
@@ -336,6 +362,7 @@ def run_ours(a, d: Dist):
         plan.execute_host(host_in, host_out, chunk=a.e2e_chunk)
     e2e_s = d.max(time.perf_counter() - t)
     e2e_value = d.sum(E * a.e2e_steps) / e2e_s
+    copy_value = copy_ceiling(host_in, host_out, a.e2e_chunk, a.e2e_steps, d)
 
     cpu = None
     if d.rank == 0 and a.gpus == 1 and not a.no_cpu_baseline:
@@ -367,7 +394,9 @@ def run_ours(a, d: Dist):
                          "hbm_equiv_gbs": pipe_bytes * value / d.world / 1e9,
                          "hbm_equiv_frac": pipe_bytes * value / d.world / 1e9 / peak},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": E * nt * nth * 4,
-                    "d2h_bytes_per_step": E * n * n * 4, "slices_per_step": E, "api": "LogPolarPlan.execute_host"},
+                    "d2h_bytes_per_step": E * n * n * 4, "slices_per_step": E, "api": "LogPolarPlan.execute_host",
+                    "copy_ceiling": copy_value, "frac_of_copy_ceiling": e2e_value / copy_value,
+                    "copy_ceiling_note": "same bytes, same chunking, H2D and D2H alone on two streams, no compute"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
