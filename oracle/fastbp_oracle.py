@@ -281,3 +281,143 @@ def relative_l2(a, b) -> float:
 
 def max_abs(a, b) -> float:
     return float(np.max(np.abs(np.asarray(a, dtype=np.float64) - np.asarray(b, dtype=np.float64))))
+
+
+# --------------------------------------------------------------------------
+# sector (partial) backprojection, logpolar.py:153-299
+# --------------------------------------------------------------------------
+
+def sector_masks(ntheta: int, sectors) -> tuple[list[np.ndarray], np.ndarray]:
+    """Extended angular masks of every sector and the coverage count per angle
+    (logpolar.py:238-248): angle j belongs to sector (theta0, beta, a_r) when its
+    distance mod pi to theta0 + beta is <= beta + 2 dtheta (+1e-12)."""
+    dtheta = math.pi / ntheta
+    theta = np.arange(ntheta) * dtheta
+    masks = []
+    for theta0, beta, _ in sectors:
+        c = theta0 + beta
+        dist = np.abs(np.mod(theta - c + math.pi / 2.0, math.pi) - math.pi / 2.0)  # logpolar.py:186-188
+        masks.append(dist <= beta + 2.0 * dtheta + 1e-12)
+    cover = np.sum(masks, axis=0).astype(np.float64)
+    return masks, cover
+
+
+def sector_validate(sectors, n_out: int, ntheta: int) -> None:
+    """Argument checks of partial_backproject (logpolar.py:218-227, 242-246)."""
+    if n_out < 2:
+        raise ValueError("n_out must be >= 2")
+    if not sectors:
+        raise ValueError("at least one sector is required")
+    for _, beta, a_r in sectors:
+        if not (0.0 < beta <= math.pi / 2.0):
+            raise ValueError("sector half-width beta must lie in (0, pi/2]")
+        if not (0.0 < a_r < 0.5):
+            raise ValueError("sector rescale a_r must lie in (0, 1/2)")
+    _, cover = sector_masks(ntheta, sectors)
+    if np.any(cover == 0):
+        th = (np.arange(ntheta) * (math.pi / ntheta))[cover == 0][0]
+        raise ValueError(f"sectors do not cover the angle range: theta = {th:.4f} uncovered")
+
+
+def sector_geometry(nt: int, ntheta: int, n_out: int, theta0: float, beta: float, a_r: float):
+    """(jc, theta_c, rho0_s, nrho_s) of one sector: centre snapped to the angle grid,
+    mesh depth from the support of the shifted, shrunk sector (logpolar.py:254-283)."""
+    dtheta = math.pi / ntheta
+    jc = int(round((theta0 + beta) / dtheta))
+    ext = 2.0 * dtheta
+    support_min = (1.0 - a_r) * math.cos(min(beta + ext, math.pi / 2.0)) - a_r
+    if support_min > 0.05:
+        rho0_s = min(math.log(support_min), math.log(1.0 - 2.0 * a_r)) - 0.2
+    else:
+        rho0_s = math.log(a_r) + adaptive_rho0(n_out, n_out)
+    nrho_s = mesh_for(nt // 2, rho0_s, None)
+    return jc, jc * dtheta, rho0_s, nrho_s
+
+
+def sector_sinogram(g: np.ndarray, jc: int, weights_rot: np.ndarray, a_r: float) -> np.ndarray:
+    """Working-frame sinogram of one sector: angles rolled by jc with the t-flip for
+    columns that wrap past pi (logpolar.py:153-172), per-angle weights, support
+    shrunk by a_r (out(t) = a_r g(t/a_r), :175-179) and shifted by (1 - a_r, 0)
+    (radon.py:137-158: out(t, theta) = g(t - (1 - a_r) cos theta))."""
+    g = np.asarray(g, dtype=np.float64)
+    nt, nth = g.shape
+    shift = jc % nth
+    rolled = np.empty_like(g)
+    for j in range(nth):
+        src = j + shift
+        col = g[:, src % nth]
+        if src >= nth:
+            col = np.concatenate([[0.0], col[:0:-1]])  # g(-t): t_0 = -1 maps off-grid to +1
+        rolled[:, j] = col
+    rolled = rolled * weights_rot[None, :]
+    dt = 2.0 / nt
+    t = -1.0 + np.arange(nt) * dt
+    scaled = a_r * lerp_rows(rolled, np.broadcast_to(((t / a_r + 1.0) / dt)[:, None], (nt, nth)).copy())
+    off = (1.0 - a_r) * np.cos(np.arange(nth) * (math.pi / nth))
+    return lerp_rows(scaled, (t[:, None] - off[None, :] + 1.0) / dt)
+
+
+def sector_weights_rot(ntheta: int, sectors, k: int) -> np.ndarray:
+    """Weights of sector k in its rotated frame: extended mask / coverage
+    (logpolar.py:263-268)."""
+    masks, cover = sector_masks(ntheta, sectors)
+    theta0, beta, _ = sectors[k]
+    jc = int(round((theta0 + beta) / (math.pi / ntheta)))
+    rot = (np.arange(ntheta) + jc) % ntheta
+    w = np.zeros(ntheta)
+    w[masks[k][rot]] = 1.0
+    return w / cover[rot]
+
+
+def lp_sample(lp: np.ndarray, rho0: float, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Bilinear log-polar sample at arbitrary points with the readout's boundary rules
+    (logpolar.py:191-215)."""
+    nrho, nphi = lp.shape
+    drho = -rho0 / nrho
+    dphi = 2.0 * math.pi / nphi
+    r = np.hypot(x, y)
+    out = np.zeros_like(r)
+    sel = (r <= 1.0) & (r > 0.0)
+    if not sel.any():
+        return out
+    rho = np.log(r[sel])
+    fi = (rho - rho0) / drho - 1.0
+    fi = np.where((fi >= -1.0) & (fi < 0.0), 0.0, fi)
+    fi = np.clip(fi, 0.0, nrho - 1.0)
+    fj = np.mod(np.arctan2(y[sel], x[sel]), 2.0 * math.pi) / dphi
+    i0 = np.floor(fi).astype(np.int64)
+    wi = fi - i0
+    i1 = np.minimum(i0 + 1, nrho - 1)
+    j0 = np.floor(fj).astype(np.int64) % nphi
+    wj = fj - np.floor(fj)
+    j1 = (j0 + 1) % nphi
+    val = ((lp[i0, j0] * (1 - wi) + lp[i1, j0] * wi) * (1 - wj)
+           + (lp[i0, j1] * (1 - wi) + lp[i1, j1] * wi) * wj)
+    out[sel] = np.where(rho >= rho0, val, 0.0)
+    return out
+
+
+def partial_backproject(g: np.ndarray, sectors, n_out: int, return_stages: bool = False):
+    """Sector-wise log-polar backprojection (logpolar.py:210-299): every sector's
+    working-frame sinogram goes through the log-polar stage on its own shallow mesh,
+    is read back at x_w = (1 - a_r, 0) + a_r R(-theta_c) x and divided by a_r; the
+    sector results are summed."""
+    g = np.asarray(g, dtype=np.float64)
+    nt, nth = g.shape
+    sectors = [tuple(map(float, s)) for s in sectors]
+    sector_validate(sectors, n_out, nth)
+    xs = -1.0 + (np.arange(n_out) + 0.5) * (2.0 / n_out)
+    X, Y = np.meshgrid(xs, xs)
+    acc = np.zeros((n_out, n_out))
+    stages = []
+    for k, (theta0, beta, a_r) in enumerate(sectors):
+        jc, theta_c, rho0_s, nrho_s = sector_geometry(nt, nth, n_out, theta0, beta, a_r)
+        gs = sector_sinogram(g, jc, sector_weights_rot(nth, sectors, k), a_r)
+        lp = lp_convolve(logpolar_resample(semipolar(gs), rho0_s, nrho_s), -rho0_s / nrho_s)
+        ct, st = math.cos(theta_c), math.sin(theta_c)
+        xw = (1.0 - a_r) + a_r * (ct * X + st * Y)
+        yw = a_r * (-st * X + ct * Y)
+        acc += lp_sample(lp, rho0_s, xw, yw) / a_r
+        if return_stages:
+            stages.append({"jc": jc, "rho0": rho0_s, "nrho": nrho_s, "sino": gs, "lp": lp})
+    return (acc, stages) if return_stages else acc

@@ -33,7 +33,81 @@ def lp_stage(g: np.ndarray, n: int):
     return _logpolar_convolve(fb.sinogram_to_semipolar(s), rho0, nrho).values
 
 
+def sector_goldens() -> None:
+    """partial_backproject (logpolar.py:210-299) on seeded inputs, with the stage
+    intermediates of one sector from the reference's own helpers."""
+    import warnings
+
+    from fastbp.logpolar import _rescale_support, _roll_angles, partial_backproject
+    from fastbp.radon import shift_sinogram
+
+    cases = {
+        "a": (phantoms.sinogram(101, 256, 180, 10, 0.05, 0.35, 0.0), 128,
+              [(k * math.pi / 4, math.pi / 8, 0.25) for k in range(4)]),
+        "b": (phantoms.sinogram(102, 256, 256, 10, 0.05, 0.35, 0.01), 256, [(0.0, math.pi / 2, 0.25)]),
+        "c": (phantoms.config_sinogram(0), 256,
+              [(0.3, math.pi / 6, 0.2), (0.3 + math.pi / 3, math.pi / 6, 0.3), (0.3 + 2 * math.pi / 3, math.pi / 6, 0.35)]),
+    }
+    arrays = {}
+    kat = {}
+    for key, (g, n, sectors) in cases.items():
+        g = g.astype(np.float32).astype(np.float64)
+        s = fb.Sinogram(*g.shape, g)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            pb = partial_backproject(s, sectors, n).values
+        arrays[f"{key}_sino"] = g.astype(np.float32)
+        arrays[f"{key}_sectors"] = np.asarray(sectors, dtype=np.float64)
+        arrays[f"{key}_n"] = np.asarray(n)
+        arrays[f"{key}_pb"] = pb
+        # stage intermediates of sector 0: rotated/weighted/shrunk/shifted sinogram and its log-polar image
+        theta0, beta, a_r = sectors[0]
+        dth = math.pi / g.shape[1]
+        jc = int(round((theta0 + beta) / dth))
+        theta = np.arange(g.shape[1]) * dth
+        masks = [np.abs(np.mod(theta - (t0 + b) + math.pi / 2, math.pi) - math.pi / 2) <= b + 2 * dth + 1e-12
+                 for t0, b, _ in sectors]
+        cover = np.sum(masks, axis=0).astype(np.float64)
+        rot = (np.arange(g.shape[1]) + jc) % g.shape[1]
+        w = np.zeros(g.shape[1])
+        w[masks[0][rot]] = 1.0
+        w /= cover[rot]
+        gr = _roll_angles(s, jc)
+        gr = fb.Sinogram(gr.nt, gr.ntheta, gr.values * w[None, :])
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            gsh = shift_sinogram(_rescale_support(gr, a_r), (1.0 - a_r, 0.0)).values
+        support_min = (1.0 - a_r) * math.cos(min(beta + 2 * dth, math.pi / 2)) - a_r
+        rho0_s = (min(math.log(support_min), math.log(1 - 2 * a_r)) - 0.2 if support_min > 0.05
+                  else math.log(a_r) + fb.adaptive_rho0(n, n))
+        nrho_s = _mesh_for(g.shape[0] // 2, rho0_s, None)
+        lp0 = _logpolar_convolve(fb.sinogram_to_semipolar(fb.Sinogram(*gsh.shape, gsh)), rho0_s, nrho_s).values
+        arrays[f"{key}_sec0_sino"] = gsh
+        arrays[f"{key}_sec0_lp"] = lp0
+        kat[f"sector_{key}"] = {"jc0": jc, "rho0_0": rho0_s, "nrho_0": nrho_s}
+        if key == "a":  # the reference's own sector experiment (scratch_fbp.py:33-49), on this seeded phantom
+            nv = fb.backproject_naive(s, n).values
+            lp = fb.logpolar_backproject(s, n).values
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                pb1 = partial_backproject(s, [(0.0, math.pi / 2, 0.25)], n).values
+            xs = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+            R = np.hypot(*np.meshgrid(xs, xs))
+            m = (R > 2 * math.exp(fb.adaptive_rho0(n, n))) & (R <= 1.0)
+            kat["sector_a"]["annulus_vs_naive"] = float(np.linalg.norm(pb[m] - nv[m]) / np.linalg.norm(nv[m]))
+            kat["sector_a"]["single_vs_lp"] = float(np.linalg.norm(pb1[m] - lp[m]) / np.linalg.norm(lp[m]))
+            arrays["a_single_pb"] = pb1
+    np.savez_compressed(os.path.join(HERE, "sector.npz"), **arrays)
+    with open(os.path.join(HERE, "kat_sector.json"), "w") as f:
+        json.dump(kat, f, indent=1, sort_keys=True)
+
+
 def main() -> None:
+    if "--only-sector" in sys.argv:
+        sector_goldens()
+        print("wrote sector goldens")
+        return
+    sector_goldens()
     out = {}
     # config 0: BP 256x256 -> 256 (BASELINE.json configs[0])
     g0 = phantoms.config_sinogram(0).astype(np.float64)

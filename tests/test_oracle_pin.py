@@ -106,3 +106,73 @@ def test_against_reference_directly(reference):
     lp = fb.semipolar_to_logpolar(p, -3.0, 300)
     assert np.abs(O.logpolar_resample(p.values, -3.0, 300) - lp.values).max() == 0.0
     assert np.abs(O.lp_readout(lp.values, -3.0, 50, 50) - fb.logpolar_to_cartesian(lp, 50, 50).values).max() < 1e-15
+
+
+# ---- sector (partial) backprojection, logpolar.py:153-299 ----
+
+def _sector_case(z, key):
+    return (z[f"{key}_sino"].astype(np.float64), [tuple(s) for s in z[f"{key}_sectors"]], int(z[f"{key}_n"]))
+
+
+@pytest.mark.parametrize("key", ["a", "b", "c"])
+def test_sector_backprojection(golden, key):
+    z = golden("sector.npz")
+    g, sectors, n = _sector_case(z, key)
+    out, stages = O.partial_backproject(g, sectors, n, return_stages=True)
+    assert rel(out, z[f"{key}_pb"]) < TOL
+    assert rel(stages[0]["sino"], z[f"{key}_sec0_sino"]) < TOL
+    assert rel(stages[0]["lp"], z[f"{key}_sec0_lp"]) < TOL
+    with open(os.path.join(GOLDEN, "kat_sector.json")) as f:
+        kat = json.load(f)[f"sector_{key}"]
+    assert (stages[0]["jc"], stages[0]["rho0"], stages[0]["nrho"]) == (kat["jc0"], kat["rho0_0"], kat["nrho_0"])
+
+
+def test_sector_known_answers(golden):
+    """The reference's own sector experiment (scratch_fbp.py:33-49) on the seeded phantom of case a."""
+    z = golden("sector.npz")
+    g, sectors, n = _sector_case(z, "a")
+    with open(os.path.join(GOLDEN, "kat_sector.json")) as f:
+        kat = json.load(f)["sector_a"]
+    xs = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+    R = np.hypot(*np.meshgrid(xs, xs))
+    m = (R > 2 * math.exp(O.adaptive_rho0(n, n))) & (R <= 1.0)
+    pb = O.partial_backproject(g, sectors, n)
+    nv = O.backproject_naive(g, n)
+    assert abs(np.linalg.norm(pb[m] - nv[m]) / np.linalg.norm(nv[m]) - kat["annulus_vs_naive"]) < 1e-12
+    pb1 = O.partial_backproject(g, [(0.0, math.pi / 2, 0.25)], n)
+    assert rel(pb1, z["a_single_pb"]) < TOL
+    lp = O.logpolar_backproject(g, n)
+    assert abs(np.linalg.norm(pb1[m] - lp[m]) / np.linalg.norm(lp[m]) - kat["single_vs_lp"]) < 1e-12
+
+
+def test_sector_errors_match_reference():
+    g = np.ones((64, 32))
+    with pytest.raises(ValueError, match="n_out must be >= 2"):
+        O.partial_backproject(g, [(0.0, math.pi / 2, 0.25)], 1)
+    with pytest.raises(ValueError, match="at least one sector is required"):
+        O.partial_backproject(g, [], 16)
+    with pytest.raises(ValueError, match=r"sector half-width beta must lie in \(0, pi/2\]"):
+        O.partial_backproject(g, [(0.0, 2.0, 0.25)], 16)
+    with pytest.raises(ValueError, match=r"sector rescale a_r must lie in \(0, 1/2\)"):
+        O.partial_backproject(g, [(0.0, 1.0, 0.5)], 16)
+    with pytest.raises(ValueError, match="sectors do not cover the angle range: theta = 1.6690 uncovered"):
+        O.partial_backproject(g, [(0.0, 0.7, 0.25)], 16)
+
+
+def test_sector_against_reference_directly(reference):
+    import warnings
+
+    from fastbp.logpolar import partial_backproject
+    fb = reference
+    rng = np.random.default_rng(11)
+    g = rng.standard_normal((128, 96)).cumsum(0) * 0.01
+    sectors = [(0.1, 0.6, 0.3), (1.3, 0.5, 0.2), (2.2, 0.6, 0.4)]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = partial_backproject(fb.Sinogram(*g.shape, g), sectors, 70).values
+    assert rel(O.partial_backproject(g, sectors, 70), ref) < TOL
+    with pytest.raises(ValueError) as e_ref:
+        partial_backproject(fb.Sinogram(64, 32, np.ones((64, 32))), [(0.0, 0.7, 0.25)], 16)
+    with pytest.raises(ValueError) as e_or:
+        O.partial_backproject(np.ones((64, 32)), [(0.0, 0.7, 0.25)], 16)
+    assert str(e_ref.value) == str(e_or.value)
