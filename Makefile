@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O3 -Xptxas -v
 SRC := paper_1608_03589_b200/csrc
 LIB := paper_1608_03589_b200/liblpbp.so
-OBJS := build/kernels.o build/capi.o build/plan_host.o
+OBJS := build/kernels.o build/sector_kernels.o build/capi.o build/plan_host.o build/sector_host.o
 
 all: $(LIB)
 
@@ -12,7 +12,7 @@ build/%.o: $(SRC)/%.cu $(SRC)/*.cuh include/lpbp.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
 
-build/plan_host.o: $(SRC)/plan_host.cpp $(SRC)/plan_host.h
+build/%.o: $(SRC)/%.cpp $(SRC)/*.h
 	@mkdir -p build
 	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC,-O3 -c $< -o $@
 

@@ -120,6 +120,51 @@ int lpbp_profile_read(lpbp_plan* plan, double* stage_ms, int64_t* stage_launches
 int lpbp_radon_ellipses(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch,
                         float* out_dev, void* stream);
 
+/* ---- sector (partial) backprojection: partial_backproject(g, sectors, n_out), logpolar.py:210-299 ----
+ * Each sector (theta0, beta, a_r) covers ray angles [theta0, theta0 + 2 beta] mod pi.  Its
+ * working-frame sinogram (angles rolled to the sector centre with the t-flip past pi,
+ * mask / coverage weights, support shrunk by a_r and shifted by 1 - a_r; logpolar.py:153-179,
+ * 260-271, radon.py:137-158) runs through the log-polar stage on the sector's own shallow mesh
+ * (logpolar.py:272-287); the sector images are sampled at x_w = (1 - a_r, 0) + a_r R(-theta_c) x,
+ * divided by a_r and summed (logpolar.py:289-297).  Validation returns LPBP_EINVAL with the
+ * reference's ValueError messages.  No filtering (the reference does not filter here). */
+typedef struct lpbp_sector_plan lpbp_sector_plan;
+
+typedef struct lpbp_sector {
+  double theta0; /* first ray angle of the sector */
+  double beta;   /* half-width, (0, pi/2]          */
+  double a_r;    /* rescale, (0, 1/2)              */
+} lpbp_sector;
+
+typedef struct lpbp_sector_info {
+  int32_t jc;          /* centre angle index round((theta0 + beta) / dtheta)      */
+  int32_t nrho;        /* sector mesh rows (_mesh_for(ns, rho0, None))            */
+  int32_t L;           /* rho FFT length of the sector's log-polar stage          */
+  int32_t nphi;        /* 2 * ntheta                                              */
+  double theta_c;      /* jc * dtheta                                             */
+  double rho0;         /* sector mesh depth (logpolar.py:279-283)                 */
+  double drho;         /* -rho0 / nrho                                            */
+  double support_min;  /* logpolar.py:278                                         */
+  double a_r;
+  size_t table_bytes;  /* device bytes of this sector's constant tables           */
+} lpbp_sector_info;
+
+int lpbp_sector_plan_create(int32_t nt, int32_t ntheta, int32_t n_out, const lpbp_sector* sectors,
+                            int32_t nsectors, int32_t device, lpbp_sector_plan** plan);
+void lpbp_sector_plan_destroy(lpbp_sector_plan* plan);
+int lpbp_sector_get_info(const lpbp_sector_plan* plan, int32_t index, lpbp_sector_info* info);
+/* Workspace for `chunk` slices in flight (256-byte aligned). */
+int lpbp_sector_workspace_bytes(const lpbp_sector_plan* plan, int32_t chunk, size_t* bytes);
+/* sino [batch][nt][ntheta] -> img [batch][n][n]; ws NULL = plan-owned workspace (calls serialise). */
+int lpbp_sector_execute(lpbp_sector_plan* plan, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
+                        size_t ws_bytes, void* stream);
+/* Stage: sector `index`'s working-frame sinogram [batch][nt][ntheta]. */
+int lpbp_sector_prepare(const lpbp_sector_plan* plan, int32_t index, const float* sino_dev, float* out_dev,
+                        int32_t batch, void* stream);
+/* Stage: the log-polar stage of sector `index` on a working-frame sinogram -> [batch][nrho][nphi]. */
+int lpbp_sector_logpolar(const lpbp_sector_plan* plan, int32_t index, const float* work_dev, float* lp_dev,
+                         int32_t batch, void* stream);
+
 /* Number of kernel launches the last lpbp_execute/lpbp_execute_host issued on the calling thread. */
 int64_t lpbp_last_launch_count(void);
 

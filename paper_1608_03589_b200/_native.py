@@ -48,6 +48,18 @@ class PlanInfo(ctypes.Structure):
     ]
 
 
+class Sector(ctypes.Structure):
+    _fields_ = [("theta0", c_double), ("beta", c_double), ("a_r", c_double)]
+
+
+class SectorInfo(ctypes.Structure):
+    _fields_ = [
+        ("jc", c_int32), ("nrho", c_int32), ("L", c_int32), ("nphi", c_int32),
+        ("theta_c", c_double), ("rho0", c_double), ("drho", c_double), ("support_min", c_double),
+        ("a_r", c_double), ("table_bytes", c_size_t),
+    ]
+
+
 # symbol -> (restype, argtypes); exactly the functions declared in include/lpbp.h
 SIGNATURES = {
     "lpbp_plan_create": (c_int32, [POINTER(Params), POINTER(c_void_p)]),
@@ -65,6 +77,14 @@ SIGNATURES = {
     "lpbp_profile_enable": (c_int32, [c_void_p, c_int32]),
     "lpbp_profile_read": (c_int32, [c_void_p, POINTER(ctypes.c_double), POINTER(c_int64), POINTER(c_int64), c_int32]),
     "lpbp_radon_ellipses": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
+    "lpbp_sector_plan_create": (c_int32, [c_int32, c_int32, c_int32, POINTER(Sector), c_int32, c_int32,
+                                          POINTER(c_void_p)]),
+    "lpbp_sector_plan_destroy": (None, [c_void_p]),
+    "lpbp_sector_get_info": (c_int32, [c_void_p, c_int32, POINTER(SectorInfo)]),
+    "lpbp_sector_workspace_bytes": (c_int32, [c_void_p, c_int32, POINTER(c_size_t)]),
+    "lpbp_sector_execute": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
+    "lpbp_sector_prepare": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
+    "lpbp_sector_logpolar": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
     "lpbp_last_launch_count": (c_int64, []),
     "lpbp_last_error": (c_char_p, []),
     "lpbp_version": (c_int32, []),

@@ -12,6 +12,7 @@
 #include "../../include/lpbp.h"
 #include "kernels.cuh"
 #include "plan_host.h"
+#include "sector_kernels.cuh"
 
 using lpbp::DevTables;
 using lpbp::Dims;
@@ -636,6 +637,233 @@ int lpbp_radon_ellipses(const double* params_dev, int32_t k, int32_t nt, int32_t
                                               static_cast<cudaStream_t>(stream));
   if (e) return cuda_fail(e, "radon_ellipses");
   return LPBP_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// sector (partial) backprojection
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct lpbp_sector_plan {
+  lpbp::SectorSetHost h;
+  std::vector<lpbp_plan*> sub;  // per-sector log-polar stage (explicit rho0, no filter)
+  std::vector<const lpbp::SectorCol*> cols;
+  std::vector<const lpbp::SectorRow*> rows;
+  std::vector<size_t> own_table_bytes;
+  std::vector<void*> allocs;
+  int device = 0;
+  std::mutex mu;
+  void* own_ws = nullptr;
+  size_t own_ws_bytes = 0;
+  ~lpbp_sector_plan() {
+    DeviceGuard g(device);
+    for (auto* p : sub) delete p;
+    for (void* p : allocs) cudaFree(p);
+    if (own_ws) cudaFree(own_ws);
+  }
+};
+
+namespace {
+
+size_t sector_ws_bytes(const lpbp_sector_plan* P, int chunk) {
+  const auto& h = P->h;
+  size_t sub = 0, lp = 0;
+  for (size_t s = 0; s < P->sub.size(); ++s) {
+    sub = std::max(sub, ws_bytes_for(P->sub[s], chunk));
+    lp += align256((size_t)chunk * P->sub[s]->d.nrho * P->sub[s]->d.nphi * sizeof(float));
+  }
+  return align256((size_t)chunk * h.nt * h.ntheta * sizeof(float)) + lp + sub;
+}
+
+int sector_chunk(const lpbp_sector_plan* P, const float* in, float* out, int c, char* ws, cudaStream_t st) {
+  const auto& h = P->h;
+  float* work = reinterpret_cast<float*>(ws);
+  char* cur = ws + align256((size_t)c * h.nt * h.ntheta * sizeof(float));
+  lpbp::SectorArgs args{};
+  const int nsec = (int)P->sub.size();
+  for (int s = 0; s < nsec; ++s) {
+    const lpbp_plan* S = P->sub[s];
+    auto& a = args.s[s];
+    a.lp = reinterpret_cast<const float*>(cur);
+    a.lp_slice = (long long)S->d.nrho * S->d.nphi;
+    a.nrho = S->d.nrho;
+    a.rho0 = S->h.rho0;
+    a.drho = S->h.drho;
+    a.ct = std::cos(h.sec[s].theta_c);
+    a.st = std::sin(h.sec[s].theta_c);
+    a.a_r = h.sec[s].spec.a_r;
+    a.inv_a = (float)(1.0 / h.sec[s].spec.a_r);
+    cur += align256((size_t)c * S->d.nrho * S->d.nphi * sizeof(float));
+  }
+  char* subws = cur;
+  for (int s = 0; s < nsec; ++s) {
+    cudaError_t e = lpbp::launch_sector_prep(in, work, h.nt, h.ntheta, c, P->cols[s], P->rows[s],
+                                             h.sec[s].spec.a_r, st);
+    if (e) return launch_fail(e, "sector_prep");
+    ++g_launches;
+    int rc = run_chunk(P->sub[s], work, nullptr, c, subws, st, true, const_cast<float*>(args.s[s].lp));
+    if (rc) return rc;
+  }
+  cudaError_t e = lpbp::launch_sector_readout(args, nsec, out, h.n, 2 * h.ntheta, c, st);
+  if (e) return launch_fail(e, "sector_readout");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lpbp_sector_plan_create(int32_t nt, int32_t ntheta, int32_t n_out, const lpbp_sector* sectors,
+                            int32_t nsectors, int32_t device, lpbp_sector_plan** plan) {
+  g_last_error.clear();
+  if (!plan || nsectors < 0 || (nsectors > 0 && !sectors)) return fail(LPBP_EINVAL, "invalid argument");
+  *plan = nullptr;
+  if (nsectors > lpbp::kMaxSectors)
+    return fail(LPBP_EINVAL, "at most " + std::to_string(lpbp::kMaxSectors) + " sectors per plan");
+  std::vector<lpbp::SectorSpec> specs;
+  for (int i = 0; i < nsectors; ++i) specs.push_back({sectors[i].theta0, sectors[i].beta, sectors[i].a_r});
+  auto* P = new (std::nothrow) lpbp_sector_plan();
+  if (!P) return fail(LPBP_ENOMEM, "host allocation failed");
+  std::string err = lpbp::build_sector_set(nt, ntheta, n_out, specs, P->h);
+  if (!err.empty()) {
+    delete P;
+    return fail(LPBP_EINVAL, err);
+  }
+  P->device = device;
+  for (const auto& S : P->h.sec) {
+    lpbp_params sp{};
+    sp.nt = nt;
+    sp.ntheta = ntheta;
+    sp.n_out = 2;  // the sub-plan's own Cartesian readout is never used
+    sp.has_rho0 = 1;
+    sp.rho0 = S.rho0;
+    sp.nrho = S.nrho;
+    sp.filter = 0;
+    sp.device = device;
+    lpbp_plan* sub = nullptr;
+    int rc = lpbp_plan_create(&sp, &sub);
+    if (rc) {
+      std::string msg = g_last_error;
+      delete P;
+      return fail(rc, msg);
+    }
+    P->sub.push_back(sub);
+  }
+  if (device >= 0) {
+    DeviceGuard g(device);
+    for (const auto& S : P->h.sec) {
+      void *c = nullptr, *r = nullptr;
+      const size_t cb = S.cols.size() * sizeof(lpbp::SectorCol), rb = S.rows.size() * sizeof(lpbp::SectorRow);
+      cudaError_t e = cudaMalloc(&c, cb);
+      if (e == cudaSuccess) P->allocs.push_back(c);
+      if (e == cudaSuccess) e = cudaMalloc(&r, rb);
+      if (e == cudaSuccess) P->allocs.push_back(r);
+      if (e == cudaSuccess) e = cudaMemcpy(c, S.cols.data(), cb, cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = cudaMemcpy(r, S.rows.data(), rb, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) {
+        delete P;
+        return cuda_fail(e, "sector tables");
+      }
+      P->cols.push_back(static_cast<const lpbp::SectorCol*>(c));
+      P->rows.push_back(static_cast<const lpbp::SectorRow*>(r));
+      P->own_table_bytes.push_back(cb + rb);
+    }
+  } else {
+    P->own_table_bytes.assign(P->h.sec.size(), 0);
+  }
+  *plan = P;
+  return LPBP_OK;
+}
+
+void lpbp_sector_plan_destroy(lpbp_sector_plan* plan) { delete plan; }
+
+int lpbp_sector_get_info(const lpbp_sector_plan* P, int32_t index, lpbp_sector_info* info) {
+  if (!P || !info || index < 0 || index >= (int)P->sub.size()) return fail(LPBP_EINVAL, "invalid argument");
+  const auto& S = P->h.sec[index];
+  const lpbp_plan* sub = P->sub[index];
+  info->jc = S.jc;
+  info->nrho = sub->h.nrho;
+  info->L = sub->h.L;
+  info->nphi = sub->h.nphi;
+  info->theta_c = S.theta_c;
+  info->rho0 = sub->h.rho0;
+  info->drho = sub->h.drho;
+  info->support_min = S.support_min;
+  info->a_r = S.spec.a_r;
+  info->table_bytes = sub->table_bytes + P->own_table_bytes[index];
+  return LPBP_OK;
+}
+
+int lpbp_sector_workspace_bytes(const lpbp_sector_plan* P, int32_t chunk, size_t* bytes) {
+  if (!P || !bytes || chunk < 1) return fail(LPBP_EINVAL, "invalid argument");
+  *bytes = sector_ws_bytes(P, chunk);
+  return LPBP_OK;
+}
+
+int lpbp_sector_execute(lpbp_sector_plan* P, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
+                        size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !img_dev) return fail(LPBP_EINVAL, "invalid argument");
+  if (ws && reinterpret_cast<uintptr_t>(ws) % 256) return fail(LPBP_EINVAL, "workspace must be 256-byte aligned");
+  DeviceGuard g(P->device);
+  std::unique_lock<std::mutex> lock(P->mu, std::defer_lock);
+  if (!ws) {
+    lock.lock();
+    const size_t need = sector_ws_bytes(P, std::max(1, std::min((int)batch, 8)));
+    if (P->own_ws_bytes < need) {
+      if (P->own_ws) cudaFree(P->own_ws);
+      P->own_ws = nullptr;
+      P->own_ws_bytes = 0;
+      cudaError_t e = cudaMalloc(&P->own_ws, need);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(sector workspace)");
+      P->own_ws_bytes = need;
+    }
+    ws = P->own_ws;
+    ws_bytes = P->own_ws_bytes;
+  }
+  int chunk = 1;
+  while (chunk < batch && sector_ws_bytes(P, chunk + 1) <= ws_bytes) ++chunk;
+  if (sector_ws_bytes(P, chunk) > ws_bytes)
+    return fail(LPBP_EINVAL, "workspace too small for one slice (need " + std::to_string(sector_ws_bytes(P, 1)) +
+                                 " bytes)");
+  const size_t in_slice = (size_t)P->h.nt * P->h.ntheta, out_slice = (size_t)P->h.n * P->h.n;
+  int64_t launches = 0;
+  for (int off = 0; off < batch; off += chunk) {
+    const int c = std::min(chunk, batch - off);
+    int rc = sector_chunk(P, sino_dev + off * in_slice, img_dev + off * out_slice, c, static_cast<char*>(ws),
+                          static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    launches += g_launches;
+    g_launches = 0;
+  }
+  g_launches = launches;
+  return LPBP_OK;
+}
+
+int lpbp_sector_prepare(const lpbp_sector_plan* P, int32_t index, const float* sino_dev, float* out_dev,
+                        int32_t batch, void* stream) {
+  g_launches = 0;
+  if (!P || batch < 0 || index < 0 || index >= (int)P->sub.size()) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !out_dev) return fail(LPBP_EINVAL, "invalid argument");
+  DeviceGuard g(P->device);
+  cudaError_t e = lpbp::launch_sector_prep(sino_dev, out_dev, P->h.nt, P->h.ntheta, batch, P->cols[index],
+                                           P->rows[index], P->h.sec[index].spec.a_r, static_cast<cudaStream_t>(stream));
+  if (e) return launch_fail(e, "sector_prep");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+int lpbp_sector_logpolar(const lpbp_sector_plan* P, int32_t index, const float* work_dev, float* lp_dev,
+                         int32_t batch, void* stream) {
+  if (!P || index < 0 || index >= (int)P->sub.size()) return fail(LPBP_EINVAL, "invalid argument");
+  return lpbp_logpolar(P->sub[index], work_dev, lp_dev, batch, nullptr, 0, stream);
 }
 
 int64_t lpbp_last_launch_count(void) { return g_launches; }

@@ -25,6 +25,7 @@ __all__ = [
     "logpolar_backproject_batch",
     "logpolar_convolve",
     "mesh_for",
+    "partial_backproject",
 ]
 
 LOGPOLAR_SCALE = 0.5  # logpolar.py:47 (folded into the plan's kernel spectrum)
@@ -96,3 +97,9 @@ def logpolar_convolve(g: Sinogram, n_out: int, opts: LogPolarOptions | None = No
     plan = plan_for(g.nt, g.ntheta, n_out, opts)
     lp = plan.logpolar(_to_device(g))
     return LogPolarImage(plan.nrho, plan.nphi, plan.rho0, lp[0].double().cpu().numpy())
+
+
+def partial_backproject(g: Sinogram, sectors, n_out: int) -> CartesianImage:
+    """fastbp.logpolar.partial_backproject (logpolar.py:210-299); see sector.py."""
+    from .sector import partial_backproject as _pb
+    return _pb(g, sectors, n_out)

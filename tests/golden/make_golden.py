@@ -53,9 +53,10 @@ def sector_goldens() -> None:
     for key, (g, n, sectors) in cases.items():
         g = g.astype(np.float32).astype(np.float64)
         s = fb.Sinogram(*g.shape, g)
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore")
+        with warnings.catch_warnings(record=True) as caught:
+            warnings.simplefilter("always")
             pb = partial_backproject(s, sectors, n).values
+        n_warn = sum(1 for w in caught if issubclass(w.category, RuntimeWarning))
         arrays[f"{key}_sino"] = g.astype(np.float32)
         arrays[f"{key}_sectors"] = np.asarray(sectors, dtype=np.float64)
         arrays[f"{key}_n"] = np.asarray(n)
@@ -84,7 +85,7 @@ def sector_goldens() -> None:
         lp0 = _logpolar_convolve(fb.sinogram_to_semipolar(fb.Sinogram(*gsh.shape, gsh)), rho0_s, nrho_s).values
         arrays[f"{key}_sec0_sino"] = gsh
         arrays[f"{key}_sec0_lp"] = lp0
-        kat[f"sector_{key}"] = {"jc0": jc, "rho0_0": rho0_s, "nrho_0": nrho_s}
+        kat[f"sector_{key}"] = {"jc0": jc, "rho0_0": rho0_s, "nrho_0": nrho_s, "runtime_warnings": n_warn}
         if key == "a":  # the reference's own sector experiment (scratch_fbp.py:33-49), on this seeded phantom
             nv = fb.backproject_naive(s, n).values
             lp = fb.logpolar_backproject(s, n).values

@@ -252,3 +252,65 @@ def test_generic_size_bluestein_tables(nt, nth):
     H = hp.table("ramp", np.float32).astype(np.float64)
     out = np.fft.ifft(np.fft.fft(g, n=i.M, axis=0) * H[:, None], axis=0).real[:nt] * i.M
     assert O.relative_l2(out, O.ramp_filter(g)) < 1e-6
+
+
+# ---- sector (partial) backprojection plans, host-only (no GPU needed) ----
+
+def _sector_plan(nt, nth, n, sectors):
+    arr = (N.Sector * max(1, len(sectors)))()
+    for i, (t0, b, a) in enumerate(sectors):
+        arr[i].theta0, arr[i].beta, arr[i].a_r = t0, b, a
+    h = c_void_p()
+    rc = N.lib().lpbp_sector_plan_create(nt, nth, n, arr, len(sectors), -1, byref(h))
+    return rc, h
+
+
+@pytest.mark.parametrize("nt,nth,n,sectors", [
+    (256, 180, 128, [(k * math.pi / 4, math.pi / 8, 0.25) for k in range(4)]),
+    (256, 256, 256, [(0.0, math.pi / 2, 0.25)]),
+    (2048, 2048, 2048, [(k * math.pi / 4, math.pi / 8, 0.25) for k in range(4)]),
+    (128, 96, 80, [(-0.4, math.pi / 6, 0.3), (math.pi / 3 - 0.4, math.pi / 6, 0.2), (2 * math.pi / 3 - 0.4, math.pi / 6, 0.45)]),
+])
+def test_sector_geometry_matches_oracle(nt, nth, n, sectors):
+    rc, h = _sector_plan(nt, nth, n, sectors)
+    assert rc == N.LPBP_OK, N.lib().lpbp_last_error()
+    try:
+        for k, (t0, b, a) in enumerate(sectors):
+            inf = N.SectorInfo()
+            assert N.lib().lpbp_sector_get_info(h, k, byref(inf)) == N.LPBP_OK
+            jc, theta_c, rho0, nrho = O.sector_geometry(nt, nth, n, t0, b, a)
+            assert (inf.jc, inf.nrho, inf.nphi) == (jc, nrho, 2 * nth)
+            assert inf.theta_c == pytest.approx(theta_c, abs=1e-15)
+            assert inf.rho0 == pytest.approx(rho0, abs=1e-15)
+            assert inf.drho == pytest.approx(-rho0 / nrho, rel=1e-15)
+            assert inf.L >= 2 * nrho - 1 and inf.L & (inf.L - 1) == 0
+        ws = c_size_t()
+        assert N.lib().lpbp_sector_workspace_bytes(h, 2, byref(ws)) == N.LPBP_OK and ws.value > 0
+        # host-only plans refuse to execute
+        assert N.lib().lpbp_sector_execute(h, c_void_p(16), c_void_p(16), 1, None, 0, None) == N.LPBP_EINVAL
+    finally:
+        N.lib().lpbp_sector_plan_destroy(h)
+
+
+def test_sector_validation_messages_match_oracle():
+    cases = [
+        (16, [(0.0, math.pi / 2, 0.25)], "n_out must be >= 2", 1),
+        (16, [], "at least one sector is required", None),
+        (16, [(0.0, 2.0, 0.25)], "sector half-width beta must lie in (0, pi/2]", None),
+        (16, [(0.0, 0.0, 0.25)], "sector half-width beta must lie in (0, pi/2]", None),
+        (16, [(0.0, 1.0, 0.5)], "sector rescale a_r must lie in (0, 1/2)", None),
+        (16, [(0.0, 0.7, 0.25)], None, None),
+        (16, [(0.0, 0.5, 0.2), (2.0, 0.5, 0.2)], None, None),
+    ]
+    for n, sectors, msg, n_override in cases:
+        nn = n_override or n
+        rc, h = _sector_plan(64, 32, nn, sectors)
+        with pytest.raises(ValueError) as e:
+            O.partial_backproject(np.ones((64, 32)), sectors, nn)
+        assert rc == N.LPBP_EINVAL
+        got = N.lib().lpbp_last_error().decode()
+        assert got == str(e.value)
+        if msg:
+            assert got == msg
+    rc, _ = _sector_plan(64, 32, 16, [(0.0, math.pi / 2, 0.25)] * 33)
+    assert rc == N.LPBP_EINVAL and "at most 32 sectors" in N.lib().lpbp_last_error().decode()
