@@ -699,7 +699,7 @@ int sector_chunk(const lpbp_sector_plan* P, const float* in, float* out, int c, 
   char* subws = cur;
   for (int s = 0; s < nsec; ++s) {
     cudaError_t e = lpbp::launch_sector_prep(in, work, h.nt, h.ntheta, c, P->cols[s], P->rows[s],
-                                             h.sec[s].spec.a_r, st);
+                                             h.sec[s].spec.a_r, h.sec[s].klo, h.sec[s].khi, st);
     if (e) return launch_fail(e, "sector_prep");
     ++g_launches;
     int rc = run_chunk(P->sub[s], work, nullptr, c, subws, st, true, const_cast<float*>(args.s[s].lp));
@@ -853,8 +853,9 @@ int lpbp_sector_prepare(const lpbp_sector_plan* P, int32_t index, const float* s
   if (batch == 0) return LPBP_OK;
   if (!sino_dev || !out_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
+  const auto& S = P->h.sec[index];
   cudaError_t e = lpbp::launch_sector_prep(sino_dev, out_dev, P->h.nt, P->h.ntheta, batch, P->cols[index],
-                                           P->rows[index], P->h.sec[index].spec.a_r, static_cast<cudaStream_t>(stream));
+                                           P->rows[index], S.spec.a_r, S.klo, S.khi, static_cast<cudaStream_t>(stream));
   if (e) return launch_fail(e, "sector_prep");
   ++g_launches;
   return LPBP_OK;

@@ -90,10 +90,17 @@ std::string build_sector_set(int nt, int ntheta, int n_out, const std::vector<Se
       const int rot = (j + S.jc % ntheta + ntheta) % ntheta;  // (arange + jc) % ntheta
       c.w = mask[q][rot] ? (float)(1.0 / out.coverage[rot]) : 0.0f;
       c.off = (1.0 - sp.a_r) * std::cos(j * dtheta);
+      // reference: fi = (t_i - off + 1) / dt with t_i = -1 + i dt, i.e. i - off / dt
+      const double base = -c.off / dt;
+      const double fl = std::floor(base);
+      c.d = (int32_t)fl;
+      c.w2 = (float)(base - fl);
       S.cols[j] = c;
     }
     // shrunk support rows: fi = (t_k / a_r + 1) / dt
     S.rows.resize(nt);
+    S.klo = 0;
+    S.khi = -1;
     for (int k = 0; k < nt; ++k) {
       const double t = -1.0 + k * dt;
       const double fi = (t / sp.a_r + 1.0) / dt;
@@ -102,6 +109,10 @@ std::string build_sector_set(int nt, int ntheta, int n_out, const std::vector<Se
       r.k1 = (fl < -2.0) ? -2 : (fl > nt + 1.0 ? nt + 1 : (int32_t)fl);  // outside: both taps read zero
       r.w1 = (float)(fi - fl);
       S.rows[k] = r;
+      if (r.k1 + 1 >= 0 && r.k1 < nt) {  // at least one tap inside the sinogram
+        if (S.khi < S.klo) S.klo = k;
+        S.khi = k;
+      }
     }
     out.sec.push_back(std::move(S));
   }

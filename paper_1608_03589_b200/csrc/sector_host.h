@@ -18,6 +18,9 @@ struct SectorCol {
   int32_t src;
   int32_t flip;
   float w;
+  // fi(i) = (t_i - off + 1) / dt = i - off / dt: floor = i + d, weight w2 constant per column
+  int32_t d;
+  float w2;
   float pad;
 };
 // Per row k of the shrunk sinogram out(t_k) = a_r g(t_k / a_r)  (logpolar.py:175-179):
@@ -36,6 +39,7 @@ struct SectorHost {
   int nrho = 0;             // _mesh_for(ns, rho0, None)
   std::vector<SectorCol> cols;  // [ntheta]
   std::vector<SectorRow> rows;  // [nt]
+  int klo = 0, khi = -1;        // rows k of the shrunk sinogram that can be nonzero (a tap in [0, nt))
 };
 
 struct SectorSetHost {

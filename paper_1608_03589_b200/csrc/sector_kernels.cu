@@ -15,20 +15,25 @@ namespace {
 //   out(i, j)     = lerp_k(scaled(., j), (t_i - off_j + 1) / dt)
 // with zero outside [0, nt) at both levels (grids.py:255-269), i.e. the reference's
 // _roll_angles -> weights -> _rescale_support -> shift_sinogram chain
-// (logpolar.py:153-179, 260-271; radon.py:137-158).  Index math in fp64.
+// (logpolar.py:153-179, 260-271; radon.py:137-158).  Weights and bases come from
+// fp64 host tables (per column: source, flip, weight, shift base; per row: the
+// shrink lerp), so a sample is 4 gathers and a few FMAs.
 __global__ void __launch_bounds__(256)
 k_sector_prep(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
-              const SectorCol* __restrict__ cols, const SectorRow* __restrict__ rows, double a_r) {
+              const SectorCol* __restrict__ cols, const SectorRow* __restrict__ rows, double a_r, int klo, int khi) {
   const int j = blockIdx.x * 32 + threadIdx.x;
   const int i = blockIdx.y * 8 + threadIdx.y;
   if (j >= ntheta || i >= nt) return;
   const size_t slice = (size_t)blockIdx.z * nt * ntheta;
   const SectorCol c = cols[j];
-  const double dt = 2.0 / nt;
-  const double fi = ((-1.0 + i * dt) - c.off + 1.0) / dt;
-  const double fl = floor(fi);
-  const float w2 = (float)(fi - fl);
-  const int k2 = fl < -2.0 ? -2 : (fl > nt + 1.0 ? nt + 1 : (int)fl);
+  const float w2 = c.w2;
+  const int k2 = i + c.d;  // floor((t_i - off + 1) / dt) with the per-column fraction w2
+  // zero-weight angle (outside this sector's extended mask) or both shrink taps outside the
+  // rows that can be nonzero: the sample is exactly zero, skip the loads
+  if (c.w == 0.f || k2 + 1 < klo || k2 > khi) {
+    out[slice + (size_t)i * ntheta + j] = 0.f;
+    return;
+  }
   const float* col = g + slice + c.src;
   auto rolled = [&](int m) -> float {
     if (m < 0 || m >= nt) return 0.f;
@@ -113,10 +118,10 @@ k_sector_readout(const __grid_constant__ SectorArgs secs, int nsec, float* __res
 }  // namespace
 
 cudaError_t launch_sector_prep(const float* g, float* out, int nt, int ntheta, int batch, const SectorCol* cols,
-                               const SectorRow* rows, double a_r, cudaStream_t s) {
+                               const SectorRow* rows, double a_r, int klo, int khi, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   const dim3 grid((ntheta + 31) / 32, (nt + 7) / 8, batch);
-  k_sector_prep<<<grid, dim3(32, 8), 0, s>>>(g, out, nt, ntheta, cols, rows, a_r);
+  k_sector_prep<<<grid, dim3(32, 8), 0, s>>>(g, out, nt, ntheta, cols, rows, a_r, klo, khi);
   return cudaGetLastError();
 }
 
