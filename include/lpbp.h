@@ -158,6 +158,9 @@ int lpbp_sector_workspace_bytes(const lpbp_sector_plan* plan, int32_t chunk, siz
 /* sino [batch][nt][ntheta] -> img [batch][n][n]; ws NULL = plan-owned workspace (calls serialise). */
 int lpbp_sector_execute(lpbp_sector_plan* plan, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
                         size_t ws_bytes, void* stream);
+/* Host -> host: chunked copies around lpbp_sector_execute on a plan-owned stream; blocks. */
+int lpbp_sector_execute_host(lpbp_sector_plan* plan, const float* sino_host, float* img_host, int32_t batch,
+                             int32_t chunk);
 /* Stage: sector `index`'s working-frame sinogram [batch][nt][ntheta]. */
 int lpbp_sector_prepare(const lpbp_sector_plan* plan, int32_t index, const float* sino_dev, float* out_dev,
                         int32_t batch, void* stream);

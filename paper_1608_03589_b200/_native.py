@@ -83,6 +83,7 @@ SIGNATURES = {
     "lpbp_sector_get_info": (c_int32, [c_void_p, c_int32, POINTER(SectorInfo)]),
     "lpbp_sector_workspace_bytes": (c_int32, [c_void_p, c_int32, POINTER(c_size_t)]),
     "lpbp_sector_execute": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
+    "lpbp_sector_execute_host": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32]),
     "lpbp_sector_prepare": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
     "lpbp_sector_logpolar": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
     "lpbp_last_launch_count": (c_int64, []),

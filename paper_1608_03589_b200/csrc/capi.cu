@@ -656,11 +656,19 @@ struct lpbp_sector_plan {
   std::mutex mu;
   void* own_ws = nullptr;
   size_t own_ws_bytes = 0;
+  // host path: device staging for `host_chunk` slices and a stream
+  int host_chunk = 0;
+  float* d_in = nullptr;
+  float* d_out = nullptr;
+  cudaStream_t s_host = nullptr;
   ~lpbp_sector_plan() {
     DeviceGuard g(device);
     for (auto* p : sub) delete p;
     for (void* p : allocs) cudaFree(p);
     if (own_ws) cudaFree(own_ws);
+    if (d_in) cudaFree(d_in);
+    if (d_out) cudaFree(d_out);
+    if (s_host) cudaStreamDestroy(s_host);
   }
 };
 
@@ -841,6 +849,50 @@ int lpbp_sector_execute(lpbp_sector_plan* P, const float* sino_dev, float* img_d
     launches += g_launches;
     g_launches = 0;
   }
+  g_launches = launches;
+  return LPBP_OK;
+}
+
+int lpbp_sector_execute_host(lpbp_sector_plan* P, const float* sino_host, float* img_host, int32_t batch,
+                             int32_t chunk) {
+  g_launches = 0;
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  if (!sino_host || !img_host) return fail(LPBP_EINVAL, "invalid argument");
+  if (chunk <= 0) chunk = 4;
+  chunk = std::min(chunk, batch);
+  DeviceGuard g(P->device);
+  const size_t in_slice = (size_t)P->h.nt * P->h.ntheta, out_slice = (size_t)P->h.n * P->h.n;
+  {
+    std::lock_guard<std::mutex> lk(P->mu);
+    if (P->host_chunk < chunk) {
+      if (P->d_in) cudaFree(P->d_in);
+      if (P->d_out) cudaFree(P->d_out);
+      P->d_in = P->d_out = nullptr;
+      P->host_chunk = 0;
+      cudaError_t e = cudaMalloc(&P->d_in, in_slice * chunk * sizeof(float));
+      if (e == cudaSuccess) e = cudaMalloc(&P->d_out, out_slice * chunk * sizeof(float));
+      if (e == cudaSuccess && !P->s_host) e = cudaStreamCreateWithFlags(&P->s_host, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "sector host staging");
+      P->host_chunk = chunk;
+    }
+  }
+  int64_t launches = 0;
+  for (int off = 0; off < batch; off += chunk) {
+    const int c = std::min(chunk, batch - off);
+    cudaError_t e = cudaMemcpyAsync(P->d_in, sino_host + off * in_slice, in_slice * c * sizeof(float),
+                                    cudaMemcpyHostToDevice, P->s_host);
+    if (e) return cuda_fail(e, "H2D");
+    int rc = lpbp_sector_execute(P, P->d_in, P->d_out, c, nullptr, 0, P->s_host);
+    if (rc) return rc;
+    launches += g_launches;
+    e = cudaMemcpyAsync(img_host + off * out_slice, P->d_out, out_slice * c * sizeof(float), cudaMemcpyDeviceToHost,
+                        P->s_host);
+    if (e) return cuda_fail(e, "D2H");
+  }
+  cudaError_t e = cudaStreamSynchronize(P->s_host);
+  if (e) return cuda_fail(e, "sector execute_host sync");
   g_launches = launches;
   return LPBP_OK;
 }

@@ -94,6 +94,21 @@ class SectorPlan:
         self.last_launches = int(lib().lpbp_last_launch_count())
         return out
 
+    def execute_host(self, sino: np.ndarray, out: np.ndarray | None = None, chunk: int = 4) -> np.ndarray:
+        """Host -> host (numpy float32 [B, nt, ntheta] -> [B, n_out, n_out]); blocks."""
+        sino = np.ascontiguousarray(sino, dtype=np.float32)
+        if sino.ndim != 3 or sino.shape[1:] != (self.nt, self.ntheta):
+            raise ValueError(f"sinogram batch must have shape (B, {self.nt}, {self.ntheta})")
+        b = sino.shape[0]
+        if out is None:
+            out = np.empty((b, self.n_out, self.n_out), dtype=np.float32)
+        if not (out.flags.c_contiguous and out.dtype == np.float32 and out.shape == (b, self.n_out, self.n_out)):
+            raise ValueError("out must be a C-contiguous float32 array of shape (B, n, n)")
+        check(lib().lpbp_sector_execute_host(self._h, c_void_p(sino.ctypes.data), c_void_p(out.ctypes.data), b,
+                                             int(chunk)))
+        self.last_launches = int(lib().lpbp_last_launch_count())
+        return out
+
     def prepare(self, index: int, sino: torch.Tensor) -> torch.Tensor:
         """Working-frame sinogram of sector `index` (rolled, weighted, shrunk, shifted)."""
         sino = self._check_sino(sino)

@@ -96,6 +96,14 @@ def test_sector_batch_and_chunk_invariance(pkg):
         assert report(f"sector batch slice {i}", full[i].cpu().numpy(), ref) <= RTOL
 
 
+def test_sector_host_path_matches_device(pkg):
+    sino = np.stack([phantoms.sinogram(400 + i, 256, 180, 8, 0.05, 0.35, 0.01) for i in range(3)])
+    sectors = [(k * math.pi / 4, math.pi / 8, 0.25) for k in range(4)]
+    plan = pkg.SectorPlan(256, 180, 128, sectors)
+    host = plan.execute_host(sino, chunk=2)
+    assert np.array_equal(host, plan.execute(dev(sino)).cpu().numpy())
+
+
 def test_sector_linearity_and_zero(pkg):
     rng = np.random.default_rng(3)
     a = rng.standard_normal((128, 96)).cumsum(0).astype(np.float32) * 0.01
