@@ -421,3 +421,160 @@ def partial_backproject(g: np.ndarray, sectors, n_out: int, return_stages: bool 
         if return_stages:
             stages.append({"jc": jc, "rho0": rho0_s, "nrho": nrho_s, "sino": gs, "lp": lp})
     return (acc, stages) if return_stages else acc
+
+
+# --------------------------------------------------------------------------
+# BST engine (frequency-domain backprojection), bst.py:1-206
+# --------------------------------------------------------------------------
+
+BST_SCALE = 4.0 * math.pi      # bst.py:47
+BST_RADIAL_OVERSAMPLE = 2      # bst.py:52
+BST_DOMAIN_PAD = 2             # bst.py:58
+
+
+def bst_validate(n_out: int, beta: float = 0.0, zero_pad: float = 2.0, dc_mode: str = "subtract_mean") -> None:
+    """BstOptions checks (bst.py:79-87)."""
+    if n_out < 2:
+        raise ValueError("n_out must be >= 2")
+    if beta < 0:
+        raise ValueError("beta must be >= 0")
+    if zero_pad < 1:
+        raise ValueError("zero_pad must be >= 1")
+    if dc_mode not in ("subtract_mean", "kernel_cap"):
+        raise ValueError("dc_mode must be 'subtract_mean' or 'kernel_cap'")
+
+
+def kaiser(ns: int, beta: float) -> np.ndarray:
+    """Kaiser-Bessel taper I0(beta sqrt(1 - u^2)) / I0(beta), u = (2i - ns + 1)/(ns - 1)
+    (bst.py:90-102; I0 = scipy.special.i0 as phantoms.py:184-186)."""
+    from scipy import special
+    if ns < 2:
+        raise ValueError("ns must be >= 2")
+    u = (2.0 * np.arange(ns) - ns + 1.0) / (ns - 1.0)
+    return np.abs(special.i0(beta * np.sqrt(np.maximum(1.0 - u * u, 0.0)))) / abs(float(special.i0(beta)))
+
+
+def bst_geometry(nt: int, n_out: int, zero_pad: float = 2.0):
+    """(ns, ds, L, dsigma, m_need) of the radial spectra (bst.py:128-143)."""
+    ns = BST_RADIAL_OVERSAMPLE * (nt // 2)
+    ds = 1.0 / (ns - 1)
+    length = sfft.next_fast_len(max(int(math.ceil(2.0 * zero_pad * (ns - 1))), ns))
+    dsigma = 2.0 * math.pi / (length * ds)
+    m_need = int(math.floor(math.sqrt(2.0) * math.pi * n_out / 2.0 / dsigma)) + 2
+    if m_need > length // 2 + 1:
+        raise ValueError(
+            f"n_out = {n_out} exceeds the resolution supported by an nt = {nt} "
+            f"sinogram (max ~ {int(math.sqrt(2) * (ns - 1))})"
+        )
+    return ns, ds, length, dsigma, m_need
+
+
+def bst_radial_spectra(g: np.ndarray, n_out: int, zero_pad: float = 2.0, beta: float = 0.0):
+    """Windowed, zero-padded real DFTs along s of every semi-polar ray, first m_need
+    bins, times ds; the s = 0 sample carries half weight (bst.py:120-143)."""
+    g = np.asarray(g, dtype=np.float64)
+    ns, ds, length, dsigma, m_need = bst_geometry(g.shape[0], n_out, zero_pad)
+    prof = semipolar(g, ns) * kaiser(ns, beta)[:, None]
+    prof[0, :] *= 0.5
+    return ds * sfft.rfft(prof, n=length, axis=0)[:m_need], dsigma
+
+
+def polar_to_cartesian(P: np.ndarray, dsigma: float, nx: int, ny: int, dw: float = math.pi) -> np.ndarray:
+    """Bilinear (sigma, theta) gridding onto the FFT-ordered lattice omega = dw k,
+    theta periodic, then Hermitian averaging with the mirror bin (grids.py:456-508)."""
+    if nx < 2 or ny < 2:
+        raise ValueError("nx and ny must be >= 2")
+    nsig, nray = P.shape
+    nyq = math.sqrt(2.0) * dw * max(nx, ny) / 2.0
+    if (nsig - 1) * dsigma < nyq * (1.0 - 1e-12):
+        raise ValueError(
+            f"polar spectrum reaches sigma = {(nsig - 1) * dsigma:.3f} but the cartesian "
+            f"grid requires coverage up to the Nyquist radius {nyq:.3f}"
+        )
+    wx = math.pi * np.fft.fftfreq(nx, d=1.0 / nx) * (dw / math.pi)
+    wy = math.pi * np.fft.fftfreq(ny, d=1.0 / ny) * (dw / math.pi)
+    WX, WY = np.meshgrid(wx, wy)
+    fi = np.minimum(np.hypot(WX, WY) / dsigma, nsig - 1.0)
+    i0 = np.floor(fi).astype(np.int64)
+    wi = fi - i0
+    i1 = np.minimum(i0 + 1, nsig - 1)
+    fj = np.mod(np.arctan2(WY, WX), 2.0 * math.pi) / (2.0 * math.pi / nray)
+    j0 = np.floor(fj).astype(np.int64)
+    wj = fj - j0
+    j0 = np.mod(j0, nray)
+    j1 = np.mod(j0 + 1, nray)
+    grid = (P[i0, j0] * (1 - wi) * (1 - wj) + P[i1, j0] * wi * (1 - wj)
+            + P[i0, j1] * (1 - wi) * wj + P[i1, j1] * wi * wj)
+    ix = (-np.arange(nx)) % nx
+    iy = (-np.arange(ny)) % ny
+    return 0.5 * (grid + np.conj(grid[np.ix_(iy, ix)]))
+
+
+def bst_spectrum_to_image(P: np.ndarray, dsigma: float, n_out: int) -> np.ndarray:
+    """Grid on the DOMAIN_PAD-times finer lattice, zero the Nyquist row/column,
+    phase-ramp so pixel p0 lands on x = -1, inverse 2-D DFT, crop (bst.py:146-170)."""
+    d = BST_DOMAIN_PAD
+    big = d * n_out
+    dw = math.pi / d
+    grid = polar_to_cartesian(P, dsigma, big, big, dw)
+    if big % 2 == 0:
+        grid[big // 2, :] = 0.0
+        grid[:, big // 2] = 0.0
+    k = np.rint(np.fft.fftfreq(big, d=1.0 / big)).astype(np.int64)
+    p0 = ((d - 1) * n_out) // 2
+    dx = 2.0 / n_out
+    tau = np.exp(1j * dw * k * ((0.5 - p0) * dx - 1.0))
+    img = sfft.ifft2(grid * tau[:, None] * tau[None, :]) * (big * big / (4.0 * d * d))
+    return img.real[p0:p0 + n_out, p0:p0 + n_out]
+
+
+def square_chord(t, theta) -> np.ndarray:
+    """Chord length of the line x . xi_theta = t through [-1, 1]^2 (radon.py:183-209)."""
+    t = np.asarray(t, dtype=np.float64)
+    theta = np.asarray(theta, dtype=np.float64)
+    c, s = np.cos(theta), np.sin(theta)
+    big = 1e30
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lo_x = np.where(np.abs(s) > 1e-15, (t * c - 1.0) / s, -big)
+        hi_x = np.where(np.abs(s) > 1e-15, (t * c + 1.0) / s, big)
+        lo_y = np.where(np.abs(c) > 1e-15, (-t * s - 1.0) / c, -big)
+        hi_y = np.where(np.abs(c) > 1e-15, (-t * s + 1.0) / c, big)
+    lo = np.maximum(np.minimum(lo_x, hi_x), np.minimum(lo_y, hi_y))
+    hi = np.minimum(np.maximum(lo_x, hi_x), np.maximum(lo_y, hi_y))
+    ok = np.where(np.abs(s) > 1e-15, True, np.abs(t * c) <= 1.0) & np.where(np.abs(c) > 1e-15, True, np.abs(t * s) <= 1.0)
+    return np.where(ok, np.maximum(0.0, hi - lo), 0.0)
+
+
+def mean_backprojection(g: np.ndarray) -> float:
+    """Spatial mean of the backprojection over [-1, 1]^2 via <B g, 1> = <g, chord>
+    (bst.py:173-180)."""
+    g = np.asarray(g, dtype=np.float64)
+    nt, nth = g.shape
+    t = (-1.0 + np.arange(nt) * (2.0 / nt))[:, None]
+    theta = (np.arange(nth) * (math.pi / nth))[None, :]
+    return float(np.sum(g * square_chord(t, theta))) * (2.0 / nt) * (math.pi / nth) / 4.0
+
+
+def bst_backproject(g: np.ndarray, n_out: int, beta: float = 0.0, zero_pad: float = 2.0,
+                    dc_mode: str = "subtract_mean") -> np.ndarray:
+    """bst.py:183-203: radial spectra, DC handling, 1/sigma kernel, gridding and
+    inverse transform, BST_SCALE, exact mean restoration in subtract_mean mode."""
+    bst_validate(n_out, beta, zero_pad, dc_mode)
+    g = np.asarray(g, dtype=np.float64)
+    H, dsigma = bst_radial_spectra(g, n_out, zero_pad, beta)
+    if dc_mode == "subtract_mean":
+        H = H.copy()
+        H[0, :] = 0.0
+    kern = np.empty(H.shape[0])
+    kern[0] = 1.0 / dsigma
+    kern[1:] = 1.0 / (np.arange(1, H.shape[0]) * dsigma)
+    img = BST_SCALE * bst_spectrum_to_image(H * kern[:, None], dsigma, n_out)
+    if dc_mode == "subtract_mean":
+        img = img + (mean_backprojection(g) - float(img.mean()))
+    return img
+
+
+def fbp_bst(g: np.ndarray, n: int, lam: float = 0.0, cutoff: float = 1.0, beta: float = 0.0,
+            zero_pad: float = 2.0, dc_mode: str = "subtract_mean") -> np.ndarray:
+    """fbp(g, FilterSpec(lam, cutoff), engine='bst', n) (filtering.py:73-98)."""
+    return FBP_SCALE * bst_backproject(ramp_filter(g, lam, cutoff), n, beta, zero_pad, dc_mode)

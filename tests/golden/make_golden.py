@@ -103,12 +103,61 @@ def sector_goldens() -> None:
         json.dump(kat, f, indent=1, sort_keys=True)
 
 
+def bst_goldens() -> None:
+    """The BST engine (bst.py:120-206) and fbp's default engine, from the reference."""
+    from fastbp.bst import BstOptions, _radial_spectra, bst_backproject, mean_backprojection
+    from fastbp.grids import PolarSpectrum, polar_to_cartesian_frequency
+
+    arrays, kat = {}, {}
+    g0 = phantoms.config_sinogram(0).astype(np.float64)
+    s0 = fb.Sinogram(*g0.shape, g0)
+    arrays["cfg0_bp"] = bst_backproject(s0, BstOptions(n_out=256)).values
+    arrays["cfg0_fbp"] = fb.fbp(s0, fb.FilterSpec(), n=256).values           # default engine = "bst"
+    g1 = phantoms.config_sinogram(1, 0).astype(np.float64)
+    s1 = fb.Sinogram(*g1.shape, g1)
+    arrays["cfg1_fbp"] = fb.fbp(s1, fb.FilterSpec(), n=512).values.astype(np.float32)
+    arrays["cfg1_fbp_tik"] = fb.fbp(s1, fb.FilterSpec(lam=0.02, cutoff=0.9), n=512).values.astype(np.float32)
+    g2 = phantoms.sinogram(201, 256, 180, 10, 0.05, 0.35, 0.01).astype(np.float32).astype(np.float64)
+    s2 = fb.Sinogram(*g2.shape, g2)
+    arrays["opt_sino"] = g2.astype(np.float32)
+    arrays["opt_beta4_zp3_cap"] = bst_backproject(s2, BstOptions(n_out=128, beta=4.0, zero_pad=3.0,
+                                                                dc_mode="kernel_cap")).values
+    arrays["opt_beta2"] = bst_backproject(s2, BstOptions(n_out=128, beta=2.0)).values
+    g3 = phantoms.sinogram(202, 200, 96, 8, 0.05, 0.35, 0.01).astype(np.float32).astype(np.float64)
+    s3 = fb.Sinogram(*g3.shape, g3)
+    arrays["odd_sino"] = g3.astype(np.float32)
+    arrays["odd_n101"] = bst_backproject(s3, BstOptions(n_out=101)).values
+    # stage intermediates on the small case: radial spectra and the padded cartesian grid
+    g4 = phantoms.sinogram(203, 128, 90, 6, 0.05, 0.35, 0.0).astype(np.float32).astype(np.float64)
+    s4 = fb.Sinogram(*g4.shape, g4)
+    H, dsig = _radial_spectra(s4, 2.0, 0.0, 64)
+    arrays["small_sino"] = g4.astype(np.float32)
+    arrays["small_H"] = H
+    ps = PolarSpectrum(H.shape[0], H.shape[1], dsig, H)
+    arrays["small_grid"] = polar_to_cartesian_frequency(ps, 128, 128, dw=math.pi / 2).values
+    arrays["small_bp"] = bst_backproject(s4, BstOptions(n_out=64)).values
+    kat["small_dsigma"] = dsig
+    kat["mean_bp_cfg0"] = mean_backprojection(s0)
+    try:
+        bst_backproject(fb.Sinogram(64, 32, np.ones((64, 32))), BstOptions(n_out=256))
+    except ValueError as e:
+        kat["too_fine_message"] = str(e)
+    np.savez_compressed(os.path.join(HERE, "bst.npz"), **arrays)
+    with open(os.path.join(HERE, "kat_bst.json"), "w") as f:
+        json.dump(kat, f, indent=1, sort_keys=True)
+
+
 def main() -> None:
+    if "--only-bst" in sys.argv:
+        bst_goldens()
+        print("wrote bst goldens")
+        return
     if "--only-sector" in sys.argv:
         sector_goldens()
         print("wrote sector goldens")
         return
     sector_goldens()
+    bst_goldens()
     out = {}
     # config 0: BP 256x256 -> 256 (BASELINE.json configs[0])
     g0 = phantoms.config_sinogram(0).astype(np.float64)

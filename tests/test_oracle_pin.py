@@ -176,3 +176,55 @@ def test_sector_against_reference_directly(reference):
     with pytest.raises(ValueError) as e_or:
         O.partial_backproject(np.ones((64, 32)), [(0.0, 0.7, 0.25)], 16)
     assert str(e_ref.value) == str(e_or.value)
+
+
+# ---- BST engine (bst.py:120-206), fbp's default engine ----
+
+def test_bst_cfg_goldens(golden):
+    z = golden("bst.npz")
+    g0 = phantoms.config_sinogram(0).astype(np.float64)
+    assert rel(O.bst_backproject(g0, 256), z["cfg0_bp"]) < TOL
+    assert rel(O.fbp_bst(g0, 256), z["cfg0_fbp"]) < TOL
+    g1 = phantoms.config_sinogram(1, 0).astype(np.float64)
+    assert rel(O.fbp_bst(g1, 512), z["cfg1_fbp"]) < 1e-6            # stored as float32
+    assert rel(O.fbp_bst(g1, 512, lam=0.02, cutoff=0.9), z["cfg1_fbp_tik"]) < 1e-6
+
+
+def test_bst_options_and_odd_size(golden):
+    z = golden("bst.npz")
+    g = z["opt_sino"].astype(np.float64)
+    assert rel(O.bst_backproject(g, 128, beta=4.0, zero_pad=3.0, dc_mode="kernel_cap"), z["opt_beta4_zp3_cap"]) < TOL
+    assert rel(O.bst_backproject(g, 128, beta=2.0), z["opt_beta2"]) < TOL
+    assert rel(O.bst_backproject(z["odd_sino"].astype(np.float64), 101), z["odd_n101"]) < TOL
+
+
+def test_bst_stages_and_known_answers(golden):
+    z = golden("bst.npz")
+    with open(os.path.join(GOLDEN, "kat_bst.json")) as f:
+        kat = json.load(f)
+    g = z["small_sino"].astype(np.float64)
+    H, dsig = O.bst_radial_spectra(g, 64)
+    assert dsig == kat["small_dsigma"]
+    assert rel(H, z["small_H"]) < TOL
+    assert rel(O.polar_to_cartesian(H, dsig, 128, 128, math.pi / 2), z["small_grid"]) < TOL
+    assert rel(O.bst_backproject(g, 64), z["small_bp"]) < TOL
+    assert abs(O.mean_backprojection(phantoms.config_sinogram(0)) - kat["mean_bp_cfg0"]) < 1e-15
+    with pytest.raises(ValueError) as e:
+        O.bst_backproject(np.ones((64, 32)), 256)
+    assert str(e.value) == kat["too_fine_message"]
+    for kw, msg in ((dict(n_out=1), "n_out must be >= 2"), (dict(n_out=8, beta=-1.0), "beta must be >= 0"),
+                    (dict(n_out=8, zero_pad=0.5), "zero_pad must be >= 1"),
+                    (dict(n_out=8, dc_mode="x"), "dc_mode must be 'subtract_mean' or 'kernel_cap'")):
+        with pytest.raises(ValueError, match=msg):
+            O.bst_validate(**kw)
+
+
+def test_bst_against_reference_directly(reference):
+    from fastbp.bst import BstOptions, bst_backproject
+    fb = reference
+    rng = np.random.default_rng(21)
+    g = rng.standard_normal((160, 120)).cumsum(0) * 0.01
+    s = fb.Sinogram(*g.shape, g)
+    for kw in ({}, dict(beta=3.0, zero_pad=1.5), dict(dc_mode="kernel_cap")):
+        assert rel(O.bst_backproject(g, 90, **kw), bst_backproject(s, BstOptions(n_out=90, **kw)).values) < TOL
+    assert rel(O.fbp_bst(g, 90, 0.1, 0.8), fb.fbp(s, fb.FilterSpec(lam=0.1, cutoff=0.8), n=90).values) < TOL
