@@ -168,6 +168,48 @@ int lpbp_sector_prepare(const lpbp_sector_plan* plan, int32_t index, const float
 int lpbp_sector_logpolar(const lpbp_sector_plan* plan, int32_t index, const float* work_dev, float* lp_dev,
                          int32_t batch, void* stream);
 
+/* ---- BST engine: bst_backproject(g, BstOptions), bst.py:183-203, and fbp(g, spec, engine="bst"),
+ * the reference fbp's default engine (filtering.py:73-98) ----
+ * Semi-polar unfolding on 2*(nt/2) radial samples with the Kaiser window, per-ray zero-padded
+ * real DFTs along s (bst.py:120-143), 1/sigma kernel, bilinear polar -> Cartesian frequency
+ * gridding with Hermitian averaging on the 2x padded lattice (grids.py:456-508), inverse 2-D
+ * DFT with the phase ramps, crop (bst.py:146-170), BST_SCALE, and in subtract_mean mode the
+ * exact spatial mean from <g, chord> (bst.py:173-180, 196-202).  This build runs power-of-two
+ * radial DFT lengths L in [512, 8192] and padded sides 2 n in [256, 4096]; other sizes return
+ * LPBP_EUNSUPPORTED after validation. */
+typedef struct lpbp_bst_plan lpbp_bst_plan;
+
+typedef struct lpbp_bst_params {
+  int32_t nt, ntheta, n_out;
+  double beta;       /* BstOptions.beta (Kaiser window; 0 = none)          */
+  double zero_pad;   /* BstOptions.zero_pad (>= 1)                         */
+  int32_t dc_mode;   /* 0 = "subtract_mean", 1 = "kernel_cap"              */
+  int32_t filter;    /* 1: fbp = filter_sinogram(FilterSpec(lam, cutoff)) first, x 1/(2 pi) */
+  double lam, cutoff;
+  int32_t device;    /* < 0: host-only plan (validation and info only)     */
+} lpbp_bst_params;
+
+typedef struct lpbp_bst_info {
+  int32_t ns, nray, L, m_need, m_pad, big, p0, supported;
+  double ds, dsigma, out_scale;
+  size_t table_bytes, workspace_per_slice;
+} lpbp_bst_info;
+
+int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan);
+void lpbp_bst_plan_destroy(lpbp_bst_plan* plan);
+int lpbp_bst_get_info(const lpbp_bst_plan* plan, lpbp_bst_info* info);
+int lpbp_bst_workspace_bytes(const lpbp_bst_plan* plan, int32_t chunk, size_t* bytes);
+/* sino [batch][nt][ntheta] -> img [batch][n][n]; ws NULL = plan-owned workspace. */
+int lpbp_bst_execute(lpbp_bst_plan* plan, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
+                     size_t ws_bytes, void* stream);
+int lpbp_bst_execute_host(lpbp_bst_plan* plan, const float* sino_host, float* img_host, int32_t batch,
+                          int32_t chunk);
+/* Stage: the weighted radial spectra P[batch][nray][m_pad] (complex; bins m < m_need hold
+ * 0.5 x the reference's spectra * sigma_kernel, the 1/2 being the Hermitian averaging of the
+ * gridding; the DC bin is zero in subtract_mean mode) of an unfiltered batch. */
+int lpbp_bst_radial(const lpbp_bst_plan* plan, const float* sino_dev, float* spectra_dev, int32_t batch,
+                    void* stream);
+
 /* Number of kernel launches the last lpbp_execute/lpbp_execute_host issued on the calling thread. */
 int64_t lpbp_last_launch_count(void);
 

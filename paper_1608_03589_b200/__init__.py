@@ -4,7 +4,8 @@ backprojection / FBP path of arXiv 1608.03589 (reference package pkg/src/fastbp)
 Same names and signatures as the reference for the path:
   Sinogram, CartesianImage, LogPolarImage, LogPolarOptions, FilterSpec,
   logpolar_backproject, filter_sinogram, fbp, backproject_naive,
-  adaptive_rho0, compute_nrho, relative_l2, partial_backproject
+  adaptive_rho0, compute_nrho, relative_l2, partial_backproject,
+  BstOptions, bst_backproject (fbp's default engine "bst")
 plus batched device entry points (torch CUDA tensors) and LogPolarPlan.
 All compute runs in liblpbp.so; there is no CPU fallback.
 """
@@ -27,5 +28,6 @@ from . import roofline
 from . import synth
 from .multi import VolumeReconstructor, shard_bounds
 from .sector import SectorPlan, partial_backproject, partial_backproject_batch
+from .bst import BST_SCALE, BstOptions, BstPlan, bst_backproject, bst_backproject_batch
 
 __version__ = "0.1.0"

@@ -60,6 +60,23 @@ class SectorInfo(ctypes.Structure):
     ]
 
 
+class BstParams(ctypes.Structure):
+    _fields_ = [
+        ("nt", c_int32), ("ntheta", c_int32), ("n_out", c_int32),
+        ("beta", c_double), ("zero_pad", c_double), ("dc_mode", c_int32), ("filter", c_int32),
+        ("lam", c_double), ("cutoff", c_double), ("device", c_int32),
+    ]
+
+
+class BstInfo(ctypes.Structure):
+    _fields_ = [
+        ("ns", c_int32), ("nray", c_int32), ("L", c_int32), ("m_need", c_int32), ("m_pad", c_int32),
+        ("big", c_int32), ("p0", c_int32), ("supported", c_int32),
+        ("ds", c_double), ("dsigma", c_double), ("out_scale", c_double),
+        ("table_bytes", c_size_t), ("workspace_per_slice", c_size_t),
+    ]
+
+
 # symbol -> (restype, argtypes); exactly the functions declared in include/lpbp.h
 SIGNATURES = {
     "lpbp_plan_create": (c_int32, [POINTER(Params), POINTER(c_void_p)]),
@@ -86,6 +103,13 @@ SIGNATURES = {
     "lpbp_sector_execute_host": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32]),
     "lpbp_sector_prepare": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
     "lpbp_sector_logpolar": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_void_p]),
+    "lpbp_bst_plan_create": (c_int32, [POINTER(BstParams), POINTER(c_void_p)]),
+    "lpbp_bst_plan_destroy": (None, [c_void_p]),
+    "lpbp_bst_get_info": (c_int32, [c_void_p, POINTER(BstInfo)]),
+    "lpbp_bst_workspace_bytes": (c_int32, [c_void_p, c_int32, POINTER(c_size_t)]),
+    "lpbp_bst_execute": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
+    "lpbp_bst_execute_host": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32]),
+    "lpbp_bst_radial": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     "lpbp_last_launch_count": (c_int64, []),
     "lpbp_last_error": (c_char_p, []),
     "lpbp_version": (c_int32, []),

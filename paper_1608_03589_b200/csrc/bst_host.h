@@ -1,0 +1,51 @@
+// Host-side (fp64) geometry and tables of the BST engine, the reference's
+// frequency-domain backprojection (fastbp.bst, bst.py:120-206) and fbp's default
+// engine (filtering.py:73-98).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "plan_host.h"
+
+namespace lpbp {
+
+struct BstParams {
+  int nt, ntheta, n;
+  double beta;      // Kaiser window shape (0 = none)
+  double zero_pad;  // radial zero padding factor
+  int dc_mode;      // 0 = subtract_mean, 1 = kernel_cap
+  bool filter;      // fbp: filter_sinogram first, then x 1/(2 pi)
+  double lam, cutoff;
+};
+
+struct BstHost {
+  BstParams p{};
+  int ns = 0;       // radial samples per half-ray (2 x nt/2, bst.py:128)
+  int nray = 0;     // 2 ntheta half-rays
+  int L = 0;        // radial DFT length next_fast_len(max(ceil(2 z (ns-1)), ns))
+  int m_need = 0;   // radial bins kept (reach the Nyquist radius of the padded grid)
+  int m_pad = 0;    // row pitch of the polar spectrum (multiple of 4)
+  int big = 0;      // padded image side DOMAIN_PAD * n
+  int p0 = 0;       // crop offset
+  double ds = 0, dsigma = 0, dw = 0;
+  double out_scale = 0;  // BST_SCALE / (4 d^2) (x FBP_SCALE for fbp)
+  // semi-polar taps with the window (and the half weight of s = 0) folded in:
+  // positive half-ray at t = +s_k, negative at t = -s_k (grids.py:290-311)
+  std::vector<I2> tap_base;  // [ns] (pos base, neg base)
+  std::vector<F4> tap_w;     // [ns] (pos w0, pos w1, neg w0, neg w1)
+  std::vector<float> kern;   // [m_need] ds * (1/sigma or DC rule) * 1/2 (Hermitian averaging)
+  std::vector<F2> tau;       // [big] phase ramp exp(i dw k ((0.5 - p0) dx - 1)), FFT order
+  std::vector<F2> cmean;     // [big] sum_{y in crop} exp(2 pi i k y / big) / n^2 (crop mean from a row)
+  // fbp: ramp filter on the M-point circular embedding (as the log-polar plan)
+  int M = 0, Lr = 0;
+  std::vector<float> ramp;
+  // support (this build): power-of-two L in [512, 8192] and big in [256, 4096]
+  bool supported = false;
+};
+
+// Validates like BstOptions / _radial_spectra (ValueError texts verbatim) and
+// builds the tables.  Returns "" on success.
+std::string build_bst_host(const BstParams& p, BstHost& h);
+
+}  // namespace lpbp

@@ -1,0 +1,392 @@
+// Device kernels of the BST engine: the reference's frequency-domain
+// backprojection (fastbp.bst, bst.py:120-206), fbp's default engine.
+//
+//   KB1 radial   g -> P[ray][m]   semi-polar unfolding with the Kaiser window,
+//                                 length-L real DFTs along s (the +s and -s
+//                                 half-rays of one angle packed as re/im of one
+//                                 complex FFT), ds / (1/sigma) kernel; also the
+//                                 <g, chord> sum for the exact mean (bst.py:173-180)
+//   KB2 grid_x   P -> X[x][ky]    bilinear (sigma, theta) gridding onto the padded
+//                                 lattice with Hermitian averaging, Nyquist row /
+//                                 column zeroed, phase ramps, inverse DFT along x
+//                                 keeping the crop; rows ky < big/2 only (the
+//                                 spectrum is Hermitian) (grids.py:456-508, bst.py:146-170)
+//   KB3 grid_y   X -> img         inverse DFT along y as a real transform (two
+//                                 columns packed as re/im), crop, scale and the
+//                                 mean offset (subtract_mean mode)
+#include <cuda_runtime.h>
+
+#include "bst_kernels.cuh"
+#include "fft.cuh"
+
+namespace lpbp {
+namespace {
+
+// Barrier of one FFT group of T threads: a named barrier for whole warps, a
+// masked __syncwarp when several groups share a warp (bar.sync counts must be
+// multiples of 32).
+template <int T>
+struct GroupBarT {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    if constexpr (T >= 32) {
+      asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(T) : "memory");
+    } else {
+      const unsigned lane0 = (threadIdx.x & 31u) & ~(unsigned)(T - 1);
+      __syncwarp(((1u << T) - 1u) << lane0);
+    }
+  }
+};
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < nw; ++i) s += red[i];
+  return s;  // valid in thread 0
+}
+
+// Chord of the line x . (cos th, sin th) = t through [-1, 1]^2 (radon.py:183-209).
+__device__ double square_chord(double t, double c, double s) {
+  const double big = 1e30;
+  const bool sx = fabs(s) > 1e-15, sy = fabs(c) > 1e-15;
+  const double lo_x = sx ? (t * c - 1.0) / s : -big, hi_x = sx ? (t * c + 1.0) / s : big;
+  const double lo_y = sy ? (-t * s - 1.0) / c : -big, hi_y = sy ? (-t * s + 1.0) / c : big;
+  const double lo = fmax(fmin(lo_x, hi_x), fmin(lo_y, hi_y));
+  const double hi = fmin(fmax(lo_x, hi_x), fmax(lo_y, hi_y));
+  const bool ok = (sx || fabs(t * c) <= 1.0) && (sy || fabs(t * s) <= 1.0);
+  return ok ? fmax(0.0, hi - lo) : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// KB1: TC sinogram columns per CTA staged in smem (coalesced float4 loads), G
+// FFT groups; column c gives half-rays c (t = +s) and c + ntheta (t = -s).
+// ---------------------------------------------------------------------------
+template <int L, int TC, int G, bool IN_HALF>
+__global__ void __launch_bounds__(G * FftPlan<L, false>::T)
+k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int ntheta, int ns, int m_need, int m_pad,
+             const int2* __restrict__ tap_base, const float4* __restrict__ tap_w, const float* __restrict__ kern,
+             const float2* __restrict__ tw, double* __restrict__ acc, int want_mean) {
+  constexpr int T = FftPlan<L, false>::T;
+  constexpr int TP = TC + 1;
+  constexpr int V = TC / 4;
+  extern __shared__ __align__(16) float2 smem_b1[];
+  float* tile = reinterpret_cast<float*>(smem_b1);  // nt * TP
+  float2* bufs = smem_b1 + ((nt * TP + 3) / 4) * 2;
+  __shared__ double red[32];
+  __shared__ double csn[TC][2];
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  float2* buf = bufs + gi * padded_len(L);
+  const int c0 = blockIdx.x * TC;
+  const int nc = min(TC, ntheta - c0);  // ragged last tile
+  const int b = blockIdx.y;
+  const float* src = g + (size_t)b * nt * ntheta + c0;
+  if (nc == TC && (ntheta & 3) == 0) {
+    for (int e = threadIdx.x; e < nt * V; e += blockDim.x) {
+      const int t = e / V, c = (e % V) * 4;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + (size_t)t * ntheta + c));
+      float* r = tile + t * TP + c;
+      r[0] = v.x;
+      r[1] = v.y;
+      r[2] = v.z;
+      r[3] = v.w;
+    }
+  } else {
+    for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
+      const int t = e / TC, c = e % TC;
+      tile[t * TP + c] = c < nc ? __ldg(src + (size_t)t * ntheta + c) : 0.f;
+    }
+  }
+  if (threadIdx.x < TC) {
+    double sn, cs;
+    sincos((c0 + threadIdx.x) * (3.14159265358979323846 / ntheta), &sn, &cs);
+    csn[threadIdx.x][0] = cs;
+    csn[threadIdx.x][1] = sn;
+  }
+  __syncthreads();
+  if (want_mean) {  // <g, chord> over this tile (bst.py:173-180), fp64
+    const double dt = 2.0 / nt, dth = 3.14159265358979323846 / ntheta;
+    double part = 0.0;
+    for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
+      const int t = e / TC, c = e % TC;
+      if (c < nc) part += (double)tile[t * TP + c] * square_chord(-1.0 + t * dt, csn[c][0], csn[c][1]);
+    }
+    const double s = block_sum(part, red);
+    if (threadIdx.x == 0) atomicAdd(acc + 2 * b, s * dt * dth / 4.0);
+  }
+  for (int round = 0; round < TC / G; ++round) {
+    const int c = round * G + gi;
+    if (round * G >= nc) break;  // uniform across the CTA
+    auto load = [&](int k) -> float2 {  // (+s half-ray, -s half-ray) samples, window folded
+      if (!IN_HALF && k >= ns) return make_float2(0.f, 0.f);
+      const int2 bb = __ldg(tap_base + k);
+      const float4 w = __ldg(tap_w + k);
+      const float a = w.x * tile[bb.x * TP + c] + w.y * tile[(bb.x + 1) * TP + c];
+      const float m = w.z * tile[bb.y * TP + c] + w.w * tile[(bb.y + 1) * TP + c];
+      return make_float2(a, m);
+    };
+    auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
+    if constexpr (IN_HALF) {
+      auto load_h = [&](int k) -> float2 { return k < ns ? load(k) : make_float2(0.f, 0.f); };
+      block_fft<L, false, true, false, true, 16>(buf, ti, tw, load_h, store, GroupBarT<T>{1 + gi});
+    } else {
+      block_fft<L, false, true, false, false, 16>(buf, ti, tw, load, store, GroupBarT<T>{1 + gi});
+    }
+    GroupBarT<T>{1 + gi}();
+    // separate the packed spectra: A = (Z[m] + conj Z[-m]) / 2, B = (Z[m] - conj Z[-m]) / 2i
+    float2* pa = P + ((size_t)b * 2 * ntheta + c0 + c) * m_pad;
+    float2* pb = P + ((size_t)b * 2 * ntheta + c0 + c + ntheta) * m_pad;
+    for (int m = ti; m < m_need && c < nc; m += T) {
+      const float2 z = buf[pad16(m)];
+      const float2 w = buf[pad16((L - m) & (L - 1))];
+      const float k = __ldg(kern + m);
+      pa[m] = make_float2(0.5f * (z.x + w.x) * k, 0.5f * (z.y - w.y) * k);
+      pb[m] = make_float2(0.5f * (z.y + w.y) * k, 0.5f * (w.x - z.x) * k);
+    }
+    GroupBarT<T>{1 + gi}();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// KB2: rows ky of the padded lattice (TR per CTA, G groups), gridded on the fly
+// inside the first FFT pass, inverse DFT along x, crop x in [p0, p0 + n),
+// written transposed X[x][ky] (TR consecutive ky per run); accumulates the
+// crop mean through cmean (sum over the crop rows of the row's DFT weights).
+// ---------------------------------------------------------------------------
+template <int BIG, int TR, int G>
+__global__ void __launch_bounds__(G * FftPlan<BIG, true>::T)
+k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int nsig, int m_pad, int n, int p0,
+             float inv_dsigma, float inv_dphi, float dw, const float2* __restrict__ tau,
+             const float2* __restrict__ cmean, const float2* __restrict__ tw, double* __restrict__ acc) {
+  constexpr int T = FftPlan<BIG, true>::T;
+  constexpr int HB = BIG / 2;
+  extern __shared__ __align__(16) float2 smem_b2[];
+  float2* stg = smem_b2;                                   // [n][TR]
+  float2* buf = stg + (size_t)n * TR + (threadIdx.x / T) * padded_len(BIG);
+  __shared__ double red[32];
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  const int ky0 = blockIdx.x * TR;
+  const int b = blockIdx.y;
+  const float2* Pb = P + (size_t)b * nray * m_pad;
+  const int half_ray = nray / 2;
+  double mean_part = 0.0;
+  for (int rr = 0; rr < TR / G; ++rr) {
+    const int r = rr * G + gi;
+    const int ky = ky0 + r;
+    const int kfy = ky < HB ? ky : ky - BIG;  // ky < BIG/2 here
+    const float wy = dw * (float)kfy;
+    const float2 ty = __ldg(tau + ky);
+    auto load = [&](int kx) -> float2 {
+      if (kx == HB || ky == HB) return make_float2(0.f, 0.f);  // Nyquist row / column (bst.py:157-160)
+      const int kfx = kx < HB ? kx : kx - BIG;
+      const float wx = dw * (float)kfx;
+      float fi = hypotf(wx, wy) * inv_dsigma;
+      fi = fminf(fi, (float)(nsig - 1));
+      const float fil = floorf(fi);
+      const int i0 = (int)fil;
+      const int i1 = min(i0 + 1, nsig - 1);
+      const float wi = fi - fil;
+      float th = atan2f(wy, wx);
+      if (th < 0.f) th += 6.28318530717958647692f;
+      const float fj = th * inv_dphi;
+      const float fjl = floorf(fj);
+      const float wj = fj - fjl;
+      int j0 = (int)fjl % nray;
+      if (j0 < 0) j0 += nray;
+      const int j1 = j0 + 1 == nray ? 0 : j0 + 1;
+      // the mirror bin -k is the same radius at theta + pi: rays shifted by nray/2
+      // (numpy pairs the origin bin with itself, not with theta + pi)
+      const bool origin = kx == 0 && ky == 0;
+      const int m0 = origin ? j0 : (j0 + half_ray >= nray ? j0 + half_ray - nray : j0 + half_ray);
+      const int m1 = origin ? j1 : (j1 + half_ray >= nray ? j1 + half_ray - nray : j1 + half_ray);
+      const float c00 = (1.f - wi) * (1.f - wj), c10 = wi * (1.f - wj), c01 = (1.f - wi) * wj, c11 = wi * wj;
+      auto tap = [&](int j, int i) { return __ldg(Pb + (size_t)j * m_pad + i); };
+      const float2 a00 = tap(j0, i0), a10 = tap(j0, i1), a01 = tap(j1, i0), a11 = tap(j1, i1);
+      const float2 b00 = tap(m0, i0), b10 = tap(m0, i1), b01 = tap(m1, i0), b11 = tap(m1, i1);
+      // G(k) + conj(G(-k)); the 1/2 is folded into the radial kernel
+      const float gx = (a00.x * c00 + a10.x * c10 + a01.x * c01 + a11.x * c11) +
+                       (b00.x * c00 + b10.x * c10 + b01.x * c01 + b11.x * c11);
+      const float gy = (a00.y * c00 + a10.y * c10 + a01.y * c01 + a11.y * c11) -
+                       (b00.y * c00 + b10.y * c10 + b01.y * c01 + b11.y * c11);
+      const float2 tx = __ldg(tau + kx);
+      const float2 t2 = make_float2(tx.x * ty.x - tx.y * ty.y, tx.x * ty.y + tx.y * ty.x);
+      return make_float2(gx * t2.x - gy * t2.y, gx * t2.y + gy * t2.x);
+    };
+    float2 rowsum = make_float2(0.f, 0.f);
+    auto store = [&](int x, float2 v) {
+      const int xc = x - p0;
+      if (xc >= 0 && xc < n) {
+        stg[(size_t)xc * TR + r] = v;
+        rowsum.x += v.x;
+        rowsum.y += v.y;
+      }
+    };
+    block_fft<BIG, true, false, false, false, 16>(buf, ti, tw, load, store, GroupBarT<T>{1 + gi});
+    GroupBarT<T>{1 + gi}();  // the next row's first pass overwrites buf
+    // crop mean: Re(sum_x X[ky][x] * cmean[ky]), rows 1..BIG/2-1 stand for their conjugate partners too
+    const float2 cm = __ldg(cmean + ky);
+    const double wgt = ky == 0 ? 1.0 : 2.0;
+    mean_part += wgt * ((double)rowsum.x * cm.x - (double)rowsum.y * cm.y);
+  }
+  const double s = block_sum(mean_part, red);
+  if (threadIdx.x == 0) atomicAdd(acc + 2 * b + 1, s);
+  __syncthreads();
+  float2* Xb = X + (size_t)b * n * HB;
+  for (int e = threadIdx.x; e < n * TR; e += blockDim.x) {
+    const int xc = e / TR, r = e % TR;
+    Xb[(size_t)xc * HB + ky0 + r] = stg[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// KB3: TC output columns per CTA (TC/2 packed FFTs over G groups); the column
+// pair (x1, x2) is Z[ky] = X[ky][x1] + i X[ky][x2] with Hermitian extension,
+// so one inverse FFT gives both real columns.  Crop y in [p0, p0 + n).
+// ---------------------------------------------------------------------------
+template <int BIG, int TC, int G>
+__global__ void __launch_bounds__(G * FftPlan<BIG, true>::T)
+k_bst_grid_y(const float2* __restrict__ X, float* __restrict__ img, int n, int p0, float s_img, float s_mean,
+             float fbp, int subtract_mean, const double* __restrict__ acc, const float2* __restrict__ tw) {
+  constexpr int T = FftPlan<BIG, true>::T;
+  constexpr int HB = BIG / 2;
+  extern __shared__ __align__(16) float2 smem_b3[];
+  float* stg = reinterpret_cast<float*>(smem_b3);  // [n][TC + 1]
+  float2* buf = smem_b3 + ((size_t)n * (TC + 1) + 1) / 2 + (threadIdx.x / T) * padded_len(BIG);
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  const int x0 = blockIdx.x * TC;
+  const int b = blockIdx.y;
+  const float2* Xb = X + (size_t)b * n * HB;
+  float offset = 0.f;
+  if (subtract_mean) {  // mean_backprojection(g) - mean(img) (bst.py:199-202), in BST image units
+    const double mean_bp = acc[2 * b], mean_img = (double)s_mean * acc[2 * b + 1];
+    offset = (float)((double)fbp * (mean_bp - mean_img));
+  }
+  for (int rr = 0; rr < TC / 2 / G; ++rr) {
+    const int q = rr * G + gi;  // column pair
+    const int xa = x0 + 2 * q, xb = xa + 1;
+    const bool hb = xb < n;
+    const float2* ca = Xb + (size_t)xa * HB;
+    const float2* cb = Xb + (size_t)(hb ? xb : xa) * HB;
+    auto load = [&](int ky) -> float2 {
+      if (ky == HB) return make_float2(0.f, 0.f);
+      const bool hi = ky > HB;
+      const int k = hi ? BIG - ky : ky;
+      float2 a = __ldg(ca + k), c = hb ? __ldg(cb + k) : make_float2(0.f, 0.f);
+      if (hi) {
+        a.y = -a.y;
+        c.y = -c.y;
+      }
+      return make_float2(a.x - c.y, a.y + c.x);  // a + i c
+    };
+    auto store = [&](int y, float2 v) {
+      const int yc = y - p0;
+      if (yc >= 0 && yc < n) {
+        stg[(size_t)yc * (TC + 1) + 2 * q] = v.x * s_img + offset;
+        stg[(size_t)yc * (TC + 1) + 2 * q + 1] = v.y * s_img + offset;
+      }
+    };
+    block_fft<BIG, true, false, false, false, 16>(buf, ti, tw, load, store, GroupBarT<T>{1 + gi});
+    GroupBarT<T>{1 + gi}();
+  }
+  __syncthreads();
+  float* ob = img + (size_t)b * n * n;
+  const int w = min(TC, n - x0);
+  for (int e = threadIdx.x; e < n * TC; e += blockDim.x) {
+    const int y = e / TC, c = e % TC;
+    if (c < w) ob[(size_t)y * n + x0 + c] = stg[(size_t)y * (TC + 1) + c];
+  }
+}
+
+template <typename K>
+cudaError_t prep(K k, size_t smem) {
+  if (smem > 48 * 1024) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return cudaSuccess;
+}
+
+template <int L>
+cudaError_t radial_impl(const BstDims& d, const BstTables& t, const float* g, float2* P, double* acc, int batch,
+                        cudaStream_t s) {
+  constexpr int T = FftPlan<L, false>::T;
+  constexpr int G = T >= 256 ? 1 : (256 / T > 4 ? 4 : 256 / T);
+  constexpr int TC = G >= 4 ? G : 4;
+  const size_t smem = (((size_t)d.nt * (TC + 1) + 3) / 4 * 2 + (size_t)G * padded_len(L)) * sizeof(float2);
+  const bool half = 2 * d.ns <= L;
+  cudaError_t e;
+  if (half) {
+    auto k = k_bst_radial<L, TC, G, true>;
+    if ((e = prep(k, smem))) return e;
+    k<<<dim3((d.ntheta + TC - 1) / TC, batch), G * T, smem, s>>>(g, P, d.nt, d.ntheta, d.ns, d.m_need, d.m_pad,
+                                                                  t.tap_base, t.tap_w, t.kern, t.tw_L, acc,
+                                                                  d.subtract_mean);
+  } else {
+    auto k = k_bst_radial<L, TC, G, false>;
+    if ((e = prep(k, smem))) return e;
+    k<<<dim3((d.ntheta + TC - 1) / TC, batch), G * T, smem, s>>>(g, P, d.nt, d.ntheta, d.ns, d.m_need, d.m_pad,
+                                                                  t.tap_base, t.tap_w, t.kern, t.tw_L, acc,
+                                                                  d.subtract_mean);
+  }
+  return cudaGetLastError();
+}
+
+template <int BIG>
+cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, float2* X, float* img, double* acc,
+                      int batch, cudaStream_t s) {
+  constexpr int T = FftPlan<BIG, true>::T;
+  constexpr int G = T >= 256 ? 2 : 4;
+  constexpr int TR = 4;
+  static_assert(TR % G == 0 || G > TR, "rows per group");
+  constexpr int GX = G > TR ? TR : G;
+  {
+    const size_t smem = ((size_t)d.n * TR + (size_t)GX * padded_len(BIG)) * sizeof(float2);
+    auto k = k_bst_grid_x<BIG, TR, GX>;
+    cudaError_t e = prep(k, smem);
+    if (e) return e;
+    k<<<dim3((BIG / 2) / TR, batch), GX * T, smem, s>>>(P, X, d.nray, d.m_need, d.m_pad, d.n, d.p0,
+                                                         (float)(1.0 / d.dsigma), (float)(d.nray / 6.283185307179586),
+                                                         (float)d.dw, t.tau, t.cmean, t.tw_big, acc);
+    if ((e = cudaGetLastError())) return e;
+  }
+  {
+    constexpr int TC = 8;
+    constexpr int GY = G > TC / 2 ? TC / 2 : G;
+    const size_t smem = (((size_t)d.n * (TC + 1) + 1) / 2 + (size_t)GY * padded_len(BIG)) * sizeof(float2);
+    auto k = k_bst_grid_y<BIG, TC, GY>;
+    cudaError_t e = prep(k, smem);
+    if (e) return e;
+    k<<<dim3((d.n + TC - 1) / TC, batch), GY * T, smem, s>>>(X, img, d.n, d.p0, d.s_img, d.s_mean, d.fbp,
+                                                            d.subtract_mean, acc, t.tw_big);
+    return cudaGetLastError();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_bst_radial(const BstDims& d, const BstTables& t, const float* g, float2* P, double* acc, int batch,
+                              cudaStream_t s) {
+  switch (d.L) {
+    case 512: return radial_impl<512>(d, t, g, P, acc, batch, s);
+    case 1024: return radial_impl<1024>(d, t, g, P, acc, batch, s);
+    case 2048: return radial_impl<2048>(d, t, g, P, acc, batch, s);
+    case 4096: return radial_impl<4096>(d, t, g, P, acc, batch, s);
+    case 8192: return radial_impl<8192>(d, t, g, P, acc, batch, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t launch_bst_grid(const BstDims& d, const BstTables& t, const float2* P, float2* X, float* img, double* acc,
+                            int batch, cudaStream_t s) {
+  switch (d.big) {
+    case 256: return grid_impl<256>(d, t, P, X, img, acc, batch, s);
+    case 512: return grid_impl<512>(d, t, P, X, img, acc, batch, s);
+    case 1024: return grid_impl<1024>(d, t, P, X, img, acc, batch, s);
+    case 2048: return grid_impl<2048>(d, t, P, X, img, acc, batch, s);
+    case 4096: return grid_impl<4096>(d, t, P, X, img, acc, batch, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace lpbp

@@ -13,6 +13,8 @@
 #include "kernels.cuh"
 #include "plan_host.h"
 #include "sector_kernels.cuh"
+#include "bst_host.h"
+#include "bst_kernels.cuh"
 
 using lpbp::DevTables;
 using lpbp::Dims;
@@ -917,6 +919,331 @@ int lpbp_sector_logpolar(const lpbp_sector_plan* P, int32_t index, const float* 
                          int32_t batch, void* stream) {
   if (!P || index < 0 || index >= (int)P->sub.size()) return fail(LPBP_EINVAL, "invalid argument");
   return lpbp_logpolar(P->sub[index], work_dev, lp_dev, batch, nullptr, 0, stream);
+}
+
+
+// ---------------------------------------------------------------------------
+// BST engine
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct lpbp_bst_plan {
+  lpbp::BstHost h;
+  lpbp::BstDims d{};
+  lpbp::BstTables t{};
+  Dims rd{};        // ramp-filter dims (fbp)
+  DevTables rt{};   // ramp-filter tables (fbp)
+  int device = 0;
+  std::vector<void*> allocs;
+  size_t table_bytes = 0;
+  std::mutex mu;
+  void* own_ws = nullptr;
+  size_t own_ws_bytes = 0;
+  int host_chunk = 0;
+  float* d_in = nullptr;
+  float* d_out = nullptr;
+  cudaStream_t s_host = nullptr;
+  template <typename T>
+  int upload(const std::vector<T>& v, const void** dst) {
+    void* p = nullptr;
+    const size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(bst table)");
+    allocs.push_back(p);
+    if (!v.empty()) e = cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(bst table)");
+    table_bytes += bytes;
+    *dst = p;
+    return LPBP_OK;
+  }
+  int twiddles(int N, const float2** dst) {
+    const int len = lpbp::twiddle_table_len(N);
+    if (len < 0) return fail(LPBP_EUNSUPPORTED, "no FFT plan for size " + std::to_string(N));
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, (size_t)len * sizeof(float2));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(twiddles)");
+    allocs.push_back(p);
+    e = lpbp::launch_init_twiddles(N, static_cast<float2*>(p), nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "init_twiddles");
+    table_bytes += (size_t)len * sizeof(float2);
+    *dst = static_cast<const float2*>(p);
+    return LPBP_OK;
+  }
+  ~lpbp_bst_plan() {
+    DeviceGuard g(device);
+    for (void* p : allocs) cudaFree(p);
+    if (own_ws) cudaFree(own_ws);
+    if (d_in) cudaFree(d_in);
+    if (d_out) cudaFree(d_out);
+    if (s_host) cudaStreamDestroy(s_host);
+  }
+};
+
+namespace {
+
+// per slice: filtered sinogram (fbp) | P [nray][m_pad] complex | X [n][big/2] complex; + 2 doubles per slice
+size_t bst_slice_bytes(const lpbp::BstHost& h, size_t* off_p, size_t* off_x) {
+  const size_t f = h.p.filter ? align256((size_t)h.p.nt * h.p.ntheta * sizeof(float)) : 0;
+  const size_t pb = align256((size_t)h.nray * h.m_pad * sizeof(float2));
+  const size_t xb = align256((size_t)h.p.n * (h.big / 2) * sizeof(float2));
+  if (off_p) *off_p = f;
+  if (off_x) *off_x = f + pb;
+  return f + pb + xb;
+}
+size_t bst_ws_bytes(const lpbp_bst_plan* P, int chunk) {
+  return bst_slice_bytes(P->h, nullptr, nullptr) * chunk + align256((size_t)chunk * 2 * sizeof(double));
+}
+
+int bst_chunk(const lpbp_bst_plan* P, const float* in, float* out, int c, char* ws, cudaStream_t st,
+              float2* spectra_only) {
+  const auto& h = P->h;
+  size_t off_p, off_x;
+  const size_t per = bst_slice_bytes(h, &off_p, &off_x);
+  (void)per;
+  // regions laid out per chunk: [filtered c slices][P c slices][X c slices][acc]
+  const size_t fb = h.p.filter ? align256((size_t)h.p.nt * h.p.ntheta * sizeof(float)) : 0;
+  const size_t pb = align256((size_t)h.nray * h.m_pad * sizeof(float2));
+  const size_t xb = align256((size_t)h.p.n * (h.big / 2) * sizeof(float2));
+  float* filt = reinterpret_cast<float*>(ws);
+  float2* Pw = spectra_only ? spectra_only : reinterpret_cast<float2*>(ws + fb * c);
+  float2* Xw = reinterpret_cast<float2*>(ws + (fb + pb) * c);
+  double* acc = reinterpret_cast<double*>(ws + (fb + pb + xb) * c);
+  cudaError_t e = cudaMemsetAsync(acc, 0, (size_t)c * 2 * sizeof(double), st);
+  if (e) return cuda_fail(e, "bst acc");
+  const float* src = in;
+  if (h.p.filter && !spectra_only) {
+    e = lpbp::launch_ramp(P->rd, P->rt, in, filt, c, st);  // column tiles need ntheta % TC == 0
+    if (e == cudaErrorNotSupported) {
+      (void)cudaGetLastError();
+      e = lpbp::launch_ramp_generic(P->rd, P->rt, in, filt, c, st);
+    }
+    if (e) return launch_fail(e, "bst ramp_filter");
+    ++g_launches;
+    src = filt;
+  }
+  e = lpbp::launch_bst_radial(P->d, P->t, src, Pw, acc, c, st);
+  if (e) return launch_fail(e, "bst_radial");
+  ++g_launches;
+  if (spectra_only) return LPBP_OK;
+  e = lpbp::launch_bst_grid(P->d, P->t, Pw, Xw, out, acc, c, st);
+  if (e) return launch_fail(e, "bst_grid");
+  g_launches += 2;
+  return LPBP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan) {
+  g_last_error.clear();
+  if (!params || !plan) return fail(LPBP_EINVAL, "null argument");
+  *plan = nullptr;
+  lpbp::BstParams bp{params->nt, params->ntheta, params->n_out, params->beta, params->zero_pad, params->dc_mode,
+                     params->filter != 0, params->lam, params->cutoff};
+  auto* P = new (std::nothrow) lpbp_bst_plan();
+  if (!P) return fail(LPBP_ENOMEM, "host allocation failed");
+  std::string err = lpbp::build_bst_host(bp, P->h);
+  if (!err.empty()) {
+    delete P;
+    return fail(LPBP_EINVAL, err);
+  }
+  const auto& h = P->h;
+  P->device = params->device;
+  if (params->device >= 0 && !h.supported) {
+    const int n = h.p.n, L = h.L;
+    delete P;
+    return fail(LPBP_EUNSUPPORTED, "BST engine: no kernel instantiation for radial DFT length L=" + std::to_string(L) +
+                                       " / padded side " + std::to_string(2 * n) +
+                                       " (this build: powers of two, L in [512, 8192], 2n in [256, 4096])");
+  }
+  auto& d = P->d;
+  d.nt = h.p.nt;
+  d.ntheta = h.p.ntheta;
+  d.n = h.p.n;
+  d.ns = h.ns;
+  d.nray = h.nray;
+  d.L = h.L;
+  d.m_need = h.m_need;
+  d.m_pad = h.m_pad;
+  d.big = h.big;
+  d.p0 = h.p0;
+  d.subtract_mean = h.p.dc_mode == 0 ? 1 : 0;
+  d.dsigma = h.dsigma;
+  d.dw = h.dw;
+  d.s_img = (float)h.out_scale;
+  d.fbp = h.p.filter ? (float)(1.0 / (2.0 * 3.14159265358979323846)) : 1.f;
+  d.s_mean = (float)(h.out_scale / d.fbp);
+  if (P->device >= 0) {
+    DeviceGuard g(P->device);
+    if (!g.ok) {
+      delete P;
+      return fail(LPBP_ECUDA, "cannot select CUDA device " + std::to_string(params->device));
+    }
+    int rc = LPBP_OK;
+    const void* p;
+    rc = rc ? rc : P->upload(h.tap_base, &p);
+    if (!rc) P->t.tap_base = static_cast<const int2*>(p);
+    rc = rc ? rc : P->upload(h.tap_w, &p);
+    if (!rc) P->t.tap_w = static_cast<const float4*>(p);
+    rc = rc ? rc : P->upload(h.kern, &p);
+    if (!rc) P->t.kern = static_cast<const float*>(p);
+    rc = rc ? rc : P->upload(h.tau, &p);
+    if (!rc) P->t.tau = static_cast<const float2*>(p);
+    rc = rc ? rc : P->upload(h.cmean, &p);
+    if (!rc) P->t.cmean = static_cast<const float2*>(p);
+    rc = rc ? rc : P->twiddles(h.L, &P->t.tw_L);
+    rc = rc ? rc : P->twiddles(h.big, &P->t.tw_big);
+    if (h.p.filter) {
+      rc = rc ? rc : P->upload(h.ramp, &p);
+      if (!rc) P->rt.ramp = static_cast<const float*>(p);
+      rc = rc ? rc : P->twiddles(h.M, &P->rt.tw_ramp);
+      P->rd.nt = h.p.nt;
+      P->rd.ntheta = h.p.ntheta;
+      P->rd.M = h.M;
+    }
+    if (rc) {
+      std::string msg = g_last_error;
+      delete P;
+      return fail(rc, msg);
+    }
+  }
+  *plan = P;
+  return LPBP_OK;
+}
+
+void lpbp_bst_plan_destroy(lpbp_bst_plan* plan) { delete plan; }
+
+int lpbp_bst_get_info(const lpbp_bst_plan* P, lpbp_bst_info* info) {
+  if (!P || !info) return fail(LPBP_EINVAL, "null argument");
+  const auto& h = P->h;
+  info->ns = h.ns;
+  info->nray = h.nray;
+  info->L = h.L;
+  info->m_need = h.m_need;
+  info->m_pad = h.m_pad;
+  info->big = h.big;
+  info->p0 = h.p0;
+  info->supported = h.supported ? 1 : 0;
+  info->ds = h.ds;
+  info->dsigma = h.dsigma;
+  info->out_scale = h.out_scale;
+  info->table_bytes = P->table_bytes;
+  info->workspace_per_slice = bst_ws_bytes(P, 1);
+  return LPBP_OK;
+}
+
+int lpbp_bst_workspace_bytes(const lpbp_bst_plan* P, int32_t chunk, size_t* bytes) {
+  if (!P || !bytes || chunk < 1) return fail(LPBP_EINVAL, "invalid argument");
+  *bytes = bst_ws_bytes(P, chunk);
+  return LPBP_OK;
+}
+
+int lpbp_bst_execute(lpbp_bst_plan* P, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
+                     size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !img_dev) return fail(LPBP_EINVAL, "invalid argument");
+  if (reinterpret_cast<uintptr_t>(sino_dev) % 16) return fail(LPBP_EINVAL, "sinogram pointer must be 16-byte aligned");
+  if (ws && reinterpret_cast<uintptr_t>(ws) % 256) return fail(LPBP_EINVAL, "workspace must be 256-byte aligned");
+  DeviceGuard g(P->device);
+  std::unique_lock<std::mutex> lock(P->mu, std::defer_lock);
+  if (!ws) {
+    lock.lock();
+    const size_t need = bst_ws_bytes(P, std::max(1, std::min((int)batch, 4)));
+    if (P->own_ws_bytes < need) {
+      if (P->own_ws) cudaFree(P->own_ws);
+      P->own_ws = nullptr;
+      P->own_ws_bytes = 0;
+      cudaError_t e = cudaMalloc(&P->own_ws, need);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(bst workspace)");
+      P->own_ws_bytes = need;
+    }
+    ws = P->own_ws;
+    ws_bytes = P->own_ws_bytes;
+  }
+  int chunk = 1;
+  while (chunk < batch && bst_ws_bytes(P, chunk + 1) <= ws_bytes) ++chunk;
+  if (bst_ws_bytes(P, chunk) > ws_bytes)
+    return fail(LPBP_EINVAL, "workspace too small for one slice (need " + std::to_string(bst_ws_bytes(P, 1)) + " bytes)");
+  const size_t in_slice = (size_t)P->h.p.nt * P->h.p.ntheta, out_slice = (size_t)P->h.p.n * P->h.p.n;
+  int64_t launches = 0;
+  for (int off = 0; off < batch; off += chunk) {
+    const int c = std::min(chunk, batch - off);
+    int rc = bst_chunk(P, sino_dev + off * in_slice, img_dev + off * out_slice, c, static_cast<char*>(ws),
+                       static_cast<cudaStream_t>(stream), nullptr);
+    if (rc) return rc;
+    launches += g_launches;
+    g_launches = 0;
+  }
+  g_launches = launches;
+  return LPBP_OK;
+}
+
+int lpbp_bst_execute_host(lpbp_bst_plan* P, const float* sino_host, float* img_host, int32_t batch, int32_t chunk) {
+  g_launches = 0;
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  if (!sino_host || !img_host) return fail(LPBP_EINVAL, "invalid argument");
+  if (chunk <= 0) chunk = 4;
+  chunk = std::min(chunk, batch);
+  DeviceGuard g(P->device);
+  const size_t in_slice = (size_t)P->h.p.nt * P->h.p.ntheta, out_slice = (size_t)P->h.p.n * P->h.p.n;
+  {
+    std::lock_guard<std::mutex> lk(P->mu);
+    if (P->host_chunk < chunk) {
+      if (P->d_in) cudaFree(P->d_in);
+      if (P->d_out) cudaFree(P->d_out);
+      P->d_in = P->d_out = nullptr;
+      P->host_chunk = 0;
+      cudaError_t e = cudaMalloc(&P->d_in, in_slice * chunk * sizeof(float));
+      if (e == cudaSuccess) e = cudaMalloc(&P->d_out, out_slice * chunk * sizeof(float));
+      if (e == cudaSuccess && !P->s_host) e = cudaStreamCreateWithFlags(&P->s_host, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "bst host staging");
+      P->host_chunk = chunk;
+    }
+  }
+  int64_t launches = 0;
+  for (int off = 0; off < batch; off += chunk) {
+    const int c = std::min(chunk, batch - off);
+    cudaError_t e = cudaMemcpyAsync(P->d_in, sino_host + off * in_slice, in_slice * c * sizeof(float),
+                                    cudaMemcpyHostToDevice, P->s_host);
+    if (e) return cuda_fail(e, "H2D");
+    int rc = lpbp_bst_execute(P, P->d_in, P->d_out, c, nullptr, 0, P->s_host);
+    if (rc) return rc;
+    launches += g_launches;
+    e = cudaMemcpyAsync(img_host + off * out_slice, P->d_out, out_slice * c * sizeof(float), cudaMemcpyDeviceToHost,
+                        P->s_host);
+    if (e) return cuda_fail(e, "D2H");
+  }
+  cudaError_t e = cudaStreamSynchronize(P->s_host);
+  if (e) return cuda_fail(e, "bst execute_host sync");
+  g_launches = launches;
+  return LPBP_OK;
+}
+
+int lpbp_bst_radial(const lpbp_bst_plan* P, const float* sino_dev, float* spectra_dev, int32_t batch, void* stream) {
+  g_launches = 0;
+  if (!P || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (P->device < 0) return fail(LPBP_EINVAL, "host-only plan (device < 0) cannot execute");
+  if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !spectra_dev) return fail(LPBP_EINVAL, "invalid argument");
+  DeviceGuard g(P->device);
+  // spectra_dev holds [batch][nray][m_pad]; the accumulators go to a small scratch
+  void* acc = nullptr;
+  cudaError_t e = cudaMallocAsync(&acc, (size_t)batch * 2 * sizeof(double) + 256, static_cast<cudaStream_t>(stream));
+  if (e) return cuda_fail(e, "bst radial scratch");
+  e = cudaMemsetAsync(acc, 0, (size_t)batch * 2 * sizeof(double), static_cast<cudaStream_t>(stream));
+  if (!e) e = lpbp::launch_bst_radial(P->d, P->t, sino_dev, reinterpret_cast<float2*>(spectra_dev),
+                                      static_cast<double*>(acc), batch, static_cast<cudaStream_t>(stream));
+  cudaFreeAsync(acc, static_cast<cudaStream_t>(stream));
+  if (e) return launch_fail(e, "bst_radial");
+  ++g_launches;
+  return LPBP_OK;
 }
 
 int64_t lpbp_last_launch_count(void) { return g_launches; }

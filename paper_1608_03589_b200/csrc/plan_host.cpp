@@ -65,6 +65,8 @@ void lerp_tap(double f, int n, int32_t& base, double& w0, double& w1) {
 
 }  // namespace
 
+void lerp_tap_public(double f, int n, int32_t& base, double& w0, double& w1) { lerp_tap(f, n, base, w0, w1); }
+
 void build_bands(HostPlan& h, int band_rows) {
   // Steps of band_rows (2 or 4) rows for the streaming fused readout: step b owns
   // the pixels with i0 in [r0 - 1, r0 + band_rows - 1), r0 = row_min + band_rows*b,
@@ -141,6 +143,55 @@ int next_fast_len(int target) {
     for (int p : {2, 3, 5, 7, 11})
       while (r % p == 0) r /= p;
     if (r == 1) return v;
+  }
+}
+
+// Ramp / Tikhonov filter (filtering.py:54-70).  The reference multiplies by resp
+// on an Lr = next_fast_len(8 nt) grid; that is a convolution with the real even
+// taps h[d] = (1/Lr) sum_k resp_k cos(2 pi k d / Lr), |d| < nt.  The same taps
+// periodised on M = pow2 >= 2 nt give an exact circular embedding; the table is
+// their M-point spectrum / M.
+void build_ramp_taps(int nt, double lam, double cutoff, int& M_out, int& Lr_out, std::vector<float>& ramp) {
+  const double dt = 2.0 / nt;
+  const int Lr = next_fast_len(8 * nt);
+  Lr_out = Lr;
+  const double val = 1.0 / (Lr * dt);  // numpy.fft.fftfreq
+  const double cut = cutoff * kPi / dt;
+  std::vector<double> resp(Lr);
+  const int Npos = (Lr - 1) / 2 + 1;
+  for (int k = 0; k < Lr; ++k) {
+    const long long f = k < Npos ? k : (long long)k - Lr;
+    const double sigma = 2.0 * kPi * ((double)f * val);
+    const double a = std::fabs(sigma);
+    resp[k] = (std::fabs(sigma) > cut) ? 0.0 : a / (1.0 + lam * a);
+  }
+  std::vector<double> cosr(Lr);
+  for (int q = 0; q < Lr; ++q) cosr[q] = std::cos(2.0 * kPi * (double)q / Lr);
+  std::vector<double> taps(nt);
+  for (int d = 0; d < nt; ++d) {
+    double acc = 0.0;
+    long long ph = 0;
+    for (int k = 0; k < Lr; ++k) {
+      acc += resp[k] * cosr[ph];
+      ph += d;
+      if (ph >= Lr) ph -= Lr;
+    }
+    taps[d] = acc / Lr;
+  }
+  M_out = std::max(512, next_pow2(2 * nt));  // any M >= 2 nt - 1 embeds the Toeplitz filter
+  const int M = M_out;
+  std::vector<double> cosm(M);
+  for (int q = 0; q < M; ++q) cosm[q] = std::cos(2.0 * kPi * (double)q / M);
+  ramp.resize(M);
+  for (int kap = 0; kap < M; ++kap) {
+    double acc = taps[0];
+    long long ph = 0;
+    for (int d = 1; d < nt; ++d) {
+      ph += kap;
+      if (ph >= M) ph -= M;
+      acc += 2.0 * taps[d] * cosm[ph];
+    }
+    ramp[kap] = (float)(acc / M);
   }
 }
 
@@ -284,52 +335,8 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
     }
   }
 
-  // --- ramp / Tikhonov filter (filtering.py:54-70).  The reference multiplies
-  // by resp on an Lr = next_fast_len(8 nt) grid; that is a convolution with the
-  // real even taps h[d] = (1/Lr) sum_k resp_k cos(2 pi k d / Lr), |d| < nt.
-  // The same taps periodised on M = 2 nt give an exact circular embedding.
-  if (p.filter) {
-    const int Lr = next_fast_len(8 * nt);
-    h.ramp_len_ref = Lr;
-    const double val = 1.0 / (Lr * dt);  // numpy.fft.fftfreq
-    const double cut = p.cutoff * kPi / dt;
-    std::vector<double> resp(Lr);
-    const int Npos = (Lr - 1) / 2 + 1;
-    for (int k = 0; k < Lr; ++k) {
-      const long long f = k < Npos ? k : (long long)k - Lr;
-      const double sigma = 2.0 * kPi * ((double)f * val);
-      const double a = std::fabs(sigma);
-      resp[k] = (std::fabs(sigma) > cut) ? 0.0 : a / (1.0 + p.lam * a);
-    }
-    std::vector<double> cosr(Lr);
-    for (int q = 0; q < Lr; ++q) cosr[q] = std::cos(2.0 * kPi * (double)q / Lr);
-    std::vector<double> taps(nt);
-    for (int d = 0; d < nt; ++d) {
-      double acc = 0.0;
-      long long ph = 0;
-      for (int k = 0; k < Lr; ++k) {
-        acc += resp[k] * cosr[ph];
-        ph += d;
-        if (ph >= Lr) ph -= Lr;
-      }
-      taps[d] = acc / Lr;
-    }
-    h.M = std::max(512, next_pow2(2 * nt));  // any M >= 2 nt - 1 embeds the Toeplitz filter
-    const int M = h.M;
-    std::vector<double> cosm(M);
-    for (int q = 0; q < M; ++q) cosm[q] = std::cos(2.0 * kPi * (double)q / M);
-    h.ramp.resize(M);
-    for (int kap = 0; kap < M; ++kap) {
-      double acc = taps[0];
-      long long ph = 0;
-      for (int d = 1; d < nt; ++d) {
-        ph += kap;
-        if (ph >= M) ph -= M;
-        acc += 2.0 * taps[d] * cosm[ph];
-      }
-      h.ramp[kap] = (float)(acc / M);
-    }
-  }
+  // --- ramp / Tikhonov filter (filtering.py:54-70)
+  if (p.filter) build_ramp_taps(nt, p.lam, p.cutoff, h.M, h.ramp_len_ref, h.ramp);
 
   // --- readout quadrant table (grids.py:399-443) at x, y >= 0; the device
   // reflects phi for the other quadrants.

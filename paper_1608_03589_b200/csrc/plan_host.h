@@ -64,5 +64,9 @@ double adaptive_rho0(int nx, int ny);
 std::string mesh_for(int ns, double rho0, int nrho_in, int& nrho_out);
 // scipy.fft.next_fast_len(target) for complex transforms: smallest 11-smooth >= target
 int next_fast_len(int target);
+// Ramp / Tikhonov filter spectrum on the circular embedding M = pow2 >= 2 nt (filtering.py:54-70)
+void build_ramp_taps(int nt, double lam, double cutoff, int& M_out, int& Lr_out, std::vector<float>& ramp);
+// _lerp_axis0 tap (grids.py:255-269) as (base in [0, n-2], w0, w1), out-of-range terms weight 0
+void lerp_tap_public(double f, int n, int32_t& base, double& w0, double& w1);
 
 }  // namespace lpbp

@@ -2,10 +2,9 @@
 
 filter_sinogram / fbp keep the reference signatures.  engine="logpolar" runs the
 fused device pipeline (ramp filter kernel + log-polar backprojection, 1/(2 pi)
-applied in the readout); engine="naive" filters on the device and runs the
-direct backprojector.  The reference's default engine "bst" (the slice-theorem
-engine, bst.py) is outside this drop-in and raises NotImplementedError — there
-is no silent substitution.
+applied in the readout); engine="bst" (the reference's default) runs the BST
+engine of bst.py with the ramp filter in front (lpbp_bst_*); engine="naive"
+filters on the device and runs the direct backprojector.
 """
 
 from __future__ import annotations
@@ -77,7 +76,13 @@ def fbp(g: Sinogram, spec: FilterSpec, engine: str = "bst", n: int = 256, engine
         img = naive_backproject(fg, n) * FBP_SCALE
         return CartesianImage(n, n, img[0].double().cpu().numpy())
     if engine == "bst":
-        raise NotImplementedError("engine 'bst' is not part of this drop-in; use engine='logpolar' or 'naive'")
+        from .bst import BstOptions, get_bst_plan
+        opts = engine_options if isinstance(engine_options, BstOptions) else BstOptions(n_out=n)
+        if opts.n_out != n:
+            opts = BstOptions(n_out=n, beta=opts.beta, zero_pad=opts.zero_pad, dc_mode=opts.dc_mode)
+        plan = get_bst_plan(g.nt, g.ntheta, opts, _spec_key(spec))
+        img = plan.execute(_to_device(g))
+        return CartesianImage(n, n, img[0].double().cpu().numpy())
     raise ValueError("engine must be 'naive', 'bst' or 'logpolar'")
 
 

@@ -1,0 +1,122 @@
+"""GPU parity of the BST engine (fastbp.bst, bst.py:120-206) and of fbp's default
+engine, through liblpbp.so's lpbp_bst_* C ABI: against the reference's golden
+vectors (tests/golden/bst.npz, made by the reference itself) and the CPU oracle.
+Bar: relative L2 <= 1e-4 in fp32, max-abs reported."""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import fastbp_oracle as O
+from oracle import phantoms
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    import paper_1608_03589_b200 as p
+    return p
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def report(name, got, ref):
+    r = O.relative_l2(got, ref)
+    print(f"{name}: rel_l2={r:.3e} max_abs={O.max_abs(got, ref):.3e}")
+    return r
+
+
+def test_bst_cfg0_vs_reference_golden(pkg, golden):
+    z = golden("bst.npz")
+    g = phantoms.config_sinogram(0).astype(np.float64)
+    s = pkg.Sinogram(*g.shape, g)
+    assert report("bst cfg0", pkg.bst_backproject(s, pkg.BstOptions(n_out=256)).values, z["cfg0_bp"]) <= RTOL
+    # fbp's default engine is "bst"
+    assert report("fbp(bst) cfg0", pkg.fbp(s, pkg.FilterSpec(), n=256).values, z["cfg0_fbp"]) <= RTOL
+
+
+def test_bst_cfg1_fbp_vs_reference_golden(pkg, golden):
+    z = golden("bst.npz")
+    g = phantoms.config_sinogram(1, 0).astype(np.float64)
+    s = pkg.Sinogram(*g.shape, g)
+    assert report("fbp(bst) cfg1", pkg.fbp(s, pkg.FilterSpec(), n=512).values, z["cfg1_fbp"]) <= RTOL
+    tik = pkg.fbp(s, pkg.FilterSpec(lam=0.02, cutoff=0.9), engine="bst", n=512).values
+    assert report("fbp(bst) cfg1 tikhonov", tik, z["cfg1_fbp_tik"]) <= RTOL
+
+
+def test_bst_options(pkg, golden):
+    z = golden("bst.npz")
+    g = z["opt_sino"].astype(np.float64)
+    s = pkg.Sinogram(*g.shape, g)
+    assert report("bst beta=2", pkg.bst_backproject(s, pkg.BstOptions(n_out=128, beta=2.0)).values,
+                  z["opt_beta2"]) <= RTOL
+    cap = pkg.bst_backproject(s, pkg.BstOptions(n_out=128, beta=4.0, dc_mode="kernel_cap")).values
+    assert report("bst kernel_cap beta=4", cap, O.bst_backproject(g, 128, beta=4.0, dc_mode="kernel_cap")) <= RTOL
+    zp = pkg.bst_backproject(s, pkg.BstOptions(n_out=128, zero_pad=1.0)).values
+    assert report("bst zero_pad=1", zp, O.bst_backproject(g, 128, zero_pad=1.0)) <= RTOL
+
+
+def test_bst_radial_stage(pkg, golden):
+    z = golden("bst.npz")
+    g = z["opt_sino"].astype(np.float64)
+    plan = pkg.BstPlan(256, 180, pkg.BstOptions(n_out=128, dc_mode="kernel_cap"))
+    got = plan.radial(dev(g)[None])[0].cpu().numpy().T  # -> [m][ray]
+    H, dsig = O.bst_radial_spectra(g, 128)
+    kern = np.empty(H.shape[0])
+    kern[0] = 1.0 / dsig
+    kern[1:] = 1.0 / (np.arange(1, H.shape[0]) * dsig)
+    assert got.shape == H.shape
+    assert report("bst radial stage", got, 0.5 * H * kern[:, None]) <= RTOL
+
+
+def test_bst_batch_host_and_linearity(pkg):
+    sino = np.stack([phantoms.sinogram(500 + i, 512, 512, 12, 0.05, 0.35, 0.01) for i in range(4)])
+    plan = pkg.BstPlan(512, 512, pkg.BstOptions(n_out=512), filter_spec=(0.0, 1.0))
+    full = plan.execute(dev(sino))
+    for chunk in (1, 3):
+        assert torch.equal(plan.execute(dev(sino), chunk=chunk), full)
+    assert np.array_equal(plan.execute_host(sino, chunk=2), full.cpu().numpy())
+    assert plan.last_launches >= 4
+    ref = O.fbp_bst(sino[1].astype(np.float64), 512)
+    assert report("fbp(bst) 512 batch slice 1", full[1].cpu().numpy(), ref) <= RTOL
+    # linearity (the mean restoration is linear too)
+    a, b = dev(sino[0]), dev(sino[2])
+    ia, ib, iab = (plan.execute(x[None])[0].double() for x in (a, b, 2 * a - 3 * b))
+    assert O.relative_l2((2 * ia - 3 * ib).cpu().numpy(), iab.cpu().numpy()) < 1e-5
+
+
+def test_bst_2048_fbp_vs_oracle(pkg):
+    """Config-3 geometry through fbp's default engine."""
+    g = phantoms.config_sinogram(3, 5)
+    img = pkg.fbp(pkg.Sinogram(*g.shape, g.astype(np.float64)), pkg.FilterSpec(), n=2048).values
+    ref = O.fbp_bst(g.astype(np.float64), 2048)
+    assert report("fbp(bst) 2048", img, ref) <= RTOL
+
+
+def test_bst_errors(pkg):
+    with open(os.path.join(GOLDEN, "kat_bst.json")) as f:
+        kat = json.load(f)
+    with pytest.raises(ValueError) as e:
+        pkg.bst_backproject(pkg.Sinogram(64, 32, np.ones((64, 32))), pkg.BstOptions(n_out=256))
+    assert str(e.value) == kat["too_fine_message"]
+    for kw, msg in ((dict(n_out=1), "n_out must be >= 2"), (dict(n_out=8, beta=-1.0), "beta must be >= 0"),
+                    (dict(n_out=8, zero_pad=0.5), "zero_pad must be >= 1"),
+                    (dict(n_out=8, dc_mode="x"), "dc_mode must be 'subtract_mean' or 'kernel_cap'")):
+        with pytest.raises(ValueError, match=msg):
+            pkg.BstOptions(**kw)
+    # sizes this build does not instantiate fail loudly (no fallback)
+    with pytest.raises(NotImplementedError):
+        pkg.bst_backproject(pkg.Sinogram(200, 96, np.ones((200, 96))), pkg.BstOptions(n_out=101))
