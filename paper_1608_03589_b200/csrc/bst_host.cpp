@@ -2,8 +2,10 @@
 // /root/reference/pkg/src/fastbp/bst.py (and grids.py:290-311, 451-508).
 #include "bst_host.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <thread>
 
 namespace lpbp {
 namespace {
@@ -27,6 +29,29 @@ double bessel_i0(double x) {
 }
 
 bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// Chord of the line x . (cos th, sin th) = t through [-1, 1]^2 (radon.py:183-209).
+double square_chord(double t, double c, double s) {
+  const double big = 1e30;
+  const bool sx = std::fabs(s) > 1e-15, sy = std::fabs(c) > 1e-15;
+  const double lo_x = sx ? (t * c - 1.0) / s : -big, hi_x = sx ? (t * c + 1.0) / s : big;
+  const double lo_y = sy ? (-t * s - 1.0) / c : -big, hi_y = sy ? (-t * s + 1.0) / c : big;
+  const double lo = std::max(std::min(lo_x, hi_x), std::min(lo_y, hi_y));
+  const double hi = std::min(std::max(lo_x, hi_x), std::max(lo_y, hi_y));
+  const bool ok = (sx || std::fabs(t * c) <= 1.0) && (sy || std::fabs(t * s) <= 1.0);
+  return ok ? std::max(0.0, hi - lo) : 0.0;
+}
+
+// (13-bit index, 19-bit fixed-point weight) of a clamped fractional coordinate
+uint32_t pack_coord(double f) {
+  double fl = std::floor(f);
+  long long q = std::llround((f - fl) * 524288.0);
+  if (q >= 524288) {
+    q = 0;
+    fl += 1.0;
+  }
+  return (uint32_t)(long long)fl | ((uint32_t)q << 13);
+}
 
 }  // namespace
 
@@ -110,7 +135,46 @@ std::string build_bst_host(const BstParams& p, BstHost& h) {
     h.cmean[k] = F2{(float)(cr * inv), (float)(ci * inv)};
   }
   if (p.filter) build_ramp_taps(nt, p.lam, p.cutoff, h.M, h.Lr, h.ramp);
+  // chord weights of the exact mean (bst.py:173-180)
+  if (p.dc_mode == 0) {
+    h.chord.resize((size_t)nt * p.ntheta);
+    const double dth = kPi / p.ntheta;
+    for (int j = 0; j < p.ntheta; ++j) {
+      const double c = std::cos(j * dth), sn = std::sin(j * dth);
+      for (int t = 0; t < nt; ++t)
+        h.chord[(size_t)t * p.ntheta + j] = (float)(square_chord(-1.0 + t * dt, c, sn) * dt * dth / 4.0);
+    }
+  }
+  // gridding coordinates on the quadrant (grids.py:477-494), fp64
+  {
+    const int hb = big / 2;
+    h.qw_pitch = hb + 1;
+    h.grid_q.assign((size_t)hb * h.qw_pitch * 2, 0u);
+    const int nsig = h.m_need, nray = h.nray;
+    const double dphi = 2.0 * kPi / nray;
+    const int nthreads = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int tid = 0; tid < nthreads; ++tid) {
+      pool.emplace_back([&, tid]() {
+        for (int ky = tid; ky < hb; ky += nthreads) {
+          const double wy = (kPi * (double)ky) * (h.dw / kPi);
+          for (int qx = 0; qx <= hb; ++qx) {
+            const double wx = (kPi * (double)qx) * (h.dw / kPi);
+            const double fi = std::min(std::hypot(wx, wy) / h.dsigma, nsig - 1.0);
+            double th = std::atan2(wy, wx);
+            if (th < 0) th += 2.0 * kPi;
+            const double fj = th / dphi;
+            uint32_t* e = &h.grid_q[((size_t)ky * h.qw_pitch + qx) * 2];
+            e[0] = pack_coord(fi);
+            e[1] = pack_coord(fj);
+          }
+        }
+      });
+    }
+    for (auto& t : pool) t.join();
+  }
   h.supported = is_pow2(h.L) && h.L >= 512 && h.L <= 8192 && is_pow2(big) && big >= 256 && big <= 4096 &&
+                h.m_need < 8192 && h.nray / 4 + 1 < 8192 &&  // 13-bit gridding indices
                 (nt % 2) == 0 && (!p.filter || h.M <= 4096);
   return "";
 }

@@ -50,27 +50,15 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;  // valid in thread 0
 }
 
-// Chord of the line x . (cos th, sin th) = t through [-1, 1]^2 (radon.py:183-209).
-__device__ double square_chord(double t, double c, double s) {
-  const double big = 1e30;
-  const bool sx = fabs(s) > 1e-15, sy = fabs(c) > 1e-15;
-  const double lo_x = sx ? (t * c - 1.0) / s : -big, hi_x = sx ? (t * c + 1.0) / s : big;
-  const double lo_y = sy ? (-t * s - 1.0) / c : -big, hi_y = sy ? (-t * s + 1.0) / c : big;
-  const double lo = fmax(fmin(lo_x, hi_x), fmin(lo_y, hi_y));
-  const double hi = fmin(fmax(lo_x, hi_x), fmax(lo_y, hi_y));
-  const bool ok = (sx || fabs(t * c) <= 1.0) && (sy || fabs(t * s) <= 1.0);
-  return ok ? fmax(0.0, hi - lo) : 0.0;
-}
-
 // ---------------------------------------------------------------------------
 // KB1: TC sinogram columns per CTA staged in smem (coalesced float4 loads), G
 // FFT groups; column c gives half-rays c (t = +s) and c + ntheta (t = -s).
 // ---------------------------------------------------------------------------
 template <int L, int TC, int G, bool IN_HALF>
-__global__ void __launch_bounds__(G * FftPlan<L, false>::T)
+__global__ void __launch_bounds__(G * FftPlan<L, false>::T, 2)
 k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int ntheta, int ns, int m_need, int m_pad,
              const int2* __restrict__ tap_base, const float4* __restrict__ tap_w, const float* __restrict__ kern,
-             const float2* __restrict__ tw, double* __restrict__ acc, int want_mean) {
+             const float2* __restrict__ tw, double* __restrict__ acc, const float* __restrict__ chord) {
   constexpr int T = FftPlan<L, false>::T;
   constexpr int TP = TC + 1;
   constexpr int V = TC / 4;
@@ -78,7 +66,6 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
   float* tile = reinterpret_cast<float*>(smem_b1);  // nt * TP
   float2* bufs = smem_b1 + ((nt * TP + 3) / 4) * 2;
   __shared__ double red[32];
-  __shared__ double csn[TC][2];
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   float2* buf = bufs + gi * padded_len(L);
   const int c0 = blockIdx.x * TC;
@@ -101,22 +88,15 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
       tile[t * TP + c] = c < nc ? __ldg(src + (size_t)t * ntheta + c) : 0.f;
     }
   }
-  if (threadIdx.x < TC) {
-    double sn, cs;
-    sincos((c0 + threadIdx.x) * (3.14159265358979323846 / ntheta), &sn, &cs);
-    csn[threadIdx.x][0] = cs;
-    csn[threadIdx.x][1] = sn;
-  }
   __syncthreads();
-  if (want_mean) {  // <g, chord> over this tile (bst.py:173-180), fp64
-    const double dt = 2.0 / nt, dth = 3.14159265358979323846 / ntheta;
+  if (chord) {  // <g, chord> dt dtheta / 4 over this tile (bst.py:173-180), fp64 accumulation
     double part = 0.0;
     for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
       const int t = e / TC, c = e % TC;
-      if (c < nc) part += (double)tile[t * TP + c] * square_chord(-1.0 + t * dt, csn[c][0], csn[c][1]);
+      if (c < nc) part += (double)tile[t * TP + c] * (double)__ldg(chord + (size_t)t * ntheta + c0 + c);
     }
     const double s = block_sum(part, red);
-    if (threadIdx.x == 0) atomicAdd(acc + 2 * b, s * dt * dth / 4.0);
+    if (threadIdx.x == 0) atomicAdd(acc + 2 * b, s);
   }
   for (int round = 0; round < TC / G; ++round) {
     const int c = round * G + gi;
@@ -160,7 +140,7 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
 template <int BIG, int TR, int G>
 __global__ void __launch_bounds__(G * FftPlan<BIG, true>::T)
 k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int nsig, int m_pad, int n, int p0,
-             float inv_dsigma, float inv_dphi, float dw, const float2* __restrict__ tau,
+             const uint2* __restrict__ gq, int qpitch, const float2* __restrict__ tau,
              const float2* __restrict__ cmean, const float2* __restrict__ tw, double* __restrict__ acc) {
   constexpr int T = FftPlan<BIG, true>::T;
   constexpr int HB = BIG / 2;
@@ -177,26 +157,29 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
   for (int rr = 0; rr < TR / G; ++rr) {
     const int r = rr * G + gi;
     const int ky = ky0 + r;
-    const int kfy = ky < HB ? ky : ky - BIG;  // ky < BIG/2 here
-    const float wy = dw * (float)kfy;
     const float2 ty = __ldg(tau + ky);
+    const uint2* gqr = gq + (size_t)ky * qpitch;
     auto load = [&](int kx) -> float2 {
       if (kx == HB || ky == HB) return make_float2(0.f, 0.f);  // Nyquist row / column (bst.py:157-160)
-      const int kfx = kx < HB ? kx : kx - BIG;
-      const float wx = dw * (float)kfx;
-      float fi = hypotf(wx, wy) * inv_dsigma;
-      fi = fminf(fi, (float)(nsig - 1));
-      const float fil = floorf(fi);
-      const int i0 = (int)fil;
+      // fp64-built coordinates of (|kfx|, ky); kfx < 0 reflects theta -> pi - theta
+      const bool neg = kx > HB;
+      const uint2 e = __ldg(gqr + (neg ? BIG - kx : kx));
+      const int i0 = (int)(e.x & 0x1FFFu);
       const int i1 = min(i0 + 1, nsig - 1);
-      const float wi = fi - fil;
-      float th = atan2f(wy, wx);
-      if (th < 0.f) th += 6.28318530717958647692f;
-      const float fj = th * inv_dphi;
-      const float fjl = floorf(fj);
-      const float wj = fj - fjl;
-      int j0 = (int)fjl % nray;
-      if (j0 < 0) j0 += nray;
+      const float wi = (float)(e.x >> 13) * (1.f / 524288.f);
+      int j0 = (int)(e.y & 0x1FFFu);
+      uint32_t qj = e.y >> 13;
+      if (neg) {  // fj' = nray/2 - fj
+        if (qj == 0) {
+          j0 = nray / 2 - j0;
+        } else {
+          j0 = nray / 2 - j0 - 1;
+          qj = 524288u - qj;
+        }
+        if (j0 < 0) j0 += nray;
+      }
+      if (j0 >= nray) j0 -= nray;
+      const float wj = (float)qj * (1.f / 524288.f);
       const int j1 = j0 + 1 == nray ? 0 : j0 + 1;
       // the mirror bin -k is the same radius at theta + pi: rays shifted by nray/2
       // (numpy pairs the origin bin with itself, not with theta + pi)
@@ -321,13 +304,13 @@ cudaError_t radial_impl(const BstDims& d, const BstTables& t, const float* g, fl
     if ((e = prep(k, smem))) return e;
     k<<<dim3((d.ntheta + TC - 1) / TC, batch), G * T, smem, s>>>(g, P, d.nt, d.ntheta, d.ns, d.m_need, d.m_pad,
                                                                   t.tap_base, t.tap_w, t.kern, t.tw_L, acc,
-                                                                  d.subtract_mean);
+                                                                  d.subtract_mean ? t.chord : nullptr);
   } else {
     auto k = k_bst_radial<L, TC, G, false>;
     if ((e = prep(k, smem))) return e;
     k<<<dim3((d.ntheta + TC - 1) / TC, batch), G * T, smem, s>>>(g, P, d.nt, d.ntheta, d.ns, d.m_need, d.m_pad,
                                                                   t.tap_base, t.tap_w, t.kern, t.tw_L, acc,
-                                                                  d.subtract_mean);
+                                                                  d.subtract_mean ? t.chord : nullptr);
   }
   return cudaGetLastError();
 }
@@ -345,9 +328,8 @@ cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, flo
     auto k = k_bst_grid_x<BIG, TR, GX>;
     cudaError_t e = prep(k, smem);
     if (e) return e;
-    k<<<dim3((BIG / 2) / TR, batch), GX * T, smem, s>>>(P, X, d.nray, d.m_need, d.m_pad, d.n, d.p0,
-                                                         (float)(1.0 / d.dsigma), (float)(d.nray / 6.283185307179586),
-                                                         (float)d.dw, t.tau, t.cmean, t.tw_big, acc);
+    k<<<dim3((BIG / 2) / TR, batch), GX * T, smem, s>>>(P, X, d.nray, d.m_need, d.m_pad, d.n, d.p0, t.grid_q,
+                                                         BIG / 2 + 1, t.tau, t.cmean, t.tw_big, acc);
     if ((e = cudaGetLastError())) return e;
   }
   {
