@@ -314,3 +314,46 @@ def test_sector_validation_messages_match_oracle():
             assert got == msg
     rc, _ = _sector_plan(64, 32, 16, [(0.0, math.pi / 2, 0.25)] * 33)
     assert rc == N.LPBP_EINVAL and "at most 32 sectors" in N.lib().lpbp_last_error().decode()
+
+
+# ---- BST engine plans, host-only ----
+
+def _bst_plan(nt, nth, n, beta=0.0, zero_pad=2.0, dc_mode=0, filt=0):
+    p = N.BstParams()
+    p.nt, p.ntheta, p.n_out, p.beta, p.zero_pad, p.dc_mode, p.filter = nt, nth, n, beta, zero_pad, dc_mode, filt
+    p.lam, p.cutoff, p.device = 0.0, 1.0, -1
+    h = c_void_p()
+    return N.lib().lpbp_bst_plan_create(byref(p), byref(h)), h
+
+
+@pytest.mark.parametrize("nt,nth,n,zp,supported", [(256, 256, 256, 2.0, 1), (512, 512, 512, 2.0, 1),
+                                                   (2048, 2048, 2048, 2.0, 1), (256, 180, 128, 3.0, 0),
+                                                   (200, 96, 101, 2.0, 0), (256, 180, 128, 1.0, 1)])
+def test_bst_geometry_matches_oracle(nt, nth, n, zp, supported):
+    rc, h = _bst_plan(nt, nth, n, zero_pad=zp)
+    assert rc == N.LPBP_OK, N.lib().lpbp_last_error()
+    try:
+        inf = N.BstInfo()
+        assert N.lib().lpbp_bst_get_info(h, byref(inf)) == N.LPBP_OK
+        ns, ds, L, dsigma, m_need = O.bst_geometry(nt, n, zp)
+        assert (inf.ns, inf.L, inf.m_need, inf.nray, inf.big) == (ns, L, m_need, 2 * nth, 2 * n)
+        assert inf.ds == pytest.approx(ds, rel=1e-15) and inf.dsigma == pytest.approx(dsigma, rel=1e-15)
+        assert inf.out_scale == pytest.approx(O.BST_SCALE / 16.0, rel=1e-15)
+        assert inf.supported == supported
+    finally:
+        N.lib().lpbp_bst_plan_destroy(h)
+
+
+def test_bst_validation_messages_match_oracle():
+    for kw, args in ((dict(n_out=1), (64, 32, 1)), (dict(n_out=8, beta=-1.0), (64, 32, 8, -1.0)),
+                     (dict(n_out=8, zero_pad=0.5), (64, 32, 8, 0.0, 0.5)),
+                     (dict(n_out=8, dc_mode="x"), (64, 32, 8, 0.0, 2.0, 7))):
+        rc, _ = _bst_plan(*args)
+        assert rc == N.LPBP_EINVAL
+        with pytest.raises(ValueError) as e:
+            O.bst_validate(**kw)
+        assert N.lib().lpbp_last_error().decode() == str(e.value)
+    rc, _ = _bst_plan(64, 32, 256)
+    with pytest.raises(ValueError) as e:
+        O.bst_geometry(64, 256)
+    assert rc == N.LPBP_EINVAL and N.lib().lpbp_last_error().decode() == str(e.value)
