@@ -37,9 +37,9 @@ try:
 except (OSError, ValueError):
     MEASURED = {}
 # dram__bytes_read.sum + dram__bytes_write.sum per slice from the committed ncu --set full
-# capture (profiles/r01d_summary.md, 32-slice launches at 2048^2 FBP)
-TRAFFIC_PER_SLICE = {"rho_conv": (1.212462e9 + 1.906935e9) / 32, "irdft_readout": (3.017933e9 + 0.816704e9) / 32,
-                     "ramp_filter": (0.536975e9 + 0.497815e9) / 32, "row_rdft": (0.536896e9 + 1.022953e9) / 32}
+# capture (profiles/r01e_summary.md, 8-slice launches at 2048^2 FBP, the bench's chunk)
+TRAFFIC_PER_SLICE = {"rho_conv": (403.260928e6 + 442.394624e6) / 8, "irdft_readout": (718.455552e6 + 181.567232e6) / 8,
+                     "ramp_filter": (134.275328e6 + 94.606080e6) / 8, "row_rdft": (134.241536e6 + 215.952384e6) / 8}
 UNIT = "slices/s"
 
 
@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--slices", type=int, default=0, help="slices per rank per step (0 = config default)")
-    ap.add_argument("--chunk", type=int, default=32, help="slices per internal pipeline chunk")
+    ap.add_argument("--chunk", type=int, default=8, help="slices per internal pipeline chunk (8 x 2 streams measured best)")
     ap.add_argument("--e2e-slices", type=int, default=128)
     ap.add_argument("--e2e-chunk", type=int, default=4)
     ap.add_argument("--streams", type=int, default=2, help="CUDA streams the device-resident chunks alternate on")
