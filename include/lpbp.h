@@ -175,7 +175,7 @@ int lpbp_sector_logpolar(const lpbp_sector_plan* plan, int32_t index, const floa
  * gridding with Hermitian averaging on the 2x padded lattice (grids.py:456-508), inverse 2-D
  * DFT with the phase ramps, crop (bst.py:146-170), BST_SCALE, and in subtract_mean mode the
  * exact spatial mean from <g, chord> (bst.py:173-180, 196-202).  This build runs power-of-two
- * radial DFT lengths L in [512, 8192] and padded sides 2 n in [256, 4096]; other sizes return
+ * radial DFT lengths L in [512, 8192] and padded sides 2 n in [128, 4096]; other sizes return
  * LPBP_EUNSUPPORTED after validation. */
 typedef struct lpbp_bst_plan lpbp_bst_plan;
 

@@ -173,7 +173,7 @@ std::string build_bst_host(const BstParams& p, BstHost& h) {
     }
     for (auto& t : pool) t.join();
   }
-  h.supported = is_pow2(h.L) && h.L >= 512 && h.L <= 8192 && is_pow2(big) && big >= 256 && big <= 4096 &&
+  h.supported = is_pow2(h.L) && h.L >= 512 && h.L <= 8192 && is_pow2(big) && big >= 128 && big <= 4096 &&
                 h.m_need < 8192 && h.nray / 4 + 1 < 8192 &&  // 13-bit gridding indices
                 (nt % 2) == 0 && (!p.filter || h.M <= 4096);
   return "";

@@ -46,7 +46,7 @@ struct BstHost {
   // fbp: ramp filter on the M-point circular embedding (as the log-polar plan)
   int M = 0, Lr = 0;
   std::vector<float> ramp;
-  // support (this build): power-of-two L in [512, 8192] and big in [256, 4096]
+  // support (this build): power-of-two L in [512, 8192] and big in [128, 4096]
   bool supported = false;
 };
 

@@ -362,6 +362,7 @@ cudaError_t launch_bst_radial(const BstDims& d, const BstTables& t, const float*
 cudaError_t launch_bst_grid(const BstDims& d, const BstTables& t, const float2* P, float2* X, float* img, double* acc,
                             int batch, cudaStream_t s) {
   switch (d.big) {
+    case 128: return grid_impl<128>(d, t, P, X, img, acc, batch, s);
     case 256: return grid_impl<256>(d, t, P, X, img, acc, batch, s);
     case 512: return grid_impl<512>(d, t, P, X, img, acc, batch, s);
     case 1024: return grid_impl<1024>(d, t, P, X, img, acc, batch, s);

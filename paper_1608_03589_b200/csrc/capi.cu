@@ -1056,7 +1056,7 @@ int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan) {
     delete P;
     return fail(LPBP_EUNSUPPORTED, "BST engine: no kernel instantiation for radial DFT length L=" + std::to_string(L) +
                                        " / padded side " + std::to_string(2 * n) +
-                                       " (this build: powers of two, L in [512, 8192], 2n in [256, 4096])");
+                                       " (this build: powers of two, L in [512, 8192], 2n in [128, 4096])");
   }
   auto& d = P->d;
   d.nt = h.p.nt;

@@ -327,6 +327,7 @@ __device__ __forceinline__ void pass_smem(float2* buf, int ti, const float2* __r
 // Radix plans (forward order; the inverse runs them reversed).  Every plan
 // starts with radix 16 so Ns >= 16 for every store after the first pass.
 template <int N> struct RadixPlan;
+template <> struct RadixPlan<128>   { static constexpr int P = 2; static constexpr int r[3] = {16, 8, 1};  static constexpr int E = 16; };
 template <> struct RadixPlan<256>   { static constexpr int P = 2; static constexpr int r[3] = {16, 16, 1}; static constexpr int E = 16; };
 template <> struct RadixPlan<512>   { static constexpr int P = 3; static constexpr int r[3] = {16, 8, 4};  static constexpr int E = 16; };
 template <> struct RadixPlan<1024>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 4}; static constexpr int E = 16; };

@@ -1079,6 +1079,7 @@ cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2
 
 int twiddle_table_len(int N) {
   switch (N) {
+    case 128: return TwTable<128>::len;
     case 256: return TwTable<256>::len;
     case 512: return TwTable<512>::len;
     case 1024: return TwTable<1024>::len;
@@ -1094,6 +1095,7 @@ cudaError_t launch_init_twiddles(int N, float2* out, cudaStream_t s) {
   if (len < 0) return cudaErrorNotSupported;
   const dim3 grid((len + 255) / 256);
   switch (N) {
+    case 128: k_init_twiddles<128><<<grid, 256, 0, s>>>(out); break;
     case 256: k_init_twiddles<256><<<grid, 256, 0, s>>>(out); break;
     case 512: k_init_twiddles<512><<<grid, 256, 0, s>>>(out); break;
     case 1024: k_init_twiddles<1024><<<grid, 256, 0, s>>>(out); break;

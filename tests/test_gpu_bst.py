@@ -69,6 +69,15 @@ def test_bst_options(pkg, golden):
     assert report("bst zero_pad=1", zp, O.bst_backproject(g, 128, zero_pad=1.0)) <= RTOL
 
 
+@pytest.mark.parametrize("nt,nth,n,kw", [(256, 180, 64, dict(zero_pad=2.0)), (256, 180, 64, dict(zero_pad=4.0, beta=8.0)),
+                                         (128, 90, 64, {}), (512, 360, 128, dict(zero_pad=8.0))])
+def test_bst_reference_script_sizes(pkg, nt, nth, n, kw):
+    """The sizes and options the reference's own BST experiments use (n 64/128, z 2/4/8)."""
+    g = phantoms.sinogram(700 + nt + n, nt, nth, 8, 0.05, 0.35, 0.01).astype(np.float64)
+    img = pkg.bst_backproject(pkg.Sinogram(nt, nth, g), pkg.BstOptions(n_out=n, **kw)).values
+    assert report(f"bst {nt}x{nth}->{n} {kw}", img, O.bst_backproject(g, n, **kw)) <= RTOL
+
+
 def test_bst_radial_stage(pkg, golden):
     z = golden("bst.npz")
     g = z["opt_sino"].astype(np.float64)
@@ -120,3 +129,5 @@ def test_bst_errors(pkg):
     # sizes this build does not instantiate fail loudly (no fallback)
     with pytest.raises(NotImplementedError):
         pkg.bst_backproject(pkg.Sinogram(200, 96, np.ones((200, 96))), pkg.BstOptions(n_out=101))
+    with pytest.raises(NotImplementedError):  # zero_pad = 3: L = 1536 is not a power of two
+        pkg.bst_backproject(pkg.Sinogram(256, 180, np.ones((256, 180))), pkg.BstOptions(n_out=128, zero_pad=3.0))
