@@ -30,18 +30,6 @@ double bessel_i0(double x) {
 
 bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
-// Chord of the line x . (cos th, sin th) = t through [-1, 1]^2 (radon.py:183-209).
-double square_chord(double t, double c, double s) {
-  const double big = 1e30;
-  const bool sx = std::fabs(s) > 1e-15, sy = std::fabs(c) > 1e-15;
-  const double lo_x = sx ? (t * c - 1.0) / s : -big, hi_x = sx ? (t * c + 1.0) / s : big;
-  const double lo_y = sy ? (-t * s - 1.0) / c : -big, hi_y = sy ? (-t * s + 1.0) / c : big;
-  const double lo = std::max(std::min(lo_x, hi_x), std::min(lo_y, hi_y));
-  const double hi = std::min(std::max(lo_x, hi_x), std::max(lo_y, hi_y));
-  const bool ok = (sx || std::fabs(t * c) <= 1.0) && (sy || std::fabs(t * s) <= 1.0);
-  return ok ? std::max(0.0, hi - lo) : 0.0;
-}
-
 // (13-bit index, 19-bit fixed-point weight) of a clamped fractional coordinate
 uint32_t pack_coord(double f) {
   double fl = std::floor(f);
@@ -135,14 +123,18 @@ std::string build_bst_host(const BstParams& p, BstHost& h) {
     h.cmean[k] = F2{(float)(cr * inv), (float)(ci * inv)};
   }
   if (p.filter) build_ramp_taps(nt, p.lam, p.cutoff, h.M, h.Lr, h.ramp);
-  // chord weights of the exact mean (bst.py:173-180)
+  // chord weights of the exact mean (bst.py:173-180): for |cos|, |sin| the chord of the line
+  // x . xi = t through [-1, 1]^2 is a trapezoid in t; the reference's degenerate axes
+  // (|cos| or |sin| <= 1e-15) give 2 on |t| <= 1
   if (p.dc_mode == 0) {
-    h.chord.resize((size_t)nt * p.ntheta);
+    h.chord_col.resize(p.ntheta);
     const double dth = kPi / p.ntheta;
     for (int j = 0; j < p.ntheta; ++j) {
-      const double c = std::cos(j * dth), sn = std::sin(j * dth);
-      for (int t = 0; t < nt; ++t)
-        h.chord[(size_t)t * p.ntheta + j] = (float)(square_chord(-1.0 + t * dt, c, sn) * dt * dth / 4.0);
+      const double c = std::fabs(std::cos(j * dth)), sn = std::fabs(std::sin(j * dth));
+      const bool deg = c <= 1e-15 || sn <= 1e-15;
+      const double t1 = deg ? 1.0 : std::fabs(c - sn), t2 = deg ? 1.0 : c + sn;
+      const double lmax = deg ? 2.0 : 2.0 / std::max(c, sn);
+      h.chord_col[j] = F4{(float)t1, (float)t2, (float)(lmax * dt * dth / 4.0), t2 > t1 ? (float)(1.0 / (t2 - t1)) : 0.f};
     }
   }
   // gridding coordinates on the quadrant (grids.py:477-494), fp64

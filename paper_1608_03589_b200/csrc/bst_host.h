@@ -37,7 +37,9 @@ struct BstHost {
   std::vector<float> kern;   // [m_need] ds * (1/sigma or DC rule) * 1/2 (Hermitian averaging)
   std::vector<F2> tau;       // [big] phase ramp exp(i dw k ((0.5 - p0) dx - 1)), FFT order
   std::vector<F2> cmean;     // [big] sum_{y in crop} exp(2 pi i k y / big) / n^2 (crop mean from a row)
-  std::vector<float> chord;  // [nt][ntheta] square_chord(t, theta) * dt * dtheta / 4 (subtract_mean)
+  // chord of the square as a trapezoid in t per angle (subtract_mean): (t1, t2, Lmax * dt * dtheta / 4,
+  // 1 / (t2 - t1)) with chord = Lmax for |t| <= t1, linear to 0 at |t| = t2 (radon.py:183-209)
+  std::vector<F4> chord_col;  // [ntheta]
   // gridding coordinates of the quadrant kx, ky >= 0 (fp64, grids.py:477-494): qx in [0, big/2],
   // ky in [0, big/2); .x = i0 | q(wi) << 13, .y = j0 | q(wj) << 13, 19-bit fixed-point weights.
   // Points with kfx < 0 reflect theta -> pi - theta in index space.

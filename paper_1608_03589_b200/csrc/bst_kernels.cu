@@ -58,7 +58,7 @@ template <int L, int TC, int G, bool IN_HALF>
 __global__ void __launch_bounds__(G * FftPlan<L, false>::T, 2)
 k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int ntheta, int ns, int m_need, int m_pad,
              const int2* __restrict__ tap_base, const float4* __restrict__ tap_w, const float* __restrict__ kern,
-             const float2* __restrict__ tw, double* __restrict__ acc, const float* __restrict__ chord) {
+             const float2* __restrict__ tw, double* __restrict__ acc, const float4* __restrict__ chord) {
   constexpr int T = FftPlan<L, false>::T;
   constexpr int TP = TC + 1;
   constexpr int V = TC / 4;
@@ -91,9 +91,15 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
   __syncthreads();
   if (chord) {  // <g, chord> dt dtheta / 4 over this tile (bst.py:173-180), fp64 accumulation
     double part = 0.0;
+    const float dt = 2.f / nt;
     for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
       const int t = e / TC, c = e % TC;
-      if (c < nc) part += (double)tile[t * TP + c] * (double)__ldg(chord + (size_t)t * ntheta + c0 + c);
+      if (c < nc) {
+        const float4 cp = __ldg(chord + c0 + c);
+        const float a = fabsf(-1.f + t * dt);
+        const float ch = a <= cp.x ? cp.z : (a < cp.y ? cp.z * (cp.y - a) * cp.w : 0.f);
+        part += (double)tile[t * TP + c] * (double)ch;
+      }
     }
     const double s = block_sum(part, red);
     if (threadIdx.x == 0) atomicAdd(acc + 2 * b, s);

@@ -10,7 +10,7 @@ struct BstTables {
   const float* kern;      // [m_need] radial kernel incl. ds and the Hermitian 1/2
   const float2* tau;      // [big] phase ramp
   const float2* cmean;    // [big] crop-mean weights
-  const float* chord;     // [nt][ntheta] chord * dt * dtheta / 4 (subtract_mean)
+  const float4* chord;    // [ntheta] chord trapezoid (t1, t2, Lmax dt dtheta / 4, 1/(t2 - t1)) (subtract_mean)
   const uint2* grid_q;    // [big/2][big/2 + 1] quadrant gridding coordinates
   const float2* tw_L;     // pass twiddles, N = L
   const float2* tw_big;   // pass twiddles, N = big

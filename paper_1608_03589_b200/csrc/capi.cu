@@ -1093,8 +1093,8 @@ int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan) {
     if (!rc) P->t.tau = static_cast<const float2*>(p);
     rc = rc ? rc : P->upload(h.cmean, &p);
     if (!rc) P->t.cmean = static_cast<const float2*>(p);
-    rc = rc ? rc : P->upload(h.chord, &p);
-    if (!rc) P->t.chord = h.chord.empty() ? nullptr : static_cast<const float*>(p);
+    rc = rc ? rc : P->upload(h.chord_col, &p);
+    if (!rc) P->t.chord = h.chord_col.empty() ? nullptr : static_cast<const float4*>(p);
     rc = rc ? rc : P->upload(h.grid_q, &p);
     if (!rc) P->t.grid_q = static_cast<const uint2*>(p);
     rc = rc ? rc : P->twiddles(h.L, &P->t.tw_L);
