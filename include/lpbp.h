@@ -174,9 +174,10 @@ int lpbp_sector_logpolar(const lpbp_sector_plan* plan, int32_t index, const floa
  * real DFTs along s (bst.py:120-143), 1/sigma kernel, bilinear polar -> Cartesian frequency
  * gridding with Hermitian averaging on the 2x padded lattice (grids.py:456-508), inverse 2-D
  * DFT with the phase ramps, crop (bst.py:146-170), BST_SCALE, and in subtract_mean mode the
- * exact spatial mean from <g, chord> (bst.py:173-180, 196-202).  This build runs power-of-two
- * radial DFT lengths L in [512, 8192] and padded sides 2 n in [128, 4096]; other sizes return
- * LPBP_EUNSUPPORTED after validation. */
+ * exact spatial mean from <g, chord> (bst.py:173-180, 196-202).  This build runs radial DFT
+ * lengths L that are powers of two in [512, 8192] or at most 4096 (Bluestein), padded sides 2 n
+ * that are powers of two in [128, 4096] or at most 4096 (Bluestein), and even nt; other sizes
+ * return LPBP_EUNSUPPORTED after validation. */
 typedef struct lpbp_bst_plan lpbp_bst_plan;
 
 typedef struct lpbp_bst_params {

@@ -165,9 +165,16 @@ std::string build_bst_host(const BstParams& p, BstHost& h) {
     }
     for (auto& t : pool) t.join();
   }
-  h.supported = is_pow2(h.L) && h.L >= 512 && h.L <= 8192 && is_pow2(big) && big >= 128 && big <= 4096 &&
+  auto pow2_at_least = [](int v) { int q = 1; while (q < v) q <<= 1; return q; };
+  const bool L_direct = is_pow2(h.L) && h.L >= 512 && h.L <= 8192;
+  const bool big_direct = is_pow2(big) && big >= 128 && big <= 4096;
+  if (!L_direct) h.mb_L = std::max(512, pow2_at_least(2 * h.L));
+  if (!big_direct) h.mb_big = std::max(256, pow2_at_least(2 * big));
+  h.supported = (L_direct || h.mb_L <= 8192) && (big_direct || h.mb_big <= 8192) &&
                 h.m_need < 8192 && h.nray / 4 + 1 < 8192 &&  // 13-bit gridding indices
                 (nt % 2) == 0 && (!p.filter || h.M <= 4096);
+  if (h.supported && h.mb_L) bluestein_tables(h.L, h.mb_L, false, h.chirp_L, h.bhat_L);
+  if (h.supported && h.mb_big) bluestein_tables(big, h.mb_big, true, h.chirp_big, h.bhat_big);
   return "";
 }
 

@@ -48,7 +48,11 @@ struct BstHost {
   // fbp: ramp filter on the M-point circular embedding (as the log-polar plan)
   int M = 0, Lr = 0;
   std::vector<float> ramp;
-  // support (this build): power-of-two L in [512, 8192] and big in [128, 4096]
+  // generic sizes: Bluestein on pow2 convolutions (0 = the direct power-of-two FFT)
+  int mb_L = 0, mb_big = 0;
+  std::vector<F2> chirp_L, bhat_L, chirp_big, bhat_big;
+  // support (this build): L a power of two in [512, 8192] or 2 L <= 8192 (Bluestein);
+  // big a power of two in [128, 4096] or 2 big <= 8192 (Bluestein)
   bool supported = false;
 };
 

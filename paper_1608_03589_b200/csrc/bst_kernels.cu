@@ -38,6 +38,34 @@ struct GroupBarT {
   }
 };
 
+// Length-`len` DFT through either the power-of-two FFT (GEN = false, N = len) or
+// Bluestein's identity on an N-point circular convolution (GEN = true, N = pow2 >=
+// 2 len): forward X[m] = c[m] sum_n x[n] c[n] conj c[m-n], inverse with conjugates,
+// c[n] = exp(-i pi n^2 / len) (the generic path of the log-polar engine, kernels.cu).
+struct Chirp {
+  const float2* c;     // [len]
+  const float2* bhat;  // [N] FFT_N of the chirp filter / N
+  int len;
+};
+template <int N, bool INV, bool GEN, bool IN_HALF, bool LAST_SYNC, typename Load, typename Store, typename Sync>
+__device__ __forceinline__ void dft(float2* buf, int ti, const float2* tw, const Chirp& ch, Load&& load, Store&& store,
+                                    Sync&& sync) {
+  if constexpr (!GEN) {
+    block_fft<N, INV, LAST_SYNC, false, IN_HALF, 16>(buf, ti, tw, load, store, sync);
+  } else {
+    auto ld = [&](int idx) -> float2 {
+      if (idx >= ch.len) return make_float2(0.f, 0.f);
+      const float2 v = load(idx);
+      return INV ? cmulc(v, __ldg(ch.c + idx)) : cmul(v, __ldg(ch.c + idx));
+    };
+    auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(ch.bhat + idx)); };
+    auto st = [&](int idx, float2 v) {
+      if (idx < ch.len) store(idx, INV ? cmulc(v, __ldg(ch.c + idx)) : cmul(v, __ldg(ch.c + idx)));
+    };
+    block_conv<N, true, 16>(buf, ti, tw, ld, mul, st, sync);  // len <= N/2: half-zero in, low half out
+  }
+}
+
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -54,11 +82,13 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // KB1: TC sinogram columns per CTA staged in smem (coalesced float4 loads), G
 // FFT groups; column c gives half-rays c (t = +s) and c + ntheta (t = -s).
 // ---------------------------------------------------------------------------
-template <int L, int TC, int G, bool IN_HALF>
+// GEN: L is the Bluestein convolution size MB and the DFT length is ch.len; the
+// spectrum then goes to a separate zbuf (block_conv has no trailing barrier).
+template <int L, int TC, int G, bool IN_HALF, bool GEN>
 __global__ void __launch_bounds__(G * FftPlan<L, false>::T, 2)
 k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int ntheta, int ns, int m_need, int m_pad,
              const int2* __restrict__ tap_base, const float4* __restrict__ tap_w, const float* __restrict__ kern,
-             const float2* __restrict__ tw, double* __restrict__ acc, const float4* __restrict__ chord) {
+             const float2* __restrict__ tw, double* __restrict__ acc, const float4* __restrict__ chord, Chirp ch) {
   constexpr int T = FftPlan<L, false>::T;
   constexpr int TP = TC + 1;
   constexpr int V = TC / 4;
@@ -68,6 +98,8 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
   __shared__ double red[32];
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   float2* buf = bufs + gi * padded_len(L);
+  float2* zbuf = GEN ? bufs + G * padded_len(L) + gi * padded_len(L / 2) : buf;
+  const int Lr = GEN ? ch.len : L;  // DFT length
   const int c0 = blockIdx.x * TC;
   const int nc = min(TC, ntheta - c0);  // ragged last tile
   const int b = blockIdx.y;
@@ -115,20 +147,20 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
       const float m = w.z * tile[bb.y * TP + c] + w.w * tile[(bb.y + 1) * TP + c];
       return make_float2(a, m);
     };
-    auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
-    if constexpr (IN_HALF) {
+    auto store = [&](int idx, float2 v) { zbuf[pad16(idx)] = v; };
+    if constexpr (IN_HALF || GEN) {
       auto load_h = [&](int k) -> float2 { return k < ns ? load(k) : make_float2(0.f, 0.f); };
-      block_fft<L, false, true, false, true, 16>(buf, ti, tw, load_h, store, GroupBarT<T>{1 + gi});
+      dft<L, false, GEN, true, true>(buf, ti, tw, ch, load_h, store, GroupBarT<T>{1 + gi});
     } else {
-      block_fft<L, false, true, false, false, 16>(buf, ti, tw, load, store, GroupBarT<T>{1 + gi});
+      dft<L, false, GEN, false, true>(buf, ti, tw, ch, load, store, GroupBarT<T>{1 + gi});
     }
     GroupBarT<T>{1 + gi}();
     // separate the packed spectra: A = (Z[m] + conj Z[-m]) / 2, B = (Z[m] - conj Z[-m]) / 2i
     float2* pa = P + ((size_t)b * 2 * ntheta + c0 + c) * m_pad;
     float2* pb = P + ((size_t)b * 2 * ntheta + c0 + c + ntheta) * m_pad;
     for (int m = ti; m < m_need && c < nc; m += T) {
-      const float2 z = buf[pad16(m)];
-      const float2 w = buf[pad16((L - m) & (L - 1))];
+      const float2 z = zbuf[pad16(m)];
+      const float2 w = zbuf[pad16(m == 0 ? 0 : Lr - m)];
       const float k = __ldg(kern + m);
       pa[m] = make_float2(0.5f * (z.x + w.x) * k, 0.5f * (z.y - w.y) * k);
       pb[m] = make_float2(0.5f * (z.y + w.y) * k, 0.5f * (w.x - z.x) * k);
@@ -143,13 +175,15 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
 // written transposed X[x][ky] (TR consecutive ky per run); accumulates the
 // crop mean through cmean (sum over the crop rows of the row's DFT weights).
 // ---------------------------------------------------------------------------
-template <int BIG, int TR, int G>
+// GEN: BIG is the Bluestein convolution size and the padded side is ch.len.
+template <int BIG, int TR, int G, bool GEN>
 __global__ void __launch_bounds__(G * FftPlan<BIG, true>::T)
 k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int nsig, int m_pad, int n, int p0,
              const uint2* __restrict__ gq, int qpitch, const float2* __restrict__ tau,
-             const float2* __restrict__ cmean, const float2* __restrict__ tw, double* __restrict__ acc) {
+             const float2* __restrict__ cmean, const float2* __restrict__ tw, double* __restrict__ acc, Chirp ch) {
   constexpr int T = FftPlan<BIG, true>::T;
-  constexpr int HB = BIG / 2;
+  const int big = GEN ? ch.len : BIG;
+  const int HB = big / 2;
   extern __shared__ __align__(16) float2 smem_b2[];
   float2* stg = smem_b2;                                   // [n][TR]
   float2* buf = stg + (size_t)n * TR + (threadIdx.x / T) * padded_len(BIG);
@@ -163,13 +197,14 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
   for (int rr = 0; rr < TR / G; ++rr) {
     const int r = rr * G + gi;
     const int ky = ky0 + r;
+    if (ky >= HB) break;  // uniform within the group
     const float2 ty = __ldg(tau + ky);
     const uint2* gqr = gq + (size_t)ky * qpitch;
     auto load = [&](int kx) -> float2 {
       if (kx == HB || ky == HB) return make_float2(0.f, 0.f);  // Nyquist row / column (bst.py:157-160)
       // fp64-built coordinates of (|kfx|, ky); kfx < 0 reflects theta -> pi - theta
       const bool neg = kx > HB;
-      const uint2 e = __ldg(gqr + (neg ? BIG - kx : kx));
+      const uint2 e = __ldg(gqr + (neg ? big - kx : kx));
       const int i0 = (int)(e.x & 0x1FFFu);
       const int i1 = min(i0 + 1, nsig - 1);
       const float wi = (float)(e.x >> 13) * (1.f / 524288.f);
@@ -214,7 +249,7 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
         rowsum.y += v.y;
       }
     };
-    block_fft<BIG, true, false, false, false, 16>(buf, ti, tw, load, store, GroupBarT<T>{1 + gi});
+    dft<BIG, true, GEN, false, false>(buf, ti, tw, ch, load, store, GroupBarT<T>{1 + gi});
     GroupBarT<T>{1 + gi}();  // the next row's first pass overwrites buf
     // crop mean: Re(sum_x X[ky][x] * cmean[ky]), rows 1..BIG/2-1 stand for their conjugate partners too
     const float2 cm = __ldg(cmean + ky);
@@ -227,7 +262,7 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
   float2* Xb = X + (size_t)b * n * HB;
   for (int e = threadIdx.x; e < n * TR; e += blockDim.x) {
     const int xc = e / TR, r = e % TR;
-    Xb[(size_t)xc * HB + ky0 + r] = stg[e];
+    if (ky0 + r < HB) Xb[(size_t)xc * HB + ky0 + r] = stg[e];
   }
 }
 
@@ -236,12 +271,13 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
 // pair (x1, x2) is Z[ky] = X[ky][x1] + i X[ky][x2] with Hermitian extension,
 // so one inverse FFT gives both real columns.  Crop y in [p0, p0 + n).
 // ---------------------------------------------------------------------------
-template <int BIG, int TC, int G>
+template <int BIG, int TC, int G, bool GEN>
 __global__ void __launch_bounds__(G * FftPlan<BIG, true>::T)
 k_bst_grid_y(const float2* __restrict__ X, float* __restrict__ img, int n, int p0, float s_img, float s_mean,
-             float fbp, int subtract_mean, const double* __restrict__ acc, const float2* __restrict__ tw) {
+             float fbp, int subtract_mean, const double* __restrict__ acc, const float2* __restrict__ tw, Chirp ch) {
   constexpr int T = FftPlan<BIG, true>::T;
-  constexpr int HB = BIG / 2;
+  const int big = GEN ? ch.len : BIG;
+  const int HB = big / 2;
   extern __shared__ __align__(16) float2 smem_b3[];
   float* stg = reinterpret_cast<float*>(smem_b3);  // [n][TC + 1]
   float2* buf = smem_b3 + ((size_t)n * (TC + 1) + 1) / 2 + (threadIdx.x / T) * padded_len(BIG);
@@ -263,7 +299,7 @@ k_bst_grid_y(const float2* __restrict__ X, float* __restrict__ img, int n, int p
     auto load = [&](int ky) -> float2 {
       if (ky == HB) return make_float2(0.f, 0.f);
       const bool hi = ky > HB;
-      const int k = hi ? BIG - ky : ky;
+      const int k = hi ? big - ky : ky;
       float2 a = __ldg(ca + k), c = hb ? __ldg(cb + k) : make_float2(0.f, 0.f);
       if (hi) {
         a.y = -a.y;
@@ -278,7 +314,7 @@ k_bst_grid_y(const float2* __restrict__ X, float* __restrict__ img, int n, int p
         stg[(size_t)yc * (TC + 1) + 2 * q + 1] = v.y * s_img + offset;
       }
     };
-    block_fft<BIG, true, false, false, false, 16>(buf, ti, tw, load, store, GroupBarT<T>{1 + gi});
+    dft<BIG, true, GEN, false, false>(buf, ti, tw, ch, load, store, GroupBarT<T>{1 + gi});
     GroupBarT<T>{1 + gi}();
   }
   __syncthreads();
@@ -296,57 +332,64 @@ cudaError_t prep(K k, size_t smem) {
   return cudaSuccess;
 }
 
-template <int L>
+// N: FFT size (the DFT length L when GEN = false, the Bluestein convolution size otherwise)
+template <int N, bool GEN>
 cudaError_t radial_impl(const BstDims& d, const BstTables& t, const float* g, float2* P, double* acc, int batch,
                         cudaStream_t s) {
-  constexpr int T = FftPlan<L, false>::T;
+  constexpr int T = FftPlan<N, false>::T;
   constexpr int G = T >= 256 ? 1 : (256 / T > 4 ? 4 : 256 / T);
   constexpr int TC = G >= 4 ? G : 4;
-  const size_t smem = (((size_t)d.nt * (TC + 1) + 3) / 4 * 2 + (size_t)G * padded_len(L)) * sizeof(float2);
-  const bool half = 2 * d.ns <= L;
+  const size_t smem = (((size_t)d.nt * (TC + 1) + 3) / 4 * 2 + (size_t)G * padded_len(N) +
+                       (GEN ? (size_t)G * padded_len(N / 2) : 0)) * sizeof(float2);
+  const Chirp ch{t.chirp_L, t.bhat_L, d.L};
+  const float2* tw = GEN ? t.tw_mbL : t.tw_L;
+  const bool half = 2 * d.ns <= N;
   cudaError_t e;
-  if (half) {
-    auto k = k_bst_radial<L, TC, G, true>;
+  if (half || GEN) {
+    auto k = k_bst_radial<N, TC, G, true, GEN>;
     if ((e = prep(k, smem))) return e;
     k<<<dim3((d.ntheta + TC - 1) / TC, batch), G * T, smem, s>>>(g, P, d.nt, d.ntheta, d.ns, d.m_need, d.m_pad,
-                                                                  t.tap_base, t.tap_w, t.kern, t.tw_L, acc,
-                                                                  d.subtract_mean ? t.chord : nullptr);
+                                                                  t.tap_base, t.tap_w, t.kern, tw, acc,
+                                                                  d.subtract_mean ? t.chord : nullptr, ch);
   } else {
-    auto k = k_bst_radial<L, TC, G, false>;
+    auto k = k_bst_radial<N, TC, G, false, GEN>;
     if ((e = prep(k, smem))) return e;
     k<<<dim3((d.ntheta + TC - 1) / TC, batch), G * T, smem, s>>>(g, P, d.nt, d.ntheta, d.ns, d.m_need, d.m_pad,
-                                                                  t.tap_base, t.tap_w, t.kern, t.tw_L, acc,
-                                                                  d.subtract_mean ? t.chord : nullptr);
+                                                                  t.tap_base, t.tap_w, t.kern, tw, acc,
+                                                                  d.subtract_mean ? t.chord : nullptr, ch);
   }
   return cudaGetLastError();
 }
 
-template <int BIG>
+template <int N, bool GEN>
 cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, float2* X, float* img, double* acc,
                       int batch, cudaStream_t s) {
-  constexpr int T = FftPlan<BIG, true>::T;
-  constexpr int G = T >= 256 ? 2 : 4;
+  constexpr int T = FftPlan<N, true>::T;
+  constexpr int G = T >= 256 ? (GEN ? 1 : 2) : 4;
   constexpr int TR = 4;
   static_assert(TR % G == 0 || G > TR, "rows per group");
   constexpr int GX = G > TR ? TR : G;
+  const Chirp ch{t.chirp_big, t.bhat_big, d.big};
+  const float2* tw = GEN ? t.tw_mbbig : t.tw_big;
+  const int hb = d.big / 2;
   {
-    const size_t smem = ((size_t)d.n * TR + (size_t)GX * padded_len(BIG)) * sizeof(float2);
-    auto k = k_bst_grid_x<BIG, TR, GX>;
+    const size_t smem = ((size_t)d.n * TR + (size_t)GX * padded_len(N)) * sizeof(float2);
+    auto k = k_bst_grid_x<N, TR, GX, GEN>;
     cudaError_t e = prep(k, smem);
     if (e) return e;
-    k<<<dim3((BIG / 2) / TR, batch), GX * T, smem, s>>>(P, X, d.nray, d.m_need, d.m_pad, d.n, d.p0, t.grid_q,
-                                                         BIG / 2 + 1, t.tau, t.cmean, t.tw_big, acc);
+    k<<<dim3((hb + TR - 1) / TR, batch), GX * T, smem, s>>>(P, X, d.nray, d.m_need, d.m_pad, d.n, d.p0, t.grid_q,
+                                                             hb + 1, t.tau, t.cmean, tw, acc, ch);
     if ((e = cudaGetLastError())) return e;
   }
   {
     constexpr int TC = 8;
     constexpr int GY = G > TC / 2 ? TC / 2 : G;
-    const size_t smem = (((size_t)d.n * (TC + 1) + 1) / 2 + (size_t)GY * padded_len(BIG)) * sizeof(float2);
-    auto k = k_bst_grid_y<BIG, TC, GY>;
+    const size_t smem = (((size_t)d.n * (TC + 1) + 1) / 2 + (size_t)GY * padded_len(N)) * sizeof(float2);
+    auto k = k_bst_grid_y<N, TC, GY, GEN>;
     cudaError_t e = prep(k, smem);
     if (e) return e;
     k<<<dim3((d.n + TC - 1) / TC, batch), GY * T, smem, s>>>(X, img, d.n, d.p0, d.s_img, d.s_mean, d.fbp,
-                                                            d.subtract_mean, acc, t.tw_big);
+                                                            d.subtract_mean, acc, tw, ch);
     return cudaGetLastError();
   }
 }
@@ -355,25 +398,46 @@ cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, flo
 
 cudaError_t launch_bst_radial(const BstDims& d, const BstTables& t, const float* g, float2* P, double* acc, int batch,
                               cudaStream_t s) {
+  if (d.mb_L > 0) {  // Bluestein (non-power-of-two L)
+    switch (d.mb_L) {
+      case 512: return radial_impl<512, true>(d, t, g, P, acc, batch, s);
+      case 1024: return radial_impl<1024, true>(d, t, g, P, acc, batch, s);
+      case 2048: return radial_impl<2048, true>(d, t, g, P, acc, batch, s);
+      case 4096: return radial_impl<4096, true>(d, t, g, P, acc, batch, s);
+      case 8192: return radial_impl<8192, true>(d, t, g, P, acc, batch, s);
+      default: return cudaErrorNotSupported;
+    }
+  }
   switch (d.L) {
-    case 512: return radial_impl<512>(d, t, g, P, acc, batch, s);
-    case 1024: return radial_impl<1024>(d, t, g, P, acc, batch, s);
-    case 2048: return radial_impl<2048>(d, t, g, P, acc, batch, s);
-    case 4096: return radial_impl<4096>(d, t, g, P, acc, batch, s);
-    case 8192: return radial_impl<8192>(d, t, g, P, acc, batch, s);
+    case 512: return radial_impl<512, false>(d, t, g, P, acc, batch, s);
+    case 1024: return radial_impl<1024, false>(d, t, g, P, acc, batch, s);
+    case 2048: return radial_impl<2048, false>(d, t, g, P, acc, batch, s);
+    case 4096: return radial_impl<4096, false>(d, t, g, P, acc, batch, s);
+    case 8192: return radial_impl<8192, false>(d, t, g, P, acc, batch, s);
     default: return cudaErrorNotSupported;
   }
 }
 
 cudaError_t launch_bst_grid(const BstDims& d, const BstTables& t, const float2* P, float2* X, float* img, double* acc,
                             int batch, cudaStream_t s) {
+  if (d.mb_big > 0) {  // Bluestein (padded side not a power of two)
+    switch (d.mb_big) {
+      case 256: return grid_impl<256, true>(d, t, P, X, img, acc, batch, s);
+      case 512: return grid_impl<512, true>(d, t, P, X, img, acc, batch, s);
+      case 1024: return grid_impl<1024, true>(d, t, P, X, img, acc, batch, s);
+      case 2048: return grid_impl<2048, true>(d, t, P, X, img, acc, batch, s);
+      case 4096: return grid_impl<4096, true>(d, t, P, X, img, acc, batch, s);
+      case 8192: return grid_impl<8192, true>(d, t, P, X, img, acc, batch, s);
+      default: return cudaErrorNotSupported;
+    }
+  }
   switch (d.big) {
-    case 128: return grid_impl<128>(d, t, P, X, img, acc, batch, s);
-    case 256: return grid_impl<256>(d, t, P, X, img, acc, batch, s);
-    case 512: return grid_impl<512>(d, t, P, X, img, acc, batch, s);
-    case 1024: return grid_impl<1024>(d, t, P, X, img, acc, batch, s);
-    case 2048: return grid_impl<2048>(d, t, P, X, img, acc, batch, s);
-    case 4096: return grid_impl<4096>(d, t, P, X, img, acc, batch, s);
+    case 128: return grid_impl<128, false>(d, t, P, X, img, acc, batch, s);
+    case 256: return grid_impl<256, false>(d, t, P, X, img, acc, batch, s);
+    case 512: return grid_impl<512, false>(d, t, P, X, img, acc, batch, s);
+    case 1024: return grid_impl<1024, false>(d, t, P, X, img, acc, batch, s);
+    case 2048: return grid_impl<2048, false>(d, t, P, X, img, acc, batch, s);
+    case 4096: return grid_impl<4096, false>(d, t, P, X, img, acc, batch, s);
     default: return cudaErrorNotSupported;
   }
 }

@@ -14,10 +14,18 @@ struct BstTables {
   const uint2* grid_q;    // [big/2][big/2 + 1] quadrant gridding coordinates
   const float2* tw_L;     // pass twiddles, N = L
   const float2* tw_big;   // pass twiddles, N = big
+  // generic sizes (Bluestein): chirps of the DFT lengths and the convolution filters
+  const float2* chirp_L;  // [L]
+  const float2* bhat_L;   // [mb_L] forward filter spectrum / mb_L
+  const float2* tw_mbL;   // pass twiddles, N = mb_L
+  const float2* chirp_big;  // [big]
+  const float2* bhat_big;   // [mb_big] inverse filter spectrum / mb_big
+  const float2* tw_mbbig;   // pass twiddles, N = mb_big
 };
 
 struct BstDims {
   int nt, ntheta, n, ns, nray, L, m_need, m_pad, big, p0;
+  int mb_L, mb_big;  // Bluestein convolution sizes (0 = power-of-two direct FFT)
   int subtract_mean;
   double dsigma, dw;
   float s_img;   // output scale (BST_SCALE / (4 d^2), x 1/(2 pi) for fbp)

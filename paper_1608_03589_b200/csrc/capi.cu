@@ -1056,7 +1056,8 @@ int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan) {
     delete P;
     return fail(LPBP_EUNSUPPORTED, "BST engine: no kernel instantiation for radial DFT length L=" + std::to_string(L) +
                                        " / padded side " + std::to_string(2 * n) +
-                                       " (this build: powers of two, L in [512, 8192], 2n in [128, 4096])");
+                                       " (this build: L a power of two in [512, 8192] or L <= 4096; padded side a "
+                                       "power of two in [128, 4096] or <= 4096; even nt)");
   }
   auto& d = P->d;
   d.nt = h.p.nt;
@@ -1069,6 +1070,8 @@ int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan) {
   d.m_pad = h.m_pad;
   d.big = h.big;
   d.p0 = h.p0;
+  d.mb_L = h.mb_L;
+  d.mb_big = h.mb_big;
   d.subtract_mean = h.p.dc_mode == 0 ? 1 : 0;
   d.dsigma = h.dsigma;
   d.dw = h.dw;
@@ -1097,8 +1100,24 @@ int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan) {
     if (!rc) P->t.chord = h.chord_col.empty() ? nullptr : static_cast<const float4*>(p);
     rc = rc ? rc : P->upload(h.grid_q, &p);
     if (!rc) P->t.grid_q = static_cast<const uint2*>(p);
-    rc = rc ? rc : P->twiddles(h.L, &P->t.tw_L);
-    rc = rc ? rc : P->twiddles(h.big, &P->t.tw_big);
+    if (h.mb_L) {
+      rc = rc ? rc : P->twiddles(h.mb_L, &P->t.tw_mbL);
+      rc = rc ? rc : P->upload(h.chirp_L, &p);
+      if (!rc) P->t.chirp_L = static_cast<const float2*>(p);
+      rc = rc ? rc : P->upload(h.bhat_L, &p);
+      if (!rc) P->t.bhat_L = static_cast<const float2*>(p);
+    } else {
+      rc = rc ? rc : P->twiddles(h.L, &P->t.tw_L);
+    }
+    if (h.mb_big) {
+      rc = rc ? rc : P->twiddles(h.mb_big, &P->t.tw_mbbig);
+      rc = rc ? rc : P->upload(h.chirp_big, &p);
+      if (!rc) P->t.chirp_big = static_cast<const float2*>(p);
+      rc = rc ? rc : P->upload(h.bhat_big, &p);
+      if (!rc) P->t.bhat_big = static_cast<const float2*>(p);
+    } else {
+      rc = rc ? rc : P->twiddles(h.big, &P->t.tw_big);
+    }
     if (h.p.filter) {
       rc = rc ? rc : P->upload(h.ramp, &p);
       if (!rc) P->rt.ramp = static_cast<const float*>(p);

@@ -67,6 +67,29 @@ void lerp_tap(double f, int n, int32_t& base, double& w0, double& w1) {
 
 void lerp_tap_public(double f, int n, int32_t& base, double& w0, double& w1) { lerp_tap(f, n, base, w0, w1); }
 
+void bluestein_tables(int len, int MB, bool inverse, std::vector<F2>& chirp, std::vector<F2>& bhat) {
+  // c[k] = exp(-i pi k^2 / len) with exact phase reduction; filter b[j] = conj c[|j|] (forward)
+  // or c[|j|] (inverse) for |j| < len on the MB-point circle; bhat = FFT_MB(b) / MB
+  std::vector<cd> c(len);
+  chirp.resize(len);
+  for (int k = 0; k < len; ++k) {
+    const long long q = ((long long)k * k) % (2LL * len);
+    c[k] = std::polar(1.0, -kPi * (double)q / len);
+    chirp[k] = F2{(float)c[k].real(), (float)c[k].imag()};
+  }
+  std::vector<cd> wM(MB / 2);
+  for (int k = 0; k < MB / 2; ++k) wM[k] = std::polar(1.0, -2.0 * kPi * (double)k / MB);
+  std::vector<cd> b(MB, cd(0, 0));
+  for (int j = 0; j < len; ++j) {
+    const cd v = inverse ? c[j] : std::conj(c[j]);
+    b[j] = v;
+    if (j) b[MB - j] = v;
+  }
+  fft_pow2(b, wM);
+  bhat.resize(MB);
+  for (int q = 0; q < MB; ++q) bhat[q] = F2{(float)(b[q].real() / MB), (float)(b[q].imag() / MB)};
+}
+
 void build_bands(HostPlan& h, int band_rows) {
   // Steps of band_rows (2 or 4) rows for the streaming fused readout: step b owns
   // the pixels with i0 in [r0 - 1, r0 + band_rows - 1), r0 = row_min + band_rows*b,

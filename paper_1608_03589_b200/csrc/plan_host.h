@@ -68,5 +68,7 @@ int next_fast_len(int target);
 void build_ramp_taps(int nt, double lam, double cutoff, int& M_out, int& Lr_out, std::vector<float>& ramp);
 // _lerp_axis0 tap (grids.py:255-269) as (base in [0, n-2], w0, w1), out-of-range terms weight 0
 void lerp_tap_public(double f, int n, int32_t& base, double& w0, double& w1);
+// Bluestein tables of a length-len DFT on an MB-point circular convolution (MB pow2 >= 2 len)
+void bluestein_tables(int len, int MB, bool inverse, std::vector<F2>& chirp, std::vector<F2>& bhat);
 
 }  // namespace lpbp

@@ -327,8 +327,9 @@ def _bst_plan(nt, nth, n, beta=0.0, zero_pad=2.0, dc_mode=0, filt=0):
 
 
 @pytest.mark.parametrize("nt,nth,n,zp,supported", [(256, 256, 256, 2.0, 1), (512, 512, 512, 2.0, 1),
-                                                   (2048, 2048, 2048, 2.0, 1), (256, 180, 128, 3.0, 0),
-                                                   (200, 96, 101, 2.0, 0), (256, 180, 128, 1.0, 1)])
+                                                   (2048, 2048, 2048, 2.0, 1), (256, 180, 128, 3.0, 1),
+                                                   (200, 96, 101, 2.0, 1), (256, 180, 128, 1.0, 1),
+                                                   (2048, 2048, 1024, 3.0, 0), (130, 64, 64, 2.0, 1)])
 def test_bst_geometry_matches_oracle(nt, nth, n, zp, supported):
     rc, h = _bst_plan(nt, nth, n, zero_pad=zp)
     assert rc == N.LPBP_OK, N.lib().lpbp_last_error()

@@ -78,6 +78,20 @@ def test_bst_reference_script_sizes(pkg, nt, nth, n, kw):
     assert report(f"bst {nt}x{nth}->{n} {kw}", img, O.bst_backproject(g, n, **kw)) <= RTOL
 
 
+def test_bst_generic_sizes_vs_reference_golden(pkg, golden):
+    """Non-power-of-two radial lengths and padded sides run through Bluestein convolutions."""
+    z = golden("bst.npz")
+    g = z["opt_sino"].astype(np.float64)  # 256 x 180, zero_pad = 3 -> L = 1536
+    img = pkg.bst_backproject(pkg.Sinogram(*g.shape, g),
+                              pkg.BstOptions(n_out=128, beta=4.0, zero_pad=3.0, dc_mode="kernel_cap")).values
+    assert report("bst zero_pad=3 (L=1536) kernel_cap beta=4", img, z["opt_beta4_zp3_cap"]) <= RTOL
+    g3 = z["odd_sino"].astype(np.float64)  # 200 x 96 -> n = 101 (padded side 202)
+    img = pkg.bst_backproject(pkg.Sinogram(*g3.shape, g3), pkg.BstOptions(n_out=101)).values
+    assert report("bst 200x96 -> 101", img, z["odd_n101"]) <= RTOL
+    img = pkg.fbp(pkg.Sinogram(*g3.shape, g3), pkg.FilterSpec(lam=0.01), n=75).values
+    assert report("fbp(bst) 200x96 -> 75", img, O.fbp_bst(g3, 75, lam=0.01)) <= RTOL
+
+
 def test_bst_radial_stage(pkg, golden):
     z = golden("bst.npz")
     g = z["opt_sino"].astype(np.float64)
@@ -127,7 +141,7 @@ def test_bst_errors(pkg):
         with pytest.raises(ValueError, match=msg):
             pkg.BstOptions(**kw)
     # sizes this build does not instantiate fail loudly (no fallback)
-    with pytest.raises(NotImplementedError):
-        pkg.bst_backproject(pkg.Sinogram(200, 96, np.ones((200, 96))), pkg.BstOptions(n_out=101))
-    with pytest.raises(NotImplementedError):  # zero_pad = 3: L = 1536 is not a power of two
-        pkg.bst_backproject(pkg.Sinogram(256, 180, np.ones((256, 180))), pkg.BstOptions(n_out=128, zero_pad=3.0))
+    with pytest.raises(NotImplementedError):  # odd nt
+        pkg.bst_backproject(pkg.Sinogram(129, 96, np.ones((129, 96))), pkg.BstOptions(n_out=64))
+    with pytest.raises(NotImplementedError):  # zero_pad = 3 at nt = 2048: L = 12288 > 4096 and not a power of two
+        pkg.bst_backproject(pkg.Sinogram(2048, 64, np.ones((2048, 64))), pkg.BstOptions(n_out=512, zero_pad=3.0))
