@@ -211,6 +211,21 @@ int lpbp_bst_execute_host(lpbp_bst_plan* plan, const float* sino_host, float* im
 int lpbp_bst_radial(const lpbp_bst_plan* plan, const float* sino_dev, float* spectra_dev, int32_t batch,
                     void* stream);
 
+/* ---- the path's resampling steps as standalone operations (the fused pipeline computes them
+ * implicitly); reference semantics and ValueError texts ----
+ * sinogram_to_semipolar(g, ns)   grids.py:290-311   sino [batch][nt][ntheta] -> p [batch][ns][2 ntheta]
+ *                                                   (ns = 0: nt / 2)
+ * semipolar_to_logpolar(p, rho0, nrho)  grids.py:332-347   p [batch][ns][nphi] -> lp [batch][nrho][nphi]
+ * logpolar_to_cartesian(l, nx, ny)      grids.py:399-443   lp -> img [batch][ny][nx] (fp64 coordinates)
+ * make_logpolar_kernel(nrho, nphi, drho) logpolar.py:66-81  dense [nrho][nphi] float64 on the host */
+int lpbp_sinogram_to_semipolar(const float* sino_dev, float* p_dev, int32_t nt, int32_t ntheta, int32_t ns,
+                               int32_t batch, void* stream);
+int lpbp_semipolar_to_logpolar(const float* p_dev, float* lp_dev, int32_t ns, int32_t nphi, double rho0, int32_t nrho,
+                               int32_t batch, void* stream);
+int lpbp_logpolar_to_cartesian(const float* lp_dev, float* img_dev, int32_t nrho, int32_t nphi, double rho0,
+                               int32_t nx, int32_t ny, int32_t batch, void* stream);
+int lpbp_logpolar_kernel(int32_t nrho, int32_t nphi, double drho, double* out_host);
+
 /* Number of kernel launches the last lpbp_execute/lpbp_execute_host issued on the calling thread. */
 int64_t lpbp_last_launch_count(void);
 

@@ -5,7 +5,9 @@ Same names and signatures as the reference for the path:
   Sinogram, CartesianImage, LogPolarImage, LogPolarOptions, FilterSpec,
   logpolar_backproject, filter_sinogram, fbp, backproject_naive,
   adaptive_rho0, compute_nrho, relative_l2, partial_backproject,
-  BstOptions, bst_backproject (fbp's default engine "bst")
+  BstOptions, bst_backproject (fbp's default engine "bst"),
+  PolarSinogram, sinogram_to_semipolar, semipolar_to_logpolar, logpolar_to_cartesian,
+  make_logpolar_kernel, truncation_error_bound
 plus batched device entry points (torch CUDA tensors) and LogPolarPlan.
 All compute runs in liblpbp.so; there is no CPU fallback.
 """
@@ -29,5 +31,13 @@ from . import synth
 from .multi import VolumeReconstructor, shard_bounds
 from .sector import SectorPlan, partial_backproject, partial_backproject_batch
 from .bst import BST_SCALE, BstOptions, BstPlan, bst_backproject, bst_backproject_batch
+from .resample import (
+    PolarSinogram,
+    logpolar_to_cartesian,
+    make_logpolar_kernel,
+    semipolar_to_logpolar,
+    sinogram_to_semipolar,
+    truncation_error_bound,
+)
 
 __version__ = "0.1.0"

@@ -110,6 +110,12 @@ SIGNATURES = {
     "lpbp_bst_execute": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
     "lpbp_bst_execute_host": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32]),
     "lpbp_bst_radial": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
+    "lpbp_sinogram_to_semipolar": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p]),
+    "lpbp_semipolar_to_logpolar": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_double, c_int32, c_int32,
+                                             c_void_p]),
+    "lpbp_logpolar_to_cartesian": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_double, c_int32, c_int32,
+                                             c_int32, c_void_p]),
+    "lpbp_logpolar_kernel": (c_int32, [c_int32, c_int32, c_double, c_void_p]),
     "lpbp_last_launch_count": (c_int64, []),
     "lpbp_last_error": (c_char_p, []),
     "lpbp_version": (c_int32, []),

@@ -15,6 +15,7 @@
 #include "sector_kernels.cuh"
 #include "bst_host.h"
 #include "bst_kernels.cuh"
+#include "resample_kernels.cuh"
 
 using lpbp::DevTables;
 using lpbp::Dims;
@@ -1266,6 +1267,72 @@ int lpbp_bst_radial(const lpbp_bst_plan* P, const float* sino_dev, float* spectr
   cudaFreeAsync(acc, static_cast<cudaStream_t>(stream));
   if (e) return launch_fail(e, "bst_radial");
   ++g_launches;
+  return LPBP_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// standalone resampling steps
+// ---------------------------------------------------------------------------
+int lpbp_sinogram_to_semipolar(const float* sino_dev, float* p_dev, int32_t nt, int32_t ntheta, int32_t ns,
+                               int32_t batch, void* stream) {
+  g_launches = 0;
+  if (ns == 0) ns = nt / 2;
+  if (ns < 2) return fail(LPBP_EINVAL, "ns must be >= 2");
+  if (nt < 2 || ntheta < 1) return fail(LPBP_EINVAL, "nt must be >= 2 and ntheta >= 1");
+  if (batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !p_dev) return fail(LPBP_EINVAL, "invalid argument");
+  cudaError_t e = lpbp::launch_semipolar(sino_dev, p_dev, nt, ntheta, ns, batch, static_cast<cudaStream_t>(stream));
+  if (e) return cuda_fail(e, "sinogram_to_semipolar");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+int lpbp_semipolar_to_logpolar(const float* p_dev, float* lp_dev, int32_t ns, int32_t nphi, double rho0, int32_t nrho,
+                               int32_t batch, void* stream) {
+  g_launches = 0;
+  if (nrho < 2) return fail(LPBP_EINVAL, "nrho must be >= 2");
+  if (!(rho0 < 0)) return fail(LPBP_EINVAL, "rho0 must be negative");
+  if (ns < 2 || nphi < 2) return fail(LPBP_EINVAL, "ns and nphi must be >= 2");
+  if (batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (batch == 0) return LPBP_OK;
+  if (!p_dev || !lp_dev) return fail(LPBP_EINVAL, "invalid argument");
+  cudaError_t e = lpbp::launch_semipolar_to_logpolar(p_dev, lp_dev, ns, nphi, rho0, nrho, batch,
+                                                     static_cast<cudaStream_t>(stream));
+  if (e) return cuda_fail(e, "semipolar_to_logpolar");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+int lpbp_logpolar_to_cartesian(const float* lp_dev, float* img_dev, int32_t nrho, int32_t nphi, double rho0,
+                               int32_t nx, int32_t ny, int32_t batch, void* stream) {
+  g_launches = 0;
+  if (nx < 2 || ny < 2) return fail(LPBP_EINVAL, "nx and ny must be >= 2");
+  if (nrho < 2 || nphi < 2) return fail(LPBP_EINVAL, "nrho and nphi must be >= 2");
+  if (!(rho0 < 0)) return fail(LPBP_EINVAL, "rho0 must be negative");
+  if (batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (batch == 0) return LPBP_OK;
+  if (!lp_dev || !img_dev) return fail(LPBP_EINVAL, "invalid argument");
+  cudaError_t e = lpbp::launch_logpolar_to_cartesian(lp_dev, img_dev, nrho, nphi, rho0, nx, ny, batch,
+                                                     static_cast<cudaStream_t>(stream));
+  if (e) return cuda_fail(e, "logpolar_to_cartesian");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+int lpbp_logpolar_kernel(int32_t nrho, int32_t nphi, double drho, double* out_host) {
+  if (nrho < 2 || nphi < 2) return fail(LPBP_EINVAL, "kernel mesh must be at least 2 x 2");
+  if (!(drho > 0)) return fail(LPBP_EINVAL, "drho must be positive");
+  if (!out_host) return fail(LPBP_EINVAL, "invalid argument");
+  constexpr double kPi = 3.14159265358979323846;
+  std::vector<double> ct(nphi);
+  for (int j = 0; j < nphi; ++j) ct[j] = std::cos(-kPi + (double)j * (2.0 * kPi / nphi));
+  for (int i = 0; i < nrho; ++i) {
+    const double e = std::exp((double)i * drho);
+    for (int j = 0; j < nphi; ++j)
+      out_host[(size_t)i * nphi + j] = std::fabs(e * ct[j] - 1.0) <= drho ? 1.0 / drho : 0.0;
+  }
   return LPBP_OK;
 }
 

@@ -103,3 +103,15 @@ def partial_backproject(g: Sinogram, sectors, n_out: int) -> CartesianImage:
     """fastbp.logpolar.partial_backproject (logpolar.py:210-299); see sector.py."""
     from .sector import partial_backproject as _pb
     return _pb(g, sectors, n_out)
+
+
+def make_logpolar_kernel(nrho: int, nphi: int, drho: float):
+    """fastbp.logpolar.make_logpolar_kernel (logpolar.py:66-81); see resample.py."""
+    from .resample import make_logpolar_kernel as _k
+    return _k(nrho, nphi, drho)
+
+
+def truncation_error_bound(rho0: float, c: float) -> float:
+    """fastbp.logpolar.truncation_error_bound (logpolar.py:138-145)."""
+    from .resample import truncation_error_bound as _t
+    return _t(rho0, c)

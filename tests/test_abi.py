@@ -358,3 +358,26 @@ def test_bst_validation_messages_match_oracle():
     with pytest.raises(ValueError) as e:
         O.bst_geometry(64, 256)
     assert rc == N.LPBP_EINVAL and N.lib().lpbp_last_error().decode() == str(e.value)
+
+
+# ---- the path's host-side kernel table (make_logpolar_kernel) ----
+
+@pytest.mark.parametrize("nrho,nphi,drho", [(353, 512, 1.570872e-2), (796, 1024, 7.837091e-3), (64, 90, 0.05),
+                                            (3900, 4096, 1.955031e-3)])
+def test_make_logpolar_kernel_matches_oracle(nrho, nphi, drho):
+    import paper_1608_03589_b200 as p
+    got = p.make_logpolar_kernel(nrho, nphi, drho)
+    assert np.array_equal(got, O.lp_kernel(nrho, nphi, drho))
+
+
+def test_make_logpolar_kernel_against_reference(reference):
+    import paper_1608_03589_b200 as p
+    from fastbp.logpolar import make_logpolar_kernel, truncation_error_bound
+    for args in ((353, 512, 1.570872e-2), (101, 77, 0.031)):
+        assert np.array_equal(p.make_logpolar_kernel(*args), make_logpolar_kernel(*args))
+    assert p.truncation_error_bound(-3.1, 0.7) == truncation_error_bound(-3.1, 0.7)
+    for call, msg in ((lambda: p.make_logpolar_kernel(1, 8, 0.1), "kernel mesh must be at least 2 x 2"),
+                      (lambda: p.make_logpolar_kernel(8, 8, 0.0), "drho must be positive"),
+                      (lambda: p.truncation_error_bound(-1.0, -1.0), "c must be >= 0")):
+        with pytest.raises(ValueError, match=msg):
+            call()
