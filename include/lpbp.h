@@ -226,6 +226,19 @@ int lpbp_logpolar_to_cartesian(const float* lp_dev, float* img_dev, int32_t nrho
                                int32_t nx, int32_t ny, int32_t batch, void* stream);
 int lpbp_logpolar_kernel(int32_t nrho, int32_t nphi, double drho, double* out_host);
 
+/* ---- BST helpers ----
+ * polar_to_cartesian_frequency(ps, nx, ny, dw)  grids.py:456-508: spectra [batch] x complex64 P with
+ *   element (m, ray) at P[m * stride_m + ray * stride_ray] (slice pitch slice_pitch, in complex
+ *   elements) -> out [batch][ny][nx] complex64, times `scale`; fp64 coordinates.
+ * mean_backprojection(g)   bst.py:173-180 -> out_dev [batch] doubles.
+ * kaiser_window(ns, beta)  bst.py:90-102 -> out_host [ns] doubles. */
+int lpbp_polar_to_cartesian_frequency(const float* spec_dev, float* out_dev, int32_t nsigma, int32_t nray,
+                                      int64_t stride_m, int64_t stride_ray, int64_t slice_pitch, double dsigma,
+                                      int32_t nx, int32_t ny, double dw, float scale, int32_t batch, void* stream);
+int lpbp_mean_backprojection(const float* sino_dev, double* out_dev, int32_t nt, int32_t ntheta, int32_t batch,
+                             void* stream);
+int lpbp_kaiser_window(int32_t ns, double beta, double* out_host);
+
 /* Number of kernel launches the last lpbp_execute/lpbp_execute_host issued on the calling thread. */
 int64_t lpbp_last_launch_count(void);
 

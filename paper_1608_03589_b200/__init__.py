@@ -30,9 +30,22 @@ from . import roofline
 from . import synth
 from .multi import VolumeReconstructor, shard_bounds
 from .sector import SectorPlan, partial_backproject, partial_backproject_batch
-from .bst import BST_SCALE, BstOptions, BstPlan, bst_backproject, bst_backproject_batch
+from .bst import (
+    BST_SCALE,
+    BstOptions,
+    BstPlan,
+    bst_backproject,
+    bst_backproject_batch,
+    bst_spectrum,
+    kaiser_window,
+    mean_backprojection,
+    sigma_kernel,
+)
 from .resample import (
+    FrequencyImage,
     PolarSinogram,
+    PolarSpectrum,
+    polar_to_cartesian_frequency,
     logpolar_to_cartesian,
     make_logpolar_kernel,
     semipolar_to_logpolar,

@@ -116,6 +116,11 @@ SIGNATURES = {
     "lpbp_logpolar_to_cartesian": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_double, c_int32, c_int32,
                                              c_int32, c_void_p]),
     "lpbp_logpolar_kernel": (c_int32, [c_int32, c_int32, c_double, c_void_p]),
+    "lpbp_polar_to_cartesian_frequency": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int64, c_int64, c_int64,
+                                                    c_double, c_int32, c_int32, c_double, ctypes.c_float, c_int32,
+                                                    c_void_p]),
+    "lpbp_mean_backprojection": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p]),
+    "lpbp_kaiser_window": (c_int32, [c_int32, c_double, c_void_p]),
     "lpbp_last_launch_count": (c_int64, []),
     "lpbp_last_error": (c_char_p, []),
     "lpbp_version": (c_int32, []),

@@ -25,7 +25,8 @@ from ._native import BstInfo, BstParams, check, lib
 from .grids import CartesianImage, Sinogram
 from .plan import _as_f32_contig, _require_cuda, _stream
 
-__all__ = ["BST_SCALE", "BstOptions", "BstPlan", "bst_backproject", "bst_backproject_batch", "get_bst_plan"]
+__all__ = ["BST_SCALE", "BstOptions", "BstPlan", "bst_backproject", "bst_backproject_batch", "bst_spectrum",
+           "get_bst_plan", "kaiser_window", "mean_backprojection", "sigma_kernel"]
 
 BST_SCALE = 4.0 * math.pi  # bst.py:47
 
@@ -175,3 +176,49 @@ def bst_backproject_batch(sino: torch.Tensor, opts: BstOptions, filter_spec=None
     """Batched device entry point: [B, nt, ntheta] float32 CUDA -> [B, n_out, n_out]."""
     plan = get_bst_plan(sino.shape[1], sino.shape[2], opts, filter_spec, device=sino.device.index)
     return plan.execute(sino, out=out)
+
+
+def kaiser_window(ns: int, beta: float) -> np.ndarray:
+    """Kaiser-Bessel taper I0(beta sqrt(1 - u^2)) / I0(beta), u = (2i - ns + 1)/(ns - 1) (bst.py:90-102)."""
+    if ns < 2:
+        raise ValueError("ns must be >= 2")
+    out = np.empty(int(ns), dtype=np.float64)
+    check(lib().lpbp_kaiser_window(int(ns), float(beta), c_void_p(out.ctypes.data)))
+    return out
+
+
+def sigma_kernel(nsigma: int, dsigma: float) -> np.ndarray:
+    """Radial weights 1/sigma_m, the DC bin capped at 1/dsigma (bst.py:105-117)."""
+    if not dsigma > 0:
+        raise ValueError("dsigma must be positive")
+    out = np.empty(nsigma)
+    out[0] = 1.0 / dsigma
+    out[1:] = 1.0 / (np.arange(1, nsigma) * dsigma)
+    return out
+
+
+def mean_backprojection(g: Sinogram) -> float:
+    """Spatial mean over [-1, 1]^2 of the backprojection of g through <B g, 1> = <g, chord>
+    (bst.py:173-180), reduced on the device in fp64."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1608_03589_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    src = torch.from_numpy(np.ascontiguousarray(g.values, dtype=np.float32)).cuda()
+    out = torch.empty(1, dtype=torch.float64, device=src.device)
+    check(lib().lpbp_mean_backprojection(c_void_p(src.data_ptr()), c_void_p(out.data_ptr()), g.nt, g.ntheta, 1,
+                                         _stream(src.device)))
+    return float(out.item())
+
+
+def bst_spectrum(g: Sinogram, opts: BstOptions):
+    """The engine's native product on the omega = pi k lattice of an n_out image:
+    BST_SCALE * polar_to_cartesian_frequency(spectra * sigma_kernel) (bst.py:206-226)."""
+    from .resample import FrequencyImage
+    plan = get_bst_plan(g.nt, g.ntheta, opts)
+    sino = torch.from_numpy(np.ascontiguousarray(g.values, dtype=np.float32)).cuda().unsqueeze(0)
+    radial = plan.radial(sino)  # [1, nray, m_need] = 0.5 x spectra * kernel (view with pitch m_pad)
+    n, m_need, nray, m_pad = opts.n_out, plan.info["m_need"], plan.info["nray"], plan.info["m_pad"]
+    out = torch.empty((n, n), dtype=torch.complex64, device=sino.device)
+    check(lib().lpbp_polar_to_cartesian_frequency(c_void_p(radial.data_ptr()), c_void_p(out.data_ptr()), m_need, nray,
+                                                  1, m_pad, nray * m_pad, float(plan.info["dsigma"]), n, n, math.pi,
+                                                  float(2.0 * BST_SCALE), 1, _stream(sino.device)))
+    return FrequencyImage(n, n, out.cpu().numpy().astype(np.complex128))

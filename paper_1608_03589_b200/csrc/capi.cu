@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -1332,6 +1333,82 @@ int lpbp_logpolar_kernel(int32_t nrho, int32_t nphi, double drho, double* out_ho
     const double e = std::exp((double)i * drho);
     for (int j = 0; j < nphi; ++j)
       out_host[(size_t)i * nphi + j] = std::fabs(e * ct[j] - 1.0) <= drho ? 1.0 / drho : 0.0;
+  }
+  return LPBP_OK;
+}
+
+
+int lpbp_polar_to_cartesian_frequency(const float* spec_dev, float* out_dev, int32_t nsigma, int32_t nray,
+                                      int64_t stride_m, int64_t stride_ray, int64_t slice_pitch, double dsigma,
+                                      int32_t nx, int32_t ny, double dw, float scale, int32_t batch, void* stream) {
+  g_launches = 0;
+  if (nx < 2 || ny < 2) return fail(LPBP_EINVAL, "nx and ny must be >= 2");
+  if (nsigma < 2 || nray < 2) return fail(LPBP_EINVAL, "nsigma and ntheta must be >= 2");
+  if (!(dsigma > 0)) return fail(LPBP_EINVAL, "dsigma must be positive");
+  const double nyq = std::sqrt(2.0) * dw * std::max(nx, ny) / 2.0, smax = (nsigma - 1) * dsigma;
+  if (smax < nyq * (1.0 - 1e-12)) {
+    char buf[200];
+    std::snprintf(buf, sizeof buf,
+                  "polar spectrum reaches sigma = %.3f but the cartesian grid requires coverage up to the Nyquist "
+                  "radius %.3f", smax, nyq);
+    return fail(LPBP_EINVAL, buf);
+  }
+  if (batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (batch == 0) return LPBP_OK;
+  if (!spec_dev || !out_dev) return fail(LPBP_EINVAL, "invalid argument");
+  cudaError_t e = lpbp::launch_polar_to_cartesian_frequency(
+      reinterpret_cast<const float2*>(spec_dev), reinterpret_cast<float2*>(out_dev), nsigma, nray, stride_m, stride_ray,
+      slice_pitch, dsigma, nx, ny, dw, scale, batch, static_cast<cudaStream_t>(stream));
+  if (e) return cuda_fail(e, "polar_to_cartesian_frequency");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+int lpbp_mean_backprojection(const float* sino_dev, double* out_dev, int32_t nt, int32_t ntheta, int32_t batch,
+                             void* stream) {
+  g_launches = 0;
+  if (nt < 2 || ntheta < 1 || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
+  if (batch == 0) return LPBP_OK;
+  if (!sino_dev || !out_dev) return fail(LPBP_EINVAL, "invalid argument");
+  // chord of the square per angle as a trapezoid in t (same fp64 construction as the BST plan)
+  const double kPi = 3.14159265358979323846, dt = 2.0 / nt, dth = kPi / ntheta;
+  std::vector<lpbp::F4> cp(ntheta);
+  for (int j = 0; j < ntheta; ++j) {
+    const double c = std::fabs(std::cos(j * dth)), sn = std::fabs(std::sin(j * dth));
+    const bool deg = c <= 1e-15 || sn <= 1e-15;
+    const double t1 = deg ? 1.0 : std::fabs(c - sn), t2 = deg ? 1.0 : c + sn;
+    const double lmax = deg ? 2.0 : 2.0 / std::max(c, sn);
+    cp[j] = lpbp::F4{(float)t1, (float)t2, (float)(lmax * dt * dth / 4.0), t2 > t1 ? (float)(1.0 / (t2 - t1)) : 0.f};
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, cp.size() * sizeof(lpbp::F4), st);
+  if (!e) e = cudaMemcpyAsync(d, cp.data(), cp.size() * sizeof(lpbp::F4), cudaMemcpyHostToDevice, st);
+  if (!e) e = cudaStreamSynchronize(st);  // the host vector goes out of scope
+  if (!e) e = lpbp::launch_mean_backprojection(sino_dev, static_cast<const float4*>(d), out_dev, nt, ntheta, batch, st);
+  if (d) cudaFreeAsync(d, st);
+  if (e) return cuda_fail(e, "mean_backprojection");
+  ++g_launches;
+  return LPBP_OK;
+}
+
+int lpbp_kaiser_window(int32_t ns, double beta, double* out_host) {
+  if (ns < 2) return fail(LPBP_EINVAL, "ns must be >= 2");
+  if (!out_host) return fail(LPBP_EINVAL, "invalid argument");
+  auto i0 = [](double x) {  // power series of I0 (all terms positive)
+    const double q = 0.25 * x * x;
+    double term = 1.0, sum = 1.0;
+    for (int k = 1; k < 500; ++k) {
+      term *= q / ((double)k * k);
+      sum += term;
+      if (term < 1e-17 * sum) break;
+    }
+    return sum;
+  };
+  const double den = std::fabs(i0(beta));
+  for (int i = 0; i < ns; ++i) {
+    const double u = (2.0 * i - ns + 1.0) / (ns - 1.0);
+    out_host[i] = std::fabs(i0(beta * std::sqrt(std::max(1.0 - u * u, 0.0)))) / den;
   }
   return LPBP_OK;
 }

@@ -18,8 +18,8 @@ import torch
 from ._native import check, lib
 from .grids import CartesianImage, LogPolarImage, Sinogram, _frozen_f64
 
-__all__ = ["PolarSinogram", "sinogram_to_semipolar", "semipolar_to_logpolar", "logpolar_to_cartesian",
-           "make_logpolar_kernel", "truncation_error_bound"]
+__all__ = ["PolarSinogram", "PolarSpectrum", "FrequencyImage", "sinogram_to_semipolar", "semipolar_to_logpolar",
+           "logpolar_to_cartesian", "polar_to_cartesian_frequency", "make_logpolar_kernel", "truncation_error_bound"]
 
 
 @dataclass(frozen=True)
@@ -48,6 +48,59 @@ class PolarSinogram:
 
     def phi(self) -> np.ndarray:
         return np.arange(self.nphi) * self.dphi
+
+
+def _frozen_c128(values, shape, label) -> np.ndarray:
+    arr = np.array(values, dtype=np.complex128, copy=True)
+    if arr.shape != shape:
+        raise ValueError(f"values must have shape {label} = {shape}")
+    if not np.all(np.isfinite(arr.view(np.float64))):
+        raise ValueError("values must contain only finite values")
+    arr = np.ascontiguousarray(arr)
+    arr.setflags(write=False)
+    return arr
+
+
+@dataclass(frozen=True)
+class PolarSpectrum:
+    """Complex samples on radial frequency rays sigma_m = m dsigma, values[nsigma][ntheta] (grids.py:200-229)."""
+
+    nsigma: int
+    ntheta: int
+    dsigma: float
+    values: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        if self.nsigma < 2 or self.ntheta < 2:
+            raise ValueError("nsigma and ntheta must be >= 2")
+        if not self.dsigma > 0:
+            raise ValueError("dsigma must be positive")
+        object.__setattr__(self, "values", _frozen_c128(self.values, (self.nsigma, self.ntheta), "(nsigma, ntheta)"))
+
+    @property
+    def dtheta(self) -> float:
+        return 2.0 * math.pi / self.ntheta
+
+    def sigma(self) -> np.ndarray:
+        return np.arange(self.nsigma) * self.dsigma
+
+    @property
+    def sigma_max(self) -> float:
+        return (self.nsigma - 1) * self.dsigma
+
+
+@dataclass(frozen=True)
+class FrequencyImage:
+    """Cartesian frequency samples in FFT layout, values[ny][nx]; bin k holds omega = pi k (grids.py:232-246)."""
+
+    nx: int
+    ny: int
+    values: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        if self.nx < 2 or self.ny < 2:
+            raise ValueError("nx and ny must be >= 2")
+        object.__setattr__(self, "values", _frozen_c128(self.values, (self.ny, self.nx), "(ny, nx)"))
 
 
 def _dev(values: np.ndarray) -> torch.Tensor:
@@ -96,6 +149,19 @@ def logpolar_to_cartesian(l: LogPolarImage, nx: int, ny: int) -> CartesianImage:
     check(lib().lpbp_logpolar_to_cartesian(c_void_p(src.data_ptr()), c_void_p(out.data_ptr()), l.nrho, l.nphi,
                                            float(l.rho0), int(nx), int(ny), 1, _stream()))
     return CartesianImage(int(nx), int(ny), out.double().cpu().numpy())
+
+
+def polar_to_cartesian_frequency(ps: PolarSpectrum, nx: int, ny: int, dw: float = math.pi) -> FrequencyImage:
+    """Bilinear (sigma, theta) gridding onto the lattice omega = dw k with the Hermitian
+    average F(k) = (G(k) + conj G(-k)) / 2 (grids.py:456-508), fp64 coordinates on the device."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1608_03589_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    src = torch.from_numpy(np.ascontiguousarray(ps.values, dtype=np.complex64)).cuda()
+    out = torch.empty((int(ny), int(nx)), dtype=torch.complex64, device=src.device)
+    check(lib().lpbp_polar_to_cartesian_frequency(c_void_p(src.data_ptr()), c_void_p(out.data_ptr()), ps.nsigma,
+                                                  ps.ntheta, ps.ntheta, 1, ps.nsigma * ps.ntheta, float(ps.dsigma),
+                                                  int(nx), int(ny), float(dw), 1.0, 1, _stream()))
+    return FrequencyImage(int(nx), int(ny), out.cpu().numpy().astype(np.complex128))
 
 
 def make_logpolar_kernel(nrho: int, nphi: int, drho: float) -> np.ndarray:

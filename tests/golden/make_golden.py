@@ -136,6 +136,8 @@ def bst_goldens() -> None:
     ps = PolarSpectrum(H.shape[0], H.shape[1], dsig, H)
     arrays["small_grid"] = polar_to_cartesian_frequency(ps, 128, 128, dw=math.pi / 2).values
     arrays["small_bp"] = bst_backproject(s4, BstOptions(n_out=64)).values
+    from fastbp.bst import bst_spectrum
+    arrays["small_spectrum"] = bst_spectrum(s4, BstOptions(n_out=64)).values
     kat["small_dsigma"] = dsig
     kat["mean_bp_cfg0"] = mean_backprojection(s0)
     try:

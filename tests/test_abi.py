@@ -381,3 +381,15 @@ def test_make_logpolar_kernel_against_reference(reference):
                       (lambda: p.truncation_error_bound(-1.0, -1.0), "c must be >= 0")):
         with pytest.raises(ValueError, match=msg):
             call()
+
+
+def test_bst_host_helpers_against_reference(reference):
+    import paper_1608_03589_b200 as p
+    from fastbp.bst import kaiser_window, sigma_kernel
+    for ns, beta in ((8, 3.0), (2048, 0.0), (513, 8.0)):
+        np.testing.assert_allclose(p.kaiser_window(ns, beta), kaiser_window(ns, beta), rtol=1e-14, atol=0)
+    assert np.array_equal(p.sigma_kernel(10, 0.3), sigma_kernel(10, 0.3))
+    with pytest.raises(ValueError, match="ns must be >= 2"):
+        p.kaiser_window(1, 1.0)
+    with pytest.raises(ValueError, match="dsigma must be positive"):
+        p.sigma_kernel(4, 0.0)

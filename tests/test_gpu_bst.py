@@ -145,3 +145,23 @@ def test_bst_errors(pkg):
         pkg.bst_backproject(pkg.Sinogram(129, 96, np.ones((129, 96))), pkg.BstOptions(n_out=64))
     with pytest.raises(NotImplementedError):  # zero_pad = 3 at nt = 2048: L = 12288 > 4096 and not a power of two
         pkg.bst_backproject(pkg.Sinogram(2048, 64, np.ones((2048, 64))), pkg.BstOptions(n_out=512, zero_pad=3.0))
+
+
+def test_bst_helpers(pkg, golden):
+    z = golden("bst.npz")
+    with open(os.path.join(GOLDEN, "kat_bst.json")) as f:
+        kat = json.load(f)
+    g = z["small_sino"].astype(np.float64)  # 128 x 90
+    # polar_to_cartesian_frequency on the reference's own polar spectrum, padded lattice (dw = pi/2)
+    H = z["small_H"]
+    ps = pkg.PolarSpectrum(H.shape[0], H.shape[1], kat["small_dsigma"], H)
+    grid = pkg.polar_to_cartesian_frequency(ps, 128, 128, dw=math.pi / 2)
+    assert report("polar_to_cartesian_frequency", grid.values, z["small_grid"]) <= 1e-6
+    # bst_spectrum: the engine's native product on the n_out lattice
+    spec = pkg.bst_spectrum(pkg.Sinogram(*g.shape, g), pkg.BstOptions(n_out=64))
+    assert report("bst_spectrum", spec.values, z["small_spectrum"]) <= RTOL
+    # exact mean through <g, chord>
+    m = pkg.mean_backprojection(pkg.Sinogram(256, 256, phantoms.config_sinogram(0).astype(np.float64)))
+    assert abs(m - kat["mean_bp_cfg0"]) <= 1e-6 * abs(kat["mean_bp_cfg0"])
+    with pytest.raises(ValueError, match="polar spectrum reaches sigma"):
+        pkg.polar_to_cartesian_frequency(ps, 1024, 1024)
