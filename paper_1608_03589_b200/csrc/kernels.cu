@@ -527,8 +527,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
 
       if (rd) {  // readout: taps from this step's rows and the previous step's last row
         auto pixel = [&](const uint4& ent) {
-          const int qq = (int)(ent.x & 0x7FFFFFFFu);
-          const int qy = qq / nq, qx = qq - (qq / nq) * nq;
+          const int qy = (int)(ent.x & 0x7FFFu), qx = (int)((ent.x >> 15) & 0xFFFFu);
           const int iyp = c + qy, iyn = n - 1 - c - qy;
           const int jxp = c + qx, jxn = n - 1 - c - qx;
           const bool dupy = iyn == iyp, dupx = jxn == jxp;  // odd n: centre row / column

@@ -134,7 +134,9 @@ void build_bands(HostPlan& h, int band_rows) {
     uint32_t wi = 0, wj = 0;
     std::memcpy(&wi, &h.qw[qq].x, 4);
     std::memcpy(&wj, &h.qw[qq].y, 4);
-    h.band_packed[4 * e + 0] = ent;
+    // qy | qx << 15 | zero flag << 31: the device reads the quadrant position without a division
+    const uint32_t qy = qq / (uint32_t)h.nq, qx = qq % (uint32_t)h.nq;
+    h.band_packed[4 * e + 0] = qy | (qx << 15) | (ent & 0x80000000u);
     h.band_packed[4 * e + 1] = h.qidx[qq];
     h.band_packed[4 * e + 2] = wi;
     h.band_packed[4 * e + 3] = wj;

@@ -41,7 +41,7 @@ struct HostPlan {
   // with i0 in [r0 - 1, r0 + 3) (bit 31 set = write zero), band_off[b..b+1).
   int band_rows = 0, row_min = 0, nbands = 0;
   std::vector<uint32_t> band_entries, band_off;
-  // self-contained 16-byte entries {qq | zero flag, qidx, wi bits, wj bits}
+  // self-contained 16-byte entries {qy | qx << 15 | zero flag << 31, qidx, wi bits, wj bits}
   std::vector<uint32_t> band_packed;
   // generic sizes (nphi not a power of two in [512, 4096], ...): Bluestein DFTs of
   // length nphi through MB-point convolutions, MB = pow2 >= 2 nphi
