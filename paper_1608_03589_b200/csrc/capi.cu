@@ -1,5 +1,6 @@
 // C ABI (include/lpbp.h): plan lifetime, device tables, chunked executors.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges per stage for timeline tools
 
 #include <algorithm>
 #include <cmath>
@@ -160,9 +161,18 @@ cudaEvent_t take_event(lpbp_plan* P) {
   return e;
 }
 
+constexpr const char* kStageNames[kStages] = {"lpbp.ramp_filter", "lpbp.row_rdft", "lpbp.rho_conv",
+                                               "lpbp.row_irdft", "lpbp.readout", "lpbp.irdft_readout"};
+
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <typename F>
 cudaError_t staged(const lpbp_plan* Pc, int stage, int slices, cudaStream_t s, F&& launch) {
   lpbp_plan* P = const_cast<lpbp_plan*>(Pc);
+  NvtxRange range(kStageNames[stage]);
   if (!P->profiling) return launch();
   std::lock_guard<std::mutex> lk(P->prof_mu);
   cudaEvent_t a = take_event(P), b = take_event(P);

@@ -228,3 +228,23 @@ def test_bst_against_reference_directly(reference):
     for kw in ({}, dict(beta=3.0, zero_pad=1.5), dict(dc_mode="kernel_cap")):
         assert rel(O.bst_backproject(g, 90, **kw), bst_backproject(s, BstOptions(n_out=90, **kw)).values) < TOL
     assert rel(O.fbp_bst(g, 90, 0.1, 0.8), fb.fbp(s, fb.FilterSpec(lam=0.1, cutoff=0.8), n=90).values) < TOL
+
+
+def _direct_stencil(lp: np.ndarray, drho: float) -> np.ndarray:
+    """The log-polar convolution summed directly over the kernel's cells: causal in rho,
+    circular in phi (the definition the FFT form of logpolar.py:100-118 implements)."""
+    nrho, nphi = lp.shape
+    kern = np.roll(O.lp_kernel(nrho, nphi, drho), -(nphi // 2), axis=1)
+    out = np.zeros_like(lp)
+    for k, l in zip(*np.nonzero(kern)):
+        out[k:, :] += kern[k, l] * np.roll(lp[:nrho - k, :], l, axis=1)
+    return 0.5 * drho * (2.0 * math.pi / nphi) * out
+
+
+def test_fft_convolution_equals_direct_stencil():
+    """SPEC's invariant (FFT convolution = direct spatial convolution) on the oracle."""
+    rng = np.random.default_rng(9)
+    for nrho, nphi in ((16, 16), (40, 64), (353, 512)):
+        lp = rng.standard_normal((nrho, nphi))
+        drho = 5.545177 / nrho
+        assert rel(O.lp_convolve(lp, drho), _direct_stencil(lp, drho)) < 1e-10
