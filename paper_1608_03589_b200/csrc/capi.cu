@@ -185,9 +185,16 @@ cudaError_t staged(const lpbp_plan* Pc, int stage, int slices, cudaStream_t s, F
 
 // Run the stages for one chunk already resident on the device.
 // stop_after_lp: write the log-polar image to lp_out and skip filter/readout.
+// win > 0: compacted input rows (sector path) of `win` floats: `win_lo` leading columns,
+// then the row's last win - win_lo columns; everything between is zero.
 int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, cudaStream_t s, bool stop_after_lp,
-              float* lp_out) {
-  const Dims& d = P->d;
+              float* lp_out, int win = 0, int win_lo = 0) {
+  Dims dl = P->d;
+  if (win > 0) {
+    dl.win = win;
+    dl.win_lo = win_lo;
+  }
+  const Dims& d = dl;
   char* A = ws;
   char* B = ws + align256(P->szA * c);
   int* counter = reinterpret_cast<int*>(B + align256(P->szB * c));
@@ -661,8 +668,13 @@ int lpbp_radon_ellipses(const double* params_dev, int32_t k, int32_t nt, int32_t
 
 struct lpbp_sector_plan {
   lpbp::SectorSetHost h;
-  std::vector<lpbp_plan*> sub;  // per-sector log-polar stage (explicit rho0, no filter)
-  std::vector<const lpbp::SectorCol*> cols;
+  // log-polar stage per sector (explicit rho0, no filter).  Sectors whose meshes coincide
+  // (same rho0_s and nrho_s, e.g. equal beta and a_r) share one plan and run as one batch.
+  std::vector<lpbp_plan*> sub;     // per sector (aliases the group's plan)
+  std::vector<lpbp_plan*> owned;   // one per group
+  std::vector<std::vector<int>> groups;  // sector indices per group
+  std::vector<const lpbp::SectorCol*> cols;   // full-width (reference layout; stage API)
+  std::vector<const lpbp::SectorCol*> ccols;  // compacted (execute)
   std::vector<const lpbp::SectorRow*> rows;
   std::vector<size_t> own_table_bytes;
   std::vector<void*> allocs;
@@ -677,7 +689,7 @@ struct lpbp_sector_plan {
   cudaStream_t s_host = nullptr;
   ~lpbp_sector_plan() {
     DeviceGuard g(device);
-    for (auto* p : sub) delete p;
+    for (auto* p : owned) delete p;
     for (void* p : allocs) cudaFree(p);
     if (own_ws) cudaFree(own_ws);
     if (d_in) cudaFree(d_in);
@@ -688,43 +700,62 @@ struct lpbp_sector_plan {
 
 namespace {
 
+// [working sinograms of the largest group][log-polar images, per group: members x chunk][sub-plan ws]
 size_t sector_ws_bytes(const lpbp_sector_plan* P, int chunk) {
   const auto& h = P->h;
-  size_t sub = 0, lp = 0;
-  for (size_t s = 0; s < P->sub.size(); ++s) {
-    sub = std::max(sub, ws_bytes_for(P->sub[s], chunk));
-    lp += align256((size_t)chunk * P->sub[s]->d.nrho * P->sub[s]->d.nphi * sizeof(float));
+  size_t sub = 0, lp = 0, work = 0;
+  for (size_t g = 0; g < P->groups.size(); ++g) {
+    const lpbp_plan* S = P->owned[g];
+    const size_t m = P->groups[g].size();
+    work = std::max(work, m * chunk * h.nt * (size_t)h.sec[P->groups[g][0]].wpad);
+    sub = std::max(sub, ws_bytes_for(S, (int)(m * chunk)));
+    lp += align256(m * chunk * S->d.nrho * S->d.nphi * sizeof(float));
   }
-  return align256((size_t)chunk * h.nt * h.ntheta * sizeof(float)) + lp + sub;
+  return align256(work * sizeof(float)) + lp + sub;
 }
 
 int sector_chunk(const lpbp_sector_plan* P, const float* in, float* out, int c, char* ws, cudaStream_t st) {
   const auto& h = P->h;
+  size_t work_floats = 0;
+  for (const auto& g : P->groups) work_floats = std::max(work_floats, g.size() * c * h.nt * (size_t)h.sec[g[0]].wpad);
   float* work = reinterpret_cast<float*>(ws);
-  char* cur = ws + align256((size_t)c * h.nt * h.ntheta * sizeof(float));
+  char* cur = ws + align256(work_floats * sizeof(float));
   lpbp::SectorArgs args{};
   const int nsec = (int)P->sub.size();
-  for (int s = 0; s < nsec; ++s) {
-    const lpbp_plan* S = P->sub[s];
-    auto& a = args.s[s];
-    a.lp = reinterpret_cast<const float*>(cur);
-    a.lp_slice = (long long)S->d.nrho * S->d.nphi;
-    a.nrho = S->d.nrho;
-    a.rho0 = S->h.rho0;
-    a.drho = S->h.drho;
-    a.ct = std::cos(h.sec[s].theta_c);
-    a.st = std::sin(h.sec[s].theta_c);
-    a.a_r = h.sec[s].spec.a_r;
-    a.inv_a = (float)(1.0 / h.sec[s].spec.a_r);
-    cur += align256((size_t)c * S->d.nrho * S->d.nphi * sizeof(float));
+  std::vector<float*> lp_group(P->groups.size());
+  for (size_t g = 0; g < P->groups.size(); ++g) {
+    const lpbp_plan* S = P->owned[g];
+    const size_t per = (size_t)c * S->d.nrho * S->d.nphi;  // one sector's images for the chunk
+    lp_group[g] = reinterpret_cast<float*>(cur);
+    for (size_t k = 0; k < P->groups[g].size(); ++k) {
+      const int s = P->groups[g][k];
+      auto& a = args.s[s];
+      a.lp = lp_group[g] + k * per;
+      a.lp_slice = (long long)S->d.nrho * S->d.nphi;
+      a.nrho = S->d.nrho;
+      a.rho0 = S->h.rho0;
+      a.drho = S->h.drho;
+      a.ct = std::cos(h.sec[s].theta_c);
+      a.st = std::sin(h.sec[s].theta_c);
+      a.a_r = h.sec[s].spec.a_r;
+      a.inv_a = (float)(1.0 / h.sec[s].spec.a_r);
+    }
+    cur += align256(P->groups[g].size() * per * sizeof(float));
   }
   char* subws = cur;
-  for (int s = 0; s < nsec; ++s) {
-    cudaError_t e = lpbp::launch_sector_prep(in, work, h.nt, h.ntheta, c, P->cols[s], P->rows[s],
-                                             h.sec[s].spec.a_r, h.sec[s].klo, h.sec[s].khi, st);
-    if (e) return launch_fail(e, "sector_prep");
-    ++g_launches;
-    int rc = run_chunk(P->sub[s], work, nullptr, c, subws, st, true, const_cast<float*>(args.s[s].lp));
+  for (size_t g = 0; g < P->groups.size(); ++g) {
+    const auto& members = P->groups[g];
+    const int wpad = h.sec[members[0]].wpad;
+    const size_t w_slice = (size_t)h.nt * wpad;
+    for (size_t k = 0; k < members.size(); ++k) {  // compacted working sinograms of the group, back to back
+      const int s = members[k];
+      cudaError_t e = lpbp::launch_sector_prep(in, work + k * c * w_slice, h.nt, wpad, h.ntheta, c, P->ccols[s],
+                                               P->rows[s], h.sec[s].spec.a_r, h.sec[s].klo, h.sec[s].khi, st);
+      if (e) return launch_fail(e, "sector_prep");
+      ++g_launches;
+    }
+    int rc = run_chunk(P->owned[g], work, nullptr, (int)(members.size() * c), subws, st, true, lp_group[g], wpad,
+                       h.sec[members[0]].lo);
     if (rc) return rc;
   }
   cudaError_t e = lpbp::launch_sector_readout(args, nsec, out, h.n, 2 * h.ntheta, c, st);
@@ -754,7 +785,19 @@ int lpbp_sector_plan_create(int32_t nt, int32_t ntheta, int32_t n_out, const lpb
     return fail(LPBP_EINVAL, err);
   }
   P->device = device;
-  for (const auto& S : P->h.sec) {
+  for (size_t q = 0; q < P->h.sec.size(); ++q) {
+    const auto& S = P->h.sec[q];
+    bool shared = false;  // an existing plan with the same mesh
+    for (size_t g = 0; g < P->groups.size() && !shared; ++g) {
+      const lpbp_plan* o = P->owned[g];
+      const auto& S0 = P->h.sec[P->groups[g][0]];
+      if (o->h.rho0 == S.rho0 && o->h.nrho == S.nrho && S0.wpad == S.wpad && S0.lo == S.lo) {
+        P->groups[g].push_back((int)q);
+        P->sub.push_back(P->owned[g]);
+        shared = true;
+      }
+    }
+    if (shared) continue;
     lpbp_params sp{};
     sp.nt = nt;
     sp.ntheta = ntheta;
@@ -771,26 +814,33 @@ int lpbp_sector_plan_create(int32_t nt, int32_t ntheta, int32_t n_out, const lpb
       delete P;
       return fail(rc, msg);
     }
+    P->owned.push_back(sub);
+    P->groups.push_back({(int)q});
     P->sub.push_back(sub);
   }
   if (device >= 0) {
     DeviceGuard g(device);
     for (const auto& S : P->h.sec) {
-      void *c = nullptr, *r = nullptr;
-      const size_t cb = S.cols.size() * sizeof(lpbp::SectorCol), rb = S.rows.size() * sizeof(lpbp::SectorRow);
+      void *c = nullptr, *cc = nullptr, *r = nullptr;
+      const size_t cb = S.cols.size() * sizeof(lpbp::SectorCol), ccb = S.ccols.size() * sizeof(lpbp::SectorCol);
+      const size_t rb = S.rows.size() * sizeof(lpbp::SectorRow);
       cudaError_t e = cudaMalloc(&c, cb);
       if (e == cudaSuccess) P->allocs.push_back(c);
+      if (e == cudaSuccess) e = cudaMalloc(&cc, ccb);
+      if (e == cudaSuccess) P->allocs.push_back(cc);
       if (e == cudaSuccess) e = cudaMalloc(&r, rb);
       if (e == cudaSuccess) P->allocs.push_back(r);
       if (e == cudaSuccess) e = cudaMemcpy(c, S.cols.data(), cb, cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = cudaMemcpy(cc, S.ccols.data(), ccb, cudaMemcpyHostToDevice);
       if (e == cudaSuccess) e = cudaMemcpy(r, S.rows.data(), rb, cudaMemcpyHostToDevice);
       if (e != cudaSuccess) {
         delete P;
         return cuda_fail(e, "sector tables");
       }
       P->cols.push_back(static_cast<const lpbp::SectorCol*>(c));
+      P->ccols.push_back(static_cast<const lpbp::SectorCol*>(cc));
       P->rows.push_back(static_cast<const lpbp::SectorRow*>(r));
-      P->own_table_bytes.push_back(cb + rb);
+      P->own_table_bytes.push_back(cb + ccb + rb);
     }
   } else {
     P->own_table_bytes.assign(P->h.sec.size(), 0);
@@ -920,8 +970,9 @@ int lpbp_sector_prepare(const lpbp_sector_plan* P, int32_t index, const float* s
   if (!sino_dev || !out_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
   const auto& S = P->h.sec[index];
-  cudaError_t e = lpbp::launch_sector_prep(sino_dev, out_dev, P->h.nt, P->h.ntheta, batch, P->cols[index],
-                                           P->rows[index], S.spec.a_r, S.klo, S.khi, static_cast<cudaStream_t>(stream));
+  cudaError_t e = lpbp::launch_sector_prep(sino_dev, out_dev, P->h.nt, P->h.ntheta, P->h.ntheta, batch,
+                                           P->cols[index], P->rows[index], S.spec.a_r, S.klo, S.khi,
+                                           static_cast<cudaStream_t>(stream));
   if (e) return launch_fail(e, "sector_prep");
   ++g_launches;
   return LPBP_OK;

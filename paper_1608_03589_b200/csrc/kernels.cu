@@ -121,10 +121,12 @@ struct RdftShape {
   static constexpr size_t SMEM = ((size_t)2 * IN + STG + G * BUF) * 8 + 64;
 };
 
-template <int NPHI>
+// NARROW: compacted input rows (the sector path): `win` (multiple of 4) floats holding the
+// row's first win_lo columns followed by its last win - win_lo columns; the rest is zero.
+template <int NPHI, bool NARROW>
 __global__ void __launch_bounds__(RdftShape<NPHI>::G * FftPlan<NPHI, false>::T, 1)
 k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int ntiles_per_slice, int ntiles,
-           const float2* __restrict__ tw) {
+           const float2* __restrict__ tw, int win, int win_lo) {
   using RS = RdftShape<NPHI>;
   constexpr int T = FftPlan<NPHI, false>::T;
   constexpr int TR = RS::TR, NTH = RS::NTH, NH = RS::NH;
@@ -134,10 +136,11 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int nti
   float2* buf = stg + RS::STG + (threadIdx.x / T) * RS::BUF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg + RS::STG + RS::G * RS::BUF);
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
-  constexpr uint32_t TILE_BYTES = TR * NTH * 4;
+  const int W = NARROW ? win : NTH;  // input row pitch (floats)
+  const uint32_t TILE_BYTES = TR * W * 4;
   auto tile_src = [&](int tile) {
     const int b = tile / ntiles_per_slice, t0 = (tile - b * ntiles_per_slice) * TR;
-    return g + ((size_t)b * nt + t0) * NTH;
+    return g + ((size_t)b * nt + t0) * W;
   };
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -160,9 +163,16 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int nti
   for (int tile = first; tile < ntiles; tile += stride, ++it) {
     const int sl = it & 1;
     mbar_wait(&bars[sl], (it >> 1) & 1);
-    const float* ra = in0 + sl * TR * NTH + (2 * gi) * NTH;
-    const float* rb = ra + NTH;
-    auto load = [&](int idx) -> float2 { return make_float2(ra[idx], rb[idx]); };  // idx < NTH (IN_HALF)
+    const float* ra = in0 + sl * TR * NTH + (2 * gi) * W;
+    const float* rb = ra + W;
+    auto load = [&](int idx) -> float2 {  // idx < NTH (IN_HALF)
+      if constexpr (NARROW) {
+        const int tail = NTH - (W - win_lo);  // first row position of the trailing block
+        if (idx >= win_lo && idx < tail) return make_float2(0.f, 0.f);
+        if (idx >= tail) idx -= tail - win_lo;
+      }
+      return make_float2(ra[idx], rb[idx]);
+    };
     auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
     block_fft<NPHI, false, true, false, true, 16>(buf, ti, tw, load, store, GroupSync{1 + gi, T});
     __syncthreads();
@@ -683,7 +693,7 @@ k_ramp_generic(const float* __restrict__ g, float* __restrict__ out, int nt, int
 
 template <int MB>
 __global__ void __launch_bounds__(FftPlan<MB, false>::T)
-k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int ntheta,
+k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int ntheta, int win, int win_lo,
                    const float2* __restrict__ chirp, const float2* __restrict__ bhat, const float2* __restrict__ tw) {
   extern __shared__ __align__(16) float2 smem_g2[];
   const int nphi = 2 * ntheta, nh = ntheta + 1;
@@ -691,11 +701,13 @@ k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt,
   float2* Z = smem_g2 + padded_len(MB);  // [nphi]
   const int ta = 2 * blockIdx.x, tb = ta + 1;
   const bool hb = tb < nt;
-  const float* ra = g + ((size_t)blockIdx.y * nt + ta) * ntheta;
-  const float* rb = ra + ntheta;
+  const float* ra = g + ((size_t)blockIdx.y * nt + ta) * win;  // rows of `win` (<= ntheta) columns
+  const float* rb = ra + win;
+  const int tail = ntheta - (win - win_lo);  // compacted rows: [0, win_lo) and [tail, ntheta) are stored
   auto load = [&](int idx) -> float2 {  // a[n] = z[n] c[n]; z is zero for n >= ntheta
-    if (idx >= ntheta) return make_float2(0.f, 0.f);
-    const float2 z = make_float2(__ldg(ra + idx), hb ? __ldg(rb + idx) : 0.f);
+    if (idx >= ntheta || (idx >= win_lo && idx < tail)) return make_float2(0.f, 0.f);
+    const int src = idx >= tail ? idx - (tail - win_lo) : idx;  // storage column
+    const float2 z = make_float2(__ldg(ra + src), hb ? __ldg(rb + src) : 0.f);
     return cmul(z, __ldg(chirp + idx));
   };
   auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(bhat + idx)); };
@@ -833,7 +845,10 @@ template <int NPHI>
 cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch, cudaStream_t s) {
   using RS = RdftShape<NPHI>;
   if (d.nt % RS::TR) return cudaErrorNotSupported;
-  auto k = k_row_rdft<NPHI>;
+  const int win = d.win > 0 ? d.win : d.ntheta;
+  const bool narrow = win < d.ntheta;
+  if (narrow && (win % 4)) return cudaErrorNotSupported;  // TMA bulk rows: 16-byte multiples
+  auto k = narrow ? k_row_rdft<NPHI, true> : k_row_rdft<NPHI, false>;
   cudaError_t e = prep(k, RS::SMEM);
   if (e) return e;
   const int per = d.nt / RS::TR, tiles = per * batch;
@@ -841,7 +856,7 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, RS::G * FftPlan<NPHI, false>::T, RS::SMEM);
   const int slots = d.nsm * (occ > 0 ? occ : 1);
   const int grid = tiles < slots ? tiles : slots;
-  k<<<grid, RS::G * FftPlan<NPHI, false>::T, RS::SMEM, s>>>(g, Gh, d.nt, per, tiles, t.tw_phi);
+  k<<<grid, RS::G * FftPlan<NPHI, false>::T, RS::SMEM, s>>>(g, Gh, d.nt, per, tiles, t.tw_phi, win, d.win_lo);
   return cudaGetLastError();
 }
 
@@ -980,8 +995,9 @@ cudaError_t rdft_generic_impl(const Dims& d, const DevTables& t, const float* g,
   auto k = k_row_rdft_generic<MB>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
-  k<<<dim3((d.nt + 1) / 2, batch), FftPlan<MB, false>::T, smem, s>>>(g, Gh, d.nt, d.ntheta, t.chirp, t.bhat_f,
-                                                                    t.tw_blue);
+  const int win = d.win > 0 ? d.win : d.ntheta, win_lo = d.win > 0 ? d.win_lo : d.ntheta;
+  k<<<dim3((d.nt + 1) / 2, batch), FftPlan<MB, false>::T, smem, s>>>(g, Gh, d.nt, d.ntheta, win, win_lo, t.chirp,
+                                                                    t.bhat_f, t.tw_blue);
   return cudaGetLastError();
 }
 template <int MB>

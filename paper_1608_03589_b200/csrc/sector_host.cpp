@@ -97,6 +97,27 @@ std::string build_sector_set(int nt, int ntheta, int n_out, const std::vector<Se
       c.w2 = (float)(base - fl);
       S.cols[j] = c;
     }
+    // compacted columns: nonzero weights form the cyclic block [ntheta - a, ntheta) u [0, b]
+    {
+      int b = -1, a = 0;
+      while (b + 1 < ntheta && S.cols[b + 1].w != 0.f) ++b;
+      while (a < ntheta - (b + 1) && S.cols[ntheta - 1 - a].w != 0.f) ++a;
+      int nz = 0;
+      for (const auto& c : S.cols) nz += c.w != 0.f;
+      const int lo = b + 1, W = a + lo;
+      const int wpad = (W + 3) / 4 * 4;
+      if (nz == W && wpad < ntheta) {  // one cyclic block, narrower than the row: compact it
+        S.lo = lo;
+        S.wpad = wpad;
+        S.ccols.assign(wpad, SectorCol{});  // padding columns: weight 0, written as zeros
+        for (int w = 0; w < lo; ++w) S.ccols[w] = S.cols[w];
+        for (int w = 0; w < a; ++w) S.ccols[wpad - a + w] = S.cols[ntheta - a + w];
+      } else {  // wide or split sectors: full width
+        S.lo = ntheta;
+        S.wpad = ntheta;
+        S.ccols = S.cols;
+      }
+    }
     // shrunk support rows: fi = (t_k / a_r + 1) / dt
     S.rows.resize(nt);
     S.klo = 0;

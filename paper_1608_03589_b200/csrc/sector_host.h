@@ -37,7 +37,14 @@ struct SectorHost {
   double support_min = 0;   // logpolar.py:278
   double rho0 = 0;          // sector mesh depth (logpolar.py:279-283)
   int nrho = 0;             // _mesh_for(ns, rho0, None)
-  std::vector<SectorCol> cols;  // [ntheta]
+  std::vector<SectorCol> cols;  // [ntheta] the reference's working-frame columns
+  // Compacted storage of the working sinogram for the log-polar stage: the nonzero-weight
+  // columns form the cyclic block [0, lo) u [ntheta - hi, ntheta); rows are stored as
+  // [lo leading columns][zero padding][hi trailing columns], wpad wide (multiple of 4).  The
+  // row DFT maps the trailing part back to the row's end, so the values are exactly the
+  // reference's; only the zero columns are never written or read.
+  int lo = 0, wpad = 0;
+  std::vector<SectorCol> ccols;  // [wpad]
   std::vector<SectorRow> rows;  // [nt]
   int klo = 0, khi = -1;        // rows k of the shrunk sinogram that can be nonzero (a tap in [0, nt))
 };

@@ -19,29 +19,30 @@ namespace {
 // fp64 host tables (per column: source, flip, weight, shift base; per row: the
 // shrink lerp), so a sample is 4 gathers and a few FMAs.
 __global__ void __launch_bounds__(256)
-k_sector_prep(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
+k_sector_prep(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta, int nin,
               const SectorCol* __restrict__ cols, const SectorRow* __restrict__ rows, double a_r, int klo, int khi) {
   const int j = blockIdx.x * 32 + threadIdx.x;
   const int i = blockIdx.y * 8 + threadIdx.y;
   if (j >= ntheta || i >= nt) return;
-  const size_t slice = (size_t)blockIdx.z * nt * ntheta;
+  const size_t slice_in = (size_t)blockIdx.z * nt * nin;
+  const size_t slice_out = (size_t)blockIdx.z * nt * ntheta;
   const SectorCol c = cols[j];
   const float w2 = c.w2;
   const int k2 = i + c.d;  // floor((t_i - off + 1) / dt) with the per-column fraction w2
   // zero-weight angle (outside this sector's extended mask) or both shrink taps outside the
   // rows that can be nonzero: the sample is exactly zero, skip the loads
   if (c.w == 0.f || k2 + 1 < klo || k2 > khi) {
-    out[slice + (size_t)i * ntheta + j] = 0.f;
+    out[slice_out + (size_t)i * ntheta + j] = 0.f;
     return;
   }
-  const float* col = g + slice + c.src;
+  const float* col = g + slice_in + c.src;
   auto rolled = [&](int m) -> float {
     if (m < 0 || m >= nt) return 0.f;
     if (c.flip) {
       if (m == 0) return 0.f;  // t = -1 maps to +1, off the grid
       m = nt - m;
     }
-    return __ldg(col + (size_t)m * ntheta);
+    return __ldg(col + (size_t)m * nin);
   };
   const float a = (float)a_r;
   auto scaled = [&](int k) -> float {
@@ -49,7 +50,7 @@ k_sector_prep(const float* __restrict__ g, float* __restrict__ out, int nt, int 
     const SectorRow r = rows[k];
     return a * ((rolled(r.k1) * c.w) * (1.f - r.w1) + (rolled(r.k1 + 1) * c.w) * r.w1);
   };
-  out[slice + (size_t)i * ntheta + j] = scaled(k2) * (1.f - w2) + scaled(k2 + 1) * w2;
+  out[slice_out + (size_t)i * ntheta + j] = scaled(k2) * (1.f - w2) + scaled(k2 + 1) * w2;
 }
 
 // Sum of every sector's bilinear log-polar sample at the working-frame image of
@@ -117,11 +118,12 @@ k_sector_readout(const __grid_constant__ SectorArgs secs, int nsec, float* __res
 
 }  // namespace
 
-cudaError_t launch_sector_prep(const float* g, float* out, int nt, int ntheta, int batch, const SectorCol* cols,
-                               const SectorRow* rows, double a_r, int klo, int khi, cudaStream_t s) {
+cudaError_t launch_sector_prep(const float* g, float* out, int nt, int ntheta, int nin, int batch,
+                               const SectorCol* cols, const SectorRow* rows, double a_r, int klo, int khi,
+                               cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   const dim3 grid((ntheta + 31) / 32, (nt + 7) / 8, batch);
-  k_sector_prep<<<grid, dim3(32, 8), 0, s>>>(g, out, nt, ntheta, cols, rows, a_r, klo, khi);
+  k_sector_prep<<<grid, dim3(32, 8), 0, s>>>(g, out, nt, ntheta, nin, cols, rows, a_r, klo, khi);
   return cudaGetLastError();
 }
 

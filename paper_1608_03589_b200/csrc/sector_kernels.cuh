@@ -18,15 +18,17 @@ struct SectorDev {
   float pad2;
 };
 
-constexpr int kSectorGroup = 8;   // slices per readout thread (coordinates computed once per group)
+constexpr int kSectorGroup = 16;  // slices per readout thread (coordinates computed once per group)
 constexpr int kMaxSectors = 32;   // sectors per plan (the readout takes them as one kernel argument)
 
 struct SectorArgs {
   SectorDev s[kMaxSectors];
 };
 
-cudaError_t launch_sector_prep(const float* g, float* out, int nt, int ntheta, int batch, const SectorCol* cols,
-                               const SectorRow* rows, double a_r, int klo, int khi, cudaStream_t s);
+// out [batch][nt][ntheta] (ntheta = output columns, the cols table's length); g [batch][nt][nin]
+cudaError_t launch_sector_prep(const float* g, float* out, int nt, int ntheta, int nin, int batch,
+                               const SectorCol* cols, const SectorRow* rows, double a_r, int klo, int khi,
+                               cudaStream_t s);
 cudaError_t launch_sector_readout(const SectorArgs& secs, int nsec, float* img, int n, int nphi, int batch,
                                   cudaStream_t s);
 
