@@ -285,11 +285,10 @@ def run_ours(a, d: Dist):
     import torch
 
     import paper_1608_03589_b200 as p
-    from oracle import phantoms
 
     torch.cuda.set_device(d.local)
     dev = torch.device("cuda", d.local)
-    c = phantoms.CONFIGS[a.config]
+    c = p.synth.CONFIGS[a.config]
     nt, nth, n = c["nt"], c["ntheta"], c["n"]
     S = a.slices or c["slices"]
     spec = (0.0, 1.0) if c["fbp"] else None
@@ -430,11 +429,10 @@ def run_direct(a, d: Dist):
     import torch
 
     import paper_1608_03589_b200 as p
-    from oracle import phantoms
 
     torch.cuda.set_device(d.local)
     dev = torch.device("cuda", d.local)
-    c = phantoms.CONFIGS[4]
+    c = p.synth.CONFIGS[4]
     S = a.slices or 16
     x = p.synth.config_batch(4, range(d.rank * S, (d.rank + 1) * S), dev)
     for _ in range(a.warmup):

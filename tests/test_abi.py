@@ -393,3 +393,15 @@ def test_bst_host_helpers_against_reference(reference):
         p.kaiser_window(1, 1.0)
     with pytest.raises(ValueError, match="dsigma must be positive"):
         p.sigma_kernel(4, 0.0)
+
+
+def test_synth_configs_match_oracle_phantoms():
+    """bench.py's measured arm reads the package's copy of the config table; it must not drift."""
+    from oracle import phantoms
+    from paper_1608_03589_b200 import synth
+    assert synth.CONFIGS == phantoms.CONFIGS
+    assert synth.BASE_SEED == phantoms.BASE_SEED
+    for seed in (phantoms.BASE_SEED, phantoms.BASE_SEED + 7919 * 3 + 11):
+        e = phantoms.random_ellipses(seed, 50, 0.01, 0.3)
+        ref = np.stack([e.cx, e.cy, e.a, e.b, e.tilt, e.rho], axis=1)
+        assert np.array_equal(synth.ellipse_params(seed, 50, 0.01, 0.3), ref)
