@@ -12,9 +12,12 @@ import csv, io, os, re, subprocess, sys, tempfile
 from collections import defaultdict
 
 rep, kre, mangled = sys.argv[1], sys.argv[2], sys.argv[3]
-so = sys.argv[4] if len(sys.argv) > 4 else os.path.join(os.path.dirname(__file__), "..", "paper_1608_03589_b200",
-                                                         "liblpbp.so")
-top = int(sys.argv[5]) if len(sys.argv) > 5 else 40
+rest = sys.argv[4:]
+top = 40
+if rest and rest[-1].isdigit():  # [SO] [TOP] in either form
+    top = int(rest.pop())
+so = rest[0] if rest else os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1608_03589_b200",
+                                       "liblpbp.so")
 NF = int(os.environ.get("NF", "2"))
 
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{kre}"],
@@ -36,7 +39,7 @@ for r in rows[2:]:
     samples[a] = (int(r[ist] or 0), r[isrc].strip(), int(r[iex] or 0))
 
 tmp = tempfile.mkdtemp()
-subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
+subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
 chain_of = {}
 for cub in os.listdir(tmp):
     dis = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
