@@ -312,7 +312,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     delete P;
     return fail(LPBP_EUNSUPPORTED, "no kernel instantiation for nt=" + std::to_string(h.nt) + ", ntheta=" +
                                        std::to_string(h.ntheta) + ", L=" + std::to_string(h.L) +
-                                       " (this build: nt even, 2*ntheta <= 4096, 2*nt <= 4096, rho FFT <= 8192)");
+                                       " (this build: 2*ntheta <= 4096, 2*nt <= 4096, rho FFT <= 8192)");
   }
   P->device = params->device;
   if (lpbp::fused_band_rows(P->h.nphi) > 0) lpbp::build_bands(P->h, lpbp::fused_band_rows(P->h.nphi));
@@ -353,6 +353,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   }
   Dims& d = P->d;
   d.nt = h.nt;
+  d.gp = h.nt + (h.nt & 1);
   d.ntheta = h.ntheta;
   d.n = h.n;
   d.ns = h.ns;
@@ -373,7 +374,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   if (P->device >= 0) cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, P->device);
   const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;
   const size_t Y = (size_t)h.nh * h.nrho_pad * sizeof(float2);
-  const size_t G = (size_t)h.nh * h.nt * sizeof(float2);
+  const size_t G = (size_t)h.nh * (h.nt + (h.nt & 1)) * sizeof(float2);
   const size_t lp = (size_t)h.nrho * h.nphi * sizeof(float);
   P->szA = std::max(fg, Y);
   P->szB = std::max(G, lp);

@@ -210,7 +210,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int nti
 // ---------------------------------------------------------------------------
 template <int L, bool PRUNE>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, 2)
-k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int ns, int nrho, int row_lo,
+k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int gp, int ns, int nrho, int row_lo,
            int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
            const int* __restrict__ ki, const float2* __restrict__ wi, const float2* __restrict__ khat,
            const float2* __restrict__ tw) {
@@ -224,7 +224,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   const float sg = (m & 1) ? -1.f : 1.f;
   const int ti = threadIdx.x;
   const float2* kcol = khat + (size_t)m * L;
-  const uint32_t col_bytes = (uint32_t)nt * sizeof(float2);
+  const uint32_t col_bytes = (uint32_t)gp * sizeof(float2);  // gp = nt rounded up to even
 
   if (ti == 0) {
     mbar_init(&bar, 1);
@@ -233,7 +233,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   __syncthreads();
   if (ti == 0) {
     mbar_arrive_expect_tx(&bar, col_bytes);
-    tma_bulk_g2s(gcol, Gh + (size_t)m * nt, col_bytes, &bar);
+    tma_bulk_g2s(gcol, Gh + (size_t)m * gp, col_bytes, &bar);
   }
 
   for (int b = 0; b < batch; ++b) {
@@ -253,7 +253,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     if (ti == 0 && b + 1 < batch) {  // the column is consumed: fetch the next slice's across the transforms
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&bar, col_bytes);
-      tma_bulk_g2s(gcol, Gh + ((size_t)(b + 1) * nh + m) * nt, col_bytes, &bar);
+      tma_bulk_g2s(gcol, Gh + ((size_t)(b + 1) * nh + m) * gp, col_bytes, &bar);
     }
     auto load = [&](int idx) -> float2 {
       if (idx >= nrho) return make_float2(0.f, 0.f);
@@ -693,7 +693,7 @@ k_ramp_generic(const float* __restrict__ g, float* __restrict__ out, int nt, int
 
 template <int MB>
 __global__ void __launch_bounds__(FftPlan<MB, false>::T)
-k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int ntheta, int win, int win_lo,
+k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int gp, int ntheta, int win, int win_lo,
                    const float2* __restrict__ chirp, const float2* __restrict__ bhat, const float2* __restrict__ tw) {
   extern __shared__ __align__(16) float2 smem_g2[];
   const int nphi = 2 * ntheta, nh = ntheta + 1;
@@ -716,11 +716,11 @@ k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt,
   };
   block_conv<MB, true>(buf, threadIdx.x, tw, load, mul, store, block_sync);
   __syncthreads();
-  float2* dst = Gh + (size_t)blockIdx.y * nh * nt + ta;
+  float2* dst = Gh + (size_t)blockIdx.y * nh * gp + ta;
   for (int m = threadIdx.x; m < nh; m += blockDim.x) {
     const float2 z = Z[m], w = Z[m == 0 ? 0 : nphi - m];
-    dst[(size_t)m * nt] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
-    if (hb) dst[(size_t)m * nt + 1] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+    dst[(size_t)m * gp] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
+    if (hb) dst[(size_t)m * gp + 1] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
   }
 }
 
@@ -863,12 +863,13 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
 template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
                       cudaStream_t s) {
-  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)d.nt) * sizeof(float2);
+  const int gp = d.gp > 0 ? d.gp : d.nt;
+  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp) * sizeof(float2);
   // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
   auto k = (2 * d.nrho <= L) ? k_rho_conv<L, true> : k_rho_conv<L, false>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
-  k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.ab, t.wab,
+  k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, gp, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.ab, t.wab,
                                               t.ki, t.wi, t.khat, t.tw_rho);
   return cudaGetLastError();
 }
@@ -996,7 +997,8 @@ cudaError_t rdft_generic_impl(const Dims& d, const DevTables& t, const float* g,
   cudaError_t e = prep(k, smem);
   if (e) return e;
   const int win = d.win > 0 ? d.win : d.ntheta, win_lo = d.win > 0 ? d.win_lo : d.ntheta;
-  k<<<dim3((d.nt + 1) / 2, batch), FftPlan<MB, false>::T, smem, s>>>(g, Gh, d.nt, d.ntheta, win, win_lo, t.chirp,
+  k<<<dim3((d.nt + 1) / 2, batch), FftPlan<MB, false>::T, smem, s>>>(g, Gh, d.nt, d.gp > 0 ? d.gp : d.nt, d.ntheta,
+                                                                    win, win_lo, t.chirp,
                                                                     t.bhat_f, t.tw_blue);
   return cudaGetLastError();
 }
@@ -1125,7 +1127,7 @@ bool sizes_supported(int nt, int ntheta, int L, int M, int MB, bool filter, bool
   auto pow2in = [](int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; };
   if (!pow2in(L, 512, 8192)) return false;
   if (filter && !pow2in(M, 512, 8192)) return false;
-  if (generic) return pow2in(MB, 512, 8192) && (nt % 2) == 0;
+  if (generic) return pow2in(MB, 512, 8192) && nt >= 2;  // odd nt: row spectra column pitch padded to even
   const int nphi = 2 * ntheta;
   if (!pow2in(nphi, 512, 4096) || nt % 4) return false;
   if (filter && (ntheta % 8 || M > 4096)) return false;

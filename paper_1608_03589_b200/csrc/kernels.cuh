@@ -39,6 +39,8 @@ struct Dims {
   int row_min, nbands, band_rows;  // fused inverse-DFT + readout quads (band_rows = 4)
   int nsm;                         // SMs of the plan's device (persistent grids)
   int generic, MB;                 // generic-size path (Bluestein length-nphi DFTs via MB-point convolutions)
+  int gp;                          // column pitch of the row spectra G[m][.] (nt rounded up to even: TMA bulk
+                                   // column loads are 16-byte multiples); 0 = nt
   int win, win_lo;                 // compacted row-DFT input (0 = plain rows of ntheta): rows of `win` floats,
                                    // win_lo leading columns + the row's last win - win_lo columns
   float out_scale;        // 1 (backprojection) or 1/(2 pi) (fbp)

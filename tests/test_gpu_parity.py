@@ -174,11 +174,26 @@ def test_cfg4_naive_cross_check(pkg):
 
 
 def test_unsupported_size_is_loud(pkg):
-    g = pkg.Sinogram(129, 90, np.ones((129, 90)))  # odd nt: no instantiation
+    g = pkg.Sinogram(4096, 8, np.ones((4096, 8)))  # rho FFT would need 16384 points: no instantiation
     with pytest.raises(NotImplementedError):
-        pkg.logpolar_backproject(g, 64)
-    with pytest.raises(NotImplementedError):
-        pkg.fbp(g, pkg.FilterSpec(), engine="bst", n=64)
+        pkg.logpolar_backproject(g, 4096)
+    with pytest.raises(NotImplementedError):  # BST: odd nt
+        pkg.fbp(pkg.Sinogram(129, 90, np.ones((129, 90))), pkg.FilterSpec(), engine="bst", n=64)
+
+
+@pytest.mark.parametrize("nt,nth,n,filt", [(129, 90, 64, False), (255, 128, 128, True), (301, 200, 150, False)])
+def test_odd_nt(pkg, nt, nth, n, filt):
+    """Odd detector counts (the reference accepts any nt >= 2): generic row DFTs, spectra
+    columns padded to an even pitch."""
+    g = phantoms.sinogram(1100 + nt, nt, nth, 8, 0.05, 0.35, 0.01).astype(np.float64)
+    s = pkg.Sinogram(nt, nth, g)
+    if filt:
+        got = pkg.fbp(s, pkg.FilterSpec(), engine="logpolar", n=n).values
+        ref = O.fbp_logpolar(g, n)
+    else:
+        got = pkg.logpolar_backproject(s, n).values
+        ref = O.logpolar_backproject(g, n)
+    assert report(f"odd nt {nt}x{nth}->{n} {'fbp' if filt else 'bp'}", got, ref) <= RTOL
 
 
 def test_device_sinogram_generator_matches_oracle(pkg):
