@@ -37,9 +37,9 @@ try:
 except (OSError, ValueError):
     MEASURED = {}
 # dram__bytes_read.sum + dram__bytes_write.sum per slice from the committed ncu --set full
-# capture (profiles/r01e_summary.md, 8-slice launches at 2048^2 FBP, the bench's chunk)
-TRAFFIC_PER_SLICE = {"rho_conv": (403.260928e6 + 442.394624e6) / 8, "irdft_readout": (718.455552e6 + 181.567232e6) / 8,
-                     "ramp_filter": (134.275328e6 + 94.606080e6) / 8, "row_rdft": (134.241536e6 + 215.952384e6) / 8}
+# capture (profiles/r01f_summary.md, 8-slice launches at 2048^2 FBP, the bench's chunk)
+TRAFFIC_PER_SLICE = {"rho_conv": (403.292416e6 + 442.629376e6) / 8, "irdft_readout": (717.406976e6 + 179.756544e6) / 8,
+                     "ramp_filter": (134.275072e6 + 94.063872e6) / 8, "row_rdft": (134.299392e6 + 215.366400e6) / 8}
 UNIT = "slices/s"
 
 
