@@ -248,3 +248,51 @@ def test_fft_convolution_equals_direct_stencil():
         lp = rng.standard_normal((nrho, nphi))
         drho = 5.545177 / nrho
         assert rel(O.lp_convolve(lp, drho), _direct_stencil(lp, drho)) < 1e-10
+
+
+# ---- SPEC.md examples and invariants, on the oracle ----
+
+def test_spec_kernel_examples():
+    for nrho, nphi, drho in ((353, 512, 1.570872e-2), (64, 90, 0.05)):
+        k = O.lp_kernel(nrho, nphi, drho)            # columns theta_j = -pi + j 2pi/nphi
+        j0 = nphi // 2                               # theta = 0
+        assert k[0, j0] == 1.0 / drho
+        if nphi % 4 == 0:
+            assert not k[:, nphi // 4 + j0 if nphi // 4 + j0 < nphi else nphi // 4].any()  # theta = pi/2
+    # support count grows linearly with nrho at fixed rho0 (ratio within [0.5, 2] per doubling)
+    rho0 = -5.0
+    counts = [int(np.count_nonzero(O.lp_kernel(nr, 512, -rho0 / nr))) for nr in (200, 400, 800)]
+    for a, b in zip(counts, counts[1:]):
+        assert 0.5 <= (b / a) / 2.0 <= 2.0
+
+
+def test_spec_truncation_bound_examples():
+    assert abs(2 * math.pi / 1024 ** 2 - 5.99e-6) < 5e-9
+    from paper_1608_03589_b200.resample import truncation_error_bound as tb
+    assert tb(-math.log(1024.0), 1.0) == pytest.approx(2 * math.pi / 1024 ** 2, rel=1e-15)
+    assert tb(-3.0 - math.log(2.0), 1.3) == pytest.approx(tb(-3.0, 1.3) / 4.0, rel=1e-14)
+    assert tb(-745.0, 1.0) == 0.0 or tb(-745.0, 1.0) < 1e-300
+
+
+def test_spec_mesh_rule_every_size():
+    """Delta rho <= Delta s for every mesh the adaptive rule builds (1 - e^{-drho} <= 2/ns)."""
+    for nt in (64, 128, 200, 256, 512, 1000, 2048):
+        for n in (32, 64, 100, 256, 512, 2048):
+            ns, r0, nr, drho = O.lp_geometry(nt, n)
+            assert 1.0 - math.exp(-drho) <= (2.0 / ns) * (1.0 + 1e-9)
+
+
+def test_spec_truncation_error_is_bounded():
+    """The squared-L2 change between two rho0 choices stays under the bound at the shallower
+    rho0 with c = max |B g| near the origin (inequality direction only)."""
+    g = phantoms.sinogram(31, 128, 90, 6, 0.05, 0.35, 0.0).astype(np.float64)
+    n = 64
+    r_deep = O.adaptive_rho0(n, n)
+    r_shallow = r_deep + math.log(4.0)
+    a = O.logpolar_backproject(g, n, rho0=r_deep)
+    b = O.logpolar_backproject(g, n, rho0=r_shallow)
+    xs = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
+    R = np.hypot(*np.meshgrid(xs, xs))
+    c = float(np.abs(a[R <= 2 * math.exp(r_shallow)]).max())
+    err2 = float(np.sum((a - b) ** 2)) * (2.0 / n) ** 2
+    assert err2 <= 2 * math.pi * c * c * math.exp(2 * r_shallow)
