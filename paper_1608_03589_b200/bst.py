@@ -134,10 +134,11 @@ class BstPlan:
         sino = self._check_sino(sino)
         b = sino.shape[0]
         nray, m_pad, m_need = self.info["nray"], self.info["m_pad"], self.info["m_need"]
-        out = torch.empty((b, nray, m_pad), dtype=torch.complex64, device=self.device)
+        raw = torch.empty((b, nray // 2, m_pad, 2), dtype=torch.complex64, device=self.device)  # ray pairs
         with torch.cuda.device(self.device):
-            check(lib().lpbp_bst_radial(self._h, c_void_p(sino.data_ptr()), c_void_p(out.data_ptr()), b,
+            check(lib().lpbp_bst_radial(self._h, c_void_p(sino.data_ptr()), c_void_p(raw.data_ptr()), b,
                                         _stream(self.device)))
+        out = raw.permute(0, 3, 1, 2).reshape(b, nray, m_pad)  # rays c then c + ntheta
         return out[:, :, :m_need]
 
 

@@ -156,14 +156,15 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
     }
     GroupBarT<T>{1 + gi}();
     // separate the packed spectra: A = (Z[m] + conj Z[-m]) / 2, B = (Z[m] - conj Z[-m]) / 2i
-    float2* pa = P + ((size_t)b * 2 * ntheta + c0 + c) * m_pad;
-    float2* pb = P + ((size_t)b * 2 * ntheta + c0 + c + ntheta) * m_pad;
+    // ray pair (c, c + ntheta) interleaved: P4[c][m] = (ray c, ray c + ntheta), the gridding's
+    // (direct, Hermitian mirror) taps of one angle in one 16-byte load
+    float4* p4 = reinterpret_cast<float4*>(P) + ((size_t)b * ntheta + c0 + c) * m_pad;
     for (int m = ti; m < m_need && c < nc; m += T) {
       const float2 z = zbuf[pad16(m)];
       const float2 w = zbuf[pad16(m == 0 ? 0 : Lr - m)];
       const float k = __ldg(kern + m);
-      pa[m] = make_float2(0.5f * (z.x + w.x) * k, 0.5f * (z.y - w.y) * k);
-      pb[m] = make_float2(0.5f * (z.y + w.y) * k, 0.5f * (w.x - z.x) * k);
+      p4[m] = make_float4(0.5f * (z.x + w.x) * k, 0.5f * (z.y - w.y) * k, 0.5f * (z.y + w.y) * k,
+                          0.5f * (w.x - z.x) * k);
     }
     GroupBarT<T>{1 + gi}();
   }
@@ -191,7 +192,7 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int ky0 = blockIdx.x * TR;
   const int b = blockIdx.y;
-  const float2* Pb = P + (size_t)b * nray * m_pad;
+  const float2* Pb = P + (size_t)b * nray * m_pad;  // [nray/2][m_pad] float4 ray pairs
   const int half_ray = nray / 2;
   double mean_part = 0.0;
   for (int rr = 0; rr < TR / G; ++rr) {
@@ -225,12 +226,26 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
       // the mirror bin -k is the same radius at theta + pi: rays shifted by nray/2
       // (numpy pairs the origin bin with itself, not with theta + pi)
       const bool origin = kx == 0 && ky == 0;
-      const int m0 = origin ? j0 : (j0 + half_ray >= nray ? j0 + half_ray - nray : j0 + half_ray);
-      const int m1 = origin ? j1 : (j1 + half_ray >= nray ? j1 + half_ray - nray : j1 + half_ray);
       const float c00 = (1.f - wi) * (1.f - wj), c10 = wi * (1.f - wj), c01 = (1.f - wi) * wj, c11 = wi * wj;
-      auto tap = [&](int j, int i) { return __ldg(Pb + (size_t)j * m_pad + i); };
-      const float2 a00 = tap(j0, i0), a10 = tap(j0, i1), a01 = tap(j1, i0), a11 = tap(j1, i1);
-      const float2 b00 = tap(m0, i0), b10 = tap(m0, i1), b01 = tap(m1, i0), b11 = tap(m1, i1);
+      // pair loads: ray j and its mirror j +- nray/2 share one float4 (direct in .xy for j < nray/2)
+      const float4* P4 = reinterpret_cast<const float4*>(Pb);
+      auto pair = [&](int j, int i, float2& d, float2& m) {
+        const bool hi = j >= half_ray;
+        const float4 q = __ldg(P4 + (size_t)(hi ? j - half_ray : j) * m_pad + i);
+        d = hi ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
+        m = hi ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
+      };
+      float2 a00, a10, a01, a11, b00, b10, b01, b11;
+      pair(j0, i0, a00, b00);
+      pair(j0, i1, a10, b10);
+      pair(j1, i0, a01, b01);
+      pair(j1, i1, a11, b11);
+      if (origin) {  // numpy pairs the origin bin with itself, not with theta + pi
+        b00 = a00;
+        b10 = a10;
+        b01 = a01;
+        b11 = a11;
+      }
       // G(k) + conj(G(-k)); the 1/2 is folded into the radial kernel
       const float gx = (a00.x * c00 + a10.x * c10 + a01.x * c01 + a11.x * c11) +
                        (b00.x * c00 + b10.x * c10 + b01.x * c01 + b11.x * c11);
