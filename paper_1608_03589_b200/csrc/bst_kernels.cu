@@ -158,13 +158,18 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
     // separate the packed spectra: A = (Z[m] + conj Z[-m]) / 2, B = (Z[m] - conj Z[-m]) / 2i
     // ray pair (c, c + ntheta) interleaved: P4[c][m] = (ray c, ray c + ntheta), the gridding's
     // (direct, Hermitian mirror) taps of one angle in one 16-byte load
-    float4* p4 = reinterpret_cast<float4*>(P) + ((size_t)b * ntheta + c0 + c) * m_pad;
+    // Row ntheta repeats row 0 swapped (ray ntheta, ray 0) so the gridding's j0 + 1 never wraps.
+    float4* p4s = reinterpret_cast<float4*>(P) + (size_t)b * (ntheta + 1) * m_pad;
+    float4* p4 = p4s + (size_t)(c0 + c) * m_pad;
+    const bool wrap_row = c0 + c == 0;
     for (int m = ti; m < m_need && c < nc; m += T) {
       const float2 z = zbuf[pad16(m)];
       const float2 w = zbuf[pad16(m == 0 ? 0 : Lr - m)];
       const float k = __ldg(kern + m);
-      p4[m] = make_float4(0.5f * (z.x + w.x) * k, 0.5f * (z.y - w.y) * k, 0.5f * (z.y + w.y) * k,
-                          0.5f * (w.x - z.x) * k);
+      const float4 v = make_float4(0.5f * (z.x + w.x) * k, 0.5f * (z.y - w.y) * k, 0.5f * (z.y + w.y) * k,
+                                   0.5f * (w.x - z.x) * k);
+      p4[m] = v;
+      if (wrap_row) p4s[(size_t)ntheta * m_pad + m] = make_float4(v.z, v.w, v.x, v.y);
     }
     GroupBarT<T>{1 + gi}();
   }
@@ -192,7 +197,8 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int ky0 = blockIdx.x * TR;
   const int b = blockIdx.y;
-  const float2* Pb = P + (size_t)b * nray * m_pad;  // [nray/2][m_pad] float4 ray pairs
+  // [nray/2 + 1][m_pad] float4 ray pairs (ray p, ray p + nray/2); row nray/2 = (ray nray/2, ray 0)
+  const float4* P4 = reinterpret_cast<const float4*>(P) + (size_t)b * (nray / 2 + 1) * m_pad;
   const int half_ray = nray / 2;
   double mean_part = 0.0;
   for (int rr = 0; rr < TR / G; ++rr) {
@@ -203,62 +209,43 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
     const uint2* gqr = gq + (size_t)ky * qpitch;
     auto load = [&](int kx) -> float2 {
       if (kx == HB || ky == HB) return make_float2(0.f, 0.f);  // Nyquist row / column (bst.py:157-160)
-      // fp64-built coordinates of (|kfx|, ky); kfx < 0 reflects theta -> pi - theta
+      // fp64-built coordinates of (|kfx|, ky); kfx < 0 reflects theta -> pi - theta.  The gridded
+      // rows ky >= 0 keep theta in [0, pi], so j0 lies in [0, nray/2] (nray/2 only at theta = pi,
+      // where wj = 0) and the pair rows j0, j0 + 1 hold the direct taps in .xy, the Hermitian
+      // mirror taps (theta + pi) in .zw.
       const bool neg = kx > HB;
       const uint2 e = __ldg(gqr + (neg ? big - kx : kx));
       const int i0 = (int)(e.x & 0x1FFFu);
-      const int i1 = min(i0 + 1, nsig - 1);
+      const int di = i0 + 1 < nsig ? 1 : 0;
       const float wi = (float)(e.x >> 13) * (1.f / 524288.f);
       int j0 = (int)(e.y & 0x1FFFu);
       uint32_t qj = e.y >> 13;
       if (neg) {  // fj' = nray/2 - fj
-        if (qj == 0) {
-          j0 = nray / 2 - j0;
-        } else {
-          j0 = nray / 2 - j0 - 1;
-          qj = 524288u - qj;
-        }
-        if (j0 < 0) j0 += nray;
+        j0 = half_ray - j0 - (qj != 0u);
+        qj = qj ? 524288u - qj : 0u;
       }
-      if (j0 >= nray) j0 -= nray;
       const float wj = (float)qj * (1.f / 524288.f);
-      const int j1 = j0 + 1 == nray ? 0 : j0 + 1;
-      // the mirror bin -k is the same radius at theta + pi: rays shifted by nray/2
-      // (numpy pairs the origin bin with itself, not with theta + pi)
-      const bool origin = kx == 0 && ky == 0;
-      const float c00 = (1.f - wi) * (1.f - wj), c10 = wi * (1.f - wj), c01 = (1.f - wi) * wj, c11 = wi * wj;
-      // pair loads: ray j and its mirror j +- nray/2 share one float4 (direct in .xy for j < nray/2)
-      const float4* P4 = reinterpret_cast<const float4*>(Pb);
-      auto pair = [&](int j, int i, float2& d, float2& m) {
-        const bool hi = j >= half_ray;
-        const float4 q = __ldg(P4 + (size_t)(hi ? j - half_ray : j) * m_pad + i);
-        d = hi ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
-        m = hi ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
-      };
-      float2 a00, a10, a01, a11, b00, b10, b01, b11;
-      pair(j0, i0, a00, b00);
-      pair(j0, i1, a10, b10);
-      pair(j1, i0, a01, b01);
-      pair(j1, i1, a11, b11);
-      if (origin) {  // numpy pairs the origin bin with itself, not with theta + pi
-        b00 = a00;
-        b10 = a10;
-        b01 = a01;
-        b11 = a11;
+      const float4* q0 = P4 + (size_t)j0 * m_pad + i0;
+      const float4* q1 = j0 < half_ray ? q0 + m_pad : q0;  // theta = pi: wj = 0
+      const float4 a00 = __ldg(q0), a10 = __ldg(q0 + di), a01 = __ldg(q1), a11 = __ldg(q1 + di);
+      // G(k) + conj(G(-k)) per tap; the 1/2 is folded into the radial kernel
+      const float s00x = a00.x + a00.z, s00y = a00.y - a00.w, s10x = a10.x + a10.z, s10y = a10.y - a10.w;
+      const float s01x = a01.x + a01.z, s01y = a01.y - a01.w, s11x = a11.x + a11.z, s11y = a11.y - a11.w;
+      const float u0x = fmaf(wi, s10x - s00x, s00x), u0y = fmaf(wi, s10y - s00y, s00y);
+      const float u1x = fmaf(wi, s11x - s01x, s01x), u1y = fmaf(wi, s11y - s01y, s01y);
+      float gx = fmaf(wj, u1x - u0x, u0x), gy = fmaf(wj, u1y - u0y, u0y);
+      if (kx == 0 && ky == 0) {  // numpy pairs the origin bin with itself, not with theta + pi
+        gx = 2.f * a00.x;
+        gy = 0.f;
       }
-      // G(k) + conj(G(-k)); the 1/2 is folded into the radial kernel
-      const float gx = (a00.x * c00 + a10.x * c10 + a01.x * c01 + a11.x * c11) +
-                       (b00.x * c00 + b10.x * c10 + b01.x * c01 + b11.x * c11);
-      const float gy = (a00.y * c00 + a10.y * c10 + a01.y * c01 + a11.y * c11) -
-                       (b00.y * c00 + b10.y * c10 + b01.y * c01 + b11.y * c11);
-      const float2 tx = __ldg(tau + kx);
-      const float2 t2 = make_float2(tx.x * ty.x - tx.y * ty.y, tx.x * ty.y + tx.y * ty.x);
-      return make_float2(gx * t2.x - gy * t2.y, gx * t2.y + gy * t2.x);
+      const float2 tx = __ldg(tau + kx);  // the row's tau[ky] is applied at the store
+      return make_float2(gx * tx.x - gy * tx.y, gx * tx.y + gy * tx.x);
     };
     float2 rowsum = make_float2(0.f, 0.f);
     auto store = [&](int x, float2 v) {
       const int xc = x - p0;
       if (xc >= 0 && xc < n) {
+        v = make_float2(v.x * ty.x - v.y * ty.y, v.x * ty.y + v.y * ty.x);
         stg[(size_t)xc * TR + r] = v;
         rowsum.x += v.x;
         rowsum.y += v.y;
