@@ -104,37 +104,50 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
   const int nc = min(TC, ntheta - c0);  // ragged last tile
   const int b = blockIdx.y;
   const float* src = g + (size_t)b * nt * ntheta + c0;
+  // <g, chord> dt dtheta / 4 (bst.py:173-180) accumulated while the tile streams in: fp32
+  // per-thread partials (<= nt TC / blockDim terms), fp64 across the CTA and the batch
+  const float dt = 2.f / nt;
+  auto chord_w = [&](const float4& cp, float a) {
+    return a <= cp.x ? cp.z : (a < cp.y ? cp.z * (cp.y - a) * cp.w : 0.f);
+  };
+  float part = 0.f;
   if (nc == TC && (ntheta & 3) == 0) {
+    static_assert((G * T) % V == 0, "a thread's column quad is fixed");
+    const int cq = (threadIdx.x % V) * 4;
+    float4 cp[4];
+    if (chord) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cp[k] = __ldg(chord + c0 + cq + k);
+    }
     for (int e = threadIdx.x; e < nt * V; e += blockDim.x) {
-      const int t = e / V, c = (e % V) * 4;
-      const float4 v = __ldg(reinterpret_cast<const float4*>(src + (size_t)t * ntheta + c));
-      float* r = tile + t * TP + c;
+      const int t = e / V;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + (size_t)t * ntheta + cq));
+      float* r = tile + t * TP + cq;
       r[0] = v.x;
       r[1] = v.y;
       r[2] = v.z;
       r[3] = v.w;
+      if (chord) {
+        const float a = fabsf(-1.f + t * dt);
+        part = fmaf(v.x, chord_w(cp[0], a), part);
+        part = fmaf(v.y, chord_w(cp[1], a), part);
+        part = fmaf(v.z, chord_w(cp[2], a), part);
+        part = fmaf(v.w, chord_w(cp[3], a), part);
+      }
     }
   } else {
     for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
       const int t = e / TC, c = e % TC;
-      tile[t * TP + c] = c < nc ? __ldg(src + (size_t)t * ntheta + c) : 0.f;
+      const float v = c < nc ? __ldg(src + (size_t)t * ntheta + c) : 0.f;
+      tile[t * TP + c] = v;
+      if (chord && c < nc) part = fmaf(v, chord_w(__ldg(chord + c0 + c), fabsf(-1.f + t * dt)), part);
     }
   }
-  __syncthreads();
-  if (chord) {  // <g, chord> dt dtheta / 4 over this tile (bst.py:173-180), fp64 accumulation
-    double part = 0.0;
-    const float dt = 2.f / nt;
-    for (int e = threadIdx.x; e < nt * TC; e += blockDim.x) {
-      const int t = e / TC, c = e % TC;
-      if (c < nc) {
-        const float4 cp = __ldg(chord + c0 + c);
-        const float a = fabsf(-1.f + t * dt);
-        const float ch = a <= cp.x ? cp.z : (a < cp.y ? cp.z * (cp.y - a) * cp.w : 0.f);
-        part += (double)tile[t * TP + c] * (double)ch;
-      }
-    }
-    const double s = block_sum(part, red);
+  if (chord) {
+    const double s = block_sum((double)part, red);  // its barriers also publish the tile
     if (threadIdx.x == 0) atomicAdd(acc + 2 * b, s);
+  } else {
+    __syncthreads();
   }
   for (int round = 0; round < TC / G; ++round) {
     const int c = round * G + gi;
