@@ -206,8 +206,9 @@ int lpbp_bst_execute(lpbp_bst_plan* plan, const float* sino_dev, float* img_dev,
 int lpbp_bst_execute_host(lpbp_bst_plan* plan, const float* sino_host, float* img_host, int32_t batch,
                           int32_t chunk);
 /* Stage: the weighted radial spectra of an unfiltered batch, laid out as ray pairs
- * P[batch][ntheta + 1][m_pad][2] complex64 (pair c = rays c and c + ntheta, the two half-lines
- * of angle c; pair ntheta repeats pair 0 swapped: rays ntheta and 0); bins m < m_need hold 0.5 x the reference's spectra * sigma_kernel, the 1/2 being
+ * P[batch][ntheta + 2][m_pad][2] complex64 (pair c = rays c and c + ntheta, the two half-lines
+ * of angle c; pair ntheta repeats pair 0 swapped: rays ntheta and 0; pair ntheta + 1 and the
+ * bins m >= m_need are zero); bins m < m_need hold 0.5 x the reference's spectra * sigma_kernel, the 1/2 being
  * the Hermitian averaging of the gridding; the DC bin is zero in subtract_mean mode. */
 int lpbp_bst_radial(const lpbp_bst_plan* plan, const float* sino_dev, float* spectra_dev, int32_t batch,
                     void* stream);

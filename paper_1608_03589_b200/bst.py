@@ -134,9 +134,9 @@ class BstPlan:
         sino = self._check_sino(sino)
         b = sino.shape[0]
         nray, m_pad, m_need = self.info["nray"], self.info["m_pad"], self.info["m_need"]
-        # ray pairs [b][ntheta + 1][m_pad][2]: pair c = (ray c, ray c + ntheta); the last pair
-        # row repeats pair 0 swapped for the gridding's wrap-free access
-        raw = torch.empty((b, nray // 2 + 1, m_pad, 2), dtype=torch.complex64, device=self.device)
+        # ray pairs [b][ntheta + 2][m_pad][2]: pair c = (ray c, ray c + ntheta); pair row ntheta
+        # repeats pair 0 swapped and row ntheta + 1 is zero (the gridding's unguarded taps)
+        raw = torch.empty((b, nray // 2 + 2, m_pad, 2), dtype=torch.complex64, device=self.device)
         with torch.cuda.device(self.device):
             check(lib().lpbp_bst_radial(self._h, c_void_p(sino.data_ptr()), c_void_p(raw.data_ptr()), b,
                                         _stream(self.device)))

@@ -71,7 +71,7 @@ std::string build_bst_host(const BstParams& p, BstHost& h) {
                   p.n, nt, (int)(std::sqrt(2.0) * (ns - 1)));
     return buf;
   }
-  h.m_pad = (h.m_need + 3) / 4 * 4;
+  h.m_pad = (h.m_need + 4) / 4 * 4;  // >= m_need + 1: the gridding reads bin i0 + 1 unguarded
   h.big = kDomainPad * p.n;
   h.dw = kPi / kDomainPad;
   h.p0 = ((kDomainPad - 1) * p.n) / 2;

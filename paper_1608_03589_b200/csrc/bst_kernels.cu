@@ -171,18 +171,25 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
     // separate the packed spectra: A = (Z[m] + conj Z[-m]) / 2, B = (Z[m] - conj Z[-m]) / 2i
     // ray pair (c, c + ntheta) interleaved: P4[c][m] = (ray c, ray c + ntheta), the gridding's
     // (direct, Hermitian mirror) taps of one angle in one 16-byte load
-    // Row ntheta repeats row 0 swapped (ray ntheta, ray 0) so the gridding's j0 + 1 never wraps.
-    float4* p4s = reinterpret_cast<float4*>(P) + (size_t)b * (ntheta + 1) * m_pad;
+    // Row ntheta repeats row 0 swapped (ray ntheta, ray 0) so the gridding's j0 + 1 never wraps;
+    // row ntheta + 1 and the bins [m_need, m_pad) are zero (read with zero weight, unguarded).
+    float4* p4s = reinterpret_cast<float4*>(P) + (size_t)b * (ntheta + 2) * m_pad;
     float4* p4 = p4s + (size_t)(c0 + c) * m_pad;
     const bool wrap_row = c0 + c == 0;
-    for (int m = ti; m < m_need && c < nc; m += T) {
-      const float2 z = zbuf[pad16(m)];
-      const float2 w = zbuf[pad16(m == 0 ? 0 : Lr - m)];
-      const float k = __ldg(kern + m);
-      const float4 v = make_float4(0.5f * (z.x + w.x) * k, 0.5f * (z.y - w.y) * k, 0.5f * (z.y + w.y) * k,
-                                   0.5f * (w.x - z.x) * k);
+    for (int m = ti; m < m_pad && c < nc; m += T) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m < m_need) {
+        const float2 z = zbuf[pad16(m)];
+        const float2 w = zbuf[pad16(m == 0 ? 0 : Lr - m)];
+        const float k = __ldg(kern + m);
+        v = make_float4(0.5f * (z.x + w.x) * k, 0.5f * (z.y - w.y) * k, 0.5f * (z.y + w.y) * k,
+                        0.5f * (w.x - z.x) * k);
+      }
       p4[m] = v;
-      if (wrap_row) p4s[(size_t)ntheta * m_pad + m] = make_float4(v.z, v.w, v.x, v.y);
+      if (wrap_row) {
+        p4s[(size_t)ntheta * m_pad + m] = make_float4(v.z, v.w, v.x, v.y);
+        p4s[(size_t)(ntheta + 1) * m_pad + m] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
     GroupBarT<T>{1 + gi}();
   }
@@ -210,8 +217,9 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int ky0 = blockIdx.x * TR;
   const int b = blockIdx.y;
-  // [nray/2 + 1][m_pad] float4 ray pairs (ray p, ray p + nray/2); row nray/2 = (ray nray/2, ray 0)
-  const float4* P4 = reinterpret_cast<const float4*>(P) + (size_t)b * (nray / 2 + 1) * m_pad;
+  // [nray/2 + 2][m_pad] float4 ray pairs (ray p, ray p + nray/2); row nray/2 = (ray nray/2, ray 0),
+  // row nray/2 + 1 and bins >= nsig zero
+  const float4* P4 = reinterpret_cast<const float4*>(P) + (size_t)b * (nray / 2 + 2) * m_pad;
   const int half_ray = nray / 2;
   double mean_part = 0.0;
   for (int rr = 0; rr < TR / G; ++rr) {
@@ -228,8 +236,7 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
       // mirror taps (theta + pi) in .zw.
       const bool neg = kx > HB;
       const uint2 e = __ldg(gqr + (neg ? big - kx : kx));
-      const int i0 = (int)(e.x & 0x1FFFu);
-      const int di = i0 + 1 < nsig ? 1 : 0;
+      const int i0 = (int)(e.x & 0x1FFFu);  // i0 = nsig - 1 only with wi = 0; bin nsig is zero
       const float wi = (float)(e.x >> 13) * (1.f / 524288.f);
       int j0 = (int)(e.y & 0x1FFFu);
       uint32_t qj = e.y >> 13;
@@ -238,9 +245,9 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
         qj = qj ? 524288u - qj : 0u;
       }
       const float wj = (float)qj * (1.f / 524288.f);
-      const float4* q0 = P4 + (size_t)j0 * m_pad + i0;
-      const float4* q1 = j0 < half_ray ? q0 + m_pad : q0;  // theta = pi: wj = 0
-      const float4 a00 = __ldg(q0), a10 = __ldg(q0 + di), a01 = __ldg(q1), a11 = __ldg(q1 + di);
+      const float4* q0 = P4 + (j0 * m_pad + i0);
+      const float4* q1 = q0 + m_pad;  // theta = pi (j0 = nray/2): the zero row, wj = 0
+      const float4 a00 = __ldg(q0), a10 = __ldg(q0 + 1), a01 = __ldg(q1), a11 = __ldg(q1 + 1);
       // G(k) + conj(G(-k)) per tap; the 1/2 is folded into the radial kernel
       const float s00x = a00.x + a00.z, s00y = a00.y - a00.w, s10x = a10.x + a10.z, s10y = a10.y - a10.w;
       const float s01x = a01.x + a01.z, s01y = a01.y - a01.w, s11x = a11.x + a11.z, s11y = a11.y - a11.w;

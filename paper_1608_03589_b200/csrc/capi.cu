@@ -1046,10 +1046,10 @@ struct lpbp_bst_plan {
 
 namespace {
 
-// per slice: filtered sinogram (fbp) | P [nray/2 + 1][m_pad] ray pairs | X [n][big/2] complex; + 2 doubles per slice
+// per slice: filtered sinogram (fbp) | P [nray/2 + 2][m_pad] ray pairs | X [n][big/2] complex; + 2 doubles per slice
 size_t bst_slice_bytes(const lpbp::BstHost& h, size_t* off_p, size_t* off_x) {
   const size_t f = h.p.filter ? align256((size_t)h.p.nt * h.p.ntheta * sizeof(float)) : 0;
-  const size_t pb = align256((size_t)(h.nray + 2) * h.m_pad * sizeof(float2));
+  const size_t pb = align256((size_t)(h.nray + 4) * h.m_pad * sizeof(float2));
   const size_t xb = align256((size_t)h.p.n * (h.big / 2) * sizeof(float2));
   if (off_p) *off_p = f;
   if (off_x) *off_x = f + pb;
@@ -1067,7 +1067,7 @@ int bst_chunk(const lpbp_bst_plan* P, const float* in, float* out, int c, char* 
   (void)per;
   // regions laid out per chunk: [filtered c slices][P c slices][X c slices][acc]
   const size_t fb = h.p.filter ? align256((size_t)h.p.nt * h.p.ntheta * sizeof(float)) : 0;
-  const size_t pb = align256((size_t)(h.nray + 2) * h.m_pad * sizeof(float2));
+  const size_t pb = align256((size_t)(h.nray + 4) * h.m_pad * sizeof(float2));
   const size_t xb = align256((size_t)h.p.n * (h.big / 2) * sizeof(float2));
   float* filt = reinterpret_cast<float*>(ws);
   float2* Pw = spectra_only ? spectra_only : reinterpret_cast<float2*>(ws + fb * c);
@@ -1320,7 +1320,7 @@ int lpbp_bst_radial(const lpbp_bst_plan* P, const float* sino_dev, float* spectr
   if (batch == 0) return LPBP_OK;
   if (!sino_dev || !spectra_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
-  // spectra_dev holds [batch][ntheta + 1][m_pad] ray pairs; the accumulators go to a small scratch
+  // spectra_dev holds [batch][ntheta + 2][m_pad] ray pairs; the accumulators go to a small scratch
   void* acc = nullptr;
   cudaError_t e = cudaMallocAsync(&acc, (size_t)batch * 2 * sizeof(double) + 256, static_cast<cudaStream_t>(stream));
   if (e) return cuda_fail(e, "bst radial scratch");
