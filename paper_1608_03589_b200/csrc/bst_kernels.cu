@@ -228,38 +228,46 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
     if (ky >= HB) break;  // uniform within the group
     const float2 ty = __ldg(tau + ky);
     const uint2* gqr = gq + (size_t)ky * qpitch;
-    auto load = [&](int kx) -> float2 {
-      if (kx == HB || ky == HB) return make_float2(0.f, 0.f);  // Nyquist row / column (bst.py:157-160)
-      // fp64-built coordinates of (|kfx|, ky); kfx < 0 reflects theta -> pi - theta.  The gridded
-      // rows ky >= 0 keep theta in [0, pi], so j0 lies in [0, nray/2] (nray/2 only at theta = pi,
-      // where wj = 0) and the pair rows j0, j0 + 1 hold the direct taps in .xy, the Hermitian
-      // mirror taps (theta + pi) in .zw.
-      const bool neg = kx > HB;
-      const uint2 e = __ldg(gqr + (neg ? big - kx : kx));
+    // fp64-built coordinates of (|kfx|, ky); kfx < 0 reflects theta -> pi - theta.  The gridded
+    // rows ky >= 0 keep theta in [0, pi], so j0 lies in [0, nray/2] (nray/2 only at theta = pi,
+    // where wj = 0) and the pair rows j0, j0 + 1 hold the direct taps in .xy, the Hermitian
+    // mirror taps (theta + pi) in .zw.
+    auto gq_at = [&](int kx) -> uint2 { return __ldg(gqr + (kx > HB ? big - kx : kx)); };
+    struct Tap {
+      const float4* q0;
+      float wi, wj;
+    };
+    auto decode = [&](int kx, uint2 e) -> Tap {
       const int i0 = (int)(e.x & 0x1FFFu);  // i0 = nsig - 1 only with wi = 0; bin nsig is zero
-      const float wi = (float)(e.x >> 13) * (1.f / 524288.f);
       int j0 = (int)(e.y & 0x1FFFu);
       uint32_t qj = e.y >> 13;
-      if (neg) {  // fj' = nray/2 - fj
+      if (kx > HB) {  // fj' = nray/2 - fj
         j0 = half_ray - j0 - (qj != 0u);
         qj = qj ? 524288u - qj : 0u;
       }
-      const float wj = (float)qj * (1.f / 524288.f);
-      const float4* q0 = P4 + (j0 * m_pad + i0);
-      const float4* q1 = q0 + m_pad;  // theta = pi (j0 = nray/2): the zero row, wj = 0
-      const float4 a00 = __ldg(q0), a10 = __ldg(q0 + 1), a01 = __ldg(q1), a11 = __ldg(q1 + 1);
+      return Tap{P4 + (j0 * m_pad + i0), (float)(e.x >> 13) * (1.f / 524288.f), (float)qj * (1.f / 524288.f)};
+    };
+    // taps a00, a10 at q0, a01, a11 at q0 + m_pad (theta = pi, j0 = nray/2: the zero row, wj = 0)
+    auto finish = [&](int kx, const Tap& t, const float4& a00, const float4& a10, const float4& a01,
+                      const float4& a11) -> float2 {
+      if (kx == HB || ky == HB) return make_float2(0.f, 0.f);  // Nyquist row / column (bst.py:157-160)
       // G(k) + conj(G(-k)) per tap; the 1/2 is folded into the radial kernel
       const float s00x = a00.x + a00.z, s00y = a00.y - a00.w, s10x = a10.x + a10.z, s10y = a10.y - a10.w;
       const float s01x = a01.x + a01.z, s01y = a01.y - a01.w, s11x = a11.x + a11.z, s11y = a11.y - a11.w;
-      const float u0x = fmaf(wi, s10x - s00x, s00x), u0y = fmaf(wi, s10y - s00y, s00y);
-      const float u1x = fmaf(wi, s11x - s01x, s01x), u1y = fmaf(wi, s11y - s01y, s01y);
-      float gx = fmaf(wj, u1x - u0x, u0x), gy = fmaf(wj, u1y - u0y, u0y);
+      const float u0x = fmaf(t.wi, s10x - s00x, s00x), u0y = fmaf(t.wi, s10y - s00y, s00y);
+      const float u1x = fmaf(t.wi, s11x - s01x, s01x), u1y = fmaf(t.wi, s11y - s01y, s01y);
+      float gx = fmaf(t.wj, u1x - u0x, u0x), gy = fmaf(t.wj, u1y - u0y, u0y);
       if (kx == 0 && ky == 0) {  // numpy pairs the origin bin with itself, not with theta + pi
         gx = 2.f * a00.x;
         gy = 0.f;
       }
       const float2 tx = __ldg(tau + kx);  // the row's tau[ky] is applied at the store
       return make_float2(gx * tx.x - gy * tx.y, gx * tx.y + gy * tx.x);
+    };
+    auto load = [&](int kx) -> float2 {
+      const Tap t = decode(kx, gq_at(kx));
+      const float4* q1 = t.q0 + m_pad;
+      return finish(kx, t, __ldg(t.q0), __ldg(t.q0 + 1), __ldg(q1), __ldg(q1 + 1));
     };
     float2 rowsum = make_float2(0.f, 0.f);
     auto store = [&](int x, float2 v) {
@@ -271,7 +279,49 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
         rowsum.y += v.y;
       }
     };
-    dft<BIG, true, GEN, false, false>(buf, ti, tw, ch, load, store, GroupBarT<T>{1 + gi});
+    if constexpr (!GEN) {
+      // Gather phase ahead of the FFT, free of its live data: this thread's points kx = ti + m T
+      // (exactly the indices its first FFT pass reads) in batches of 4 (16 float4 taps in
+      // flight, the next batch's table entries prefetched), written to buf[kx]; the FFT then
+      // reads them back (same thread) and its first-pass barrier orders the in-place stores.
+      constexpr int E = BIG / T, B4 = 4;
+      static_assert(E % B4 == 0, "batches of 4 points");
+      uint2 gcur[B4];
+#pragma unroll
+      for (int q = 0; q < B4; ++q) gcur[q] = gq_at(ti + q * T);
+#pragma unroll
+      for (int m0 = 0; m0 < E; m0 += B4) {
+        uint2 gnext[B4];
+        if (m0 + B4 < E) {
+#pragma unroll
+          for (int q = 0; q < B4; ++q) gnext[q] = gq_at(ti + (m0 + B4 + q) * T);
+        }
+        Tap tp[B4];
+        float4 a[B4][4];
+#pragma unroll
+        for (int q = 0; q < B4; ++q) {
+          tp[q] = decode(ti + (m0 + q) * T, gcur[q]);
+          const float4* q1 = tp[q].q0 + m_pad;
+          a[q][0] = __ldg(tp[q].q0);
+          a[q][1] = __ldg(tp[q].q0 + 1);
+          a[q][2] = __ldg(q1);
+          a[q][3] = __ldg(q1 + 1);
+        }
+#pragma unroll
+        for (int q = 0; q < B4; ++q) {
+          const int kx = ti + (m0 + q) * T;
+          buf[kx] = finish(kx, tp[q], a[q][0], a[q][1], a[q][2], a[q][3]);
+        }
+        if (m0 + B4 < E) {
+#pragma unroll
+          for (int q = 0; q < B4; ++q) gcur[q] = gnext[q];
+        }
+      }
+      auto ld = [&](int kx) -> float2 { return buf[kx]; };
+      block_fft<BIG, true, false, true, false, 16>(buf, ti, tw, ld, store, GroupBarT<T>{1 + gi});
+    } else {
+      dft<BIG, true, GEN, false, false>(buf, ti, tw, ch, load, store, GroupBarT<T>{1 + gi});
+    }
     GroupBarT<T>{1 + gi}();  // the next row's first pass overwrites buf
     // crop mean: Re(sum_x X[ky][x] * cmean[ky]), rows 1..BIG/2-1 stand for their conjugate partners too
     const float2 cm = __ldg(cmean + ky);
