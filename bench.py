@@ -222,6 +222,11 @@ def cpu_model() -> str:
 
 
 # ----------------------------------------------------------------------------
+def workload_name(config: int, c: dict) -> str:
+    """The workload string both arms report (the driver pairs the lines on it)."""
+    return f"config{config}: {'FBP' if c['fbp'] else 'BP'} {c['nt']} bins x {c['ntheta']} angles -> {c['n']}^2"
+
+
 def run_reference(a, d: Dist):
     """--impl reference: the reference algorithm on the host cores, rank 0 only."""
     if d.rank != 0:
@@ -242,8 +247,7 @@ def run_reference(a, d: Dist):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded random-ellipse sinograms + 1% Gaussian noise)",
-        "config": {"workload": f"config{a.config}: {'FBP' if c['fbp'] else 'BP'} {c['nt']}x{c['ntheta']} -> {c['n']}^2",
-                   "slices_per_step": workers},
+        "config": {"workload": workload_name(a.config, c), "slices_per_step": workers},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": f"{workers} slices per step, one per concurrent worker process, reconstruction "
                                    f"only (inputs generated untimed), oracle/fastbp_oracle.py (numpy/scipy "
@@ -394,7 +398,7 @@ def run_ours(a, d: Dist):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (device-generated seeded random-ellipse sinograms, K=50, 1% Gaussian noise)",
-            "config": {"workload": f"config{a.config}: {'FBP' if c['fbp'] else 'BP'} {nt} bins x {nth} angles -> {n}^2 fp32",
+            "config": {"workload": workload_name(a.config, c),
                        "slices_per_rank": S, "chunk": chunk, "streams": nstreams,
                        "parallelism": f"slice-shard x{d.world}",
                        "l2": "no flush: 34 GB input per step >> 126 MB L2",
