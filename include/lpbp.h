@@ -114,11 +114,17 @@ int lpbp_profile_enable(lpbp_plan* plan, int32_t enable);
 int lpbp_profile_read(lpbp_plan* plan, double* stage_ms, int64_t* stage_launches, int64_t* stage_slices,
                       int32_t nstages);
 
-/* Analytic ellipse-phantom sinograms (harness input generator; restates
- * fastbp.radon.radon_ellipses, radon.py:38-61, in fp64 on the device).
- * params_dev: [batch][k][6] doubles (cx, cy, a, b, tilt, rho); out: [batch][nt][ntheta] fp32. */
+/* Analytic ellipse-phantom sinograms: fastbp.radon.radon_ellipses (radon.py:38-61), the
+ * step before the path, in fp64 on the device with the reference's accumulation order.
+ * params_dev: [batch][k][6] doubles (cx, cy, a, b, tilt, rho), any k >= 1;
+ * out: [batch][nt][ntheta], fp32 (lpbp_radon_ellipses) or fp64 (lpbp_radon_ellipses_f64). */
 int lpbp_radon_ellipses(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch,
                         float* out_dev, void* stream);
+int lpbp_radon_ellipses_f64(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch,
+                            double* out_dev, void* stream);
+/* Same from host buffers (fp64 params in, fp64 sinograms out; synchronous on `device`). */
+int lpbp_radon_ellipses_host(const double* params, int32_t k, int32_t nt, int32_t ntheta, int32_t batch, double* out,
+                             int32_t device);
 
 /* ---- sector (partial) backprojection: partial_backproject(g, sectors, n_out), logpolar.py:210-299 ----
  * Each sector (theta0, beta, a_r) covers ray angles [theta0, theta0 + 2 beta] mod pi.  Its

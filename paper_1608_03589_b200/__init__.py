@@ -7,7 +7,8 @@ Same names and signatures as the reference for the path:
   adaptive_rho0, compute_nrho, relative_l2, partial_backproject,
   BstOptions, bst_backproject (fbp's default engine "bst"),
   PolarSinogram, sinogram_to_semipolar, semipolar_to_logpolar, logpolar_to_cartesian,
-  make_logpolar_kernel, truncation_error_bound
+  make_logpolar_kernel, truncation_error_bound,
+  Ellipse, EllipseSet, radon_ellipses (the input generator, on the device)
 plus batched device entry points (torch CUDA tensors) and LogPolarPlan.
 All compute runs in liblpbp.so; there is no CPU fallback.
 """
@@ -28,6 +29,7 @@ from .plan import LogPolarPlan, get_plan, naive_backproject
 from .roofline import algorithmic_bytes
 from . import roofline
 from . import synth
+from .synth import Ellipse, EllipseSet, radon_ellipses
 from .multi import VolumeReconstructor, shard_bounds
 from .sector import SectorPlan, partial_backproject, partial_backproject_batch
 from .bst import (

@@ -94,6 +94,8 @@ SIGNATURES = {
     "lpbp_profile_enable": (c_int32, [c_void_p, c_int32]),
     "lpbp_profile_read": (c_int32, [c_void_p, POINTER(ctypes.c_double), POINTER(c_int64), POINTER(c_int64), c_int32]),
     "lpbp_radon_ellipses": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
+    "lpbp_radon_ellipses_f64": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
+    "lpbp_radon_ellipses_host": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_int32]),
     "lpbp_sector_plan_create": (c_int32, [c_int32, c_int32, c_int32, POINTER(Sector), c_int32, c_int32,
                                           POINTER(c_void_p)]),
     "lpbp_sector_plan_destroy": (None, [c_void_p]),

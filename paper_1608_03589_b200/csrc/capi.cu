@@ -650,14 +650,50 @@ int lpbp_profile_read(lpbp_plan* P, double* stage_ms, int64_t* stage_launches, i
   return rc;
 }
 
-int lpbp_radon_ellipses(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch,
-                        float* out_dev, void* stream) {
-  if (!params_dev || !out_dev || k < 1 || k > 256 || nt < 2 || ntheta < 1 || batch < 0)
+extern "C++" {
+namespace {
+template <typename OutT>
+int radon_ellipses_abi(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch, OutT* out_dev,
+                       void* stream) {
+  if (!params_dev || !out_dev || k < 1 || nt < 2 || ntheta < 1 || batch < 0 || batch > 65535)
     return fail(LPBP_EINVAL, "invalid argument");
   if (batch == 0) return LPBP_OK;
   cudaError_t e = lpbp::launch_radon_ellipses(params_dev, k, nt, ntheta, batch, out_dev,
                                               static_cast<cudaStream_t>(stream));
   if (e) return cuda_fail(e, "radon_ellipses");
+  return LPBP_OK;
+}
+}  // namespace
+}  // extern "C++"
+
+int lpbp_radon_ellipses(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch,
+                        float* out_dev, void* stream) {
+  return radon_ellipses_abi(params_dev, k, nt, ntheta, batch, out_dev, stream);
+}
+
+int lpbp_radon_ellipses_f64(const double* params_dev, int32_t k, int32_t nt, int32_t ntheta, int32_t batch,
+                            double* out_dev, void* stream) {
+  return radon_ellipses_abi(params_dev, k, nt, ntheta, batch, out_dev, stream);
+}
+
+int lpbp_radon_ellipses_host(const double* params, int32_t k, int32_t nt, int32_t ntheta, int32_t batch, double* out,
+                             int32_t device) {
+  if (!params || !out || k < 1 || nt < 2 || ntheta < 1 || batch < 0 || batch > 65535 || device < 0)
+    return fail(LPBP_EINVAL, "invalid argument");
+  if (batch == 0) return LPBP_OK;
+  DeviceGuard g(device);
+  if (!g.ok) return fail(LPBP_ECUDA, "cannot select the device");
+  const size_t pb = (size_t)batch * k * 6 * sizeof(double), ob = (size_t)batch * nt * ntheta * sizeof(double);
+  void *dp = nullptr, *dout = nullptr;
+  cudaError_t e = cudaMalloc(&dp, pb);
+  if (!e) e = cudaMalloc(&dout, ob);
+  if (!e) e = cudaMemcpy(dp, params, pb, cudaMemcpyHostToDevice);
+  if (!e) e = lpbp::launch_radon_ellipses(static_cast<const double*>(dp), k, nt, ntheta, batch,
+                                          static_cast<double*>(dout), nullptr);
+  if (!e) e = cudaMemcpy(out, dout, ob, cudaMemcpyDeviceToHost);
+  if (dp) cudaFree(dp);
+  if (dout) cudaFree(dout);
+  if (e) return cuda_fail(e, "radon_ellipses_host");
   return LPBP_OK;
 }
 

@@ -762,59 +762,78 @@ k_row_irdft_generic(const float2* __restrict__ Yh, float* __restrict__ lp, int n
 }
 
 // ---------------------------------------------------------------------------
-// Harness input generator: exact ellipse line integrals (radon.py:38-61) in fp64,
+// Input generator: exact ellipse line integrals (radon.py:38-61) in fp64,
 // 2 rho A B sqrt(w^2 - tau^2) / w^2, tau = t - c.xi_theta,
-// w^2 = A^2 cos^2(theta - gamma) + B^2 sin^2(theta - gamma).
-// Block: 32 angles x 64 rows; per-(ellipse, angle) terms staged in smem.
+// w^2 = A^2 cos^2(theta - gamma) + B^2 sin^2(theta - gamma), summed over the
+// ellipses in order (the reference's accumulation order).  Block: 32 angles x 64
+// rows, 8 rows per thread in registers; per-(ellipse, angle) terms staged in smem
+// in chunks of KC ellipses, so any ellipse count runs.
 // ---------------------------------------------------------------------------
+constexpr int kRadonKC = 64;
+
+template <typename OutT>
 __global__ void __launch_bounds__(256)
-k_radon_ellipses(const double* __restrict__ params, int K, int nt, int ntheta, float* __restrict__ out) {
-  extern __shared__ double sm_r[];
-  double* w2s = sm_r;
-  double* cps = sm_r + K * 32;
-  double* c2s = sm_r + 2 * K * 32;
+k_radon_ellipses(const double* __restrict__ params, int K, int nt, int ntheta, OutT* __restrict__ out) {
+  __shared__ double w2s[kRadonKC * 32], cps[kRadonKC * 32], c2s[kRadonKC * 32];
   const int b = blockIdx.z, j0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const double* P = params + (size_t)b * K * 6;
   const double kPi = 3.14159265358979323846;
-  for (int idx = threadIdx.x; idx < K * 32; idx += blockDim.x) {
-    const int e = idx >> 5, jj = idx & 31;
-    const int j = min(j0 + jj, ntheta - 1);
-    const double cx = P[e * 6], cy = P[e * 6 + 1], a = P[e * 6 + 2], bb = P[e * 6 + 3];
-    const double tilt = P[e * 6 + 4], rho = P[e * 6 + 5];
-    const double th = (double)j * (kPi / ntheta);
-    const double ang = th - tilt;
-    const double ac = a * cos(ang), bs = bb * sin(ang);
-    w2s[idx] = ac * ac + bs * bs;
-    cps[idx] = cx * cos(th) + cy * sin(th);
-    c2s[idx] = 2.0 * rho * a * bb;
-  }
-  __syncthreads();
   const int j = j0 + tx;
-  if (j >= ntheta) return;
-  const int i1 = min(nt, (int)(blockIdx.y + 1) * 64);
-  for (int i = blockIdx.y * 64 + ty; i < i1; i += 8) {
-    const double t = -1.0 + (double)i * (2.0 / nt);
-    double acc = 0.0;
-    for (int e = 0; e < K; ++e) {
-      const double tau = t - cps[e * 32 + tx];
-      const double w2 = w2s[e * 32 + tx];
-      const double under = w2 - tau * tau;
-      if (under > 0.0) acc += c2s[e * 32 + tx] * sqrt(under) / w2;
+  double acc[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+  for (int e0 = 0; e0 < K; e0 += kRadonKC) {
+    const int kc = min(kRadonKC, K - e0);
+    __syncthreads();  // the previous chunk's terms are consumed
+    for (int idx = threadIdx.x; idx < kc * 32; idx += blockDim.x) {
+      const int e = e0 + (idx >> 5), jj = idx & 31;
+      const int jc = min(j0 + jj, ntheta - 1);
+      const double cx = P[e * 6], cy = P[e * 6 + 1], a = P[e * 6 + 2], bb = P[e * 6 + 3];
+      const double tilt = P[e * 6 + 4], rho = P[e * 6 + 5];
+      const double th = (double)jc * (kPi / ntheta);
+      const double ang = th - tilt;
+      const double ac = a * cos(ang), bs = bb * sin(ang);
+      w2s[idx] = ac * ac + bs * bs;
+      cps[idx] = cx * cos(th) + cy * sin(th);
+      c2s[idx] = 2.0 * rho * a * bb;
     }
-    out[((size_t)b * nt + i) * ntheta + j] = (float)acc;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = blockIdx.y * 64 + ty + 8 * r;
+      const double t = -1.0 + (double)i * (2.0 / nt);
+      double s = acc[r];
+      for (int e = 0; e < kc; ++e) {
+        const double tau = t - cps[e * 32 + tx];
+        const double w2 = w2s[e * 32 + tx];
+        const double under = w2 - tau * tau;
+        if (under > 0.0) s += c2s[e * 32 + tx] * sqrt(under) / w2;
+      }
+      acc[r] = s;
+    }
+  }
+  if (j >= ntheta) return;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = blockIdx.y * 64 + ty + 8 * r;
+    if (i < nt) out[((size_t)b * nt + i) * ntheta + j] = (OutT)acc[r];
   }
 }
 
+template <typename OutT>
+cudaError_t radon_ellipses_impl(const double* params, int K, int nt, int ntheta, int batch, OutT* out,
+                                cudaStream_t s) {
+  k_radon_ellipses<OutT><<<dim3((ntheta + 31) / 32, (nt + 63) / 64, batch), 256, 0, s>>>(params, K, nt, ntheta, out);
+  return cudaGetLastError();
+}
 cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int ntheta, int batch, float* out,
                                   cudaStream_t s) {
-  const size_t smem = (size_t)3 * K * 32 * sizeof(double);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_radon_ellipses, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-  }
-  k_radon_ellipses<<<dim3((ntheta + 31) / 32, (nt + 63) / 64, batch), 256, smem, s>>>(params, K, nt, ntheta, out);
-  return cudaGetLastError();
+  return radon_ellipses_impl(params, K, nt, ntheta, batch, out, s);
+}
+cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int ntheta, int batch, double* out,
+                                  cudaStream_t s) {
+  return radon_ellipses_impl(params, K, nt, ntheta, batch, out, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -66,6 +66,8 @@ cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dthe
 
 cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int ntheta, int batch, float* out,
                                   cudaStream_t s);
+cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int ntheta, int batch, double* out,
+                                  cudaStream_t s);
 
 bool sizes_supported(int nt, int ntheta, int L, int M, int MB, bool filter, bool generic);
 // generic-size kernels: ramp over bounds-checked column pairs, Bluestein row DFT / inverse DFT

@@ -149,7 +149,46 @@ def bst_goldens() -> None:
         json.dump(kat, f, indent=1, sort_keys=True)
 
 
+def radon_goldens() -> None:
+    """The input generator radon_ellipses (radon.py:38-61) on EllipseSets (phantoms.py:36-62)."""
+    from fastbp.phantoms import Ellipse, EllipseSet
+    from fastbp.radon import radon_ellipses
+
+    arrays, kat = {}, {}
+    rng = np.random.Generator(np.random.PCG64(4242))
+
+    def random_set(k):
+        return [((rng.uniform(-0.7, 0.7), rng.uniform(-0.7, 0.7)), (rng.uniform(0.02, 0.5), rng.uniform(0.02, 0.5)),
+                 rng.uniform(0.0, math.pi), rng.uniform(-1.0, 1.0)) for _ in range(k)]
+
+    cases = {
+        # hand-picked: one ellipse crossing the unit circle, one thin tilted, one at the origin
+        "small": ([((0.0, 0.0), (0.6, 0.4), 0.3, 1.0), ((0.8, 0.1), (0.5, 0.2), 1.1, -0.5),
+                   ((-0.2, 0.35), (1e-3, 0.3), math.pi / 3, 2.0), ((0.1, -0.5), (0.05, 0.05), 0.0, 0.7),
+                   ((-0.45, -0.2), (0.25, 0.1), 2.9, 0.25)], 64, 45),
+        "many": (random_set(300), 100, 70),      # > 256 ellipses, ragged 64-row / 32-angle tiles
+        "odd": (random_set(7), 33, 17),
+    }
+    for name, (ell, nt, nth) in cases.items():
+        es = EllipseSet(tuple(Ellipse(c, ab, t, r) for c, ab, t, r in ell))
+        arrays[f"{name}_params"] = np.array([[c[0], c[1], ab[0], ab[1], t, r] for c, ab, t, r in ell])
+        arrays[f"{name}_sino"] = radon_ellipses(es, nt, nth).values
+    for key, fn in (("semi_axes_message", lambda: Ellipse((0.0, 0.0), (0.0, 0.1), 0.0, 1.0)),
+                    ("empty_set_message", lambda: EllipseSet(()))):
+        try:
+            fn()
+        except ValueError as e:
+            kat[key] = str(e)
+    np.savez_compressed(os.path.join(HERE, "radon.npz"), **arrays)
+    with open(os.path.join(HERE, "kat_radon.json"), "w") as f:
+        json.dump(kat, f, indent=1, sort_keys=True)
+
+
 def main() -> None:
+    if "--only-radon" in sys.argv:
+        radon_goldens()
+        print("wrote radon goldens")
+        return
     if "--only-bst" in sys.argv:
         bst_goldens()
         print("wrote bst goldens")
@@ -214,6 +253,9 @@ def main() -> None:
         kat[f"const_mean_{nt}_{nth}_{n}"] = float(b.values[inner].mean())
     with open(os.path.join(HERE, "kat.json"), "w") as f:
         json.dump(kat, f, indent=1, sort_keys=True)
+    sector_goldens()
+    bst_goldens()
+    radon_goldens()
     print("wrote goldens:", sorted(os.listdir(HERE)))
 
 

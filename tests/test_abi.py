@@ -405,3 +405,25 @@ def test_synth_configs_match_oracle_phantoms():
         e = phantoms.random_ellipses(seed, 50, 0.01, 0.3)
         ref = np.stack([e.cx, e.cy, e.a, e.b, e.tilt, e.rho], axis=1)
         assert np.array_equal(synth.ellipse_params(seed, 50, 0.01, 0.3), ref)
+
+
+def test_ellipse_containers_mirror_reference():
+    """Ellipse / EllipseSet (phantoms.py:36-62): same fields, same ValueError messages; the
+    device entry point fails loudly without CUDA."""
+    import json as _json
+    import paper_1608_03589_b200 as p
+    with open(os.path.join(REPO, "tests", "golden", "kat_radon.json")) as f:
+        kat = _json.load(f)
+    with pytest.raises(ValueError) as e:
+        p.Ellipse((0.0, 0.0), (0.0, 0.1), 0.0, 1.0)
+    assert str(e.value) == kat["semi_axes_message"]
+    with pytest.raises(ValueError) as e:
+        p.EllipseSet(())
+    assert str(e.value) == kat["empty_set_message"]
+    es = p.EllipseSet((p.Ellipse((0.1, -0.2), (0.3, 0.2), 0.5, 1.5), p.Ellipse((0.0, 0.0), (0.1, 0.1), 0.0, -1.0)))
+    assert len(es) == 2 and [x.intensity for x in es] == [1.5, -1.0]
+    assert np.array_equal(es.params(), [[0.1, -0.2, 0.3, 0.2, 0.5, 1.5], [0.0, 0.0, 0.1, 0.1, 0.0, -1.0]])
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises(RuntimeError, match="no CUDA device"):
+            p.radon_ellipses(es, 16, 8)

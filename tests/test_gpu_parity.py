@@ -204,7 +204,7 @@ def test_device_sinogram_generator_matches_oracle(pkg):
         seed = phantoms.BASE_SEED + 7919 * cfg + idx
         prm = synth.ellipse_params(seed, c["k"], c["amin"], c["amax"])
         ref = phantoms.radon_ellipses(phantoms.random_ellipses(seed, c["k"], c["amin"], c["amax"]), c["nt"], c["ntheta"])
-        got = synth.radon_ellipses(prm[None], c["nt"], c["ntheta"], torch.device("cuda"))[0].cpu().numpy()
+        got = synth.radon_ellipses_batch(prm[None], c["nt"], c["ntheta"], torch.device("cuda"))[0].cpu().numpy()
         assert report(f"synth cfg{cfg}", got, ref) < 1e-6
 
 

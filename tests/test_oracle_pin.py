@@ -296,3 +296,15 @@ def test_spec_truncation_error_is_bounded():
     c = float(np.abs(a[R <= 2 * math.exp(r_shallow)]).max())
     err2 = float(np.sum((a - b) ** 2)) * (2.0 / n) ** 2
     assert err2 <= 2 * math.pi * c * c * math.exp(2 * r_shallow)
+
+
+def test_oracle_radon_ellipses_pinned_to_reference(golden):
+    """oracle/phantoms.radon_ellipses (the harness generator) vs the reference's radon_ellipses
+    on the committed EllipseSet goldens (hand-picked, 300 ellipses, odd sizes)."""
+    z = golden("radon.npz")
+    for name in ("small", "many", "odd"):
+        p = z[f"{name}_params"]
+        ref = z[f"{name}_sino"]
+        e = phantoms.EllipseParams(*(p[:, i].copy() for i in range(6)))
+        got = phantoms.radon_ellipses(e, *ref.shape)
+        assert np.max(np.abs(got - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))), name
