@@ -337,6 +337,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     rc = rc ? rc : P->upload(h.wab, reinterpret_cast<const lpbp::F4**>(&P->t.wab));
     rc = rc ? rc : P->upload(h.ki, &P->t.ki);
     rc = rc ? rc : P->upload(h.wi, reinterpret_cast<const lpbp::F2**>(&P->t.wi));
+    rc = rc ? rc : P->upload(h.kw, &P->t.kw);
     rc = rc ? rc : P->upload(h.khat, reinterpret_cast<const lpbp::F2**>(&P->t.khat));
     rc = rc ? rc : P->upload(h.qidx, &P->t.qidx);
     rc = rc ? rc : P->upload(h.qw, reinterpret_cast<const lpbp::F2**>(&P->t.qw));
@@ -1225,6 +1226,8 @@ int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan) {
       P->rd.nt = h.p.nt;
       P->rd.ntheta = h.p.ntheta;
       P->rd.M = h.M;
+      P->rd.nsm = 148;
+      cudaDeviceGetAttribute(&P->rd.nsm, cudaDevAttrMultiProcessorCount, P->device);
     }
     if (rc) {
       std::string msg = g_last_error;

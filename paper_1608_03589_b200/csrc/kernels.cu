@@ -212,14 +212,14 @@ template <int L, bool PRUNE>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, 2)
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int gp, int ns, int nrho, int row_lo,
            int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
-           const int* __restrict__ ki, const float2* __restrict__ wi, const float2* __restrict__ khat,
-           const float2* __restrict__ tw) {
+           const uint32_t* __restrict__ kw, const float2* __restrict__ khat, const float2* __restrict__ tw) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
   __shared__ __align__(8) uint64_t bar;
   float2* buf = smem_k3;                          // padded_len(L)
   float2* p = buf + padded_len(L);                // ns
   float2* gcol = p + ((ns + 1) & ~1);             // nt (16-B aligned); refilled as soon as the row mix is done
+  uint32_t* kws = reinterpret_cast<uint32_t*>(gcol + gp);  // nrho packed log-polar taps, same for every column
   const int m = blockIdx.x;
   const float sg = (m & 1) ? -1.f : 1.f;
   const int ti = threadIdx.x;
@@ -235,6 +235,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     mbar_arrive_expect_tx(&bar, col_bytes);
     tma_bulk_g2s(gcol, Gh + (size_t)m * gp, col_bytes, &bar);
   }
+  for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
 
   for (int b = 0; b < batch; ++b) {
     mbar_wait(&bar, b & 1);
@@ -257,10 +258,11 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     }
     auto load = [&](int idx) -> float2 {
       if (idx >= nrho) return make_float2(0.f, 0.f);
-      const int k = __ldg(ki + idx);
-      const float2 w = __ldg(wi + idx);
+      const uint32_t e = kws[idx];
+      const int k = (int)(e & 0x7FFu);
+      const float w1 = (float)(e >> 11) * (1.f / 1048576.f);
       const float2 p0 = p[k], p1 = p[k + 1];
-      return make_float2(fmaf(w.x, p0.x, w.y * p1.x), fmaf(w.x, p0.y, w.y * p1.y));
+      return make_float2(fmaf(w1, p1.x - p0.x, p0.x), fmaf(w1, p1.y - p0.y, p0.y));
     };
     auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(kcol + idx)); };
     float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
@@ -458,17 +460,25 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     fence_mbar_init();
   }
   uint32_t phase = 0;  // bit r: parity of the next wait on bars[r] (uniform across threads)
+  // called by all lanes of warp 0: lane 0 arms the barrier, then one box per lane
+  static_assert(G * (NFULL + 1) <= 32, "one TMA box per lane of warp 0");
   auto issue = [&](int region, int step, int slice) {
-    fence_proxy_async_smem();  // order earlier generic accesses to the region before the TMA writes
-    mbar_arrive_expect_tx(&bars[region], STEP_BYTES);
-    for (int g = 0; g < G; ++g) {  // rows (r0 + 2g, r0 + 2g + 1) -> group g's input as [m][2]
-      const int c0 = 2 * (row_min + S * step + 2 * g);
-      float2* dst = smem_k45 + region * QREG + g * FS::IN_PITCH;
-      for (int bx = 0; bx < NFULL; ++bx) tma_load_3d(dst + 2 * (bx * 256), &ymap, c0, bx * 256, slice, &bars[region]);
-      tma_load_3d(dst + 2 * (NFULL * 256), &ytail, c0, NFULL * 256, slice, &bars[region]);
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+      fence_proxy_async_smem();  // order earlier generic accesses to the region before the TMA writes
+      mbar_arrive_expect_tx(&bars[region], STEP_BYTES);
     }
-    const uint32_t a = __ldg(step_off + step), b = __ldg(step_off + step + 1);  // warm L2 with its pixels
-    if (b > a) prefetch_l2_bulk(entries + a, 16u * (b - a));
+    __syncwarp();
+    if (lane < G * (NFULL + 1)) {  // rows (r0 + 2g, r0 + 2g + 1) -> group g's input as [m][2]
+      const int g = lane / (NFULL + 1), bx = lane - g * (NFULL + 1);
+      const int c0 = 2 * (row_min + S * step + 2 * g);
+      float2* dst = smem_k45 + region * QREG + g * FS::IN_PITCH + 2 * (bx * 256);
+      if (bx < NFULL) tma_load_3d(dst, &ymap, c0, bx * 256, slice, &bars[region]);
+      else tma_load_3d(dst, &ytail, c0, NFULL * 256, slice, &bars[region]);
+    } else if (lane == 31) {
+      const uint32_t a = __ldg(step_off + step), b = __ldg(step_off + step + 1);  // warm L2 with its pixels
+      if (b > a) prefetch_l2_bulk(entries + a, 16u * (b - a));
+    }
   };
   auto row_of = [&](const float2* Q, int li) -> const float* {  // row li in [0, S) of a step region
     return reinterpret_cast<const float*>(Q + (li >> 1) * HALF) + (li & 1) * RPITCH;
@@ -484,7 +494,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     const int k0 = (units_per_slice - 1 - u / batch) * UQ;  // outermost units first
     const int k1 = min(k0 + UQ, nsteps);
     const int ks = k0 > 0 ? k0 - 1 : 0;  // the previous step only feeds its last row
-    if (threadIdx.x == 0)
+    if (threadIdx.x < 32)
       for (int q = ks; q < min(ks + 2, k1); ++q) issue((q - ks) % NR, q, slice);
     float* out = img + (size_t)slice * n * n;
 
@@ -592,7 +602,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
         }
       }
       __syncthreads();  // region of kk-1 is free now: refill it with step kk+2
-      if (threadIdx.x == 0 && kk + 2 < k1) issue((kk + 2 - ks) % NR, kk + 2, slice);
+      if (threadIdx.x < 32 && kk + 2 < k1) issue((kk + 2 - ks) % NR, kk + 2, slice);
     }
   }
 }
@@ -883,13 +893,13 @@ template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
                       cudaStream_t s) {
   const int gp = d.gp > 0 ? d.gp : d.nt;
-  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp) * sizeof(float2);
+  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp) * sizeof(float2) + (size_t)d.nrho * 4;
   // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
   auto k = (2 * d.nrho <= L) ? k_rho_conv<L, true> : k_rho_conv<L, false>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
   k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, gp, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.ab, t.wab,
-                                              t.ki, t.wi, t.khat, t.tw_rho);
+                                              t.kw, t.khat, t.tw_rho);
   return cudaGetLastError();
 }
 

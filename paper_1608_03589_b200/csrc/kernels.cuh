@@ -21,6 +21,7 @@ struct DevTables {
   const float4* wab;      // [ns] weights (wa0, wa1, wb0, wb1)
   const int* ki;          // [nrho] s-row of the log-polar lerp
   const float2* wi;       // [nrho] weights (w0, w1)
+  const uint32_t* kw;     // [nrho] packed ki | w1 * 2^20 << 11 (K3 stages it in shared memory)
   const float2* khat;     // [nh][L] kernel spectrum incl. 0.5*drho*dphi/(L*nphi)
   const uint32_t* qidx;   // [nq][nq] readout quadrant table: i0 | j0 << 16, ~0 = zero pixel
   const float2* qw;       // [nq][nq] readout weights (wi, wj)

@@ -270,6 +270,14 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
     h.ki[i] = k;
     h.wi[i] = F2{(float)w0, (float)w1};
   }
+  // packed taps for K3's shared-memory copy: f = e^rho (ns-1) lies in (0, ns-1], so
+  // lerp_tap always gives w0 = 1 - w1 here; w1 keeps 20 fractional bits (error <= 2^-21)
+  if (ns - 1 > 0x7FF) return "ns too large for the packed log-polar taps (ns <= 2048)";
+  h.kw.resize(nrho);
+  for (int i = 0; i < nrho; ++i) {
+    const long long wq = std::llround((double)h.wi[i].y * 1048576.0);
+    h.kw[i] = (uint32_t)h.ki[i] | ((uint32_t)wq << 11);
+  }
 
   // --- kernel support (logpolar.py:66-81, rolled by -nphi/2 at :110):
   // cell (k, l) holds 1/drho iff |e^{k drho} cos(theta_j) - 1| <= drho with

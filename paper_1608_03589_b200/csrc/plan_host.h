@@ -35,6 +35,7 @@ struct HostPlan {
   std::vector<I2> ab;
   std::vector<F4> wab;
   std::vector<int32_t> ki;
+  std::vector<uint32_t> kw;  // [nrho] packed log-polar tap: ki | round(w1 * 2^20) << 11 (w0 = 1 - w1)
   std::vector<uint32_t> qidx;
   // fused inverse-DFT + readout: quads of band_rows (4) log-polar rows starting at
   // r0 = row_min + 4b (row_min even); band_entries lists the quadrant pixels (qy*nq + qx)
