@@ -94,6 +94,106 @@ k_ramp(const float* __restrict__ g, float* __restrict__ out, int nt, int ntheta,
   }
 }
 
+// Persistent TMA variant (nt a multiple of 256): one CTA per SM, two FFT groups,
+// two tile slots.  Tiles of 8 columns x nt rows arrive by 2-D TMA boxes {8, 256}
+// and leave by TMA stores, both issued by one thread, so HBM traffic runs behind
+// the convolutions of the other slot with no load/store instructions in the
+// warps.  The slot layout is TMA's 32-byte swizzle: float (t, c) sits at
+// t*8 + (c ^ 4*((t >> 2) & 1)), which spreads a column pair of 16 consecutive rows
+// over 8 bank pairs (2-way) instead of 4 (4-way) for the dense layout.
+template <int M>
+struct RampTmaShape {
+  static constexpr int G = 2, TC = 8, BOXR = 256;
+  static constexpr int T = FftPlan<M, false>::T;
+  static size_t smem(int nt) {
+    return 1024 + 2 * (size_t)nt * TC * sizeof(float) + (size_t)G * padded_len(M) * sizeof(float2) +
+           (size_t)M * sizeof(float) + 64;
+  }
+};
+
+template <int M>
+__global__ void __launch_bounds__(RampTmaShape<M>::G * FftPlan<M, false>::T, 1)
+k_ramp_tma(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUtensorMap omap, int nt,
+           int tiles_per_slice, int ntiles, const float* __restrict__ resp, const float2* __restrict__ tw) {
+  using RS = RampTmaShape<M>;
+  constexpr int T = RS::T, G = RS::G, TC = RS::TC, BOXR = RS::BOXR;
+  static_assert((M / 16) % 8 == 0 && T % 8 == 0, "pass-0 rows must keep (idx >> 2) & 1 = (ti >> 2) & 1");
+  extern __shared__ unsigned char smem_k1t[];
+  // 1024-byte aligned slots (TMA swizzle atoms); offset from the shared symbol itself so the
+  // compiler keeps every access in the shared window (LDS/STS, not generic LD/ST)
+  float* slots = reinterpret_cast<float*>(smem_k1t + ((1024u - (smem_u32(smem_k1t) & 1023u)) & 1023u));
+  const int slot_floats = nt * TC;
+  float2* bufs = reinterpret_cast<float2*>(slots + 2 * slot_floats);
+  float* resp_s = reinterpret_cast<float*>(bufs + G * padded_len(M));  // the response, read by every convolution
+  uint64_t* bars = reinterpret_cast<uint64_t*>(resp_s + M);
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  float2* buf = bufs + gi * padded_len(M);
+  const uint32_t tile_bytes = (uint32_t)slot_floats * sizeof(float);
+  const int first = blockIdx.x, stride = gridDim.x;
+  auto corner = [&](int tile, int& c0, int& r0) {
+    const int b = tile / tiles_per_slice;
+    c0 = (tile - b * tiles_per_slice) * TC;
+    r0 = b * nt;
+  };
+  auto load_tile = [&](int tile, int s) {  // one thread
+    int c0, r0;
+    corner(tile, c0, r0);
+    mbar_arrive_expect_tx(&bars[s], tile_bytes);
+    for (int k = 0; k < nt / BOXR; ++k) tma_load_2d(slots + s * slot_floats + k * BOXR * TC, &gmap, c0, r0 + k * BOXR, &bars[s]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < M; i += blockDim.x) resp_s[i] = __ldg(resp + i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (first < ntiles) load_tile(first, 0);
+    if (first + stride < ntiles) load_tile(first + stride, 1);
+  }
+  const int sw = ((ti >> 2) & 1) << 2;  // this thread's rows all share the swizzle bit
+  const GroupSync gsync{1 + gi, T};
+  int it = 0;
+  int refill = -1;  // (thread 0) tile whose slot waits to be refilled once its TMA stores have read it
+#pragma unroll 1
+  for (int tile = first; tile < ntiles; tile += stride, ++it) {
+    const int s = it & 1;
+    float* tl = slots + s * slot_floats;
+    mbar_wait(&bars[s], (it >> 1) & 1);
+#pragma unroll 1
+    for (int round = 0; round < TC / 2 / G; ++round) {
+      if (round == 1 && threadIdx.x == 0 && refill >= 0) {
+        // the previous tile's stores have had a round to drain: refill its slot two tiles ahead
+        bulk_wait_group_read<0>();
+        load_tile(refill + 2 * stride, s ^ 1);
+        refill = -1;
+      }
+      const int q = round * G + gi;
+      float* col = tl + ((2 * q) ^ sw);  // row idx at col + 8 idx
+      auto load = [&](int idx) -> float2 {
+        return idx < nt ? *reinterpret_cast<const float2*>(col + idx * TC) : make_float2(0.f, 0.f);
+      };
+      auto mul = [&](int idx, float2 v) -> float2 { return cscale(v, resp_s[idx]); };
+      auto store = [&](int idx, float2 v) {
+        if (idx < nt) *reinterpret_cast<float2*>(col + idx * TC) = v;
+      };
+      block_conv<M, true, 16>(buf, ti, tw, load, mul, store, gsync);  // M = 2 nt: half-zero in, low half out
+      gsync();                                                       // buf is reused by the next round
+    }
+    __syncthreads();  // every group's results are in the slot
+    if (threadIdx.x == 0) {
+      int c0, r0;
+      corner(tile, c0, r0);
+      fence_proxy_async_smem();  // the convolutions' generic stores before the TMA reads
+      for (int k = 0; k < nt / BOXR; ++k) tma_store_2d(&omap, c0, r0 + k * BOXR, tl + k * BOXR * TC);
+      bulk_commit_group();
+      if (tile + 2 * stride < ntiles) refill = tile;
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_group<0>();
+}
+
 // ---------------------------------------------------------------------------
 // K2: real DFT of sinogram rows, zero-padded from ntheta to nphi = 2 ntheta.
 // Rows t, t+1 are packed as re/im; spectra are separated with
@@ -916,7 +1016,16 @@ cudaError_t irdft_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
 }  // namespace
 
 // Tile shapes per size: (columns or rows per CTA, concurrent FFTs per CTA).
+namespace {
+template <int M>
+cudaError_t ramp_tma_impl(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s);
+}  // namespace
+
 cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s) {
+  if (d.M == 4096) {
+    const cudaError_t e = ramp_tma_impl<4096>(d, t, g, out, batch, s);
+    if (e != cudaErrorNotSupported) return e;  // nt % 256 != 0 takes the tile kernel below
+  }
   switch (d.M) {
     case 512: return ramp_impl<512, 16, 4>(d, t, g, out, batch, s);
     case 1024: return ramp_impl<1024, 16, 2>(d, t, g, out, batch, s);
@@ -1005,6 +1114,40 @@ cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, 
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// Sinogram batch as a 2-D tensor {ntheta, batch * nt} of fp32, box {8, 256}, 32-byte swizzle.
+cudaError_t encode_sino_map(CUtensorMap* map, const float* g, int nt, int ntheta, int batch) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {(cuuint64_t)ntheta, (cuuint64_t)nt * batch};
+  const cuuint64_t strides[1] = {(cuuint64_t)ntheta * 4};
+  const cuuint32_t box[2] = {8, 256};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(g), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int M>
+cudaError_t ramp_tma_impl(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s) {
+  using RS = RampTmaShape<M>;
+  if (d.ntheta % RS::TC || d.nt % RS::BOXR || (reinterpret_cast<uintptr_t>(g) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15) || (d.ntheta * 4) % 16)
+    return cudaErrorNotSupported;
+  CUtensorMap gm, om;
+  cudaError_t e = encode_sino_map(&gm, g, d.nt, d.ntheta, batch);
+  if (!e) e = encode_sino_map(&om, out, d.nt, d.ntheta, batch);
+  if (e) return e;
+  const size_t smem = RS::smem(d.nt);
+  auto k = k_ramp_tma<M>;
+  e = prep(k, smem);
+  if (e) return e;
+  const int per = d.ntheta / RS::TC, tiles = per * batch;
+  const int grid = tiles < d.nsm ? tiles : d.nsm;
+  k<<<grid, RS::G * RS::T, smem, s>>>(gm, om, d.nt, per, tiles, t.ramp, t.tw_ramp);
+  return cudaGetLastError();
 }
 }  // namespace
 
