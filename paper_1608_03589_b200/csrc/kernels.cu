@@ -218,21 +218,28 @@ struct RdftShape {
   static constexpr int IN = TR * NTH / 2;                    // float2 per input tile
   static constexpr int STG = ((NH * TR) + 15) & ~15;         // float2 staging
   static constexpr int BUF = (padded_len(NPHI) + 15) & ~15;  // float2 per FFT buffer
-  static constexpr size_t SMEM = ((size_t)2 * IN + STG + G * BUF) * 8 + 64;
+  static constexpr size_t SMEM = ((size_t)2 * IN + STG + G * BUF) * 8 + 64 + 1024;  // + alignment slack
+  static constexpr int NFULL = (NPHI / 2) / 256;  // 256-row TMA store boxes of the spectra; one 1-row tail box
 };
 
 // NARROW: compacted input rows (the sector path): `win` (multiple of 4) floats holding the
 // row's first win_lo columns followed by its last win - win_lo columns; the rest is zero.
 template <int NPHI, bool NARROW>
 __global__ void __launch_bounds__(RdftShape<NPHI>::G * FftPlan<NPHI, false>::T, 1)
-k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int ntiles_per_slice, int ntiles,
+k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUtensorMap gtail,
+           const float* __restrict__ g, int nt, int ntiles_per_slice, int ntiles,
            const float2* __restrict__ tw, int win, int win_lo) {
   using RS = RdftShape<NPHI>;
   constexpr int T = FftPlan<NPHI, false>::T;
-  constexpr int TR = RS::TR, NTH = RS::NTH, NH = RS::NH;
-  extern __shared__ __align__(128) float2 smem_k2[];
+  constexpr int TR = RS::TR, NTH = RS::NTH, NH = RS::NH, NFULL = RS::NFULL;
+  static_assert(TR == 4 && NFULL * 256 + 1 == NH, "32-byte staging rows, full boxes + one tail row");
+  extern __shared__ __align__(128) float2 smem_k2_raw[];
+  // 1024-byte aligned base (TMA swizzle atoms), offset from the shared symbol to stay in the shared window
+  float2* smem_k2 = smem_k2_raw + ((1024u - (smem_u32(smem_k2_raw) & 1023u)) & 1023u) / sizeof(float2);
   float* in0 = reinterpret_cast<float*>(smem_k2);               // 2 x TR*NTH floats
-  float2* stg = smem_k2 + 2 * RS::IN;                            // [NH][TR], swizzled columns
+  // [NH][TR] spectra staging in TMA's 32-byte swizzle: complex (m, c) at m*TR + (c ^ 2*((m >> 2) & 1));
+  // leaves by TMA stores into G[b][m][t0 .. t0+TR)
+  float2* stg = smem_k2 + 2 * RS::IN;
   float2* buf = stg + RS::STG + (threadIdx.x / T) * RS::BUF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg + RS::STG + RS::G * RS::BUF);
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
@@ -275,6 +282,7 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int nti
     };
     auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
     block_fft<NPHI, false, true, false, true, 16>(buf, ti, tw, load, store, GroupSync{1 + gi, T});
+    if (threadIdx.x == 0) bulk_wait_group_read<0>();  // the previous tile's TMA stores have read stg
     __syncthreads();
     // every thread is past pass 0: the input slot is free for the tile two ahead
     if (threadIdx.x == 0 && tile + 2 * stride < ntiles) {
@@ -285,19 +293,21 @@ k_row_rdft(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int nti
     for (int m = ti; m < NH; m += T) {
       const float2 z = buf[pad16(m)];
       const float2 w = buf[pad16((NPHI - m) & (NPHI - 1))];
-      stg[m * TR + stg_col<TR>(m, 2 * gi)] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
-      stg[m * TR + stg_col<TR>(m, 2 * gi + 1)] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+      const int sw = ((m >> 2) & 1) << 1;
+      stg[m * TR + ((2 * gi) ^ sw)] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
+      stg[m * TR + ((2 * gi + 1) ^ sw)] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
     }
     __syncthreads();
-    const int b = tile / ntiles_per_slice, t0 = (tile - b * ntiles_per_slice) * TR;
-    float2* dst = Gh + (size_t)b * NH * nt + t0;
-#pragma unroll 8
-    for (int e = threadIdx.x; e < NH * TR; e += blockDim.x) {
-      const int m = e / TR, c = e % TR;
-      dst[(size_t)m * nt + c] = stg[m * TR + stg_col<TR>(m, c)];
+    if (threadIdx.x == 0) {
+      const int b = tile / ntiles_per_slice, t0 = (tile - b * ntiles_per_slice) * TR;
+      fence_proxy_async_smem();  // the separation's generic stores before the TMA reads
+      for (int bx = 0; bx < NFULL; ++bx) tma_store_2d(&gmap, 2 * t0, b * NH + bx * 256, stg + bx * 256 * TR);
+      tma_store_2d(&gtail, 2 * t0, b * NH + NFULL * 256, stg + NFULL * 256 * TR);
+      bulk_commit_group();
     }
-    // next tile's separation rewrites stg only after its FFT's barriers
+    // next tile's separation rewrites stg only after its FFT and the store-read wait above
   }
+  if (threadIdx.x == 0) bulk_wait_group<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -950,6 +960,8 @@ cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int nthet
 // launchers
 // ---------------------------------------------------------------------------
 namespace {
+cudaError_t encode_rowspec_map(CUtensorMap* map, const float2* G, int nt, int nh, int batch, int box_m);
+
 template <typename K>
 cudaError_t prep(K kernel, size_t smem) {
   if (smem > 48 * 1024) {
@@ -978,14 +990,19 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
   const bool narrow = win < d.ntheta;
   if (narrow && (win % 4)) return cudaErrorNotSupported;  // TMA bulk rows: 16-byte multiples
   auto k = narrow ? k_row_rdft<NPHI, true> : k_row_rdft<NPHI, false>;
-  cudaError_t e = prep(k, RS::SMEM);
+  if ((reinterpret_cast<uintptr_t>(Gh) & 15) || (d.nt * 8) % 16) return cudaErrorNotSupported;
+  CUtensorMap gm, gt;
+  cudaError_t e = encode_rowspec_map(&gm, Gh, d.nt, RS::NH, batch, 256);
+  if (!e) e = encode_rowspec_map(&gt, Gh, d.nt, RS::NH, batch, 1);
+  if (e) return e;
+  e = prep(k, RS::SMEM);
   if (e) return e;
   const int per = d.nt / RS::TR, tiles = per * batch;
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, RS::G * FftPlan<NPHI, false>::T, RS::SMEM);
   const int slots = d.nsm * (occ > 0 ? occ : 1);
   const int grid = tiles < slots ? tiles : slots;
-  k<<<grid, RS::G * FftPlan<NPHI, false>::T, RS::SMEM, s>>>(g, Gh, d.nt, per, tiles, t.tw_phi, win, d.win_lo);
+  k<<<grid, RS::G * FftPlan<NPHI, false>::T, RS::SMEM, s>>>(gm, gt, g, d.nt, per, tiles, t.tw_phi, win, d.win_lo);
   return cudaGetLastError();
 }
 
@@ -1112,6 +1129,21 @@ cudaError_t encode_spectra_map(CUtensorMap* map, const float2* Y, int nrho_pad, 
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(Y), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// Row spectra G[b][m][t] (complex, t pitch nt) as a 2-D tensor {2 nt floats, batch * nh rows}; box {8 floats
+// (4 complex t), box_m rows}, 32-byte swizzle (K2's staging layout).
+cudaError_t encode_rowspec_map(CUtensorMap* map, const float2* G, int nt, int nh, int batch, int box_m) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {(cuuint64_t)(2 * nt), (cuuint64_t)nh * batch};
+  const cuuint64_t strides[1] = {(cuuint64_t)nt * 8};
+  const cuuint32_t box[2] = {8, (cuuint32_t)box_m};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(G), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
