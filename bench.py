@@ -38,8 +38,8 @@ except (OSError, ValueError):
     MEASURED = {}
 # dram__bytes_read.sum + dram__bytes_write.sum per slice from the committed ncu --set full
 # capture (profiles/r01f_summary.md, 8-slice launches at 2048^2 FBP, the bench's chunk)
-TRAFFIC_PER_SLICE = {"rho_conv": (403.292416e6 + 442.629376e6) / 8, "irdft_readout": (717.406976e6 + 179.756544e6) / 8,
-                     "ramp_filter": (134.275072e6 + 94.063872e6) / 8, "row_rdft": (134.299392e6 + 215.366400e6) / 8}
+TRAFFIC_PER_SLICE = {"rho_conv": (403.542528e6 + 442.195200e6) / 8, "irdft_readout": (717.420288e6 + 180.011008e6) / 8,
+                     "ramp_filter": (134.268160e6 + 90.103808e6) / 8, "row_rdft": (134.237440e6 + 215.784704e6) / 8}
 UNIT = "slices/s"
 
 
