@@ -275,6 +275,19 @@ def test_empty_batch_and_stage_api_full_size(pkg):
     assert report("cfg2 logpolar stage", lp, ref) <= RTOL
 
 
+@pytest.mark.parametrize("nt,nth", [(1100, 256), (1536, 256)])
+def test_ramp_filter_both_m4096_kernels(pkg, nt, nth):
+    """M = 4096 filters take the persistent TMA kernel when nt % 256 == 0 (1536) and the
+    smem tile kernel otherwise (1100); both must match filter_sinogram (filtering.py:54-70)."""
+    g = phantoms.sinogram(2200 + nt, nt, nth, 12, 0.05, 0.35, 0.01).astype(np.float64)
+    s = pkg.Sinogram(nt, nth, g)
+    got = pkg.filter_sinogram(s, pkg.FilterSpec()).values
+    ref = O.ramp_filter(g, 0.0, 1.0)
+    assert report(f"ramp M=4096 nt={nt}", got, ref) <= RTOL
+    img = pkg.fbp(s, pkg.FilterSpec(), engine="logpolar", n=128).values
+    assert report(f"fbp nt={nt}", img, O.fbp_logpolar(g, 128)) <= RTOL
+
+
 @pytest.mark.parametrize("nt,n,fbp", [(256, 256, False), (256, 255, True), (512, 300, True), (2048, 2048, True)])
 def test_no_out_of_bounds_writes(pkg, nt, n, fbp):
     """compute-sanitizer is unavailable on this pool: carve input, output and
