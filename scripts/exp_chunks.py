@@ -12,7 +12,7 @@ sino = p.synth.config_batch(3, range(B), device="cuda")
 out = torch.empty(B, 2048, 2048, device="cuda")
 plan = p.LogPolarPlan(2048, 2048, 2048, filter_spec=(0.0, 1.0))
 streams = [torch.cuda.Stream() for _ in range(3)]
-for C in (4, 8, 12):
+for C in (4, 8, 16):
     ws = [torch.empty(plan.workspace_bytes(C), dtype=torch.uint8, device="cuda") for _ in range(3)]
     for ns in (2, 3):
         def run():
