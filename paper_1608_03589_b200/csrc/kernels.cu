@@ -198,15 +198,8 @@ k_ramp_tma(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
 // K2: real DFT of sinogram rows, zero-padded from ntheta to nphi = 2 ntheta.
 // Rows t, t+1 are packed as re/im; spectra are separated with
 //   A[m] = (Z[m] + conj Z[-m]) / 2,  B[m] = (Z[m] - conj Z[-m]) / 2i
-// and staged as [m][TR] so the write of G[m][t0..t0+TR) is contiguous.
+// and staged as [m][TR] (TMA 32-byte swizzle) so G[m][t0..t0+TR) leaves by TMA stores.
 // ---------------------------------------------------------------------------
-// Dense staging [m][TR] with an XOR swizzle of the column: for 16 consecutive m the
-// 8-byte slots (TR*m + (c ^ sw(m))) mod 16 are all distinct -> conflict-free.
-template <int TR>
-__device__ __forceinline__ int stg_col(int m, int c) {
-  static_assert(TR >= 2 && TR <= 16 && (TR & (TR - 1)) == 0, "TR power of two <= 16");
-  return c ^ ((m / (16 / TR)) & (TR - 1));
-}
 
 // Persistent: each CTA walks tiles (slice, 4 consecutive rows); a tile's rows are
 // contiguous (4 x NTH floats) and arrive by one TMA bulk copy into a double
