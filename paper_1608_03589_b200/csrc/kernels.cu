@@ -135,11 +135,14 @@ k_ramp_tma(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
     c0 = (tile - b * tiles_per_slice) * TC;
     r0 = b * nt;
   };
-  auto load_tile = [&](int tile, int s) {  // one thread
+  auto load_tile = [&](int tile, int s) {  // warp 0: lane 0 arms the barrier, one box per lane
+    const int lane = threadIdx.x;
     int c0, r0;
     corner(tile, c0, r0);
-    mbar_arrive_expect_tx(&bars[s], tile_bytes);
-    for (int k = 0; k < nt / BOXR; ++k) tma_load_2d(slots + s * slot_floats + k * BOXR * TC, &gmap, c0, r0 + k * BOXR, &bars[s]);
+    if (lane == 0) mbar_arrive_expect_tx(&bars[s], tile_bytes);
+    __syncwarp();
+    for (int k = lane; k < nt / BOXR; k += 32)
+      tma_load_2d(slots + s * slot_floats + k * BOXR * TC, &gmap, c0, r0 + k * BOXR, &bars[s]);
   };
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -148,7 +151,7 @@ k_ramp_tma(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
   }
   for (int i = threadIdx.x; i < M; i += blockDim.x) resp_s[i] = __ldg(resp + i);
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     if (first < ntiles) load_tile(first, 0);
     if (first + stride < ntiles) load_tile(first + stride, 1);
   }
@@ -163,9 +166,10 @@ k_ramp_tma(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
     mbar_wait(&bars[s], (it >> 1) & 1);
 #pragma unroll 1
     for (int round = 0; round < TC / 2 / G; ++round) {
-      if (round == 1 && threadIdx.x == 0 && refill >= 0) {
-        // the previous tile's stores have had a round to drain: refill its slot two tiles ahead
+      if (round == 1 && threadIdx.x < 32 && refill >= 0) {
+        // the previous tile's stores (one per lane) have had a round to drain: refill the slot two tiles ahead
         bulk_wait_group_read<0>();
+        __syncwarp();
         load_tile(refill + 2 * stride, s ^ 1);
         refill = -1;
       }
@@ -182,16 +186,16 @@ k_ramp_tma(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
       gsync();                                                       // buf is reused by the next round
     }
     __syncthreads();  // every group's results are in the slot
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // one TMA store box per lane
       int c0, r0;
       corner(tile, c0, r0);
-      fence_proxy_async_smem();  // the convolutions' generic stores before the TMA reads
-      for (int k = 0; k < nt / BOXR; ++k) tma_store_2d(&omap, c0, r0 + k * BOXR, tl + k * BOXR * TC);
+      fence_proxy_async_smem();  // the convolutions' generic stores before this lane's TMA reads
+      for (int k = threadIdx.x; k < nt / BOXR; k += 32) tma_store_2d(&omap, c0, r0 + k * BOXR, tl + k * BOXR * TC);
       bulk_commit_group();
       if (tile + 2 * stride < ntiles) refill = tile;
     }
   }
-  if (threadIdx.x == 0) bulk_wait_group<0>();
+  if (threadIdx.x < 32) bulk_wait_group<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -225,7 +229,7 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
   using RS = RdftShape<NPHI>;
   constexpr int T = FftPlan<NPHI, false>::T;
   constexpr int TR = RS::TR, NTH = RS::NTH, NH = RS::NH, NFULL = RS::NFULL;
-  static_assert(TR == 4 && NFULL * 256 + 1 == NH, "32-byte staging rows, full boxes + one tail row");
+  static_assert(TR == 4 && NFULL * 256 + 1 == NH && NFULL < 32, "32-byte staging rows, full boxes + one tail row");
   extern __shared__ __align__(128) float2 smem_k2_raw[];
   // 1024-byte aligned base (TMA swizzle atoms), offset from the shared symbol to stay in the shared window
   float2* smem_k2 = smem_k2_raw + ((1024u - (smem_u32(smem_k2_raw) & 1023u)) & 1023u) / sizeof(float2);
@@ -275,7 +279,7 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
     };
     auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
     block_fft<NPHI, false, true, false, true, 16>(buf, ti, tw, load, store, GroupSync{1 + gi, T});
-    if (threadIdx.x == 0) bulk_wait_group_read<0>();  // the previous tile's TMA stores have read stg
+    if (threadIdx.x < 32) bulk_wait_group_read<0>();  // the previous tile's TMA stores (warp 0's lanes) have read stg
     __syncthreads();
     // every thread is past pass 0: the input slot is free for the tile two ahead
     if (threadIdx.x == 0 && tile + 2 * stride < ntiles) {
@@ -291,16 +295,17 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
       stg[m * TR + ((2 * gi + 1) ^ sw)] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x <= NFULL) {  // one TMA store box per lane of warp 0
       const int b = tile / ntiles_per_slice, t0 = (tile - b * ntiles_per_slice) * TR;
-      fence_proxy_async_smem();  // the separation's generic stores before the TMA reads
-      for (int bx = 0; bx < NFULL; ++bx) tma_store_2d(&gmap, 2 * t0, b * NH + bx * 256, stg + bx * 256 * TR);
-      tma_store_2d(&gtail, 2 * t0, b * NH + NFULL * 256, stg + NFULL * 256 * TR);
+      const int bx = threadIdx.x;
+      fence_proxy_async_smem();  // the separation's generic stores before this lane's TMA reads
+      if (bx < NFULL) tma_store_2d(&gmap, 2 * t0, b * NH + bx * 256, stg + bx * 256 * TR);
+      else tma_store_2d(&gtail, 2 * t0, b * NH + NFULL * 256, stg + NFULL * 256 * TR);
       bulk_commit_group();
     }
     // next tile's separation rewrites stg only after its FFT and the store-read wait above
   }
-  if (threadIdx.x == 0) bulk_wait_group<0>();
+  if (threadIdx.x < 32) bulk_wait_group<0>();
 }
 
 // ---------------------------------------------------------------------------
