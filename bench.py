@@ -37,9 +37,9 @@ try:
 except (OSError, ValueError):
     MEASURED = {}
 # dram__bytes_read.sum + dram__bytes_write.sum per slice from the committed ncu --set full
-# capture (profiles/r01i_summary.md, 8-slice launches at 2048^2 FBP, the bench's chunk)
-TRAFFIC_PER_SLICE = {"rho_conv": (403.542528e6 + 442.195200e6) / 8, "irdft_readout": (717.420288e6 + 180.011008e6) / 8,
-                     "ramp_filter": (134.268160e6 + 90.103808e6) / 8, "row_rdft": (134.237440e6 + 215.784704e6) / 8}
+# capture (profiles/r01j_summary.md, 8-slice launches at 2048^2 FBP, the bench's chunk)
+TRAFFIC_PER_SLICE = {"rho_conv": (403.552768e6 + 441.297408e6) / 8, "irdft_readout": (717.000704e6 + 179.214336e6) / 8,
+                     "ramp_filter": (134.266112e6 + 90.483200e6) / 8, "row_rdft": (134.241024e6 + 215.762432e6) / 8}
 UNIT = "slices/s"
 
 
