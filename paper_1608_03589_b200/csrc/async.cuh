@@ -67,6 +67,11 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, int c0, int c1, c
                "r"(c1), "r"(smem_u32(src))
                : "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const void* tmap, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(tmap),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // the committed bulk stores have finished reading shared memory (all but N groups)
 template <int N>

@@ -14,8 +14,11 @@
 //   KB3 grid_y   X -> img         inverse DFT along y as a real transform (two
 //                                 columns packed as re/im), crop, scale and the
 //                                 mean offset (subtract_mean mode)
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include "async.cuh"
 #include "bst_kernels.cuh"
 #include "fft.cuh"
 
@@ -343,16 +346,24 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
 // pair (x1, x2) is Z[ky] = X[ky][x1] + i X[ky][x2] with Hermitian extension,
 // so one inverse FFT gives both real columns.  Crop y in [p0, p0 + n).
 // ---------------------------------------------------------------------------
-template <int BIG, int TC, int G, bool GEN>
+// TMA_OUT: the crop leaves by 2-D TMA stores (boxes {8 columns, 256 rows}, 3-D map {n, n, batch});
+// the staging then is [n][8] in TMA's 32-byte swizzle (float (y, c) at y*8 + (c ^ 4*((y >> 2) & 1)))
+// instead of the [n][TC + 1] pitch the thread write-out uses.
+template <int BIG, int TC, int G, bool GEN, bool TMA_OUT>
 __global__ void __launch_bounds__(G * FftPlan<BIG, true>::T)
-k_bst_grid_y(const float2* __restrict__ X, float* __restrict__ img, int n, int p0, float s_img, float s_mean,
-             float fbp, int subtract_mean, const double* __restrict__ acc, const float2* __restrict__ tw, Chirp ch) {
+k_bst_grid_y(const __grid_constant__ CUtensorMap omap, const float2* __restrict__ X, float* __restrict__ img, int n,
+             int p0, float s_img, float s_mean, float fbp, int subtract_mean, const double* __restrict__ acc,
+             const float2* __restrict__ tw, Chirp ch) {
   constexpr int T = FftPlan<BIG, true>::T;
+  static_assert(!TMA_OUT || TC == 8, "32-byte staging rows");
+  constexpr int SP = TMA_OUT ? TC : TC + 1;  // staging pitch (floats)
   const int big = GEN ? ch.len : BIG;
   const int HB = big / 2;
-  extern __shared__ __align__(16) float2 smem_b3[];
-  float* stg = reinterpret_cast<float*>(smem_b3);  // [n][TC + 1]
-  float2* buf = smem_b3 + ((size_t)n * (TC + 1) + 1) / 2 + (threadIdx.x / T) * padded_len(BIG);
+  extern __shared__ __align__(16) float2 smem_b3_raw[];
+  // 1024-byte aligned (TMA swizzle atoms), offset from the shared symbol to stay in the shared window
+  float2* smem_b3 = smem_b3_raw + ((1024u - (smem_u32(smem_b3_raw) & 1023u)) & 1023u) / sizeof(float2);
+  float* stg = reinterpret_cast<float*>(smem_b3);  // [n][SP]
+  float2* buf = smem_b3 + ((size_t)n * SP + 1) / 2 + (threadIdx.x / T) * padded_len(BIG);
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int x0 = blockIdx.x * TC;
   const int b = blockIdx.y;
@@ -382,20 +393,55 @@ k_bst_grid_y(const float2* __restrict__ X, float* __restrict__ img, int n, int p
     auto store = [&](int y, float2 v) {
       const int yc = y - p0;
       if (yc >= 0 && yc < n) {
-        stg[(size_t)yc * (TC + 1) + 2 * q] = v.x * s_img + offset;
-        stg[(size_t)yc * (TC + 1) + 2 * q + 1] = v.y * s_img + offset;
+        const float2 o = make_float2(v.x * s_img + offset, v.y * s_img + offset);
+        if constexpr (TMA_OUT)
+          *reinterpret_cast<float2*>(stg + (size_t)yc * SP + ((2 * q) ^ (((yc >> 2) & 1) << 2))) = o;
+        else {
+          stg[(size_t)yc * SP + 2 * q] = o.x;
+          stg[(size_t)yc * SP + 2 * q + 1] = o.y;
+        }
       }
     };
     dft<BIG, true, GEN, false, false>(buf, ti, tw, ch, load, store, GroupBarT<T>{1 + gi});
     GroupBarT<T>{1 + gi}();
   }
   __syncthreads();
-  float* ob = img + (size_t)b * n * n;
-  const int w = min(TC, n - x0);
-  for (int e = threadIdx.x; e < n * TC; e += blockDim.x) {
-    const int y = e / TC, c = e % TC;
-    if (c < w) ob[(size_t)y * n + x0 + c] = stg[(size_t)y * (TC + 1) + c];
+  if constexpr (TMA_OUT) {
+    const int nbox = (n + 255) / 256;  // rows past n and columns past n are clipped by the map
+    if (threadIdx.x < 32) {
+      fence_proxy_async_smem();  // the transforms' generic stores before this lane's TMA reads
+      for (int k = threadIdx.x; k < nbox; k += 32) tma_store_3d(&omap, x0, k * 256, b, stg + (size_t)k * 256 * SP);
+      bulk_commit_group();
+      bulk_wait_group_read<0>();  // the staging must outlive the reads
+    }
+  } else {
+    float* ob = img + (size_t)b * n * n;
+    const int w = min(TC, n - x0);
+    for (int e = threadIdx.x; e < n * TC; e += blockDim.x) {
+      const int y = e / TC, c = e % TC;
+      if (c < w) ob[(size_t)y * n + x0 + c] = stg[(size_t)y * SP + c];
+    }
   }
+}
+
+// Images [batch][n][n] fp32 as a 3-D tensor {n, n, batch}; box {8, 256, 1}, 32-byte swizzle (grid_y's staging).
+bool encode_image_map(CUtensorMap* map, const float* img, int n, int batch) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)n * 4, (cuuint64_t)n * n * 4};
+  const cuuint32_t box[3] = {8, 256, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(img), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <typename K>
@@ -456,11 +502,13 @@ cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, flo
   {
     constexpr int TC = 8;
     constexpr int GY = G > TC / 2 ? TC / 2 : G;
-    const size_t smem = (((size_t)d.n * (TC + 1) + 1) / 2 + (size_t)GY * padded_len(N)) * sizeof(float2);
-    auto k = k_bst_grid_y<N, TC, GY, GEN>;
+    CUtensorMap om{};
+    const bool tma = (reinterpret_cast<uintptr_t>(img) & 15) == 0 && (d.n % 4) == 0 && encode_image_map(&om, img, d.n, batch);
+    const size_t smem = 1024 + (((size_t)d.n * (tma ? TC : TC + 1) + 1) / 2 + (size_t)GY * padded_len(N)) * sizeof(float2);
+    auto k = tma ? k_bst_grid_y<N, TC, GY, GEN, true> : k_bst_grid_y<N, TC, GY, GEN, false>;
     cudaError_t e = prep(k, smem);
     if (e) return e;
-    k<<<dim3((d.n + TC - 1) / TC, batch), GY * T, smem, s>>>(X, img, d.n, d.p0, d.s_img, d.s_mean, d.fbp,
+    k<<<dim3((d.n + TC - 1) / TC, batch), GY * T, smem, s>>>(om, X, img, d.n, d.p0, d.s_img, d.s_mean, d.fbp,
                                                             d.subtract_mean, acc, tw, ch);
     return cudaGetLastError();
   }
