@@ -205,15 +205,19 @@ k_bst_radial(const float* __restrict__ g, float2* __restrict__ P, int nt, int nt
 // crop mean through cmean (sum over the crop rows of the row's DFT weights).
 // ---------------------------------------------------------------------------
 // GEN: BIG is the Bluestein convolution size and the padded side is ch.len.
-template <int BIG, int TR, int G, bool GEN>
+// TMA_OUT: X leaves by 2-D TMA stores (boxes {TR complex, 256 x}, 3-D map {2 HB floats, n, batch}) from
+// a [n][TR] staging in TMA's 32-byte swizzle (complex (x, r) at x*TR + (r ^ 2*((x >> 2) & 1))).
+template <int BIG, int TR, int G, bool GEN, bool TMA_OUT>
 __global__ void __launch_bounds__(G * FftPlan<BIG, true>::T)
-k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int nsig, int m_pad, int n, int p0,
-             const uint2* __restrict__ gq, int qpitch, const float2* __restrict__ tau,
+k_bst_grid_x(const __grid_constant__ CUtensorMap xmap, const float2* __restrict__ P, float2* __restrict__ X, int nray,
+             int nsig, int m_pad, int n, int p0, const uint2* __restrict__ gq, int qpitch, const float2* __restrict__ tau,
              const float2* __restrict__ cmean, const float2* __restrict__ tw, double* __restrict__ acc, Chirp ch) {
   constexpr int T = FftPlan<BIG, true>::T;
+  static_assert(!TMA_OUT || TR == 4, "32-byte staging rows");
   const int big = GEN ? ch.len : BIG;
   const int HB = big / 2;
-  extern __shared__ __align__(16) float2 smem_b2[];
+  extern __shared__ __align__(16) float2 smem_b2_raw[];
+  float2* smem_b2 = smem_b2_raw + ((1024u - (smem_u32(smem_b2_raw) & 1023u)) & 1023u) / sizeof(float2);
   float2* stg = smem_b2;                                   // [n][TR]
   float2* buf = stg + (size_t)n * TR + (threadIdx.x / T) * padded_len(BIG);
   __shared__ double red[32];
@@ -277,7 +281,7 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
       const int xc = x - p0;
       if (xc >= 0 && xc < n) {
         v = make_float2(v.x * ty.x - v.y * ty.y, v.x * ty.y + v.y * ty.x);
-        stg[(size_t)xc * TR + r] = v;
+        stg[(size_t)xc * TR + (TMA_OUT ? (r ^ (((xc >> 2) & 1) << 1)) : r)] = v;
         rowsum.x += v.x;
         rowsum.y += v.y;
       }
@@ -334,10 +338,20 @@ k_bst_grid_x(const float2* __restrict__ P, float2* __restrict__ X, int nray, int
   const double s = block_sum(mean_part, red);
   if (threadIdx.x == 0) atomicAdd(acc + 2 * b + 1, s);
   __syncthreads();
-  float2* Xb = X + (size_t)b * n * HB;
-  for (int e = threadIdx.x; e < n * TR; e += blockDim.x) {
-    const int xc = e / TR, r = e % TR;
-    if (ky0 + r < HB) Xb[(size_t)xc * HB + ky0 + r] = stg[e];
+  if constexpr (TMA_OUT) {
+    const int nbox = (n + 255) / 256;  // x past n and ky past HB are clipped by the map
+    if (threadIdx.x < 32) {
+      fence_proxy_async_smem();  // the transforms' generic stores before this lane's TMA reads
+      for (int k = threadIdx.x; k < nbox; k += 32) tma_store_3d(&xmap, 2 * ky0, k * 256, b, stg + (size_t)k * 256 * TR);
+      bulk_commit_group();
+      bulk_wait_group_read<0>();  // the staging must outlive the reads
+    }
+  } else {
+    float2* Xb = X + (size_t)b * n * HB;
+    for (int e = threadIdx.x; e < n * TR; e += blockDim.x) {
+      const int xc = e / TR, r = e % TR;
+      if (ky0 + r < HB) Xb[(size_t)xc * HB + ky0 + r] = stg[e];
+    }
   }
 }
 
@@ -425,7 +439,7 @@ k_bst_grid_y(const __grid_constant__ CUtensorMap omap, const float2* __restrict_
 }
 
 // Images [batch][n][n] fp32 as a 3-D tensor {n, n, batch}; box {8, 256, 1}, 32-byte swizzle (grid_y's staging).
-bool encode_image_map(CUtensorMap* map, const float* img, int n, int batch) {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -434,12 +448,30 @@ bool encode_image_map(CUtensorMap* map, const float* img, int n, int batch) {
       p = nullptr;
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }();
+  return enc;
+}
+
+bool encode_image_map(CUtensorMap* map, const float* img, int n, int batch) {
+  auto enc = tensor_encoder();
   if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch};
   const cuuint64_t strides[2] = {(cuuint64_t)n * 4, (cuuint64_t)n * n * 4};
   const cuuint32_t box[3] = {8, 256, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(img), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// X[b][x][ky] (complex, ky pitch hb) as floats {2 hb, n, batch}; box {8 floats = 4 ky, 256 x, 1}, 32-byte swizzle.
+bool encode_spectra_x_map(CUtensorMap* map, const float2* X, int hb, int n, int batch) {
+  auto enc = tensor_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * hb), (cuuint64_t)n, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)hb * 8, (cuuint64_t)hb * 8 * n};
+  const cuuint32_t box[3] = {8, 256, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(X), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -491,11 +523,13 @@ cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, flo
   const float2* tw = GEN ? t.tw_mbbig : t.tw_big;
   const int hb = d.big / 2;
   {
-    const size_t smem = ((size_t)d.n * TR + (size_t)GX * padded_len(N)) * sizeof(float2);
-    auto k = k_bst_grid_x<N, TR, GX, GEN>;
+    CUtensorMap xm{};
+    const bool tma = (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (hb % 2) == 0 && encode_spectra_x_map(&xm, X, hb, d.n, batch);
+    const size_t smem = 1024 + ((size_t)d.n * TR + (size_t)GX * padded_len(N)) * sizeof(float2);
+    auto k = tma ? k_bst_grid_x<N, TR, GX, GEN, true> : k_bst_grid_x<N, TR, GX, GEN, false>;
     cudaError_t e = prep(k, smem);
     if (e) return e;
-    k<<<dim3((hb + TR - 1) / TR, batch), GX * T, smem, s>>>(P, X, d.nray, d.m_need, d.m_pad, d.n, d.p0, t.grid_q,
+    k<<<dim3((hb + TR - 1) / TR, batch), GX * T, smem, s>>>(xm, P, X, d.nray, d.m_need, d.m_pad, d.n, d.p0, t.grid_q,
                                                              hb + 1, t.tau, t.cmean, tw, acc, ch);
     if ((e = cudaGetLastError())) return e;
   }
