@@ -54,10 +54,14 @@ def parse():
     ap.add_argument("--chunk", type=int, default=8, help="slices per internal pipeline chunk (8 x 2 streams measured best)")
     ap.add_argument("--e2e-slices", type=int, default=128)
     ap.add_argument("--e2e-chunk", type=int, default=4)
-    ap.add_argument("--streams", type=int, default=2, help="CUDA streams the device-resident chunks alternate on")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="CUDA streams the device-resident chunks alternate on (0 = 2 for logpolar, 1 for bst: "
+                         "two BST chunks in flight halve the L2 its gridding gathers hit)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = min(cores, memory/2.5GB, 32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--engine", default="logpolar", choices=["logpolar", "bst"],
+                    help="logpolar (the north-star path, default) or bst (fbp's default engine in the reference)")
     return ap.parse_args()
 
 
@@ -172,11 +176,14 @@ def _cpu_worker_many(jobs):
     from oracle import fastbp_oracle as O
     from oracle import phantoms
 
-    inputs = [(phantoms.CONFIGS[cfg], phantoms.config_sinogram(cfg, idx).astype("float64")) for cfg, idx in jobs]
+    inputs = [(phantoms.CONFIGS[cfg], phantoms.config_sinogram(cfg, idx).astype("float64"), eng)
+              for cfg, idx, eng in jobs]
     times = []
-    for c, g in inputs:
+    for c, g, eng in inputs:
         t = time.perf_counter()
-        if c["fbp"]:
+        if eng == "bst":
+            O.fbp_bst(g, c["n"]) if c["fbp"] else O.bst_backproject(g, c["n"])
+        elif c["fbp"]:
             O.fbp_logpolar(g, c["n"])
         else:
             O.logpolar_backproject(g, c["n"])
@@ -195,14 +202,14 @@ def cpu_workers(requested: int) -> int:
     return max(1, min(ncpu, int(avail_gb / 2.5), 32))
 
 
-def cpu_baseline(cfg: int, workers: int, slices_per_worker: int = 1):
+def cpu_baseline(cfg: int, workers: int, slices_per_worker: int = 1, engine: str = "logpolar"):
     """Throughput of the oracle port on `workers` host cores: one process per core,
     all running concurrently, each reconstructing whole slices.  Only the
     reconstruction is timed (each worker generates its input first, untimed):
     throughput = slices / (longest per-worker reconstruction time)."""
     env = {"OMP_NUM_THREADS": "1", "OPENBLAS_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"}
     os.environ.update(env)
-    jobs = [[(cfg, 1000 + w * slices_per_worker + i) for i in range(slices_per_worker)] for w in range(workers)]
+    jobs = [[(cfg, 1000 + w * slices_per_worker + i, engine) for i in range(slices_per_worker)] for w in range(workers)]
     ctx = mp.get_context("spawn")
     with ctx.Pool(workers) as pool:
         per = pool.map(_cpu_worker_many, jobs, chunksize=1)
@@ -296,16 +303,24 @@ def run_ours(a, d: Dist):
     nt, nth, n = c["nt"], c["ntheta"], c["n"]
     S = a.slices or c["slices"]
     spec = (0.0, 1.0) if c["fbp"] else None
-    plan = p.get_plan(nt, nth, n, None, None, spec)
+    bst = a.engine == "bst"
+    plan = p.BstPlan(nt, nth, p.BstOptions(n_out=n), spec) if bst else p.get_plan(nt, nth, n, None, None, spec)
 
     # ---- synthetic inputs, generated on the device (per-slice seeds)
     global_ids = range(d.rank * S, (d.rank + 1) * S)  # weak scaling: S slices per rank
     sino = p.synth.config_batch(a.config, list(global_ids), dev)
     out = torch.empty((S, n, n), dtype=torch.float32, device=dev)
     chunk = min(a.chunk, S)
-    nstreams = max(1, a.streams)
+    nstreams = a.streams if a.streams > 0 else (1 if bst else 2)
     # one workspace per stream: the plan is immutable, chunks on different streams overlap
-    wss = [torch.empty(plan.workspace_bytes(chunk), dtype=torch.uint8, device=dev) for _ in range(nstreams)]
+    wss = [None if bst else torch.empty(plan.workspace_bytes(chunk), dtype=torch.uint8, device=dev)
+           for _ in range(nstreams)]
+
+    def run(x, o, ws):
+        if bst:
+            plan.execute(x, out=o, chunk=chunk)
+        else:
+            plan.execute(x, out=o, workspace=ws)
     streams = [torch.cuda.Stream(dev) for _ in range(nstreams)]
     main = torch.cuda.current_stream(dev)
 
@@ -315,7 +330,7 @@ def run_ours(a, d: Dist):
             st.wait_stream(main)
         for i, k in enumerate(range(0, S, chunk)):
             with torch.cuda.stream(streams[i % nstreams]):
-                plan.execute(sino[k:k + chunk], out=out[k:k + chunk], workspace=wss[i % nstreams])
+                run(sino[k:k + chunk], out[k:k + chunk], wss[i % nstreams])
             n_l += plan.last_launches
         for st in streams:
             main.wait_stream(st)
@@ -342,7 +357,8 @@ def run_ours(a, d: Dist):
     # per-stage breakdown (roofline inputs): one extra, untimed single-stream pass with CUDA
     # events around every launch (overlapping streams would blur per-kernel durations)
     plan.profile(True)
-    plan.execute(sino, out=out, workspace=wss[0])
+    for k in range(0, S, chunk):
+        run(sino[k:k + chunk], out[k:k + chunk], wss[0])
     torch.cuda.synchronize()
     stages = plan.profile_read()
     plan.profile(False)
@@ -353,7 +369,7 @@ def run_ours(a, d: Dist):
 
     # ---- roofline of the dominant kernel (largest share of device time)
     info = plan.info
-    ab = p.algorithmic_bytes(plan)
+    ab = p.roofline.bst_algorithmic_bytes(plan) if bst else p.algorithmic_bytes(plan)
     dom = max(stages, key=lambda k: stages[k]["ms"])
     st = stages[dom]
     per_launch_ms = st["ms"] / max(1, st["launches"])
@@ -362,10 +378,10 @@ def run_ours(a, d: Dist):
     peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
     achieved = bytes_per_launch / (per_launch_ms / 1000.0) / 1e9
-    flops = p.roofline.nominal_flops(plan)
+    flops = p.roofline.bst_nominal_flops(plan) if bst else p.roofline.nominal_flops(plan)
     fp_ach = flops.get(dom, 0.0) * slices_per_launch / (per_launch_ms / 1000.0) / 1e12
     fp_peak = p.roofline.fp32_peak_tflops(float(MEASURED.get("sm_max_mhz", 1965.0)))
-    traffic = TRAFFIC_PER_SLICE.get(dom)
+    traffic = None if bst else TRAFFIC_PER_SLICE.get(dom)
     traffic = traffic * slices_per_launch if traffic else None
     pipe_bytes = sum(ab[k]["per_slice"] for k in ab if k in stages) + sum(
         ab[k]["per_launch"] * stages[k]["launches"] for k in stages) / max(1, S * a.steps)
@@ -375,11 +391,12 @@ def run_ours(a, d: Dist):
     host_in = torch.empty((E, nt, nth), dtype=torch.float32, pin_memory=True)
     host_in.copy_(sino[:E])
     host_out = torch.empty((E, n, n), dtype=torch.float32, pin_memory=True)
-    plan.execute_host(host_in, host_out, chunk=a.e2e_chunk)
+    hin, hout = (host_in.numpy(), host_out.numpy()) if bst else (host_in, host_out)
+    plan.execute_host(hin, hout, chunk=a.e2e_chunk)
     d.barrier()
     t = time.perf_counter()
     for _ in range(a.e2e_steps):
-        plan.execute_host(host_in, host_out, chunk=a.e2e_chunk)
+        plan.execute_host(hin, hout, chunk=a.e2e_chunk)
     e2e_s = d.max(time.perf_counter() - t)
     e2e_value = d.sum(E * a.e2e_steps) / e2e_s
     copy_value = copy_ceiling(host_in, host_out, a.e2e_chunk, a.e2e_steps, d)
@@ -387,26 +404,28 @@ def run_ours(a, d: Dist):
     cpu = None
     if d.rank == 0 and a.gpus == 1 and not a.no_cpu_baseline:
         w = cpu_workers(a.cpu_workers)
-        v, busy, per = cpu_baseline(a.config, w, 1)
+        v, busy, per = cpu_baseline(a.config, w, 1, a.engine)
         cpu = {"value": v, "unit": UNIT, "cores": w, "kind": "port",
                "sample": f"{w} config-{a.config} slices, one per concurrent worker process (reconstruction only, "
                          f"slowest worker {busy:.1f} s, mean {np.mean(per):.2f} s/slice/core), "
-                         f"oracle/fastbp_oracle.py, CPU {cpu_model()}"}
+                         f"oracle/fastbp_oracle.py ({'fbp_bst' if bst else 'fbp_logpolar'}), CPU {cpu_model()}"}
 
     if d.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (device-generated seeded random-ellipse sinograms, K=50, 1% Gaussian noise)",
-            "config": {"workload": workload_name(a.config, c),
-                       "slices_per_rank": S, "chunk": chunk, "streams": nstreams,
-                       "parallelism": f"slice-shard x{d.world}",
-                       "l2": "no flush: 34 GB input per step >> 126 MB L2",
-                       "nrho": info["nrho"], "L": info["L"], "nphi": info["nphi"]},
+            "config": dict({"workload": workload_name(a.config, c) + (" (BST engine)" if bst else ""),
+                            "slices_per_rank": S, "chunk": chunk, "streams": nstreams,
+                            "parallelism": f"slice-shard x{d.world}",
+                            "l2": "no flush: 34 GB input per step >> 126 MB L2"},
+                           **({"engine": "bst", "L": info["L"], "big": info["big"], "m_need": info["m_need"]} if bst
+                              else {"nrho": info["nrho"], "L": info["L"], "nphi": info["nphi"]})),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": per_launch_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                         "traffic_note": None if not bst else "no ncu capture of the BST kernels in this bench",
                          "fp32_pipe": {"achieved_tflops": fp_ach, "peak_tflops": fp_peak, "frac": fp_ach / fp_peak,
                                        "note": "nominal FFT flops (5 N log2 N) of the kernel / launch time vs "
                                                "148 SMs x 128 lanes x 2 x clock; FFT stages are FP32-pipe bound"}},
@@ -415,7 +434,8 @@ def run_ours(a, d: Dist):
                          "hbm_equiv_gbs": pipe_bytes * value / d.world / 1e9,
                          "hbm_equiv_frac": pipe_bytes * value / d.world / 1e9 / peak},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": E * nt * nth * 4,
-                    "d2h_bytes_per_step": E * n * n * 4, "slices_per_step": E, "api": "LogPolarPlan.execute_host",
+                    "d2h_bytes_per_step": E * n * n * 4, "slices_per_step": E,
+                    "api": "BstPlan.execute_host" if bst else "LogPolarPlan.execute_host",
                     "copy_ceiling": copy_value, "frac_of_copy_ceiling": e2e_value / copy_value,
                     "copy_ceiling_note": "same bytes, same chunking, H2D and D2H alone on two streams, no compute"},
             "gpu_launches": launches,

@@ -206,6 +206,12 @@ int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan);
 void lpbp_bst_plan_destroy(lpbp_bst_plan* plan);
 int lpbp_bst_get_info(const lpbp_bst_plan* plan, lpbp_bst_info* info);
 int lpbp_bst_workspace_bytes(const lpbp_bst_plan* plan, int32_t chunk, size_t* bytes);
+/* Per-stage CUDA-event timing of lpbp_bst_execute / _execute_host (stages: 0 ramp filter (fbp
+ * plans), 1 radial spectra, 2 gridding + inverse DFT along x, 3 inverse DFT along y + crop);
+ * lpbp_bst_profile_read waits for the events, returns the sums since the last read and resets. */
+int lpbp_bst_profile_enable(lpbp_bst_plan* plan, int32_t enable);
+int lpbp_bst_profile_read(lpbp_bst_plan* plan, double* stage_ms, int64_t* stage_launches, int64_t* stage_slices,
+                          int32_t nstages);
 /* sino [batch][nt][ntheta] -> img [batch][n][n]; ws NULL = plan-owned workspace. */
 int lpbp_bst_execute(lpbp_bst_plan* plan, const float* sino_dev, float* img_dev, int32_t batch, void* ws,
                      size_t ws_bytes, void* stream);

@@ -92,6 +92,9 @@ SIGNATURES = {
     "lpbp_naive_backproject": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "lpbp_plan_table": (c_int32, [c_void_p, c_char_p, c_void_p, c_size_t, POINTER(c_size_t)]),
     "lpbp_profile_enable": (c_int32, [c_void_p, c_int32]),
+    "lpbp_bst_profile_enable": (c_int32, [c_void_p, c_int32]),
+    "lpbp_bst_profile_read": (c_int32, [c_void_p, POINTER(ctypes.c_double), POINTER(c_int64), POINTER(c_int64),
+                                        c_int32]),
     "lpbp_profile_read": (c_int32, [c_void_p, POINTER(ctypes.c_double), POINTER(c_int64), POINTER(c_int64), c_int32]),
     "lpbp_radon_ellipses": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "lpbp_radon_ellipses_f64": (c_int32, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),

@@ -15,6 +15,7 @@ from __future__ import annotations
 import math
 import threading
 from collections import OrderedDict
+import ctypes
 from ctypes import byref, c_size_t, c_void_p
 from dataclasses import dataclass
 
@@ -90,6 +91,22 @@ class BstPlan:
         v = c_size_t()
         check(lib().lpbp_bst_workspace_bytes(self._h, int(chunk), byref(v)))
         return v.value
+
+    STAGES = ("ramp_filter", "bst_radial", "bst_grid_x", "bst_grid_y")
+
+    def profile(self, enable: bool) -> None:
+        """Record CUDA events around every stage launch (on the launching stream)."""
+        check(lib().lpbp_bst_profile_enable(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{stage: {"ms", "launches", "slices"}} summed since the last read (waits for the events)."""
+        n = len(self.STAGES)
+        ms = (ctypes.c_double * n)()
+        launches = (ctypes.c_int64 * n)()
+        slices = (ctypes.c_int64 * n)()
+        check(lib().lpbp_bst_profile_read(self._h, ms, launches, slices, n))
+        return {name: {"ms": ms[i], "launches": launches[i], "slices": slices[i]}
+                for i, name in enumerate(self.STAGES) if launches[i]}
 
     def _check_sino(self, sino: torch.Tensor) -> torch.Tensor:
         _require_cuda(sino)

@@ -513,7 +513,7 @@ cudaError_t radial_impl(const BstDims& d, const BstTables& t, const float* g, fl
 
 template <int N, bool GEN>
 cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, float2* X, float* img, double* acc,
-                      int batch, cudaStream_t s) {
+                      int batch, cudaStream_t s, cudaEvent_t mid) {
   constexpr int T = FftPlan<N, true>::T;
   constexpr int G = T >= 256 ? (GEN ? 1 : 2) : 4;
   constexpr int TR = 4;
@@ -532,6 +532,7 @@ cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, flo
     k<<<dim3((hb + TR - 1) / TR, batch), GX * T, smem, s>>>(xm, P, X, d.nray, d.m_need, d.m_pad, d.n, d.p0, t.grid_q,
                                                              hb + 1, t.tau, t.cmean, tw, acc, ch);
     if ((e = cudaGetLastError())) return e;
+    if (mid) cudaEventRecord(mid, s);  // profiling: between grid_x and grid_y
   }
   {
     constexpr int TC = 8;
@@ -573,25 +574,25 @@ cudaError_t launch_bst_radial(const BstDims& d, const BstTables& t, const float*
 }
 
 cudaError_t launch_bst_grid(const BstDims& d, const BstTables& t, const float2* P, float2* X, float* img, double* acc,
-                            int batch, cudaStream_t s) {
+                            int batch, cudaStream_t s, cudaEvent_t mid) {
   if (d.mb_big > 0) {  // Bluestein (padded side not a power of two)
     switch (d.mb_big) {
-      case 256: return grid_impl<256, true>(d, t, P, X, img, acc, batch, s);
-      case 512: return grid_impl<512, true>(d, t, P, X, img, acc, batch, s);
-      case 1024: return grid_impl<1024, true>(d, t, P, X, img, acc, batch, s);
-      case 2048: return grid_impl<2048, true>(d, t, P, X, img, acc, batch, s);
-      case 4096: return grid_impl<4096, true>(d, t, P, X, img, acc, batch, s);
-      case 8192: return grid_impl<8192, true>(d, t, P, X, img, acc, batch, s);
+      case 256: return grid_impl<256, true>(d, t, P, X, img, acc, batch, s, mid);
+      case 512: return grid_impl<512, true>(d, t, P, X, img, acc, batch, s, mid);
+      case 1024: return grid_impl<1024, true>(d, t, P, X, img, acc, batch, s, mid);
+      case 2048: return grid_impl<2048, true>(d, t, P, X, img, acc, batch, s, mid);
+      case 4096: return grid_impl<4096, true>(d, t, P, X, img, acc, batch, s, mid);
+      case 8192: return grid_impl<8192, true>(d, t, P, X, img, acc, batch, s, mid);
       default: return cudaErrorNotSupported;
     }
   }
   switch (d.big) {
-    case 128: return grid_impl<128, false>(d, t, P, X, img, acc, batch, s);
-    case 256: return grid_impl<256, false>(d, t, P, X, img, acc, batch, s);
-    case 512: return grid_impl<512, false>(d, t, P, X, img, acc, batch, s);
-    case 1024: return grid_impl<1024, false>(d, t, P, X, img, acc, batch, s);
-    case 2048: return grid_impl<2048, false>(d, t, P, X, img, acc, batch, s);
-    case 4096: return grid_impl<4096, false>(d, t, P, X, img, acc, batch, s);
+    case 128: return grid_impl<128, false>(d, t, P, X, img, acc, batch, s, mid);
+    case 256: return grid_impl<256, false>(d, t, P, X, img, acc, batch, s, mid);
+    case 512: return grid_impl<512, false>(d, t, P, X, img, acc, batch, s, mid);
+    case 1024: return grid_impl<1024, false>(d, t, P, X, img, acc, batch, s, mid);
+    case 2048: return grid_impl<2048, false>(d, t, P, X, img, acc, batch, s, mid);
+    case 4096: return grid_impl<4096, false>(d, t, P, X, img, acc, batch, s, mid);
     default: return cudaErrorNotSupported;
   }
 }

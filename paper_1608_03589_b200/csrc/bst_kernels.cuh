@@ -37,7 +37,8 @@ struct BstDims {
 cudaError_t launch_bst_radial(const BstDims& d, const BstTables& t, const float* g, float2* P, double* acc, int batch,
                               cudaStream_t s);
 // X: [B][n][big/2] complex workspace; img: [B][n][n]
+// mid (optional): recorded on s between the grid_x and grid_y launches (stage profiling)
 cudaError_t launch_bst_grid(const BstDims& d, const BstTables& t, const float2* P, float2* X, float* img, double* acc,
-                            int batch, cudaStream_t s);
+                            int batch, cudaStream_t s, cudaEvent_t mid = nullptr);
 
 }  // namespace lpbp

@@ -1040,10 +1040,47 @@ struct lpbp_bst_plan {
   std::mutex mu;
   void* own_ws = nullptr;
   size_t own_ws_bytes = 0;
-  int host_chunk = 0;
-  float* d_in = nullptr;
-  float* d_out = nullptr;
-  cudaStream_t s_host = nullptr;
+  // host pipeline (lpbp_bst_execute_host): two staging slots, H2D / compute / D2H on three streams
+  struct Pipe {
+    int chunk = 0;
+    float* in[2] = {nullptr, nullptr};
+    float* out[2] = {nullptr, nullptr};
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  } pipe;
+  void release_pipe() {
+    for (int i = 0; i < 2; ++i) {
+      if (pipe.in[i]) cudaFree(pipe.in[i]);
+      if (pipe.out[i]) cudaFree(pipe.out[i]);
+      if (pipe.ev_in[i]) cudaEventDestroy(pipe.ev_in[i]);
+      if (pipe.ev_comp[i]) cudaEventDestroy(pipe.ev_comp[i]);
+      if (pipe.ev_out[i]) cudaEventDestroy(pipe.ev_out[i]);
+    }
+    if (pipe.ws) cudaFree(pipe.ws);
+    if (pipe.s_in) cudaStreamDestroy(pipe.s_in);
+    if (pipe.s_comp) cudaStreamDestroy(pipe.s_comp);
+    if (pipe.s_out) cudaStreamDestroy(pipe.s_out);
+    pipe = Pipe{};
+  }
+  // optional per-stage CUDA-event profiling (lpbp_bst_profile_enable / _read):
+  // ev[0..4] = before ramp, before radial, before grid_x, between grid_x and grid_y, after grid_y
+  struct Rec { int slices; bool ramp; cudaEvent_t ev[5]; };
+  bool profiling = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  std::mutex prof_mu;
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
   template <typename T>
   int upload(const std::vector<T>& v, const void** dst) {
     void* p = nullptr;
@@ -1073,11 +1110,12 @@ struct lpbp_bst_plan {
   }
   ~lpbp_bst_plan() {
     DeviceGuard g(device);
+    release_pipe();
+    for (auto& r : recs)
+      for (cudaEvent_t e : r.ev) ev_pool.push_back(e);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (own_ws) cudaFree(own_ws);
-    if (d_in) cudaFree(d_in);
-    if (d_out) cudaFree(d_out);
-    if (s_host) cudaStreamDestroy(s_host);
   }
 };
 
@@ -1113,7 +1151,17 @@ int bst_chunk(const lpbp_bst_plan* P, const float* in, float* out, int c, char* 
   cudaError_t e = cudaMemsetAsync(acc, 0, (size_t)c * 2 * sizeof(double), st);
   if (e) return cuda_fail(e, "bst acc");
   const float* src = in;
+  lpbp_bst_plan* Pm = const_cast<lpbp_bst_plan*>(P);
+  std::unique_lock<std::mutex> plk(Pm->prof_mu, std::defer_lock);
+  lpbp_bst_plan::Rec rec{c, false, {}};
+  const bool prof = Pm->profiling && !spectra_only;
+  if (prof) {
+    plk.lock();
+    for (auto& ev : rec.ev) ev = Pm->take_event();
+    cudaEventRecord(rec.ev[0], st);
+  }
   if (h.p.filter && !spectra_only) {
+    rec.ramp = true;
     e = lpbp::launch_ramp(P->rd, P->rt, in, filt, c, st);  // column tiles need ntheta % TC == 0
     if (e == cudaErrorNotSupported) {
       (void)cudaGetLastError();
@@ -1123,19 +1171,62 @@ int bst_chunk(const lpbp_bst_plan* P, const float* in, float* out, int c, char* 
     ++g_launches;
     src = filt;
   }
+  if (prof) cudaEventRecord(rec.ev[1], st);
   e = lpbp::launch_bst_radial(P->d, P->t, src, Pw, acc, c, st);
   if (e) return launch_fail(e, "bst_radial");
   ++g_launches;
   if (spectra_only) return LPBP_OK;
-  e = lpbp::launch_bst_grid(P->d, P->t, Pw, Xw, out, acc, c, st);
+  if (prof) cudaEventRecord(rec.ev[2], st);
+  e = lpbp::launch_bst_grid(P->d, P->t, Pw, Xw, out, acc, c, st, prof ? rec.ev[3] : nullptr);
   if (e) return launch_fail(e, "bst_grid");
   g_launches += 2;
+  if (prof) {
+    cudaEventRecord(rec.ev[4], st);
+    Pm->recs.push_back(rec);
+  }
   return LPBP_OK;
 }
 
 }  // namespace
 
 extern "C" {
+
+int lpbp_bst_profile_enable(lpbp_bst_plan* P, int32_t enable) {
+  if (!P) return fail(LPBP_EINVAL, "invalid argument");
+  std::lock_guard<std::mutex> lk(P->prof_mu);
+  P->profiling = enable != 0;
+  return LPBP_OK;
+}
+
+int lpbp_bst_profile_read(lpbp_bst_plan* P, double* stage_ms, int64_t* stage_launches, int64_t* stage_slices,
+                          int32_t nstages) {
+  constexpr int kBstStages = 4;  // ramp filter, radial, grid_x, grid_y
+  if (!P || !stage_ms || !stage_launches || !stage_slices || nstages < kBstStages)
+    return fail(LPBP_EINVAL, "invalid argument");
+  DeviceGuard g(P->device);
+  std::lock_guard<std::mutex> lk(P->prof_mu);
+  for (int i = 0; i < nstages; ++i) {
+    stage_ms[i] = 0;
+    stage_launches[i] = 0;
+    stage_slices[i] = 0;
+  }
+  int rc = LPBP_OK;
+  for (auto& r : P->recs) {
+    cudaError_t e = cudaEventSynchronize(r.ev[4]);
+    for (int k = 0; k < kBstStages; ++k) {
+      if (k == 0 && !r.ramp) continue;
+      float ms = 0.f;
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.ev[k], r.ev[k + 1]);
+      stage_ms[k] += ms;
+      stage_launches[k] += 1;
+      stage_slices[k] += r.slices;
+    }
+    if (e != cudaSuccess && rc == LPBP_OK) rc = cuda_fail(e, "bst profile_read");
+    for (cudaEvent_t ev : r.ev) P->ev_pool.push_back(ev);
+  }
+  P->recs.clear();
+  return rc;
+}
 
 int lpbp_bst_plan_create(const lpbp_bst_params* params, lpbp_bst_plan** plan) {
   g_last_error.clear();
@@ -1318,35 +1409,56 @@ int lpbp_bst_execute_host(lpbp_bst_plan* P, const float* sino_host, float* img_h
   if (chunk <= 0) chunk = 4;
   chunk = std::min(chunk, batch);
   DeviceGuard g(P->device);
+  std::lock_guard<std::mutex> lk(P->mu);
+  auto& pp = P->pipe;
   const size_t in_slice = (size_t)P->h.p.nt * P->h.p.ntheta, out_slice = (size_t)P->h.p.n * P->h.p.n;
-  {
-    std::lock_guard<std::mutex> lk(P->mu);
-    if (P->host_chunk < chunk) {
-      if (P->d_in) cudaFree(P->d_in);
-      if (P->d_out) cudaFree(P->d_out);
-      P->d_in = P->d_out = nullptr;
-      P->host_chunk = 0;
-      cudaError_t e = cudaMalloc(&P->d_in, in_slice * chunk * sizeof(float));
-      if (e == cudaSuccess) e = cudaMalloc(&P->d_out, out_slice * chunk * sizeof(float));
-      if (e == cudaSuccess && !P->s_host) e = cudaStreamCreateWithFlags(&P->s_host, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return cuda_fail(e, "bst host staging");
-      P->host_chunk = chunk;
+  if (pp.chunk < chunk) {  // chunk k+1's H2D and chunk k-1's D2H run beside chunk k's kernels
+    P->release_pipe();
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaMalloc(&pp.in[i], in_slice * chunk * sizeof(float));
+      if (e == cudaSuccess) e = cudaMalloc(&pp.out[i], out_slice * chunk * sizeof(float));
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_in[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_comp[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_out[i], cudaEventDisableTiming);
     }
+    pp.ws_bytes = bst_ws_bytes(P, chunk);
+    if (e == cudaSuccess) e = cudaMalloc(&pp.ws, pp.ws_bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_comp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_out, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      P->release_pipe();
+      return cuda_fail(e, "bst host pipeline setup");
+    }
+    pp.chunk = chunk;
   }
   int64_t launches = 0;
-  for (int off = 0; off < batch; off += chunk) {
+  const int nchunks = (batch + chunk - 1) / chunk;
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int slot = ci & 1;
+    const int off = ci * chunk;
     const int c = std::min(chunk, batch - off);
-    cudaError_t e = cudaMemcpyAsync(P->d_in, sino_host + off * in_slice, in_slice * c * sizeof(float),
-                                    cudaMemcpyHostToDevice, P->s_host);
+    if (ci >= 2) cudaStreamWaitEvent(pp.s_in, pp.ev_comp[slot], 0);  // slot's previous input consumed
+    cudaError_t e = cudaMemcpyAsync(pp.in[slot], sino_host + (size_t)off * in_slice, in_slice * c * sizeof(float),
+                                    cudaMemcpyHostToDevice, pp.s_in);
     if (e) return cuda_fail(e, "H2D");
-    int rc = lpbp_bst_execute(P, P->d_in, P->d_out, c, nullptr, 0, P->s_host);
+    cudaEventRecord(pp.ev_in[slot], pp.s_in);
+    cudaStreamWaitEvent(pp.s_comp, pp.ev_in[slot], 0);
+    if (ci >= 2) cudaStreamWaitEvent(pp.s_comp, pp.ev_out[slot], 0);  // slot's previous output copied out
+    const int64_t before = g_launches;
+    const int rc = bst_chunk(P, pp.in[slot], pp.out[slot], c, static_cast<char*>(pp.ws), pp.s_comp, nullptr);
     if (rc) return rc;
-    launches += g_launches;
-    e = cudaMemcpyAsync(img_host + off * out_slice, P->d_out, out_slice * c * sizeof(float), cudaMemcpyDeviceToHost,
-                        P->s_host);
+    launches += g_launches - before;
+    cudaEventRecord(pp.ev_comp[slot], pp.s_comp);
+    cudaStreamWaitEvent(pp.s_out, pp.ev_comp[slot], 0);
+    e = cudaMemcpyAsync(img_host + (size_t)off * out_slice, pp.out[slot], out_slice * c * sizeof(float),
+                        cudaMemcpyDeviceToHost, pp.s_out);
     if (e) return cuda_fail(e, "D2H");
+    cudaEventRecord(pp.ev_out[slot], pp.s_out);
   }
-  cudaError_t e = cudaStreamSynchronize(P->s_host);
+  cudaError_t e = cudaStreamSynchronize(pp.s_out);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(pp.s_comp);
   if (e) return cuda_fail(e, "bst execute_host sync");
   g_launches = launches;
   return LPBP_OK;

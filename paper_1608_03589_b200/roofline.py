@@ -58,3 +58,35 @@ def nominal_flops(plan) -> dict:
         "rho_conv": nh * (2 * f(L) + 6 * L),
         "irdft_readout": (nrho / 2) * f(nphi),
     }
+
+
+def bst_algorithmic_bytes(plan) -> dict:
+    """{stage: {"per_slice", "per_launch"}} for a BstPlan: each stage reads its input once and
+    writes its output once.  Radial: sinogram in, ray-pair spectra P [(nray/2 + 2)][m_pad] float4
+    out; grid_x: P in (each bin once), X [n][big/2] complex out; grid_y: X in, image out."""
+    i = plan.info
+    nt, nth, n = plan.nt, plan.ntheta, plan.n_out
+    sino = nt * nth * 4
+    P = (i["nray"] // 2 + 2) * i["m_pad"] * 16
+    X = n * (i["big"] // 2) * 8
+    img = n * n * 4
+    return {
+        "ramp_filter": {"per_slice": 2 * sino, "per_launch": 0},
+        "bst_radial": {"per_slice": sino + P, "per_launch": 0},
+        "bst_grid_x": {"per_slice": P + X, "per_launch": 0},
+        "bst_grid_y": {"per_slice": X + img, "per_launch": 0},
+    }
+
+
+def bst_nominal_flops(plan) -> dict:
+    """Nominal FFT flops per slice of the BST stages (5 N log2 N per complex FFT)."""
+    import math
+
+    i = plan.info
+    f = lambda n: 5.0 * n * math.log2(n)  # noqa: E731
+    L, big, n = i["L"], i["big"], plan.n_out
+    return {
+        "bst_radial": plan.ntheta * f(L),        # one packed (+s, -s) FFT per angle
+        "bst_grid_x": (big // 2) * f(big),       # rows ky < big/2
+        "bst_grid_y": (n / 2) * f(big),          # packed column pairs
+    }
