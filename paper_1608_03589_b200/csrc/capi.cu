@@ -704,6 +704,96 @@ int lpbp_radon_ellipses_host(const double* params, int32_t k, int32_t nt, int32_
 // ---------------------------------------------------------------------------
 }  // extern "C"
 
+// Host-to-host pipeline shared by the sector and BST plans: two device staging slots, chunk k+1's
+// H2D and chunk k-1's D2H on their own streams beside chunk k's kernels (the log-polar plan's
+// lpbp_execute_host does the same with its own workspace layout).
+struct HostPipe {
+  int chunk = 0;
+  size_t ws_bytes = 0;
+  float* in[2] = {nullptr, nullptr};
+  float* out[2] = {nullptr, nullptr};
+  void* ws = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  std::mutex mu;
+  void release() {  // the owner's device must be current
+    for (int i = 0; i < 2; ++i) {
+      if (in[i]) cudaFree(in[i]);
+      if (out[i]) cudaFree(out[i]);
+      if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+      if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
+      if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+      in[i] = out[i] = nullptr;
+      ev_in[i] = ev_comp[i] = ev_out[i] = nullptr;
+    }
+    if (ws) cudaFree(ws);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_comp) cudaStreamDestroy(s_comp);
+    if (s_out) cudaStreamDestroy(s_out);
+    ws = nullptr;
+    s_in = s_comp = s_out = nullptr;
+    chunk = 0;
+    ws_bytes = 0;
+  }
+};
+
+// run(in_dev, out_dev, c, ws, ws_bytes, stream) -> LPBP status; counts its launches in g_launches
+template <typename Run>
+int host_pipeline(HostPipe& pp, int batch, int chunk, size_t in_slice, size_t out_slice, size_t ws_bytes,
+                  const float* sino_host, float* img_host, Run&& run) {
+  std::lock_guard<std::mutex> lk(pp.mu);
+  if (pp.chunk < chunk || pp.ws_bytes < ws_bytes) {
+    pp.release();
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaMalloc(&pp.in[i], in_slice * chunk * sizeof(float));
+      if (e == cudaSuccess) e = cudaMalloc(&pp.out[i], out_slice * chunk * sizeof(float));
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_in[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_comp[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_out[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&pp.ws, ws_bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_comp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_out, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      pp.release();
+      return cuda_fail(e, "host pipeline setup");
+    }
+    pp.chunk = chunk;
+    pp.ws_bytes = ws_bytes;
+  }
+  int64_t launches = 0;
+  const int nchunks = (batch + chunk - 1) / chunk;
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int slot = ci & 1;
+    const int off = ci * chunk;
+    const int c = std::min(chunk, batch - off);
+    if (ci >= 2) cudaStreamWaitEvent(pp.s_in, pp.ev_comp[slot], 0);  // slot's previous input consumed
+    cudaError_t e = cudaMemcpyAsync(pp.in[slot], sino_host + (size_t)off * in_slice, in_slice * c * sizeof(float),
+                                    cudaMemcpyHostToDevice, pp.s_in);
+    if (e) return cuda_fail(e, "H2D");
+    cudaEventRecord(pp.ev_in[slot], pp.s_in);
+    cudaStreamWaitEvent(pp.s_comp, pp.ev_in[slot], 0);
+    if (ci >= 2) cudaStreamWaitEvent(pp.s_comp, pp.ev_out[slot], 0);  // slot's previous output copied out
+    g_launches = 0;
+    const int rc = run(pp.in[slot], pp.out[slot], c, pp.ws, pp.ws_bytes, pp.s_comp);
+    if (rc) return rc;
+    launches += g_launches;
+    cudaEventRecord(pp.ev_comp[slot], pp.s_comp);
+    cudaStreamWaitEvent(pp.s_out, pp.ev_comp[slot], 0);
+    e = cudaMemcpyAsync(img_host + (size_t)off * out_slice, pp.out[slot], out_slice * c * sizeof(float),
+                        cudaMemcpyDeviceToHost, pp.s_out);
+    if (e) return cuda_fail(e, "D2H");
+    cudaEventRecord(pp.ev_out[slot], pp.s_out);
+  }
+  cudaError_t e = cudaStreamSynchronize(pp.s_out);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(pp.s_comp);
+  if (e) return cuda_fail(e, "execute_host sync");
+  g_launches = launches;
+  return LPBP_OK;
+}
+
 struct lpbp_sector_plan {
   lpbp::SectorSetHost h;
   // log-polar stage per sector (explicit rho0, no filter).  Sectors whose meshes coincide
@@ -720,19 +810,13 @@ struct lpbp_sector_plan {
   std::mutex mu;
   void* own_ws = nullptr;
   size_t own_ws_bytes = 0;
-  // host path: device staging for `host_chunk` slices and a stream
-  int host_chunk = 0;
-  float* d_in = nullptr;
-  float* d_out = nullptr;
-  cudaStream_t s_host = nullptr;
+  HostPipe pipe;  // host path (lpbp_sector_execute_host)
   ~lpbp_sector_plan() {
     DeviceGuard g(device);
+    pipe.release();
     for (auto* p : owned) delete p;
     for (void* p : allocs) cudaFree(p);
     if (own_ws) cudaFree(own_ws);
-    if (d_in) cudaFree(d_in);
-    if (d_out) cudaFree(d_out);
-    if (s_host) cudaStreamDestroy(s_host);
   }
 };
 
@@ -966,37 +1050,10 @@ int lpbp_sector_execute_host(lpbp_sector_plan* P, const float* sino_host, float*
   chunk = std::min(chunk, batch);
   DeviceGuard g(P->device);
   const size_t in_slice = (size_t)P->h.nt * P->h.ntheta, out_slice = (size_t)P->h.n * P->h.n;
-  {
-    std::lock_guard<std::mutex> lk(P->mu);
-    if (P->host_chunk < chunk) {
-      if (P->d_in) cudaFree(P->d_in);
-      if (P->d_out) cudaFree(P->d_out);
-      P->d_in = P->d_out = nullptr;
-      P->host_chunk = 0;
-      cudaError_t e = cudaMalloc(&P->d_in, in_slice * chunk * sizeof(float));
-      if (e == cudaSuccess) e = cudaMalloc(&P->d_out, out_slice * chunk * sizeof(float));
-      if (e == cudaSuccess && !P->s_host) e = cudaStreamCreateWithFlags(&P->s_host, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return cuda_fail(e, "sector host staging");
-      P->host_chunk = chunk;
-    }
-  }
-  int64_t launches = 0;
-  for (int off = 0; off < batch; off += chunk) {
-    const int c = std::min(chunk, batch - off);
-    cudaError_t e = cudaMemcpyAsync(P->d_in, sino_host + off * in_slice, in_slice * c * sizeof(float),
-                                    cudaMemcpyHostToDevice, P->s_host);
-    if (e) return cuda_fail(e, "H2D");
-    int rc = lpbp_sector_execute(P, P->d_in, P->d_out, c, nullptr, 0, P->s_host);
-    if (rc) return rc;
-    launches += g_launches;
-    e = cudaMemcpyAsync(img_host + off * out_slice, P->d_out, out_slice * c * sizeof(float), cudaMemcpyDeviceToHost,
-                        P->s_host);
-    if (e) return cuda_fail(e, "D2H");
-  }
-  cudaError_t e = cudaStreamSynchronize(P->s_host);
-  if (e) return cuda_fail(e, "sector execute_host sync");
-  g_launches = launches;
-  return LPBP_OK;
+  return host_pipeline(P->pipe, batch, chunk, in_slice, out_slice, sector_ws_bytes(P, chunk), sino_host, img_host,
+                       [&](const float* in, float* out, int c, void* ws, size_t wsb, cudaStream_t st) {
+                         return lpbp_sector_execute(P, in, out, c, ws, wsb, st);
+                       });
 }
 
 int lpbp_sector_prepare(const lpbp_sector_plan* P, int32_t index, const float* sino_dev, float* out_dev,
@@ -1040,30 +1097,7 @@ struct lpbp_bst_plan {
   std::mutex mu;
   void* own_ws = nullptr;
   size_t own_ws_bytes = 0;
-  // host pipeline (lpbp_bst_execute_host): two staging slots, H2D / compute / D2H on three streams
-  struct Pipe {
-    int chunk = 0;
-    float* in[2] = {nullptr, nullptr};
-    float* out[2] = {nullptr, nullptr};
-    void* ws = nullptr;
-    size_t ws_bytes = 0;
-    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
-    cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
-  } pipe;
-  void release_pipe() {
-    for (int i = 0; i < 2; ++i) {
-      if (pipe.in[i]) cudaFree(pipe.in[i]);
-      if (pipe.out[i]) cudaFree(pipe.out[i]);
-      if (pipe.ev_in[i]) cudaEventDestroy(pipe.ev_in[i]);
-      if (pipe.ev_comp[i]) cudaEventDestroy(pipe.ev_comp[i]);
-      if (pipe.ev_out[i]) cudaEventDestroy(pipe.ev_out[i]);
-    }
-    if (pipe.ws) cudaFree(pipe.ws);
-    if (pipe.s_in) cudaStreamDestroy(pipe.s_in);
-    if (pipe.s_comp) cudaStreamDestroy(pipe.s_comp);
-    if (pipe.s_out) cudaStreamDestroy(pipe.s_out);
-    pipe = Pipe{};
-  }
+  HostPipe pipe;  // host path (lpbp_bst_execute_host)
   // optional per-stage CUDA-event profiling (lpbp_bst_profile_enable / _read):
   // ev[0..4] = before ramp, before radial, before grid_x, between grid_x and grid_y, after grid_y
   struct Rec { int slices; bool ramp; cudaEvent_t ev[5]; };
@@ -1110,7 +1144,7 @@ struct lpbp_bst_plan {
   }
   ~lpbp_bst_plan() {
     DeviceGuard g(device);
-    release_pipe();
+    pipe.release();
     for (auto& r : recs)
       for (cudaEvent_t e : r.ev) ev_pool.push_back(e);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
@@ -1409,59 +1443,11 @@ int lpbp_bst_execute_host(lpbp_bst_plan* P, const float* sino_host, float* img_h
   if (chunk <= 0) chunk = 4;
   chunk = std::min(chunk, batch);
   DeviceGuard g(P->device);
-  std::lock_guard<std::mutex> lk(P->mu);
-  auto& pp = P->pipe;
   const size_t in_slice = (size_t)P->h.p.nt * P->h.p.ntheta, out_slice = (size_t)P->h.p.n * P->h.p.n;
-  if (pp.chunk < chunk) {  // chunk k+1's H2D and chunk k-1's D2H run beside chunk k's kernels
-    P->release_pipe();
-    cudaError_t e = cudaSuccess;
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
-      e = cudaMalloc(&pp.in[i], in_slice * chunk * sizeof(float));
-      if (e == cudaSuccess) e = cudaMalloc(&pp.out[i], out_slice * chunk * sizeof(float));
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_in[i], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_comp[i], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_out[i], cudaEventDisableTiming);
-    }
-    pp.ws_bytes = bst_ws_bytes(P, chunk);
-    if (e == cudaSuccess) e = cudaMalloc(&pp.ws, pp.ws_bytes);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_in, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_comp, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.s_out, cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
-      P->release_pipe();
-      return cuda_fail(e, "bst host pipeline setup");
-    }
-    pp.chunk = chunk;
-  }
-  int64_t launches = 0;
-  const int nchunks = (batch + chunk - 1) / chunk;
-  for (int ci = 0; ci < nchunks; ++ci) {
-    const int slot = ci & 1;
-    const int off = ci * chunk;
-    const int c = std::min(chunk, batch - off);
-    if (ci >= 2) cudaStreamWaitEvent(pp.s_in, pp.ev_comp[slot], 0);  // slot's previous input consumed
-    cudaError_t e = cudaMemcpyAsync(pp.in[slot], sino_host + (size_t)off * in_slice, in_slice * c * sizeof(float),
-                                    cudaMemcpyHostToDevice, pp.s_in);
-    if (e) return cuda_fail(e, "H2D");
-    cudaEventRecord(pp.ev_in[slot], pp.s_in);
-    cudaStreamWaitEvent(pp.s_comp, pp.ev_in[slot], 0);
-    if (ci >= 2) cudaStreamWaitEvent(pp.s_comp, pp.ev_out[slot], 0);  // slot's previous output copied out
-    const int64_t before = g_launches;
-    const int rc = bst_chunk(P, pp.in[slot], pp.out[slot], c, static_cast<char*>(pp.ws), pp.s_comp, nullptr);
-    if (rc) return rc;
-    launches += g_launches - before;
-    cudaEventRecord(pp.ev_comp[slot], pp.s_comp);
-    cudaStreamWaitEvent(pp.s_out, pp.ev_comp[slot], 0);
-    e = cudaMemcpyAsync(img_host + (size_t)off * out_slice, pp.out[slot], out_slice * c * sizeof(float),
-                        cudaMemcpyDeviceToHost, pp.s_out);
-    if (e) return cuda_fail(e, "D2H");
-    cudaEventRecord(pp.ev_out[slot], pp.s_out);
-  }
-  cudaError_t e = cudaStreamSynchronize(pp.s_out);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(pp.s_comp);
-  if (e) return cuda_fail(e, "bst execute_host sync");
-  g_launches = launches;
-  return LPBP_OK;
+  return host_pipeline(P->pipe, batch, chunk, in_slice, out_slice, bst_ws_bytes(P, chunk), sino_host, img_host,
+                       [&](const float* in, float* out, int c, void* ws, size_t, cudaStream_t st) {
+                         return bst_chunk(P, in, out, c, static_cast<char*>(ws), st, nullptr);
+                       });
 }
 
 int lpbp_bst_radial(const lpbp_bst_plan* P, const float* sino_dev, float* spectra_dev, int32_t batch, void* stream) {
