@@ -40,6 +40,10 @@ except (OSError, ValueError):
 # capture (profiles/r01j_summary.md, 8-slice launches at 2048^2 FBP, the bench's chunk)
 TRAFFIC_PER_SLICE = {"rho_conv": (403.552768e6 + 441.297408e6) / 8, "irdft_readout": (717.000704e6 + 179.214336e6) / 8,
                      "ramp_filter": (134.266112e6 + 90.483200e6) / 8, "row_rdft": (134.241024e6 + 215.762432e6) / 8}
+# the same for the BST engine (profiles/r01j_bst_summary.md)
+TRAFFIC_PER_SLICE_BST = {"bst_grid_x": (860.662016e6 + 247.000576e6) / 8, "bst_radial": (134.635776e6 + 702.642688e6) / 8,
+                         "bst_grid_y": (268.454656e6 + 107.348224e6) / 8,
+                         "ramp_filter": (134.266368e6 + 90.408192e6) / 8}
 UNIT = "slices/s"
 
 
@@ -381,7 +385,7 @@ def run_ours(a, d: Dist):
     flops = p.roofline.bst_nominal_flops(plan) if bst else p.roofline.nominal_flops(plan)
     fp_ach = flops.get(dom, 0.0) * slices_per_launch / (per_launch_ms / 1000.0) / 1e12
     fp_peak = p.roofline.fp32_peak_tflops(float(MEASURED.get("sm_max_mhz", 1965.0)))
-    traffic = None if bst else TRAFFIC_PER_SLICE.get(dom)
+    traffic = (TRAFFIC_PER_SLICE_BST if bst else TRAFFIC_PER_SLICE).get(dom)
     traffic = traffic * slices_per_launch if traffic else None
     pipe_bytes = sum(ab[k]["per_slice"] for k in ab if k in stages) + sum(
         ab[k]["per_launch"] * stages[k]["launches"] for k in stages) / max(1, S * a.steps)
@@ -425,7 +429,6 @@ def run_ours(a, d: Dist):
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": per_launch_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
-                         "traffic_note": None if not bst else "no ncu capture of the BST kernels in this bench",
                          "fp32_pipe": {"achieved_tflops": fp_ach, "peak_tflops": fp_peak, "frac": fp_ach / fp_peak,
                                        "note": "nominal FFT flops (5 N log2 N) of the kernel / launch time vs "
                                                "148 SMs x 128 lanes x 2 x clock; FFT stages are FP32-pipe bound"}},
