@@ -121,6 +121,25 @@ def test_bst_batch_host_and_linearity(pkg):
     assert O.relative_l2((2 * ia - 3 * ib).cpu().numpy(), iab.cpu().numpy()) < 1e-5
 
 
+def test_bst_profiling_and_pipelined_host_path(pkg):
+    """Stage events cover ramp / radial / grid_x / grid_y once per chunk; the pipelined host path
+    (two staging slots, H2D / compute / D2H streams) is bitwise equal to the device path for ragged
+    chunking and for a chunk size change between calls (the staging is re-sized)."""
+    sino = np.stack([phantoms.sinogram(700 + i, 256, 256, 8, 0.05, 0.35, 0.01) for i in range(7)])
+    plan = pkg.BstPlan(256, 256, pkg.BstOptions(n_out=256), filter_spec=(0.0, 1.0))
+    plan.profile(True)
+    full = plan.execute(dev(sino), chunk=3)
+    st = plan.profile_read()
+    plan.profile(False)
+    assert set(st) == {"ramp_filter", "bst_radial", "bst_grid_x", "bst_grid_y"}
+    assert all(v["launches"] == 3 and v["slices"] == 7 and v["ms"] > 0 for v in st.values())
+    ref = full.cpu().numpy()
+    for chunk in (2, 5, 3):
+        got = plan.execute_host(sino, chunk=chunk)
+        assert np.array_equal(got, ref), chunk
+    assert plan.last_launches == 4 * 3
+
+
 def test_bst_2048_fbp_vs_oracle(pkg):
     """Config-3 geometry through fbp's default engine."""
     g = phantoms.config_sinogram(3, 5)
