@@ -55,7 +55,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--slices", type=int, default=0, help="slices per rank per step (0 = config default)")
-    ap.add_argument("--chunk", type=int, default=8, help="slices per internal pipeline chunk (8 x 2 streams measured best)")
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="slices per internal pipeline chunk (0 = 8 for logpolar (x 2 streams), 16 for bst (x 1 stream): "
+                         "the measured best of 4 / 8 / 16)")
     ap.add_argument("--e2e-slices", type=int, default=128)
     ap.add_argument("--e2e-chunk", type=int, default=4)
     ap.add_argument("--streams", type=int, default=0,
@@ -314,7 +316,7 @@ def run_ours(a, d: Dist):
     global_ids = range(d.rank * S, (d.rank + 1) * S)  # weak scaling: S slices per rank
     sino = p.synth.config_batch(a.config, list(global_ids), dev)
     out = torch.empty((S, n, n), dtype=torch.float32, device=dev)
-    chunk = min(a.chunk, S)
+    chunk = min(a.chunk if a.chunk > 0 else (16 if bst else 8), S)
     nstreams = a.streams if a.streams > 0 else (1 if bst else 2)
     # one workspace per stream: the plan is immutable, chunks on different streams overlap
     wss = [None if bst else torch.empty(plan.workspace_bytes(chunk), dtype=torch.uint8, device=dev)
