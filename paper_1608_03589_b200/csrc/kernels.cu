@@ -339,11 +339,16 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     fence_mbar_init();
   }
   __syncthreads();
+  // the packed taps ride on the first column's barrier as one more bulk copy (16-byte multiple)
+  const uint32_t kw_bytes = (uint32_t)nrho * 4u;
+  const bool kw_bulk = (kw_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(kw) & 15u) == 0;
   if (ti == 0) {
-    mbar_arrive_expect_tx(&bar, col_bytes);
+    mbar_arrive_expect_tx(&bar, col_bytes + (kw_bulk ? kw_bytes : 0u));
     tma_bulk_g2s(gcol, Gh + (size_t)m * gp, col_bytes, &bar);
+    if (kw_bulk) tma_bulk_g2s(kws, kw, kw_bytes, &bar);
   }
-  for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
+  if (!kw_bulk)
+    for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
 
   for (int b = 0; b < batch; ++b) {
     mbar_wait(&bar, b & 1);
