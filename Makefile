@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O3 -Xptxas -v
 SRC := paper_1608_03589_b200/csrc
 LIB := paper_1608_03589_b200/liblpbp.so
-OBJS := build/kernels.o build/sector_kernels.o build/bst_kernels.o build/resample_kernels.o build/capi.o build/plan_host.o build/sector_host.o build/bst_host.o
+OBJS := build/kernels.o build/direct_kernels.o build/sector_kernels.o build/bst_kernels.o build/resample_kernels.o build/capi.o build/plan_host.o build/sector_host.o build/bst_host.o
 
 all: $(LIB)
 

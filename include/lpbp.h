@@ -92,8 +92,10 @@ int lpbp_logpolar(const lpbp_plan* plan, const float* sino_dev, float* lp_dev, i
                   size_t ws_bytes, void* stream);
 int lpbp_readout(const lpbp_plan* plan, const float* lp_dev, float* img_dev, int32_t batch, void* stream);
 
-/* Direct O(n^2 ntheta) pixel-driven backprojector.  ws_dev: lpbp_naive_workspace_bytes
- * (a zero-padded angle-major copy of the batch).  Synchronises `stream`. */
+/* Direct O(n^2 ntheta) pixel-driven backprojector (reference.py:21-37, configs[4]).
+ * ws_dev: lpbp_naive_workspace_bytes, 256-byte aligned (the fp64-built angle table and a
+ * zero-padded angle-major copy of the batch, 4 slices interleaved per entry).  Two kernel
+ * launches on `stream`; asynchronous (no host synchronisation). */
 int lpbp_naive_workspace_bytes(int32_t nt, int32_t ntheta, int32_t batch, size_t* bytes);
 int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, int32_t ntheta, int32_t n,
                            int32_t batch, float* ws_dev, void* stream);

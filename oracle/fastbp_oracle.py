@@ -267,10 +267,18 @@ def backproject_naive(g: np.ndarray, n: int, rows: np.ndarray | None = None) -> 
     return acc * dtheta
 
 
+def _as_exact(a) -> np.ndarray:
+    """Widen to float64 / complex128 without dropping anything: complex inputs stay
+    complex (an fp64 cast would silently discard their imaginary parts)."""
+    x = np.asarray(a)
+    return x.astype(np.complex128 if np.iscomplexobj(x) else np.float64, copy=False)
+
+
 def relative_l2(a, b) -> float:
-    """metrics.py:29-36: ||a - b|| / ||b||, b the reference."""
-    x = np.asarray(a, dtype=np.float64)
-    y = np.asarray(b, dtype=np.float64)
+    """metrics.py:29-36: ||a - b|| / ||b||, b the reference.  Complex arrays are
+    compared as complex (the norm of the complex difference)."""
+    x = _as_exact(a)
+    y = _as_exact(b)
     if x.shape != y.shape:
         raise ValueError(f"dimension mismatch: {x.shape} vs {y.shape}")
     den = np.linalg.norm(y)
@@ -280,7 +288,8 @@ def relative_l2(a, b) -> float:
 
 
 def max_abs(a, b) -> float:
-    return float(np.max(np.abs(np.asarray(a, dtype=np.float64) - np.asarray(b, dtype=np.float64))))
+    """Largest |a - b| (complex modulus for complex inputs)."""
+    return float(np.max(np.abs(_as_exact(a) - _as_exact(b))))
 
 
 # --------------------------------------------------------------------------

@@ -24,7 +24,7 @@ import torch
 
 from ._native import BstInfo, BstParams, check, lib
 from .grids import CartesianImage, Sinogram
-from .plan import _as_f32_contig, _require_cuda, _stream
+from .plan import _as_f32_contig, _check_out_device, _check_out_host, _require_cuda, _stream
 
 __all__ = ["BST_SCALE", "BstOptions", "BstPlan", "bst_backproject", "bst_backproject_batch", "bst_spectrum",
            "get_bst_plan", "kaiser_window", "mean_backprojection", "sigma_kernel"]
@@ -125,6 +125,8 @@ class BstPlan:
         b = sino.shape[0]
         if out is None:
             out = torch.empty((b, self.n_out, self.n_out), dtype=torch.float32, device=self.device)
+        else:
+            _check_out_device(out, (b, self.n_out, self.n_out), self.device)
         c = max(1, min(b, chunk or 4))
         nbytes = self.workspace_bytes(c)
         ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -141,7 +143,8 @@ class BstPlan:
         b = sino.shape[0]
         if out is None:
             out = np.empty((b, self.n_out, self.n_out), dtype=np.float32)
-        check(lib().lpbp_bst_execute_host(self._h, c_void_p(sino.ctypes.data), c_void_p(out.ctypes.data), b,
+        dst = _check_out_host(out, (b, self.n_out, self.n_out))
+        check(lib().lpbp_bst_execute_host(self._h, c_void_p(sino.ctypes.data), c_void_p(dst), b,
                                           int(chunk)))
         self.last_launches = int(lib().lpbp_last_launch_count())
         return out

@@ -13,6 +13,7 @@
 
 #include "../../include/lpbp.h"
 #include "kernels.cuh"
+#include "direct_kernels.cuh"
 #include "plan_host.h"
 #include "sector_kernels.cuh"
 #include "bst_host.h"
@@ -539,7 +540,7 @@ int lpbp_execute_host(lpbp_plan* P, const float* sino_host, float* img_host, int
 
 int lpbp_naive_workspace_bytes(int32_t nt, int32_t ntheta, int32_t batch, size_t* bytes) {
   if (!bytes || nt < 2 || ntheta < 1 || batch < 0) return fail(LPBP_EINVAL, "invalid argument");
-  *bytes = lpbp::naive_workspace_floats(nt, ntheta, batch) * sizeof(float);
+  *bytes = lpbp::direct_geom(nt, ntheta, 2, batch).ws_bytes;  // independent of n
   return LPBP_OK;
 }
 
@@ -551,26 +552,11 @@ int lpbp_naive_backproject(const float* sino_dev, float* img_dev, int32_t nt, in
   if (nt < 2 || ntheta < 1) return fail(LPBP_EINVAL, "nt must be >= 2 and ntheta >= 1");
   if (batch == 0) return LPBP_OK;
   if (!sino_dev || !img_dev || !ws_dev) return fail(LPBP_EINVAL, "invalid argument");
-  // angle table (reference.py:30-36): cos/sin(k*pi/ntheta) * nt/(2n)
-  std::vector<lpbp::F2> cs(ntheta);
-  const double dtheta = 3.14159265358979323846 / ntheta;
-  for (int k = 0; k < ntheta; ++k) {
-    const double th = k * dtheta;
-    cs[k] = lpbp::F2{(float)(std::cos(th) * nt / (2.0 * n)), (float)(std::sin(th) * nt / (2.0 * n))};
-  }
-  void* dcs = nullptr;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMallocAsync(&dcs, cs.size() * sizeof(lpbp::F2), s);
-  if (e) return cuda_fail(e, "cudaMallocAsync(angles)");
-  e = cudaMemcpyAsync(dcs, cs.data(), cs.size() * sizeof(lpbp::F2), cudaMemcpyHostToDevice, s);
-  if (e) return cuda_fail(e, "angles H2D");
-  e = lpbp::launch_naive(nt, ntheta, n, static_cast<const float2*>(dcs), (float)dtheta, sino_dev, ws_dev, img_dev,
-                         batch, s);
+  if (reinterpret_cast<uintptr_t>(ws_dev) % 256) return fail(LPBP_EINVAL, "workspace must be 256-byte aligned");
+  const lpbp::DirectGeom g = lpbp::direct_geom(nt, ntheta, n, batch);
+  cudaError_t e = lpbp::launch_direct(g, sino_dev, ws_dev, img_dev, batch, static_cast<cudaStream_t>(stream));
   g_launches += 2;
-  cudaError_t e2 = cudaStreamSynchronize(s);  // cs lives on the host stack until the copy completes
-  cudaFreeAsync(dcs, s);
   if (e) return cuda_fail(e, "naive_backproject");
-  if (e2) return cuda_fail(e2, "naive_backproject");
   return LPBP_OK;
 }
 

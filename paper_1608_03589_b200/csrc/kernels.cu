@@ -721,68 +721,6 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
-// Direct pixel-driven backprojector (reference.py:21-37), the accuracy
-// cross-check: b(x) = dtheta * sum_k lerp_t(g[:, k], (x . xi_k + 1) / dt).
-// The sinogram is transposed to angle-major first so a warp's 32 pixels read
-// one or two sectors per angle.
-// ---------------------------------------------------------------------------
-// gT[k][PAD + t] = g[t][k]; the PAD zeros on each side make every tap of a pixel
-// inside [-1,1]^2 addressable without bounds checks (|t| <= sqrt 2).
-__global__ void k_transpose(const float* __restrict__ g, float* __restrict__ gT, int nt, int ntheta, int ntp,
-                            int pad) {
-  __shared__ float tile[32][33];
-  const size_t slice = (size_t)blockIdx.z * nt * ntheta;
-  const size_t tslice = (size_t)blockIdx.z * ntheta * ntp;
-  const int th0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int t = t0 + r, th = th0 + threadIdx.x;
-    if (t < nt && th < ntheta) tile[r][threadIdx.x] = g[slice + (size_t)t * ntheta + th];
-  }
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int th = th0 + r, t = t0 + threadIdx.x;
-    if (t < nt && th < ntheta) gT[tslice + (size_t)th * ntp + pad + t] = tile[threadIdx.x][r];
-  }
-}
-
-// 4 pixels per thread (rows iy, iy+8, iy+16, iy+24 of a 32x32 tile) share each
-// angle's table entry; f = a*C + b*S + nt/2 + PAD is positive, so truncation is floor.
-__global__ void __launch_bounds__(256)
-k_naive(const float* __restrict__ gT, float* __restrict__ img, int nt, int ntheta, int n, int ntp, int pad,
-        const float2* __restrict__ cs, float dtheta) {
-  const int jx = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int iy0 = blockIdx.y * 32 + (threadIdx.x >> 5);
-  const float a = (float)(2 * jx + 1 - n);
-  float b[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) b[u] = (float)(2 * (iy0 + 8 * u) + 1 - n);
-  const float off = 0.5f * (float)nt + (float)pad;
-  const float* src = gT + (size_t)blockIdx.z * ntheta * ntp;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-  for (int k = 0; k < ntheta; ++k) {
-    const float2 c = __ldg(cs + k);
-    const float base = fmaf(a, c.x, off);
-    const float* row = src + (size_t)k * ntp;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float f = fmaf(b[u], c.y, base);
-      const int i0 = (int)f;
-      const float w = f - (float)i0;
-      const float v0 = __ldg(row + i0), v1 = __ldg(row + i0 + 1);
-      acc[u] += fmaf(w, v1 - v0, v0);
-    }
-  }
-  if (jx < n) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int iy = iy0 + 8 * u;
-      if (iy < n) img[(size_t)blockIdx.z * n * n + (size_t)iy * n + jx] = acc[u] * dtheta;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Generic sizes (any nt, any ntheta; nphi = 2 ntheta need not be a power of two).
 // The length-nphi DFTs use Bluestein's identity with the same pow2 block_conv:
 //   X[k] = c[k] sum_n (x[n] c[n]) conj c[k-n],  c[n] = exp(-i pi n^2 / nphi),
@@ -1089,23 +1027,6 @@ cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, f
                                                             d.out_scale);
   return cudaGetLastError();
 }
-int naive_pad(int nt) { return nt / 4 + 8; }  // >= (sqrt 2 - 1) nt/2 + 2
-size_t naive_workspace_floats(int nt, int ntheta, int batch) {
-  return (size_t)batch * ntheta * (nt + 2 * naive_pad(nt));
-}
-
-cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dtheta, const float* g, float* gT,
-                         float* img, int batch, cudaStream_t s) {
-  const int pad = naive_pad(nt), ntp = nt + 2 * pad;
-  cudaError_t e = cudaMemsetAsync(gT, 0, naive_workspace_floats(nt, ntheta, batch) * sizeof(float), s);
-  if (e) return e;
-  k_transpose<<<dim3((ntheta + 31) / 32, (nt + 31) / 32, batch), dim3(32, 8), 0, s>>>(g, gT, nt, ntheta, ntp, pad);
-  e = cudaGetLastError();
-  if (e) return e;
-  k_naive<<<dim3((n + 31) / 32, (n + 31) / 32, batch), 256, 0, s>>>(gT, img, nt, ntheta, n, ntp, pad, cs, dtheta);
-  return cudaGetLastError();
-}
-
 namespace {
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {

@@ -60,10 +60,6 @@ cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2
                                  int* counter, cudaStream_t s);
 int fused_band_rows(int nphi);
 cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, float* img, int batch, cudaStream_t s);
-// direct backprojector workspace: zero-padded angle-major copy of the batch
-size_t naive_workspace_floats(int nt, int ntheta, int batch);
-cudaError_t launch_naive(int nt, int ntheta, int n, const float2* cs, float dtheta, const float* g, float* gT,
-                         float* img, int batch, cudaStream_t s);
 
 cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int ntheta, int batch, float* out,
                                   cudaStream_t s);

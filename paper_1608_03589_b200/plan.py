@@ -36,6 +36,41 @@ def _as_f32_contig(t: torch.Tensor, ndim: int, name: str) -> torch.Tensor:
     return t.contiguous()
 
 
+def _check_out_device(out: torch.Tensor, shape: tuple, device: torch.device) -> torch.Tensor:
+    """Caller-supplied device output: the kernels write prod(shape) floats through a raw
+    pointer, so anything but an exact float32, C-contiguous tensor of that shape on the
+    plan's device is refused before the pointer crosses the ABI."""
+    if not isinstance(out, torch.Tensor):
+        raise ValueError("out must be a torch.Tensor")
+    if tuple(out.shape) != tuple(shape) or out.dtype != torch.float32 or not out.is_contiguous():
+        raise ValueError(f"out must be a C-contiguous float32 tensor of shape {tuple(shape)}, "
+                         f"got {out.dtype} {tuple(out.shape)}")
+    if out.device != device:
+        raise ValueError(f"out on {out.device}, plan on {device}")
+    return out
+
+
+def _check_out_host(out, shape: tuple):
+    """Caller-supplied host output (numpy array or CPU tensor) for the *_host entry points."""
+    if isinstance(out, torch.Tensor):
+        if out.is_cuda or out.dtype != torch.float32 or not out.is_contiguous() or tuple(out.shape) != tuple(shape):
+            raise ValueError(f"out must be a contiguous float32 CPU tensor of shape {tuple(shape)}")
+        return out.data_ptr()
+    if not (isinstance(out, np.ndarray) and out.flags.c_contiguous and out.flags.writeable
+            and out.dtype == np.float32 and out.shape == tuple(shape)):
+        raise ValueError(f"out must be a C-contiguous writeable float32 array of shape {tuple(shape)}")
+    return out.ctypes.data
+
+
+def _check_workspace(ws: torch.Tensor, need: int, device: torch.device) -> int:
+    if not isinstance(ws, torch.Tensor) or not ws.is_contiguous() or ws.device != device:
+        raise ValueError(f"workspace must be a contiguous tensor on {device}")
+    nbytes = ws.numel() * ws.element_size()
+    if nbytes < need:
+        raise ValueError(f"workspace holds {nbytes} bytes, the plan needs {need}")
+    return nbytes
+
+
 def _stream(device: torch.device) -> c_void_p:
     return c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
@@ -110,10 +145,12 @@ class LogPolarPlan:
         b = sino.shape[0]
         if out is None:
             out = torch.empty((b, self.n_out, self.n_out), dtype=torch.float32, device=self.device)
+        else:
+            _check_out_device(out, (b, self.n_out, self.n_out), self.device)
         if workspace is None:
             workspace, nbytes = self._workspace(b, chunk)
         else:
-            nbytes = workspace.numel() * workspace.element_size()
+            nbytes = _check_workspace(workspace, self.workspace_bytes(1), self.device)
         with torch.cuda.device(self.device):
             check(lib().lpbp_execute(self._h, c_void_p(sino.data_ptr()), c_void_p(out.data_ptr()), b,
                                      c_void_p(workspace.data_ptr()), nbytes, _stream(self.device)))
@@ -164,17 +201,16 @@ class LogPolarPlan:
             src_ptr = sino.data_ptr()
             if out is None:
                 out = torch.empty((b, self.n_out, self.n_out), dtype=torch.float32, pin_memory=sino.is_pinned())
-            dst_ptr = out.data_ptr()
         else:
             sino = np.ascontiguousarray(sino, dtype=np.float32)
             b = sino.shape[0]
             src_ptr = sino.ctypes.data
             if out is None:
                 out = np.empty((b, self.n_out, self.n_out), dtype=np.float32)
-            if not (out.flags.c_contiguous and out.dtype == np.float32 and out.shape == (b, self.n_out, self.n_out)):
-                raise ValueError("out must be a C-contiguous float32 array of shape (B, n, n)")
-            dst_ptr = out.ctypes.data
-        if sino.shape[1:] != (self.nt, self.ntheta):
+        if sino.dim() != 3 if is_torch else sino.ndim != 3:
+            raise ValueError(f"sinogram batch must have shape (B, {self.nt}, {self.ntheta})")
+        dst_ptr = _check_out_host(out, (b, self.n_out, self.n_out))
+        if tuple(sino.shape[1:]) != (self.nt, self.ntheta):
             raise ValueError(f"sinogram batch must have shape (B, {self.nt}, {self.ntheta})")
         check(lib().lpbp_execute_host(self._h, c_void_p(src_ptr), c_void_p(dst_ptr), b, int(chunk)))
         self.last_launches = int(lib().lpbp_last_launch_count())

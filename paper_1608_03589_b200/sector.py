@@ -25,7 +25,7 @@ import torch
 
 from ._native import Sector, SectorInfo, check, lib
 from .grids import CartesianImage, LogPolarImage, Sinogram
-from .plan import _as_f32_contig, _require_cuda, _stream
+from .plan import _as_f32_contig, _check_out_device, _check_out_host, _require_cuda, _stream
 
 __all__ = ["SectorPlan", "partial_backproject", "partial_backproject_batch", "get_sector_plan"]
 
@@ -85,6 +85,8 @@ class SectorPlan:
         b = sino.shape[0]
         if out is None:
             out = torch.empty((b, self.n_out, self.n_out), dtype=torch.float32, device=self.device)
+        else:
+            _check_out_device(out, (b, self.n_out, self.n_out), self.device)
         c = max(1, min(b, chunk or 8))
         nbytes = self.workspace_bytes(c)
         ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -102,9 +104,8 @@ class SectorPlan:
         b = sino.shape[0]
         if out is None:
             out = np.empty((b, self.n_out, self.n_out), dtype=np.float32)
-        if not (out.flags.c_contiguous and out.dtype == np.float32 and out.shape == (b, self.n_out, self.n_out)):
-            raise ValueError("out must be a C-contiguous float32 array of shape (B, n, n)")
-        check(lib().lpbp_sector_execute_host(self._h, c_void_p(sino.ctypes.data), c_void_p(out.ctypes.data), b,
+        dst = _check_out_host(out, (b, self.n_out, self.n_out))
+        check(lib().lpbp_sector_execute_host(self._h, c_void_p(sino.ctypes.data), c_void_p(dst), b,
                                              int(chunk)))
         self.last_launches = int(lib().lpbp_last_launch_count())
         return out

@@ -115,13 +115,14 @@ def radon_ellipses_batch(params: np.ndarray, nt: int, ntheta: int, device, dtype
 
 def config_batch(cfg: int, slice_ids, device, gen_chunk: int = 64) -> torch.Tensor:
     """Sinograms of config `cfg` for the given global slice indices (seed = BASE_SEED
-    + 7919*cfg + index, as oracle/phantoms.config_sinogram)."""
+    + 7919*cfg + index, as oracle/phantoms.config_sinogram; config 4 reuses config 2's
+    seeds: BASELINE.json configs[4] runs on the same 64 slices)."""
     c = CONFIGS[cfg]
     ids = list(slice_ids)
     out = torch.empty((len(ids), c["nt"], c["ntheta"]), dtype=torch.float32, device=device)
     for lo in range(0, len(ids), gen_chunk):
         part = ids[lo:lo + gen_chunk]
-        seeds = [BASE_SEED + 7919 * cfg + i for i in part]
+        seeds = [BASE_SEED + 7919 * (2 if cfg == 4 else cfg) + i for i in part]
         prm = np.stack([ellipse_params(s, c["k"], c["amin"], c["amax"]) for s in seeds])
         g = radon_ellipses_batch(prm, c["nt"], c["ntheta"], device)
         if c["noise"] > 0:

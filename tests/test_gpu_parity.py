@@ -154,25 +154,6 @@ def test_cfg3_fbp_full_size_sample(pkg):
     assert report("cfg3 slice5 fbp", out, ref) <= RTOL
 
 
-@pytest.mark.slow
-def test_cfg4_naive_cross_check(pkg):
-    """Direct backprojector at 2048^2: parity vs the oracle on sampled rows, and the
-    LP-vs-direct discretisation gap inside the unit disk (a property, not a 1e-4 bar)."""
-    s = phantoms.config_sinogram(4, 0)
-    d = dev(s)[None]
-    nv = pkg.backproject_naive_batch(d, 2048)[0].cpu().numpy()
-    rows = np.arange(3, 2048, 97)
-    ref_rows = O.backproject_naive(s.astype(np.float64), 2048, rows=rows)
-    assert report("cfg4 naive rows", nv[rows], ref_rows) <= RTOL
-    lp = pkg.logpolar_backproject_batch(d, 2048)[0].cpu().numpy()
-    xs = -1.0 + (np.arange(2048) + 0.5) * (2.0 / 2048)
-    X, Y = np.meshgrid(xs, xs)
-    disk = np.hypot(X, Y) <= 1.0
-    gap = O.relative_l2(lp[disk], nv[disk])
-    print(f"cfg4 LP vs direct in unit disk: {gap:.3e}")
-    assert gap < 1e-2
-
-
 def test_unsupported_size_is_loud(pkg):
     g = pkg.Sinogram(4096, 8, np.ones((4096, 8)))  # rho FFT would need 16384 points: no instantiation
     with pytest.raises(NotImplementedError):
