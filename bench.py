@@ -3,14 +3,18 @@
 "backprojected 2048^2 slices/sec at 1/2/4/8 B200; HBM GB/s vs peak").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 3] [--slices S] [--e2e-slices E]
+                    [--config 3] [--slices S] [--scaling strong|weak] [--e2e-slices E]
 
 One process per GPU (torchrun for N > 1).  A step is one pass of the FBP hot
-path over the rank's resident batch of S slices (default: configs[3], S = 2048
-slices of 2048 angles x 2048 bins per rank -> weak scaling; no inter-GPU data
-exchange, torch.distributed carries only the barrier and the max-over-ranks
-timing).  Inputs (34 GB per rank) are far larger than L2, so no L2 flush is
-needed between steps.
+path over the rank's resident slices.  Default workload: configs[3], the
+2048-slice volume of 2048 angles x 2048 bins, sharded by slice index over the N
+ranks (strong scaling: rank r takes the contiguous block bench.shard(2048, N, r),
+seeds = global slice index); --scaling weak gives every rank S slices of its own.
+There is no inter-GPU data exchange: torch.distributed carries only the barrier,
+the max-over-ranks timing and the shard bookkeeping.  Inputs (>= 4 GB per rank
+at N = 8) are far larger than L2, so no L2 flush is needed between steps.
+
+--config 4 times the direct pixel-driven backprojector on the 64 config-2 slices.
 
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port, oracle/fastbp_oracle.py: numpy/scipy restatement of fastbp) on the
@@ -36,14 +40,27 @@ try:
     MEASURED = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
 except (OSError, ValueError):
     MEASURED = {}
-# dram__bytes_read.sum + dram__bytes_write.sum per slice from the committed ncu --set full
-# capture (profiles/r01j_summary.md, 8-slice launches at 2048^2 FBP, the bench's chunk)
-TRAFFIC_PER_SLICE = {"rho_conv": (403.552768e6 + 441.297408e6) / 8, "irdft_readout": (717.000704e6 + 179.214336e6) / 8,
-                     "ramp_filter": (134.266112e6 + 90.483200e6) / 8, "row_rdft": (134.241024e6 + 215.762432e6) / 8}
-# the same for the BST engine (profiles/r01j_bst_summary.md)
-TRAFFIC_PER_SLICE_BST = {"bst_grid_x": (860.662016e6 + 247.000576e6) / 8, "bst_radial": (134.635776e6 + 702.642688e6) / 8,
-                         "bst_grid_y": (268.454656e6 + 107.348224e6) / 8,
-                         "ramp_filter": (134.266368e6 + 90.408192e6) / 8}
+# dram__bytes_read.sum + dram__bytes_write.sum per slice and kernel, from the committed ncu
+# --set full capture named in profiles/traffic.json; used only when that capture was taken
+# on the same kernel sources (sha256 of paper_1608_03589_b200/csrc), else reported as null
+TRAFFIC_FILE = os.path.join(REPO, "profiles", "traffic.json")
+
+
+def load_traffic(engine: str):
+    """(per-slice DRAM bytes by kernel, provenance) of the committed capture for `engine`."""
+    from paper_1608_03589_b200 import roofline
+    try:
+        t = json.load(open(TRAFFIC_FILE))[engine]
+    except (OSError, ValueError, KeyError):
+        return None, {"source": None, "note": "no committed capture"}
+    here = roofline.kernel_source_digest()
+    prov = {"source": t.get("capture"), "csrc_sha256": t.get("csrc_sha256"), "current_csrc_sha256": here}
+    if t.get("csrc_sha256") != here:
+        prov["note"] = "capture predates the current kernel sources: traffic not reported"
+        return None, prov
+    return t["per_slice"], prov
+
+
 UNIT = "slices/s"
 
 
@@ -66,6 +83,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = min(cores, memory/2.5GB, 32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default): the config's volume (2048 slices for config 3) is sharded by slice index "
+                         "over the ranks; weak: every rank processes --slices (or the config's count) of its own")
     ap.add_argument("--engine", default="logpolar", choices=["logpolar", "bst"],
                     help="logpolar (the north-star path, default) or bst (fbp's default engine in the reference)")
     return ap.parse_args()
@@ -109,6 +129,14 @@ class Dist:
         self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
         return float(t.item())
 
+    def gather(self, obj) -> list:
+        """Every rank's `obj`, in rank order (host-side bookkeeping only)."""
+        if not self.pg:
+            return [obj]
+        out = [None] * self.world
+        self.pg.all_gather_object(out, obj)
+        return out
+
     def close(self):
         if self.pg:
             self.pg.destroy_process_group()
@@ -119,6 +147,15 @@ def shard(total: int, world: int, rank: int) -> range:
     lo = total * rank // world
     hi = total * (rank + 1) // world
     return range(lo, hi)
+
+
+def rank_slices(total: int, world: int, rank: int, scaling: str) -> list[int]:
+    """Global slice indices rank `rank` reconstructs (their per-slice seeds make the inputs).
+    strong: the `total`-slice volume split into contiguous blocks; weak:
+    `total` slices per rank, rank r taking [r total, (r + 1) total)."""
+    if scaling == "strong":
+        return list(shard(total, world, rank))
+    return list(range(rank * total, (rank + 1) * total))
 
 
 # ----------------------------------------------------------------------------
@@ -258,7 +295,7 @@ def run_reference(a, d: Dist):
     ms = sum(w for _, w in vals) / len(vals) * 1000.0
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded random-ellipse sinograms + 1% Gaussian noise)",
         "config": {"workload": workload_name(a.config, c), "slices_per_step": workers},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
@@ -307,14 +344,16 @@ def run_ours(a, d: Dist):
     dev = torch.device("cuda", d.local)
     c = p.synth.CONFIGS[a.config]
     nt, nth, n = c["nt"], c["ntheta"], c["n"]
-    S = a.slices or c["slices"]
+    total = a.slices or c["slices"]
     spec = (0.0, 1.0) if c["fbp"] else None
     bst = a.engine == "bst"
     plan = p.BstPlan(nt, nth, p.BstOptions(n_out=n), spec) if bst else p.get_plan(nt, nth, n, None, None, spec)
 
-    # ---- synthetic inputs, generated on the device (per-slice seeds)
-    global_ids = range(d.rank * S, (d.rank + 1) * S)  # weak scaling: S slices per rank
-    sino = p.synth.config_batch(a.config, list(global_ids), dev)
+    # ---- synthetic inputs, generated on the device (per-slice seeds = global slice index)
+    global_ids = rank_slices(total, d.world, d.rank, a.scaling)
+    S = len(global_ids)
+    shards = d.gather([global_ids[0], global_ids[-1] + 1] if global_ids else [0, 0])
+    sino = p.synth.config_batch(a.config, global_ids, dev)
     out = torch.empty((S, n, n), dtype=torch.float32, device=dev)
     chunk = min(a.chunk if a.chunk > 0 else (16 if bst else 8), S)
     nstreams = a.streams if a.streams > 0 else (1 if bst else 2)
@@ -352,6 +391,9 @@ def run_ours(a, d: Dist):
     stream = main
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
+    # CUDA events around every kernel launch, on its launching stream, during the timed steps
+    # (lpbp_profile_*): the roofline's per-launch durations are measured live
+    plan.profile(True)
     with clk:
         time.sleep(0.3)
         e0.record(stream)
@@ -359,14 +401,15 @@ def run_ours(a, d: Dist):
             launches += step()
         e1.record(stream)
         torch.cuda.synchronize()
+    stages = plan.profile_read()
+    plan.profile(False)
     d.barrier()
-    # per-stage breakdown (roofline inputs): one extra, untimed single-stream pass with CUDA
-    # events around every launch (overlapping streams would blur per-kernel durations)
+    # the same kernels once more in isolation (one stream, no overlap), for the per-stage split
     plan.profile(True)
     for k in range(0, S, chunk):
         run(sino[k:k + chunk], out[k:k + chunk], wss[0])
     torch.cuda.synchronize()
-    stages = plan.profile_read()
+    iso = plan.profile_read()
     plan.profile(False)
     ms_total = e0.elapsed_time(e1)
     ms_max = d.max(ms_total)
@@ -387,10 +430,15 @@ def run_ours(a, d: Dist):
     flops = p.roofline.bst_nominal_flops(plan) if bst else p.roofline.nominal_flops(plan)
     fp_ach = flops.get(dom, 0.0) * slices_per_launch / (per_launch_ms / 1000.0) / 1e12
     fp_peak = p.roofline.fp32_peak_tflops(float(MEASURED.get("sm_max_mhz", 1965.0)))
-    traffic = (TRAFFIC_PER_SLICE_BST if bst else TRAFFIC_PER_SLICE).get(dom)
+    tr_table, tr_prov = load_traffic("bst" if bst else "logpolar")
+    traffic = (tr_table or {}).get(dom)
     traffic = traffic * slices_per_launch if traffic else None
     pipe_bytes = sum(ab[k]["per_slice"] for k in ab if k in stages) + sum(
         ab[k]["per_launch"] * stages[k]["launches"] for k in stages) / max(1, S * a.steps)
+    survey_bytes = None if bst else p.roofline.survey_bytes_per_slice(plan)
+    share_live = st["ms"] / max(1e-9, sum(v["ms"] for v in stages.values()))
+    iso_dom = iso.get(dom, {"ms": 0.0, "launches": 1, "slices": 1})
+    iso_ms = iso_dom["ms"] / max(1, iso_dom["launches"])
 
     # ---- end to end through the public host API (pinned host in/out, H2D + D2H inside)
     E = min(a.e2e_slices, S)
@@ -419,30 +467,44 @@ def run_ours(a, d: Dist):
     if d.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (device-generated seeded random-ellipse sinograms, K=50, 1% Gaussian noise)",
             "config": dict({"workload": workload_name(a.config, c) + (" (BST engine)" if bst else ""),
-                            "slices_per_rank": S, "chunk": chunk, "streams": nstreams,
-                            "parallelism": f"slice-shard x{d.world}",
-                            "l2": "no flush: 34 GB input per step >> 126 MB L2"},
+                            "slices_total": int(d.sum(S)), "slices_per_rank": S, "rank_slice_ranges": shards,
+                            "chunk": chunk, "streams": nstreams,
+                            "parallelism": f"slice-shard x{d.world} ({a.scaling} scaling, no inter-GPU exchange)",
+                            "l2": f"no flush: {S * nt * nth * 4 / 1e9:.1f} GB of sinograms per rank per step "
+                                  f">> 126 MB L2"},
                            **({"engine": "bst", "L": info["L"], "big": info["big"], "m_need": info["m_need"]} if bst
                               else {"nrho": info["nrho"], "L": info["L"], "nphi": info["nphi"]})),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": per_launch_ms,
+                         "timing": f"CUDA events on the launching stream around each of the {st['launches']} "
+                                   f"launches inside the timed steps ({nstreams} streams overlap)",
+                         "share_of_step_live": share_live,
+                         "isolated_launch_ms": iso_ms,
+                         "isolated_frac": bytes_per_launch / (iso_ms / 1000.0) / 1e9 / peak if iso_ms else None,
+                         "traffic_provenance": tr_prov,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                          "fp32_pipe": {"achieved_tflops": fp_ach, "peak_tflops": fp_peak, "frac": fp_ach / fp_peak,
                                        "note": "nominal FFT flops (5 N log2 N) of the kernel / launch time vs "
                                                "148 SMs x 128 lanes x 2 x clock; FFT stages are FP32-pipe bound"}},
-            "pipeline": {"stage_ms_per_slice": {k: v["ms"] / max(1, v["slices"]) for k, v in stages.items()},
+            "pipeline": {"stage_ms_per_slice_live": {k: v["ms"] / max(1, v["slices"]) for k, v in stages.items()},
+                         "stage_ms_per_slice_isolated": {k: v["ms"] / max(1, v["slices"]) for k, v in iso.items()},
                          "algorithmic_bytes_per_slice": pipe_bytes,
                          "hbm_equiv_gbs": pipe_bytes * value / d.world / 1e9,
-                         "hbm_equiv_frac": pipe_bytes * value / d.world / 1e9 / peak},
+                         "hbm_equiv_frac": pipe_bytes * value / d.world / 1e9 / peak,
+                         "survey_bytes_per_slice": survey_bytes,
+                         "survey_hbm_equiv_frac": (survey_bytes * value / d.world / 1e9 / peak) if survey_bytes
+                         else None,
+                         "survey_basis": "SURVEY §8(d) stage decomposition (S1+S2+S3+S4, K-hat once per batch)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": E * nt * nth * 4,
                     "d2h_bytes_per_step": E * n * n * 4, "slices_per_step": E,
                     "api": "BstPlan.execute_host" if bst else "LogPolarPlan.execute_host",
                     "copy_ceiling": copy_value, "frac_of_copy_ceiling": e2e_value / copy_value,
-                    "copy_ceiling_note": "same bytes, same chunking, H2D and D2H alone on two streams, no compute"},
+                    "copy_ceiling_note": "same bytes, same chunking, H2D and D2H alone on two streams, no compute, "
+                                         "all ranks at once (so at N > 1 it is the shared host-DRAM / PCIe ceiling)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -33,6 +33,22 @@ def algorithmic_bytes(plan) -> dict:
     }
 
 
+def kernel_source_digest() -> str:
+    """sha256 over the kernel sources (csrc/*.cu, *.cuh, *.cpp, *.h, sorted by name): ties a
+    committed ncu traffic capture to the code it measured."""
+    import hashlib
+    import os
+
+    d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc")
+    h = hashlib.sha256()
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".cpp", ".h")):
+            h.update(f.encode())
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()
+
+
 def survey_bytes_per_slice(plan) -> float | None:
     return SURVEY_BYTES_PER_SLICE.get((plan.info["n_out"], bool(plan.info["filter"])))
 

@@ -126,6 +126,47 @@ def test_host_to_host_matches_device(pkg):
     assert np.array_equal(out2, ref)
 
 
+@pytest.mark.slow
+def test_host_paths_2048_bitwise(pkg):
+    """Config-3 geometry (2048^2 FBP): the pipelined host->host path (pinned tensors and numpy,
+    ragged chunking) and a VolumeReconstructor with two plans sharding the slices are bitwise
+    equal to the device-resident path."""
+    ids = [0, 1, 2, 5, 9, 11]
+    sinos = torch.stack([torch.from_numpy(phantoms.config_sinogram(3, i)) for i in ids])
+    plan = pkg.get_plan(2048, 2048, 2048, None, None, (0.0, 1.0))
+    ref = plan.execute(sinos.cuda(), chunk=4).cpu()
+    host = sinos.pin_memory()
+    assert torch.equal(plan.execute_host(host, chunk=4), ref)
+    assert np.array_equal(plan.execute_host(sinos.numpy(), chunk=3), ref.numpy())
+    vr = pkg.VolumeReconstructor(2048, 2048, 2048, filter_spec=(0.0, 1.0), devices=[0, 0], chunk=2)
+    assert torch.equal(vr.run(host), ref)
+    assert np.array_equal(vr.run(sinos.numpy()), ref.numpy())
+    with pytest.raises(ValueError):
+        plan.execute_host(host, out=torch.empty((6, 2048, 2047)))
+    with pytest.raises(ValueError):
+        plan.execute(sinos.cuda(), out=torch.empty((6, 2048, 2048), device="cuda", dtype=torch.float64))
+
+
+@pytest.mark.slow
+def test_bench_generated_input_parity(pkg):
+    """The benched workload is the parity-tested one: a config-3 slice made by the bench's
+    device generator (synth.config_batch), downloaded, reconstructed by the oracle, and compared
+    with the GPU FBP of the same device-resident slice."""
+    k = 1234
+    x = pkg.synth.config_batch(3, [k], torch.device("cuda"))
+    g = x[0].cpu().numpy().astype(np.float64)
+    out = pkg.fbp_batch(x, pkg.FilterSpec(), 2048)[0].cpu().numpy()
+    assert report("bench input slice 1234 fbp", out, O.fbp_logpolar(g, 2048)) <= RTOL
+    # and the device generator's noiseless part is the reference's radon_ellipses
+    c = pkg.synth.CONFIGS[3]
+    prm = pkg.synth.ellipse_params(pkg.synth.BASE_SEED + 7919 * 3 + k, c["k"], c["amin"], c["amax"])
+    clean = pkg.synth.radon_ellipses_batch(prm[None], 2048, 2048, torch.device("cuda"),
+                                           dtype=torch.float64)[0].cpu().numpy()
+    e = phantoms.random_ellipses(pkg.synth.BASE_SEED + 7919 * 3 + k, c["k"], c["amin"], c["amax"])
+    assert np.allclose(prm, np.stack([e.cx, e.cy, e.a, e.b, e.tilt, e.rho], axis=1), rtol=0, atol=0)
+    assert report("bench input noiseless part", clean, phantoms.radon_ellipses(e, 2048, 2048)) <= 1e-12
+
+
 def test_naive_backprojector(pkg, golden):
     z = golden("cfg0.npz")
     g = pkg.Sinogram(256, 256, z["sino"].astype(np.float64))

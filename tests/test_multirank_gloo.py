@@ -1,7 +1,8 @@
-"""World-size-2 gloo run of bench.py's multi-rank plumbing on CPU: contiguous
-slice sharding covers every slice exactly once, and the max/sum reductions the
-bench uses for timing and throughput agree across ranks.  (The data path has no
-collective: slices are independent.)"""
+"""World-size-2 gloo run of bench.py's multi-rank plumbing on CPU: the slice
+ranks run_ours reconstructs (bench.rank_slices, strong and weak scaling) cover the
+volume exactly once, the gathered shard table every rank reports agrees, and the
+max/sum reductions the bench uses for timing and throughput agree across ranks.
+(The data path has no collective: slices are independent.)"""
 
 import os
 import socket
@@ -18,33 +19,55 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, total, q):
+def _rank(rank, world, port, total, scaling, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                       LOCAL_RANK=str(rank))
     import bench
 
     d = bench.Dist()
-    ids = list(bench.shard(total, world, rank))
+    ids = bench.rank_slices(total, world, rank, scaling)
+    shards = d.gather([ids[0], ids[-1] + 1] if ids else [0, 0])
     t_max = d.max(float(rank + 1))
     n_sum = d.sum(float(len(ids)))
     d.barrier()
-    q.put((rank, ids, t_max, n_sum))
+    q.put((rank, ids, shards, t_max, n_sum))
     d.close()
 
 
-@pytest.mark.parametrize("total", [2048, 7])
-def test_two_rank_shard_and_reductions(total):
+def _run(world, total, scaling):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, total, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, total, scaling, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("total", [2048, 7])
+def test_two_rank_strong_shards_and_reductions(total):
+    res = _run(2, total, "strong")
     all_ids = res[0][1] + res[1][1]
-    assert all_ids == list(range(total))
-    assert all(r[2] == 2.0 for r in res)          # max over ranks
-    assert all(r[3] == float(total) for r in res)  # total slices
+    assert all_ids == list(range(total))                 # every slice exactly once, in order
+    assert res[0][2] == res[1][2] == [[r[1][0], r[1][-1] + 1] for r in res]
+    assert all(r[3] == 2.0 for r in res)                  # max over ranks
+    assert all(r[4] == float(total) for r in res)         # total slices
+
+
+def test_two_rank_weak_slices():
+    res = _run(2, 5, "weak")
+    assert res[0][1] == list(range(0, 5)) and res[1][1] == list(range(5, 10))
+    assert all(r[4] == 10.0 for r in res)
+
+
+def test_rank_slices_config3_at_1_2_4_8():
+    import bench
+
+    for world in (1, 2, 4, 8):
+        ids = [i for r in range(world) for i in bench.rank_slices(2048, world, r, "strong")]
+        assert ids == list(range(2048))
+        assert {len(bench.rank_slices(2048, world, r, "strong")) for r in range(world)} == {2048 // world}
