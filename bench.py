@@ -83,6 +83,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = min(cores, memory/2.5GB, 32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--geometry", default="",
+                    help="NTxNTHETA: the config's phantoms and output size at another sinogram shape, e.g. 3200x2048 "
+                         "(the paper's LNLS datasets, PAPER.md:151-153)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong (default): the config's volume (2048 slices for config 3) is sharded by slice index "
                          "over the ranks; weak: every rank processes --slices (or the config's count) of its own")
@@ -219,8 +222,9 @@ def _cpu_worker_many(jobs):
     from oracle import fastbp_oracle as O
     from oracle import phantoms
 
-    inputs = [(phantoms.CONFIGS[cfg], phantoms.config_sinogram(cfg, idx).astype("float64"), eng)
-              for cfg, idx, eng in jobs]
+    inputs = [(c, phantoms.sinogram(phantoms.config_seed(cfg, idx), c["nt"], c["ntheta"], c["k"], c["amin"],
+                                    c["amax"], c["noise"]).astype("float64"), eng)
+              for cfg, c, idx, eng in jobs]
     times = []
     for c, g, eng in inputs:
         t = time.perf_counter()
@@ -245,14 +249,18 @@ def cpu_workers(requested: int) -> int:
     return max(1, min(ncpu, int(avail_gb / 2.5), 32))
 
 
-def cpu_baseline(cfg: int, workers: int, slices_per_worker: int = 1, engine: str = "logpolar"):
+def cpu_baseline(cfg: int, workers: int, slices_per_worker: int = 1, engine: str = "logpolar", c: dict | None = None):
     """Throughput of the oracle port on `workers` host cores: one process per core,
     all running concurrently, each reconstructing whole slices.  Only the
     reconstruction is timed (each worker generates its input first, untimed):
     throughput = slices / (longest per-worker reconstruction time)."""
     env = {"OMP_NUM_THREADS": "1", "OPENBLAS_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"}
     os.environ.update(env)
-    jobs = [[(cfg, 1000 + w * slices_per_worker + i, engine) for i in range(slices_per_worker)] for w in range(workers)]
+    if c is None:
+        from oracle import phantoms
+        c = phantoms.CONFIGS[cfg]
+    jobs = [[(cfg, c, 1000 + w * slices_per_worker + i, engine) for i in range(slices_per_worker)]
+            for w in range(workers)]
     ctx = mp.get_context("spawn")
     with ctx.Pool(workers) as pool:
         per = pool.map(_cpu_worker_many, jobs, chunksize=1)
@@ -274,7 +282,18 @@ def cpu_model() -> str:
 # ----------------------------------------------------------------------------
 def workload_name(config: int, c: dict) -> str:
     """The workload string both arms report (the driver pairs the lines on it)."""
-    return f"config{config}: {'FBP' if c['fbp'] else 'BP'} {c['nt']} bins x {c['ntheta']} angles -> {c['n']}^2"
+    tag = f"config{config}" + (" phantoms" if c.get("geometry") else "")
+    return f"{tag}: {'FBP' if c['fbp'] else 'BP'} {c['nt']} bins x {c['ntheta']} angles -> {c['n']}^2"
+
+
+def bench_config(a) -> dict:
+    """The config's workload, with --geometry NTxNTHETA overriding the sinogram shape."""
+    from oracle import phantoms
+    c = dict(phantoms.CONFIGS[a.config])
+    if a.geometry:
+        nt, nth = (int(v) for v in a.geometry.lower().split("x"))
+        c.update(nt=nt, ntheta=nth, geometry=a.geometry)
+    return c
 
 
 def run_reference(a, d: Dist):
@@ -284,11 +303,11 @@ def run_reference(a, d: Dist):
         return
     from oracle import phantoms
 
-    c = phantoms.CONFIGS[a.config]
+    c = bench_config(a)
     workers = cpu_workers(a.cpu_workers)
     vals = []
     for i in range(a.warmup + a.steps):
-        v, busy, _ = cpu_baseline(a.config, workers, 1)
+        v, busy, _ = cpu_baseline(a.config, workers, 1, c=c)
         if i >= a.warmup:
             vals.append((v, busy))
     v = sum(x for x, _ in vals) / len(vals)
@@ -342,7 +361,7 @@ def run_ours(a, d: Dist):
 
     torch.cuda.set_device(d.local)
     dev = torch.device("cuda", d.local)
-    c = p.synth.CONFIGS[a.config]
+    c = bench_config(a)
     nt, nth, n = c["nt"], c["ntheta"], c["n"]
     total = a.slices or c["slices"]
     spec = (0.0, 1.0) if c["fbp"] else None
@@ -353,7 +372,7 @@ def run_ours(a, d: Dist):
     global_ids = rank_slices(total, d.world, d.rank, a.scaling)
     S = len(global_ids)
     shards = d.gather([global_ids[0], global_ids[-1] + 1] if global_ids else [0, 0])
-    sino = p.synth.config_batch(a.config, global_ids, dev)
+    sino = p.synth.config_batch(a.config, global_ids, dev, geometry=(nt, nth))
     out = torch.empty((S, n, n), dtype=torch.float32, device=dev)
     chunk = min(a.chunk if a.chunk > 0 else (16 if bst else 8), S)
     nstreams = a.streams if a.streams > 0 else (1 if bst else 2)
@@ -458,7 +477,7 @@ def run_ours(a, d: Dist):
     cpu = None
     if d.rank == 0 and a.gpus == 1 and not a.no_cpu_baseline:
         w = cpu_workers(a.cpu_workers)
-        v, busy, per = cpu_baseline(a.config, w, 1, a.engine)
+        v, busy, per = cpu_baseline(a.config, w, 1, a.engine, c=c)
         cpu = {"value": v, "unit": UNIT, "cores": w, "kind": "port",
                "sample": f"{w} config-{a.config} slices, one per concurrent worker process (reconstruction only, "
                          f"slowest worker {busy:.1f} s, mean {np.mean(per):.2f} s/slice/core), "

@@ -313,7 +313,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     delete P;
     return fail(LPBP_EUNSUPPORTED, "no kernel instantiation for nt=" + std::to_string(h.nt) + ", ntheta=" +
                                        std::to_string(h.ntheta) + ", L=" + std::to_string(h.L) +
-                                       " (this build: 2*ntheta <= 4096, 2*nt <= 4096, rho FFT <= 8192)");
+                                       " (this build: ramp embedding 2*nt <= 8192, rho FFT <= 16384, Bluestein row DFT length <= 16384)");
   }
   P->device = params->device;
   if (lpbp::fused_band_rows(P->h.nphi) > 0) lpbp::build_bands(P->h, lpbp::fused_band_rows(P->h.nphi));

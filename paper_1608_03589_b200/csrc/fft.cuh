@@ -334,6 +334,7 @@ template <> struct RadixPlan<1024>  { static constexpr int P = 3; static constex
 template <> struct RadixPlan<2048>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 8}; static constexpr int E = 16; };
 template <> struct RadixPlan<4096>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 16}; static constexpr int E = 16; };
 template <> struct RadixPlan<8192>  { static constexpr int P = 3; static constexpr int r[3] = {16, 16, 32}; static constexpr int E = 32; };
+template <> struct RadixPlan<16384> { static constexpr int P = 3; static constexpr int r[3] = {16, 32, 32}; static constexpr int E = 32; };
 
 template <int N, bool INV>
 struct FftPlan {

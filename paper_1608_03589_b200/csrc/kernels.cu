@@ -316,8 +316,9 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
 // The row mix is evaluated inside the first forward pass; the multiply by
 // Khat is fused between the last forward and first inverse pass.
 // ---------------------------------------------------------------------------
+// 16384-point columns (nt >~ 2900): 512 threads and ~200 KB of shared memory, one CTA per SM
 template <int L, bool PRUNE>
-__global__ void __launch_bounds__(FftPlan<L, false>::T, 2)
+__global__ void __launch_bounds__(FftPlan<L, false>::T, (L >= 16384 ? 1 : 2))
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int gp, int ns, int nrho, int row_lo,
            int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
            const uint32_t* __restrict__ kw, const float2* __restrict__ khat, const float2* __restrict__ tw) {
@@ -989,6 +990,7 @@ cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float
     case 1024: return ramp_impl<1024, 16, 2>(d, t, g, out, batch, s);
     case 2048: return ramp_impl<2048, 8, 1>(d, t, g, out, batch, s);
     case 4096: return ramp_impl<4096, 8, 1>(d, t, g, out, batch, s);
+    case 8192: return ramp_impl<8192, 8, 1>(d, t, g, out, batch, s);  // nt in (2048, 4096]
     default: return cudaErrorNotSupported;
   }
 }
@@ -1009,6 +1011,7 @@ cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh,
     case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, row_lo, s);
     case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, row_lo, s);
     case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, row_lo, s);
+    case 16384: return conv_impl<16384>(d, t, Gh, Yh, batch, row_lo, s);
     default: return cudaErrorNotSupported;
   }
 }
@@ -1150,6 +1153,7 @@ cudaError_t irdft_generic_impl(const Dims& d, const DevTables& t, const float2* 
     case 2048: return CALL(2048);                 \
     case 4096: return CALL(4096);                 \
     case 8192: return CALL(8192);                 \
+    case 16384: return CALL(16384);               \
     default: return cudaErrorNotSupported;        \
   }
 
@@ -1231,6 +1235,7 @@ int twiddle_table_len(int N) {
     case 2048: return TwTable<2048>::len;
     case 4096: return TwTable<4096>::len;
     case 8192: return TwTable<8192>::len;
+    case 16384: return TwTable<16384>::len;
     default: return -1;
   }
 }
@@ -1247,18 +1252,20 @@ cudaError_t launch_init_twiddles(int N, float2* out, cudaStream_t s) {
     case 2048: k_init_twiddles<2048><<<grid, 256, 0, s>>>(out); break;
     case 4096: k_init_twiddles<4096><<<grid, 256, 0, s>>>(out); break;
     case 8192: k_init_twiddles<8192><<<grid, 256, 0, s>>>(out); break;
+    case 16384: k_init_twiddles<16384><<<grid, 256, 0, s>>>(out); break;
   }
   return cudaGetLastError();
 }
 
 bool sizes_supported(int nt, int ntheta, int L, int M, int MB, bool filter, bool generic) {
   auto pow2in = [](int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; };
-  if (!pow2in(L, 512, 8192)) return false;
+  // rho FFT up to 16384 points (nt up to ~5800 at n = nt), ramp embedding up to 8192 (nt <= 4096)
+  if (!pow2in(L, 512, 16384)) return false;
   if (filter && !pow2in(M, 512, 8192)) return false;
-  if (generic) return pow2in(MB, 512, 8192) && nt >= 2;  // odd nt: row spectra column pitch padded to even
+  if (generic) return pow2in(MB, 512, 16384) && nt >= 2;  // odd nt: row spectra column pitch padded to even
   const int nphi = 2 * ntheta;
   if (!pow2in(nphi, 512, 4096) || nt % 4) return false;
-  if (filter && (ntheta % 8 || M > 4096)) return false;
+  if (filter && ntheta % 8) return false;
   return true;
 }
 

@@ -113,11 +113,13 @@ def radon_ellipses_batch(params: np.ndarray, nt: int, ntheta: int, device, dtype
     return out
 
 
-def config_batch(cfg: int, slice_ids, device, gen_chunk: int = 64) -> torch.Tensor:
+def config_batch(cfg: int, slice_ids, device, gen_chunk: int = 64, geometry: tuple[int, int] | None = None) -> torch.Tensor:
     """Sinograms of config `cfg` for the given global slice indices (seed = BASE_SEED
     + 7919*cfg + index, as oracle/phantoms.config_sinogram; config 4 reuses config 2's
     seeds: BASELINE.json configs[4] runs on the same 64 slices)."""
-    c = CONFIGS[cfg]
+    c = dict(CONFIGS[cfg])
+    if geometry is not None:  # the config's phantoms sampled at another (nt, ntheta)
+        c.update(nt=int(geometry[0]), ntheta=int(geometry[1]))
     ids = list(slice_ids)
     out = torch.empty((len(ids), c["nt"], c["ntheta"]), dtype=torch.float32, device=device)
     for lo in range(0, len(ids), gen_chunk):

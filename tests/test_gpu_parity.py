@@ -196,11 +196,31 @@ def test_cfg3_fbp_full_size_sample(pkg):
 
 
 def test_unsupported_size_is_loud(pkg):
-    g = pkg.Sinogram(4096, 8, np.ones((4096, 8)))  # rho FFT would need 16384 points: no instantiation
+    g = pkg.Sinogram(64, 5000, np.ones((64, 5000)))  # Bluestein row DFT would need 32768 points
     with pytest.raises(NotImplementedError):
-        pkg.logpolar_backproject(g, 4096)
+        pkg.logpolar_backproject(g, 64)
     with pytest.raises(NotImplementedError):  # BST: odd nt
         pkg.fbp(pkg.Sinogram(129, 90, np.ones((129, 90))), pkg.FilterSpec(), engine="bst", n=64)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("nt,nth", [(3200, 2048), (2048, 3200)])
+def test_paper_lnls_sizes(pkg, nt, nth):
+    """The paper's motivating workload (reconstructions from 3200 x 2048
+    datasets), both orientations, FBP to 2048^2 against the oracle.
+    3200 bins x 2048 angles: ns = 1600, nrho = 6096 -> a 16384-point rho FFT and an
+    8192-point ramp embedding; 2048 bins x 3200 angles: nphi = 6400 -> Bluestein row DFTs
+    on 16384-point convolutions."""
+    g = phantoms.sinogram(4242 + nt, nt, nth, 50, 0.01, 0.3, 0.01)
+    plan = pkg.get_plan(nt, nth, 2048, None, None, (0.0, 1.0))
+    assert (plan.info["L"], plan.info["M"]) == ((16384, 8192) if nt == 3200 else (8192, 4096))
+    if nth == 3200:
+        assert plan.info["generic"] == 1 and plan.info["MB"] == 16384
+    out = pkg.fbp_batch(dev(g)[None], pkg.FilterSpec(), 2048)[0].cpu().numpy()
+    ref = O.fbp_logpolar(g.astype(np.float64), 2048)
+    assert report(f"paper size {nt}x{nth} fbp -> 2048", out, ref) <= RTOL
+    bp = pkg.logpolar_backproject_batch(dev(g)[None], 2048)[0].cpu().numpy()
+    assert report(f"paper size {nt}x{nth} bp -> 2048", bp, O.logpolar_backproject(g.astype(np.float64), 2048)) <= RTOL
 
 
 @pytest.mark.parametrize("nt,nth,n,filt", [(129, 90, 64, False), (255, 128, 128, True), (301, 200, 150, False)])
