@@ -218,8 +218,11 @@ k_bst_grid_x(const __grid_constant__ CUtensorMap xmap, const float2* __restrict_
   const int HB = big / 2;
   extern __shared__ __align__(16) float2 smem_b2_raw[];
   float2* smem_b2 = smem_b2_raw + ((1024u - (smem_u32(smem_b2_raw) & 1023u)) & 1023u) / sizeof(float2);
-  float2* stg = smem_b2;                                   // [n][TR]
-  float2* buf = stg + (size_t)n * TR + (threadIdx.x / T) * padded_len(BIG);
+  // [n][TR]; with TMA stores the staging spans whole 256-row boxes (the last box's clipped rows
+  // stay inside this CTA's allocation)
+  const int nst = TMA_OUT ? (n + 255) / 256 * 256 : n;
+  float2* stg = smem_b2;
+  float2* buf = stg + (size_t)nst * TR + (threadIdx.x / T) * padded_len(BIG);
   __shared__ double red[32];
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int ky0 = blockIdx.x * TR;
@@ -376,8 +379,9 @@ k_bst_grid_y(const __grid_constant__ CUtensorMap omap, const float2* __restrict_
   extern __shared__ __align__(16) float2 smem_b3_raw[];
   // 1024-byte aligned (TMA swizzle atoms), offset from the shared symbol to stay in the shared window
   float2* smem_b3 = smem_b3_raw + ((1024u - (smem_u32(smem_b3_raw) & 1023u)) & 1023u) / sizeof(float2);
+  const int nst = TMA_OUT ? (n + 255) / 256 * 256 : n;  // whole 256-row TMA boxes (see k_bst_grid_x)
   float* stg = reinterpret_cast<float*>(smem_b3);  // [n][SP]
-  float2* buf = smem_b3 + ((size_t)n * SP + 1) / 2 + (threadIdx.x / T) * padded_len(BIG);
+  float2* buf = smem_b3 + ((size_t)nst * SP + 1) / 2 + (threadIdx.x / T) * padded_len(BIG);
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int x0 = blockIdx.x * TC;
   const int b = blockIdx.y;
@@ -525,7 +529,8 @@ cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, flo
   {
     CUtensorMap xm{};
     const bool tma = (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (hb % 2) == 0 && encode_spectra_x_map(&xm, X, hb, d.n, batch);
-    const size_t smem = 1024 + ((size_t)d.n * TR + (size_t)GX * padded_len(N)) * sizeof(float2);
+    const size_t nst = tma ? ((size_t)d.n + 255) / 256 * 256 : (size_t)d.n;  // whole TMA store boxes
+    const size_t smem = 1024 + (nst * TR + (size_t)GX * padded_len(N)) * sizeof(float2);
     auto k = tma ? k_bst_grid_x<N, TR, GX, GEN, true> : k_bst_grid_x<N, TR, GX, GEN, false>;
     cudaError_t e = prep(k, smem);
     if (e) return e;
@@ -539,7 +544,8 @@ cudaError_t grid_impl(const BstDims& d, const BstTables& t, const float2* P, flo
     constexpr int GY = G > TC / 2 ? TC / 2 : G;
     CUtensorMap om{};
     const bool tma = (reinterpret_cast<uintptr_t>(img) & 15) == 0 && (d.n % 4) == 0 && encode_image_map(&om, img, d.n, batch);
-    const size_t smem = 1024 + (((size_t)d.n * (tma ? TC : TC + 1) + 1) / 2 + (size_t)GY * padded_len(N)) * sizeof(float2);
+    const size_t nst = tma ? ((size_t)d.n + 255) / 256 * 256 : (size_t)d.n;  // whole TMA store boxes
+    const size_t smem = 1024 + ((nst * (tma ? TC : TC + 1) + 1) / 2 + (size_t)GY * padded_len(N)) * sizeof(float2);
     auto k = tma ? k_bst_grid_y<N, TC, GY, GEN, true> : k_bst_grid_y<N, TC, GY, GEN, false>;
     cudaError_t e = prep(k, smem);
     if (e) return e;

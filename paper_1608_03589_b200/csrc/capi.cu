@@ -55,6 +55,16 @@ struct DeviceGuard {
 
 size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
+
+// Error exit of a host pipeline: copies already queued on the three streams still read the
+// caller's host buffers, so wait for them before handing the (first) error back.
+int drain_streams(cudaStream_t a, cudaStream_t b, cudaStream_t c, int rc) {
+  if (a) cudaStreamSynchronize(a);
+  if (b) cudaStreamSynchronize(b);
+  if (c) cudaStreamSynchronize(c);
+  return rc;
+}
+
 }  // namespace
 
 struct lpbp_plan {
@@ -516,25 +526,24 @@ int lpbp_execute_host(lpbp_plan* P, const float* sino_host, float* img_host, int
     if (ci >= 2) cudaStreamWaitEvent(pp.s_in, pp.ev_comp[slot], 0);
     e = cudaMemcpyAsync(pp.in[slot], sino_host + (size_t)off * (in_slice / sizeof(float)), in_slice * c,
                         cudaMemcpyHostToDevice, pp.s_in);
-    if (e) return cuda_fail(e, "H2D");
+    if (e) return drain_streams(pp.s_in, pp.s_comp, pp.s_out, cuda_fail(e, "H2D"));
     cudaEventRecord(pp.ev_in[slot], pp.s_in);
     cudaStreamWaitEvent(pp.s_comp, pp.ev_in[slot], 0);
     if (ci >= 2) cudaStreamWaitEvent(pp.s_comp, pp.ev_out[slot], 0);
     const int64_t before = g_launches;
     int rc = run_chunk(P, pp.in[slot], pp.out[slot], c, static_cast<char*>(pp.ws), pp.s_comp, false, nullptr);  // cudaMalloc'd: aligned
-    if (rc) return rc;
+    if (rc) return drain_streams(pp.s_in, pp.s_comp, pp.s_out, rc);
     (void)before;
     cudaEventRecord(pp.ev_comp[slot], pp.s_comp);
     cudaStreamWaitEvent(pp.s_out, pp.ev_comp[slot], 0);
     e = cudaMemcpyAsync(img_host + (size_t)off * (out_slice / sizeof(float)), pp.out[slot], out_slice * c,
                         cudaMemcpyDeviceToHost, pp.s_out);
-    if (e) return cuda_fail(e, "D2H");
+    if (e) return drain_streams(pp.s_in, pp.s_comp, pp.s_out, cuda_fail(e, "D2H"));
     cudaEventRecord(pp.ev_out[slot], pp.s_out);
   }
   cudaError_t e = cudaStreamSynchronize(pp.s_out);
-  if (e) return cuda_fail(e, "execute_host sync");
-  e = cudaStreamSynchronize(pp.s_comp);
-  if (e) return cuda_fail(e, "execute_host sync");
+  if (e == cudaSuccess) e = cudaStreamSynchronize(pp.s_comp);
+  if (e) return drain_streams(pp.s_in, pp.s_comp, pp.s_out, cuda_fail(e, "execute_host sync"));
   return LPBP_OK;
 }
 
@@ -758,24 +767,24 @@ int host_pipeline(HostPipe& pp, int batch, int chunk, size_t in_slice, size_t ou
     if (ci >= 2) cudaStreamWaitEvent(pp.s_in, pp.ev_comp[slot], 0);  // slot's previous input consumed
     cudaError_t e = cudaMemcpyAsync(pp.in[slot], sino_host + (size_t)off * in_slice, in_slice * c * sizeof(float),
                                     cudaMemcpyHostToDevice, pp.s_in);
-    if (e) return cuda_fail(e, "H2D");
+    if (e) return drain_streams(pp.s_in, pp.s_comp, pp.s_out, cuda_fail(e, "H2D"));
     cudaEventRecord(pp.ev_in[slot], pp.s_in);
     cudaStreamWaitEvent(pp.s_comp, pp.ev_in[slot], 0);
     if (ci >= 2) cudaStreamWaitEvent(pp.s_comp, pp.ev_out[slot], 0);  // slot's previous output copied out
     g_launches = 0;
     const int rc = run(pp.in[slot], pp.out[slot], c, pp.ws, pp.ws_bytes, pp.s_comp);
-    if (rc) return rc;
+    if (rc) return drain_streams(pp.s_in, pp.s_comp, pp.s_out, rc);
     launches += g_launches;
     cudaEventRecord(pp.ev_comp[slot], pp.s_comp);
     cudaStreamWaitEvent(pp.s_out, pp.ev_comp[slot], 0);
     e = cudaMemcpyAsync(img_host + (size_t)off * out_slice, pp.out[slot], out_slice * c * sizeof(float),
                         cudaMemcpyDeviceToHost, pp.s_out);
-    if (e) return cuda_fail(e, "D2H");
+    if (e) return drain_streams(pp.s_in, pp.s_comp, pp.s_out, cuda_fail(e, "D2H"));
     cudaEventRecord(pp.ev_out[slot], pp.s_out);
   }
   cudaError_t e = cudaStreamSynchronize(pp.s_out);
   if (e == cudaSuccess) e = cudaStreamSynchronize(pp.s_comp);
-  if (e) return cuda_fail(e, "execute_host sync");
+  if (e) return drain_streams(pp.s_in, pp.s_comp, pp.s_out, cuda_fail(e, "execute_host sync"));
   g_launches = launches;
   return LPBP_OK;
 }
@@ -1180,6 +1189,12 @@ int bst_chunk(const lpbp_bst_plan* P, const float* in, float* out, int c, char* 
     for (auto& ev : rec.ev) ev = Pm->take_event();
     cudaEventRecord(rec.ev[0], st);
   }
+  // error exits hand the events taken for this chunk back to the pool
+  auto fail_chunk = [&](cudaError_t err, const char* where) {
+    if (prof)
+      for (cudaEvent_t ev : rec.ev) Pm->ev_pool.push_back(ev);
+    return launch_fail(err, where);
+  };
   if (h.p.filter && !spectra_only) {
     rec.ramp = true;
     e = lpbp::launch_ramp(P->rd, P->rt, in, filt, c, st);  // column tiles need ntheta % TC == 0
@@ -1187,18 +1202,18 @@ int bst_chunk(const lpbp_bst_plan* P, const float* in, float* out, int c, char* 
       (void)cudaGetLastError();
       e = lpbp::launch_ramp_generic(P->rd, P->rt, in, filt, c, st);
     }
-    if (e) return launch_fail(e, "bst ramp_filter");
+    if (e) return fail_chunk(e, "bst ramp_filter");
     ++g_launches;
     src = filt;
   }
   if (prof) cudaEventRecord(rec.ev[1], st);
   e = lpbp::launch_bst_radial(P->d, P->t, src, Pw, acc, c, st);
-  if (e) return launch_fail(e, "bst_radial");
+  if (e) return fail_chunk(e, "bst_radial");
   ++g_launches;
   if (spectra_only) return LPBP_OK;
   if (prof) cudaEventRecord(rec.ev[2], st);
   e = lpbp::launch_bst_grid(P->d, P->t, Pw, Xw, out, acc, c, st, prof ? rec.ev[3] : nullptr);
-  if (e) return launch_fail(e, "bst_grid");
+  if (e) return fail_chunk(e, "bst_grid");
   g_launches += 2;
   if (prof) {
     cudaEventRecord(rec.ev[4], st);
