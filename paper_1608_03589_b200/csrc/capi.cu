@@ -346,6 +346,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     rc = rc ? rc : P->upload(h.ramp, &P->t.ramp);
     rc = rc ? rc : P->upload(h.ab, reinterpret_cast<const lpbp::I2**>(&P->t.ab));
     rc = rc ? rc : P->upload(h.wab, reinterpret_cast<const lpbp::F4**>(&P->t.wab));
+    rc = rc ? rc : P->upload(h.abw, reinterpret_cast<const uint32_t**>(&P->t.abw));
     rc = rc ? rc : P->upload(h.ki, &P->t.ki);
     rc = rc ? rc : P->upload(h.wi, reinterpret_cast<const lpbp::F2**>(&P->t.wi));
     rc = rc ? rc : P->upload(h.kw, &P->t.kw);

@@ -320,15 +320,15 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
 template <int L, bool PRUNE>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, (L >= 16384 ? 1 : 2))
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int gp, int ns, int nrho, int row_lo,
-           int nrho_pad, int nh, const int2* __restrict__ ab, const float4* __restrict__ wab,
+           int nrho_pad, int nh, const uint2* __restrict__ abw,
            const uint32_t* __restrict__ kw, const float2* __restrict__ khat, const float2* __restrict__ tw) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
   __shared__ __align__(8) uint64_t bar;
   float2* buf = smem_k3;                          // padded_len(L)
   float2* p = buf + padded_len(L);                // ns
-  float2* gcol = p + ((ns + 1) & ~1);             // nt (16-B aligned); refilled as soon as the row mix is done
-  uint32_t* kws = reinterpret_cast<uint32_t*>(gcol + gp);  // nrho packed log-polar taps, same for every column
+  float2* gcol = p + ((ns + 1) & ~1);             // gp + 2 (16-B aligned); refilled as soon as the row mix is done
+  uint32_t* kws = reinterpret_cast<uint32_t*>(gcol + gp + 2);  // nrho packed log-polar taps, same for every column
   const int m = blockIdx.x;
   const float sg = (m & 1) ? -1.f : 1.f;
   const int ti = threadIdx.x;
@@ -350,19 +350,37 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   }
   if (!kw_bulk)
     for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
+  if (ti < 2) gcol[gp + ti] = make_float2(0.f, 0.f);  // rows nt, nt+1 of the packed taps read zero (visible
+                                                       // after the first mbarrier wait's __syncthreads below)
+  __syncthreads();
 
   for (int b = 0; b < batch; ++b) {
     mbar_wait(&bar, b & 1);
     const float2* col = gcol;
-    for (int k = ti; k < ns; k += T) {
-      const int2 A = __ldg(ab + k);
-      const float4 W = __ldg(wab + k);
-      const float2 g0 = col[A.x], g1 = col[A.x + 1];
-      const float2 h0 = col[A.y], h1 = col[A.y + 1];
-      float2 v;
-      v.x = fmaf(W.x, g0.x, W.y * g1.x) + sg * fmaf(W.z, h0.x, W.w * h1.x);
-      v.y = fmaf(W.x, g0.y, W.y * g1.y) + sg * fmaf(W.z, h0.y, W.w * h1.y);
-      p[k] = v;
+    // p[k] = (1 - wa) G[a] + wa G[a+1] + (-1)^m ((1 - wb) G[b] + wb G[b+1]); taps for 4 rows in flight
+    constexpr float kW = 1.f / 524288.f;
+#pragma unroll 1
+    for (int k0 = 0; k0 < ns; k0 += 4 * T) {
+      uint2 e[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + ti + u * T;
+        e[u] = k < ns ? __ldg(abw + k) : make_uint2(0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + ti + u * T;
+        if (k < ns) {
+          const int a = (int)(e[u].x & 0x1FFFu), b = (int)(e[u].y & 0x1FFFu);
+          const float wa = (float)(e[u].x >> 13) * kW, wb = (float)(e[u].y >> 13) * kW;
+          const float2 g0 = col[a], g1 = col[a + 1];
+          const float2 h0 = col[b], h1 = col[b + 1];
+          float2 v;
+          v.x = fmaf(wa, g1.x, fmaf(-wa, g0.x, g0.x)) + sg * fmaf(wb, h1.x, fmaf(-wb, h0.x, h0.x));
+          v.y = fmaf(wa, g1.y, fmaf(-wa, g0.y, g0.y)) + sg * fmaf(wb, h1.y, fmaf(-wb, h0.y, h0.y));
+          p[k] = v;
+        }
+      }
     }
     __syncthreads();
     if (ti == 0 && b + 1 < batch) {  // the column is consumed: fetch the next slice's across the transforms
@@ -529,12 +547,18 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 // region plus a carry copy of the previous quad's last row.  The log-polar image
 // never reaches HBM and no row is transformed twice inside a unit.
 // ---------------------------------------------------------------------------
+#ifndef K45_S
+#define K45_S 4
+#endif
+#ifndef K45_UQ
+#define K45_UQ 16
+#endif
 template <int NPHI>
 struct FusedShape {
-  static constexpr int S = 4;       // log-polar rows per step (one packed pair per FFT group); 2 measured slower
+  static constexpr int S = K45_S;   // log-polar rows per step (one packed pair per FFT group)
   static constexpr int G = S / 2;   // FFT groups
   static constexpr int NR = 3;      // ring regions (previous, current, next step)
-  static constexpr int UQ = 16;     // steps per work unit
+  static constexpr int UQ = K45_UQ; // steps per work unit
   // spectra m = 0 .. NPHI/2: NFULL boxes of 256 rows + one 1-row tail box
   static constexpr int NFULL = (NPHI / 2) / 256;
   static_assert(NFULL * 256 + 1 == NPHI / 2 + 1, "tail box is one row");
@@ -542,13 +566,13 @@ struct FusedShape {
   static constexpr int HALF = (padded_len(NPHI) + 15) / 16 * 16 + 8;
   // group g's two spectra rows arrive as [m][2] at g * IN_PITCH (128-B aligned, inside its own half)
   static constexpr int IN_PITCH = (HALF + 15) / 16 * 16;
-  static_assert(IN_PITCH + 2 * (NPHI / 2 + 1) <= G * HALF, "group input inside its FFT half");
+  static_assert((G - 1) * IN_PITCH + 2 * (NPHI / 2 + 1) <= G * HALF, "group input inside its FFT half");
   static constexpr int QREG = (G * HALF + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
-  static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 128;  // regions + barriers
+  static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 128 + 4 * (UQ + 2);  // regions + barriers + unit slot, offsets
 };
 
 template <int NPHI>
-__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 1)
+__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, (FusedShape<NPHI>::G == 1 ? 2 : 1))
 k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ytail,
                 float* __restrict__ img, int nrho, int n, int nq,
                 int row_min, int nsteps, int batch, int* __restrict__ counter, const uint32_t* __restrict__ step_off,
@@ -564,6 +588,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
   extern __shared__ __align__(128) float2 smem_k45[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NR * QREG);  // NR
   int* unit_slot = reinterpret_cast<int*>(bars + NR);
+  uint32_t* soff = reinterpret_cast<uint32_t*>(unit_slot + 1);  // [UQ + 1] entry offsets of the unit's steps
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   const int units_per_slice = (nsteps + UQ - 1) / UQ;
   const int total_units = units_per_slice * batch;
@@ -602,7 +627,6 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     if (threadIdx.x == 0) *unit_slot = atomicAdd(counter, 1);
     __syncthreads();
     const int u = *unit_slot;
-    __syncthreads();
     if (u >= total_units) break;
     const int slice = u % batch;
     const int k0 = (units_per_slice - 1 - u / batch) * UQ;  // outermost units first
@@ -610,6 +634,11 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     const int ks = k0 > 0 ? k0 - 1 : 0;  // the previous step only feeds its last row
     if (threadIdx.x < 32)
       for (int q = ks; q < min(ks + 2, k1); ++q) issue((q - ks) % NR, q, slice);
+    // the unit's pixel-entry ranges, once (a per-step load would put an L2 round trip in front of
+    // every step's entry prefetch)
+    if (threadIdx.x >= 32 && threadIdx.x <= 32 + UQ && k0 + (int)threadIdx.x - 32 <= k1)
+      soff[threadIdx.x - 32] = __ldg(step_off + k0 + threadIdx.x - 32);
+    __syncthreads();  // soff visible; every thread has read unit_slot
     float* out = img + (size_t)slice * n * n;
 
 #pragma unroll 1
@@ -620,7 +649,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       const int r0 = row_min + S * kk;
       // first pixel entries of this step: loads in flight across the transforms
       const bool rd = kk >= k0;
-      const uint32_t e0 = rd ? __ldg(step_off + kk) : 0u, e1 = rd ? __ldg(step_off + kk + 1) : 0u;
+      const uint32_t e0 = rd ? soff[kk - k0] : 0u, e1 = rd ? soff[kk - k0 + 1] : 0u;
       uint4 pre = make_uint4(0x80000000u, 0, 0, 0), pre2 = pre;
       const uint32_t ep = e0 + threadIdx.x;
       if (ep < e1) pre = __ldg(entries + ep);
@@ -783,6 +812,7 @@ k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt,
     const float2 z = Z[m], w = Z[m == 0 ? 0 : nphi - m];
     dst[(size_t)m * gp] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
     if (hb) dst[(size_t)m * gp + 1] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+    else if (tb < gp) dst[(size_t)m * gp + 1] = make_float2(0.f, 0.f);  // odd nt: the pad column reads zero (K3 taps)
   }
 }
 
@@ -952,12 +982,12 @@ template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
                       cudaStream_t s) {
   const int gp = d.gp > 0 ? d.gp : d.nt;
-  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp) * sizeof(float2) + (size_t)d.nrho * 4;
+  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp + 2) * sizeof(float2) + (size_t)d.nrho * 4;
   // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
   auto k = (2 * d.nrho <= L) ? k_rho_conv<L, true> : k_rho_conv<L, false>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
-  k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, gp, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.ab, t.wab,
+  k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, gp, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.abw,
                                               t.kw, t.khat, t.tw_rho);
   return cudaGetLastError();
 }

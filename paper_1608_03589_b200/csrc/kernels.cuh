@@ -19,6 +19,7 @@ struct DevTables {
   const float* ramp;      // [M] real even filter response incl. 1/M (FBP only)
   const int2* ab;         // [ns] t-rows (a_k, b_k) of the semi-polar lerp
   const float4* wab;      // [ns] weights (wa0, wa1, wb0, wb1)
+  const uint2* abw;       // [ns] packed (a | w1a << 13, b | w1b << 13), plan_host abw
   const int* ki;          // [nrho] s-row of the log-polar lerp
   const float2* wi;       // [nrho] weights (w0, w1)
   const uint32_t* kw;     // [nrho] packed ki | w1 * 2^20 << 11 (K3 stages it in shared memory)

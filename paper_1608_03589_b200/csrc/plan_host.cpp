@@ -259,6 +259,21 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
     h.ab[k] = I2{a, b};
     h.wab[k] = F4{(float)wa0, (float)wa1, (float)wb0, (float)wb1};
   }
+  // packed semi-polar taps for K3 (8 bytes per s-row instead of 24): row floor(f) with weights
+  // (1 - w, w); f = (+-s + 1)/dt lies in [0, nt], so rows nt and nt + 1 (zero in K3's column
+  // buffer) stand in for the reference's out-of-range zeros; w keeps 19 fractional bits
+  if (nt > 8191) return "nt too large for the packed semi-polar taps (nt < 8192)";
+  h.abw.resize(2 * (size_t)ns);
+  for (int k = 0; k < ns; ++k) {
+    const double s = (double)k / (ns - 1.0);
+    for (int side = 0; side < 2; ++side) {
+      const double f = ((side ? -s : s) + 1.0) / dt;
+      const double fl = std::floor(f);
+      long long wq = std::llround((f - fl) * 524288.0);
+      if (wq > 524287) wq = 524287;
+      h.abw[2 * (size_t)k + side] = (uint32_t)fl | ((uint32_t)wq << 13);
+    }
+  }
   // --- log-polar taps (grids.py:332-347): rho_i = rho0 + (i+1) drho, f = e^rho (ns-1)
   h.ki.resize(nrho);
   h.wi.resize(nrho);

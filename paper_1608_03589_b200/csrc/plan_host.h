@@ -34,6 +34,7 @@ struct HostPlan {
   std::vector<float> ramp;
   std::vector<I2> ab;
   std::vector<F4> wab;
+  std::vector<uint32_t> abw;  // [2 ns] packed semi-polar taps for K3: a | w1a << 13, b | w1b << 13 (rows past nt read zero)
   std::vector<int32_t> ki;
   std::vector<uint32_t> kw;  // [nrho] packed log-polar tap: ki | round(w1 * 2^20) << 11 (w0 = 1 - w1)
   std::vector<uint32_t> qidx;
