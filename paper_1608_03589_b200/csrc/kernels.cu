@@ -291,8 +291,10 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
       const float2 z = buf[pad16(m)];
       const float2 w = buf[pad16((NPHI - m) & (NPHI - 1))];
       const int sw = ((m >> 2) & 1) << 1;
-      stg[m * TR + ((2 * gi) ^ sw)] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
-      stg[m * TR + ((2 * gi + 1) ^ sw)] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+      // rows 2 gi and 2 gi + 1 sit side by side in the swizzled [m][4] staging (sw is even): one
+      // 16-byte store (a warp's 32 stores fill 8 distinct 16-byte bank groups: 4 wavefronts, no conflict)
+      *reinterpret_cast<float4*>(stg + m * TR + ((2 * gi) ^ sw)) =
+          make_float4(0.5f * (z.x + w.x), 0.5f * (z.y - w.y), 0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
     }
     __syncthreads();
     if (threadIdx.x <= NFULL) {  // one TMA store box per lane of warp 0
