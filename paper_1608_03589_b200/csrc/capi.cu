@@ -303,6 +303,8 @@ int run_batched(const lpbp_plan* Pc, const float* in, float* out, int batch, voi
 
 }  // namespace
 
+static_assert(lpbp::kMaxUnitBands == lpbp::kFusedMaxUnit, "host work units must fit the fused kernel's arrays");
+
 extern "C" {
 
 int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
@@ -357,6 +359,8 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     if (!rc) {
       rc = P->upload(P->h.band_off, &P->t.band_off);
       rc = rc ? rc : P->upload(P->h.band_packed, &P->t.band_entries);
+      rc = rc ? rc : P->upload(P->h.band_need, &P->t.band_need);
+      rc = rc ? rc : P->upload(P->h.units, &P->t.units);
     }
     if (rc) {
       std::string msg = g_last_error;
@@ -380,6 +384,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   d.out_scale = (float)h.out_scale;
   d.row_min = h.row_min;
   d.nbands = h.nbands;
+  d.nunits = h.nunits;
   d.band_rows = h.band_rows;
   d.generic = h.generic ? 1 : 0;
   d.MB = h.MB;
@@ -610,6 +615,8 @@ int lpbp_plan_table(const lpbp_plan* P, const char* which, void* dst, size_t cap
   if (!std::strcmp(which, "bhat_i")) return copy_vec(h.bhat_i);    // float2 MB
   if (!std::strcmp(which, "band_off")) return copy_vec(h.band_off);          // uint32 nbands+1
   if (!std::strcmp(which, "band_entries")) return copy_vec(h.band_entries);  // uint32
+  if (!std::strcmp(which, "band_need")) return copy_vec(h.band_need);        // uint32 nbands
+  if (!std::strcmp(which, "units")) return copy_vec(h.units);                // uint32 pairs [k0, k1), outermost first
   return fail(LPBP_EINVAL, std::string("unknown table ") + which);
 }
 

@@ -552,15 +552,12 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 #ifndef K45_S
 #define K45_S 4
 #endif
-#ifndef K45_UQ
-#define K45_UQ 16
-#endif
 template <int NPHI>
 struct FusedShape {
   static constexpr int S = K45_S;   // log-polar rows per step (one packed pair per FFT group)
   static constexpr int G = S / 2;   // FFT groups
   static constexpr int NR = 3;      // ring regions (previous, current, next step)
-  static constexpr int UQ = K45_UQ; // steps per work unit
+  static constexpr int UQ = kFusedMaxUnit;  // max steps per work unit (plan_host kMaxUnitBands)
   // spectra m = 0 .. NPHI/2: NFULL boxes of 256 rows + one 1-row tail box
   static constexpr int NFULL = (NPHI / 2) / 256;
   static_assert(NFULL * 256 + 1 == NPHI / 2 + 1, "tail box is one row");
@@ -570,7 +567,7 @@ struct FusedShape {
   static constexpr int IN_PITCH = (HALF + 15) / 16 * 16;
   static_assert((G - 1) * IN_PITCH + 2 * (NPHI / 2 + 1) <= G * HALF, "group input inside its FFT half");
   static constexpr int QREG = (G * HALF + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
-  static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 128 + 4 * (UQ + 2);  // regions + barriers + unit slot, offsets
+  static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 128 + 4 * (2 * UQ + 4);  // regions + barriers + unit slot, offsets, step list
 };
 
 template <int NPHI>
@@ -578,6 +575,7 @@ __global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, 
 k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ytail,
                 float* __restrict__ img, int nrho, int n, int nq,
                 int row_min, int nsteps, int batch, int* __restrict__ counter, const uint32_t* __restrict__ step_off,
+                const uint32_t* __restrict__ step_need, const uint2* __restrict__ units, int nunits,
                 const uint4* __restrict__ entries, float scale, const float2* __restrict__ tw) {
   using FS = FusedShape<NPHI>;
   constexpr int S = FS::S, G = FS::G, NR = FS::NR, UQ = FS::UQ, QREG = FS::QREG, HALF = FS::HALF;
@@ -591,9 +589,11 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NR * QREG);  // NR
   int* unit_slot = reinterpret_cast<int*>(bars + NR);
   uint32_t* soff = reinterpret_cast<uint32_t*>(unit_slot + 1);  // [UQ + 1] entry offsets of the unit's steps
+  int* ulist = reinterpret_cast<int*>(soff + UQ + 1);            // [UQ + 1] the unit's needed steps, in order,
+                                                                 // then their count at ulist[UQ + 1]
+  static_assert(UQ + 1 <= 32, "one lane per step of a unit");
   const int gi = threadIdx.x / T, ti = threadIdx.x % T;
-  const int units_per_slice = (nsteps + UQ - 1) / UQ;
-  const int total_units = units_per_slice * batch;
+  const int total_units = nunits * batch;
   const int c = n / 2;
 
   if (threadIdx.x == 0) {
@@ -631,22 +631,37 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     const int u = *unit_slot;
     if (u >= total_units) break;
     const int slice = u % batch;
-    const int k0 = (units_per_slice - 1 - u / batch) * UQ;  // outermost units first
-    const int k1 = min(k0 + UQ, nsteps);
+    const uint2 ub = __ldg(units + u / batch);  // outermost (heaviest) units first, slices interleaved
+    const int k0 = (int)ub.x, k1 = (int)ub.y;
     const int ks = k0 > 0 ? k0 - 1 : 0;  // the previous step only feeds its last row
-    if (threadIdx.x < 32)
-      for (int q = ks; q < min(ks + 2, k1); ++q) issue((q - ks) % NR, q, slice);
+    // steps none of whose rows any pixel taps are neither loaded nor transformed: warp 0 compacts
+    // the unit's needed steps (ks .. k1-1) by ballot and issues the first two
+    int nlist;
+    if (threadIdx.x < 32) {
+      const int st = ks + (int)threadIdx.x;
+      const bool nd = st < k1 && __ldg(step_need + st) != 0u;
+      const unsigned bal = __ballot_sync(0xFFFFFFFFu, nd);
+      if (nd) ulist[__popc(bal & ((1u << threadIdx.x) - 1u))] = st;
+      nlist = __popc(bal);
+      __syncwarp();
+      for (int pos = 0; pos < min(2, nlist); ++pos) issue(pos % NR, ulist[pos], slice);
+    }
     // the unit's pixel-entry ranges, once (a per-step load would put an L2 round trip in front of
     // every step's entry prefetch)
     if (threadIdx.x >= 32 && threadIdx.x <= 32 + UQ && k0 + (int)threadIdx.x - 32 <= k1)
       soff[threadIdx.x - 32] = __ldg(step_off + k0 + threadIdx.x - 32);
-    __syncthreads();  // soff visible; every thread has read unit_slot
+    if (threadIdx.x == 0) ulist[UQ + 1] = nlist;
+    __syncthreads();  // soff, ulist, the list length visible; every thread has read unit_slot
+    nlist = ulist[UQ + 1];
     float* out = img + (size_t)slice * n * n;
 
+    // a skipped step's rows are tapped by no pixel, so Qprev (the previous processed step) is
+    // read only when that step is kk - 1
 #pragma unroll 1
-    for (int kk = ks; kk < k1; ++kk) {
-      const int R = (kk - ks) % NR;
-      const float2* Qprev = smem_k45 + ((kk - ks + NR - 1) % NR) * QREG;
+    for (int pos = 0; pos < nlist; ++pos) {
+      const int kk = ulist[pos];
+      const int R = pos % NR;
+      const float2* Qprev = smem_k45 + ((pos + NR - 1) % NR) * QREG;
       float2* Q = smem_k45 + R * QREG;
       const int r0 = row_min + S * kk;
       // first pixel entries of this step: loads in flight across the transforms
@@ -747,7 +762,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
         }
       }
       __syncthreads();  // region of kk-1 is free now: refill it with step kk+2
-      if (threadIdx.x < 32 && kk + 2 < k1) issue((kk + 2 - ks) % NR, kk + 2, slice);
+      if (threadIdx.x < 32 && pos + 2 < nlist) issue((pos + 2) % NR, ulist[pos + 2], slice);
     }
   }
 }
@@ -1234,13 +1249,14 @@ cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
   if (e) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), s);
   if (e) return e;
-  const int units = (d.nbands + FS::UQ - 1) / FS::UQ * batch;
+  const int units = d.nunits * batch;
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, FS::G * FftPlan<NPHI, true>::T, FS::SMEM);
   const int slots = d.nsm * (occ > 0 ? occ : 1);
   const int grid = units < slots ? units : slots;
   k<<<grid, FS::G * FftPlan<NPHI, true>::T, FS::SMEM, s>>>(map, tail, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, batch,
-                                                          counter, t.band_off,
+                                                          counter, t.band_off, t.band_need,
+                                                          reinterpret_cast<const uint2*>(t.units), d.nunits,
                                                           reinterpret_cast<const uint4*>(t.band_entries),
                                                           d.out_scale, t.tw_phi);
   return cudaGetLastError();

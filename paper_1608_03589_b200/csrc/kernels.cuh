@@ -29,6 +29,8 @@ struct DevTables {
   const float2* naive_cs; // [ntheta] (cos, sin) * nt/(2n) for the direct backprojector
   const uint32_t* band_off;      // [nbands+1] fused readout: entry range per band
   const uint32_t* band_entries;  // per band: uint4 {qq | bit31 zero, qidx, wi, wj} (plan_host band_packed)
+  const uint32_t* band_need;     // [nbands] 1 = some pixel taps one of the band's rows
+  const uint32_t* units;         // [nunits][2] fused work units: band range [k0, k1), outermost first
   // generic sizes (Bluestein)
   const float2* chirp;   // [nphi]
   const float2* bhat_f;  // [MB]
@@ -39,6 +41,7 @@ struct DevTables {
 struct Dims {
   int nt, ntheta, n, ns, nphi, nh, nrho, nrho_pad, L, M, nq;
   int row_min, nbands, band_rows;  // fused inverse-DFT + readout quads (band_rows = 4)
+  int nunits;                      // fused work units (plan_host build_bands)
   int nsm;                         // SMs of the plan's device (persistent grids)
   int generic, MB;                 // generic-size path (Bluestein length-nphi DFTs via MB-point convolutions)
   int gp;                          // column pitch of the row spectra G[m][.] (nt rounded up to even: TMA bulk
@@ -60,6 +63,7 @@ cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y,
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Y, float* img, int batch,
                                  int* counter, cudaStream_t s);
 int fused_band_rows(int nphi);
+constexpr int kFusedMaxUnit = 24;  // longest fused work unit in bands (per-unit arrays, one lane per band + 1)
 cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, float* img, int batch, cudaStream_t s);
 
 cudaError_t launch_radon_ellipses(const double* params, int K, int nt, int ntheta, int batch, float* out,

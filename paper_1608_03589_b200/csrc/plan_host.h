@@ -43,6 +43,15 @@ struct HostPlan {
   // with i0 in [r0 - 1, r0 + 3) (bit 31 set = write zero), band_off[b..b+1).
   int band_rows = 0, row_min = 0, nbands = 0;
   std::vector<uint32_t> band_entries, band_off;
+  // band_need[b] = 1 iff some pixel taps one of band b's rows: the fused kernel neither loads nor
+  // transforms the others (~1/3 of the bands at 2048^2 lie between the discrete radii of the
+  // innermost pixels); zero-writes are dealt to needed bands only
+  std::vector<uint32_t> band_need;
+  // fused-kernel work units: contiguous band ranges [units[2u], units[2u+1]), outermost first, cut
+  // so each unit's cost (needed bands + pixel entries / unit_entry_equiv) is about unit_cost; at most
+  // kMaxUnitBands bands per unit
+  std::vector<uint32_t> units;
+  int nunits = 0;
   // self-contained 16-byte entries {qy | qx << 15 | zero flag << 31, qidx, wi bits, wj bits}
   std::vector<uint32_t> band_packed;
   // generic sizes (nphi not a power of two in [512, 4096], ...): Bluestein DFTs of
@@ -58,6 +67,7 @@ struct HostPlan {
 // Returns "" on success, else the error message (ValueError semantics).
 std::string build_host_plan(const HostPlanParams& p, HostPlan& out);
 // Fill band_* for bands of `band_rows` rows (needs qidx built).
+constexpr int kMaxUnitBands = 24;  // the fused kernel's per-unit arrays (one lane per band + 1)
 void build_bands(HostPlan& h, int band_rows);
 
 // fastbp.grids.adaptive_rho0 (grids.py:385-391)

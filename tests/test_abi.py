@@ -219,6 +219,22 @@ def test_fused_readout_bands_cover_every_pixel_once(nt, nth, n, rho0):
             np.add.at(writes.reshape(-1), pix, 1)
             zero.reshape(-1)[(iy * n + jx)[keep & z]] = True
     assert writes.min() == 1 and writes.max() == 1
+    # bands whose rows no pixel taps carry no entries (the fused kernel skips them); every tapped
+    # row's band is flagged
+    need = hp.table("band_need", np.uint32)
+    assert len(need) == i.nbands
+    assert np.all(off[1:][need == 0] == off[:-1][need == 0])
+    qv = qidx[qidx != 0xFFFFFFFF]
+    i0 = (qv & 0xFFFF).astype(np.int64)
+    for r in (i0, np.minimum(i0 + 1, i.nrho - 1)):
+        assert np.all(need[(r - i.row_min) // i.band_rows] == 1)
+    if (nt, n) == (2048, 2048):
+        assert need.sum() < 0.7 * i.nbands  # ~1/3 of the bands lie between the innermost pixels' radii
+    # work units: contiguous band ranges, outermost first, covering every band once, <= 24 bands each
+    units = hp.table("units", np.uint32).reshape(-1, 2).astype(np.int64)
+    assert units[0, 1] == i.nbands and units[-1, 0] == 0
+    assert np.all(units[:-1, 0] == units[1:, 1]) and np.all(units[:, 1] > units[:, 0])
+    assert np.all(units[:, 1] - units[:, 0] <= 24)
     xs = -1.0 + (np.arange(n) + 0.5) * (2.0 / n)
     X, Y = np.meshgrid(xs, xs)
     R = np.hypot(X, Y)
