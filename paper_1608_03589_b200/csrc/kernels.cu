@@ -603,7 +603,9 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
   uint32_t phase = 0;  // bit r: parity of the next wait on bars[r] (uniform across threads)
   // called by all lanes of warp 0: lane 0 arms the barrier, then one box per lane
   static_assert(G * (NFULL + 1) <= 32, "one TMA box per lane of warp 0");
-  auto issue = [&](int region, int step, int slice) {
+  // pf_k0 >= 0: also warm L2 with the step's pixel entries, their range read from soff (the unit
+  // starting at band pf_k0; no global round trip in front of the issuing warp)
+  auto issue = [&](int region, int step, int slice, int pf_k0) {
     const int lane = threadIdx.x;
     if (lane == 0) {
       fence_proxy_async_smem();  // order earlier generic accesses to the region before the TMA writes
@@ -616,8 +618,8 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       float2* dst = smem_k45 + region * QREG + g * FS::IN_PITCH + 2 * (bx * 256);
       if (bx < NFULL) tma_load_3d(dst, &ymap, c0, bx * 256, slice, &bars[region]);
       else tma_load_3d(dst, &ytail, c0, NFULL * 256, slice, &bars[region]);
-    } else if (lane == 31) {
-      const uint32_t a = __ldg(step_off + step), b = __ldg(step_off + step + 1);  // warm L2 with its pixels
+    } else if (lane == 31 && pf_k0 >= 0 && step >= pf_k0) {
+      const uint32_t a = soff[step - pf_k0], b = soff[step - pf_k0 + 1];
       if (b > a) prefetch_l2_bulk(entries + a, 16u * (b - a));
     }
   };
@@ -644,7 +646,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       if (nd) ulist[__popc(bal & ((1u << threadIdx.x) - 1u))] = st;
       nlist = __popc(bal);
       __syncwarp();
-      for (int pos = 0; pos < min(2, nlist); ++pos) issue(pos % NR, ulist[pos], slice);
+      for (int pos = 0; pos < min(2, nlist); ++pos) issue(pos % NR, ulist[pos], slice, -1);
     }
     // the unit's pixel-entry ranges, once (a per-step load would put an L2 round trip in front of
     // every step's entry prefetch)
@@ -762,7 +764,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
         }
       }
       __syncthreads();  // region of kk-1 is free now: refill it with step kk+2
-      if (threadIdx.x < 32 && pos + 2 < nlist) issue((pos + 2) % NR, ulist[pos + 2], slice);
+      if (threadIdx.x < 32 && pos + 2 < nlist) issue((pos + 2) % NR, ulist[pos + 2], slice, k0);
     }
   }
 }
