@@ -567,204 +567,222 @@ struct FusedShape {
   static constexpr int IN_PITCH = (HALF + 15) / 16 * 16;
   static_assert((G - 1) * IN_PITCH + 2 * (NPHI / 2 + 1) <= G * HALF, "group input inside its FFT half");
   static constexpr int QREG = (G * HALF + 15) / 16 * 16;  // float2, 128-B multiple (TMA destination)
-  static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 128 + 4 * (2 * UQ + 4);  // regions + barriers + unit slot, offsets, step list
+  static constexpr size_t SMEM = (size_t)NR * QREG * 8 + 2 * NR * 8 + 4 * 16 + 64;  // regions + full/empty + step descriptors
 };
 
 template <int NPHI>
-__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T, (FusedShape<NPHI>::G == 1 ? 2 : 1))
+__global__ void __launch_bounds__(FusedShape<NPHI>::G * FftPlan<NPHI, true>::T + 32, 1)
 k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap ytail,
                 float* __restrict__ img, int nrho, int n, int nq,
                 int row_min, int nsteps, int batch, int* __restrict__ counter, const uint32_t* __restrict__ step_off,
                 const uint32_t* __restrict__ step_need, const uint2* __restrict__ units, int nunits,
                 const uint4* __restrict__ entries, float scale, const float2* __restrict__ tw) {
   using FS = FusedShape<NPHI>;
-  constexpr int S = FS::S, G = FS::G, NR = FS::NR, UQ = FS::UQ, QREG = FS::QREG, HALF = FS::HALF;
+  constexpr int S = FS::S, G = FS::G, NR = FS::NR, QREG = FS::QREG, HALF = FS::HALF;
   constexpr int NFULL = FS::NFULL;
   static_assert(NR == 3, "ring = previous (its last row feeds the readout), current, next");
   constexpr int T = FftPlan<NPHI, true>::T;
+  constexpr int NC = G * T, NCW = NC / 32;  // consumer threads: the FFT groups, which also sample the readout
   constexpr int RPITCH = NPHI + 8;  // floats from row a to row b inside a group half (8-bank skew)
   static_assert(RPITCH + NPHI <= 2 * HALF, "row storage");
   constexpr uint32_t STEP_BYTES = (NFULL * 256 + 1) * S * 8;
+  static_assert(G * (NFULL + 1) <= 31, "one TMA box per producer lane, lane 31 prefetches entries");
   extern __shared__ __align__(128) float2 smem_k45[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_k45 + NR * QREG);  // NR
-  int* unit_slot = reinterpret_cast<int*>(bars + NR);
-  uint32_t* soff = reinterpret_cast<uint32_t*>(unit_slot + 1);  // [UQ + 1] entry offsets of the unit's steps
-  int* ulist = reinterpret_cast<int*>(soff + UQ + 1);            // [UQ + 1] the unit's needed steps, in order,
-                                                                 // then their count at ulist[UQ + 1]
-  static_assert(UQ + 1 <= 32, "one lane per step of a unit");
-  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_k45 + NR * QREG);  // [NR] region landed (TMA bytes)
+  uint64_t* empty = full + NR;                                         // [NR] region released by the consumers
+  int4* items = reinterpret_cast<int4*>(empty + NR);                   // [4] step descriptors, ring by item
   const int total_units = nunits * batch;
   const int c = n / 2;
 
   if (threadIdx.x == 0) {
-    for (int r = 0; r < NR; ++r) mbar_init(&bars[r], 1);
+    for (int r = 0; r < NR; ++r) {
+      mbar_init(&full[r], 1);
+      mbar_init(&empty[r], NCW);
+    }
     fence_mbar_init();
   }
-  uint32_t phase = 0;  // bit r: parity of the next wait on bars[r] (uniform across threads)
-  // called by all lanes of warp 0: lane 0 arms the barrier, then one box per lane
-  static_assert(G * (NFULL + 1) <= 32, "one TMA box per lane of warp 0");
-  // pf_k0 >= 0: also warm L2 with the step's pixel entries, their range read from soff (the unit
-  // starting at band pf_k0; no global round trip in front of the issuing warp)
-  auto issue = [&](int region, int step, int slice, int pf_k0) {
-    const int lane = threadIdx.x;
-    if (lane == 0) {
-      fence_proxy_async_smem();  // order earlier generic accesses to the region before the TMA writes
-      mbar_arrive_expect_tx(&bars[region], STEP_BYTES);
+  __syncthreads();
+
+  if (threadIdx.x >= NC) {
+    // ---- producer warp: walks work units (taken dynamically, outermost first) and their needed
+    // steps, runs up to two steps ahead of the consumers: waits until a ring region is released,
+    // publishes the step's descriptor and lands its spectra there by TMA.
+    const int lane = threadIdx.x - NC;
+    int slice = 0, k0 = 0, ks = 0, nl = 0, lpos = 0;
+    unsigned bits = 0;
+    for (int i = 0;; ++i) {
+      bool done = false;
+      while (lpos >= nl) {  // next unit with at least one needed step
+        int uu = 0;
+        if (lane == 0) uu = atomicAdd(counter, 1);
+        uu = __shfl_sync(0xFFFFFFFFu, uu, 0);
+        if (uu >= total_units) {
+          done = true;
+          break;
+        }
+        slice = uu % batch;
+        const uint2 ub = __ldg(units + uu / batch);
+        k0 = (int)ub.x;
+        const int k1 = (int)ub.y;
+        ks = k0 > 0 ? k0 - 1 : 0;  // the band before the unit feeds its first band's carried row
+        const int st = ks + lane;
+        bits = __ballot_sync(0xFFFFFFFFu, st < k1 && __ldg(step_need + st) != 0u);
+        nl = __popc(bits);
+        lpos = 0;
+      }
+      const int r = i % NR;
+      if (i >= NR) mbar_wait(&empty[r], (uint32_t)((i / NR - 1) & 1));
+      if (done) {
+        if (lane == 0) {
+          items[i & 3] = make_int4(-1, 0, 0, 0);
+          mbar_arrive(&full[r]);
+        }
+        break;
+      }
+      const int kk = ks + (int)__fns(bits, 0, lpos + 1);
+      ++lpos;
+      const bool rd = kk >= k0;  // the reloaded band before the unit only provides its last row
+      uint32_t e0 = 0, e1 = 0;
+      if (rd && lane == 0) {
+        e0 = __ldg(step_off + kk);
+        e1 = __ldg(step_off + kk + 1);
+      }
+      if (lane == 0) {
+        items[i & 3] = make_int4(slice, kk | (rd ? 1 << 30 : 0), (int)e0, (int)e1);
+        fence_proxy_async_smem();  // the consumers' generic accesses to the region before the TMA writes
+        mbar_arrive_expect_tx(&full[r], STEP_BYTES);  // releases the descriptor store with the arrival
+      }
+      __syncwarp();
+      if (lane < G * (NFULL + 1)) {  // rows (r0 + 2g, r0 + 2g + 1) -> group g's input as [m][2]
+        const int g = lane / (NFULL + 1), bx = lane - g * (NFULL + 1);
+        const int c0 = 2 * (row_min + S * kk + 2 * g);
+        float2* dst = smem_k45 + r * QREG + g * FS::IN_PITCH + 2 * (bx * 256);
+        if (bx < NFULL) tma_load_3d(dst, &ymap, c0, bx * 256, slice, &full[r]);
+        else tma_load_3d(dst, &ytail, c0, NFULL * 256, slice, &full[r]);
+      }
+      const uint32_t pa = __shfl_sync(0xFFFFFFFFu, e0, 0), pb = __shfl_sync(0xFFFFFFFFu, e1, 0);
+      if (lane == 31 && pb > pa) prefetch_l2_bulk(entries + pa, 16u * (pb - pa));  // warm L2 with its pixels
     }
-    __syncwarp();
-    if (lane < G * (NFULL + 1)) {  // rows (r0 + 2g, r0 + 2g + 1) -> group g's input as [m][2]
-      const int g = lane / (NFULL + 1), bx = lane - g * (NFULL + 1);
-      const int c0 = 2 * (row_min + S * step + 2 * g);
-      float2* dst = smem_k45 + region * QREG + g * FS::IN_PITCH + 2 * (bx * 256);
-      if (bx < NFULL) tma_load_3d(dst, &ymap, c0, bx * 256, slice, &bars[region]);
-      else tma_load_3d(dst, &ytail, c0, NFULL * 256, slice, &bars[region]);
-    } else if (lane == 31 && pf_k0 >= 0 && step >= pf_k0) {
-      const uint32_t a = soff[step - pf_k0], b = soff[step - pf_k0 + 1];
-      if (b > a) prefetch_l2_bulk(entries + a, 16u * (b - a));
-    }
-  };
+    return;
+  }
+
+  // ---- consumers: one step per item, in the producer's order
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
   auto row_of = [&](const float2* Q, int li) -> const float* {  // row li in [0, S) of a step region
     return reinterpret_cast<const float*>(Q + (li >> 1) * HALF) + (li & 1) * RPITCH;
   };
-
-  for (;;) {
-    if (threadIdx.x == 0) *unit_slot = atomicAdd(counter, 1);
-    __syncthreads();
-    const int u = *unit_slot;
-    if (u >= total_units) break;
-    const int slice = u % batch;
-    const uint2 ub = __ldg(units + u / batch);  // outermost (heaviest) units first, slices interleaved
-    const int k0 = (int)ub.x, k1 = (int)ub.y;
-    const int ks = k0 > 0 ? k0 - 1 : 0;  // the previous step only feeds its last row
-    // steps none of whose rows any pixel taps are neither loaded nor transformed: warp 0 compacts
-    // the unit's needed steps (ks .. k1-1) by ballot and issues the first two
-    int nlist;
-    if (threadIdx.x < 32) {
-      const int st = ks + (int)threadIdx.x;
-      const bool nd = st < k1 && __ldg(step_need + st) != 0u;
-      const unsigned bal = __ballot_sync(0xFFFFFFFFu, nd);
-      if (nd) ulist[__popc(bal & ((1u << threadIdx.x) - 1u))] = st;
-      nlist = __popc(bal);
-      __syncwarp();
-      for (int pos = 0; pos < min(2, nlist); ++pos) issue(pos % NR, ulist[pos], slice, -1);
-    }
-    // the unit's pixel-entry ranges, once (a per-step load would put an L2 round trip in front of
-    // every step's entry prefetch)
-    if (threadIdx.x >= 32 && threadIdx.x <= 32 + UQ && k0 + (int)threadIdx.x - 32 <= k1)
-      soff[threadIdx.x - 32] = __ldg(step_off + k0 + threadIdx.x - 32);
-    if (threadIdx.x == 0) ulist[UQ + 1] = nlist;
-    __syncthreads();  // soff, ulist, the list length visible; every thread has read unit_slot
-    nlist = ulist[UQ + 1];
-    float* out = img + (size_t)slice * n * n;
-
-    // a skipped step's rows are tapped by no pixel, so Qprev (the previous processed step) is
-    // read only when that step is kk - 1
 #pragma unroll 1
-    for (int pos = 0; pos < nlist; ++pos) {
-      const int kk = ulist[pos];
-      const int R = pos % NR;
-      const float2* Qprev = smem_k45 + ((pos + NR - 1) % NR) * QREG;
-      float2* Q = smem_k45 + R * QREG;
-      const int r0 = row_min + S * kk;
-      // first pixel entries of this step: loads in flight across the transforms
-      const bool rd = kk >= k0;
-      const uint32_t e0 = rd ? soff[kk - k0] : 0u, e1 = rd ? soff[kk - k0 + 1] : 0u;
-      uint4 pre = make_uint4(0x80000000u, 0, 0, 0), pre2 = pre;
-      const uint32_t ep = e0 + threadIdx.x;
-      if (ep < e1) pre = __ldg(entries + ep);
-      if (ep + blockDim.x < e1) pre2 = __ldg(entries + ep + blockDim.x);
+  for (int i = 0;; ++i) {
+    const int R = i % NR;
+    mbar_wait(&full[R], (uint32_t)((i / NR) & 1));
+    const int4 itm = items[i & 3];
+    if (itm.x < 0) break;
+    const int slice = itm.x, kk = itm.y & 0x3FFFFFFF;
+    const bool rd = (itm.y >> 30) & 1;
+    const uint32_t e0 = (uint32_t)itm.z, e1 = (uint32_t)itm.w;
+    // a band nobody taps is never loaded and the band before a unit is reloaded, so the previous item's
+    // region (Qprev) is read only when it holds band kk - 1 of the same slice
+    const float2* Qprev = smem_k45 + ((i + NR - 1) % NR) * QREG;
+    float2* Q = smem_k45 + R * QREG;
+    const int r0 = row_min + S * kk;
+    float* out = img + (size_t)slice * n * n;
+    // first pixel entries of this step: loads in flight across the transforms
+    uint4 pre = make_uint4(0x80000000u, 0, 0, 0), pre2 = pre;
+    const uint32_t ep = e0 + threadIdx.x;
+    if (ep < e1) pre = __ldg(entries + ep);
+    if (ep + NC < e1) pre2 = __ldg(entries + ep + NC);
 
-      mbar_wait(&bars[R], (phase >> R) & 1);
-      phase ^= 1u << R;
-      // inverse DFTs of rows (r0 + 2 gi, r0 + 2 gi + 1), in place in this group's part
-      float2* H = Q + gi * HALF;
-      float* Hf = reinterpret_cast<float*>(H);
-      const float2* Qin = Q + gi * FS::IN_PITCH;
-      // packed Z[k] = Xa[k] + i Xb[k], Hermitian extension for k > nphi/2; element r of pass 0
-      // (k = j + r*QS) sits in the low half for r < R0/2.  DC / Nyquist imaginary parts dropped.
-      // Rows in [nrho, nrho_pad) are zero (written by K3), rows past nrho_pad arrive as TMA zero fill.
-      constexpr int R0 = FftPlan<NPHI, true>::radix(0), QS = NPHI / R0;
-      auto load = [&](int j, auto rc) -> float2 {
-        constexpr int r = decltype(rc)::value;
-        if constexpr (r < R0 / 2) {
-          const float4 x = *reinterpret_cast<const float4*>(Qin + 2 * (j + r * QS));
-          float2 z = make_float2(x.x - x.w, x.y + x.z);
-          if constexpr (r == 0)
-            if (j == 0) z = make_float2(x.x, x.z);
-          return z;
-        } else {
-          const float4 x = *reinterpret_cast<const float4*>(Qin + 2 * ((R0 - r) * QS - j));
-          float2 z = make_float2(x.x + x.w, x.z - x.y);
-          if constexpr (r == R0 / 2)
-            if (j == 0) z = make_float2(x.x, x.z);
-          return z;
+    // inverse DFTs of rows (r0 + 2 gi, r0 + 2 gi + 1), in place in this group's part
+    float2* H = Q + gi * HALF;
+    float* Hf = reinterpret_cast<float*>(H);
+    const float2* Qin = Q + gi * FS::IN_PITCH;
+    // packed Z[k] = Xa[k] + i Xb[k], Hermitian extension for k > nphi/2; element r of pass 0
+    // (k = j + r*QS) sits in the low half for r < R0/2.  DC / Nyquist imaginary parts dropped.
+    // Rows in [nrho, nrho_pad) are zero (written by K3), rows past nrho_pad arrive as TMA zero fill.
+    constexpr int R0 = FftPlan<NPHI, true>::radix(0), QS = NPHI / R0;
+    auto load = [&](int j, auto rc) -> float2 {
+      constexpr int r = decltype(rc)::value;
+      if constexpr (r < R0 / 2) {
+        const float4 x = *reinterpret_cast<const float4*>(Qin + 2 * (j + r * QS));
+        float2 z = make_float2(x.x - x.w, x.y + x.z);
+        if constexpr (r == 0)
+          if (j == 0) z = make_float2(x.x, x.z);
+        return z;
+      } else {
+        const float4 x = *reinterpret_cast<const float4*>(Qin + 2 * ((R0 - r) * QS - j));
+        float2 z = make_float2(x.x + x.w, x.z - x.y);
+        if constexpr (r == R0 / 2)
+          if (j == 0) z = make_float2(x.x, x.z);
+        return z;
+      }
+    };
+    auto store = [&](int idx, float2 v) {
+      Hf[idx] = v.x;
+      Hf[RPITCH + idx] = v.y;
+    };
+    block_fft<NPHI, true, true, true, false, 16>(H, ti, tw, load, store, GroupSync{1 + gi, T});  // group-local
+    GroupSync{1 + G, NC}();  // both groups' rows are in place (consumers only; the producer runs ahead)
+
+    if (rd) {  // readout: taps from this step's rows and the previous step's last row
+      auto pixel = [&](const uint4& ent) {
+        const int qy = (int)(ent.x & 0x7FFFu), qx = (int)((ent.x >> 15) & 0xFFFFu);
+        const int iyp = c + qy, iyn = n - 1 - c - qy;
+        const int jxp = c + qx, jxn = n - 1 - c - qx;
+        const bool dupy = iyn == iyp, dupx = jxn == jxp;  // odd n: centre row / column
+        float v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f;
+        if (!(ent.x & 0x80000000u)) {
+          const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
+          const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
+          const int l0 = i0 - r0, l1 = min(i0 + 1, nrho - 1) - r0;
+          const float* row0 = l0 < 0 ? row_of(Qprev, S - 1) : row_of(Q, l0);
+          const float* row1 = row_of(Q, l1);
+          auto sample = [&](int j0, float wj) {
+            if (j0 >= NPHI) j0 -= NPHI;
+            const int j1 = (j0 + 1 == NPHI) ? 0 : j0 + 1;
+            const float a0 = fmaf(wj, row0[j1] - row0[j0], row0[j0]);
+            const float a1 = fmaf(wj, row1[j1] - row1[j0], row1[j0]);
+            return fmaf(wi, a1 - a0, a0) * scale;
+          };
+          const bool wz = wjr == 0.f;
+          const float wm = wz ? 0.f : 1.f - wjr;
+          v1 = sample(jr, wjr);                                      // x >= 0, y >= 0
+          v2 = sample(wz ? NPHI / 2 - jr : NPHI / 2 - jr - 1, wm);  // x < 0, y >= 0: pi - phi
+          v3 = sample(NPHI / 2 + jr, wjr);                           // x < 0, y < 0: pi + phi
+          v4 = sample(wz ? NPHI - jr : NPHI - jr - 1, wm);          // x >= 0, y < 0: 2 pi - phi
+        }
+        out[(size_t)iyp * n + jxp] = v1;
+        if (!dupx) out[(size_t)iyp * n + jxn] = v2;
+        if (!dupy) {
+          out[(size_t)iyn * n + jxp] = v4;
+          if (!dupx) out[(size_t)iyn * n + jxn] = v3;
         }
       };
-      auto store = [&](int idx, float2 v) {
-        Hf[idx] = v.x;
-        Hf[RPITCH + idx] = v.y;
-      };
-      block_fft<NPHI, true, true, true, false, 16>(H, ti, tw, load, store, GroupSync{1 + gi, T});  // group-local
-      __syncthreads();
-
-      if (rd) {  // readout: taps from this step's rows and the previous step's last row
-        auto pixel = [&](const uint4& ent) {
-          const int qy = (int)(ent.x & 0x7FFFu), qx = (int)((ent.x >> 15) & 0xFFFFu);
-          const int iyp = c + qy, iyn = n - 1 - c - qy;
-          const int jxp = c + qx, jxn = n - 1 - c - qx;
-          const bool dupy = iyn == iyp, dupx = jxn == jxp;  // odd n: centre row / column
-          float v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f;
-          if (!(ent.x & 0x80000000u)) {
-            const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
-            const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
-            const int l0 = i0 - r0, l1 = min(i0 + 1, nrho - 1) - r0;
-            const float* row0 = l0 < 0 ? row_of(Qprev, S - 1) : row_of(Q, l0);
-            const float* row1 = row_of(Q, l1);
-            auto sample = [&](int j0, float wj) {
-              if (j0 >= NPHI) j0 -= NPHI;
-              const int j1 = (j0 + 1 == NPHI) ? 0 : j0 + 1;
-              const float a0 = fmaf(wj, row0[j1] - row0[j0], row0[j0]);
-              const float a1 = fmaf(wj, row1[j1] - row1[j0], row1[j0]);
-              return fmaf(wi, a1 - a0, a0) * scale;
-            };
-            const bool wz = wjr == 0.f;
-            const float wm = wz ? 0.f : 1.f - wjr;
-            v1 = sample(jr, wjr);                                      // x >= 0, y >= 0
-            v2 = sample(wz ? NPHI / 2 - jr : NPHI / 2 - jr - 1, wm);  // x < 0, y >= 0: pi - phi
-            v3 = sample(NPHI / 2 + jr, wjr);                           // x < 0, y < 0: pi + phi
-            v4 = sample(wz ? NPHI - jr : NPHI - jr - 1, wm);          // x >= 0, y < 0: 2 pi - phi
-          }
-          out[(size_t)iyp * n + jxp] = v1;
-          if (!dupx) out[(size_t)iyp * n + jxn] = v2;
-          if (!dupy) {
-            out[(size_t)iyn * n + jxp] = v4;
-            if (!dupx) out[(size_t)iyn * n + jxn] = v3;
-          }
+      if (ep < e1) {  // entry loads run two pixels ahead; three rotating registers, no copies
+        uint4 ea = pre, eb = pre2, ec;
+        const uint32_t stp = NC;
+        uint32_t e = ep;
+        auto fetch = [&](uint4& dst) {
+          dst = make_uint4(0x80000000u, 0, 0, 0);
+          if (e + 2 * stp < e1) dst = __ldg(entries + e + 2 * stp);
         };
-        if (ep < e1) {  // entry loads run two pixels ahead; three rotating registers, no copies
-          uint4 ea = pre, eb = pre2, ec;
-          const uint32_t stp = blockDim.x;
-          uint32_t e = ep;
-          auto fetch = [&](uint4& dst) {
-            dst = make_uint4(0x80000000u, 0, 0, 0);
-            if (e + 2 * stp < e1) dst = __ldg(entries + e + 2 * stp);
-          };
 #pragma unroll 1
-          for (;;) {
-            fetch(ec);
-            pixel(ea);
-            if ((e += stp) >= e1) break;
-            fetch(ea);
-            pixel(eb);
-            if ((e += stp) >= e1) break;
-            fetch(eb);
-            pixel(ec);
-            if ((e += stp) >= e1) break;
-          }
+        for (;;) {
+          fetch(ec);
+          pixel(ea);
+          if ((e += stp) >= e1) break;
+          fetch(ea);
+          pixel(eb);
+          if ((e += stp) >= e1) break;
+          fetch(eb);
+          pixel(ec);
+          if ((e += stp) >= e1) break;
         }
       }
-      __syncthreads();  // region of kk-1 is free now: refill it with step kk+2
-      if (threadIdx.x < 32 && pos + 2 < nlist) issue((pos + 2) % NR, ulist[pos + 2], slice, k0);
+    }
+    // this warp is done with the previous item's region (its last row fed this readout)
+    if (i >= 1) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[(i + NR - 1) % NR]);
     }
   }
 }
@@ -1253,10 +1271,11 @@ cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
   if (e) return e;
   const int units = d.nunits * batch;
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, FS::G * FftPlan<NPHI, true>::T, FS::SMEM);
+  constexpr int NTHR = FS::G * FftPlan<NPHI, true>::T + 32;  // FFT groups + the producer warp
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTHR, FS::SMEM);
   const int slots = d.nsm * (occ > 0 ? occ : 1);
   const int grid = units < slots ? units : slots;
-  k<<<grid, FS::G * FftPlan<NPHI, true>::T, FS::SMEM, s>>>(map, tail, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, batch,
+  k<<<grid, NTHR, FS::SMEM, s>>>(map, tail, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, batch,
                                                           counter, t.band_off, t.band_need,
                                                           reinterpret_cast<const uint2*>(t.units), d.nunits,
                                                           reinterpret_cast<const uint4*>(t.band_entries),

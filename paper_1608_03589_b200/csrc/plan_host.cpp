@@ -145,8 +145,9 @@ void build_bands(HostPlan& h, int band_rows) {
   // unit bounds the kernel: units are taken dynamically, largest-first), the sparse inner bands in long
   // ones (each unit re-transforms the band before it for its carried row).
   {
-    // measured on B200 at 2048^2 (E0 x cost target in {1500, 3000, 6000} x {4, 8, 16}: 32.0 - 36.7 us/slice)
-    const double kEntryEquiv = 3000.0, kUnitCost = 8.0;
+    // measured on B200 at 2048^2 with the warp-specialised kernel (E0 x cost target in {2000, 3000, 5000} x
+    // {4, 6, 8, 12}: 28.7 - 32.5 us/slice)
+    const double kEntryEquiv = 2000.0, kUnitCost = 8.0;
     std::vector<std::pair<uint32_t, uint32_t>> us;
     int hi = h.nbands;
     while (hi > 0) {
