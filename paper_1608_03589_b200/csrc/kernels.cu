@@ -540,24 +540,29 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 
 // ---------------------------------------------------------------------------
 // K45: fused inverse phi-DFT + Cartesian readout, streamed along rho.
-// Persistent CTAs take work units (slice, 16 consecutive quads of 4 log-polar
-// rows) from an atomic counter, outermost (pixel-heavy) units first.  Per quad:
-// a 3-D TMA tensor map over Y[b][m][rho] with box {4 rows (32 B), 256 m} lands
-// the quad's spectra ([m][2] per row pair) in one of NR ring regions (prefetched NR-1 quads
-// ahead); the two FFT groups inverse-transform the quad's two row pairs in place;
-// the quad's pixels (taps i0, i0+1 with i0 in [r0-1, r0+3)) are sampled from the
-// region plus a carry copy of the previous quad's last row.  The log-polar image
-// never reaches HBM and no row is transformed twice inside a unit.
+// Bands of 4 log-polar rows ("steps"); band b owns the pixels whose taps are
+// i0, i0+1 with i0 in [r0-1, r0+3), r0 = row_min + 4b, i.e. its own rows and the
+// last row of band b-1.  Persistent CTAs, warp-specialised:
+//  * a producer warp takes work units (host-built band ranges, cost-balanced,
+//    outermost = pixel-heaviest first, slices interleaved) from an atomic counter,
+//    compacts each unit's needed bands (bands no pixel taps are never loaded) plus
+//    the band before the unit (its last row feeds the unit's first band), and for
+//    each step waits until a ring region is free (`empty` mbarrier), publishes the
+//    step descriptor and lands the spectra there by 3-D TMA boxes {2 rows, 256 m}
+//    (one box set per FFT group, [m][2] inside the group's half; `full` mbarrier);
+//  * the two FFT groups inverse-transform a row pair each in place, meet at one
+//    consumer barrier, sample their pixels from the region (and the previous
+//    region's last row), and release the previous region.
+// The log-polar image never reaches HBM; there are no CTA-wide barriers per step.
 // ---------------------------------------------------------------------------
-#ifndef K45_S
-#define K45_S 4
-#endif
 template <int NPHI>
 struct FusedShape {
-  static constexpr int S = K45_S;   // log-polar rows per step (one packed pair per FFT group)
+  static constexpr int S = 4;       // log-polar rows per step (one packed pair per FFT group)
   static constexpr int G = S / 2;   // FFT groups
   static constexpr int NR = 3;      // ring regions (previous, current, next step)
-  static constexpr int UQ = kFusedMaxUnit;  // max steps per work unit (plan_host kMaxUnitBands)
+  static constexpr int UQ = kFusedMaxUnit;  // max bands per work unit (plan_host kMaxUnitBands); the producer's
+                                            // ballot covers them and the reloaded band before the unit
+  static_assert(UQ + 1 <= 32, "one producer lane per band of a unit");
   // spectra m = 0 .. NPHI/2: NFULL boxes of 256 rows + one 1-row tail box
   static constexpr int NFULL = (NPHI / 2) / 256;
   static_assert(NFULL * 256 + 1 == NPHI / 2 + 1, "tail box is one row");
