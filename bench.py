@@ -110,6 +110,19 @@ class Dist:
             dist.init_process_group("gloo")
             self.pg = dist
 
+    def cuda_index(self) -> int:
+        """This rank's GPU: LOCAL_RANK, wrapped onto the visible devices.  On a box with fewer GPUs
+        than local ranks (functional checks of the N > 1 path only) ranks share a device and the
+        line says so in config.shared_device; such a run is not a scaling measurement."""
+        import torch
+
+        nd = torch.cuda.device_count()
+        self.shared_device = nd < int(os.environ.get("LOCAL_WORLD_SIZE", str(self.world)))
+        if self.shared_device:
+            print(f"[bench] rank {self.rank}: {nd} visible GPU(s) for the local ranks: devices are shared "
+                  "(functional check, not a scaling number)", file=sys.stderr)
+        return self.local % max(nd, 1)
+
     def barrier(self):
         if self.pg:
             self.pg.barrier()
@@ -359,8 +372,9 @@ def run_ours(a, d: Dist):
 
     import paper_1608_03589_b200 as p
 
-    torch.cuda.set_device(d.local)
-    dev = torch.device("cuda", d.local)
+    ci = d.cuda_index()
+    torch.cuda.set_device(ci)
+    dev = torch.device("cuda", ci)
     c = bench_config(a)
     nt, nth, n = c["nt"], c["ntheta"], c["n"]
     total = a.slices or c["slices"]
@@ -483,17 +497,19 @@ def run_ours(a, d: Dist):
                          f"slowest worker {busy:.1f} s, mean {np.mean(per):.2f} s/slice/core), "
                          f"oracle/fastbp_oracle.py ({'fbp_bst' if bst else 'fbp_logpolar'}), CPU {cpu_model()}"}
 
+    slices_total = int(d.sum(S))  # a collective: every rank takes part
     if d.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (device-generated seeded random-ellipse sinograms, K=50, 1% Gaussian noise)",
             "config": dict({"workload": workload_name(a.config, c) + (" (BST engine)" if bst else ""),
-                            "slices_total": int(d.sum(S)), "slices_per_rank": S, "rank_slice_ranges": shards,
+                            "slices_total": slices_total, "slices_per_rank": S, "rank_slice_ranges": shards,
                             "chunk": chunk, "streams": nstreams,
                             "parallelism": f"slice-shard x{d.world} ({a.scaling} scaling, no inter-GPU exchange)",
                             "l2": f"no flush: {S * nt * nth * 4 / 1e9:.1f} GB of sinograms per rank per step "
                                   f">> 126 MB L2"},
+                           **({"shared_device": True} if getattr(d, "shared_device", False) else {}),
                            **({"engine": "bst", "L": info["L"], "big": info["big"], "m_need": info["m_need"]} if bst
                               else {"nrho": info["nrho"], "L": info["L"], "nphi": info["nphi"]})),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -541,8 +557,9 @@ def run_direct(a, d: Dist):
 
     import paper_1608_03589_b200 as p
 
-    torch.cuda.set_device(d.local)
-    dev = torch.device("cuda", d.local)
+    ci = d.cuda_index()
+    torch.cuda.set_device(ci)
+    dev = torch.device("cuda", ci)
     c = p.synth.CONFIGS[4]
     S = a.slices or c["slices"]
     n, nt, nth = c["n"], c["nt"], c["ntheta"]

@@ -544,7 +544,7 @@ k_readout(const float* __restrict__ lp, float* __restrict__ img, int n, int nq, 
 // i0, i0+1 with i0 in [r0-1, r0+3), r0 = row_min + 4b, i.e. its own rows and the
 // last row of band b-1.  Persistent CTAs, warp-specialised:
 //  * a producer warp takes work units (host-built band ranges, cost-balanced,
-//    outermost = pixel-heaviest first, slices interleaved) from an atomic counter,
+//    outermost = pixel-heaviest first, slices interleaved in pairs) from an atomic counter,
 //    compacts each unit's needed bands (bands no pixel taps are never loaded) plus
 //    the band before the unit (its last row feeds the unit's first band), and for
 //    each step waits until a ring region is free (`empty` mbarrier), publishes the
@@ -625,8 +625,16 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
           done = true;
           break;
         }
-        slice = uu % batch;
-        const uint2 ub = __ldg(units + uu / batch);
+        // slices interleaved in pairs: a unit's pixel entries serve two slices from L2, and only two
+        // slices' images are written at a time, so partial image sectors complete in L2 (measured:
+        // all slices interleaved 28.7 us/slice with 1.39x image write traffic, pairs 26.8 us at 1.02x,
+        // one slice at a time 27.7 us with the entry table re-read from DRAM)
+        constexpr int SG = 2;
+        const int grp = uu / (nunits * SG);
+        const int gs = min(SG, batch - grp * SG);
+        const int within = uu - grp * nunits * SG;
+        slice = grp * SG + within % gs;
+        const uint2 ub = __ldg(units + within / gs);
         k0 = (int)ub.x;
         const int k1 = (int)ub.y;
         ks = k0 > 0 ? k0 - 1 : 0;  // the band before the unit feeds its first band's carried row
