@@ -436,6 +436,17 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
   }
 }
 
+// Pointwise multiply of the fused middle: mul(idx, val), or mul(integral_constant<e>, idx, val) where
+// e = b*R + r is the value's compile-time position among the thread's E outputs of the forward
+// transform (lets a multiplier keep per-thread operands in registers or TMEM, chunk by chunk).
+template <int E_IDX, typename Mul>
+__device__ __forceinline__ float2 mul_at(Mul& mul, int idx, float2 v) {
+  if constexpr (std::is_invocable_v<Mul&, std::integral_constant<int, E_IDX>, int, float2>)
+    return mul(std::integral_constant<int, E_IDX>{}, idx, v);
+  else
+    return mul(idx, v);
+}
+
 // Circular convolution core: y = IFFT_N( mul(FFT_N(x)) ), unnormalised inverse.
 // The last forward pass and the first inverse pass share their radix and the
 // butterfly->thread map, so the spectrum never touches shared memory: each
@@ -486,17 +497,19 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
     constexpr int Ns = F::ns(P - 1);
     constexpr int NB = (N / R) / T;
     float2 v[NB][R];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
+    static_for<0, NB>([&](auto bc) {
+      constexpr int b = decltype(bc)::value;
       const int j = ti + b * T;
       pass_load<N, R, F::S>(buf, j, v[b]);
       if constexpr (SFU_MIN > 0 && Ns >= SFU_MIN) apply_twiddles_sfu4<R, Ns, false>(v[b], j);
       else apply_twiddles<R, Ns>(v[b], j, twf + F::tw_off(P - 1));
       Dft<R, false>::run(v[b]);
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[b][r] = mul(j + r * Ns, v[b][r]);
+      static_for<0, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        v[b][r] = mul_at<b * R + r>(mul, j + r * Ns, v[b][r]);
+      });
       Dft<R, true>::run(v[b]);  // inverse pass 0 (Ns = 1: no twiddles)
-    }
+    });
     sync();
 #pragma unroll
     for (int b = 0; b < NB; ++b) pass_store<N, R, 1, B::S>(buf, ti + b * T, v[b]);

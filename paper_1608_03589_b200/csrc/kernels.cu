@@ -16,11 +16,13 @@
 // phi-DFTs of sinogram rows (the phi>=pi half picks up (-1)^m from its nphi/2
 // shift).  nt row FFTs replace nrho (~1.9x fewer) and the row mix moves into K3,
 // where it feeds the first rho-FFT pass straight from shared memory.
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include "async.cuh"
 #include "fft.cuh"
+#include "tmem.cuh"
 #include "kernels.cuh"
 
 namespace lpbp {
@@ -316,10 +318,12 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
 //   x[i]  = w0 p[k_i] + w1 p[k_i+1], i < nrho, 0 for i >= nrho            (log-polar, grids.py:332-347)
 //   Y[m]  = IFFT_L( FFT_L(x) * Khat[m] )[:nrho]                           (logpolar.py:112-117)
 // The row mix is evaluated inside the first forward pass; the multiply by
-// Khat is fused between the last forward and first inverse pass.
+// Khat is fused between the last forward and first inverse pass.  TM: each
+// thread's 32 Khat values of the CTA's column are read from L2 once and kept in
+// its TMEM lane (tensor memory, otherwise idle here) for all slices of the chunk.
 // ---------------------------------------------------------------------------
 // 16384-point columns (nt >~ 2900): 512 threads and ~200 KB of shared memory, one CTA per SM
-template <int L, bool PRUNE>
+template <int L, bool PRUNE, bool TM>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, (L >= 16384 ? 1 : 2))
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int gp, int ns, int nrho, int row_lo,
            int nrho_pad, int nh, const uint2* __restrict__ abw,
@@ -327,6 +331,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
   __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tslot;
   float2* buf = smem_k3;                          // padded_len(L)
   float2* p = buf + padded_len(L);                // ns
   float2* gcol = p + ((ns + 1) & ~1);             // gp + 2 (16-B aligned); refilled as soon as the row mix is done
@@ -337,11 +342,38 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   const float2* kcol = khat + (size_t)m * L;
   const uint32_t col_bytes = (uint32_t)gp * sizeof(float2);  // gp = nt rounded up to even
 
+  // TM: the thread's E Khat values of this column live in its TMEM lane for all slices of the chunk
+  // (one L2 read of the column per CTA instead of one per slice)
+  // (the twiddles, also per-thread invariants, were measured slower from TMEM than from the SFU:
+  // 73.0 vs 69.3 us/slice; the SFU work overlaps the pass's shared-memory loads)
+  constexpr int E = FftPlan<L, false>::E;
+  constexpr int TCOLS = pow2_at_least(2 * E * (T >= 128 ? T / 128 : 1));
+  const int warp = ti >> 5;
+  if (TM && warp == 0) tmem_alloc<TCOLS>(&tslot);
   if (ti == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
+  tmem_fence_before();
   __syncthreads();
+  tmem_fence_after();
+  const uint32_t kt = TM ? tmem_addr(tslot, warp, (warp >> 2) * 2 * E) : 0u;
+  if constexpr (TM) {  // value e = b R + r of the fused middle multiplies Khat[ti + b T + r L/R]
+    constexpr int RL = FftPlan<L, false>::radix(FftPlan<L, false>::P - 1);
+#pragma unroll 1
+    for (int c = 0; c < E / 8; ++c) {
+      float t16[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = 8 * c + q, bb = e / RL, r = e % RL;
+        const float2 kv = __ldg(kcol + ti + bb * T + r * (L / RL));
+        t16[2 * q] = kv.x;
+        t16[2 * q + 1] = kv.y;
+      }
+      tmem_st16(kt + 16 * c, t16);
+    }
+    tmem_wait_st();
+  }
   // the packed taps ride on the first column's barrier as one more bulk copy (16-byte multiple)
   const uint32_t kw_bytes = (uint32_t)nrho * 4u;
   const bool kw_bulk = (kw_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(kw) & 15u) == 0;
@@ -398,13 +430,28 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       const float2 p0 = p[k], p1 = p[k + 1];
       return make_float2(fmaf(w1, p1.x - p0.x, p0.x), fmaf(w1, p1.y - p0.y, p0.y));
     };
-    auto mul = [&](int idx, float2 v) -> float2 { return cmul(v, __ldg(kcol + idx)); };
+    float kr[32];
+    auto mul = [&](auto ec, int idx, float2 v) -> float2 {
+      constexpr int e = decltype(ec)::value;
+      if constexpr (TM) {  // 16 values per TMEM round trip
+        if constexpr (e % 16 == 0) tmem_ld32(kt + 2 * e, kr);
+        return cmul(v, make_float2(kr[2 * (e % 16)], kr[2 * (e % 16) + 1]));
+      } else {
+        return cmul(v, __ldg(kcol + idx));
+      }
+    };
     float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
     auto store = [&](int idx, float2 v) {  // rows below row_lo are never read downstream
       if (idx < nrho && idx >= row_lo) ycol[idx] = v;
     };
     if (ti < nrho_pad - nrho) ycol[nrho + ti] = make_float2(0.f, 0.f);  // padding rows read as zero (K45)
     block_conv<L, PRUNE, 16>(buf, ti, tw, load, mul, store, block_sync);  // SFU twiddles for every pass
+  }
+  if constexpr (TM) {
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_free<TCOLS>(tslot);
   }
 }
 
@@ -1034,7 +1081,18 @@ cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float
   const int gp = d.gp > 0 ? d.gp : d.nt;
   const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp + 2) * sizeof(float2) + (size_t)d.nrho * 4;
   // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
-  auto k = (2 * d.nrho <= L) ? k_rho_conv<L, true> : k_rho_conv<L, false>;
+  // Khat in TMEM where L is in [4096, 8192]: at most two 256-thread CTAs per SM (128 columns each), so
+  // an allocation never waits; LPBP_K3_TMEM=0 selects the L2 path (A/B measurements)
+  static const bool tmv = [] {
+    const char* v = getenv("LPBP_K3_TMEM");
+    return v ? atoi(v) != 0 : true;
+  }();
+  constexpr bool kTmemOk = L >= 4096 && L <= 8192;
+  const bool pr = 2 * d.nrho <= L;
+  auto k = pr ? k_rho_conv<L, true, false> : k_rho_conv<L, false, false>;
+  if constexpr (kTmemOk) {
+    if (tmv) k = pr ? k_rho_conv<L, true, true> : k_rho_conv<L, false, true>;
+  }
   cudaError_t e = prep(k, smem);
   if (e) return e;
   k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, gp, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.abw,
