@@ -436,6 +436,16 @@ __device__ __forceinline__ void block_fft(float2* buf, int ti, const float2* __r
   }
 }
 
+// First-pass input of block_conv: load(idx), or load(integral_constant<e>, idx) where e = b*RL + r is
+// the value's compile-time position among the thread's first-pass loads (RL loads per butterfly).
+template <int E_IDX, typename Load>
+__device__ __forceinline__ float2 load_e(Load& load, int idx) {
+  if constexpr (std::is_invocable_v<Load&, std::integral_constant<int, E_IDX>, int>)
+    return load(std::integral_constant<int, E_IDX>{}, idx);
+  else
+    return load(idx);
+}
+
 // Pointwise multiply of the fused middle: mul(idx, val), or mul(integral_constant<e>, idx, val) where
 // e = b*R + r is the value's compile-time position among the thread's E outputs of the forward
 // transform (lets a multiplier keep per-thread operands in registers or TMEM, chunk by chunk).
@@ -469,20 +479,18 @@ __device__ __forceinline__ void block_conv(float2* buf, int ti, const float2* __
   {  // forward pass 0
     constexpr int R = F::radix(0);
     constexpr int NB = (N / R) / T;
+    constexpr int RL = PRUNE ? R / 2 : R;  // loads per butterfly
     float2 v[NB][R];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
+    static_for<0, NB>([&](auto bc) {
+      constexpr int b = decltype(bc)::value;
       const int j = ti + b * T;
-      if constexpr (PRUNE) {
-#pragma unroll
-        for (int r = 0; r < R / 2; ++r) v[b][r] = load(j + r * (N / R));
-        Dft<R, false>::run_zu(v[b]);
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[b][r] = load(j + r * (N / R));
-        Dft<R, false>::run(v[b]);
-      }
-    }
+      static_for<0, RL>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        v[b][r] = load_e<b * RL + r>(load, j + r * (N / R));
+      });
+      if constexpr (PRUNE) Dft<R, false>::run_zu(v[b]);
+      else Dft<R, false>::run(v[b]);
+    });
 #pragma unroll
     for (int b = 0; b < NB; ++b) pass_store<N, R, 1, F::S>(buf, ti + b * T, v[b]);
   }

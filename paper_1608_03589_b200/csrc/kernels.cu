@@ -342,12 +342,17 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   const float2* kcol = khat + (size_t)m * L;
   const uint32_t col_bytes = (uint32_t)gp * sizeof(float2);  // gp = nt rounded up to even
 
-  // TM: the thread's E Khat values of this column live in its TMEM lane for all slices of the chunk
-  // (one L2 read of the column per CTA instead of one per slice)
-  // (the twiddles, also per-thread invariants, were measured slower from TMEM than from the SFU:
-  // 73.0 vs 69.3 us/slice; the SFU work overlaps the pass's shared-memory loads)
+  // TM: loop invariants live in the thread's TMEM lane for all slices of the chunk: its E Khat values
+  // of this column (one L2 read of the column per CTA instead of one per slice, columns [0, 2E)), its
+  // first-pass log-polar taps ([2E, 2E + 16), TKW) and its semi-polar row-mix taps ([2E + 16, 2E + 32),
+  // when ns <= 4T).  (The twiddles, also per-thread invariants, were measured slower from TMEM than
+  // from the SFU: 73.0 vs 69.3 us/slice; the SFU work overlaps the pass's shared-memory loads.)
   constexpr int E = FftPlan<L, false>::E;
-  constexpr int TCOLS = pow2_at_least(2 * E * (T >= 128 ? T / 128 : 1));
+  constexpr int R0 = FftPlan<L, false>::radix(0), RL0 = PRUNE ? R0 / 2 : R0, KWN = (E / R0) * RL0;
+  constexpr bool TKW = TM && KWN <= 16;
+  constexpr int WCOLS = 2 * E + 32;
+  constexpr int TCOLS = pow2_at_least(WCOLS * (T >= 128 ? T / 128 : 1));
+  const bool tab = TM && ns <= 4 * T;  // row-mix taps from TMEM (uniform over the CTA)
   const int warp = ti >> 5;
   if (TM && warp == 0) tmem_alloc<TCOLS>(&tslot);
   if (ti == 0) {
@@ -357,7 +362,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t kt = TM ? tmem_addr(tslot, warp, (warp >> 2) * 2 * E) : 0u;
+  const uint32_t kt = TM ? tmem_addr(tslot, warp, (warp >> 2) * WCOLS) : 0u;
   if constexpr (TM) {  // value e = b R + r of the fused middle multiplies Khat[ti + b T + r L/R]
     constexpr int RL = FftPlan<L, false>::radix(FftPlan<L, false>::P - 1);
 #pragma unroll 1
@@ -372,17 +377,39 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       }
       tmem_st16(kt + 16 * c, t16);
     }
+    if constexpr (TKW) {  // first-pass input e = b RL0 + r reads taps at ti + b T + r L/R0
+      uint32_t t[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int idx = ti + (q / RL0) * T + (q % RL0) * (L / R0);
+        t[q] = (q < KWN && idx < nrho) ? __ldg(kw + idx) : 0u;
+      }
+      tmem_st16(kt + 2 * E, t);
+    }
+    if (tab) {  // row-mix rows ti + u T
+      uint32_t t[16];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = ti + u * T;
+        const uint2 e = k < ns ? __ldg(abw + k) : make_uint2(0u, 0u);
+        t[2 * u] = e.x;
+        t[2 * u + 1] = e.y;
+      }
+#pragma unroll
+      for (int q = 8; q < 16; ++q) t[q] = 0u;
+      tmem_st16(kt + 2 * E + 16, t);
+    }
     tmem_wait_st();
   }
   // the packed taps ride on the first column's barrier as one more bulk copy (16-byte multiple)
   const uint32_t kw_bytes = (uint32_t)nrho * 4u;
   const bool kw_bulk = (kw_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(kw) & 15u) == 0;
   if (ti == 0) {
-    mbar_arrive_expect_tx(&bar, col_bytes + (kw_bulk ? kw_bytes : 0u));
+    mbar_arrive_expect_tx(&bar, col_bytes + (kw_bulk && !TKW ? kw_bytes : 0u));
     tma_bulk_g2s(gcol, Gh + (size_t)m * gp, col_bytes, &bar);
-    if (kw_bulk) tma_bulk_g2s(kws, kw, kw_bytes, &bar);
+    if (kw_bulk && !TKW) tma_bulk_g2s(kws, kw, kw_bytes, &bar);
   }
-  if (!kw_bulk)
+  if (!kw_bulk && !TKW)
     for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
   if (ti < 2) gcol[gp + ti] = make_float2(0.f, 0.f);  // rows nt, nt+1 of the packed taps read zero (visible
                                                        // after the first mbarrier wait's __syncthreads below)
@@ -396,10 +423,17 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
 #pragma unroll 1
     for (int k0 = 0; k0 < ns; k0 += 4 * T) {
       uint2 e[4];
+      if (tab) {
+        uint32_t t[16];
+        tmem_ld16(kt + 2 * E + 16, t);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k = k0 + ti + u * T;
-        e[u] = k < ns ? __ldg(abw + k) : make_uint2(0u, 0u);
+        for (int u = 0; u < 4; ++u) e[u] = make_uint2(t[2 * u], t[2 * u + 1]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + ti + u * T;
+          e[u] = k < ns ? __ldg(abw + k) : make_uint2(0u, 0u);
+        }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -422,9 +456,15 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       mbar_arrive_expect_tx(&bar, col_bytes);
       tma_bulk_g2s(gcol, Gh + ((size_t)(b + 1) * nh + m) * gp, col_bytes, &bar);
     }
-    auto load = [&](int idx) -> float2 {
+    uint32_t kwr[16];
+    auto load = [&](auto ec, int idx) -> float2 {
+      constexpr int q = decltype(ec)::value;
+      if constexpr (TKW)
+        if constexpr (q == 0) tmem_ld16(kt + 2 * E, kwr);
       if (idx >= nrho) return make_float2(0.f, 0.f);
-      const uint32_t e = kws[idx];
+      uint32_t e;
+      if constexpr (TKW) e = kwr[q];
+      else e = kws[idx];
       const int k = (int)(e & 0x7FFu);
       const float w1 = (float)(e >> 11) * (1.f / 1048576.f);
       const float2 p0 = p[k], p1 = p[k + 1];
