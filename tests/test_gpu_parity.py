@@ -426,3 +426,34 @@ def test_spec_single_sector_reproduces_logpolar(pkg):
     gap = float(np.linalg.norm(pb[m] - lp[m]) / np.linalg.norm(lp[m]))
     print(f"single sector vs logpolar: {gap:.3e}")
     assert gap <= 5e-2
+
+
+_TMEM_AB = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1608_03589_b200 as p
+from oracle import phantoms
+g = torch.stack([torch.from_numpy(phantoms.config_sinogram(3, i)) for i in (0, 7)]).cuda()
+plan = p.get_plan(2048, 2048, 2048, None, None, (0.0, 1.0))
+np.save(sys.argv[2], plan.execute(g, chunk=2).cpu().numpy())
+"""
+
+
+def test_rho_conv_tmem_operands_bitwise(tmp_path):
+    """K3 holds its loop invariants (K-hat column, first-pass taps, row-mix taps) in TMEM by default;
+    LPBP_K3_TMEM=0 reads them from L2 / shared memory each slice.  Same arithmetic, so the two
+    2048^2 FBP outputs are bitwise equal (each run in its own process: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("1", "0"):
+        f = str(tmp_path / f"k3_tmem_{v}.npy")
+        env = dict(os.environ, LPBP_K3_TMEM=v)
+        r = subprocess.run([sys.executable, "-c", _TMEM_AB, repo, f], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.isfinite(outs[0]).all() and np.abs(outs[0]).max() > 0
+    assert np.array_equal(outs[0], outs[1])
