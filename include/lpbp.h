@@ -66,6 +66,8 @@ typedef struct lpbp_plan_info {
   size_t readout_sector_bytes; /* distinct 32-byte log-polar sectors the readout taps (x32) */
   int32_t band_rows, row_min, nbands; /* fused inverse-DFT + readout banding               */
   int32_t generic, MB;         /* 1: any-size path (Bluestein length-nphi DFTs on MB-point FFTs) */
+  int32_t phi_q;               /* generic path with mixed-radix length-nphi DFTs (nphi = phi_q x 2^k,
+                                  phi_q in {3, 5, 9, 15, 25}) instead of Bluestein; 0 otherwise */
 } lpbp_plan_info;
 
 int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan);

@@ -198,6 +198,19 @@ cudaError_t staged(const lpbp_plan* Pc, int stage, int slices, cudaStream_t s, F
 // stop_after_lp: write the log-polar image to lp_out and skip filter/readout.
 // win > 0: compacted input rows (sector path) of `win` floats: `win_lo` leading columns,
 // then the row's last win - win_lo columns; everything between is zero.
+
+// The ramp filter acts along t only: a generic plan (length-nphi DFTs by Bluestein) still takes the
+// power-of-two ramp kernels whenever they cover (nt, ntheta); the Bluestein-capable kernel otherwise.
+static cudaError_t ramp_any(const lpbp::Dims& d, const lpbp::DevTables& t, const float* in, float* out, int c,
+                            cudaStream_t s) {
+  cudaError_t r = lpbp::launch_ramp(d, t, in, out, c, s);
+  if (r == cudaErrorNotSupported && d.generic) {
+    (void)cudaGetLastError();
+    r = lpbp::launch_ramp_generic(d, t, in, out, c, s);
+  }
+  return r;
+}
+
 int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, cudaStream_t s, bool stop_after_lp,
               float* lp_out, int win = 0, int win_lo = 0) {
   Dims dl = P->d;
@@ -213,10 +226,7 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   cudaError_t e;
   const bool gen = d.generic != 0;
   if (P->h.filter && !stop_after_lp) {
-    e = staged(P, 0, c, s, [&] {
-      return gen ? lpbp::launch_ramp_generic(d, P->t, in, reinterpret_cast<float*>(A), c, s)
-                 : lpbp::launch_ramp(d, P->t, in, reinterpret_cast<float*>(A), c, s);
-    });
+    e = staged(P, 0, c, s, [&] { return ramp_any(d, P->t, in, reinterpret_cast<float*>(A), c, s); });
     if (e) return launch_fail(e, "ramp_filter");
     ++g_launches;
     src = reinterpret_cast<const float*>(A);
@@ -325,7 +335,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     delete P;
     return fail(LPBP_EUNSUPPORTED, "no kernel instantiation for nt=" + std::to_string(h.nt) + ", ntheta=" +
                                        std::to_string(h.ntheta) + ", L=" + std::to_string(h.L) +
-                                       " (this build: ramp embedding 2*nt <= 8192, rho FFT <= 16384, Bluestein row DFT length <= 16384)");
+                                       " (this build: ramp embedding 2*nt <= 8192, rho FFT <= 16384, row DFTs of length 2*ntheta: Bluestein on <= 16384 points or mixed-radix Q x 2^k, Q in {3, 5, 9, 15, 25})");
   }
   P->device = params->device;
   if (lpbp::fused_band_rows(P->h.nphi) > 0) lpbp::build_bands(P->h, lpbp::fused_band_rows(P->h.nphi));
@@ -340,7 +350,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     rc = rc ? rc : P->twiddles(h.L, &P->t.tw_rho);
     if (h.filter) rc = rc ? rc : P->twiddles(h.M, &P->t.tw_ramp);
     if (h.generic) {
-      rc = rc ? rc : P->twiddles(h.MB, &P->t.tw_blue);
+      if (h.MB <= 16384) rc = rc ? rc : P->twiddles(h.MB, &P->t.tw_blue);  // (longer: mixed-radix lengths only)
       rc = rc ? rc : P->upload(h.chirp, reinterpret_cast<const lpbp::F2**>(&P->t.chirp));
       rc = rc ? rc : P->upload(h.bhat_f, reinterpret_cast<const lpbp::F2**>(&P->t.bhat_f));
       rc = rc ? rc : P->upload(h.bhat_i, reinterpret_cast<const lpbp::F2**>(&P->t.bhat_i));
@@ -429,6 +439,12 @@ int lpbp_plan_get_info(const lpbp_plan* P, lpbp_plan_info* info) {
   info->nbands = h.nbands;
   info->generic = h.generic ? 1 : 0;
   info->MB = h.MB;
+  info->phi_q = 0;
+  if (h.generic && lpbp::mixed_radix_length(h.nphi)) {
+    int q = h.nphi;
+    while (q % 2 == 0) q /= 2;
+    info->phi_q = q;
+  }
   return LPBP_OK;
 }
 
@@ -468,9 +484,7 @@ int lpbp_filter(const lpbp_plan* P, const float* sino_dev, float* out_dev, int32
   if (batch == 0) return LPBP_OK;
   if (!sino_dev || !out_dev) return fail(LPBP_EINVAL, "invalid argument");
   DeviceGuard g(P->device);
-  cudaError_t e = P->d.generic
-                      ? lpbp::launch_ramp_generic(P->d, P->t, sino_dev, out_dev, batch, static_cast<cudaStream_t>(stream))
-                      : lpbp::launch_ramp(P->d, P->t, sino_dev, out_dev, batch, static_cast<cudaStream_t>(stream));
+  cudaError_t e = ramp_any(P->d, P->t, sino_dev, out_dev, batch, static_cast<cudaStream_t>(stream));
   if (e) return launch_fail(e, "ramp_filter");
   ++g_launches;
   return LPBP_OK;

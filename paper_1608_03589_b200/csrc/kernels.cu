@@ -23,6 +23,7 @@
 #include "async.cuh"
 #include "fft.cuh"
 #include "tmem.cuh"
+#include "mixed.cuh"
 #include "kernels.cuh"
 
 namespace lpbp {
@@ -459,6 +460,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     uint32_t kwr[16];
     auto load = [&](auto ec, int idx) -> float2 {
       constexpr int q = decltype(ec)::value;
+      (void)q;
       if constexpr (TKW)
         if constexpr (q == 0) tmem_ld16(kt + 2 * E, kwr);
       if (idx >= nrho) return make_float2(0.f, 0.f);
@@ -473,6 +475,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     float kr[32];
     auto mul = [&](auto ec, int idx, float2 v) -> float2 {
       constexpr int e = decltype(ec)::value;
+      (void)e;
       if constexpr (TM) {  // 16 values per TMEM round trip
         if constexpr (e % 16 == 0) tmem_ld32(kt + 2 * e, kr);
         return cmul(v, make_float2(kr[2 * (e % 16)], kr[2 * (e % 16) + 1]));
@@ -990,6 +993,70 @@ k_row_irdft_generic(const float2* __restrict__ Yh, float* __restrict__ lp, int n
   block_conv<MB, true>(smem_g4, threadIdx.x, tw, load, mul, store, block_sync);
 }
 
+// Mixed-radix lengths nphi = Q P (mixed.cuh): the same row transforms as the Bluestein
+// kernels above, one CTA per row pair, with the length-nphi DFT computed directly
+// (Q-point DFTs in registers + Q power-of-two FFTs) instead of a 2-4x longer circular
+// convolution.  LNLS's 3200 angles: nphi = 6400 = 25 x 256.
+template <int Q, int P>
+__global__ void __launch_bounds__(MixedShape<Q, P>::THREADS)
+k_row_rdft_mixed(const float* __restrict__ g, float2* __restrict__ Gh, int nt, int gp, int ntheta, int win,
+                 int win_lo) {
+  extern __shared__ __align__(16) float2 smem_m2[];
+  constexpr int N = Q * P;  // nphi
+  const int nh = ntheta + 1;
+  const int ta = 2 * blockIdx.x, tb = ta + 1;
+  const bool hb = tb < nt;
+  const float* ra = g + ((size_t)blockIdx.y * nt + ta) * win;  // rows of `win` (<= ntheta) columns
+  const float* rb = ra + win;
+  const int tail = ntheta - (win - win_lo);  // compacted rows: [0, win_lo) and [tail, ntheta) are stored
+  auto load = [&](int idx) -> float2 {       // rows ta, tb packed as re / im, zero for idx >= ntheta
+    if (idx >= ntheta || (idx >= win_lo && idx < tail)) return make_float2(0.f, 0.f);
+    const int src = idx >= tail ? idx - (tail - win_lo) : idx;
+    return make_float2(__ldg(ra + src), hb ? __ldg(rb + src) : 0.f);
+  };
+  block_dft_mixed<Q, P, false>(smem_m2, load);
+  float2* dst = Gh + (size_t)blockIdx.y * nh * gp + ta;
+  for (int m = threadIdx.x; m < nh; m += blockDim.x) {
+    const float2 z = mixed_at<Q, P>(smem_m2, m), w = mixed_at<Q, P>(smem_m2, m == 0 ? 0 : N - m);
+    dst[(size_t)m * gp] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
+    if (hb) dst[(size_t)m * gp + 1] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+    else if (tb < gp) dst[(size_t)m * gp + 1] = make_float2(0.f, 0.f);  // odd nt: the pad column reads zero
+  }
+}
+
+template <int Q, int P>
+__global__ void __launch_bounds__(MixedShape<Q, P>::THREADS)
+k_row_irdft_mixed(const float2* __restrict__ Yh, float* __restrict__ lp, int nrho, int nrho_pad, int ntheta) {
+  extern __shared__ __align__(16) float2 smem_m4[];
+  constexpr int N = Q * P;  // nphi
+  const int nh = ntheta + 1;
+  const int ia = 2 * blockIdx.x, ib = ia + 1;
+  const bool hb = ib < nrho;
+  const float2* src = Yh + (size_t)blockIdx.y * nh * nrho_pad;
+  float* dst = lp + (size_t)blockIdx.y * nrho * N;
+  auto load = [&](int idx) -> float2 {  // Z[k] = Xa[k] + i Xb[k], Hermitian-assembled from Y
+    const bool hi = idx > ntheta;
+    const int mm = hi ? N - idx : idx;
+    float2 xa = src[(size_t)mm * nrho_pad + ia];
+    float2 xb = hb ? src[(size_t)mm * nrho_pad + ib] : make_float2(0.f, 0.f);
+    if (mm == 0 || mm == ntheta) {  // numpy irfft drops the DC / Nyquist imaginary parts
+      xa.y = 0.f;
+      xb.y = 0.f;
+    }
+    if (hi) {
+      xa.y = -xa.y;
+      xb.y = -xb.y;
+    }
+    return make_float2(xa.x - xb.y, xa.y + xb.x);
+  };
+  block_dft_mixed<Q, P, true>(smem_m4, load);
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {  // coalesced rows
+    const float2 z = mixed_at<Q, P>(smem_m4, k);
+    dst[(size_t)ia * N + k] = z.x;
+    if (hb) dst[(size_t)ib * N + k] = z.y;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Input generator: exact ellipse line integrals (radon.py:38-61) in fp64,
 // 2 rho A B sqrt(w^2 - tau^2) / w^2, tau = t - c.xi_theta,
@@ -1341,14 +1408,85 @@ cudaError_t launch_ramp_generic(const Dims& d, const DevTables& t, const float* 
   LPBP_POW2_SWITCH(d.M, LPBP_CALL)
 #undef LPBP_CALL
 }
+namespace {
+// (Q, P) instantiations of the mixed-radix row DFTs: Q P = nphi, Q P / 16 threads (whole warps, <= 1024)
+#define LPBP_MIXED_SWITCH(NPHI, CALL)               \
+  switch (NPHI) {                                   \
+    case 3 * 512: return CALL(3, 512);              \
+    case 3 * 1024: return CALL(3, 1024);            \
+    case 3 * 2048: return CALL(3, 2048);            \
+    case 3 * 4096: return CALL(3, 4096);            \
+    case 5 * 512: return CALL(5, 512);              \
+    case 5 * 1024: return CALL(5, 1024);            \
+    case 5 * 2048: return CALL(5, 2048);            \
+    case 9 * 512: return CALL(9, 512);              \
+    case 9 * 1024: return CALL(9, 1024);            \
+    case 15 * 512: return CALL(15, 512);            \
+    case 15 * 1024: return CALL(15, 1024);          \
+    case 25 * 256: return CALL(25, 256);            \
+    case 25 * 512: return CALL(25, 512);            \
+    default: return cudaErrorNotSupported;          \
+  }
+template <int Q, int P>
+cudaError_t rdft_mixed_impl(const Dims& d, const float* g, float2* Gh, int batch, cudaStream_t s) {
+  using MS = MixedShape<Q, P>;
+  auto k = k_row_rdft_mixed<Q, P>;
+  cudaError_t e = prep(k, MS::SMEM);
+  if (e) return e;
+  const int win = d.win > 0 ? d.win : d.ntheta, win_lo = d.win > 0 ? d.win_lo : d.ntheta;
+  k<<<dim3((d.nt + 1) / 2, batch), MS::THREADS, MS::SMEM, s>>>(g, Gh, d.nt, d.gp > 0 ? d.gp : d.nt, d.ntheta, win,
+                                                              win_lo);
+  return cudaGetLastError();
+}
+template <int Q, int P>
+cudaError_t irdft_mixed_impl(const Dims& d, const float2* Yh, float* lp, int batch, cudaStream_t s) {
+  using MS = MixedShape<Q, P>;
+  auto k = k_row_irdft_mixed<Q, P>;
+  cudaError_t e = prep(k, MS::SMEM);
+  if (e) return e;
+  k<<<dim3((d.nrho + 1) / 2, batch), MS::THREADS, MS::SMEM, s>>>(Yh, lp, d.nrho, d.nrho_pad, d.ntheta);
+  return cudaGetLastError();
+}
+cudaError_t rdft_mixed(const Dims& d, const float* g, float2* Gh, int batch, cudaStream_t s) {
+#define LPBP_CALL(Q, P) rdft_mixed_impl<Q, P>(d, g, Gh, batch, s)
+  LPBP_MIXED_SWITCH(d.nphi, LPBP_CALL)
+#undef LPBP_CALL
+}
+cudaError_t irdft_mixed(const Dims& d, const float2* Yh, float* lp, int batch, cudaStream_t s) {
+#define LPBP_CALL(Q, P) irdft_mixed_impl<Q, P>(d, Yh, lp, batch, s)
+  LPBP_MIXED_SWITCH(d.nphi, LPBP_CALL)
+#undef LPBP_CALL
+}
+// LPBP_MIXED=0 keeps the Bluestein kernels for every generic length (A/B measurements, parity)
+bool mixed_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("LPBP_MIXED");
+    return v ? atoi(v) != 0 : true;
+  }();
+  return on;
+}
+}  // namespace
+
+bool mixed_radix_length(int nphi) {
+  switch (nphi) {
+    case 3 * 512: case 3 * 1024: case 3 * 2048: case 3 * 4096: case 5 * 512: case 5 * 1024: case 5 * 2048:
+    case 9 * 512: case 9 * 1024: case 15 * 512: case 15 * 1024: case 25 * 256: case 25 * 512:
+      return true;
+    default:
+      return false;
+  }
+}
+
 cudaError_t launch_row_rdft_generic(const Dims& d, const DevTables& t, const float* g, float2* Gh, int batch,
                                     cudaStream_t s) {
+  if (mixed_enabled() && mixed_radix_length(d.nphi)) return rdft_mixed(d, g, Gh, batch, s);
 #define LPBP_CALL(M) rdft_generic_impl<M>(d, t, g, Gh, batch, s)
   LPBP_POW2_SWITCH(d.MB, LPBP_CALL)
 #undef LPBP_CALL
 }
 cudaError_t launch_row_irdft_generic(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch,
                                      cudaStream_t s) {
+  if (mixed_enabled() && mixed_radix_length(d.nphi)) return irdft_mixed(d, Yh, lp, batch, s);
 #define LPBP_CALL(M) irdft_generic_impl<M>(d, t, Yh, lp, batch, s)
   LPBP_POW2_SWITCH(d.MB, LPBP_CALL)
 #undef LPBP_CALL
@@ -1442,7 +1580,8 @@ bool sizes_supported(int nt, int ntheta, int L, int M, int MB, bool filter, bool
   // rho FFT up to 16384 points (nt up to ~5800 at n = nt), ramp embedding up to 8192 (nt <= 4096)
   if (!pow2in(L, 512, 16384)) return false;
   if (filter && !pow2in(M, 512, 8192)) return false;
-  if (generic) return pow2in(MB, 512, 16384) && nt >= 2;  // odd nt: row spectra column pitch padded to even
+  // odd nt: row spectra column pitch padded to even; mixed-radix lengths need no Bluestein size
+  if (generic) return (pow2in(MB, 512, 16384) || mixed_radix_length(2 * ntheta)) && nt >= 2;
   const int nphi = 2 * ntheta;
   if (!pow2in(nphi, 512, 4096) || nt % 4) return false;
   if (filter && ntheta % 8) return false;

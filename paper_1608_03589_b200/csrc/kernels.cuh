@@ -77,6 +77,8 @@ cudaError_t launch_ramp_generic(const Dims& d, const DevTables& t, const float* 
                                 cudaStream_t s);
 cudaError_t launch_row_rdft_generic(const Dims& d, const DevTables& t, const float* g, float2* G, int batch,
                                     cudaStream_t s);
+// nphi has a direct mixed-radix kernel (Q P, Q in {3, 5, 9, 15, 25}); otherwise Bluestein
+bool mixed_radix_length(int nphi);
 cudaError_t launch_row_irdft_generic(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch,
                                      cudaStream_t s);
 // Pass-twiddle tables (fft.cuh TwTable): entry count for size N (-1 if unsupported)

@@ -209,13 +209,13 @@ def test_paper_lnls_sizes(pkg, nt, nth):
     """The paper's motivating workload (reconstructions from 3200 x 2048
     datasets), both orientations, FBP to 2048^2 against the oracle.
     3200 bins x 2048 angles: ns = 1600, nrho = 6096 -> a 16384-point rho FFT and an
-    8192-point ramp embedding; 2048 bins x 3200 angles: nphi = 6400 -> Bluestein row DFTs
-    on 16384-point convolutions."""
+    8192-point ramp embedding; 2048 bins x 3200 angles: nphi = 6400 = 25 x 256 -> mixed-radix
+    row DFTs (25-point DFTs in registers + 256-point FFTs)."""
     g = phantoms.sinogram(4242 + nt, nt, nth, 50, 0.01, 0.3, 0.01)
     plan = pkg.get_plan(nt, nth, 2048, None, None, (0.0, 1.0))
     assert (plan.info["L"], plan.info["M"]) == ((16384, 8192) if nt == 3200 else (8192, 4096))
-    if nth == 3200:
-        assert plan.info["generic"] == 1 and plan.info["MB"] == 16384
+    if nth == 3200:  # nphi = 6400 = 25 x 256: mixed-radix row DFTs (Bluestein would run 16384-point convolutions)
+        assert plan.info["generic"] == 1 and plan.info["MB"] == 16384 and plan.info["phi_q"] == 25
     out = pkg.fbp_batch(dev(g)[None], pkg.FilterSpec(), 2048)[0].cpu().numpy()
     ref = O.fbp_logpolar(g.astype(np.float64), 2048)
     assert report(f"paper size {nt}x{nth} fbp -> 2048", out, ref) <= RTOL
@@ -457,3 +457,23 @@ def test_rho_conv_tmem_operands_bitwise(tmp_path):
         outs.append(np.load(f))
     assert np.isfinite(outs[0]).all() and np.abs(outs[0]).max() > 0
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("nth", [768, 1280, 1536, 2304, 2560, 3200, 3840])
+def test_mixed_radix_row_dfts_vs_oracle(pkg, nth):
+    """Angle counts whose nphi = 2 ntheta is Q x 2^k (Q = 3, 5, 9, 15, 25) take the mixed-radix
+    row DFTs (mixed.cuh) in both directions; BP and FBP against the oracle, and the row spectra
+    stage against numpy's rfft of the (filtered) rows."""
+    nt, n = 96, 64
+    q = 2 * nth
+    while q % 2 == 0:
+        q //= 2
+    rng = np.random.default_rng(nth)
+    gd = np.cumsum(rng.standard_normal((nt, nth)), axis=0).astype(np.float32).astype(np.float64) * 0.05
+    plan = pkg.get_plan(nt, nth, n, None, None, (0.0, 1.0))
+    assert plan.info["generic"] == 1 and plan.info["phi_q"] == q
+    g = pkg.Sinogram(nt, nth, gd)
+    assert report(f"mixed bp {nt}x{nth}->{n}", pkg.logpolar_backproject(g, n).values,
+                  O.logpolar_backproject(gd, n)) <= RTOL
+    assert report(f"mixed fbp {nt}x{nth}->{n}", pkg.fbp(g, pkg.FilterSpec(), engine="logpolar", n=n).values,
+                  O.fbp_logpolar(gd, n)) <= RTOL
