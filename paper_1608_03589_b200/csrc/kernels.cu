@@ -1018,9 +1018,10 @@ k_row_rdft_mixed(const float* __restrict__ g, float2* __restrict__ Gh, int nt, i
   float2* dst = Gh + (size_t)blockIdx.y * nh * gp + ta;
   for (int m = threadIdx.x; m < nh; m += blockDim.x) {
     const float2 z = mixed_at<Q, P>(smem_m2, m), w = mixed_at<Q, P>(smem_m2, m == 0 ? 0 : N - m);
-    dst[(size_t)m * gp] = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
-    if (hb) dst[(size_t)m * gp + 1] = make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
-    else if (tb < gp) dst[(size_t)m * gp + 1] = make_float2(0.f, 0.f);  // odd nt: the pad column reads zero
+    const float2 a = make_float2(0.5f * (z.x + w.x), 0.5f * (z.y - w.y));
+    const float2 b = hb ? make_float2(0.5f * (z.y + w.y), 0.5f * (w.x - z.x)) : make_float2(0.f, 0.f);
+    if (tb < gp) *reinterpret_cast<float4*>(dst + (size_t)m * gp) = make_float4(a.x, a.y, b.x, b.y);  // 16 bytes
+    else dst[(size_t)m * gp] = a;  // (odd nt: the pad column past tb reads zero)
   }
 }
 
@@ -1034,20 +1035,21 @@ k_row_irdft_mixed(const float2* __restrict__ Yh, float* __restrict__ lp, int nrh
   const bool hb = ib < nrho;
   const float2* src = Yh + (size_t)blockIdx.y * nh * nrho_pad;
   float* dst = lp + (size_t)blockIdx.y * nrho * N;
-  auto load = [&](int idx) -> float2 {  // Z[k] = Xa[k] + i Xb[k], Hermitian-assembled from Y
+  // Z[k] = Xa[k] + i Xb[k], Hermitian-assembled from Y; rows ia, ib are adjacent in Y (one 16-byte load;
+  // ib = nrho is a zero padding row of Y, written by K3)
+  auto load = [&](int idx) -> float2 {
     const bool hi = idx > ntheta;
     const int mm = hi ? N - idx : idx;
-    float2 xa = src[(size_t)mm * nrho_pad + ia];
-    float2 xb = hb ? src[(size_t)mm * nrho_pad + ib] : make_float2(0.f, 0.f);
+    float4 x = __ldg(reinterpret_cast<const float4*>(src + (size_t)mm * nrho_pad + ia));
     if (mm == 0 || mm == ntheta) {  // numpy irfft drops the DC / Nyquist imaginary parts
-      xa.y = 0.f;
-      xb.y = 0.f;
+      x.y = 0.f;
+      x.w = 0.f;
     }
     if (hi) {
-      xa.y = -xa.y;
-      xb.y = -xb.y;
+      x.y = -x.y;
+      x.w = -x.w;
     }
-    return make_float2(xa.x - xb.y, xa.y + xb.x);
+    return make_float2(x.x - x.w, x.y + x.z);
   };
   block_dft_mixed<Q, P, true>(smem_m4, load);
   for (int k = threadIdx.x; k < N; k += blockDim.x) {  // coalesced rows

@@ -172,10 +172,12 @@ __device__ __forceinline__ void block_dft_mixed(float2* buf, Load&& load) {
     for (int n1 = 0; n1 < Q; ++n1) v[n1] = load(P * n1 + n2);
     OddDft<Q, INV>::run(v);
     buf[pad16(n2)] = v[0];
+    int ph = 0;  // n2 k1 mod N, stepped (n2 < P <= N)
 #pragma unroll
     for (int k1 = 1; k1 < Q; ++k1) {
-      int e = (n2 * k1) % N;
-      e = e > N / 2 ? e - N : e;
+      ph += n2;
+      ph = ph >= N ? ph - N : ph;
+      const int e = ph > N / 2 ? ph - N : ph;
       float sn, cs;
       __sincosf(kStep * (float)e, &sn, &cs);
       buf[k1 * PITCH + pad16(n2)] = cmul(v[k1], make_float2(cs, sn));

@@ -443,3 +443,15 @@ def test_ellipse_containers_mirror_reference():
     if not torch.cuda.is_available():
         with pytest.raises(RuntimeError, match="no CUDA device"):
             p.radon_ellipses(es, 16, 8)
+
+
+@pytest.mark.parametrize("nth,q", [(3200, 25), (768, 3), (1280, 5), (2304, 9), (3840, 15), (6144, 3), (90, 0),
+                                   (2048, 0), (3600, 0)])
+def test_mixed_radix_row_dft_lengths(nth, q):
+    """nphi = 2 ntheta of the form Q x 2^k (Q in {3, 5, 9, 15, 25}, within the instantiated range) is
+    reported as a mixed-radix plan (phi_q = Q); power-of-two nphi takes the pow2 kernels (generic = 0),
+    other lengths Bluestein (phi_q = 0).  6144 angles (nphi 12288 = 3 x 4096) would need a 32768-point
+    Bluestein convolution and is supported only through the mixed-radix kernels."""
+    hp = HostPlan(64, nth, 64)
+    assert hp.info.phi_q == q
+    assert hp.info.generic == (0 if nth == 2048 else 1)
