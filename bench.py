@@ -388,8 +388,12 @@ def run_ours(a, d: Dist):
     shards = d.gather([global_ids[0], global_ids[-1] + 1] if global_ids else [0, 0])
     sino = p.synth.config_batch(a.config, global_ids, dev, geometry=(nt, nth))
     out = torch.empty((S, n, n), dtype=torch.float32, device=dev)
-    chunk = min(a.chunk if a.chunk > 0 else (16 if bst else 8), S)
-    nstreams = a.streams if a.streams > 0 else (1 if bst else 2)
+    # the generic-size path (non-power-of-two nphi: unfused inverse DFT + readout through an HBM
+    # log-polar image) runs best on one stream, like BST: two chunks in flight halve the L2 the
+    # readout's gathers hit (LNLS 2048 x 3200: 3175 slices/s on one stream with chunks of 16, 2373 on two)
+    single = bst or bool(plan.info.get("generic", 0))
+    chunk = min(a.chunk if a.chunk > 0 else (16 if single else 8), S)
+    nstreams = a.streams if a.streams > 0 else (1 if single else 2)
     # one workspace per stream: the plan is immutable, chunks on different streams overlap
     wss = [None if bst else torch.empty(plan.workspace_bytes(chunk), dtype=torch.uint8, device=dev)
            for _ in range(nstreams)]
