@@ -1190,13 +1190,13 @@ cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float
   const int gp = d.gp > 0 ? d.gp : d.nt;
   const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp + 2) * sizeof(float2) + (size_t)d.nrho * 4;
   // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
-  // Khat in TMEM where L is in [4096, 8192]: at most two 256-thread CTAs per SM (128 columns each), so
-  // an allocation never waits; LPBP_K3_TMEM=0 selects the L2 path (A/B measurements)
+  // Khat in TMEM where L is in [4096, 16384]: at most two 256-thread CTAs per SM (256 columns each) or
+  // one 512-thread CTA (512 columns), so an allocation never waits; LPBP_K3_TMEM=0 selects the L2 path
   static const bool tmv = [] {
     const char* v = getenv("LPBP_K3_TMEM");
     return v ? atoi(v) != 0 : true;
   }();
-  constexpr bool kTmemOk = L >= 4096 && L <= 8192;
+  constexpr bool kTmemOk = L >= 4096 && L <= 16384;  // 16384: one 512-thread CTA per SM, 512 columns
   const bool pr = 2 * d.nrho <= L;
   auto k = pr ? k_rho_conv<L, true, false> : k_rho_conv<L, false, false>;
   if constexpr (kTmemOk) {

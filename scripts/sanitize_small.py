@@ -14,5 +14,12 @@ plan.execute(g1, chunk=1); plan.filter(g1); lp = plan.logpolar(g1); plan.readout
 plan.execute_host(g1.cpu().numpy(), chunk=1)
 p.backproject_naive_batch(g0, 200)
 p.VolumeReconstructor(256, 256, 256, devices=[0, 0]).run(g0.cpu().numpy())
+# K3 with its TMEM-held operands (L = 4096 at 1024^2) and the mixed-radix row DFTs (nphi = 1536 = 3 x 512,
+# 2560 = 5 x 512, 6400 = 25 x 256) in both directions
+g2 = torch.randn(2, 1024, 1024, device="cuda")
+p.get_plan(1024, 1024, 1024, None, None, (0.0, 1.0)).execute(g2)
+for nth in (768, 1280, 3200):
+    gm = torch.randn(2, 96, nth, device="cuda")
+    p.get_plan(96, nth, 64, None, None, (0.0, 1.0)).execute(gm)
 torch.cuda.synchronize()
 print("sanitize run ok")

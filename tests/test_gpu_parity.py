@@ -477,3 +477,33 @@ def test_mixed_radix_row_dfts_vs_oracle(pkg, nth):
                   O.logpolar_backproject(gd, n)) <= RTOL
     assert report(f"mixed fbp {nt}x{nth}->{n}", pkg.fbp(g, pkg.FilterSpec(), engine="logpolar", n=n).values,
                   O.fbp_logpolar(gd, n)) <= RTOL
+
+
+@pytest.mark.parametrize("nt,nth,n,fbp", [(96, 3200, 64, True), (96, 768, 64, False), (130, 1280, 100, True)])
+def test_no_out_of_bounds_writes_mixed(pkg, nt, nth, n, fbp):
+    """Guard zones (NaN) around input, output and workspace for the mixed-radix row DFTs and the
+    unfused generic path (odd ntheta multiples, odd-looking nt), as test_no_out_of_bounds_writes does
+    for the power-of-two path."""
+    plan = pkg.get_plan(nt, nth, n, None, None, (0.0, 1.0) if fbp else None)
+    assert plan.info["phi_q"] > 0
+    b = 3
+    guard = 1 << 16
+    n_in, n_out = b * nt * nth, b * n * n
+    ws_floats = (plan.workspace_bytes(2) + 3) // 4
+    up = lambda v: (v + 63) // 64 * 64  # noqa: E731
+    o_in = guard
+    o_out = up(o_in + n_in + guard)
+    o_ws = up(o_out + n_out + guard)
+    total = o_ws + ws_floats + guard
+    big = torch.full((total,), float("nan"), device="cuda")
+    x = torch.randn(b, nt, nth, device="cuda")
+    big[o_in:o_in + n_in] = x.reshape(-1)
+    sino = big[o_in:o_in + n_in].view(b, nt, nth)
+    out = big[o_out:o_out + n_out].view(b, n, n)
+    ws = big[o_ws:o_ws + ws_floats].view(torch.uint8)
+    plan.execute(sino, out=out, workspace=ws, chunk=2)
+    torch.cuda.synchronize()
+    for lo, hi in ((0, o_in), (o_in + n_in, o_out), (o_out + n_out, o_ws), (o_ws + ws_floats, total)):
+        assert torch.isnan(big[lo:hi]).all(), f"guard [{lo},{hi}) overwritten"
+    assert torch.isfinite(out).all()
+    assert torch.equal(out, plan.execute(x, chunk=2))
