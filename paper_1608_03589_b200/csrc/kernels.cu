@@ -364,6 +364,14 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   __syncthreads();
   tmem_fence_after();
   const uint32_t kt = TM ? tmem_addr(tslot, warp, (warp >> 2) * WCOLS) : 0u;
+  // first column (in flight under the TMEM prologue); the packed taps ride on the first column's barrier as one more bulk copy (16-byte multiple)
+  const uint32_t kw_bytes = (uint32_t)nrho * 4u;
+  const bool kw_bulk = (kw_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(kw) & 15u) == 0;
+  if (ti == 0) {
+    mbar_arrive_expect_tx(&bar, col_bytes + (kw_bulk && !TKW ? kw_bytes : 0u));
+    tma_bulk_g2s(gcol, Gh + (size_t)m * gp, col_bytes, &bar);
+    if (kw_bulk && !TKW) tma_bulk_g2s(kws, kw, kw_bytes, &bar);
+  }
   if constexpr (TM) {  // value e = b R + r of the fused middle multiplies Khat[ti + b T + r L/R]
     constexpr int RL = FftPlan<L, false>::radix(FftPlan<L, false>::P - 1);
 #pragma unroll 1
@@ -401,14 +409,6 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       tmem_st16(kt + 2 * E + 16, t);
     }
     tmem_wait_st();
-  }
-  // the packed taps ride on the first column's barrier as one more bulk copy (16-byte multiple)
-  const uint32_t kw_bytes = (uint32_t)nrho * 4u;
-  const bool kw_bulk = (kw_bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(kw) & 15u) == 0;
-  if (ti == 0) {
-    mbar_arrive_expect_tx(&bar, col_bytes + (kw_bulk && !TKW ? kw_bytes : 0u));
-    tma_bulk_g2s(gcol, Gh + (size_t)m * gp, col_bytes, &bar);
-    if (kw_bulk && !TKW) tma_bulk_g2s(kws, kw, kw_bytes, &bar);
   }
   if (!kw_bulk && !TKW)
     for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
