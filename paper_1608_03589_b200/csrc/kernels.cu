@@ -1027,20 +1027,35 @@ k_row_rdft_mixed(const float* __restrict__ g, float2* __restrict__ Gh, int nt, i
 
 template <int Q, int P>
 __global__ void __launch_bounds__(MixedShape<Q, P>::THREADS)
-k_row_irdft_mixed(const float2* __restrict__ Yh, float* __restrict__ lp, int nrho, int nrho_pad, int ntheta) {
-  extern __shared__ __align__(16) float2 smem_m4[];
+k_row_irdft_mixed(const __grid_constant__ CUtensorMap ymap, float* __restrict__ lp, int nrho, int ntheta, int nbox) {
+  extern __shared__ __align__(128) float2 smem_m4[];
+  // the CTA's two rows of every spectrum column, [nbox * 256][2] (3-D TMA boxes {2 rows, 256 m}), then
+  // the mixed-radix rows
+  const float4* stg = reinterpret_cast<const float4*>(smem_m4);
+  float2* buf = smem_m4 + 2 * 256 * nbox;
+  __shared__ __align__(8) uint64_t bar;
   constexpr int N = Q * P;  // nphi
-  const int nh = ntheta + 1;
   const int ia = 2 * blockIdx.x, ib = ia + 1;
   const bool hb = ib < nrho;
-  const float2* src = Yh + (size_t)blockIdx.y * nh * nrho_pad;
   float* dst = lp + (size_t)blockIdx.y * nrho * N;
-  // Z[k] = Xa[k] + i Xb[k], Hermitian-assembled from Y; rows ia, ib are adjacent in Y (one 16-byte load;
-  // ib = nrho is a zero padding row of Y, written by K3)
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) mbar_arrive_expect_tx(&bar, (uint32_t)nbox * 256u * 16u);
+    __syncwarp();
+    for (int bx = threadIdx.x; bx < nbox; bx += 32)
+      tma_load_3d(const_cast<float4*>(stg) + bx * 256, &ymap, 2 * ia, bx * 256, blockIdx.y, &bar);
+  }
+  mbar_wait(&bar, 0);
+  // Z[k] = Xa[k] + i Xb[k], Hermitian-assembled from the staged columns (row ib = nrho is a zero
+  // padding row of Y, written by K3)
   auto load = [&](int idx) -> float2 {
     const bool hi = idx > ntheta;
     const int mm = hi ? N - idx : idx;
-    float4 x = __ldg(reinterpret_cast<const float4*>(src + (size_t)mm * nrho_pad + ia));
+    float4 x = stg[mm];
     if (mm == 0 || mm == ntheta) {  // numpy irfft drops the DC / Nyquist imaginary parts
       x.y = 0.f;
       x.w = 0.f;
@@ -1051,9 +1066,9 @@ k_row_irdft_mixed(const float2* __restrict__ Yh, float* __restrict__ lp, int nrh
     }
     return make_float2(x.x - x.w, x.y + x.z);
   };
-  block_dft_mixed<Q, P, true>(smem_m4, load);
+  block_dft_mixed<Q, P, true>(buf, load);
   for (int k = threadIdx.x; k < N; k += blockDim.x) {  // coalesced rows
-    const float2 z = mixed_at<Q, P>(smem_m4, k);
+    const float2 z = mixed_at<Q, P>(buf, k);
     dst[(size_t)ia * N + k] = z.x;
     if (hb) dst[(size_t)ib * N + k] = z.y;
   }
@@ -1444,9 +1459,15 @@ template <int Q, int P>
 cudaError_t irdft_mixed_impl(const Dims& d, const float2* Yh, float* lp, int batch, cudaStream_t s) {
   using MS = MixedShape<Q, P>;
   auto k = k_row_irdft_mixed<Q, P>;
-  cudaError_t e = prep(k, MS::SMEM);
+  const int nh = d.ntheta + 1, nbox = (nh + 255) / 256;
+  if (reinterpret_cast<uintptr_t>(Yh) & 15) return cudaErrorNotSupported;
+  CUtensorMap ym;
+  cudaError_t e = encode_spectra_map(&ym, Yh, d.nrho_pad, nh, batch, 2, 256);
   if (e) return e;
-  k<<<dim3((d.nrho + 1) / 2, batch), MS::THREADS, MS::SMEM, s>>>(Yh, lp, d.nrho, d.nrho_pad, d.ntheta);
+  const size_t smem = (size_t)nbox * 256 * 16 + MS::SMEM;
+  e = prep(k, smem);
+  if (e) return e;
+  k<<<dim3((d.nrho + 1) / 2, batch), MS::THREADS, smem, s>>>(ym, lp, d.nrho, d.ntheta, nbox);
   return cudaGetLastError();
 }
 cudaError_t rdft_mixed(const Dims& d, const float* g, float2* Gh, int batch, cudaStream_t s) {

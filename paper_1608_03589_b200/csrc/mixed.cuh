@@ -190,7 +190,14 @@ __device__ __forceinline__ void block_dft_mixed(float2* buf, Load&& load) {
   float2* row = buf + g * PITCH;
   auto ld = [&](int idx) -> float2 { return row[pad16(idx)]; };
   auto st = [&](int idx, float2 v) { row[pad16(idx)] = v; };
-  block_fft<P, INV, true, true, false, 1>(row, ti, nullptr, ld, st, [] { __syncthreads(); });
+  // a group's passes exchange data only inside its own row: warp-level barriers for groups of <= 32
+  // threads (two 16-thread groups share a warp and its barrier), a named barrier per group otherwise
+  auto gsync = [&] {
+    if constexpr (TP <= 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(TP) : "memory");
+  };
+  static_assert(TP <= 32 || MS::ROWS <= 15, "named barriers 1..15");
+  block_fft<P, INV, true, true, false, 1>(row, ti, nullptr, ld, st, gsync);
   __syncthreads();
 }
 
