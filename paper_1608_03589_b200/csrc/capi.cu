@@ -237,17 +237,19 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   });
   if (e) return launch_fail(e, "row_rdft");
   ++g_launches;
-  e = staged(P, 2, c, s, [&] {
+  e = staged(P, 2, c, s, [&] {  // rows below the first tapped one (pair) are never read downstream
     return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c,
-                                 (stop_after_lp || gen) ? 0 : d.row_min, s);
+                                 stop_after_lp ? 0 : d.row_min, s);
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
   if (stop_after_lp || gen) {
     // generic sizes: unfused inverse DFT into B (or the caller's buffer), then the readout
     float* lp = stop_after_lp ? lp_out : reinterpret_cast<float*>(B);
+    lpbp::Dims dp = d;  // the full log-polar image for the stage API; the tapped row pairs otherwise
+    if (stop_after_lp) dp.npairs = 0;
     e = staged(P, 3, c, s, [&] {
-      return gen ? lpbp::launch_row_irdft_generic(d, P->t, reinterpret_cast<const float2*>(A), lp, c, s)
+      return gen ? lpbp::launch_row_irdft_generic(dp, P->t, reinterpret_cast<const float2*>(A), lp, c, s)
                  : lpbp::launch_row_irdft(d, P->t, reinterpret_cast<const float2*>(A), lp, c, s);
     });
     if (e) return launch_fail(e, "row_irdft");
@@ -371,6 +373,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
       rc = rc ? rc : P->upload(P->h.band_packed, &P->t.band_entries);
       rc = rc ? rc : P->upload(P->h.band_need, &P->t.band_need);
       rc = rc ? rc : P->upload(P->h.units, &P->t.units);
+      rc = rc ? rc : P->upload(P->h.pair_list, &P->t.pairs);
     }
     if (rc) {
       std::string msg = g_last_error;
@@ -398,6 +401,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   d.band_rows = h.band_rows;
   d.generic = h.generic ? 1 : 0;
   d.MB = h.MB;
+  d.npairs = (int)h.pair_list.size();
   d.nsm = 148;
   if (P->device >= 0) cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, P->device);
   const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;

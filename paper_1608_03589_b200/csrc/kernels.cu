@@ -959,10 +959,11 @@ k_row_rdft_generic(const float* __restrict__ g, float2* __restrict__ Gh, int nt,
 template <int MB>
 __global__ void __launch_bounds__(FftPlan<MB, false>::T)
 k_row_irdft_generic(const float2* __restrict__ Yh, float* __restrict__ lp, int nrho, int nrho_pad, int ntheta,
-                    const float2* __restrict__ chirp, const float2* __restrict__ bhat, const float2* __restrict__ tw) {
+                    const float2* __restrict__ chirp, const float2* __restrict__ bhat, const float2* __restrict__ tw,
+                    const uint32_t* __restrict__ pairs) {
   extern __shared__ __align__(16) float2 smem_g4[];
   const int nphi = 2 * ntheta, nh = ntheta + 1;
-  const int ia = 2 * blockIdx.x, ib = ia + 1;
+  const int ia = 2 * (pairs ? (int)pairs[blockIdx.x] : (int)blockIdx.x), ib = ia + 1;
   const bool hb = ib < nrho;
   const float2* src = Yh + (size_t)blockIdx.y * nh * nrho_pad;
   float* dst = lp + (size_t)blockIdx.y * nrho * nphi;
@@ -1027,7 +1028,8 @@ k_row_rdft_mixed(const float* __restrict__ g, float2* __restrict__ Gh, int nt, i
 
 template <int Q, int P>
 __global__ void __launch_bounds__(MixedShape<Q, P>::THREADS)
-k_row_irdft_mixed(const __grid_constant__ CUtensorMap ymap, float* __restrict__ lp, int nrho, int ntheta, int nbox) {
+k_row_irdft_mixed(const __grid_constant__ CUtensorMap ymap, float* __restrict__ lp, int nrho, int ntheta, int nbox,
+                  const uint32_t* __restrict__ pairs) {
   extern __shared__ __align__(128) float2 smem_m4[];
   // the CTA's two rows of every spectrum column, [nbox * 256][2] (3-D TMA boxes {2 rows, 256 m}), then
   // the mixed-radix rows
@@ -1035,7 +1037,7 @@ k_row_irdft_mixed(const __grid_constant__ CUtensorMap ymap, float* __restrict__ 
   float2* buf = smem_m4 + 2 * 256 * nbox;
   __shared__ __align__(8) uint64_t bar;
   constexpr int N = Q * P;  // nphi
-  const int ia = 2 * blockIdx.x, ib = ia + 1;
+  const int ia = 2 * (pairs ? (int)pairs[blockIdx.x] : (int)blockIdx.x), ib = ia + 1;
   const bool hb = ib < nrho;
   float* dst = lp + (size_t)blockIdx.y * nrho * N;
   if (threadIdx.x == 0) {
@@ -1402,8 +1404,9 @@ cudaError_t irdft_generic_impl(const Dims& d, const DevTables& t, const float2* 
   auto k = k_row_irdft_generic<MB>;
   cudaError_t e = prep(k, smem);
   if (e) return e;
-  k<<<dim3((d.nrho + 1) / 2, batch), FftPlan<MB, false>::T, smem, s>>>(Yh, lp, d.nrho, d.nrho_pad, d.ntheta,
-                                                                      t.chirp, t.bhat_i, t.tw_blue);
+  const int grid = d.npairs > 0 ? d.npairs : (d.nrho + 1) / 2;
+  k<<<dim3(grid, batch), FftPlan<MB, false>::T, smem, s>>>(Yh, lp, d.nrho, d.nrho_pad, d.ntheta, t.chirp, t.bhat_i,
+                                                          t.tw_blue, d.npairs > 0 ? t.pairs : nullptr);
   return cudaGetLastError();
 }
 }  // namespace
@@ -1456,7 +1459,7 @@ cudaError_t rdft_mixed_impl(const Dims& d, const float* g, float2* Gh, int batch
   return cudaGetLastError();
 }
 template <int Q, int P>
-cudaError_t irdft_mixed_impl(const Dims& d, const float2* Yh, float* lp, int batch, cudaStream_t s) {
+cudaError_t irdft_mixed_impl(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch, cudaStream_t s) {
   using MS = MixedShape<Q, P>;
   auto k = k_row_irdft_mixed<Q, P>;
   const int nh = d.ntheta + 1, nbox = (nh + 255) / 256;
@@ -1467,7 +1470,8 @@ cudaError_t irdft_mixed_impl(const Dims& d, const float2* Yh, float* lp, int bat
   const size_t smem = (size_t)nbox * 256 * 16 + MS::SMEM;
   e = prep(k, smem);
   if (e) return e;
-  k<<<dim3((d.nrho + 1) / 2, batch), MS::THREADS, smem, s>>>(ym, lp, d.nrho, d.ntheta, nbox);
+  const int grid = d.npairs > 0 ? d.npairs : (d.nrho + 1) / 2;
+  k<<<dim3(grid, batch), MS::THREADS, smem, s>>>(ym, lp, d.nrho, d.ntheta, nbox, d.npairs > 0 ? t.pairs : nullptr);
   return cudaGetLastError();
 }
 cudaError_t rdft_mixed(const Dims& d, const float* g, float2* Gh, int batch, cudaStream_t s) {
@@ -1475,8 +1479,8 @@ cudaError_t rdft_mixed(const Dims& d, const float* g, float2* Gh, int batch, cud
   LPBP_MIXED_SWITCH(d.nphi, LPBP_CALL)
 #undef LPBP_CALL
 }
-cudaError_t irdft_mixed(const Dims& d, const float2* Yh, float* lp, int batch, cudaStream_t s) {
-#define LPBP_CALL(Q, P) irdft_mixed_impl<Q, P>(d, Yh, lp, batch, s)
+cudaError_t irdft_mixed(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch, cudaStream_t s) {
+#define LPBP_CALL(Q, P) irdft_mixed_impl<Q, P>(d, t, Yh, lp, batch, s)
   LPBP_MIXED_SWITCH(d.nphi, LPBP_CALL)
 #undef LPBP_CALL
 }
@@ -1509,7 +1513,7 @@ cudaError_t launch_row_rdft_generic(const Dims& d, const DevTables& t, const flo
 }
 cudaError_t launch_row_irdft_generic(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch,
                                      cudaStream_t s) {
-  if (mixed_enabled() && mixed_radix_length(d.nphi)) return irdft_mixed(d, Yh, lp, batch, s);
+  if (mixed_enabled() && mixed_radix_length(d.nphi)) return irdft_mixed(d, t, Yh, lp, batch, s);
 #define LPBP_CALL(M) irdft_generic_impl<M>(d, t, Yh, lp, batch, s)
   LPBP_POW2_SWITCH(d.MB, LPBP_CALL)
 #undef LPBP_CALL

@@ -36,6 +36,7 @@ struct DevTables {
   const float2* bhat_f;  // [MB]
   const float2* bhat_i;  // [MB]
   const float2* tw_blue; // pass twiddles, N = MB
+  const uint32_t* pairs; // [npairs] row pairs the readout taps (generic path's inverse DFT), ascending
 };
 
 struct Dims {
@@ -49,6 +50,7 @@ struct Dims {
   int win, win_lo;                 // compacted row-DFT input (0 = plain rows of ntheta): rows of `win` floats,
                                    // win_lo leading columns + the row's last win - win_lo columns
   float out_scale;        // 1 (backprojection) or 1/(2 pi) (fbp)
+  int npairs;             // > 0: the generic inverse DFT runs over t.pairs only (0 = every row pair)
 };
 
 // Each returns cudaGetLastError() after the launch (0 on success) or

@@ -452,6 +452,18 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
       h.qw[(size_t)qy * h.nq + qx] = F2{(float)(fi - i0), (float)(fj - j0)};
     }
   }
+  if (h.generic) {  // tapped row pairs; the first one (even row) bounds the rows K3 must store
+    std::vector<uint8_t> need((nrho + 1) / 2, 0);
+    for (const uint32_t e : h.qidx) {
+      if (e == 0xFFFFFFFFu) continue;
+      const int i0 = (int)(e & 0xFFFFu), i1 = std::min(i0 + 1, nrho - 1);
+      need[i0 / 2] = need[i1 / 2] = 1;
+    }
+    h.pair_list.clear();
+    for (int j = 0; j < (int)need.size(); ++j)
+      if (need[j]) h.pair_list.push_back((uint32_t)j);
+    h.row_min = h.pair_list.empty() ? 0 : 2 * (int)h.pair_list[0];
+  }
 
   // --- distinct 32-byte sectors of the fp32 log-polar image read by the readout
   // taps over the whole image (reflections as on the device): the readout's

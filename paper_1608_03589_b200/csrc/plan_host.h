@@ -58,6 +58,9 @@ struct HostPlan {
   // length nphi through MB-point convolutions, MB = pow2 >= 2 nphi
   bool generic = false;
   int MB = 0;
+  // generic path (unfused inverse DFT + readout): the row pairs (2j, 2j+1) some pixel taps, ascending;
+  // the inverse DFT runs over these only (a third of the rows at 2048^2 are tapped by no pixel)
+  std::vector<uint32_t> pair_list;
   std::vector<F2> chirp;          // [nphi] exp(-i pi n^2 / nphi)
   std::vector<F2> bhat_f, bhat_i; // [MB] FFT_MB of the forward / inverse chirp filter, incl. 1/MB
   // kernel support (for diagnostics/tests): cells (k, l) of the rolled kernel
