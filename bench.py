@@ -388,12 +388,16 @@ def run_ours(a, d: Dist):
     shards = d.gather([global_ids[0], global_ids[-1] + 1] if global_ids else [0, 0])
     sino = p.synth.config_batch(a.config, global_ids, dev, geometry=(nt, nth))
     out = torch.empty((S, n, n), dtype=torch.float32, device=dev)
-    # the generic-size path (non-power-of-two nphi: unfused inverse DFT + readout through an HBM
-    # log-polar image) runs best on one stream, like BST: two chunks in flight halve the L2 the
-    # readout's gathers hit (LNLS 2048 x 3200: 3175 slices/s on one stream with chunks of 16, 2373 on two)
-    single = bst or bool(plan.info.get("generic", 0))
-    chunk = min(a.chunk if a.chunk > 0 else (16 if single else 8), S)
-    nstreams = a.streams if a.streams > 0 else (1 if single else 2)
+    # a generic-size plan whose inverse DFT + readout stay unfused (Bluestein lengths, odd nt: through an
+    # HBM log-polar image) runs best on one stream, like BST: two chunks in flight halve the L2 the
+    # readout's gathers hit (LNLS before its fused path: 3175 slices/s on one stream, 2373 on two); the
+    # fused mixed-radix path takes two streams like the power-of-two one (LNLS: 4800 vs 4596); generic
+    # plans take chunks of 16
+    info = {} if bst else plan.info
+    generic = bool(info.get("generic", 0))
+    unfused = generic and not (info.get("phi_q", 0) > 0 and info.get("band_rows", 0) == 2)
+    chunk = min(a.chunk if a.chunk > 0 else (16 if (bst or generic) else 8), S)
+    nstreams = a.streams if a.streams > 0 else (1 if (bst or unfused) else 2)
     # one workspace per stream: the plan is immutable, chunks on different streams overlap
     wss = [None if bst else torch.empty(plan.workspace_bytes(chunk), dtype=torch.uint8, device=dev)
            for _ in range(nstreams)]

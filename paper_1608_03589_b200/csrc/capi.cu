@@ -243,7 +243,7 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
-  if (stop_after_lp || gen) {
+  if (stop_after_lp || (gen && !lpbp::fused_mixed_available(d))) {
     // generic sizes: unfused inverse DFT into B (or the caller's buffer), then the readout
     float* lp = stop_after_lp ? lp_out : reinterpret_cast<float*>(B);
     lpbp::Dims dp = d;  // the full log-polar image for the stage API; the tapped row pairs otherwise

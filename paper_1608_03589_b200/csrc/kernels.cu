@@ -891,6 +891,222 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// K45 for mixed-radix lengths nphi = Q P (mixed.cuh): the same streaming scheme as
+// k_irdft_readout — a producer warp walks the work units and their needed bands, the
+// consumers inverse-transform each band and sample its pixels in shared memory, so the
+// log-polar image never reaches HBM — with bands of 2 rows (one packed pair: the
+// mixed-radix transform of a pair needs the whole CTA's Q P / 16 threads) and a
+// two-stage ring: the band's spectra land by 3-D TMA boxes {2 rows, 256 m} in one of two
+// input buffers (released to the producer as soon as step A has read them), and the
+// transform runs in one of two row buffers (the other holds the previous band, whose
+// second row is the current band's carried row).
+// ---------------------------------------------------------------------------
+template <int Q, int P>
+struct FusedMixedShape {
+  using MS = MixedShape<Q, P>;
+  static constexpr int N = Q * P, NH = N / 2 + 1, S = 2;
+  static constexpr int NBOX = (NH + 255) / 256;
+  static constexpr int IN = NBOX * 256 * 2;        // float2 per input buffer ([m][2 rows])
+  static constexpr int RB = MS::ROWS * MS::PITCH;  // float2 per row buffer (mixed layout)
+  static constexpr int RBA = (RB + 15) / 16 * 16;  // 128-B multiple
+  static constexpr int NC = MS::THREADS, NTHR = NC + 32;
+  static constexpr uint32_t STEP_BYTES = (uint32_t)NBOX * 256 * 16;
+  static constexpr size_t SMEM = ((size_t)2 * IN + 2 * (size_t)RBA) * 8 + 4 * 8 + 4 * 16 + 64;
+  static_assert(NBOX <= 31, "one TMA box per producer lane, lane 31 prefetches entries");
+};
+
+template <int Q, int P>
+__global__ void __launch_bounds__(FusedMixedShape<Q, P>::NTHR, 1)
+k_irdft_readout_mixed(const __grid_constant__ CUtensorMap ymap, float* __restrict__ img, int nrho, int n, int nq,
+                      int row_min, int batch, int* __restrict__ counter, const uint32_t* __restrict__ step_off,
+                      const uint32_t* __restrict__ step_need, const uint2* __restrict__ units, int nunits,
+                      const uint4* __restrict__ entries, float scale) {
+  using FS = FusedMixedShape<Q, P>;
+  constexpr int N = FS::N, S = FS::S, NC = FS::NC, NCW = NC / 32, IN = FS::IN, RBA = FS::RBA;
+  extern __shared__ __align__(128) float2 smem_kx[];
+  float2* inbuf = smem_kx;               // [2][IN]
+  float2* rows = smem_kx + 2 * IN;       // [2][RBA]
+  uint64_t* full = reinterpret_cast<uint64_t*>(rows + 2 * RBA);  // [2] input landed (TMA bytes)
+  uint64_t* empty = full + 2;                                    // [2] input consumed by step A
+  int4* items = reinterpret_cast<int4*>(empty + 2);              // [4] step descriptors, ring by item
+  const int total_units = nunits * batch;
+  const int c = n / 2;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < 2; ++r) {
+      mbar_init(&full[r], 1);
+      mbar_init(&empty[r], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (threadIdx.x >= NC) {  // ---- producer warp (as in k_irdft_readout, two input buffers)
+    const int lane = threadIdx.x - NC;
+    int slice = 0, k0 = 0, ks = 0, nl = 0, lpos = 0;
+    unsigned bits = 0;
+    for (int i = 0;; ++i) {
+      bool done = false;
+      while (lpos >= nl) {
+        int uu = 0;
+        if (lane == 0) uu = atomicAdd(counter, 1);
+        uu = __shfl_sync(0xFFFFFFFFu, uu, 0);
+        if (uu >= total_units) {
+          done = true;
+          break;
+        }
+        constexpr int SG = 2;  // slices in pairs (see k_irdft_readout)
+        const int grp = uu / (nunits * SG);
+        const int gs = min(SG, batch - grp * SG);
+        const int within = uu - grp * nunits * SG;
+        slice = grp * SG + within % gs;
+        const uint2 ub = __ldg(units + within / gs);
+        k0 = (int)ub.x;
+        const int k1 = (int)ub.y;
+        ks = k0 > 0 ? k0 - 1 : 0;
+        const int st = ks + lane;
+        bits = __ballot_sync(0xFFFFFFFFu, st < k1 && __ldg(step_need + st) != 0u);
+        nl = __popc(bits);
+        lpos = 0;
+      }
+      const int r = i & 1;
+      if (i >= 2) mbar_wait(&empty[r], (uint32_t)((i / 2 - 1) & 1));
+      if (done) {
+        if (lane == 0) {
+          items[i & 3] = make_int4(-1, 0, 0, 0);
+          mbar_arrive(&full[r]);
+        }
+        break;
+      }
+      const int kk = ks + (int)__fns(bits, 0, lpos + 1);
+      ++lpos;
+      const bool rd = kk >= k0;
+      uint32_t e0 = 0, e1 = 0;
+      if (rd && lane == 0) {
+        e0 = __ldg(step_off + kk);
+        e1 = __ldg(step_off + kk + 1);
+      }
+      if (lane == 0) {
+        items[i & 3] = make_int4(slice, kk | (rd ? 1 << 30 : 0), (int)e0, (int)e1);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[r], FS::STEP_BYTES);
+      }
+      __syncwarp();
+      if (lane < FS::NBOX)  // rows (r0, r0 + 1) as [m][2]; m >= nh is zero fill
+        tma_load_3d(inbuf + r * IN + 2 * (lane * 256), &ymap, 2 * (row_min + S * kk), lane * 256, slice, &full[r]);
+      const uint32_t pa = __shfl_sync(0xFFFFFFFFu, e0, 0), pb = __shfl_sync(0xFFFFFFFFu, e1, 0);
+      if (lane == 31 && pb > pa) prefetch_l2_bulk(entries + pa, 16u * (pb - pa));
+    }
+    return;
+  }
+
+  // ---- consumers
+  const int tid = threadIdx.x;
+  auto team = [] { asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory"); };
+  const int ntheta = N / 2;
+#pragma unroll 1
+  for (int i = 0;; ++i) {
+    const int r = i & 1;
+    mbar_wait(&full[r], (uint32_t)((i / 2) & 1));
+    const int4 itm = items[i & 3];
+    if (itm.x < 0) break;
+    const int slice = itm.x, kk = itm.y & 0x3FFFFFFF;
+    const bool rd = (itm.y >> 30) & 1;
+    const uint32_t e0 = (uint32_t)itm.z, e1 = (uint32_t)itm.w;
+    const float4* stg = reinterpret_cast<const float4*>(inbuf + r * IN);
+    float2* cur = rows + (i & 1) * RBA;
+    const float2* prev = rows + ((i + 1) & 1) * RBA;  // the previous item's rows: band kk - 1 when used
+    const int r0 = row_min + S * kk;
+    float* out = img + (size_t)slice * n * n;
+    uint4 pre = make_uint4(0x80000000u, 0, 0, 0), pre2 = pre;
+    const uint32_t ep = e0 + tid;
+    if (ep < e1) pre = __ldg(entries + ep);
+    if (ep + NC < e1) pre2 = __ldg(entries + ep + NC);
+    team();  // the previous item's readout is done with `cur` (it was that item's `prev`)
+    auto load = [&](int idx) -> float2 {  // Hermitian assembly of the packed pair, as k_row_irdft_mixed
+      const bool hi = idx > ntheta;
+      const int mm = hi ? N - idx : idx;
+      float4 x = stg[mm];
+      if (mm == 0 || mm == ntheta) {
+        x.y = 0.f;
+        x.w = 0.f;
+      }
+      if (hi) {
+        x.y = -x.y;
+        x.w = -x.w;
+      }
+      return make_float2(x.x - x.w, x.y + x.z);
+    };
+    // step A reads the input buffer (returned to the producer at the first team barrier), step B
+    // transforms `cur` in place; the call ends with a team barrier
+    int nsync = 0;
+    block_dft_mixed_team<Q, P, true, 2>(cur, tid, load, [&] {
+      team();
+      if (nsync++ == 0 && (tid & 31) == 0) mbar_arrive(&empty[r]);
+    });
+    if (rd) {  // readout: rows r0 (.x) and r0 + 1 (.y) of `cur`, row r0 - 1 = the previous band's .y
+      auto val = [&](int li, int j) -> float {
+        if (li < 0) return mixed_at<Q, P>(prev, j).y;
+        const float2 z = mixed_at<Q, P>(cur, j);
+        return li == 0 ? z.x : z.y;
+      };
+      auto pixel = [&](const uint4& ent) {
+        const int qy = (int)(ent.x & 0x7FFFu), qx = (int)((ent.x >> 15) & 0xFFFFu);
+        const int iyp = c + qy, iyn = n - 1 - c - qy;
+        const int jxp = c + qx, jxn = n - 1 - c - qx;
+        const bool dupy = iyn == iyp, dupx = jxn == jxp;
+        float v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f;
+        if (!(ent.x & 0x80000000u)) {
+          const int i0 = (int)(ent.y & 0xFFFFu), jr = (int)(ent.y >> 16);
+          const float wi = __uint_as_float(ent.z), wjr = __uint_as_float(ent.w);
+          const int l0 = i0 - r0, l1 = min(i0 + 1, nrho - 1) - r0;
+          auto sample = [&](int j0, float wj) {
+            if (j0 >= N) j0 -= N;
+            const int j1 = (j0 + 1 == N) ? 0 : j0 + 1;
+            const float a00 = val(l0, j0), a01 = val(l0, j1), a10 = val(l1, j0), a11 = val(l1, j1);
+            const float a0 = fmaf(wj, a01 - a00, a00);
+            const float a1 = fmaf(wj, a11 - a10, a10);
+            return fmaf(wi, a1 - a0, a0) * scale;
+          };
+          const bool wz = wjr == 0.f;
+          const float wm = wz ? 0.f : 1.f - wjr;
+          v1 = sample(jr, wjr);
+          v2 = sample(wz ? N / 2 - jr : N / 2 - jr - 1, wm);
+          v3 = sample(N / 2 + jr, wjr);
+          v4 = sample(wz ? N - jr : N - jr - 1, wm);
+        }
+        out[(size_t)iyp * n + jxp] = v1;
+        if (!dupx) out[(size_t)iyp * n + jxn] = v2;
+        if (!dupy) {
+          out[(size_t)iyn * n + jxp] = v4;
+          if (!dupx) out[(size_t)iyn * n + jxn] = v3;
+        }
+      };
+      if (ep < e1) {
+        uint4 ea = pre, eb = pre2, ec;
+        const uint32_t stp = NC;
+        uint32_t e = ep;
+        auto fetch = [&](uint4& dst) {
+          dst = make_uint4(0x80000000u, 0, 0, 0);
+          if (e + 2 * stp < e1) dst = __ldg(entries + e + 2 * stp);
+        };
+#pragma unroll 1
+        for (;;) {
+          fetch(ec);
+          pixel(ea);
+          if ((e += stp) >= e1) break;
+          fetch(ea);
+          pixel(eb);
+          if ((e += stp) >= e1) break;
+          fetch(eb);
+          pixel(ec);
+          if ((e += stp) >= e1) break;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic sizes (any nt, any ntheta; nphi = 2 ntheta need not be a power of two).
 // The length-nphi DFTs use Bluestein's identity with the same pow2 block_conv:
 //   X[k] = c[k] sum_n (x[n] c[n]) conj c[k-n],  c[n] = exp(-i pi n^2 / nphi),
@@ -1525,8 +1741,14 @@ int fused_band_rows(int nphi) {
     case 1024: return FusedShape<1024>::S;
     case 2048: return FusedShape<2048>::S;
     case 4096: return FusedShape<4096>::S;
+    case 25 * 256: case 3 * 512: case 5 * 512: case 9 * 512: case 3 * 1024: case 5 * 1024:
+      return 2;  // FusedMixedShape::S
     default: return -1;
   }
+}
+
+bool fused_mixed_available(const Dims& d) {
+  return d.band_rows == 2 && mixed_enabled() && mixed_radix_length(d.nphi);
 }
 
 namespace {
@@ -1560,8 +1782,42 @@ cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
 }
 }  // namespace
 
+namespace {
+template <int Q, int P>
+cudaError_t fused_mixed_impl(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch, int* counter,
+                             cudaStream_t s) {
+  using FS = FusedMixedShape<Q, P>;
+  if (d.band_rows != FS::S || (reinterpret_cast<uintptr_t>(Yh) & 15)) return cudaErrorInvalidValue;
+  auto k = k_irdft_readout_mixed<Q, P>;
+  cudaError_t e = prep(k, FS::SMEM);
+  if (e) return e;
+  CUtensorMap map;
+  e = encode_spectra_map(&map, Yh, d.nrho_pad, FS::NH, batch, 2, 256);
+  if (e) return e;
+  e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+  if (e) return e;
+  const int units = d.nunits * batch;
+  const int grid = units < d.nsm ? units : d.nsm;
+  k<<<grid, FS::NTHR, FS::SMEM, s>>>(map, img, d.nrho, d.n, d.nq, d.row_min, batch, counter, t.band_off,
+                                     t.band_need, reinterpret_cast<const uint2*>(t.units), d.nunits,
+                                     reinterpret_cast<const uint4*>(t.band_entries), d.out_scale);
+  return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Yh, float* img, int batch,
                                  int* counter, cudaStream_t s) {
+  if (fused_mixed_available(d)) {
+    switch (d.nphi) {
+      case 25 * 256: return fused_mixed_impl<25, 256>(d, t, Yh, img, batch, counter, s);
+      case 3 * 512: return fused_mixed_impl<3, 512>(d, t, Yh, img, batch, counter, s);
+      case 5 * 512: return fused_mixed_impl<5, 512>(d, t, Yh, img, batch, counter, s);
+      case 9 * 512: return fused_mixed_impl<9, 512>(d, t, Yh, img, batch, counter, s);
+      case 3 * 1024: return fused_mixed_impl<3, 1024>(d, t, Yh, img, batch, counter, s);
+      case 5 * 1024: return fused_mixed_impl<5, 1024>(d, t, Yh, img, batch, counter, s);
+      default: return cudaErrorNotSupported;
+    }
+  }
   switch (d.nphi) {
     case 512: return fused_impl<512>(d, t, Yh, img, batch, counter, s);
     case 1024: return fused_impl<1024>(d, t, Yh, img, batch, counter, s);

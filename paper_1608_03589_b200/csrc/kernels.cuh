@@ -65,6 +65,8 @@ cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y,
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Y, float* img, int batch,
                                  int* counter, cudaStream_t s);
 int fused_band_rows(int nphi);
+// generic plan whose mixed-radix nphi runs the fused inverse DFT + readout (bands of 2 rows)
+bool fused_mixed_available(const Dims& d);
 constexpr int kFusedMaxUnit = 24;  // longest fused work unit in bands (per-unit arrays, one lane per band + 1)
 cudaError_t launch_readout(const Dims& d, const DevTables& t, const float* lp, float* img, int batch, cudaStream_t s);
 

@@ -159,14 +159,17 @@ struct MixedShape {
 // Length-N DFT of load(n) (n in [0, N)) into the group buffers: afterwards X[k1 + Q k2] sits
 // at buf[k1 * PITCH + pad16(k2)] (read it with mixed_at).  Every thread of the CTA calls this
 // (blockDim.x == MixedShape::THREADS); ends with a CTA barrier.
-template <int Q, int P, bool INV, typename Load>
-__device__ __forceinline__ void block_dft_mixed(float2* buf, Load&& load) {
+// Team variant: `team` threads (tid in [0, THREADS)) call this with their own barrier for all of them
+// (team_sync) and named barriers from BAR0 for the length-P groups (when a group spans several warps);
+// no CTA-wide barrier, so other warps of the CTA (a TMA producer) may run independently.
+template <int Q, int P, bool INV, int BAR0, typename Load, typename TeamSync>
+__device__ __forceinline__ void block_dft_mixed_team(float2* buf, int tid, Load&& load, TeamSync&& team_sync) {
   using MS = MixedShape<Q, P>;
   constexpr int N = MS::N, TP = MS::TP, PITCH = MS::PITCH;
   constexpr float kStep = (INV ? 6.283185307179586f : -6.283185307179586f) / (float)N;
   // step A: DFT-Q over n1 for each n2, then the inter-step twiddle W_N^(n2 k1)
 #pragma unroll 1
-  for (int n2 = threadIdx.x; n2 < P; n2 += MS::THREADS) {
+  for (int n2 = tid; n2 < P; n2 += MS::THREADS) {
     float2 v[Q];
 #pragma unroll
     for (int n1 = 0; n1 < Q; ++n1) v[n1] = load(P * n1 + n2);
@@ -183,10 +186,10 @@ __device__ __forceinline__ void block_dft_mixed(float2* buf, Load&& load) {
       buf[k1 * PITCH + pad16(n2)] = cmul(v[k1], make_float2(cs, sn));
     }
   }
-  __syncthreads();
+  team_sync();
   // step B: group k1 transforms its row in place (every pass's twiddles from the SFU, SFU_MIN = 1:
   // no table; the inverse plans of 512 / 1024 points start with radix 4, so Ns = 4 passes occur)
-  const int g = threadIdx.x / TP, ti = threadIdx.x % TP;
+  const int g = tid / TP, ti = tid % TP;
   float2* row = buf + g * PITCH;
   auto ld = [&](int idx) -> float2 { return row[pad16(idx)]; };
   auto st = [&](int idx, float2 v) { row[pad16(idx)] = v; };
@@ -194,11 +197,16 @@ __device__ __forceinline__ void block_dft_mixed(float2* buf, Load&& load) {
   // threads (two 16-thread groups share a warp and its barrier), a named barrier per group otherwise
   auto gsync = [&] {
     if constexpr (TP <= 32) __syncwarp();
-    else asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(TP) : "memory");
+    else asm volatile("bar.sync %0, %1;" ::"r"(BAR0 + g), "r"(TP) : "memory");
   };
-  static_assert(TP <= 32 || MS::ROWS <= 15, "named barriers 1..15");
+  static_assert(TP <= 32 || BAR0 + MS::ROWS <= 16, "named barriers up to 15");
   block_fft<P, INV, true, true, false, 1>(row, ti, nullptr, ld, st, gsync);
-  __syncthreads();
+  team_sync();
+}
+
+template <int Q, int P, bool INV, typename Load>
+__device__ __forceinline__ void block_dft_mixed(float2* buf, Load&& load) {
+  block_dft_mixed_team<Q, P, INV, 1>(buf, threadIdx.x, load, [] { __syncthreads(); });
 }
 
 // X[k] after block_dft_mixed
