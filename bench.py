@@ -73,8 +73,8 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--slices", type=int, default=0, help="slices per rank per step (0 = config default)")
     ap.add_argument("--chunk", type=int, default=0,
-                    help="slices per internal pipeline chunk (0 = 8 for logpolar (x 2 streams), 16 for bst (x 1 stream): "
-                         "the measured best of 4 / 8 / 16)")
+                    help="slices per internal pipeline chunk (0 = 32 for the power-of-two log-polar path (x 2 streams), "
+                         "16 for generic sizes and bst: the measured bests)")
     ap.add_argument("--e2e-slices", type=int, default=128)
     ap.add_argument("--e2e-chunk", type=int, default=4)
     ap.add_argument("--streams", type=int, default=0,
@@ -396,7 +396,10 @@ def run_ours(a, d: Dist):
     info = {} if bst else plan.info
     generic = bool(info.get("generic", 0))
     unfused = generic and not (info.get("phi_q", 0) > 0 and info.get("band_rows", 0) == 2)
-    chunk = min(a.chunk if a.chunk > 0 else (16 if (bst or generic) else 8), S)
+    # chunks of 32 slices: with K3's K-hat column held in TMEM per CTA, longer launches amortise each
+    # CTA's prologue and the launches' tails (measured at 2048^2: chunk 8 / 16 / 24 / 32 / 48 / 64 / 128 ->
+    # 8720 / 8906 / 8973 / 9000 / 8953 / 8977 / 8887 slices/s on two streams)
+    chunk = min(a.chunk if a.chunk > 0 else (16 if (bst or generic) else 32), S)
     nstreams = a.streams if a.streams > 0 else (1 if (bst or unfused) else 2)
     # one workspace per stream: the plan is immutable, chunks on different streams overlap
     wss = [None if bst else torch.empty(plan.workspace_bytes(chunk), dtype=torch.uint8, device=dev)

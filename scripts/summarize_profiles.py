@@ -59,7 +59,7 @@ if os.path.exists(rep):
             ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smem st conflicts"),
             ("launch__registers_per_thread", "regs"), ("launch__grid_size", "grid"), ("launch__block_size", "block")]
     stall = [i for i, n in enumerate(h) if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")]
-    out.append("## ncu --set full (one launch per kernel, chunk of 8 slices 2048^2 FBP (bench default))\n\n")
+    out.append("## ncu --set full (one launch per kernel, chunk of 32 slices 2048^2 FBP (bench default))\n\n")
     names = [re.sub(r"\(.*", "", r[h.index("Kernel Name")]).replace("void ", "") for r in rows[2:]]
     out.append("| metric | " + " | ".join(names) + " |\n|---|" + "---|" * len(names) + "\n")
     for k, label in keys:

@@ -8,7 +8,7 @@ sys.path.insert(0, root)
 from paper_1608_03589_b200 import roofline  # noqa: E402
 
 rep, tag, engine = sys.argv[1], sys.argv[2], (sys.argv[3] if len(sys.argv) > 3 else "logpolar")
-slices = 8
+slices = int(sys.argv[4]) if len(sys.argv) > 4 else 32  # slices per captured launch (the bench chunk)
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, units = rows[0], rows[1]
