@@ -1,3 +1,5 @@
+"""Mixed-radix row-DFT smoke over several angle counts, with LPBP_MIXED=1 / 0 (Bluestein) and
+CUDA_LAUNCH_BLOCKING=1 so a failing kernel names its stage: python scripts/dbg_mixed.py."""
 import os, sys, subprocess
 code = r'''
 import sys, numpy as np, torch
