@@ -123,6 +123,32 @@ class Dist:
                   "(functional check, not a scaling number)", file=sys.stderr)
         return self.local % max(nd, 1)
 
+    def bind_numa(self, cuda_index: int) -> str:
+        """N > 1: pin this rank's process to the host cores local to its GPU (the PCI device's
+        local_cpulist in sysfs), so the pinned buffers of the e2e leg are allocated on the GPU's own
+        socket and every rank's H2D / D2H stays off the inter-socket link.  Returns what was done."""
+        if self.world <= 1 or getattr(self, "shared_device", False):
+            return "not bound (one rank)" if self.world <= 1 else "not bound (ranks share a device)"
+        try:
+            import torch
+
+            pr = torch.cuda.get_device_properties(cuda_index)
+            dev = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            with open(f"/sys/bus/pci/devices/{dev}/local_cpulist") as f:
+                spec = f.read().strip()
+            cpus = set()
+            for part in spec.split(","):
+                if part:
+                    lo, _, hi = part.partition("-")
+                    cpus.update(range(int(lo), int(hi or lo) + 1))
+            cpus &= os.sched_getaffinity(0)
+            if cpus:
+                os.sched_setaffinity(0, cpus)
+                return f"{len(cpus)} cores local to GPU {dev} (sysfs local_cpulist)"
+            return "not bound (no local cores in this process's set)"
+        except Exception as e:  # no sysfs entry: leave the scheduler's placement
+            return f"not bound ({type(e).__name__})"
+
     def barrier(self):
         if self.pg:
             self.pg.barrier()
@@ -375,6 +401,7 @@ def run_ours(a, d: Dist):
     ci = d.cuda_index()
     torch.cuda.set_device(ci)
     dev = torch.device("cuda", ci)
+    numa = d.bind_numa(ci)
     c = bench_config(a)
     nt, nth, n = c["nt"], c["ntheta"], c["n"]
     total = a.slices or c["slices"]
@@ -521,6 +548,7 @@ def run_ours(a, d: Dist):
                             "l2": f"no flush: {S * nt * nth * 4 / 1e9:.1f} GB of sinograms per rank per step "
                                   f">> 126 MB L2"},
                            **({"shared_device": True} if getattr(d, "shared_device", False) else {}),
+                           **({"host_binding": numa} if d.world > 1 else {}),
                            **({"engine": "bst", "L": info["L"], "big": info["big"], "m_need": info["m_need"]} if bst
                               else {"nrho": info["nrho"], "L": info["L"], "nphi": info["nphi"]})),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
