@@ -523,3 +523,19 @@ def test_mixed_fused_batch_invariance(pkg, nt, nth, n):
     lp = plan.logpolar(plan.filter(x))
     b = plan.readout(lp)
     assert O.relative_l2(b.cpu().numpy(), a.cpu().numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("nt,nth,n,fbp", [(97, 1280, 64, True), (131, 3200, 90, False), (64, 2304, 33, True)])
+def test_mixed_radix_odd_and_small_shapes(pkg, nt, nth, n, fbp):
+    """Mixed-radix angle counts with odd nt (row-spectra pitch padded to even), odd n and a small
+    image: BP / FBP against the oracle."""
+    rng = np.random.default_rng(nt * 7 + nth)
+    gd = np.cumsum(rng.standard_normal((nt, nth)), axis=0).astype(np.float32).astype(np.float64) * 0.05
+    g = pkg.Sinogram(nt, nth, gd)
+    if fbp:
+        got = pkg.fbp(g, pkg.FilterSpec(), engine="logpolar", n=n).values
+        ref = O.fbp_logpolar(gd, n)
+    else:
+        got = pkg.logpolar_backproject(g, n).values
+        ref = O.logpolar_backproject(gd, n)
+    assert report(f"mixed odd {nt}x{nth}->{n} fbp={fbp}", got, ref) <= RTOL
