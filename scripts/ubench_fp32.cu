@@ -48,6 +48,9 @@ __global__ void k(float* out, float s, long long* cyc) {
       if constexpr (MODE == 5) { x[i] = f2(x[i], y[i], c); fx[i] = fmaf(fx[i], fy[i], s); }  // mixed
       if constexpr (MODE == 7) x[i] = f2(x[i], 0x3f8000003f800000ull, y[i]);   // FFMA2 broadcast immediate
       if constexpr (MODE == 6) { x[i] = f2(x[i], y[i], c); fx[i] = fx[i] + fy[i]; }          // FFMA2 + FADD
+      if constexpr (MODE == 8) { x[i] = f2(x[i], y[i], c); y[i] = a2(y[i], c); }              // FFMA2 + FADD2
+      if constexpr (MODE == 9) { x[i] = m2(x[i], c); y[i] = a2(y[i], c); }                   // FMUL2 + FADD2
+      if constexpr (MODE == 10) { x[i] = f2(x[i], y[i], c); x[(i + 4) & 7] = f2(x[(i + 4) & 7], y[i], c); y[i] = a2(y[i], c); }  // 2 FFMA2 + FADD2
     }
   }
   long long t1 = clock64();
@@ -62,10 +65,10 @@ int main() {
   long long* cyc;
   cudaMalloc(&out, 4);
   cudaMalloc(&cyc, 8);
-  const char* names[] = {"FFMA2 (3 reg)", "FADD2", "FMUL2", "FFMA (3 reg)", "FFMA (imm)", "FFMA2 + FFMA", "FFMA2 + FADD", "FFMA2 (imm)"};
-  const int per_iter[] = {8, 8, 8, 8, 8, 16, 16, 8};
+  const char* names[] = {"FFMA2 (3 reg)", "FADD2", "FMUL2", "FFMA (3 reg)", "FFMA (imm)", "FFMA2 + FFMA", "FFMA2 + FADD", "FFMA2 (imm)", "FFMA2 + FADD2", "FMUL2 + FADD2", "2 FFMA2 + FADD2"};
+  const int per_iter[] = {8, 8, 8, 8, 8, 16, 16, 8, 16, 16, 24};
   for (int warps : {8, 16, 32}) {
-    for (int mode = 0; mode < 8; ++mode) {
+    for (int mode = 0; mode < 11; ++mode) {
       auto run = [&]() {
         switch (mode) {
           case 0: k<0><<<148, warps * 32>>>(out, 1.f, cyc); break;
@@ -76,6 +79,9 @@ int main() {
           case 5: k<5><<<148, warps * 32>>>(out, 1.f, cyc); break;
           case 6: k<6><<<148, warps * 32>>>(out, 1.f, cyc); break;
           case 7: k<7><<<148, warps * 32>>>(out, 1.f, cyc); break;
+          case 8: k<8><<<148, warps * 32>>>(out, 1.f, cyc); break;
+          case 9: k<9><<<148, warps * 32>>>(out, 1.f, cyc); break;
+          case 10: k<10><<<148, warps * 32>>>(out, 1.f, cyc); break;
         }
       };
       run();
