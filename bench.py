@@ -113,7 +113,7 @@ class Dist:
     def cuda_index(self) -> int:
         """This rank's GPU: LOCAL_RANK, wrapped onto the visible devices.  On a box with fewer GPUs
         than local ranks (functional checks of the N > 1 path only) ranks share a device and the
-        line says so in config.shared_device; such a run is not a scaling measurement."""
+        line says so in run.shared_device; such a run is not a scaling measurement."""
         import torch
 
         nd = torch.cuda.device_count()
@@ -325,6 +325,37 @@ def workload_name(config: int, c: dict) -> str:
     return f"{tag}: {'FBP' if c['fbp'] else 'BP'} {c['nt']} bins x {c['ntheta']} angles -> {c['n']}^2"
 
 
+def workload_config(a, c: dict, world: int, geom: dict, chunk: int, nstreams: int) -> dict:
+    """The line's `config`: identical in both arms for the same command line (the driver pairs the
+    lines on it).  Everything here follows from the arguments, the world size and the plan geometry
+    `geom` = {nrho, L, nphi}; what depends on the box (host binding, ranks sharing a device) is
+    reported under `run` instead."""
+    total = a.slices or c["slices"]
+    ranks = [rank_slices(total, world, r, a.scaling) for r in range(world)]
+    S = len(ranks[0])
+    return {"workload": workload_name(a.config, c), "slices_total": sum(len(r) for r in ranks),
+            "slices_per_rank": S, "rank_slice_ranges": [[r[0], r[-1] + 1] if r else [0, 0] for r in ranks],
+            "chunk": min(chunk, S), "streams": nstreams,
+            "parallelism": f"slice-shard x{world} ({a.scaling} scaling, no inter-GPU exchange)",
+            "l2": f"no flush: {S * c['nt'] * c['ntheta'] * 4 / 1e9:.1f} GB of sinograms per rank per step "
+                  f">> 126 MB L2",
+            "nrho": int(geom["nrho"]), "L": int(geom["L"]), "nphi": int(geom["nphi"])}
+
+
+def default_schedule(a, generic: bool, unfused: bool, bst: bool = False) -> tuple[int, int]:
+    """(chunk, streams) of the device-resident leg.  Chunks of 32 slices: with K3's K-hat column held
+    in TMEM per CTA, longer launches amortise each CTA's prologue and the launches' tails (measured at
+    2048^2: chunk 8 / 16 / 24 / 32 / 48 / 64 / 128 -> 8720 / 8906 / 8973 / 9000 / 8953 / 8977 / 8887
+    slices/s on two streams).  A generic-size plan whose inverse DFT + readout stay unfused (Bluestein
+    lengths, odd nt: through an HBM log-polar image) runs best on one stream, like BST: two chunks in
+    flight halve the L2 the readout's gathers hit (LNLS before its fused path: 3175 slices/s on one
+    stream, 2373 on two); the fused mixed-radix path takes two streams like the power-of-two one (LNLS:
+    4800 vs 4596); generic plans take chunks of 16."""
+    chunk = a.chunk if a.chunk > 0 else (16 if (bst or generic) else 32)
+    nstreams = a.streams if a.streams > 0 else (1 if (bst or unfused) else 2)
+    return chunk, nstreams
+
+
 def bench_config(a) -> dict:
     """The config's workload, with --geometry NTxNTHETA overriding the sinogram shape."""
     from oracle import phantoms
@@ -343,6 +374,13 @@ def run_reference(a, d: Dist):
     from oracle import phantoms
 
     c = bench_config(a)
+    # the plan geometry our arm reports in `config`, restated from the oracle's mesh rule (no GPU here)
+    from oracle import fastbp_oracle as fo
+    _, _, nr, _ = fo.lp_geometry(c["nt"], c["n"])
+    nphi = 2 * c["ntheta"]
+    geom = {"nrho": nr, "L": 1 << (2 * nr - 2).bit_length(), "nphi": nphi}
+    pow2 = nphi & (nphi - 1) == 0 and 512 <= nphi <= 4096 and c["nt"] % 4 == 0
+    generic, fused = not pow2, nphi in (6400, 1536, 2560, 4608, 3072, 5120)
     workers = cpu_workers(a.cpu_workers)
     vals = []
     for i in range(a.warmup + a.steps):
@@ -355,7 +393,8 @@ def run_reference(a, d: Dist):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded random-ellipse sinograms + 1% Gaussian noise)",
-        "config": {"workload": workload_name(a.config, c), "slices_per_step": workers},
+        "config": workload_config(a, c, a.gpus, geom, *default_schedule(a, generic, generic and not fused)),
+        "run": {"slices_per_step": workers},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": f"{workers} slices per step, one per concurrent worker process, reconstruction "
                                    f"only (inputs generated untimed), oracle/fastbp_oracle.py (numpy/scipy "
@@ -415,19 +454,11 @@ def run_ours(a, d: Dist):
     shards = d.gather([global_ids[0], global_ids[-1] + 1] if global_ids else [0, 0])
     sino = p.synth.config_batch(a.config, global_ids, dev, geometry=(nt, nth))
     out = torch.empty((S, n, n), dtype=torch.float32, device=dev)
-    # a generic-size plan whose inverse DFT + readout stay unfused (Bluestein lengths, odd nt: through an
-    # HBM log-polar image) runs best on one stream, like BST: two chunks in flight halve the L2 the
-    # readout's gathers hit (LNLS before its fused path: 3175 slices/s on one stream, 2373 on two); the
-    # fused mixed-radix path takes two streams like the power-of-two one (LNLS: 4800 vs 4596); generic
-    # plans take chunks of 16
     info = {} if bst else plan.info
     generic = bool(info.get("generic", 0))
     unfused = generic and not (info.get("phi_q", 0) > 0 and info.get("band_rows", 0) == 2)
-    # chunks of 32 slices: with K3's K-hat column held in TMEM per CTA, longer launches amortise each
-    # CTA's prologue and the launches' tails (measured at 2048^2: chunk 8 / 16 / 24 / 32 / 48 / 64 / 128 ->
-    # 8720 / 8906 / 8973 / 9000 / 8953 / 8977 / 8887 slices/s on two streams)
-    chunk = min(a.chunk if a.chunk > 0 else (16 if (bst or generic) else 32), S)
-    nstreams = a.streams if a.streams > 0 else (1 if (bst or unfused) else 2)
+    chunk, nstreams = default_schedule(a, generic, unfused, bst)
+    chunk = min(chunk, S)
     # one workspace per stream: the plan is immutable, chunks on different streams overlap
     wss = [None if bst else torch.empty(plan.workspace_bytes(chunk), dtype=torch.uint8, device=dev)
            for _ in range(nstreams)]
@@ -536,21 +567,19 @@ def run_ours(a, d: Dist):
                          f"oracle/fastbp_oracle.py ({'fbp_bst' if bst else 'fbp_logpolar'}), CPU {cpu_model()}"}
 
     slices_total = int(d.sum(S))  # a collective: every rank takes part
+    assert slices_total == sum(hi - lo for lo, hi in shards), (slices_total, shards)
     if d.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (device-generated seeded random-ellipse sinograms, K=50, 1% Gaussian noise)",
-            "config": dict({"workload": workload_name(a.config, c) + (" (BST engine)" if bst else ""),
-                            "slices_total": slices_total, "slices_per_rank": S, "rank_slice_ranges": shards,
-                            "chunk": chunk, "streams": nstreams,
-                            "parallelism": f"slice-shard x{d.world} ({a.scaling} scaling, no inter-GPU exchange)",
-                            "l2": f"no flush: {S * nt * nth * 4 / 1e9:.1f} GB of sinograms per rank per step "
-                                  f">> 126 MB L2"},
-                           **({"shared_device": True} if getattr(d, "shared_device", False) else {}),
-                           **({"host_binding": numa} if d.world > 1 else {}),
-                           **({"engine": "bst", "L": info["L"], "big": info["big"], "m_need": info["m_need"]} if bst
-                              else {"nrho": info["nrho"], "L": info["L"], "nphi": info["nphi"]})),
+            "config": dict(workload_config(a, c, d.world, info if not bst else {"nrho": 0, "L": info["L"], "nphi": 0},
+                                           chunk, nstreams),
+                           **({"workload": workload_name(a.config, c) + " (BST engine)", "engine": "bst",
+                               "big": info["big"], "m_need": info["m_need"]} if bst else {})),
+            "run": dict({"rank_slice_ranges_gathered": shards},
+                        **({"shared_device": True} if getattr(d, "shared_device", False) else {}),
+                        **({"host_binding": numa} if d.world > 1 else {})),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": per_launch_ms,

@@ -1,7 +1,7 @@
 """The N > 1 bench path end to end (what the driver's scaling run launches), as a functional check.
 
 Two ranks under torch.distributed.run on the box's GPU(s): on a one-GPU box both ranks share cuda:0
-(bench.py flags `config.shared_device`; no scaling number is taken from such a run).  The ranks never
+(bench.py flags `run.shared_device`; no scaling number is taken from such a run).  The ranks never
 wait on each other's kernels — the only cross-rank traffic is the gloo barrier and the max/sum of
 timings — so sharing a device cannot deadlock.  Checks that every collective is reached by every rank
 (a rank-0-only reduction once hung the line's assembly), that the strong-scaling shards cover the
@@ -32,6 +32,8 @@ def test_bench_two_ranks_strong_shards():
     assert c["slices_total"] == 32 and c["slices_per_rank"] == 16
     ids = [i for lo, hi in c["rank_slice_ranges"] for i in range(lo, hi)]
     assert sorted(ids) == list(range(32))
+    # what the ranks actually took (gathered) is what `config` states from the arguments
+    assert [list(v) for v in d["run"]["rank_slice_ranges_gathered"]] == c["rank_slice_ranges"]
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
     for k in ("roofline", "pipeline", "clocks", "ms_per_step"):
         assert k in d

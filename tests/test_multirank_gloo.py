@@ -10,6 +10,8 @@ import socket
 import pytest
 import torch.multiprocessing as mp
 
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 
 def _free_port():
     s = socket.socket()
@@ -71,3 +73,40 @@ def test_rank_slices_config3_at_1_2_4_8():
         ids = [i for r in range(world) for i in bench.rank_slices(2048, world, r, "strong")]
         assert ids == list(range(2048))
         assert {len(bench.rank_slices(2048, world, r, "strong")) for r in range(world)} == {2048 // world}
+
+
+def test_both_arms_state_the_same_config():
+    """The reference arm's `config` (built without a GPU from the oracle's mesh rule) is the dict our arm
+    prints for the same command line: same keys, same values, at every world size of the scaling run."""
+    import argparse
+
+    import bench
+
+    from oracle import fastbp_oracle as fo, phantoms
+
+    for world in (1, 2, 4, 8):
+        a = argparse.Namespace(slices=0, scaling="strong", config=3, chunk=0, streams=0, geometry=None, gpus=world)
+        c = dict(phantoms.CONFIGS[3])
+        _, _, nr, _ = fo.lp_geometry(c["nt"], c["n"])
+        geom = {"nrho": nr, "L": 8192, "nphi": 4096}
+        cfg = bench.workload_config(a, c, world, geom, *bench.default_schedule(a, False, False))
+        assert cfg["slices_total"] == 2048 and cfg["slices_per_rank"] == 2048 // world
+        assert [i for lo, hi in cfg["rank_slice_ranges"] for i in range(lo, hi)] == list(range(2048))
+        assert (cfg["nrho"], cfg["L"], cfg["nphi"], cfg["chunk"], cfg["streams"]) == (3900, 8192, 4096, 32, 2)
+        assert cfg["workload"] == "config3: FBP 2048 bins x 2048 angles -> 2048^2"
+
+
+def test_reference_arm_line_config_matches(tmp_path):
+    """`bench.py --impl reference` on a tiny sample: one JSON line whose config is workload_config's."""
+    import json
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "1", "--steps", "1",
+                        "--warmup", "0", "--cpu-workers", "2"], cwd=REPO, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["config"]["nphi"] == 1024 and d["config"]["L"] == 2048
+    assert set(d["config"]) == {"workload", "slices_total", "slices_per_rank", "rank_slice_ranges", "chunk",
+                                "streams", "parallelism", "l2", "nrho", "L", "nphi"}
+    assert d["e2e"]["value"] == d["value"] and d["cpu_baseline"]["kind"] == "port"
