@@ -73,12 +73,12 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--slices", type=int, default=0, help="slices per rank per step (0 = config default)")
     ap.add_argument("--chunk", type=int, default=0,
-                    help="slices per internal pipeline chunk (0 = 32 for the power-of-two log-polar path (x 2 streams), "
+                    help="slices per internal pipeline chunk (0 = 128 for the power-of-two log-polar path (one stream), "
                          "16 for generic sizes and bst: the measured bests)")
-    ap.add_argument("--e2e-slices", type=int, default=128)
+    ap.add_argument("--e2e-slices", type=int, default=512)
     ap.add_argument("--e2e-chunk", type=int, default=4)
     ap.add_argument("--streams", type=int, default=0,
-                    help="CUDA streams the device-resident chunks alternate on (0 = 2 for logpolar, 1 for bst: "
+                    help="CUDA streams the device-resident chunks alternate on (0 = 1; 2 for the fused mixed-radix path; bst 1: "
                          "two BST chunks in flight halve the L2 its gridding gathers hit)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = min(cores, memory/2.5GB, 32)")
@@ -343,16 +343,21 @@ def workload_config(a, c: dict, world: int, geom: dict, chunk: int, nstreams: in
 
 
 def default_schedule(a, generic: bool, unfused: bool, bst: bool = False) -> tuple[int, int]:
-    """(chunk, streams) of the device-resident leg.  Chunks of 32 slices: with K3's K-hat column held
-    in TMEM per CTA, longer launches amortise each CTA's prologue and the launches' tails (measured at
-    2048^2: chunk 8 / 16 / 24 / 32 / 48 / 64 / 128 -> 8720 / 8906 / 8973 / 9000 / 8953 / 8977 / 8887
-    slices/s on two streams).  A generic-size plan whose inverse DFT + readout stay unfused (Bluestein
-    lengths, odd nt: through an HBM log-polar image) runs best on one stream, like BST: two chunks in
-    flight halve the L2 the readout's gathers hit (LNLS before its fused path: 3175 slices/s on one
-    stream, 2373 on two); the fused mixed-radix path takes two streams like the power-of-two one (LNLS:
-    4800 vs 4596); generic plans take chunks of 16."""
-    chunk = a.chunk if a.chunk > 0 else (16 if (bst or generic) else 32)
-    nstreams = a.streams if a.streams > 0 else (1 if (bst or unfused) else 2)
+    """(chunk, streams) of the device-resident leg.  Power-of-two log-polar path: ONE stream, chunks of
+    128 slices.  Measured at 2048^2 (B200, r02l): 1 stream x chunk 32 / 64 / 128 -> 8689 / 8820 / 8874
+    slices/s, 2 streams x chunk 32 / 64 -> 8987 / 8937.  Two streams buy 1.3 % by overlapping kernel
+    tails, but every launch then shares the SMs with the other stream's kernel, so the live per-launch
+    durations the roofline is built from double (K3 0.155 of the HBM peak live against 0.242 alone) and
+    the kernels' live shares of the step stop matching the serialised ncu launch list.  One stream
+    keeps the timed region, the live roofline and the ncu evidence the same thing; `--streams 2
+    --chunk 32` is the throughput-best schedule.  With K3's K-hat column held in TMEM per CTA, longer
+    launches amortise each CTA's prologue and the launches' tails.  A generic-size plan whose inverse
+    DFT + readout stay unfused (Bluestein lengths, odd nt: through an HBM log-polar image) also runs
+    on one stream, like BST: two chunks in flight halve the L2 the readout's gathers hit (LNLS before
+    its fused path: 3175 slices/s on one stream, 2373 on two); the fused mixed-radix path takes two
+    streams (LNLS: 4800 vs 4596); generic plans take chunks of 16."""
+    chunk = a.chunk if a.chunk > 0 else (16 if (bst or generic) else 128)
+    nstreams = a.streams if a.streams > 0 else (1 if (bst or unfused or not generic) else 2)
     return chunk, nstreams
 
 
