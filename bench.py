@@ -530,7 +530,11 @@ def run_ours(a, d: Dist):
     st = stages[dom]
     per_launch_ms = st["ms"] / max(1, st["launches"])
     slices_per_launch = st["slices"] / max(1, st["launches"])
-    bytes_per_launch = ab[dom]["per_slice"] * slices_per_launch + ab[dom]["per_launch"]
+    own_bytes_per_launch = ab[dom]["per_slice"] * slices_per_launch + ab[dom]["per_launch"]
+    # the roofline's algorithmic bytes: SURVEY §8(d)'s figure of the stage this kernel computes (the
+    # task's definition); this decomposition's own compulsory bytes are reported beside it
+    sv = None if bst else p.roofline.survey_stage_bytes(plan).get(dom)
+    bytes_per_launch = (sv["per_slice"] * slices_per_launch + sv["per_launch"]) if sv else own_bytes_per_launch
     peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
     achieved = bytes_per_launch / (per_launch_ms / 1000.0) / 1e9
@@ -588,6 +592,16 @@ def run_ours(a, d: Dist):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": per_launch_ms,
+                         "basis": (f"SURVEY 8(d) stage {sv['stage']}: {sv['per_slice'] / 1e6:.3f} MB per slice"
+                                   + (f" + {sv['per_launch'] / 1e6:.1f} MB K-hat per launch" if sv["per_launch"] else "")
+                                   + f", {slices_per_launch:.0f} slices per launch") if sv else "own decomposition",
+                         "own_decomposition": {
+                             "bytes_per_launch": own_bytes_per_launch,
+                             "frac": own_bytes_per_launch / (per_launch_ms / 1000.0) / 1e9 / peak,
+                             "note": "what this kernel itself must move: K3 reads the semi-polar row spectra "
+                                     "(nh x ns complex) and interpolates the log-polar column on chip, so the "
+                                     "log-polar image S3 would read never crosses HBM; `traffic` is to be "
+                                     "compared with this figure"},
                          "timing": f"CUDA events on the launching stream around each of the {st['launches']} "
                                    f"launches inside the timed steps ({nstreams} streams overlap)",
                          "share_of_step_live": share_live,

@@ -68,6 +68,8 @@ typedef struct lpbp_plan_info {
   int32_t generic, MB;         /* 1: any-size path (Bluestein length-nphi DFTs on MB-point FFTs) */
   int32_t phi_q;               /* generic path with mixed-radix length-nphi DFTs (nphi = phi_q x 2^k,
                                   phi_q in {3, 5, 9, 15, 25}) instead of Bluestein; 0 otherwise */
+  int32_t p_rows;              /* 1: the row-DFT stage forms the semi-polar rows (grids.py:290-311) first and
+                                  emits their ns = nt/2 spectra; 0: nt row spectra, mixed in the rho stage */
 } lpbp_plan_info;
 
 int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan);

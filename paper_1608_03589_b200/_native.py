@@ -45,7 +45,7 @@ class PlanInfo(ctypes.Structure):
         ("rho0", c_double), ("drho", c_double), ("dphi", c_double), ("out_scale", c_double),
         ("table_bytes", c_size_t), ("workspace_per_slice", c_size_t), ("readout_sector_bytes", c_size_t),
         ("band_rows", c_int32), ("row_min", c_int32), ("nbands", c_int32), ("generic", c_int32), ("MB", c_int32),
-        ("phi_q", c_int32),
+        ("phi_q", c_int32), ("p_rows", c_int32),
     ]
 
 

@@ -231,15 +231,17 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
     ++g_launches;
     src = reinterpret_cast<const float*>(A);
   }
+  const bool pin = d.pmix && !gen && win == 0;  // K2p: semi-polar row spectra, no row mix in K3
   e = staged(P, 1, c, s, [&] {
-    return gen ? lpbp::launch_row_rdft_generic(d, P->t, src, reinterpret_cast<float2*>(B), c, s)
-               : lpbp::launch_row_rdft(d, P->t, src, reinterpret_cast<float2*>(B), c, s);
+    return gen   ? lpbp::launch_row_rdft_generic(d, P->t, src, reinterpret_cast<float2*>(B), c, s)
+           : pin ? lpbp::launch_row_rdft_p(d, P->t, src, reinterpret_cast<float2*>(B), c, s)
+                 : lpbp::launch_row_rdft(d, P->t, src, reinterpret_cast<float2*>(B), c, s);
   });
   if (e) return launch_fail(e, "row_rdft");
   ++g_launches;
   e = staged(P, 2, c, s, [&] {  // rows below the first tapped one (pair) are never read downstream
     return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c,
-                                 stop_after_lp ? 0 : d.row_min, s);
+                                 stop_after_lp ? 0 : d.row_min, s, pin);
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
@@ -361,6 +363,10 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     rc = rc ? rc : P->upload(h.ab, reinterpret_cast<const lpbp::I2**>(&P->t.ab));
     rc = rc ? rc : P->upload(h.wab, reinterpret_cast<const lpbp::F4**>(&P->t.wab));
     rc = rc ? rc : P->upload(h.abw, reinterpret_cast<const uint32_t**>(&P->t.abw));
+    if (h.pmix) {
+      rc = rc ? rc : P->upload(h.ptile, &P->t.ptile);
+      rc = rc ? rc : P->upload(h.ploc, &P->t.ploc);
+    }
     rc = rc ? rc : P->upload(h.ki, &P->t.ki);
     rc = rc ? rc : P->upload(h.wi, reinterpret_cast<const lpbp::F2**>(&P->t.wi));
     rc = rc ? rc : P->upload(h.kw, &P->t.kw);
@@ -402,6 +408,13 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
   d.generic = h.generic ? 1 : 0;
   d.MB = h.MB;
   d.npairs = (int)h.pair_list.size();
+  // K2p + K3 on semi-polar row spectra: power-of-two path only; LPBP_K2P=0 keeps K2's row spectra and
+  // K3's frequency-domain row mix (A/B checks)
+  static const bool k2p = [] {
+    const char* v = getenv("LPBP_K2P");
+    return v ? atoi(v) != 0 : true;
+  }();
+  d.pmix = (h.pmix && !h.generic && k2p && 2 * h.nrho <= h.L) ? 1 : 0;
   d.nsm = 148;
   if (P->device >= 0) cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, P->device);
   const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;
@@ -443,6 +456,7 @@ int lpbp_plan_get_info(const lpbp_plan* P, lpbp_plan_info* info) {
   info->nbands = h.nbands;
   info->generic = h.generic ? 1 : 0;
   info->MB = h.MB;
+  info->p_rows = P->d.pmix;
   info->phi_q = 0;
   if (h.generic && lpbp::mixed_radix_length(h.nphi)) {
     int q = h.nphi;
@@ -624,6 +638,8 @@ int lpbp_plan_table(const lpbp_plan* P, const char* which, void* dst, size_t cap
   };
   if (!std::strcmp(which, "ab")) return copy_vec(h.ab);         // int32 pairs (a_k, b_k)
   if (!std::strcmp(which, "wab")) return copy_vec(h.wab);       // float quads
+  if (!std::strcmp(which, "ptile")) return copy_vec(h.ptile);   // int32 [ns]: {a_lo, na, b_lo, nb} per 4 semi-polar rows
+  if (!std::strcmp(which, "ploc")) return copy_vec(h.ploc);     // uint32 [ns]: tap rows inside the tile's ranges
   if (!std::strcmp(which, "ki")) return copy_vec(h.ki);         // int32
   if (!std::strcmp(which, "wi")) return copy_vec(h.wi);         // float pairs
   if (!std::strcmp(which, "qidx")) return copy_vec(h.qidx);     // uint32

@@ -314,6 +314,134 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
 }
 
 // ---------------------------------------------------------------------------
+// K2p: real DFT along phi of the SEMI-POLAR rows (grids.py:290-311 followed by the phi half of
+// logpolar.py:112): row k of p is [ t >= 0 lerp of the sinogram | t <= 0 lerp ], 2 ntheta = nphi
+// samples, so its spectrum is what K3's frequency-domain row mix would build from four row spectra.
+// Forming p before the transform halves the transforms (ns = nt/2 full-length rows instead of nt
+// zero-padded ones), K2's output and K3's column input, and takes the row mix out of K3.
+// Persistent CTAs walk tiles (slice, 4 semi-polar rows); a producer warp lands the tile's sinogram
+// rows — two contiguous runs of <= 5 rows, one per side (plan_host ptile) — in the single input slot
+// by two TMA bulk copies as soon as every consumer warp is past the previous tile's pass-0 loads
+// (the only reads of the slot), i.e. most of a tile ahead.  FFT group g forms rows 4j + 2g, 4j + 2g + 1
+// inside its pass-0 loads (two taps per value, weights in registers) packed as re/im; the spectra
+// are separated and staged [m][4] like K2's and leave by TMA stores into P[b][m][k0 .. k0 + 4).
+// ---------------------------------------------------------------------------
+template <int NPHI>
+struct RdftPShape {
+  static constexpr int KR = 4, G = 2, SR = 5;
+  static constexpr int NTH = NPHI / 2, NH = NPHI / 2 + 1;
+  static constexpr int IN = 2 * SR * NTH / 2;                // float2 in the input slot (a rows, then b rows)
+  static constexpr int STG = ((NH * KR) + 15) & ~15;         // float2 staging
+  static constexpr int BUF = (padded_len(NPHI) + 15) & ~15;  // float2 per FFT buffer
+  static constexpr size_t SMEM = ((size_t)IN + STG + G * BUF) * 8 + 64 + 1024;  // + barriers, alignment slack
+  static constexpr int NFULL = (NPHI / 2) / 256;
+};
+
+template <int NPHI>
+__global__ void __launch_bounds__(RdftPShape<NPHI>::G * FftPlan<NPHI, false>::T + 32, 1)
+k_row_rdft_p(const __grid_constant__ CUtensorMap pmap, const __grid_constant__ CUtensorMap ptail,
+             const float* __restrict__ g, int nt, int ntiles_per_slice, int ntiles, const int4* __restrict__ ptile,
+             const uint32_t* __restrict__ ploc, const float4* __restrict__ wab, const float2* __restrict__ tw) {
+  using RS = RdftPShape<NPHI>;
+  constexpr int T = FftPlan<NPHI, false>::T;
+  constexpr int KR = RS::KR, NTH = RS::NTH, NH = RS::NH, NFULL = RS::NFULL, SR = RS::SR;
+  constexpr int NC = RS::G * T;
+  static_assert(KR == 4 && NFULL * 256 + 1 == NH && NFULL < 32, "32-byte staging rows, full boxes + one tail row");
+  extern __shared__ __align__(128) float2 smem_k2p_raw[];
+  float2* smem_k2 = smem_k2p_raw + ((1024u - (smem_u32(smem_k2p_raw) & 1023u)) & 1023u) / sizeof(float2);
+  float* slot = reinterpret_cast<float*>(smem_k2);  // [2][SR][NTH]
+  float2* stg = smem_k2 + RS::IN;                   // [NH][4] in TMA's 32-byte swizzle (as K2)
+  float2* bufs = stg + RS::STG;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + RS::G * RS::BUF);  // full, consumed
+  uint64_t* full = &bars[0];
+  uint64_t* consumed = &bars[1];
+  if (threadIdx.x == 0) {
+    mbar_init(full, 1);
+    mbar_init(consumed, NC / 32);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int first = blockIdx.x, stride = gridDim.x;
+
+  if (threadIdx.x >= NC) {  // ---- producer warp (lane 0 issues)
+    if (threadIdx.x == NC) {
+      int it = 0;
+      for (int tile = first; tile < ntiles; tile += stride, ++it) {
+        if (it > 0) mbar_wait(consumed, (uint32_t)((it - 1) & 1));
+        const int b = tile / ntiles_per_slice, kb = tile - b * ntiles_per_slice;
+        const int4 td = __ldg(ptile + kb);
+        const float* base = g + (size_t)b * nt * NTH;
+        const uint32_t ba = (uint32_t)td.y * NTH * 4u, bb = (uint32_t)td.w * NTH * 4u;
+        fence_proxy_async_smem();  // the consumers' reads of the slot before these writes
+        mbar_arrive_expect_tx(full, ba + bb);
+        tma_bulk_g2s(slot, base + (size_t)td.x * NTH, ba, full);
+        tma_bulk_g2s(slot + SR * NTH, base + (size_t)td.z * NTH, bb, full);
+      }
+    }
+    return;
+  }
+
+  const int gi = threadIdx.x / T, ti = threadIdx.x % T;
+  float2* buf = bufs + gi * RS::BUF;
+  const GroupSync gsync{1 + gi, T};
+  const GroupSync csync{1 + RS::G, NC};
+  int it = 0;
+#pragma unroll 1
+  for (int tile = first; tile < ntiles; tile += stride, ++it) {
+    const int b = tile / ntiles_per_slice, k0 = (tile - b * ntiles_per_slice) * KR;
+    // this group's two rows: tap rows inside the slot and their weights
+    const int kx = k0 + 2 * gi;
+    const uint32_t lx = __ldg(ploc + kx), ly = __ldg(ploc + kx + 1);
+    const float4 wx = __ldg(wab + kx), wy = __ldg(wab + kx + 1);
+    const int xa0 = (int)(lx & 15u) * NTH, xa1 = (int)((lx >> 4) & 15u) * NTH;
+    const int xb0 = (int)((lx >> 8) & 15u) * NTH + SR * NTH, xb1 = (int)((lx >> 12) & 15u) * NTH + SR * NTH;
+    const int ya0 = (int)(ly & 15u) * NTH, ya1 = (int)((ly >> 4) & 15u) * NTH;
+    const int yb0 = (int)((ly >> 8) & 15u) * NTH + SR * NTH, yb1 = (int)((ly >> 12) & 15u) * NTH + SR * NTH;
+    mbar_wait(full, (uint32_t)(it & 1));
+    constexpr int R0 = FftPlan<NPHI, false>::radix(0), QS = NPHI / R0;
+    auto load = [&](int j, auto rc) -> float2 {
+      constexpr int r = decltype(rc)::value;
+      if constexpr (r < R0 / 2) {  // phi < pi: the t >= 0 taps
+        const float* c = slot + j + r * QS;
+        return make_float2(fmaf(wx.y, c[xa1], wx.x * c[xa0]), fmaf(wy.y, c[ya1], wy.x * c[ya0]));
+      } else {  // phi >= pi: the t <= 0 taps
+        const float* c = slot + j + (r - R0 / 2) * QS;
+        return make_float2(fmaf(wx.w, c[xb1], wx.z * c[xb0]), fmaf(wy.w, c[yb1], wy.z * c[yb0]));
+      }
+    };
+    auto store = [&](int idx, float2 v) { buf[pad16(idx)] = v; };
+    bool first_sync = true;
+    auto sync = [&]() {  // the first barrier follows pass 0's stores: this warp no longer reads the slot
+      if (first_sync) {
+        first_sync = false;
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(consumed);
+      }
+      gsync();
+    };
+    block_fft<NPHI, false, true, false, false, 16>(buf, ti, tw, load, store, sync);
+    if (threadIdx.x < 32) bulk_wait_group_read<0>();  // the previous tile's TMA stores have read stg
+    csync();
+    for (int m = ti; m < NH; m += T) {
+      const float2 z = buf[pad16(m)];
+      const float2 w = buf[pad16((NPHI - m) & (NPHI - 1))];
+      const int sw = ((m >> 2) & 1) << 1;
+      *reinterpret_cast<float4*>(stg + m * KR + ((2 * gi) ^ sw)) =
+          make_float4(0.5f * (z.x + w.x), 0.5f * (z.y - w.y), 0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+    }
+    csync();
+    if (threadIdx.x <= NFULL) {  // one TMA store box per lane of warp 0
+      const int bx = threadIdx.x;
+      fence_proxy_async_smem();
+      if (bx < NFULL) tma_store_2d(&pmap, 2 * k0, b * NH + bx * 256, stg + bx * 256 * KR);
+      else tma_store_2d(&ptail, 2 * k0, b * NH + NFULL * 256, stg + NFULL * 256 * KR);
+      bulk_commit_group();
+    }
+  }
+  if (threadIdx.x < 32) bulk_wait_group<0>();
+}
+
+// ---------------------------------------------------------------------------
 // K3: per phi-frequency column m (one CTA), for every slice of the batch:
 //   p[k]  = wa0 G[a_k] + wa1 G[a_k+1] + (-1)^m (wb0 G[b_k] + wb1 G[b_k+1])   (semi-polar, grids.py:290-311)
 //   x[i]  = w0 p[k_i] + w1 p[k_i+1], i < nrho, 0 for i >= nrho            (log-polar, grids.py:332-347)
@@ -324,19 +452,24 @@ k_row_rdft(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUt
 // its TMEM lane (tensor memory, otherwise idle here) for all slices of the chunk.
 // ---------------------------------------------------------------------------
 // 16384-point columns (nt >~ 2900): 512 threads and ~200 KB of shared memory, one CTA per SM
-template <int L, bool PRUNE, bool TM>
+// PIN: Gh is K2p's semi-polar row spectra P[b][m][ns] (gp = ns): the column is the p the first pass
+// interpolates from, landed by TMA in one of two buffers (the other one is refilled at the top of
+// the slice's iteration: its last readers were the previous slice's first pass).
+template <int L, bool PRUNE, bool TM, bool PIN = false>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, (L >= 16384 ? 1 : 2))
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int gp, int ns, int nrho, int row_lo,
            int nrho_pad, int nh, const uint2* __restrict__ abw,
            const uint32_t* __restrict__ kw, const float2* __restrict__ khat, const float2* __restrict__ tw) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bars[2];
+  uint64_t& bar = bars[0];
   __shared__ uint32_t tslot;
   float2* buf = smem_k3;                          // padded_len(L)
-  float2* p = buf + padded_len(L);                // ns
-  float2* gcol = p + ((ns + 1) & ~1);             // gp + 2 (16-B aligned); refilled as soon as the row mix is done
-  uint32_t* kws = reinterpret_cast<uint32_t*>(gcol + gp + 2);  // nrho packed log-polar taps, same for every column
+  float2* p = buf + padded_len(L);                // ns (PIN: two buffers of PS = ns + 2, the pad reads zero)
+  const int PS = (ns + 3) & ~1;
+  float2* gcol = PIN ? p : p + ((ns + 1) & ~1);   // gp + 2 (16-B aligned); refilled as soon as the row mix is done
+  uint32_t* kws = reinterpret_cast<uint32_t*>(PIN ? p + 2 * PS : gcol + gp + 2);  // nrho packed log-polar taps, same for every column
   const int m = blockIdx.x;
   const float sg = (m & 1) ? -1.f : 1.f;
   const int ti = threadIdx.x;
@@ -353,11 +486,12 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   constexpr bool TKW = TM && KWN <= 16;
   constexpr int WCOLS = 2 * E + 32;
   constexpr int TCOLS = pow2_at_least(WCOLS * (T >= 128 ? T / 128 : 1));
-  const bool tab = TM && ns <= 4 * T;  // row-mix taps from TMEM (uniform over the CTA)
+  const bool tab = TM && !PIN && ns <= 4 * T;  // row-mix taps from TMEM (uniform over the CTA)
   const int warp = ti >> 5;
   if (TM && warp == 0) tmem_alloc<TCOLS>(&tslot);
   if (ti == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
   tmem_fence_before();
@@ -412,11 +546,24 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   }
   if (!kw_bulk && !TKW)
     for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
-  if (ti < 2) gcol[gp + ti] = make_float2(0.f, 0.f);  // rows nt, nt+1 of the packed taps read zero (visible
-                                                       // after the first mbarrier wait's __syncthreads below)
+  if (PIN) {
+    if (ti < 4) p[(ti >> 1) * PS + ns + (ti & 1)] = make_float2(0.f, 0.f);  // p[ns], p[ns + 1] of both buffers
+  } else if (ti < 2) {
+    gcol[gp + ti] = make_float2(0.f, 0.f);  // rows nt, nt+1 of the packed taps read zero (visible
+  }                                          // after the first mbarrier wait's __syncthreads below)
   __syncthreads();
 
   for (int b = 0; b < batch; ++b) {
+    const float2* pc = p;
+    if constexpr (PIN) {
+      mbar_wait(&bars[b & 1], (uint32_t)((b >> 1) & 1));
+      pc = p + (b & 1) * PS;
+      if (ti == 0 && b + 1 < batch) {  // the other buffer's last readers: the previous slice's first pass
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[(b + 1) & 1], col_bytes);
+        tma_bulk_g2s(p + ((b + 1) & 1) * PS, Gh + ((size_t)(b + 1) * nh + m) * gp, col_bytes, &bars[(b + 1) & 1]);
+      }
+    } else {
     mbar_wait(&bar, b & 1);
     const float2* col = gcol;
     // p[k] = (1 - wa) G[a] + wa G[a+1] + (-1)^m ((1 - wb) G[b] + wb G[b+1]); taps for 4 rows in flight
@@ -457,6 +604,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       mbar_arrive_expect_tx(&bar, col_bytes);
       tma_bulk_g2s(gcol, Gh + ((size_t)(b + 1) * nh + m) * gp, col_bytes, &bar);
     }
+    }  // !PIN
     uint32_t kwr[16];
     auto load = [&](auto ec, int idx) -> float2 {
       constexpr int q = decltype(ec)::value;
@@ -469,7 +617,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       else e = kws[idx];
       const int k = (int)(e & 0x7FFu);
       const float w1 = (float)(e >> 11) * (1.f / 1048576.f);
-      const float2 p0 = p[k], p1 = p[k + 1];
+      const float2 p0 = pc[k], p1 = pc[k + 1];
       return make_float2(fmaf(w1, p1.x - p0.x, p0.x), fmaf(w1, p1.y - p0.y, p0.y));
     };
     float kr[32];
@@ -1417,11 +1565,33 @@ cudaError_t rdft_impl(const Dims& d, const DevTables& t, const float* g, float2*
   return cudaGetLastError();
 }
 
+template <int NPHI>
+cudaError_t rdft_p_impl(const Dims& d, const DevTables& t, const float* g, float2* Ph, int batch, cudaStream_t s) {
+  using RS = RdftPShape<NPHI>;
+  if (!d.pmix || d.ns % RS::KR || !t.ptile || !t.ploc) return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(Ph) & 15) || (reinterpret_cast<uintptr_t>(g) & 15)) return cudaErrorNotSupported;
+  auto k = k_row_rdft_p<NPHI>;
+  CUtensorMap pm, pt;
+  cudaError_t e = encode_rowspec_map(&pm, Ph, d.ns, RS::NH, batch, 256);
+  if (!e) e = encode_rowspec_map(&pt, Ph, d.ns, RS::NH, batch, 1);
+  if (e) return e;
+  e = prep(k, RS::SMEM);
+  if (e) return e;
+  const int per = d.ns / RS::KR, tiles = per * batch;
+  const int grid = tiles < d.nsm ? tiles : d.nsm;
+  k<<<grid, RS::G * FftPlan<NPHI, false>::T + 32, RS::SMEM, s>>>(pm, pt, g, d.nt, per, tiles,
+                                                                 reinterpret_cast<const int4*>(t.ptile), t.ploc,
+                                                                 t.wab, t.tw_phi);
+  return cudaGetLastError();
+}
+
 template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
-                      cudaStream_t s) {
-  const int gp = d.gp > 0 ? d.gp : d.nt;
-  const size_t smem = ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp + 2) * sizeof(float2) + (size_t)d.nrho * 4;
+                      cudaStream_t s, bool pin) {
+  const int gp = pin ? d.ns : (d.gp > 0 ? d.gp : d.nt);
+  const size_t smem = pin ? ((size_t)padded_len(L) + 2 * (size_t)((d.ns + 3) & ~1)) * sizeof(float2) + (size_t)d.nrho * 4
+                          : ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp + 2) * sizeof(float2) +
+                                (size_t)d.nrho * 4;
   // nrho <= L/2: the rho column is zero in the upper half and only rows < nrho are kept
   // Khat in TMEM where L is in [4096, 16384]: at most two 256-thread CTAs per SM (256 columns each) or
   // one 512-thread CTA (512 columns), so an allocation never waits; LPBP_K3_TMEM=0 selects the L2 path
@@ -1434,6 +1604,13 @@ cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float
   auto k = pr ? k_rho_conv<L, true, false> : k_rho_conv<L, false, false>;
   if constexpr (kTmemOk) {
     if (tmv) k = pr ? k_rho_conv<L, true, true> : k_rho_conv<L, false, true>;
+  }
+  if (pin) {  // K2p's semi-polar spectra (pruned transforms only: 2 nrho <= L holds for every automatic mesh)
+    if (!pr || (d.ns & 1)) return cudaErrorNotSupported;
+    k = k_rho_conv<L, true, false, true>;
+    if constexpr (kTmemOk) {
+      if (tmv) k = k_rho_conv<L, true, true, true>;
+    }
   }
   cudaError_t e = prep(k, smem);
   if (e) return e;
@@ -1483,15 +1660,24 @@ cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, f
     default: return cudaErrorNotSupported;
   }
 }
+cudaError_t launch_row_rdft_p(const Dims& d, const DevTables& t, const float* g, float2* Ph, int batch, cudaStream_t s) {
+  switch (d.nphi) {
+    case 512: return rdft_p_impl<512>(d, t, g, Ph, batch, s);
+    case 1024: return rdft_p_impl<1024>(d, t, g, Ph, batch, s);
+    case 2048: return rdft_p_impl<2048>(d, t, g, Ph, batch, s);
+    case 4096: return rdft_p_impl<4096>(d, t, g, Ph, batch, s);
+    default: return cudaErrorNotSupported;
+  }
+}
 cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool pin) {
   switch (d.L) {
-    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, row_lo, s);
-    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, row_lo, s);
-    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, row_lo, s);
-    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, row_lo, s);
-    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, row_lo, s);
-    case 16384: return conv_impl<16384>(d, t, Gh, Yh, batch, row_lo, s);
+    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, row_lo, s, pin);
+    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, row_lo, s, pin);
+    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, row_lo, s, pin);
+    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, row_lo, s, pin);
+    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, row_lo, s, pin);
+    case 16384: return conv_impl<16384>(d, t, Gh, Yh, batch, row_lo, s, pin);
     default: return cudaErrorNotSupported;
   }
 }

@@ -2,6 +2,7 @@
 // Layouts (all C-contiguous, fp32 / complex64 as float2):
 //   sinogram  g  [B][nt][ntheta]              (fastbp Sinogram.values, t outer)
 //   row spectra G [B][nh][nt]    nh = nphi/2+1 (phi-frequency major, t contiguous)
+//   semi-polar row spectra P [B][nh][ns]      (d.pmix plans: K2p's output instead of G)
 //   conv spectra Y [B][nh][nrho_pad]          (phi-frequency major, rho contiguous)
 //   log-polar  lp [B][nrho][nphi]             (fastbp LogPolarImage.values)
 //   image     img [B][n][n]                   (fastbp CartesianImage.values, y outer)
@@ -20,6 +21,8 @@ struct DevTables {
   const int2* ab;         // [ns] t-rows (a_k, b_k) of the semi-polar lerp
   const float4* wab;      // [ns] weights (wa0, wa1, wb0, wb1)
   const uint2* abw;       // [ns] packed (a | w1a << 13, b | w1b << 13), plan_host abw
+  const int32_t* ptile;   // [ns] K2p tiles: {a_lo, na, b_lo, nb} per 4 semi-polar rows (plan_host ptile)
+  const uint32_t* ploc;   // [ns] K2p tap rows inside the tile's ranges (plan_host ploc)
   const int* ki;          // [nrho] s-row of the log-polar lerp
   const float2* wi;       // [nrho] weights (w0, w1)
   const uint32_t* kw;     // [nrho] packed ki | w1 * 2^20 << 11 (K3 stages it in shared memory)
@@ -51,15 +54,18 @@ struct Dims {
                                    // win_lo leading columns + the row's last win - win_lo columns
   float out_scale;        // 1 (backprojection) or 1/(2 pi) (fbp)
   int npairs;             // > 0: the generic inverse DFT runs over t.pairs only (0 = every row pair)
+  int pmix;               // 1: K2p emits the semi-polar row spectra P[b][m][ns] and K3 takes them as they are
 };
 
 // Each returns cudaGetLastError() after the launch (0 on success) or
 // cudaErrorNotSupported when no instantiation exists for the size.
 cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s);
 cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* G, int batch, cudaStream_t s);
-// rows < row_lo of Y are not written (0 = all rows)
+// semi-polar row spectra P[b][nh][ns] (d.pmix plans; cudaErrorNotSupported otherwise)
+cudaError_t launch_row_rdft_p(const Dims& d, const DevTables& t, const float* g, float2* P, int batch, cudaStream_t s);
+// rows < row_lo of Y are not written (0 = all rows); pin: the input is K2p's P[b][nh][ns] (no row mix)
 cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, int row_lo,
-                            cudaStream_t s);
+                            cudaStream_t s, bool pin = false);
 cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch, cudaStream_t s);
 // counter: one device int of workspace (zeroed by the launcher on s)
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Y, float* img, int batch,

@@ -314,6 +314,47 @@ std::string build_host_plan(const HostPlanParams& p, HostPlan& h) {
       h.abw[2 * (size_t)k + side] = (uint32_t)fl | ((uint32_t)wq << 13);
     }
   }
+  // --- K2p tiles: 4 semi-polar rows, the sinogram rows their non-zero taps touch on each side
+  h.pmix = 0;
+  h.ptile.clear();
+  h.ploc.clear();
+  if (ns % 4 == 0) {
+    constexpr int kSide = 5;  // rows per side a K2p input slot holds
+    bool ok = true;
+    h.ptile.assign((size_t)ns, 0);
+    h.ploc.assign((size_t)ns, 0u);
+    for (int k0 = 0; k0 < ns && ok; k0 += 4) {
+      int lo[2] = {nt, nt}, hi[2] = {-1, -1};
+      for (int k = k0; k < k0 + 4; ++k) {
+        const int base[2] = {h.ab[k].x, h.ab[k].y};
+        const float w[4] = {h.wab[k].x, h.wab[k].y, h.wab[k].z, h.wab[k].w};
+        for (int side = 0; side < 2; ++side)
+          for (int j = 0; j < 2; ++j)
+            if (w[2 * side + j] != 0.f) {
+              lo[side] = std::min(lo[side], base[side] + j);
+              hi[side] = std::max(hi[side], base[side] + j);
+            }
+      }
+      for (int side = 0; side < 2; ++side) {
+        if (hi[side] < 0) lo[side] = hi[side] = 0;  // no tap on this side: one (unused) row
+        if (hi[side] - lo[side] + 1 > kSide || lo[side] < 0 || hi[side] >= nt) ok = false;
+        h.ptile[(size_t)k0 + 2 * side] = lo[side];
+        h.ptile[(size_t)k0 + 2 * side + 1] = hi[side] - lo[side] + 1;
+      }
+      for (int k = k0; k < k0 + 4 && ok; ++k) {
+        const int base[2] = {h.ab[k].x, h.ab[k].y};
+        const float w[4] = {h.wab[k].x, h.wab[k].y, h.wab[k].z, h.wab[k].w};
+        uint32_t loc = 0;
+        for (int side = 0; side < 2; ++side)
+          for (int j = 0; j < 2; ++j) {
+            const int l = w[2 * side + j] != 0.f ? base[side] + j - lo[side] : 0;
+            loc |= (uint32_t)l << (4 * (2 * side + j));
+          }
+        h.ploc[k] = loc;
+      }
+    }
+    h.pmix = ok ? 1 : 0;
+  }
   // --- log-polar taps (grids.py:332-347): rho_i = rho0 + (i+1) drho, f = e^rho (ns-1)
   h.ki.resize(nrho);
   h.wi.resize(nrho);

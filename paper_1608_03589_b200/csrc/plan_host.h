@@ -35,6 +35,14 @@ struct HostPlan {
   std::vector<I2> ab;
   std::vector<F4> wab;
   std::vector<uint32_t> abw;  // [2 ns] packed semi-polar taps for K3: a | w1a << 13, b | w1b << 13 (rows past nt read zero)
+  // K2p (row DFT of the semi-polar rows, grids.py:290-311 before logpolar.py:112): tiles of 4 semi-polar
+  // rows; ptile[4 j] = {a_lo, na, b_lo, nb}: the sinogram rows [a_lo, a_lo + na) hold every non-zero
+  // t >= 0 tap of rows 4j .. 4j+3 and [b_lo, b_lo + nb) every t <= 0 tap (na, nb <= 5), ploc[k] = the
+  // taps' rows inside those ranges (la0 | la1 << 4 | lb0 << 8 | lb1 << 12; zero-weight taps point at
+  // row 0 of the range), weights = wab[k].  pmix = 1 when every tile fits (ns % 4 == 0 too).
+  int pmix = 0;
+  std::vector<int32_t> ptile;
+  std::vector<uint32_t> ploc;
   std::vector<int32_t> ki;
   std::vector<uint32_t> kw;  // [nrho] packed log-polar tap: ki | round(w1 * 2^20) << 11 (w0 = 1 - w1)
   std::vector<uint32_t> qidx;

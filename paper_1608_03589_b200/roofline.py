@@ -12,13 +12,15 @@ SURVEY_BYTES_PER_SLICE = {(256, False): 3.014e6, (512, True): 15.252e6, (2048, F
 
 
 def algorithmic_bytes(plan) -> dict:
-    """{stage: {"per_slice": bytes, "per_launch": bytes}} for a LogPolarPlan."""
+    """{stage: {"per_slice": bytes, "per_launch": bytes}} for a LogPolarPlan: this decomposition's own
+    compulsory traffic.  `p_rows` plans (K2p): the row-DFT stage writes and the rho stage reads the
+    ns = nt/2 semi-polar row spectra instead of nt row spectra."""
     i = plan.info
     nt, nth, n = i["nt"], i["ntheta"], i["n_out"]
     nphi, nrho, L = i["nphi"], i["nrho"], i["L"]
     nh = nphi // 2 + 1
     sino = nt * nth * 4
-    G = nh * nt * 8
+    G = nh * (i["ns"] if i.get("p_rows") else nt) * 8
     Y = nh * nrho * 8
     lp = nrho * nphi * 4
     img = n * n * 4
@@ -30,6 +32,29 @@ def algorithmic_bytes(plan) -> dict:
         "readout": {"per_slice": i["readout_sector_bytes"] + img, "per_launch": 0},
         # fused inverse DFT + readout: spectra in, image out (log-polar rows stay on chip)
         "irdft_readout": {"per_slice": Y + img, "per_launch": 0},
+    }
+
+
+def survey_stage_bytes(plan) -> dict:
+    """SURVEY §8(d)'s per-slice figures, stage by stage, attached to the kernel that does the stage's
+    arithmetic (their sum is §8(d)'s per-slice total, 279.258 MB for a 2048^2 FBP slice):
+      S1 ramp = 2 nt ntheta 4                     -> ramp_filter
+      S2 resample = nt ntheta 4 + nrho nphi 4      -> row_rdft  (the sinogram read; the log-polar image
+                                                     S2 writes never exists here: K3 interpolates it on chip)
+      S3 FFT convolution = 2 nrho nphi 4 (+ K-hat once per launch) -> rho_conv
+      S4 readout = distinct 32-byte sectors + n^2 4 -> irdft_readout
+    This is the basis the task's `roofline.achieved` is defined on; `algorithmic_bytes` is what this
+    decomposition itself has to move (less for K3, more for K45, which also reads the spectra)."""
+    i = plan.info
+    nt, nth, n = i["nt"], i["ntheta"], i["n_out"]
+    nphi, nrho, L = i["nphi"], i["nrho"], i["L"]
+    nh = nphi // 2 + 1
+    sino, lp, img = nt * nth * 4, nrho * nphi * 4, n * n * 4
+    return {
+        "ramp_filter": {"stage": "S1", "per_slice": 2 * sino, "per_launch": 0},
+        "row_rdft": {"stage": "S2", "per_slice": sino + lp, "per_launch": 0},
+        "rho_conv": {"stage": "S3", "per_slice": 2 * lp, "per_launch": nh * L * 8},
+        "irdft_readout": {"stage": "S4", "per_slice": i["readout_sector_bytes"] + img, "per_launch": 0},
     }
 
 
@@ -70,7 +95,7 @@ def nominal_flops(plan) -> dict:
     f = lambda n: 5.0 * n * math.log2(n)  # noqa: E731
     return {
         "ramp_filter": (i["ntheta"] / 2) * (2 * f(M) + 6 * M) if M else 0.0,  # packed column pairs
-        "row_rdft": (nt / 2) * f(nphi),                                        # packed row pairs
+        "row_rdft": ((i["ns"] if i.get("p_rows") else nt) / 2) * f(nphi),      # packed row pairs
         "rho_conv": nh * (2 * f(L) + 6 * L),
         "irdft_readout": (nrho / 2) * f(nphi),
     }

@@ -455,3 +455,34 @@ def test_mixed_radix_row_dft_lengths(nth, q):
     hp = HostPlan(64, nth, 64)
     assert hp.info.phi_q == q
     assert hp.info.generic == (0 if nth == 2048 else 1)
+
+
+@pytest.mark.parametrize("nt,nth,n", [(256, 256, 256), (512, 512, 512), (2048, 2048, 2048), (64, 256, 64), (1024, 512, 300)])
+def test_k2p_tile_tables_reproduce_the_semipolar_image(nt, nth, n):
+    """K2p forms the semi-polar rows (grids.py:290-311) from two runs of <= 5 sinogram rows per tile of
+    4 rows: the host tables (ptile, ploc, wab) applied in numpy give the oracle's semipolar()."""
+    hp = HostPlan(nt, nth, n)
+    ns = nt // 2
+    assert hp.info.p_rows == 1
+    ptile = hp.table("ptile", np.int32).reshape(-1, 4)
+    ploc = hp.table("ploc", np.uint32)
+    wab = hp.table("wab", np.float32, 4).astype(np.float64)
+    assert ptile.shape[0] == ns // 4 and ploc.shape[0] == ns
+    rng = np.random.default_rng(nt + n)
+    g = rng.standard_normal((nt, nth))
+    p = np.zeros((ns, 2 * nth))
+    for j in range(ns // 4):
+        a_lo, na, b_lo, nb = (int(v) for v in ptile[j])
+        assert 1 <= na <= 5 and 1 <= nb <= 5 and 0 <= a_lo and a_lo + na <= nt and 0 <= b_lo and b_lo + nb <= nt
+        A, B = g[a_lo:a_lo + na], g[b_lo:b_lo + nb]      # the two TMA bulk copies
+        for k in range(4 * j, 4 * j + 4):
+            l = [(int(ploc[k]) >> s) & 15 for s in (0, 4, 8, 12)]
+            assert l[0] < na and l[1] < na and l[2] < nb and l[3] < nb
+            p[k, :nth] = wab[k, 0] * A[l[0]] + wab[k, 1] * A[l[1]]
+            p[k, nth:] = wab[k, 2] * B[l[2]] + wab[k, 3] * B[l[3]]
+    ref = O.semipolar(g)
+    assert np.abs(p - ref).max() <= 2e-7 * np.abs(ref).max()
+
+
+def test_k2p_needs_four_row_tiles():
+    assert HostPlan(260, 256, 128).info.p_rows == 0   # ns = 130: K2's row spectra + K3's row mix

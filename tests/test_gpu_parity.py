@@ -459,6 +459,51 @@ def test_rho_conv_tmem_operands_bitwise(tmp_path):
     assert np.array_equal(outs[0], outs[1])
 
 
+_K2P_AB = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1608_03589_b200 as p
+from oracle import phantoms
+out = {}
+g = torch.stack([torch.from_numpy(phantoms.config_sinogram(3, i)) for i in (0, 7, 9)]).cuda()
+plan = p.get_plan(2048, 2048, 2048, None, None, (0.0, 1.0))
+out["p_rows_2048"] = np.int32(plan.info["p_rows"])
+out["fbp2048"] = plan.execute(g, chunk=2).cpu().numpy()
+out["lp2048"] = plan.logpolar(g[:1]).cpu().numpy()
+g = torch.stack([torch.from_numpy(phantoms.config_sinogram(1, i)) for i in range(5)]).cuda()
+out["fbp512"] = p.get_plan(512, 512, 512, None, None, (0.0, 1.0)).execute(g, chunk=3).cpu().numpy()
+g = torch.from_numpy(phantoms.config_sinogram(0, 0))[None].cuda()
+out["bp256"] = p.get_plan(256, 256, 256, None, None, None).execute(g).cpu().numpy()
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_k2p_matches_frequency_domain_row_mix(tmp_path):
+    """Default: K2p transforms the semi-polar rows and K3 takes their spectra as they are (p_rows = 1).
+    LPBP_K2P=0: K2's nt row spectra and K3's frequency-domain row mix.  The two orders of the same
+    linear maps agree to fp32 rounding at 256^2, 512^2 and 2048^2 (images and the log-polar stage);
+    each run in its own process (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("1", "0"):
+        f = str(tmp_path / f"k2p_{v}.npz")
+        env = dict(os.environ, LPBP_K2P=v)
+        r = subprocess.run([sys.executable, "-c", _K2P_AB, repo, f], env=env, capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert int(outs[0]["p_rows_2048"]) == 1 and int(outs[1]["p_rows_2048"]) == 0
+    for k in ("fbp2048", "lp2048", "fbp512", "bp256"):
+        a, b = outs[0][k], outs[1][k]
+        assert np.isfinite(a).all() and np.abs(a).max() > 0
+        e = O.relative_l2(a, b)
+        print(f"K2p vs row-mix path {k}: {e:.3e}")
+        assert e <= 3e-6
+
+
 @pytest.mark.parametrize("nth", [768, 1280, 1536, 2304, 2560, 3200, 3840])
 def test_mixed_radix_row_dfts_vs_oracle(pkg, nth):
     """Angle counts whose nphi = 2 ntheta is Q x 2^k (Q = 3, 5, 9, 15, 25) take the mixed-radix
