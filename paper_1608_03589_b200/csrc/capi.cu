@@ -239,9 +239,11 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   });
   if (e) return launch_fail(e, "row_rdft");
   ++g_launches;
-  e = staged(P, 2, c, s, [&] {  // rows below the first tapped one (pair) are never read downstream
+  const bool unfused = stop_after_lp || (gen && !lpbp::fused_mixed_available(d));
+  e = staged(P, 2, c, s, [&] {  // rows below the first tapped one (pair) are never read downstream; ahead of the
+                                // fused inverse DFT + readout only the rows of the bands it loads are written
     return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c,
-                                 stop_after_lp ? 0 : d.row_min, s, pin);
+                                 stop_after_lp ? 0 : d.row_min, s, pin, !unfused && P->t.row_need != nullptr);
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
@@ -379,6 +381,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
       rc = rc ? rc : P->upload(P->h.band_packed, &P->t.band_entries);
       rc = rc ? rc : P->upload(P->h.band_need, &P->t.band_need);
       rc = rc ? rc : P->upload(P->h.units, &P->t.units);
+      rc = rc ? rc : P->upload(P->h.row_need, &P->t.row_need);
       rc = rc ? rc : P->upload(P->h.pair_list, &P->t.pairs);
     }
     if (rc) {
@@ -651,6 +654,7 @@ int lpbp_plan_table(const lpbp_plan* P, const char* which, void* dst, size_t cap
   if (!std::strcmp(which, "band_entries")) return copy_vec(h.band_entries);  // uint32
   if (!std::strcmp(which, "band_need")) return copy_vec(h.band_need);        // uint32 nbands
   if (!std::strcmp(which, "units")) return copy_vec(h.units);                // uint32 pairs [k0, k1), outermost first
+  if (!std::strcmp(which, "row_need")) return copy_vec(h.row_need);          // uint32 bitmap over log-polar rows
   return fail(LPBP_EINVAL, std::string("unknown table ") + which);
 }
 

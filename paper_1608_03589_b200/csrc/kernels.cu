@@ -459,7 +459,8 @@ template <int L, bool PRUNE, bool TM, bool PIN = false>
 __global__ void __launch_bounds__(FftPlan<L, false>::T, (L >= 16384 ? 1 : 2))
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int gp, int ns, int nrho, int row_lo,
            int nrho_pad, int nh, const uint2* __restrict__ abw,
-           const uint32_t* __restrict__ kw, const float2* __restrict__ khat, const float2* __restrict__ tw) {
+           const uint32_t* __restrict__ kw, const float2* __restrict__ khat, const float2* __restrict__ tw,
+           const uint32_t* __restrict__ row_need) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
   __shared__ __align__(8) uint64_t bars[2];
@@ -484,6 +485,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   constexpr int E = FftPlan<L, false>::E;
   constexpr int R0 = FftPlan<L, false>::radix(0), RL0 = PRUNE ? R0 / 2 : R0, KWN = (E / R0) * RL0;
   constexpr bool TKW = TM && KWN <= 16;
+  constexpr bool TKF = TKW && PIN;  // taps kept unpacked (row, fp32 weight) in the 32 columns the row-mix taps left free
   constexpr int WCOLS = 2 * E + 32;
   constexpr int TCOLS = pow2_at_least(WCOLS * (T >= 128 ? T / 128 : 1));
   const bool tab = TM && !PIN && ns <= 4 * T;  // row-mix taps from TMEM (uniform over the CTA)
@@ -527,7 +529,20 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
         const int idx = ti + (q / RL0) * T + (q % RL0) * (L / R0);
         t[q] = (q < KWN && idx < nrho) ? __ldg(kw + idx) : 0u;
       }
-      tmem_st16(kt + 2 * E, t);
+      if constexpr (TKF) {  // (row, w1 as fp32: the 20-bit fixed-point weight x 2^-20 is exact) pairs
+        uint32_t u[16];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            u[2 * q] = t[8 * h + q] & 0x7FFu;
+            u[2 * q + 1] = __float_as_uint((float)(t[8 * h + q] >> 11) * (1.f / 1048576.f));
+          }
+          tmem_st16(kt + 2 * E + 16 * h, u);
+        }
+      } else {
+        tmem_st16(kt + 2 * E, t);
+      }
     }
     if (tab) {  // row-mix rows ti + u T
       uint32_t t[16];
@@ -543,6 +558,19 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       tmem_st16(kt + 2 * E + 16, t);
     }
     tmem_wait_st();
+  }
+  // the thread's output rows are the same for every slice: one bit per store of the last inverse pass
+  // (row < nrho, >= row_lo and, with row_need, in a band the fused readout loads; the others are never read)
+  constexpr int RLS = FftPlan<L, true>::radix(FftPlan<L, true>::P - 1), NSL = FftPlan<L, true>::ns(FftPlan<L, true>::P - 1);
+  constexpr int ROS = PRUNE ? RLS / 2 : RLS, NST = (E / RLS) * ROS;
+  static_assert(NST <= 32, "one mask bit per store");
+  uint32_t smask = 0;
+#pragma unroll
+  for (int q = 0; q < NST; ++q) {
+    const int idx = ti + (q / ROS) * T + (q % ROS) * NSL;
+    bool on = idx < nrho && idx >= row_lo;
+    if (on && row_need) on = (__ldg(row_need + (idx >> 5)) >> (idx & 31)) & 1u;
+    smask |= on ? 1u << q : 0u;
   }
   if (!kw_bulk && !TKW)
     for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
@@ -606,17 +634,28 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     }
     }  // !PIN
     uint32_t kwr[16];
+    float kwf[32];
     auto load = [&](auto ec, int idx) -> float2 {
       constexpr int q = decltype(ec)::value;
       (void)q;
-      if constexpr (TKW)
+      if constexpr (TKF) {
+        if constexpr (q == 0) tmem_ld32(kt + 2 * E, kwf);
+      } else if constexpr (TKW) {
         if constexpr (q == 0) tmem_ld16(kt + 2 * E, kwr);
+      }
       if (idx >= nrho) return make_float2(0.f, 0.f);
-      uint32_t e;
-      if constexpr (TKW) e = kwr[q];
-      else e = kws[idx];
-      const int k = (int)(e & 0x7FFu);
-      const float w1 = (float)(e >> 11) * (1.f / 1048576.f);
+      int k;
+      float w1;
+      if constexpr (TKF) {
+        k = __float_as_int(kwf[2 * q]);
+        w1 = kwf[2 * q + 1];
+      } else {
+        uint32_t e;
+        if constexpr (TKW) e = kwr[q];
+        else e = kws[idx];
+        k = (int)(e & 0x7FFu);
+        w1 = (float)(e >> 11) * (1.f / 1048576.f);
+      }
       const float2 p0 = pc[k], p1 = pc[k + 1];
       return make_float2(fmaf(w1, p1.x - p0.x, p0.x), fmaf(w1, p1.y - p0.y, p0.y));
     };
@@ -632,8 +671,10 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
       }
     };
     float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
-    auto store = [&](int idx, float2 v) {  // rows below row_lo are never read downstream
-      if (idx < nrho && idx >= row_lo) ycol[idx] = v;
+    int sq = 0;  // position among the thread's stores (block_conv's last pass is fully unrolled)
+    auto store = [&](int idx, float2 v) {  // rows below row_lo / outside the readout's bands are never read downstream
+      if ((smask >> sq) & 1u) ycol[idx] = v;
+      ++sq;
     };
     if (ti < nrho_pad - nrho) ycol[nrho + ti] = make_float2(0.f, 0.f);  // padding rows read as zero (K45)
     block_conv<L, PRUNE, 16>(buf, ti, tw, load, mul, store, block_sync);  // SFU twiddles for every pass
@@ -1587,7 +1628,7 @@ cudaError_t rdft_p_impl(const Dims& d, const DevTables& t, const float* g, float
 
 template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
-                      cudaStream_t s, bool pin) {
+                      cudaStream_t s, bool pin, const uint32_t* row_need) {
   const int gp = pin ? d.ns : (d.gp > 0 ? d.gp : d.nt);
   const size_t smem = pin ? ((size_t)padded_len(L) + 2 * (size_t)((d.ns + 3) & ~1)) * sizeof(float2) + (size_t)d.nrho * 4
                           : ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp + 2) * sizeof(float2) +
@@ -1615,7 +1656,7 @@ cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float
   cudaError_t e = prep(k, smem);
   if (e) return e;
   k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, gp, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.abw,
-                                              t.kw, t.khat, t.tw_rho);
+                                              t.kw, t.khat, t.tw_rho, row_need);
   return cudaGetLastError();
 }
 
@@ -1670,14 +1711,15 @@ cudaError_t launch_row_rdft_p(const Dims& d, const DevTables& t, const float* g,
   }
 }
 cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
-                            cudaStream_t s, bool pin) {
+                            cudaStream_t s, bool pin, bool fused_rows) {
+  const uint32_t* row_need = fused_rows ? t.row_need : nullptr;
   switch (d.L) {
-    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, row_lo, s, pin);
-    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, row_lo, s, pin);
-    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, row_lo, s, pin);
-    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, row_lo, s, pin);
-    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, row_lo, s, pin);
-    case 16384: return conv_impl<16384>(d, t, Gh, Yh, batch, row_lo, s, pin);
+    case 512: return conv_impl<512>(d, t, Gh, Yh, batch, row_lo, s, pin, row_need);
+    case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, row_lo, s, pin, row_need);
+    case 2048: return conv_impl<2048>(d, t, Gh, Yh, batch, row_lo, s, pin, row_need);
+    case 4096: return conv_impl<4096>(d, t, Gh, Yh, batch, row_lo, s, pin, row_need);
+    case 8192: return conv_impl<8192>(d, t, Gh, Yh, batch, row_lo, s, pin, row_need);
+    case 16384: return conv_impl<16384>(d, t, Gh, Yh, batch, row_lo, s, pin, row_need);
     default: return cudaErrorNotSupported;
   }
 }

@@ -34,6 +34,7 @@ struct DevTables {
   const uint32_t* band_entries;  // per band: uint4 {qq | bit31 zero, qidx, wi, wj} (plan_host band_packed)
   const uint32_t* band_need;     // [nbands] 1 = some pixel taps one of the band's rows
   const uint32_t* units;         // [nunits][2] fused work units: band range [k0, k1), outermost first
+  const uint32_t* row_need;      // bitmap over log-polar rows: 1 = the row lies in a band the fused readout loads
   // generic sizes (Bluestein)
   const float2* chirp;   // [nphi]
   const float2* bhat_f;  // [MB]
@@ -64,8 +65,9 @@ cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, f
 // semi-polar row spectra P[b][nh][ns] (d.pmix plans; cudaErrorNotSupported otherwise)
 cudaError_t launch_row_rdft_p(const Dims& d, const DevTables& t, const float* g, float2* P, int batch, cudaStream_t s);
 // rows < row_lo of Y are not written (0 = all rows); pin: the input is K2p's P[b][nh][ns] (no row mix)
+// fused_rows: only the rows of bands the fused inverse DFT + readout loads are written (t.row_need)
 cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, int row_lo,
-                            cudaStream_t s, bool pin = false);
+                            cudaStream_t s, bool pin = false, bool fused_rows = false);
 cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch, cudaStream_t s);
 // counter: one device int of workspace (zeroed by the launcher on s)
 cudaError_t launch_irdft_readout(const Dims& d, const DevTables& t, const float2* Y, float* img, int batch,

@@ -167,6 +167,11 @@ void build_bands(HostPlan& h, int band_rows) {
       h.units[2 * u + 1] = us[u].second;
     }
   }
+  h.row_need.assign(((size_t)h.nrho_pad + 31) / 32 + 1, 0u);
+  for (int b = 0; b < h.nbands; ++b)
+    if (h.band_need[b])
+      for (int r = rmin + band_rows * b; r < rmin + band_rows * (b + 1) && r < h.nrho_pad; ++r)
+        h.row_need[(size_t)r >> 5] |= 1u << (r & 31);
   h.band_packed.resize(h.band_entries.size() * 4);
   for (size_t e = 0; e < h.band_entries.size(); ++e) {
     const uint32_t ent = h.band_entries[e];

@@ -60,6 +60,10 @@ struct HostPlan {
   // kMaxUnitBands bands per unit
   std::vector<uint32_t> units;
   int nunits = 0;
+  // bitmap over the log-polar rows [0, nrho_pad): 1 = the row belongs to a needed band (the fused kernel
+  // loads and transforms whole bands, so every row of a needed band must hold K3's output); K3 writes
+  // these rows only
+  std::vector<uint32_t> row_need;
   // self-contained 16-byte entries {qy | qx << 15 | zero flag << 31, qidx, wi bits, wj bits}
   std::vector<uint32_t> band_packed;
   // generic sizes (nphi not a power of two in [512, 4096], ...): Bluestein DFTs of

@@ -241,6 +241,8 @@ class LogPolarPlan:
             a = np.empty(n.value, dtype=np.float32)
         elif which == "khat":
             a = np.empty(n.value, dtype=np.complex64)
+        elif which in ("row_need", "ploc", "band_need"):
+            a = np.empty(n.value, dtype=np.uint32)
         else:
             raise ValueError(which)
         check(lib().lpbp_plan_table(self._h, which.encode(), c_void_p(a.ctypes.data), n.value, byref(n)))

@@ -24,14 +24,23 @@ def algorithmic_bytes(plan) -> dict:
     Y = nh * nrho * 8
     lp = nrho * nphi * 4
     img = n * n * 4
+    # ahead of the fused inverse DFT + readout K3 writes, and K45 reads, only the rows of the bands some
+    # pixel taps (plan table row_need; about two thirds of the rows at 2048^2)
+    Yf = Y
+    if i.get("band_rows", 0) > 0 and hasattr(plan, "table"):
+        try:
+            bits = plan.table("row_need")
+            Yf = nh * 8 * int(sum(bin(int(w)).count("1") for w in bits))
+        except Exception:
+            Yf = Y
     return {
         "ramp_filter": {"per_slice": 2 * sino, "per_launch": 0},
         "row_rdft": {"per_slice": sino + G, "per_launch": 0},
-        "rho_conv": {"per_slice": G + Y, "per_launch": nh * L * 8},  # kernel spectrum once per launch
+        "rho_conv": {"per_slice": G + Yf, "per_launch": nh * L * 8},  # kernel spectrum once per launch
         "row_irdft": {"per_slice": Y + lp, "per_launch": 0},
         "readout": {"per_slice": i["readout_sector_bytes"] + img, "per_launch": 0},
         # fused inverse DFT + readout: spectra in, image out (log-polar rows stay on chip)
-        "irdft_readout": {"per_slice": Y + img, "per_launch": 0},
+        "irdft_readout": {"per_slice": Yf + img, "per_launch": 0},
     }
 
 

@@ -9,7 +9,7 @@ CMD="python bench.py --steps 2 --warmup 3 --slices 128 --no-cpu-baseline --e2e-s
 $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD \
     > gpurun_out/ncu_launches_${TAG}.log 2>&1
-CMD2="python scripts/time_stages.py --n 2048 --batch 32 --reps 1"  # 32-slice launches: the bench chunk
+CMD2="python scripts/time_stages.py --n 2048 --batch 128 --reps 1"  # 128-slice launches: the bench chunk
 $CMD2 > gpurun_out/plain2_${TAG}.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"k_ramp|k_row_rdft|k_rho_conv|k_irdft_readout" \
     -s 4 -c 4 -o gpurun_out/full_${TAG} $CMD2 > gpurun_out/ncu_full_${TAG}.log 2>&1
