@@ -243,7 +243,7 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
   e = staged(P, 2, c, s, [&] {  // rows below the first tapped one (pair) are never read downstream; ahead of the
                                 // fused inverse DFT + readout only the rows of the bands it loads are written
     return lpbp::launch_rho_conv(d, P->t, reinterpret_cast<const float2*>(B), reinterpret_cast<float2*>(A), c,
-                                 stop_after_lp ? 0 : d.row_min, s, pin, !unfused && P->t.row_need != nullptr);
+                                 stop_after_lp ? 0 : d.row_min, s, pin, !unfused && P->t.rowmap_id != nullptr);
   });
   if (e) return launch_fail(e, "rho_conv");
   ++g_launches;
@@ -381,7 +381,10 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
       rc = rc ? rc : P->upload(P->h.band_packed, &P->t.band_entries);
       rc = rc ? rc : P->upload(P->h.band_need, &P->t.band_need);
       rc = rc ? rc : P->upload(P->h.units, &P->t.units);
-      rc = rc ? rc : P->upload(P->h.row_need, &P->t.row_need);
+      rc = rc ? rc : P->upload(P->h.rowmap_cp, &P->t.rowmap_cp);
+      rc = rc ? rc : P->upload(P->h.rowmap_id, &P->t.rowmap_id);
+      rc = rc ? rc : P->upload(P->h.band_row_cp, &P->t.band_row_cp);
+      rc = rc ? rc : P->upload(P->h.band_row_id, &P->t.band_row_id);
       rc = rc ? rc : P->upload(P->h.pair_list, &P->t.pairs);
     }
     if (rc) {
@@ -418,6 +421,13 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     return v ? atoi(v) != 0 : true;
   }();
   d.pmix = (h.pmix && !h.generic && k2p && 2 * h.nrho <= h.L) ? 1 : 0;
+  // the fused path's Y columns hold the needed bands back to back; LPBP_YCOMPACT=0 leaves every row in place
+  static const bool ycp = [] {
+    const char* v = getenv("LPBP_YCOMPACT");
+    return v ? atoi(v) != 0 : true;
+  }();
+  d.ycompact = ycp ? 1 : 0;
+  d.row_end = P->h.row_end;
   d.nsm = 148;
   if (P->device >= 0) cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, P->device);
   const size_t fg = h.filter ? (size_t)h.nt * h.ntheta * sizeof(float) : 0;
@@ -655,6 +665,10 @@ int lpbp_plan_table(const lpbp_plan* P, const char* which, void* dst, size_t cap
   if (!std::strcmp(which, "band_need")) return copy_vec(h.band_need);        // uint32 nbands
   if (!std::strcmp(which, "units")) return copy_vec(h.units);                // uint32 pairs [k0, k1), outermost first
   if (!std::strcmp(which, "row_need")) return copy_vec(h.row_need);          // uint32 bitmap over log-polar rows
+  if (!std::strcmp(which, "rowmap_cp")) return copy_vec(h.rowmap_cp);        // int32 [row_end]: compacted position or -1
+  if (!std::strcmp(which, "rowmap_id")) return copy_vec(h.rowmap_id);        // int32 [row_end]: the row itself or -1
+  if (!std::strcmp(which, "band_row_cp")) return copy_vec(h.band_row_cp);    // uint32 [nbands]: 1 + compacted first row, 0 = unneeded
+  if (!std::strcmp(which, "band_row_id")) return copy_vec(h.band_row_id);    // uint32 [nbands]: 1 + first row, 0 = unneeded
   return fail(LPBP_EINVAL, std::string("unknown table ") + which);
 }
 

@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(FftPlan<L, false>::T, (L >= 16384 ? 1 : 2))
 k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, int nt, int gp, int ns, int nrho, int row_lo,
            int nrho_pad, int nh, const uint2* __restrict__ abw,
            const uint32_t* __restrict__ kw, const float2* __restrict__ khat, const float2* __restrict__ tw,
-           const uint32_t* __restrict__ row_need) {
+           const int32_t* __restrict__ rowmap, int zend) {
   constexpr int T = FftPlan<L, false>::T;
   extern __shared__ __align__(16) float2 smem_k3[];
   __shared__ __align__(8) uint64_t bars[2];
@@ -486,7 +486,7 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
   constexpr int R0 = FftPlan<L, false>::radix(0), RL0 = PRUNE ? R0 / 2 : R0, KWN = (E / R0) * RL0;
   constexpr bool TKW = TM && KWN <= 16;
   constexpr bool TKF = TKW && PIN;  // taps kept unpacked (row, fp32 weight) in the 32 columns the row-mix taps left free
-  constexpr int WCOLS = 2 * E + 32;
+  constexpr int WCOLS = 2 * E + 48;  // K-hat | first-pass taps | row-mix taps (or the taps' weights) | store rows
   constexpr int TCOLS = pow2_at_least(WCOLS * (T >= 128 ? T / 128 : 1));
   const bool tab = TM && !PIN && ns <= 4 * T;  // row-mix taps from TMEM (uniform over the CTA)
   const int warp = ti >> 5;
@@ -559,18 +559,30 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     }
     tmem_wait_st();
   }
-  // the thread's output rows are the same for every slice: one bit per store of the last inverse pass
-  // (row < nrho, >= row_lo and, with row_need, in a band the fused readout loads; the others are never read)
+  // The thread's output rows are the same for every slice: one bit per store of the last inverse pass
+  // (row < nrho and >= row_lo).  rowmap (ahead of the fused inverse DFT + readout): row -> where the row
+  // is stored in the column, -1 for rows of bands no pixel taps (never read): the bands the readout
+  // loads sit back to back, so each of its 32-byte band reads shares its DRAM burst with the next band
+  // it needs, not with a skipped one.  TMC: the 16 store rows live in the thread's TMEM lane.
   constexpr int RLS = FftPlan<L, true>::radix(FftPlan<L, true>::P - 1), NSL = FftPlan<L, true>::ns(FftPlan<L, true>::P - 1);
   constexpr int ROS = PRUNE ? RLS / 2 : RLS, NST = (E / RLS) * ROS;
   static_assert(NST <= 32, "one mask bit per store");
+  constexpr bool TMC = TM && NST <= 16;
   uint32_t smask = 0;
+  {
+    uint32_t crow[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-  for (int q = 0; q < NST; ++q) {
-    const int idx = ti + (q / ROS) * T + (q % ROS) * NSL;
-    bool on = idx < nrho && idx >= row_lo;
-    if (on && row_need) on = (__ldg(row_need + (idx >> 5)) >> (idx & 31)) & 1u;
-    smask |= on ? 1u << q : 0u;
+    for (int q = 0; q < NST; ++q) {
+      const int idx = ti + (q / ROS) * T + (q % ROS) * NSL;
+      int c = (idx < nrho && idx >= row_lo) ? (rowmap ? __ldg(rowmap + idx) : idx) : -1;
+      if (c >= nrho_pad) c = -1;
+      smask |= c >= 0 ? 1u << q : 0u;
+      if constexpr (TMC) crow[q] = (uint32_t)max(c, 0);
+    }
+    if constexpr (TMC) {
+      tmem_st16(kt + 2 * E + 32, crow);
+      tmem_wait_st();
+    }
   }
   if (!kw_bulk && !TKW)
     for (int i = ti; i < nrho; i += T) kws[i] = __ldg(kw + i);  // visible after the row mix's barrier
@@ -672,11 +684,20 @@ k_rho_conv(const float2* __restrict__ Gh, float2* __restrict__ Yh, int batch, in
     };
     float2* ycol = Yh + ((size_t)b * nh + m) * nrho_pad;
     int sq = 0;  // position among the thread's stores (block_conv's last pass is fully unrolled)
+    uint32_t crs[16];
     auto store = [&](int idx, float2 v) {  // rows below row_lo / outside the readout's bands are never read downstream
-      if ((smask >> sq) & 1u) ycol[idx] = v;
+      if constexpr (TMC) {
+        if (sq == 0) tmem_ld16(kt + 2 * E + 32, crs);
+        if ((smask >> sq) & 1u) ycol[crs[sq]] = v;
+      } else {
+        if ((smask >> sq) & 1u) ycol[rowmap ? __ldg(rowmap + idx) : idx] = v;
+      }
       ++sq;
     };
-    if (ti < nrho_pad - nrho) ycol[nrho + ti] = make_float2(0.f, 0.f);  // padding rows read as zero (K45)
+    if (nrho + ti < zend) {  // padding rows read as zero (K45)
+      const int c = rowmap ? __ldg(rowmap + nrho + ti) : nrho + ti;
+      if (c >= 0 && c < nrho_pad) ycol[c] = make_float2(0.f, 0.f);
+    }
     block_conv<L, PRUNE, 16>(buf, ti, tw, load, mul, store, block_sync);  // SFU twiddles for every pass
   }
   if constexpr (TM) {
@@ -893,7 +914,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
     // publishes the step's descriptor and lands its spectra there by TMA.
     const int lane = threadIdx.x - NC;
     int slice = 0, k0 = 0, ks = 0, nl = 0, lpos = 0;
-    unsigned bits = 0;
+    unsigned bits = 0, snv = 0;
     for (int i = 0;; ++i) {
       bool done = false;
       while (lpos >= nl) {  // next unit with at least one needed step
@@ -918,7 +939,8 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
         const int k1 = (int)ub.y;
         ks = k0 > 0 ? k0 - 1 : 0;  // the band before the unit feeds its first band's carried row
         const int st = ks + lane;
-        bits = __ballot_sync(0xFFFFFFFFu, st < k1 && __ldg(step_need + st) != 0u);
+        snv = st < k1 ? __ldg(step_need + st) : 0u;  // 0 = nobody taps the band, else 1 + its first row in Y
+        bits = __ballot_sync(0xFFFFFFFFu, snv != 0u);
         nl = __popc(bits);
         lpos = 0;
       }
@@ -933,6 +955,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       }
       const int kk = ks + (int)__fns(bits, 0, lpos + 1);
       ++lpos;
+      const int yrow = (int)__shfl_sync(0xFFFFFFFFu, snv, kk - ks) - 1;  // where K3 stored the band's first row
       const bool rd = kk >= k0;  // the reloaded band before the unit only provides its last row
       uint32_t e0 = 0, e1 = 0;
       if (rd && lane == 0) {
@@ -947,7 +970,7 @@ k_irdft_readout(const __grid_constant__ CUtensorMap ymap, const __grid_constant_
       __syncwarp();
       if (lane < G * (NFULL + 1)) {  // rows (r0 + 2g, r0 + 2g + 1) -> group g's input as [m][2]
         const int g = lane / (NFULL + 1), bx = lane - g * (NFULL + 1);
-        const int c0 = 2 * (row_min + S * kk + 2 * g);
+        const int c0 = 2 * (yrow + 2 * g);
         float2* dst = smem_k45 + r * QREG + g * FS::IN_PITCH + 2 * (bx * 256);
         if (bx < NFULL) tma_load_3d(dst, &ymap, c0, bx * 256, slice, &full[r]);
         else tma_load_3d(dst, &ytail, c0, NFULL * 256, slice, &full[r]);
@@ -1132,7 +1155,7 @@ k_irdft_readout_mixed(const __grid_constant__ CUtensorMap ymap, float* __restric
   if (threadIdx.x >= NC) {  // ---- producer warp (as in k_irdft_readout, two input buffers)
     const int lane = threadIdx.x - NC;
     int slice = 0, k0 = 0, ks = 0, nl = 0, lpos = 0;
-    unsigned bits = 0;
+    unsigned bits = 0, snv = 0;
     for (int i = 0;; ++i) {
       bool done = false;
       while (lpos >= nl) {
@@ -1153,7 +1176,8 @@ k_irdft_readout_mixed(const __grid_constant__ CUtensorMap ymap, float* __restric
         const int k1 = (int)ub.y;
         ks = k0 > 0 ? k0 - 1 : 0;
         const int st = ks + lane;
-        bits = __ballot_sync(0xFFFFFFFFu, st < k1 && __ldg(step_need + st) != 0u);
+        snv = st < k1 ? __ldg(step_need + st) : 0u;  // 0 = nobody taps the band, else 1 + its first row in Y
+        bits = __ballot_sync(0xFFFFFFFFu, snv != 0u);
         nl = __popc(bits);
         lpos = 0;
       }
@@ -1168,6 +1192,7 @@ k_irdft_readout_mixed(const __grid_constant__ CUtensorMap ymap, float* __restric
       }
       const int kk = ks + (int)__fns(bits, 0, lpos + 1);
       ++lpos;
+      const int yrow = (int)__shfl_sync(0xFFFFFFFFu, snv, kk - ks) - 1;
       const bool rd = kk >= k0;
       uint32_t e0 = 0, e1 = 0;
       if (rd && lane == 0) {
@@ -1181,7 +1206,7 @@ k_irdft_readout_mixed(const __grid_constant__ CUtensorMap ymap, float* __restric
       }
       __syncwarp();
       if (lane < FS::NBOX)  // rows (r0, r0 + 1) as [m][2]; m >= nh is zero fill
-        tma_load_3d(inbuf + r * IN + 2 * (lane * 256), &ymap, 2 * (row_min + S * kk), lane * 256, slice, &full[r]);
+        tma_load_3d(inbuf + r * IN + 2 * (lane * 256), &ymap, 2 * yrow, lane * 256, slice, &full[r]);
       const uint32_t pa = __shfl_sync(0xFFFFFFFFu, e0, 0), pb = __shfl_sync(0xFFFFFFFFu, e1, 0);
       if (lane == 31 && pb > pa) prefetch_l2_bulk(entries + pa, 16u * (pb - pa));
     }
@@ -1628,7 +1653,7 @@ cudaError_t rdft_p_impl(const Dims& d, const DevTables& t, const float* g, float
 
 template <int L>
 cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
-                      cudaStream_t s, bool pin, const uint32_t* row_need) {
+                      cudaStream_t s, bool pin, const int32_t* rowmap) {
   const int gp = pin ? d.ns : (d.gp > 0 ? d.gp : d.nt);
   const size_t smem = pin ? ((size_t)padded_len(L) + 2 * (size_t)((d.ns + 3) & ~1)) * sizeof(float2) + (size_t)d.nrho * 4
                           : ((size_t)padded_len(L) + ((d.ns + 1) & ~1) + (size_t)gp + 2) * sizeof(float2) +
@@ -1656,7 +1681,7 @@ cudaError_t conv_impl(const Dims& d, const DevTables& t, const float2* Gh, float
   cudaError_t e = prep(k, smem);
   if (e) return e;
   k<<<d.nh, FftPlan<L, false>::T, smem, s>>>(Gh, Yh, batch, d.nt, gp, d.ns, d.nrho, row_lo, d.nrho_pad, d.nh, t.abw,
-                                              t.kw, t.khat, t.tw_rho, row_need);
+                                              t.kw, t.khat, t.tw_rho, rowmap, rowmap ? d.row_end : d.nrho_pad);
   return cudaGetLastError();
 }
 
@@ -1712,7 +1737,7 @@ cudaError_t launch_row_rdft_p(const Dims& d, const DevTables& t, const float* g,
 }
 cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* Gh, float2* Yh, int batch, int row_lo,
                             cudaStream_t s, bool pin, bool fused_rows) {
-  const uint32_t* row_need = fused_rows ? t.row_need : nullptr;
+  const int32_t* row_need = fused_rows ? (d.ycompact ? t.rowmap_cp : t.rowmap_id) : nullptr;
   switch (d.L) {
     case 512: return conv_impl<512>(d, t, Gh, Yh, batch, row_lo, s, pin, row_need);
     case 1024: return conv_impl<1024>(d, t, Gh, Yh, batch, row_lo, s, pin, row_need);
@@ -2002,7 +2027,7 @@ cudaError_t fused_impl(const Dims& d, const DevTables& t, const float2* Yh, floa
   const int slots = d.nsm * (occ > 0 ? occ : 1);
   const int grid = units < slots ? units : slots;
   k<<<grid, NTHR, FS::SMEM, s>>>(map, tail, img, d.nrho, d.n, d.nq, d.row_min, d.nbands, batch,
-                                                          counter, t.band_off, t.band_need,
+                                                          counter, t.band_off, d.ycompact ? t.band_row_cp : t.band_row_id,
                                                           reinterpret_cast<const uint2*>(t.units), d.nunits,
                                                           reinterpret_cast<const uint4*>(t.band_entries),
                                                           d.out_scale, t.tw_phi);
@@ -2027,7 +2052,7 @@ cudaError_t fused_mixed_impl(const Dims& d, const DevTables& t, const float2* Yh
   const int units = d.nunits * batch;
   const int grid = units < d.nsm ? units : d.nsm;
   k<<<grid, FS::NTHR, FS::SMEM, s>>>(map, img, d.nrho, d.n, d.nq, d.row_min, batch, counter, t.band_off,
-                                     t.band_need, reinterpret_cast<const uint2*>(t.units), d.nunits,
+                                     d.ycompact ? t.band_row_cp : t.band_row_id, reinterpret_cast<const uint2*>(t.units), d.nunits,
                                      reinterpret_cast<const uint4*>(t.band_entries), d.out_scale);
   return cudaGetLastError();
 }

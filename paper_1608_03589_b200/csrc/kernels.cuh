@@ -34,7 +34,13 @@ struct DevTables {
   const uint32_t* band_entries;  // per band: uint4 {qq | bit31 zero, qidx, wi, wj} (plan_host band_packed)
   const uint32_t* band_need;     // [nbands] 1 = some pixel taps one of the band's rows
   const uint32_t* units;         // [nunits][2] fused work units: band range [k0, k1), outermost first
-  const uint32_t* row_need;      // bitmap over log-polar rows: 1 = the row lies in a band the fused readout loads
+  // where the fused path keeps the convolved spectra's rows inside a Y column (plan_host build_bands):
+  // rowmap_*[row] = position or -1 (a band nobody taps: never written, never read), band_row_*[band] =
+  // 1 + position of the band's first row or 0; _id: rows stay in place, _cp: needed bands back to back
+  const int32_t* rowmap_cp;
+  const int32_t* rowmap_id;
+  const uint32_t* band_row_cp;
+  const uint32_t* band_row_id;
   // generic sizes (Bluestein)
   const float2* chirp;   // [nphi]
   const float2* bhat_f;  // [MB]
@@ -55,6 +61,8 @@ struct Dims {
                                    // win_lo leading columns + the row's last win - win_lo columns
   float out_scale;        // 1 (backprojection) or 1/(2 pi) (fbp)
   int npairs;             // > 0: the generic inverse DFT runs over t.pairs only (0 = every row pair)
+  int ycompact;           // 1: the fused path packs the needed bands of Y back to back (rowmap_cp / band_row_cp)
+  int row_end;            // rows the band tables span: row_min + band_rows * nbands (>= nrho)
   int pmix;               // 1: K2p emits the semi-polar row spectra P[b][m][ns] and K3 takes them as they are
 };
 
@@ -65,7 +73,7 @@ cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, f
 // semi-polar row spectra P[b][nh][ns] (d.pmix plans; cudaErrorNotSupported otherwise)
 cudaError_t launch_row_rdft_p(const Dims& d, const DevTables& t, const float* g, float2* P, int batch, cudaStream_t s);
 // rows < row_lo of Y are not written (0 = all rows); pin: the input is K2p's P[b][nh][ns] (no row mix)
-// fused_rows: only the rows of bands the fused inverse DFT + readout loads are written (t.row_need)
+// fused_rows: only the rows of bands the fused inverse DFT + readout loads are written (t.rowmap_*)
 cudaError_t launch_rho_conv(const Dims& d, const DevTables& t, const float2* G, float2* Y, int batch, int row_lo,
                             cudaStream_t s, bool pin = false, bool fused_rows = false);
 cudaError_t launch_row_irdft(const Dims& d, const DevTables& t, const float2* Y, float* lp, int batch, cudaStream_t s);

@@ -172,6 +172,25 @@ void build_bands(HostPlan& h, int band_rows) {
     if (h.band_need[b])
       for (int r = rmin + band_rows * b; r < rmin + band_rows * (b + 1) && r < h.nrho_pad; ++r)
         h.row_need[(size_t)r >> 5] |= 1u << (r & 31);
+  h.row_end = rmin + band_rows * h.nbands;
+  h.rowmap_cp.assign((size_t)h.row_end, -1);
+  h.rowmap_id.assign((size_t)h.row_end, -1);
+  h.band_row_cp.assign((size_t)h.nbands, 0u);
+  h.band_row_id.assign((size_t)h.nbands, 0u);
+  {
+    int cpos = 0;
+    for (int b = 0; b < h.nbands; ++b) {
+      if (!h.band_need[b]) continue;
+      const int r0 = rmin + band_rows * b;
+      h.band_row_cp[b] = (uint32_t)cpos + 1u;
+      h.band_row_id[b] = (uint32_t)r0 + 1u;
+      for (int j = 0; j < band_rows; ++j) {
+        h.rowmap_cp[(size_t)r0 + j] = cpos + j;
+        h.rowmap_id[(size_t)r0 + j] = r0 + j;
+      }
+      cpos += band_rows;
+    }
+  }
   h.band_packed.resize(h.band_entries.size() * 4);
   for (size_t e = 0; e < h.band_entries.size(); ++e) {
     const uint32_t ent = h.band_entries[e];

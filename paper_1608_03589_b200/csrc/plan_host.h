@@ -64,6 +64,10 @@ struct HostPlan {
   // loads and transforms whole bands, so every row of a needed band must hold K3's output); K3 writes
   // these rows only
   std::vector<uint32_t> row_need;
+  // the same as maps (see kernels.cuh DevTables): rows [0, row_end), row_end = row_min + band_rows * nbands
+  int row_end = 0;
+  std::vector<int32_t> rowmap_cp, rowmap_id;
+  std::vector<uint32_t> band_row_cp, band_row_id;
   // self-contained 16-byte entries {qy | qx << 15 | zero flag << 31, qidx, wi bits, wj bits}
   std::vector<uint32_t> band_packed;
   // generic sizes (nphi not a power of two in [512, 4096], ...): Bluestein DFTs of

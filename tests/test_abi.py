@@ -486,3 +486,34 @@ def test_k2p_tile_tables_reproduce_the_semipolar_image(nt, nth, n):
 
 def test_k2p_needs_four_row_tiles():
     assert HostPlan(260, 256, 128).info.p_rows == 0   # ns = 130: K2's row spectra + K3's row mix
+
+
+@pytest.mark.parametrize("nt,nth,n", [(256, 256, 256), (2048, 2048, 2048), (96, 1280, 64)])
+def test_fused_row_maps(nt, nth, n):
+    """The fused path's row placement (plan_host build_bands): K3 writes row r of a column at rowmap[r]
+    (-1: a band no pixel taps, never written) and the fused readout fetches band b at band_row[b] - 1.
+    Compacted: the needed bands sit back to back in row order; identity: every needed row in place."""
+    hp = HostPlan(nt, nth, n)
+    i = hp.info
+    if i.band_rows == 0:
+        pytest.skip("no fused readout for this nphi")
+    need = hp.table("band_need", np.uint32)
+    cp, ident = hp.table("rowmap_cp", np.int32), hp.table("rowmap_id", np.int32)
+    bcp, bid = hp.table("band_row_cp", np.uint32), hp.table("band_row_id", np.uint32)
+    bits = hp.table("row_need", np.uint32)
+    S, r_min = i.band_rows, i.row_min
+    assert len(need) == i.nbands and len(cp) == len(ident) == r_min + S * i.nbands
+    pos = 0
+    for b in range(i.nbands):
+        rows = np.arange(r_min + S * b, r_min + S * (b + 1))
+        if need[b]:
+            assert bid[b] == rows[0] + 1 and bcp[b] == pos + 1
+            assert np.array_equal(ident[rows], rows) and np.array_equal(cp[rows], pos + np.arange(S))
+            pos += S
+        else:
+            assert bid[b] == 0 and bcp[b] == 0 and (ident[rows] == -1).all() and (cp[rows] == -1).all()
+    assert (cp[:r_min] == -1).all()
+    nrho_pad = (i.nrho + 15) // 16 * 16
+    for r in range(min(len(cp), nrho_pad)):
+        assert ((int(bits[r >> 5]) >> (r & 31)) & 1) == (1 if cp[r] >= 0 else 0)
+    assert 0 < pos <= len(cp) and (n < 2048 or pos < 0.75 * i.nrho)   # about a third of the rows is skipped at 2048^2
