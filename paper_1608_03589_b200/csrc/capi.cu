@@ -231,10 +231,10 @@ int run_chunk(const lpbp_plan* P, const float* in, float* out, int c, char* ws, 
     ++g_launches;
     src = reinterpret_cast<const float*>(A);
   }
-  const bool pin = d.pmix && !gen && win == 0;  // K2p: semi-polar row spectra, no row mix in K3
+  const bool pin = (gen ? d.pmix == 2 : d.pmix == 1) && win == 0;  // semi-polar row spectra, no row mix in K3
   e = staged(P, 1, c, s, [&] {
-    return gen   ? lpbp::launch_row_rdft_generic(d, P->t, src, reinterpret_cast<float2*>(B), c, s)
-           : pin ? lpbp::launch_row_rdft_p(d, P->t, src, reinterpret_cast<float2*>(B), c, s)
+    return pin   ? lpbp::launch_row_rdft_p(d, P->t, src, reinterpret_cast<float2*>(B), c, s)
+           : gen ? lpbp::launch_row_rdft_generic(d, P->t, src, reinterpret_cast<float2*>(B), c, s)
                  : lpbp::launch_row_rdft(d, P->t, src, reinterpret_cast<float2*>(B), c, s);
   });
   if (e) return launch_fail(e, "row_rdft");
@@ -421,6 +421,7 @@ int lpbp_plan_create(const lpbp_params* params, lpbp_plan** plan) {
     return v ? atoi(v) != 0 : true;
   }();
   d.pmix = (h.pmix && !h.generic && k2p && 2 * h.nrho <= h.L) ? 1 : 0;
+  if (h.generic && k2p && lpbp::mixed_p_available(h.nphi, h.ns, h.nrho, h.L)) d.pmix = 2;  // mixed-radix lengths
   // the fused path's Y columns hold the needed bands back to back; LPBP_YCOMPACT=0 leaves every row in place
   static const bool ycp = [] {
     const char* v = getenv("LPBP_YCOMPACT");
@@ -469,7 +470,7 @@ int lpbp_plan_get_info(const lpbp_plan* P, lpbp_plan_info* info) {
   info->nbands = h.nbands;
   info->generic = h.generic ? 1 : 0;
   info->MB = h.MB;
-  info->p_rows = P->d.pmix;
+  info->p_rows = P->d.pmix ? 1 : 0;
   info->phi_q = 0;
   if (h.generic && lpbp::mixed_radix_length(h.nphi)) {
     int q = h.nphi;

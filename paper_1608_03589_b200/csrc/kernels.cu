@@ -1456,6 +1456,43 @@ k_row_rdft_mixed(const float* __restrict__ g, float2* __restrict__ Gh, int nt, i
   }
 }
 
+// The same for the SEMI-POLAR rows (K2p's order of the two linear maps, grids.py:290-311 before the phi DFT):
+// rows ka = 2 blockIdx.x and ka + 1 of p, each value two taps of the sinogram (t >= 0 taps for phi < pi,
+// t <= 0 taps for phi >= pi; rows `ab`, weights `wab`: out-of-range taps carry weight 0 on a valid row);
+// ns = nt/2 full-length transforms instead of nt zero-padded ones, output P[b][m][ns].
+template <int Q, int P>
+__global__ void __launch_bounds__(MixedShape<Q, P>::THREADS)
+k_row_rdft_mixed_p(const float* __restrict__ g, float2* __restrict__ Ph, int nt, int ns, int ntheta,
+                   const int2* __restrict__ ab, const float4* __restrict__ wab) {
+  extern __shared__ __align__(16) float2 smem_m2p[];
+  constexpr int N = Q * P;  // nphi
+  const int nh = ntheta + 1;
+  const int ka = 2 * blockIdx.x, kb = ka + 1;
+  const bool hb = kb < ns;
+  const float* base = g + (size_t)blockIdx.y * nt * ntheta;
+  const int2 ia = __ldg(ab + ka), ib = hb ? __ldg(ab + kb) : ia;
+  const float4 wa = __ldg(wab + ka), wb = hb ? __ldg(wab + kb) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* xa = base + (size_t)ia.x * ntheta;  // taps xa[j], xa[ntheta + j]
+  const float* xb = base + (size_t)ia.y * ntheta;
+  const float* ya = base + (size_t)ib.x * ntheta;
+  const float* yb = base + (size_t)ib.y * ntheta;
+  auto load = [&](int idx) -> float2 {  // rows ka, kb packed as re / im
+    if (idx < ntheta)
+      return make_float2(fmaf(wa.y, __ldg(xa + ntheta + idx), wa.x * __ldg(xa + idx)),
+                         fmaf(wb.y, __ldg(ya + ntheta + idx), wb.x * __ldg(ya + idx)));
+    const int j = idx - ntheta;
+    return make_float2(fmaf(wa.w, __ldg(xb + ntheta + j), wa.z * __ldg(xb + j)),
+                       fmaf(wb.w, __ldg(yb + ntheta + j), wb.z * __ldg(yb + j)));
+  };
+  block_dft_mixed<Q, P, false>(smem_m2p, load);
+  float2* dst = Ph + (size_t)blockIdx.y * nh * ns + ka;  // ns even: both rows by one 16-byte store
+  for (int m = threadIdx.x; m < nh; m += blockDim.x) {
+    const float2 z = mixed_at<Q, P>(smem_m2p, m), w = mixed_at<Q, P>(smem_m2p, m == 0 ? 0 : N - m);
+    *reinterpret_cast<float4*>(dst + (size_t)m * ns) =
+        make_float4(0.5f * (z.x + w.x), 0.5f * (z.y - w.y), 0.5f * (z.y + w.y), 0.5f * (w.x - z.x));
+  }
+}
+
 template <int Q, int P>
 __global__ void __launch_bounds__(MixedShape<Q, P>::THREADS)
 k_row_irdft_mixed(const __grid_constant__ CUtensorMap ymap, float* __restrict__ lp, int nrho, int ntheta, int nbox,
@@ -1726,7 +1763,15 @@ cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, f
     default: return cudaErrorNotSupported;
   }
 }
+namespace {
+bool mixed_enabled();
+cudaError_t rdft_mixed_p(const Dims& d, const DevTables& t, const float* g, float2* Ph, int batch, cudaStream_t s);
+}  // namespace
+bool mixed_p_available(int nphi, int ns, int nrho, int L) {
+  return mixed_enabled() && mixed_radix_length(nphi) && !(ns & 1) && 2 * nrho <= L;
+}
 cudaError_t launch_row_rdft_p(const Dims& d, const DevTables& t, const float* g, float2* Ph, int batch, cudaStream_t s) {
+  if (d.generic) return d.pmix == 2 ? rdft_mixed_p(d, t, g, Ph, batch, s) : cudaErrorNotSupported;
   switch (d.nphi) {
     case 512: return rdft_p_impl<512>(d, t, g, Ph, batch, s);
     case 1024: return rdft_p_impl<1024>(d, t, g, Ph, batch, s);
@@ -1928,6 +1973,16 @@ cudaError_t rdft_mixed_impl(const Dims& d, const float* g, float2* Gh, int batch
   return cudaGetLastError();
 }
 template <int Q, int P>
+cudaError_t rdft_mixed_p_impl(const Dims& d, const DevTables& t, const float* g, float2* Ph, int batch, cudaStream_t s) {
+  using MS = MixedShape<Q, P>;
+  if ((d.ns & 1) || (reinterpret_cast<uintptr_t>(Ph) & 15)) return cudaErrorNotSupported;
+  auto k = k_row_rdft_mixed_p<Q, P>;
+  cudaError_t e = prep(k, MS::SMEM);
+  if (e) return e;
+  k<<<dim3(d.ns / 2, batch), MS::THREADS, MS::SMEM, s>>>(g, Ph, d.nt, d.ns, d.ntheta, t.ab, t.wab);
+  return cudaGetLastError();
+}
+template <int Q, int P>
 cudaError_t irdft_mixed_impl(const Dims& d, const DevTables& t, const float2* Yh, float* lp, int batch, cudaStream_t s) {
   using MS = MixedShape<Q, P>;
   auto k = k_row_irdft_mixed<Q, P>;
@@ -1945,6 +2000,11 @@ cudaError_t irdft_mixed_impl(const Dims& d, const DevTables& t, const float2* Yh
 }
 cudaError_t rdft_mixed(const Dims& d, const float* g, float2* Gh, int batch, cudaStream_t s) {
 #define LPBP_CALL(Q, P) rdft_mixed_impl<Q, P>(d, g, Gh, batch, s)
+  LPBP_MIXED_SWITCH(d.nphi, LPBP_CALL)
+#undef LPBP_CALL
+}
+cudaError_t rdft_mixed_p(const Dims& d, const DevTables& t, const float* g, float2* Ph, int batch, cudaStream_t s) {
+#define LPBP_CALL(Q, P) rdft_mixed_p_impl<Q, P>(d, t, g, Ph, batch, s)
   LPBP_MIXED_SWITCH(d.nphi, LPBP_CALL)
 #undef LPBP_CALL
 }

@@ -63,13 +63,15 @@ struct Dims {
   int npairs;             // > 0: the generic inverse DFT runs over t.pairs only (0 = every row pair)
   int ycompact;           // 1: the fused path packs the needed bands of Y back to back (rowmap_cp / band_row_cp)
   int row_end;            // rows the band tables span: row_min + band_rows * nbands (>= nrho)
-  int pmix;               // 1: K2p emits the semi-polar row spectra P[b][m][ns] and K3 takes them as they are
+  int pmix;               // 2: the same through the mixed-radix row DFT of a generic plan (k_row_rdft_mixed_p); 1: K2p emits the semi-polar row spectra P[b][m][ns] and K3 takes them as they are
 };
 
 // Each returns cudaGetLastError() after the launch (0 on success) or
 // cudaErrorNotSupported when no instantiation exists for the size.
 cudaError_t launch_ramp(const Dims& d, const DevTables& t, const float* g, float* out, int batch, cudaStream_t s);
 cudaError_t launch_row_rdft(const Dims& d, const DevTables& t, const float* g, float2* G, int batch, cudaStream_t s);
+// generic plan whose mixed-radix row DFT can transform the semi-polar rows (d.pmix = 2)
+bool mixed_p_available(int nphi, int ns, int nrho, int L);
 // semi-polar row spectra P[b][nh][ns] (d.pmix plans; cudaErrorNotSupported otherwise)
 cudaError_t launch_row_rdft_p(const Dims& d, const DevTables& t, const float* g, float2* P, int batch, cudaStream_t s);
 // rows < row_lo of Y are not written (0 = all rows); pin: the input is K2p's P[b][nh][ns] (no row mix)

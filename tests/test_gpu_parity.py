@@ -474,6 +474,11 @@ g = torch.stack([torch.from_numpy(phantoms.config_sinogram(1, i)) for i in range
 out["fbp512"] = p.get_plan(512, 512, 512, None, None, (0.0, 1.0)).execute(g, chunk=3).cpu().numpy()
 g = torch.from_numpy(phantoms.config_sinogram(0, 0))[None].cuda()
 out["bp256"] = p.get_plan(256, 256, 256, None, None, None).execute(g).cpu().numpy()
+torch.manual_seed(5)
+g = torch.randn(3, 96, 1280, device="cuda").cumsum(1) * 0.05     # mixed-radix row DFTs (nphi = 5 x 512)
+plan = p.get_plan(96, 1280, 64, None, None, (0.0, 1.0))
+out["p_rows_mixed"] = np.int32(plan.info["p_rows"])
+out["fbp_mixed"] = plan.execute(g, chunk=2).cpu().numpy()
 np.savez(sys.argv[2], **out)
 """
 
@@ -481,7 +486,8 @@ np.savez(sys.argv[2], **out)
 def test_k2p_matches_frequency_domain_row_mix(tmp_path):
     """Default: K2p transforms the semi-polar rows and K3 takes their spectra as they are (p_rows = 1).
     LPBP_K2P=0: K2's nt row spectra and K3's frequency-domain row mix.  The two orders of the same
-    linear maps agree to fp32 rounding at 256^2, 512^2 and 2048^2 (images and the log-polar stage);
+    linear maps agree to fp32 rounding at 256^2, 512^2 and 2048^2 (images and the log-polar stage) and on a
+    mixed-radix plan (k_row_rdft_mixed_p against k_row_rdft_mixed + the row mix);
     each run in its own process (the switch is read once)."""
     import os
     import subprocess
@@ -496,7 +502,8 @@ def test_k2p_matches_frequency_domain_row_mix(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
     assert int(outs[0]["p_rows_2048"]) == 1 and int(outs[1]["p_rows_2048"]) == 0
-    for k in ("fbp2048", "lp2048", "fbp512", "bp256"):
+    assert int(outs[0]["p_rows_mixed"]) == 1 and int(outs[1]["p_rows_mixed"]) == 0
+    for k in ("fbp2048", "lp2048", "fbp512", "bp256", "fbp_mixed"):
         a, b = outs[0][k], outs[1][k]
         assert np.isfinite(a).all() and np.abs(a).max() > 0
         e = O.relative_l2(a, b)
