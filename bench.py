@@ -73,7 +73,7 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--slices", type=int, default=0, help="slices per rank per step (0 = config default)")
     ap.add_argument("--chunk", type=int, default=0,
-                    help="slices per internal pipeline chunk (0 = 128 for the power-of-two log-polar path (one stream), "
+                    help="slices per internal pipeline chunk (0 = 256 for the power-of-two log-polar path (one stream), "
                          "16 for generic sizes and bst: the measured bests)")
     ap.add_argument("--e2e-slices", type=int, default=512)
     ap.add_argument("--e2e-chunk", type=int, default=4)
@@ -344,7 +344,8 @@ def workload_config(a, c: dict, world: int, geom: dict, chunk: int, nstreams: in
 
 def default_schedule(a, generic: bool, unfused: bool, bst: bool = False) -> tuple[int, int]:
     """(chunk, streams) of the device-resident leg.  Power-of-two log-polar path: ONE stream, chunks of
-    128 slices.  Measured at 2048^2 (B200, r02l): 1 stream x chunk 32 / 64 / 128 -> 8689 / 8820 / 8874
+    256 slices (a 32.8 GB workspace; with K2p, r02n: chunk 128 / 256 / 512 -> 9576 / 9630 / 9649 slices/s).
+    Measured at 2048^2 before K2p (B200, r02l): 1 stream x chunk 32 / 64 / 128 -> 8689 / 8820 / 8874
     slices/s, 2 streams x chunk 32 / 64 -> 8987 / 8937.  Two streams buy 1.3 % by overlapping kernel
     tails, but every launch then shares the SMs with the other stream's kernel, so the live per-launch
     durations the roofline is built from double (K3 0.155 of the HBM peak live against 0.242 alone) and
@@ -356,7 +357,7 @@ def default_schedule(a, generic: bool, unfused: bool, bst: bool = False) -> tupl
     on one stream, like BST: two chunks in flight halve the L2 the readout's gathers hit (LNLS before
     its fused path: 3175 slices/s on one stream, 2373 on two); the fused mixed-radix path takes two
     streams (LNLS: 4800 vs 4596); generic plans take chunks of 16."""
-    chunk = a.chunk if a.chunk > 0 else (16 if (bst or generic) else 128)
+    chunk = a.chunk if a.chunk > 0 else (16 if (bst or generic) else 256)
     nstreams = a.streams if a.streams > 0 else (1 if (bst or unfused or not generic) else 2)
     return chunk, nstreams
 

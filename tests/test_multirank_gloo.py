@@ -92,7 +92,7 @@ def test_both_arms_state_the_same_config():
         cfg = bench.workload_config(a, c, world, geom, *bench.default_schedule(a, False, False))
         assert cfg["slices_total"] == 2048 and cfg["slices_per_rank"] == 2048 // world
         assert [i for lo, hi in cfg["rank_slice_ranges"] for i in range(lo, hi)] == list(range(2048))
-        assert (cfg["nrho"], cfg["L"], cfg["nphi"], cfg["chunk"], cfg["streams"]) == (3900, 8192, 4096, min(128, 2048 // world), 1)
+        assert (cfg["nrho"], cfg["L"], cfg["nphi"], cfg["chunk"], cfg["streams"]) == (3900, 8192, 4096, min(256, 2048 // world), 1)
         assert cfg["workload"] == "config3: FBP 2048 bins x 2048 angles -> 2048^2"
 
 
